@@ -1,0 +1,216 @@
+/*
+ * hydra.h -- C ABI of the B200 (sm_100a) shared-prefix decode-attention library
+ * (libhydra.so).  Hydragen, arXiv 2402.05099; "P:NNN" = /root/reference/PAPER.md line.
+ *
+ * The library computes exact softmax attention (Eq. 1) for one decode step
+ * (Nq = 1) of B sequences that share a prefix, by the paper's decomposition:
+ *   prefix attention with all B*g queries of a KV head stacked into one dense
+ *   matrix (inter-sequence batching, §3.2) -> (O_p, LSE_p);
+ *   suffix attention, one query per sequence over its own KV (§3.2)
+ *   -> (O_s, LSE_s);
+ *   LSE combine (Eq. 5; App. B combine_lse P:321-344) -> O.
+ * Tree-shaped sharing applies the decomposition at every tree vertex (§3.3).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Pointers are DEVICE pointers unless marked "host".  The caller owns every
+ *    buffer; the library never allocates on the hot path (the only owned object
+ *    is hydra_tree, created and destroyed by the caller).
+ *  - Strides are in ELEMENTS.  The innermost (head_dim) axis must be contiguous.
+ *    Tensor layouts follow App. B with Nq = 1:
+ *        q        [B, Hq, d]            element (b,h,i) at q[b*q_sb + h*q_sh + i]
+ *        prefix   [P, Hkv, d]           element (t,j,i) at k[t*kv_st + j*kv_sh + i]
+ *        suffix   [B, S_cap, Hkv, d]    element (b,t,j,i) at k[b*s_sb + t*s_st + j*s_sh + i]
+ *        o_part   [B, Hq, d] float32 contiguous,  lse_part [B, Hq] float32 contiguous
+ *        out      [B, Hq, d] contiguous in out_dtype
+ *  - Query head h reads KV head floor(h / (Hq/Hkv)) (reading R3).
+ *  - Softmax scale: heads.scale, or 1/sqrt(d) when 0 (Eq. 1).
+ *  - LSE values are NATURAL logs of the softmax denominator over scaled scores
+ *    (Eq. 4).  An empty key set (P == 0, lens[b] == 0) yields the sentinel
+ *    O = 0, LSE = -inf, which every combine treats as the identity (reading R6).
+ *  - Every call is asynchronous and stream-ordered on `stream` (a cudaStream_t
+ *    passed as void*), never synchronises the host and never reads device data
+ *    on the host, so it can be captured in a CUDA graph (the paper's requirement,
+ *    P:149).  Exception: the first hydra_tree_attn call for a given head grouping
+ *    uploads the tree's work list (see hydra_tree_attn).
+ *  - Errors: host-visible arguments are validated synchronously; on a non-OK
+ *    status nothing has been launched and hydra_last_error() describes why.
+ *    Launch failures return HYDRA_ECUDA.  Device-resident lens values are a
+ *    documented precondition (0 <= lens[b] <= S_cap), not checked.
+ *  - Thread safety: all entry points are reentrant; hydra_last_error is
+ *    thread-local.
+ *  - Precision: HYDRA_BF16 inputs use fp32 accumulation, fp32 partials and a
+ *    bf16 (round-to-nearest-even) final output; HYDRA_F32 inputs run an all-fp32
+ *    reference mode (SIMT kernels, accurate exp).
+ */
+#ifndef HYDRA_H_
+#define HYDRA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define HYDRA_API __attribute__((visibility("default")))
+#else
+#define HYDRA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t hydra_status;
+#define HYDRA_OK 0
+#define HYDRA_EINVAL 1       /* null pointer / negative size / bad enum         */
+#define HYDRA_ESHAPE 2       /* Hq % Hkv != 0, stride or shape mismatch, B == 0   */
+#define HYDRA_EUNSUPPORTED 3 /* head_dim / dtype combination not compiled        */
+#define HYDRA_ECUDA 4        /* CUDA launch or runtime failure                    */
+#define HYDRA_ENCCL 5        /* reserved for the multi-GPU layer                  */
+#define HYDRA_ENOMEM 6       /* workspace too small / host allocation failed      */
+
+typedef enum {
+  HYDRA_BF16 = 0,
+  HYDRA_F32 = 1,
+  HYDRA_F16 = 2 /* only for exchanged partial outputs (hydra_combine o_dtype) */
+} hydra_dtype;
+
+/* Attention head configuration (SPEC AttentionConfig). */
+typedef struct {
+  int32_t num_q_heads;  /* Hq                                  */
+  int32_t num_kv_heads; /* Hkv, Hq % Hkv == 0                  */
+  int32_t head_dim;     /* d: 16, 32, 64, 128 or 256           */
+  float scale;          /* 0 => 1/sqrt(d)                      */
+  hydra_dtype dtype;    /* dtype of q and all K/V: BF16 or F32 */
+} hydra_heads;
+
+/* Workspace queries: op codes for hydra_workspace_size. */
+#define HYDRA_OP_PREFIX 0
+#define HYDRA_OP_SUFFIX 1
+#define HYDRA_OP_ATTN 2
+
+/*
+ * hydra_prefix_attn -- inter-sequence batched attention over the shared prefix
+ * (§3.2; App. B `attention(batched_q, prefix_k, prefix_v)` P:366-378).
+ * For KV head j the B*g query rows r = b*g + i (q[b, j*g+i, :]) are stacked into
+ * one matrix and attend, as one dense GEMM-shaped problem, to prefix K/V
+ * [P, Hkv, d] read once.  Output: o_part[b,h,:] = SDP(q[b,h], K_p, V_p) (fp32,
+ * normalised) and lse_part[b,h] = LSE(q[b,h], K_p) (Eq. 4).
+ * BF16 with d == 128 runs the tcgen05/TMEM/TMA kernel; other shapes and F32 run
+ * the SIMT kernel.  ws may be NULL when hydra_workspace_size(HYDRA_OP_PREFIX,...)
+ * returns 0.
+ */
+HYDRA_API hydra_status hydra_prefix_attn(const hydra_heads *h, int64_t B,
+                               const void *q, int64_t q_sb, int64_t q_sh,
+                               int64_t P, const void *k, const void *v, int64_t kv_st, int64_t kv_sh,
+                               float *o_part, float *lse_part,
+                               void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * hydra_suffix_attn -- per-sequence attention over each sequence's own suffix
+ * ("computed normally, with a single query per sequence", §3.2; App. B
+ * P:381-388 with the per-sequence q, reading R4).  Sequence b attends to its
+ * first lens[b] suffix tokens (device int32 array [B]; positions >= lens[b] are
+ * never read).  Split-K over tokens when B*Hkv is small.  Output as
+ * hydra_prefix_attn.
+ */
+HYDRA_API hydra_status hydra_suffix_attn(const hydra_heads *h, int64_t B,
+                               const void *q, int64_t q_sb, int64_t q_sh,
+                               const void *k, const void *v, int64_t s_sb, int64_t s_st, int64_t s_sh,
+                               int64_t S_cap, const int32_t *lens,
+                               float *o_part, float *lse_part,
+                               void *ws, size_t ws_bytes, void *stream);
+
+/*
+ * hydra_combine -- n-ary LSE combine (Eq. 5 P:98-105 in App. B's max-stabilised
+ * form P:333-344, folded over n_parts; associativity S:154).  For each row r:
+ *   m = max_p lse_p[r];  w_p = exp(lse_p[r] - m);  O[r] = sum_p w_p O_p[r] / sum_p w_p;
+ *   lse_out[r] = m + ln(sum_p w_p).
+ * Parts whose lse is -inf are skipped (their O is never read).  Part p row r is at
+ * o_parts + p*o_part_stride + r*d (elements of o_dtype = F32 or F16) and
+ * lse_parts[p*lse_part_stride + r]; strides let it read an all-gathered
+ * [rank][O|LSE] buffer in place.  out_dtype BF16 or F32; lse_out may be NULL.
+ * Setting the environment variable HYDRA_INJECT_COMBINE_BUG=1 drops the
+ * rescaling (w_p = 1): a sabotage switch the parity suite must catch.
+ */
+HYDRA_API hydra_status hydra_combine(int64_t rows, int32_t d, int32_t n_parts,
+                           const void *o_parts, hydra_dtype o_dtype, int64_t o_part_stride,
+                           const float *lse_parts, int64_t lse_part_stride,
+                           void *out, hydra_dtype out_dtype, float *lse_out, void *stream);
+
+/*
+ * hydra_attn -- the whole decode-step attention of App. B `hydragen_attention`
+ * (P:347-399): prefix (hydra_prefix_attn) || suffix (hydra_suffix_attn) ->
+ * combine, writing out[B,Hq,d] (out_dtype) and optionally lse_out[B,Hq].
+ * If s_aux is non-NULL the prefix runs on s_aux concurrently with the suffix on
+ * stream and is joined back into stream with an event before the combine.
+ * Requires ws_bytes >= hydra_workspace_size(HYDRA_OP_ATTN, h, B, P, S_cap, 0).
+ */
+HYDRA_API hydra_status hydra_attn(const hydra_heads *h, int64_t B,
+                        const void *q, int64_t q_sb, int64_t q_sh,
+                        int64_t P, const void *pk, const void *pv, int64_t kv_st, int64_t kv_sh,
+                        const void *sk, const void *sv, int64_t s_sb, int64_t s_st, int64_t s_sh,
+                        int64_t S_cap, const int32_t *lens,
+                        void *out, hydra_dtype out_dtype, float *lse_out,
+                        void *ws, size_t ws_bytes, void *stream, void *s_aux);
+
+/*
+ * Sharing tree (§3.3, Fig. 2; SPEC SharingTree S:182-193).
+ * Host arrays: parent[n_nodes] (root = -1, exactly one root), node_off/node_len
+ * [n_nodes] (node n owns tokens node_off[n] .. node_off[n]+node_len[n]-1 of the
+ * pooled node K/V [T_nodes, Hkv, d]), leaf_of_seq[B] (sequence b's leaf node).
+ * Validation: one root, parents in range, no cycles, node_len >= 1 for
+ * every non-root node (the root may be empty), node_off >= 0, every sequence on a
+ * leaf (a node without children) and every leaf used by >= 1 sequence.
+ * hydra_tree_create builds the per-node query groups (ascending sequence ids of
+ * every sequence whose root->leaf path passes through the node) and
+ * copies them to the device (synchronous; call outside graph capture).
+ */
+struct hydra_tree;
+HYDRA_API hydra_status hydra_tree_create(const int32_t *parent, const int64_t *node_off, const int64_t *node_len,
+                               int32_t n_nodes, const int32_t *leaf_of_seq, int64_t B,
+                               struct hydra_tree **out);
+HYDRA_API void hydra_tree_destroy(struct hydra_tree *t);
+/* Depth (number of nodes on the longest root->leaf path) and group sizes, for tooling. */
+HYDRA_API int32_t hydra_tree_depth(const struct hydra_tree *t);
+HYDRA_API int64_t hydra_tree_group_size(const struct hydra_tree *t, int32_t node);
+HYDRA_API size_t hydra_tree_workspace_size(const hydra_heads *h, const struct hydra_tree *t, int64_t S_cap);
+
+/*
+ * hydra_tree_attn -- tree attention: for every node, the stacked queries of all
+ * sequences in its group attend to the node's K/V (one grouped launch over
+ * (node, KV head, query tile)); each sequence's suffix attention; then an n-ary
+ * combine over the path partials and the suffix (decomposition at every vertex,
+ * §3.3).  Output as hydra_attn.  The first call for a given Hq/Hkv grouping
+ * uploads a small work list to the device synchronously (not capturable); later
+ * calls are pure launches.
+ */
+HYDRA_API hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra_tree *t,
+                             const void *q, int64_t q_sb, int64_t q_sh,
+                             const void *node_k, const void *node_v, int64_t kv_st, int64_t kv_sh,
+                             const void *sk, const void *sv, int64_t s_sb, int64_t s_st, int64_t s_sh,
+                             int64_t S_cap, const int32_t *lens,
+                             void *out, hydra_dtype out_dtype, float *lse_out,
+                             void *ws, size_t ws_bytes, void *stream);
+
+/* Bytes of device workspace the op needs for these sizes (0 if none). */
+HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, int64_t P, int64_t S_cap,
+                            int32_t n_parts);
+
+/*
+ * Tuning / test switches (process-wide):
+ *   "prefix_impl"   0 auto (tcgen05 when supported), 1 force SIMT, 2 force tcgen05
+ *   "prefix_splits" 0 auto, else number of KV splits of the prefix kernel
+ *   "suffix_splits" 0 auto, else number of KV splits of the suffix kernel
+ * Returns HYDRA_EINVAL for an unknown key.
+ */
+HYDRA_API hydra_status hydra_set_config(const char *key, int64_t value);
+HYDRA_API int64_t hydra_get_config(const char *key);
+
+/* Message for the last non-OK status on this thread ("" if none). */
+HYDRA_API const char *hydra_last_error(void);
+HYDRA_API const char *hydra_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HYDRA_H_ */

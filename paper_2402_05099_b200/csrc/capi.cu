@@ -1,0 +1,735 @@
+// capi.cu -- the exported C ABI of libhydra.so (declared in include/hydra.h).
+//
+// Host-side argument validation, work decomposition (KV splits), workspace layout
+// and stream orchestration of the prefix / suffix / combine kernels.  No device
+// allocation and no host<->device synchronisation on any hot-path entry point.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+using namespace hydra;
+
+// ------------------------------------------------------------------ errors / config
+static thread_local std::string g_last_error;
+
+static hydra_status fail(hydra_status st, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+static hydra_status cuda_fail(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  return fail(HYDRA_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+static std::atomic<int64_t> g_prefix_impl{0}, g_prefix_splits{0}, g_suffix_splits{0}, g_tc_debug{0};
+
+extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
+  if (!key) return fail(HYDRA_EINVAL, "null key");
+  if (!strcmp(key, "prefix_impl")) g_prefix_impl = value;
+  else if (!strcmp(key, "prefix_splits")) g_prefix_splits = value;
+  else if (!strcmp(key, "suffix_splits")) g_suffix_splits = value;
+  else if (!strcmp(key, "tc_debug_variant")) g_tc_debug = value;
+  else return fail(HYDRA_EINVAL, "unknown config key '%s'", key);
+  return HYDRA_OK;
+}
+
+extern "C" int64_t hydra_get_config(const char *key) {
+  if (!key) return -1;
+  if (!strcmp(key, "prefix_impl")) return g_prefix_impl;
+  if (!strcmp(key, "prefix_splits")) return g_prefix_splits;
+  if (!strcmp(key, "suffix_splits")) return g_suffix_splits;
+  if (!strcmp(key, "tc_debug_variant")) return g_tc_debug;
+  return -1;
+}
+
+extern "C" const char *hydra_last_error(void) { return g_last_error.c_str(); }
+extern "C" const char *hydra_version(void) { return "hydra-b200 0.1.0 (sm_100a)"; }
+
+static bool inject_combine_bug() {
+  const char *e = getenv("HYDRA_INJECT_COMBINE_BUG");
+  return e && e[0] && strcmp(e, "0") != 0;
+}
+
+// ------------------------------------------------------------------ validation helpers
+static size_t elem_size(hydra_dtype d) { return d == HYDRA_F32 ? 4 : 2; }
+
+static hydra_status check_heads(const hydra_heads *h) {
+  if (!h) return fail(HYDRA_EINVAL, "heads is NULL");
+  if (h->num_q_heads <= 0 || h->num_kv_heads <= 0)
+    return fail(HYDRA_ESHAPE, "head counts must be positive (Hq=%d, Hkv=%d)", h->num_q_heads, h->num_kv_heads);
+  if (h->num_q_heads % h->num_kv_heads)
+    return fail(HYDRA_ESHAPE, "Hq %% Hkv != 0 (Hq=%d, Hkv=%d)", h->num_q_heads, h->num_kv_heads);
+  if (h->dtype != HYDRA_BF16 && h->dtype != HYDRA_F32) return fail(HYDRA_EUNSUPPORTED, "dtype must be BF16 or F32");
+  const int d = h->head_dim;
+  const bool ok = (d == 16 || d == 32 || d == 64 || d == 128) || (d == 256 && h->dtype == HYDRA_BF16);
+  if (!ok) return fail(HYDRA_EUNSUPPORTED, "head_dim %d unsupported for this dtype", d);
+  if (!(h->scale >= 0.f) || std::isinf(h->scale)) return fail(HYDRA_EINVAL, "scale must be finite and >= 0");
+  return HYDRA_OK;
+}
+
+static float scale_of(const hydra_heads *h) { return h->scale > 0.f ? h->scale : 1.0f / sqrtf((float)h->head_dim); }
+
+// 16-byte vector loads need 16-B aligned rows: base and every stride a multiple of 16 B.
+static bool aligned16(const void *p, size_t es, std::initializer_list<int64_t> strides) {
+  if (reinterpret_cast<uintptr_t>(p) % 16) return false;
+  for (int64_t s : strides)
+    if ((s * (int64_t)es) % 16) return false;
+  return true;
+}
+
+static int heads_per_cta(int g) {
+  for (int c : {8, 4, 2, 1})
+    if (g % c == 0) return c;
+  return 1;
+}
+
+// ------------------------------------------------------------------ work decomposition
+// KV splits of the suffix kernel: enough CTAs to keep every SM streaming
+// (~16 resident 128-thread CTAs per SM), never fewer than 32 tokens per split.
+static int suffix_splits(const hydra_heads *h, int64_t B, int64_t S_cap) {
+  if (g_suffix_splits > 0) return (int)std::min<int64_t>(g_suffix_splits, std::max<int64_t>(1, S_cap));
+  if (S_cap <= 0) return 1;
+  const int g = h->num_q_heads / h->num_kv_heads;
+  const int64_t items = B * h->num_kv_heads * (g / heads_per_cta(g));
+  const int64_t target = (int64_t)device_sm_count() * 16;
+  int64_t s = (target + items - 1) / items;
+  s = std::min<int64_t>(s, std::max<int64_t>(1, S_cap / 32));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(s, 64));
+}
+
+static bool use_tc(const hydra_heads *h) {
+  if (g_prefix_impl == 1) return false;
+  return prefix_tc_supported(h);
+}
+
+// Splits of the tensor-core prefix kernel: minimise (waves x blocks per CTA) plus the
+// HBM cost of writing/reading the extra fp32 partials, in units of one KV block.
+static int prefix_splits_tc(int64_t tiles, int64_t P) {
+  if (g_prefix_splits > 0) return (int)g_prefix_splits;
+  const int64_t nblk = (P + 127) / 128;
+  if (nblk <= 1) return 1;
+  const int64_t sms = device_sm_count();
+  double best = 1e300;
+  int best_s = 1;
+  for (int s = 1; s <= std::min<int64_t>(nblk, 32); ++s) {
+    const double waves = std::ceil((double)tiles * s / sms);
+    const double per = std::ceil((double)nblk / s);
+    // one block ~ 0.6 us per wave; one extra split moves tiles*128 rows*1 KB (~0.16 us/tile/148)
+    const double cost = waves * per * 0.6 + (s - 1) * tiles * 128.0 * 1032.0 / 6.5e3 / 1e3;
+    if (cost < best - 1e-9) {
+      best = cost;
+      best_s = s;
+    }
+  }
+  return best_s;
+}
+
+static int prefix_splits_simt(const hydra_heads *h, int64_t B, int64_t P) {
+  if (g_prefix_splits > 0) return (int)g_prefix_splits;
+  if (P <= 0) return 1;
+  const int g = h->num_q_heads / h->num_kv_heads;
+  const int64_t items = B * h->num_kv_heads * (g / heads_per_cta(g));
+  const int64_t target = (int64_t)device_sm_count() * 16;
+  int64_t s = (target + items - 1) / items;
+  s = std::min<int64_t>(s, std::max<int64_t>(1, P / 64));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(s, 64));
+}
+
+static int prefix_splits(const hydra_heads *h, int64_t B, int64_t P) {
+  if (P <= 0) return 1;
+  if (use_tc(h)) {
+    const int g = h->num_q_heads / h->num_kv_heads;
+    const int64_t tiles = ((B * g + 127) / 128) * h->num_kv_heads;
+    return prefix_splits_tc(tiles, P);
+  }
+  return prefix_splits_simt(h, B, P);
+}
+
+static size_t part_bytes(const hydra_heads *h, int64_t B) {
+  return (size_t)B * h->num_q_heads * ((size_t)h->head_dim + 1) * sizeof(float);
+}
+
+// ------------------------------------------------------------------ launch helpers
+struct PartsView {  // n slots of [B,Hq,d] f32 followed by n slots of [B,Hq] f32
+  float *o;
+  float *lse;
+  int64_t o_stride, lse_stride;
+};
+
+static PartsView parts_in_ws(void *ws, const hydra_heads *h, int64_t B, int n) {
+  PartsView v;
+  v.o_stride = B * h->num_q_heads * (int64_t)h->head_dim;
+  v.lse_stride = B * h->num_q_heads;
+  v.o = reinterpret_cast<float *>(ws);
+  v.lse = v.o + v.o_stride * n;
+  return v;
+}
+
+static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, int64_t q_sb, int64_t q_sh,
+                               int64_t P, const void *k, const void *v, int64_t kv_st, int64_t kv_sh, int splits,
+                               const PartsView &dst, cudaStream_t s) {
+  const int g = h->num_q_heads / h->num_kv_heads;
+  const float sl2 = scale_of(h) * 1.4426950408889634f;
+  if (use_tc(h)) {
+    PrefixTcArgs a{};
+    a.q = q;
+    a.q_sb = q_sb;
+    a.q_sh = q_sh;
+    a.k = k;
+    a.v = v;
+    a.kv_st = kv_st;
+    a.kv_sh = kv_sh;
+    a.kv_total = P;
+    a.Hq = h->num_q_heads;
+    a.Hkv = h->num_kv_heads;
+    a.g = g;
+    a.scale_log2 = sl2;
+    a.P = P;
+    a.B = (int32_t)B;
+    a.n_splits = splits;
+    a.o = dst.o;
+    a.lse = dst.lse;
+    a.o_slot_stride = dst.o_stride;
+    a.lse_slot_stride = dst.lse_stride;
+    a.debug_variant = (int32_t)g_tc_debug;
+    hydra_status st = launch_prefix_tc(a, s);
+    return st == HYDRA_OK ? st : cuda_fail("prefix tcgen05 launch");
+  }
+  DecodeParams p{};
+  p.q = q;
+  p.q_sb = q_sb;
+  p.q_sh = q_sh;
+  p.k = k;
+  p.v = v;
+  p.kv_sb = 0;
+  p.kv_st = kv_st;
+  p.kv_sh = kv_sh;
+  p.lens = nullptr;
+  p.len_uniform = P;
+  p.n_seq = (int32_t)B;
+  p.Hq = h->num_q_heads;
+  p.Hkv = h->num_kv_heads;
+  p.g = g;
+  p.scale_log2 = sl2;
+  p.n_splits = splits;
+  p.split_len = (P + splits - 1) / splits;
+  p.heads_per_cta = heads_per_cta(g);
+  p.o = dst.o;
+  p.lse = dst.lse;
+  p.o_split_stride = dst.o_stride;
+  p.lse_split_stride = dst.lse_stride;
+  hydra_status st = launch_decode(p, h->dtype, h->head_dim, s);
+  return st == HYDRA_OK ? st : (st == HYDRA_ECUDA ? cuda_fail("prefix SIMT launch") : fail(st, "prefix SIMT"));
+}
+
+static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, int64_t q_sb, int64_t q_sh,
+                               const void *k, const void *v, int64_t s_sb, int64_t s_st, int64_t s_sh,
+                               int64_t S_cap, const int32_t *lens, int splits, const PartsView &dst,
+                               cudaStream_t s) {
+  const int g = h->num_q_heads / h->num_kv_heads;
+  DecodeParams p{};
+  p.q = q;
+  p.q_sb = q_sb;
+  p.q_sh = q_sh;
+  p.k = k;
+  p.v = v;
+  p.kv_sb = s_sb;
+  p.kv_st = s_st;
+  p.kv_sh = s_sh;
+  p.lens = lens;
+  p.len_uniform = 0;
+  p.n_seq = (int32_t)B;
+  p.Hq = h->num_q_heads;
+  p.Hkv = h->num_kv_heads;
+  p.g = g;
+  p.scale_log2 = scale_of(h) * 1.4426950408889634f;
+  p.n_splits = splits;
+  p.split_len = (S_cap + splits - 1) / splits;
+  p.heads_per_cta = heads_per_cta(g);
+  p.o = dst.o;
+  p.lse = dst.lse;
+  p.o_split_stride = dst.o_stride;
+  p.lse_split_stride = dst.lse_stride;
+  hydra_status st = launch_decode(p, h->dtype, h->head_dim, s);
+  return st == HYDRA_OK ? st : (st == HYDRA_ECUDA ? cuda_fail("suffix launch") : fail(st, "suffix"));
+}
+
+static hydra_status run_combine(int64_t rows, int d, int n, const PartsView &src, void *out, hydra_dtype out_dtype,
+                                float *lse_out, cudaStream_t s) {
+  CombineParams c{};
+  c.rows = rows;
+  c.d = d;
+  c.n_parts = n;
+  c.o_parts = src.o;
+  c.o_part_stride = src.o_stride;
+  c.lse_parts = src.lse;
+  c.lse_part_stride = src.lse_stride;
+  c.out = out;
+  c.lse_out = lse_out;
+  c.inject_bug = inject_combine_bug() ? 1 : 0;
+  hydra_status st = launch_combine(c, HYDRA_F32, out_dtype, s);
+  return st == HYDRA_OK ? st : cuda_fail("combine launch");
+}
+
+// ------------------------------------------------------------------ workspace
+extern "C" size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, int64_t P, int64_t S_cap,
+                                       int32_t n_parts) {
+  (void)n_parts;
+  if (check_heads(h) != HYDRA_OK || B <= 0) return 0;
+  const size_t pb = part_bytes(h, B);
+  switch (op) {
+    case HYDRA_OP_PREFIX: {
+      const int s = prefix_splits(h, B, P);
+      return s > 1 ? pb * s : 0;
+    }
+    case HYDRA_OP_SUFFIX: {
+      const int s = suffix_splits(h, B, S_cap);
+      return s > 1 ? pb * s : 0;
+    }
+    case HYDRA_OP_ATTN:
+      return pb * (size_t)(prefix_splits(h, B, P) + suffix_splits(h, B, S_cap));
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------------ prefix / suffix / combine
+extern "C" hydra_status hydra_prefix_attn(const hydra_heads *h, int64_t B, const void *q, int64_t q_sb,
+                                          int64_t q_sh, int64_t P, const void *k, const void *v, int64_t kv_st,
+                                          int64_t kv_sh, float *o_part, float *lse_part, void *ws,
+                                          size_t ws_bytes, void *stream) {
+  hydra_status st = check_heads(h);
+  if (st) return st;
+  if (B <= 0) return fail(HYDRA_ESHAPE, "B must be > 0 (S:291)");
+  if (P < 0) return fail(HYDRA_ESHAPE, "P must be >= 0");
+  if (!q || !o_part || !lse_part || (P > 0 && (!k || !v))) return fail(HYDRA_EINVAL, "null pointer argument");
+  const size_t es = elem_size(h->dtype);
+  if (!aligned16(q, es, {q_sb, q_sh}) || (P > 0 && (!aligned16(k, es, {kv_st, kv_sh}) || !aligned16(v, es, {}))))
+    return fail(HYDRA_EINVAL, "q/k/v base pointers and strides must be 16-byte aligned");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int d = h->head_dim;
+  PartsView out{o_part, lse_part, B * h->num_q_heads * (int64_t)d, B * h->num_q_heads};
+  if (P == 0) {  // empty prefix: sentinel (reading R6)
+    if (cudaMemsetAsync(o_part, 0, sizeof(float) * B * h->num_q_heads * d, s) != cudaSuccess)
+      return cuda_fail("memset");
+    st = launch_fill_neg_inf(lse_part, B * h->num_q_heads, s);
+    return st ? cuda_fail("fill") : HYDRA_OK;
+  }
+  const int splits = prefix_splits(h, B, P);
+  if (splits == 1) return run_prefix(h, B, q, q_sb, q_sh, P, k, v, kv_st, kv_sh, 1, out, s);
+  const size_t need = part_bytes(h, B) * splits;
+  if (!ws || ws_bytes < need) return fail(HYDRA_ENOMEM, "workspace too small: need %zu bytes", need);
+  PartsView parts = parts_in_ws(ws, h, B, splits);
+  st = run_prefix(h, B, q, q_sb, q_sh, P, k, v, kv_st, kv_sh, splits, parts, s);
+  if (st) return st;
+  return run_combine(B * h->num_q_heads, d, splits, parts, o_part, HYDRA_F32, lse_part, s);
+}
+
+extern "C" hydra_status hydra_suffix_attn(const hydra_heads *h, int64_t B, const void *q, int64_t q_sb,
+                                          int64_t q_sh, const void *k, const void *v, int64_t s_sb, int64_t s_st,
+                                          int64_t s_sh, int64_t S_cap, const int32_t *lens, float *o_part,
+                                          float *lse_part, void *ws, size_t ws_bytes, void *stream) {
+  hydra_status st = check_heads(h);
+  if (st) return st;
+  if (B <= 0) return fail(HYDRA_ESHAPE, "B must be > 0 (S:291)");
+  if (S_cap < 0) return fail(HYDRA_ESHAPE, "S_cap must be >= 0");
+  if (!q || !o_part || !lse_part || (S_cap > 0 && (!k || !v || !lens)))
+    return fail(HYDRA_EINVAL, "null pointer argument");
+  const size_t es = elem_size(h->dtype);
+  if (!aligned16(q, es, {q_sb, q_sh}) || (S_cap > 0 && (!aligned16(k, es, {s_sb, s_st, s_sh}) || !aligned16(v, es, {}))))
+    return fail(HYDRA_EINVAL, "q/k/v base pointers and strides must be 16-byte aligned");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int d = h->head_dim;
+  PartsView out{o_part, lse_part, B * h->num_q_heads * (int64_t)d, B * h->num_q_heads};
+  if (S_cap == 0) {
+    if (cudaMemsetAsync(o_part, 0, sizeof(float) * B * h->num_q_heads * d, s) != cudaSuccess)
+      return cuda_fail("memset");
+    st = launch_fill_neg_inf(lse_part, B * h->num_q_heads, s);
+    return st ? cuda_fail("fill") : HYDRA_OK;
+  }
+  const int splits = suffix_splits(h, B, S_cap);
+  if (splits == 1) return run_suffix(h, B, q, q_sb, q_sh, k, v, s_sb, s_st, s_sh, S_cap, lens, 1, out, s);
+  const size_t need = part_bytes(h, B) * splits;
+  if (!ws || ws_bytes < need) return fail(HYDRA_ENOMEM, "workspace too small: need %zu bytes", need);
+  PartsView parts = parts_in_ws(ws, h, B, splits);
+  st = run_suffix(h, B, q, q_sb, q_sh, k, v, s_sb, s_st, s_sh, S_cap, lens, splits, parts, s);
+  if (st) return st;
+  return run_combine(B * h->num_q_heads, d, splits, parts, o_part, HYDRA_F32, lse_part, s);
+}
+
+extern "C" hydra_status hydra_combine(int64_t rows, int32_t d, int32_t n_parts, const void *o_parts,
+                                      hydra_dtype o_dtype, int64_t o_part_stride, const float *lse_parts,
+                                      int64_t lse_part_stride, void *out, hydra_dtype out_dtype, float *lse_out,
+                                      void *stream) {
+  if (rows < 0 || d <= 0 || n_parts <= 0) return fail(HYDRA_ESHAPE, "rows >= 0, d > 0, n_parts > 0 required");
+  if (!o_parts || !lse_parts || !out) return fail(HYDRA_EINVAL, "null pointer argument");
+  if (o_dtype != HYDRA_F32 && o_dtype != HYDRA_F16) return fail(HYDRA_EUNSUPPORTED, "o_dtype must be F32 or F16");
+  if (out_dtype != HYDRA_F32 && out_dtype != HYDRA_BF16) return fail(HYDRA_EUNSUPPORTED, "out_dtype must be F32 or BF16");
+  if (n_parts > 1 && (o_part_stride < rows * d || lse_part_stride < rows))
+    return fail(HYDRA_ESHAPE, "part strides overlap the rows of a part");
+  if ((d == 128 || d == 256) && (reinterpret_cast<uintptr_t>(o_parts) % 16 ||
+                                 (o_part_stride * (int64_t)elem_size(o_dtype == HYDRA_F16 ? HYDRA_BF16 : HYDRA_F32)) % 16))
+    return fail(HYDRA_EINVAL, "o_parts and o_part_stride must be 16-byte aligned");
+  CombineParams c{};
+  c.rows = rows;
+  c.d = d;
+  c.n_parts = n_parts;
+  c.o_parts = o_parts;
+  c.o_part_stride = o_part_stride;
+  c.lse_parts = lse_parts;
+  c.lse_part_stride = lse_part_stride;
+  c.out = out;
+  c.lse_out = lse_out;
+  c.inject_bug = inject_combine_bug() ? 1 : 0;
+  hydra_status st = launch_combine(c, o_dtype, out_dtype, reinterpret_cast<cudaStream_t>(stream));
+  return st == HYDRA_OK ? st : cuda_fail("combine launch");
+}
+
+// ------------------------------------------------------------------ composite
+namespace {
+struct StreamEvents {
+  cudaEvent_t fork = nullptr, join = nullptr;
+  StreamEvents() {
+    cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&join, cudaEventDisableTiming);
+  }
+};
+thread_local StreamEvents *tl_events = nullptr;
+StreamEvents &events() {
+  if (!tl_events) tl_events = new StreamEvents();
+  return *tl_events;
+}
+}  // namespace
+
+extern "C" hydra_status hydra_attn(const hydra_heads *h, int64_t B, const void *q, int64_t q_sb, int64_t q_sh,
+                                   int64_t P, const void *pk, const void *pv, int64_t kv_st, int64_t kv_sh,
+                                   const void *sk, const void *sv, int64_t s_sb, int64_t s_st, int64_t s_sh,
+                                   int64_t S_cap, const int32_t *lens, void *out, hydra_dtype out_dtype,
+                                   float *lse_out, void *ws, size_t ws_bytes, void *stream, void *s_aux) {
+  hydra_status st = check_heads(h);
+  if (st) return st;
+  if (B <= 0) return fail(HYDRA_ESHAPE, "B must be > 0 (S:291)");
+  if (P < 0 || S_cap < 0) return fail(HYDRA_ESHAPE, "P and S_cap must be >= 0");
+  if (!q || !out || (P > 0 && (!pk || !pv)) || (S_cap > 0 && (!sk || !sv || !lens)))
+    return fail(HYDRA_EINVAL, "null pointer argument");
+  if (out_dtype != HYDRA_BF16 && out_dtype != HYDRA_F32) return fail(HYDRA_EUNSUPPORTED, "out_dtype must be BF16 or F32");
+  const size_t es = elem_size(h->dtype);
+  if (!aligned16(q, es, {q_sb, q_sh}) || (P > 0 && (!aligned16(pk, es, {kv_st, kv_sh}) || !aligned16(pv, es, {}))) ||
+      (S_cap > 0 && (!aligned16(sk, es, {s_sb, s_st, s_sh}) || !aligned16(sv, es, {}))))
+    return fail(HYDRA_EINVAL, "q/k/v base pointers and strides must be 16-byte aligned");
+  const int np = prefix_splits(h, B, P), ns = suffix_splits(h, B, S_cap);
+  const size_t need = part_bytes(h, B) * (np + ns);
+  if (!ws || ws_bytes < need) return fail(HYDRA_ENOMEM, "workspace too small: need %zu bytes", need);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaStream_t sa = s_aux ? reinterpret_cast<cudaStream_t>(s_aux) : s;
+  PartsView all = parts_in_ws(ws, h, B, np + ns);
+  PartsView pre = all, suf = all;
+  suf.o = all.o + all.o_stride * np;
+  suf.lse = all.lse + all.lse_stride * np;
+  const int64_t rows = B * h->num_q_heads;
+
+  if (sa != s) {
+    if (cudaEventRecord(events().fork, s) != cudaSuccess || cudaStreamWaitEvent(sa, events().fork, 0) != cudaSuccess)
+      return cuda_fail("fork");
+  }
+  if (P > 0) {
+    st = run_prefix(h, B, q, q_sb, q_sh, P, pk, pv, kv_st, kv_sh, np, pre, sa);
+  } else {
+    st = launch_fill_neg_inf(pre.lse, rows, sa);
+    if (st) st = cuda_fail("fill");
+  }
+  if (st) return st;
+  if (S_cap > 0) {
+    st = run_suffix(h, B, q, q_sb, q_sh, sk, sv, s_sb, s_st, s_sh, S_cap, lens, ns, suf, s);
+  } else {
+    st = launch_fill_neg_inf(suf.lse, rows, s);
+    if (st) st = cuda_fail("fill");
+  }
+  if (st) return st;
+  if (sa != s) {
+    if (cudaEventRecord(events().join, sa) != cudaSuccess || cudaStreamWaitEvent(s, events().join, 0) != cudaSuccess)
+      return cuda_fail("join");
+  }
+  return run_combine(rows, h->head_dim, np + ns, all, out, out_dtype, lse_out, s);
+}
+
+// ------------------------------------------------------------------ sharing tree
+struct hydra_tree {
+  int32_t n_nodes = 0;
+  int64_t B = 0;
+  std::vector<int32_t> parent, depth, leaf_of_seq;
+  std::vector<int64_t> node_off, node_len;
+  std::vector<int32_t> grp_off, grp_seq;  // CSR: sequences of node n = grp_seq[grp_off[n]..grp_off[n+1])
+  int32_t max_depth = 0;                  // nodes on the longest root->leaf path
+  int32_t *d_grp_seq = nullptr;           // device copy of grp_seq
+  mutable std::mutex mu;
+  mutable std::map<std::pair<int, int>, std::pair<PrefixTask *, int>> work;  // (g, splits) -> device tasks
+};
+
+extern "C" hydra_status hydra_tree_create(const int32_t *parent, const int64_t *node_off, const int64_t *node_len,
+                                          int32_t n_nodes, const int32_t *leaf_of_seq, int64_t B,
+                                          struct hydra_tree **out) {
+  if (!out) return fail(HYDRA_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!parent || !node_off || !node_len || !leaf_of_seq) return fail(HYDRA_EINVAL, "null host array");
+  if (n_nodes <= 0) return fail(HYDRA_ESHAPE, "tree needs at least one node");
+  if (B <= 0) return fail(HYDRA_ESHAPE, "B must be > 0");
+  int root = -1;
+  for (int n = 0; n < n_nodes; ++n) {
+    if (parent[n] == -1) {
+      if (root >= 0) return fail(HYDRA_ESHAPE, "multiple roots (nodes %d and %d)", root, n);
+      root = n;
+    } else if (parent[n] < 0 || parent[n] >= n_nodes || parent[n] == n) {
+      return fail(HYDRA_ESHAPE, "node %d has invalid parent %d", n, parent[n]);
+    }
+    if (node_off[n] < 0 || node_len[n] < 0) return fail(HYDRA_ESHAPE, "node %d has negative offset/length", n);
+  }
+  if (root < 0) return fail(HYDRA_ESHAPE, "no root (parent == -1)");
+  auto t = new hydra_tree();
+  t->n_nodes = n_nodes;
+  t->B = B;
+  t->parent.assign(parent, parent + n_nodes);
+  t->node_off.assign(node_off, node_off + n_nodes);
+  t->node_len.assign(node_len, node_len + n_nodes);
+  t->leaf_of_seq.assign(leaf_of_seq, leaf_of_seq + B);
+  t->depth.assign(n_nodes, -1);
+  for (int n = 0; n < n_nodes; ++n) {  // depth by walking to the root; detects cycles
+    int d = 0, x = n;
+    while (x != root) {
+      x = t->parent[x];
+      if (++d > n_nodes) {
+        delete t;
+        return fail(HYDRA_ESHAPE, "cycle through node %d", n);
+      }
+    }
+    t->depth[n] = d;
+    if (n != root && t->node_len[n] < 1) {
+      delete t;
+      return fail(HYDRA_ESHAPE, "non-root node %d is empty (only the root may be empty, S:186)", n);
+    }
+  }
+  std::vector<int> n_children(n_nodes, 0), n_users(n_nodes, 0);
+  for (int n = 0; n < n_nodes; ++n)
+    if (n != root) n_children[t->parent[n]]++;
+  for (int64_t b = 0; b < B; ++b) {
+    const int lf = leaf_of_seq[b];
+    if (lf < 0 || lf >= n_nodes) {
+      delete t;
+      return fail(HYDRA_ESHAPE, "sequence %lld assigned to invalid node %d", (long long)b, lf);
+    }
+    if (n_children[lf]) {
+      delete t;
+      return fail(HYDRA_ESHAPE, "sequence %lld assigned to non-leaf node %d", (long long)b, lf);
+    }
+    n_users[lf]++;
+  }
+  for (int n = 0; n < n_nodes; ++n)
+    if (!n_children[n] && !n_users[n]) {
+      delete t;
+      return fail(HYDRA_ESHAPE, "leaf node %d has no sequences (S:191)", n);
+    }
+  // CSR groups: ascending sequence ids of every sequence whose path passes through n
+  std::vector<std::vector<int32_t>> groups(n_nodes);
+  for (int64_t b = 0; b < B; ++b)
+    for (int x = leaf_of_seq[b];; x = t->parent[x]) {
+      groups[x].push_back((int32_t)b);
+      if (x == root) break;
+    }
+  t->grp_off.assign(n_nodes + 1, 0);
+  for (int n = 0; n < n_nodes; ++n) t->grp_off[n + 1] = t->grp_off[n] + (int32_t)groups[n].size();
+  for (int n = 0; n < n_nodes; ++n) t->grp_seq.insert(t->grp_seq.end(), groups[n].begin(), groups[n].end());
+  for (int n = 0; n < n_nodes; ++n) t->max_depth = std::max(t->max_depth, t->depth[n] + 1);
+  if (cudaMalloc(&t->d_grp_seq, sizeof(int32_t) * std::max<size_t>(1, t->grp_seq.size())) != cudaSuccess ||
+      cudaMemcpy(t->d_grp_seq, t->grp_seq.data(), sizeof(int32_t) * t->grp_seq.size(), cudaMemcpyHostToDevice) !=
+          cudaSuccess) {
+    cudaFree(t->d_grp_seq);
+    delete t;
+    return cuda_fail("tree device upload");
+  }
+  *out = t;
+  return HYDRA_OK;
+}
+
+extern "C" void hydra_tree_destroy(struct hydra_tree *t) {
+  if (!t) return;
+  for (auto &kv : t->work) cudaFree(kv.second.first);
+  cudaFree(t->d_grp_seq);
+  delete t;
+}
+
+extern "C" int32_t hydra_tree_depth(const struct hydra_tree *t) { return t ? t->max_depth : -1; }
+
+extern "C" int64_t hydra_tree_group_size(const struct hydra_tree *t, int32_t node) {
+  if (!t || node < 0 || node >= t->n_nodes) return -1;
+  return t->grp_off[node + 1] - t->grp_off[node];
+}
+
+static int tree_prefix_splits(const hydra_heads *h, const hydra_tree *t) {
+  if (g_prefix_splits > 0) return (int)g_prefix_splits;
+  if (!use_tc(h)) {
+    int64_t maxlen = 0;
+    for (auto L : t->node_len) maxlen = std::max(maxlen, L);
+    return prefix_splits_simt(h, t->B, maxlen);
+  }
+  // total tiles over all non-empty nodes, longest node sets the per-tile work
+  const int g = h->num_q_heads / h->num_kv_heads;
+  int64_t tiles = 0, maxlen = 0;
+  for (int n = 0; n < t->n_nodes; ++n) {
+    if (t->node_len[n] <= 0) continue;
+    tiles += ((int64_t)(t->grp_off[n + 1] - t->grp_off[n]) * g + 127) / 128;
+    maxlen = std::max(maxlen, t->node_len[n]);
+  }
+  return prefix_splits_tc(tiles * h->num_kv_heads, maxlen);
+}
+
+extern "C" size_t hydra_tree_workspace_size(const hydra_heads *h, const struct hydra_tree *t, int64_t S_cap) {
+  if (!t || check_heads(h) != HYDRA_OK) return 0;
+  return part_bytes(h, t->B) * (size_t)(t->max_depth * tree_prefix_splits(h, t) + suffix_splits(h, t->B, S_cap));
+}
+
+extern "C" hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra_tree *t, const void *q, int64_t q_sb,
+                                        int64_t q_sh, const void *node_k, const void *node_v, int64_t kv_st,
+                                        int64_t kv_sh, const void *sk, const void *sv, int64_t s_sb, int64_t s_st,
+                                        int64_t s_sh, int64_t S_cap, const int32_t *lens, void *out,
+                                        hydra_dtype out_dtype, float *lse_out, void *ws, size_t ws_bytes,
+                                        void *stream) {
+  hydra_status st = check_heads(h);
+  if (st) return st;
+  if (!t) return fail(HYDRA_EINVAL, "tree is NULL");
+  const int64_t B = t->B;
+  int64_t T = 0;
+  for (int n = 0; n < t->n_nodes; ++n) T = std::max(T, t->node_off[n] + t->node_len[n]);
+  if (!q || !out || (T > 0 && (!node_k || !node_v)) || (S_cap > 0 && (!sk || !sv || !lens)))
+    return fail(HYDRA_EINVAL, "null pointer argument");
+  if (out_dtype != HYDRA_BF16 && out_dtype != HYDRA_F32) return fail(HYDRA_EUNSUPPORTED, "out_dtype must be BF16 or F32");
+  const size_t es = elem_size(h->dtype);
+  if (!aligned16(q, es, {q_sb, q_sh}) || (T > 0 && (!aligned16(node_k, es, {kv_st, kv_sh}) || !aligned16(node_v, es, {}))) ||
+      (S_cap > 0 && (!aligned16(sk, es, {s_sb, s_st, s_sh}) || !aligned16(sv, es, {}))))
+    return fail(HYDRA_EINVAL, "q/k/v base pointers and strides must be 16-byte aligned");
+  const int np = tree_prefix_splits(h, t);
+  const int ns = suffix_splits(h, B, S_cap);
+  const int n_parts = t->max_depth * np + ns;
+  const size_t need = part_bytes(h, B) * n_parts;
+  if (!ws || ws_bytes < need) return fail(HYDRA_ENOMEM, "workspace too small: need %zu bytes", need);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int g = h->num_q_heads / h->num_kv_heads;
+  const int64_t rows = B * h->num_q_heads;
+  PartsView all = parts_in_ws(ws, h, B, n_parts);
+  // Sequences whose path is shorter than max_depth leave slots empty: mark all node slots -inf.
+  st = launch_fill_neg_inf(all.lse, all.lse_stride * (int64_t)(t->max_depth * np), s);
+  if (st) return cuda_fail("fill");
+  const float sl2 = scale_of(h) * 1.4426950408889634f;
+
+  if (use_tc(h) && T > 0) {
+    PrefixTask *d_tasks = nullptr;
+    int n_tasks = 0;
+    {
+      std::lock_guard<std::mutex> lock(t->mu);
+      auto it = t->work.find({g, np});
+      if (it == t->work.end()) {
+        std::vector<PrefixTask> tasks;
+        for (int n = 0; n < t->n_nodes; ++n) {
+          if (t->node_len[n] <= 0) continue;
+          const int32_t ns_ = t->grp_off[n + 1] - t->grp_off[n];
+          const int tiles = (int)(((int64_t)ns_ * g + 127) / 128);
+          for (int tl = 0; tl < tiles; ++tl)
+            tasks.push_back(PrefixTask{t->node_off[n], t->node_len[n], t->grp_off[n], ns_, t->depth[n] * np, tl});
+        }
+        PrefixTask *dt = nullptr;
+        if (!tasks.empty()) {
+          if (cudaMalloc(&dt, sizeof(PrefixTask) * tasks.size()) != cudaSuccess ||
+              cudaMemcpy(dt, tasks.data(), sizeof(PrefixTask) * tasks.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+            return cuda_fail("tree work-list upload");
+        }
+        it = t->work.emplace(std::make_pair(g, np), std::make_pair(dt, (int)tasks.size())).first;
+      }
+      d_tasks = it->second.first;
+      n_tasks = it->second.second;
+    }
+    if (n_tasks > 0) {
+      PrefixTcArgs a{};
+      a.q = q;
+      a.q_sb = q_sb;
+      a.q_sh = q_sh;
+      a.k = node_k;
+      a.v = node_v;
+      a.kv_st = kv_st;
+      a.kv_sh = kv_sh;
+      a.kv_total = T;
+      a.Hq = h->num_q_heads;
+      a.Hkv = h->num_kv_heads;
+      a.g = g;
+      a.scale_log2 = sl2;
+      a.tasks = d_tasks;
+      a.n_tasks = n_tasks;
+      a.seq_list = t->d_grp_seq;
+      a.n_splits = np;
+      a.o = all.o;
+      a.lse = all.lse;
+      a.o_slot_stride = all.o_stride;
+      a.lse_slot_stride = all.lse_stride;
+      a.debug_variant = (int32_t)g_tc_debug;
+      st = launch_prefix_tc(a, s);
+      if (st) return cuda_fail("tree prefix tcgen05 launch");
+    }
+  } else {
+    for (int n = 0; n < t->n_nodes; ++n) {
+      if (t->node_len[n] <= 0) continue;
+      DecodeParams p{};
+      p.q = q;
+      p.q_sb = q_sb;
+      p.q_sh = q_sh;
+      p.k = node_k;
+      p.v = node_v;
+      p.kv_sb = 0;
+      p.kv_st = kv_st;
+      p.kv_sh = kv_sh;
+      p.kv_tok_off = t->node_off[n];
+      p.lens = nullptr;
+      p.len_uniform = t->node_len[n];
+      p.seq_map = t->d_grp_seq + t->grp_off[n];
+      p.n_seq = t->grp_off[n + 1] - t->grp_off[n];
+      p.Hq = h->num_q_heads;
+      p.Hkv = h->num_kv_heads;
+      p.g = g;
+      p.scale_log2 = sl2;
+      p.n_splits = np;
+      p.split_len = (t->node_len[n] + np - 1) / np;
+      p.heads_per_cta = heads_per_cta(g);
+      p.o = all.o + all.o_stride * (int64_t)(t->depth[n] * np);
+      p.lse = all.lse + all.lse_stride * (int64_t)(t->depth[n] * np);
+      p.o_split_stride = all.o_stride;
+      p.lse_split_stride = all.lse_stride;
+      st = launch_decode(p, h->dtype, h->head_dim, s);
+      if (st) return st == HYDRA_ECUDA ? cuda_fail("tree node SIMT launch") : fail(st, "tree node SIMT");
+    }
+  }
+  PartsView suf = all;
+  suf.o = all.o + all.o_stride * (int64_t)(t->max_depth * np);
+  suf.lse = all.lse + all.lse_stride * (int64_t)(t->max_depth * np);
+  if (S_cap > 0) {
+    st = run_suffix(h, B, q, q_sb, q_sh, sk, sv, s_sb, s_st, s_sh, S_cap, lens, ns, suf, s);
+    if (st) return st;
+  } else {
+    st = launch_fill_neg_inf(suf.lse, rows, s);
+    if (st) return cuda_fail("fill");
+  }
+  return run_combine(rows, h->head_dim, n_parts, all, out, out_dtype, lse_out, s);
+}

@@ -1,0 +1,133 @@
+// combine.cu -- n-ary LSE combine (Eq. 5 P:98-105 in App. B's
+// max-stabilised form P:333-344, folded over n parts; associativity S:154).
+//
+// One warp per output row.  For row r:
+//   m   = max_p lse_p[r]                     (parts with lse = -inf are empty: skipped)
+//   w_p = exp(lse_p[r] - m)
+//   O   = sum_p w_p * O_p[r] / sum_p w_p     -> out (bf16 RNE or f32)
+//   lse = m + ln(sum_p w_p)                  (the merged LSE a recursive combine needs)
+// Partial outputs are read with 16-byte vector loads (d % 128 == 0 for f32 parts,
+// d % 256 == 0 for f16 parts), otherwise element-wise.  HBM-bound: it reads
+// n*(d*sizeof(O)+4) and writes d*sizeof(out)(+4) bytes per row.
+#include "common.cuh"
+#include "internal.h"
+
+namespace hydra {
+
+template <typename OT>
+__device__ __forceinline__ float ld_part(const OT *p);
+template <>
+__device__ __forceinline__ float ld_part<float>(const float *p) { return __ldg(p); }
+template <>
+__device__ __forceinline__ float ld_part<__half>(const __half *p) { return __half2float(__ldg(p)); }
+
+template <typename OT, typename OutT, int VEC>
+__global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
+  const int64_t row = (int64_t)blockIdx.x * 8 + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= p.rows) return;
+  const OT *o_parts = reinterpret_cast<const OT *>(p.o_parts);
+
+  float m = -INFINITY;
+  for (int q = 0; q < p.n_parts; ++q) m = fmaxf(m, __ldg(p.lse_parts + q * p.lse_part_stride + row));
+  OutT *out = reinterpret_cast<OutT *>(p.out) + row * p.d;
+  if (m == -INFINITY) {  // every part empty: sentinel (0, -inf)
+    for (int e = lane; e < p.d; e += 32) out[e] = OutT(0.f);
+    if (p.lse_out && lane == 0) p.lse_out[row] = -INFINITY;
+    return;
+  }
+  float acc[VEC > 0 ? VEC : 1];
+  const int per_lane = VEC > 0 ? VEC : 0;
+  (void)per_lane;
+  float den = 0.f;
+  if constexpr (VEC > 0) {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
+    for (int q = 0; q < p.n_parts; ++q) {
+      const float lq = __ldg(p.lse_parts + q * p.lse_part_stride + row);
+      if (lq == -INFINITY) continue;
+      const float w = p.inject_bug ? 1.f : expf(lq - m);
+      den += w;
+      const OT *src = o_parts + q * p.o_part_stride + row * p.d;
+#pragma unroll
+      for (int c = 0; c < VEC / 4; ++c) {
+        const int e = (c * 32 + lane) * 4;
+        float f[4];
+        if constexpr (sizeof(OT) == 4) {
+          const float4 v = __ldg(reinterpret_cast<const float4 *>(src + e));
+          f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w;
+        } else {
+          const uint2 v = __ldg(reinterpret_cast<const uint2 *>(src + e));
+          const __half2 a = *reinterpret_cast<const __half2 *>(&v.x);
+          const __half2 b = *reinterpret_cast<const __half2 *>(&v.y);
+          f[0] = __low2float(a); f[1] = __high2float(a); f[2] = __low2float(b); f[3] = __high2float(b);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[c * 4 + i] = fmaf(w, f[i], acc[c * 4 + i]);
+      }
+    }
+    const float inv = 1.f / den;
+#pragma unroll
+    for (int c = 0; c < VEC / 4; ++c) {
+      const int e = (c * 32 + lane) * 4;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) out[e + i] = OutT(acc[c * 4 + i] * inv);
+    }
+  } else {
+    for (int q = 0; q < p.n_parts; ++q) {
+      const float lq = __ldg(p.lse_parts + q * p.lse_part_stride + row);
+      if (lq != -INFINITY) den += p.inject_bug ? 1.f : expf(lq - m);
+    }
+    const float inv = 1.f / den;
+    for (int e = lane; e < p.d; e += 32) {
+      float a = 0.f;
+      for (int q = 0; q < p.n_parts; ++q) {
+        const float lq = __ldg(p.lse_parts + q * p.lse_part_stride + row);
+        if (lq == -INFINITY) continue;
+        const float w = p.inject_bug ? 1.f : expf(lq - m);
+        a = fmaf(w, ld_part<OT>(o_parts + q * p.o_part_stride + row * p.d + e), a);
+      }
+      out[e] = OutT(a * inv);
+    }
+  }
+  if (p.lse_out && lane == 0) p.lse_out[row] = m + logf(den);
+}
+
+template <typename OT, typename OutT>
+static cudaError_t launch_c(const CombineParams &p, cudaStream_t s) {
+  const dim3 grid((unsigned)((p.rows + 7) / 8));
+  if (p.d == 128)
+    combine_kernel<OT, OutT, 4><<<grid, 256, 0, s>>>(p);
+  else if (p.d == 256)
+    combine_kernel<OT, OutT, 8><<<grid, 256, 0, s>>>(p);
+  else
+    combine_kernel<OT, OutT, 0><<<grid, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+hydra_status launch_combine(const CombineParams &p, hydra_dtype o_dtype, hydra_dtype out_dtype,
+                            cudaStream_t s) {
+  if (p.rows == 0) return HYDRA_OK;
+  cudaError_t e;
+  if (o_dtype == HYDRA_F32 && out_dtype == HYDRA_BF16) e = launch_c<float, __nv_bfloat16>(p, s);
+  else if (o_dtype == HYDRA_F32 && out_dtype == HYDRA_F32) e = launch_c<float, float>(p, s);
+  else if (o_dtype == HYDRA_F16 && out_dtype == HYDRA_BF16) e = launch_c<__half, __nv_bfloat16>(p, s);
+  else if (o_dtype == HYDRA_F16 && out_dtype == HYDRA_F32) e = launch_c<__half, float>(p, s);
+  else return HYDRA_EUNSUPPORTED;
+  return e == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
+}
+
+__global__ void fill_neg_inf_kernel(float *x, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = -INFINITY;
+}
+
+hydra_status launch_fill_neg_inf(float *lse, int64_t n, cudaStream_t s) {
+  if (n <= 0) return HYDRA_OK;
+  const int64_t nb = (n + 255) / 256;
+  const int blocks = (int)(nb < 4096 ? nb : 4096);
+  fill_neg_inf_kernel<<<blocks, 256, 0, s>>>(lse, n);
+  return cudaGetLastError() == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
+}
+
+}  // namespace hydra

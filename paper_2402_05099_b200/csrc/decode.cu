@@ -1,0 +1,215 @@
+// decode.cu -- memory-bound split-K decode attention (one query per sequence).
+//
+// This is the suffix kernel of the paper's decomposition ("suffix attention is
+// therefore computed normally, with a single query per sequence", §3.2 P:116;
+// App. B) and also the SIMT fallback for the prefix in the fp32
+// reference mode (the prefix then is a KV segment with batch stride 0).
+//
+// Work decomposition: one 128-thread CTA per (sequence b, KV head j, chunk of GQ
+// query heads of that group, KV split).  Each token row of K/V (d elements) is
+// read by TPR = d*sizeof(T)/16 threads with 16-byte non-caching vector loads, so a
+// warp reads 32*16 = 512 contiguous-per-row bytes per instruction; the CTA's
+// NG = 128/TPR row groups walk the tokens with stride NG, U tokens in flight per
+// group.  Scores are reduced across the TPR lanes of a row with xor-shuffles; each
+// row group keeps an online softmax state (running max m, sum l, accumulator) per
+// query head in the log2 domain; the NG states are merged through shared memory at
+// the end with the same rescaling (Eq. 5 math).  Positions >= lens[b] are never
+// loaded (poisoned padding cannot leak in).
+#include "common.cuh"
+#include "internal.h"
+
+namespace hydra {
+
+template <typename T, int D, int GQ, int U, bool kStream>
+__global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeParams p) {
+  constexpr int EPT = Vec16<T>::N;          // elements per thread per row
+  constexpr int TPR = D / EPT;              // threads per token row
+  constexpr int NG = 128 / TPR;             // row groups per CTA
+  static_assert(TPR >= 1 && TPR <= 32 && (TPR & (TPR - 1)) == 0, "bad TPR");
+
+  __shared__ float sm_m[NG][GQ];
+  __shared__ float sm_l[NG][GQ];
+  __shared__ float sm_acc[NG][GQ][D];
+
+  const int tid = threadIdx.x;
+  const int lane = tid % TPR;
+  const int grp = tid / TPR;
+  const int split = blockIdx.x;
+  const int n_chunks = p.g / GQ;
+  const int j = blockIdx.y / n_chunks;
+  const int chunk = blockIdx.y % n_chunks;
+  const int slot = blockIdx.z;
+  const int b = p.seq_map ? p.seq_map[slot] : slot;
+  const int h0 = j * p.g + chunk * GQ;
+
+  const int64_t len = p.lens ? (int64_t)p.lens[b] : p.len_uniform;
+  const int64_t t_begin = (int64_t)split * p.split_len;
+  const int64_t t_end = min(len, t_begin + p.split_len);
+
+  // query fragments, pre-scaled by scale*log2(e) so scores come out in log2 units
+  float qf[GQ][EPT];
+#pragma unroll
+  for (int i = 0; i < GQ; ++i) {
+    const T *qp = reinterpret_cast<const T *>(p.q) + (int64_t)b * p.q_sb + (int64_t)(h0 + i) * p.q_sh + lane * EPT;
+    Vec16<T>::unpack(ld_v4<false>(qp), qf[i]);
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) qf[i][e] *= p.scale_log2;
+  }
+
+  float m[GQ], l[GQ], acc[GQ][EPT];
+#pragma unroll
+  for (int i = 0; i < GQ; ++i) {
+    m[i] = -INFINITY;
+    l[i] = 0.f;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) acc[i][e] = 0.f;
+  }
+
+  const T *kb = reinterpret_cast<const T *>(p.k) + (int64_t)b * p.kv_sb + (int64_t)j * p.kv_sh + lane * EPT;
+  const T *vb = reinterpret_cast<const T *>(p.v) + (int64_t)b * p.kv_sb + (int64_t)j * p.kv_sh + lane * EPT;
+
+  // Trip count is uniform across the CTA (shuffles below need converged warps).
+  for (int64_t tb = t_begin; tb < t_end; tb += (int64_t)NG * U) {
+    uint4 kr[U], vr[U];
+    bool valid[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t t = tb + grp + (int64_t)u * NG;
+      valid[u] = t < t_end;
+      const int64_t off = (p.kv_tok_off + t) * p.kv_st;
+      if (valid[u]) {
+        kr[u] = ld_v4<kStream>(kb + off);
+        vr[u] = ld_v4<kStream>(vb + off);
+      } else {
+        kr[u] = make_uint4(0, 0, 0, 0);
+        vr[u] = make_uint4(0, 0, 0, 0);
+      }
+    }
+    float s[U][GQ];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      float kf[EPT];
+      Vec16<T>::unpack(kr[u], kf);
+#pragma unroll
+      for (int i = 0; i < GQ; ++i) {
+        float a = 0.f;
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) a = fmaf(qf[i][e], kf[e], a);
+#pragma unroll
+        for (int off = TPR / 2; off >= 1; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+        s[u][i] = valid[u] ? a : -INFINITY;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < GQ; ++i) {
+      float mx = m[i];
+#pragma unroll
+      for (int u = 0; u < U; ++u) mx = fmaxf(mx, s[u][i]);
+      if (mx == -INFINITY) continue;  // nothing valid yet (uniform across the row group)
+      const float alpha = exp2f(m[i] - mx);
+      float pu[U];
+      float ps = 0.f;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        pu[u] = exp2f(s[u][i] - mx);
+        ps += pu[u];
+      }
+      l[i] = l[i] * alpha + ps;
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) acc[i][e] *= alpha;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        float vf[EPT];
+        Vec16<T>::unpack(vr[u], vf);
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) acc[i][e] = fmaf(pu[u], vf[e], acc[i][e]);
+      }
+      m[i] = mx;
+    }
+  }
+
+  // ---- merge the NG row-group states (Eq. 5 rescaling in the log2 domain)
+#pragma unroll
+  for (int i = 0; i < GQ; ++i) {
+    if (lane == 0) {
+      sm_m[grp][i] = m[i];
+      sm_l[grp][i] = l[i];
+    }
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) sm_acc[grp][i][lane * EPT + e] = acc[i][e];
+  }
+  __syncthreads();
+  for (int idx = tid; idx < GQ * D; idx += 128) {
+    const int i = idx / D, e = idx % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int gi = 0; gi < NG; ++gi) M = fmaxf(M, sm_m[gi][i]);
+    const int h = h0 + i;
+    float *o = p.o + (int64_t)split * p.o_split_stride + ((int64_t)b * p.Hq + h) * D;
+    if (M == -INFINITY) {  // empty key set: (0, -inf) sentinel
+      o[e] = 0.f;
+      if (e == 0) p.lse[(int64_t)split * p.lse_split_stride + (int64_t)b * p.Hq + h] = -INFINITY;
+      continue;
+    }
+    float L = 0.f, A = 0.f;
+#pragma unroll
+    for (int gi = 0; gi < NG; ++gi) {
+      const float w = exp2f(sm_m[gi][i] - M);
+      L += sm_l[gi][i] * w;
+      A += sm_acc[gi][i][e] * w;
+    }
+    o[e] = A / L;
+    if (e == 0)
+      p.lse[(int64_t)split * p.lse_split_stride + (int64_t)b * p.Hq + h] = (M + log2f(L)) * HYDRA_LN2;
+  }
+}
+
+template <typename T, int D, int GQ>
+static cudaError_t launch_t(const DecodeParams &p, cudaStream_t s) {
+  const dim3 grid(p.n_splits, p.Hkv * (p.g / GQ), p.n_seq);
+  constexpr int U = (sizeof(T) == 2) ? 4 : 4;
+  if (p.kv_sb == 0)  // shared KV (prefix in SIMT mode): let L1 keep it
+    decode_attn_kernel<T, D, GQ, U, false><<<grid, 128, 0, s>>>(p);
+  else
+    decode_attn_kernel<T, D, GQ, U, true><<<grid, 128, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T, int D>
+static cudaError_t launch_d(const DecodeParams &p, cudaStream_t s) {
+  switch (p.heads_per_cta) {
+    case 1: return launch_t<T, D, 1>(p, s);
+    case 2: return launch_t<T, D, 2>(p, s);
+    case 4: return launch_t<T, D, 4>(p, s);
+    case 8: return launch_t<T, D, 8>(p, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+hydra_status launch_decode(const DecodeParams &p, hydra_dtype dt, int d, cudaStream_t s) {
+  if (p.n_seq <= 0 || p.n_splits <= 0) return HYDRA_OK;
+  cudaError_t e = cudaErrorInvalidValue;
+  if (dt == HYDRA_BF16) {
+    switch (d) {
+      case 16: e = launch_d<__nv_bfloat16, 16>(p, s); break;
+      case 32: e = launch_d<__nv_bfloat16, 32>(p, s); break;
+      case 64: e = launch_d<__nv_bfloat16, 64>(p, s); break;
+      case 128: e = launch_d<__nv_bfloat16, 128>(p, s); break;
+      case 256: e = launch_d<__nv_bfloat16, 256>(p, s); break;
+      default: return HYDRA_EUNSUPPORTED;
+    }
+  } else if (dt == HYDRA_F32) {
+    switch (d) {
+      case 16: e = launch_d<float, 16>(p, s); break;
+      case 32: e = launch_d<float, 32>(p, s); break;
+      case 64: e = launch_d<float, 64>(p, s); break;
+      case 128: e = launch_d<float, 128>(p, s); break;
+      default: return HYDRA_EUNSUPPORTED;
+    }
+  } else {
+    return HYDRA_EUNSUPPORTED;
+  }
+  return e == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
+}
+
+}  // namespace hydra

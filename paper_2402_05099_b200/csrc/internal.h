@@ -1,0 +1,87 @@
+// internal.h -- launch parameter blocks and launchers behind the C ABI (not exported).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hydra.h"
+
+namespace hydra {
+
+// ---------------------------------------------------------------- SIMT decode kernel
+// One CTA = one (sequence-slot b, KV head j, head chunk, KV split).  Used for the
+// suffix (§3.2), the fp32 reference-mode prefix / tree nodes, and odd shapes.
+struct DecodeParams {
+  const void *q;
+  int64_t q_sb, q_sh;
+  const void *k, *v;
+  int64_t kv_sb, kv_st, kv_sh;  // kv_sb == 0: every sequence reads the same KV (shared prefix)
+  int64_t kv_tok_off;           // token offset added to every position (tree node offset)
+  const int32_t *lens;          // device [n_seq]; nullptr -> len_uniform for every sequence
+  int64_t len_uniform;
+  const int32_t *seq_map;       // device [n_seq] slot -> sequence id; nullptr -> identity
+  int32_t n_seq, Hq, Hkv, g;
+  float scale_log2;             // softmax scale * log2(e)
+  int32_t n_splits;
+  int64_t split_len;            // tokens per split
+  int32_t heads_per_cta;        // GQ: query heads of one KV group handled per CTA
+  float *o;                     // [split][B][Hq][d] partial outputs (fp32, normalised)
+  float *lse;                   // [split][B][Hq] natural-log LSE
+  int64_t o_split_stride, lse_split_stride;
+};
+
+hydra_status launch_decode(const DecodeParams &p, hydra_dtype dt, int d, cudaStream_t s);
+
+// ---------------------------------------------------------------- combine
+struct CombineParams {
+  int64_t rows;
+  int32_t d, n_parts;
+  const void *o_parts;
+  int64_t o_part_stride;
+  const float *lse_parts;
+  int64_t lse_part_stride;
+  void *out;
+  float *lse_out;
+  int32_t inject_bug;
+};
+hydra_status launch_combine(const CombineParams &p, hydra_dtype o_dtype, hydra_dtype out_dtype,
+                            cudaStream_t s);
+// Fill lse[i] = -inf for i < n (marks empty partial slots).
+hydra_status launch_fill_neg_inf(float *lse, int64_t n, cudaStream_t s);
+
+// ---------------------------------------------------------------- tcgen05 prefix kernel
+// A work item of the tensor-core prefix kernel: one KV segment (flat prefix or a
+// tree node) and the list of sequences whose stacked queries attend to it.
+struct PrefixTask {
+  int64_t kv_off;    // first token of the segment in the pooled K/V
+  int64_t kv_len;    // tokens in the segment
+  int32_t seq_off;   // offset into the sequence list
+  int32_t n_seq;     // sequences in the group
+  int32_t slot;      // output slot (tree depth * splits); split index is added
+  int32_t tile;      // query tile index within the group (128 stacked rows each)
+};
+
+struct PrefixTcArgs {
+  const void *q;
+  int64_t q_sb, q_sh;
+  const void *k, *v;      // pooled [T, Hkv, 128] bf16
+  int64_t kv_st, kv_sh;
+  int64_t kv_total;       // T (tokens addressable by the tensor maps)
+  int32_t Hq, Hkv, g;
+  float scale_log2;
+  // flat mode (tasks == nullptr): one segment [0, P) for B sequences
+  int64_t P;
+  int32_t B;
+  // task mode
+  const PrefixTask *tasks;   // device
+  int32_t n_tasks;
+  const int32_t *seq_list;   // device
+  int32_t n_splits;
+  float *o, *lse;
+  int64_t o_slot_stride, lse_slot_stride;
+  int32_t debug_variant;
+};
+bool prefix_tc_supported(const hydra_heads *h);
+hydra_status launch_prefix_tc(const PrefixTcArgs &a, cudaStream_t s);
+int device_sm_count();
+
+}  // namespace hydra

@@ -1,0 +1,243 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle, element by element.
+
+Gates (north_star): bf16 inputs -> max|d| <= 2e-2, mean|d| <= 2e-3 on the delivered bf16
+output, plus |dLSE| <= 1e-3; fp32 reference mode -> 1e-5.  Inputs use the 'mixed' /
+'boundary' needle distributions and NaN-poisoned suffix padding (SURVEY §8(c)
+sensitivity analysis), sizes span several 128-token tiles with ragged tails.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests.util import assert_parity, errors, problem_to, tree_to
+
+hydra = pytest.importorskip("paper_2402_05099_b200")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _reset_config():
+    for k in ("prefix_impl", "prefix_splits", "suffix_splits", "tc_debug_variant"):
+        hydra.set_config(k, 0)
+    yield
+    for k in ("prefix_impl", "prefix_splits", "suffix_splits", "tc_debug_variant"):
+        hydra.set_config(k, 0)
+
+
+DEV = "cuda:0"
+
+
+def run_flat(pb, aux=False, **kw):
+    t = problem_to(pb, DEV)
+    aux_stream = torch.cuda.Stream() if aux else None
+    out, lse = hydra.hydragen_attention(t["q"], t["pk"], t["pv"], t["sk"], t["sv"], t["lens"], return_lse=True,
+                                        aux_stream=aux_stream, **kw)
+    torch.cuda.synchronize()
+    return out, lse
+
+
+# ---------------------------------------------------------------- C1 tiny, fp32 reference mode
+@pytest.mark.parametrize("Hq,Hkv", [(2, 1), (4, 2)])
+@pytest.mark.parametrize("dist", ["plain", "mixed", "boundary"])
+def test_tiny_fp32(Hq, Hkv, dist):
+    pb = synth.make_problem(4, Hq, Hkv, 16, 32, 12, lens=[5, 8, 10, 12], dtype="f32", dist=dist, seed=1)
+    out, lse = run_flat(pb)
+    ref, lref = oracle.flat_attention(pb)
+    assert_parity(out, ref, lse, lref, dtype="f32", what="C1")
+
+
+# ---------------------------------------------------------------- prefix kernel (tcgen05)
+PREFIX_SHAPES = [
+    # B, Hq, Hkv, P
+    (3, 4, 2, 300),     # GQA g=2, ragged tail, 1 q-tile
+    (40, 8, 8, 1000),   # MHA
+    (300, 4, 1, 257),   # g=4 -> 1200 stacked rows = 10 tiles, one token past a tile
+    (1, 1, 1, 1),       # single row, single token
+    (130, 1, 1, 128),   # exactly one KV block, 2 q-tiles (ragged rows)
+    (16, 32, 8, 2048),  # Llama-3 GQA shape, g=4
+]
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,P", PREFIX_SHAPES)
+@pytest.mark.parametrize("dist", ["mixed", "boundary"])
+def test_prefix_tc_parity(B, Hq, Hkv, P, dist):
+    pb = synth.make_problem(B, Hq, Hkv, 128, P, 1, dtype="bf16", dist=dist, seed=3)
+    t = problem_to(pb, DEV)
+    o, lse = hydra.prefix_attn(t["q"], t["pk"], t["pv"])
+    torch.cuda.synchronize()
+    ref, lref = oracle.prefix_only(pb)
+    assert_parity(o, ref, lse, lref, what=f"prefix {B},{Hq},{Hkv},{P}")
+
+
+@pytest.mark.parametrize("splits", [1, 2, 3, 7])
+def test_prefix_tc_splits(splits):
+    hydra.set_config("prefix_splits", splits)
+    pb = synth.make_problem(20, 8, 2, 128, 1100, 1, dtype="bf16", dist="mixed", seed=4)
+    t = problem_to(pb, DEV)
+    o, lse = hydra.prefix_attn(t["q"], t["pk"], t["pv"])
+    torch.cuda.synchronize()
+    ref, lref = oracle.prefix_only(pb)
+    assert_parity(o, ref, lse, lref, what=f"prefix splits={splits}")
+
+
+def test_prefix_simt_bf16():
+    hydra.set_config("prefix_impl", 1)
+    pb = synth.make_problem(9, 8, 2, 128, 333, 1, dtype="bf16", dist="mixed", seed=5)
+    t = problem_to(pb, DEV)
+    o, lse = hydra.prefix_attn(t["q"], t["pk"], t["pv"])
+    torch.cuda.synchronize()
+    ref, lref = oracle.prefix_only(pb)
+    assert_parity(o, ref, lse, lref, what="prefix SIMT")
+
+
+# ---------------------------------------------------------------- suffix kernel
+@pytest.mark.parametrize("B,Hq,Hkv,d,S", [(7, 8, 8, 128, 300), (5, 16, 4, 128, 77), (6, 16, 1, 128, 40),
+                                          (4, 8, 2, 64, 129), (3, 32, 2, 128, 64)])
+def test_suffix_parity(B, Hq, Hkv, d, S):
+    rng = np.random.default_rng(B * S)
+    lens = rng.integers(0, S + 1, B)
+    lens[0] = S
+    pb = synth.make_problem(B, Hq, Hkv, d, 0, S, lens=lens, dtype="bf16", dist="mixed", seed=6)
+    t = problem_to(pb, DEV)
+    o, lse = hydra.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
+    torch.cuda.synchronize()
+    ref, lref = oracle.suffix_only(pb)
+    assert_parity(o, ref, lse, lref, what="suffix")
+
+
+@pytest.mark.parametrize("splits", [1, 2, 5])
+def test_suffix_splits(splits):
+    hydra.set_config("suffix_splits", splits)
+    pb = synth.make_problem(6, 8, 2, 128, 0, 200, lens=[200, 3, 0, 150, 64, 1], dtype="bf16", dist="boundary",
+                            seed=7)
+    t = problem_to(pb, DEV)
+    o, lse = hydra.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
+    torch.cuda.synchronize()
+    ref, lref = oracle.suffix_only(pb)
+    assert_parity(o, ref, lse, lref, what=f"suffix splits={splits}")
+
+
+# ---------------------------------------------------------------- composite (App. B)
+COMPOSITE = [
+    (4, 8, 1, 128, 300, 40),     # paper microbenchmark head shape (8 q / 1 kv), ragged
+    (32, 32, 32, 128, 700, 64),  # CodeLlama-7b head shape (MHA)
+    (24, 32, 8, 128, 513, 33),   # Llama-3 GQA
+    (5, 4, 2, 64, 100, 20),      # d=64 (SIMT prefix)
+]
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,d,P,S", COMPOSITE)
+@pytest.mark.parametrize("dist", ["mixed", "boundary"])
+@pytest.mark.parametrize("aux", [False, True])
+def test_composite_parity(B, Hq, Hkv, d, P, S, dist, aux):
+    rng = np.random.default_rng(P + S)
+    lens = rng.integers(S // 2, S + 1, B)
+    pb = synth.make_problem(B, Hq, Hkv, d, P, S, lens=lens, dtype="bf16", dist=dist, seed=8)
+    out, lse = run_flat(pb, aux=aux)
+    ref, lref = oracle.flat_attention(pb)
+    assert out.dtype == torch.bfloat16
+    assert_parity(out, ref, lse, lref, what="composite")
+
+
+def test_composite_f32_output_is_tighter():
+    pb = synth.make_problem(16, 8, 2, 128, 600, 50, dtype="bf16", dist="mixed", seed=9)
+    out, lse = run_flat(pb, out_dtype=torch.float32)
+    ref, _ = oracle.flat_attention(pb)
+    mx, mean, _ = errors(out, ref)
+    assert mx <= 5e-3 and mean <= 5e-4, (mx, mean)
+
+
+@pytest.mark.parametrize("P,lens", [(0, [5, 0, 9]), (200, [0, 0, 0]), (0, [0, 0, 0]), (1, [0, 1, 17]),
+                                    (129, [128, 127, 1])])
+def test_edge_cases(P, lens):
+    pb = synth.make_problem(3, 4, 2, 128, P, 17 if max(lens) <= 17 else 128, lens=lens, dtype="bf16",
+                            dist="mixed", seed=10)
+    out, lse = run_flat(pb)
+    ref, lref = oracle.flat_attention(pb)
+    if P == 0 and max(lens) == 0:  # no keys at all: out = 0, lse = -inf (reading R6)
+        assert (out.float() == 0).all() and torch.isneginf(lse).all()
+        return
+    assert_parity(out, ref, lse, lref, what=f"edge P={P} lens={lens}")
+
+
+def test_determinism_bitwise():
+    pb = synth.make_problem(64, 8, 2, 128, 1500, 100, dtype="bf16", dist="mixed", seed=11)
+    a, la = run_flat(pb)
+    b, lb = run_flat(pb)
+    assert torch.equal(a, b) and torch.equal(la, lb)
+
+
+def test_sabotage_combine_bug_is_caught(monkeypatch):
+    """dropping the rescaling factor of the combine must fail parity."""
+    pb = synth.make_problem(8, 8, 2, 128, 500, 60, dtype="bf16", dist="mixed", seed=12)
+    ref, _ = oracle.flat_attention(pb)
+    monkeypatch.setenv("HYDRA_INJECT_COMBINE_BUG", "1")
+    out, _ = run_flat(pb)
+    mx, mean, _ = errors(out, ref)
+    assert mx > 2e-2 or mean > 2e-3, "sabotaged combine passed the parity gate"
+
+
+# ---------------------------------------------------------------- tree (§3.3)
+@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_tree_parity(impl, dtype):
+    if dtype == "f32" and impl == 0:
+        pytest.skip("f32 always runs the SIMT path")
+    hydra.set_config("prefix_impl", impl)
+    parent, node_len, leaf = synth.two_level_tree(300, 3, 150, 5)
+    # add a third level under branch 1 to exercise depth > 2 and ragged paths
+    parent = list(parent) + [1]
+    node_len = list(node_len) + [70]
+    leaf = np.array(leaf)
+    leaf[:5] = 4  # branch 1's sequences now sit one level deeper
+    d = 128
+    tp = synth.make_tree_problem(parent, node_len, leaf, 8, 2, d, 40, lens=np.arange(15) % 41, dtype=dtype,
+                                 dist="mixed", seed=13)
+    t = tree_to(tp, DEV)
+    tree = hydra.Tree(tp.parent, tp.node_off, tp.node_len, tp.leaf_of_seq)
+    assert tree.depth() == 3 and tree.group_size(0) == 15 and tree.group_size(4) == 5
+    out, lse = hydra.tree_attention(t["q"], tree, t["node_k"], t["node_v"], t["sk"], t["sv"], t["lens"],
+                                    return_lse=True)
+    torch.cuda.synchronize()
+    ref, lref = oracle.tree_attention(tp)
+    assert_parity(out, ref, lse, lref, dtype=dtype, what=f"tree impl={impl}")
+    tree.destroy()
+
+
+def test_one_level_tree_equals_flat():
+    pb = synth.make_problem(20, 8, 2, 128, 400, 30, dtype="bf16", dist="mixed", seed=14)
+    t = problem_to(pb, DEV)
+    tree = hydra.Tree([-1], [0], [pb.P], np.zeros(pb.B, np.int32))
+    a = hydra.tree_attention(t["q"], tree, t["pk"], t["pv"], t["sk"], t["sv"], t["lens"])
+    b = hydra.hydragen_attention(t["q"], t["pk"], t["pv"], t["sk"], t["sv"], t["lens"])
+    torch.cuda.synchronize()
+    ref, _ = oracle.flat_attention(pb)
+    assert_parity(a, ref, what="one-level tree")
+    assert torch.equal(a, b)
+
+
+# ---------------------------------------------------------------- combine as a standalone op
+def test_combine_f16_parts_and_identity():
+    rng = np.random.default_rng(15)
+    n, rows, d = 3, 50, 128
+    o = rng.standard_normal((n, rows, d))
+    l = rng.uniform(-5, 5, (n, rows))
+    l[1, :10] = -np.inf  # empty parts are skipped
+    ref_o, ref_l = o[0], l[0]
+    for i in range(1, n):
+        ref_o, ref_l = oracle.combine(ref_o, ref_l, o[i], l[i])
+    ot = torch.tensor(o, dtype=torch.float16, device=DEV)
+    lt = torch.tensor(l, dtype=torch.float32, device=DEV)
+    out, lse = hydra.combine(ot, lt, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    ref16 = o.astype(np.float16).astype(np.float64)
+    ro, rl = ref16[0], l[0]
+    for i in range(1, n):
+        ro, rl = oracle.combine(ro, rl, ref16[i], l[i])
+    np.testing.assert_allclose(out.cpu().numpy(), ro, atol=2e-6)
+    np.testing.assert_allclose(lse.cpu().numpy(), rl, atol=2e-6)
