@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""bench.py -- decode-attention queries/s for shared-prefix attention (Hydragen) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3_16k] [--impl hydra|reference]
+
+One "step" = the whole hot path for one decode step of one attention layer over the
+configured batch: batched prefix attention (tcgen05) + per-sequence suffix attention +
+LSE combine, i.e. App. B `hydragen_attention`.  The unit is one
+decode query = one sequence's new token across all query heads.
+
+Default workload: BASELINE.json configs[2] at its headline point -- CodeLlama-13b head
+shape (40 q / 40 kv heads, d = 128), batch 1024, shared prefix 16384 tokens, suffix 256
+tokens, bf16 K/V/Q with fp32 accumulation.  For N > 1 (torchrun) the KV heads are sharded
+across ranks (40/N each, no collective): the batch and total work are fixed -> strong
+scaling; value = B / max-over-ranks step time.
+
+Inputs come from the seeded generator (`synth`, 'mixed' needle distribution), are
+resident in HBM for `value`, and total 5.7 GB per step (> 126 MB L2), so no L2 flush is
+needed between steps (stated in config.l2).  Timing: CUDA graph of one step, W warm-up
+replays, K timed replays between CUDA events after a barrier + synchronize.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c3_16k": dict(B=1024, Hq=40, Hkv=40, d=128, P=16384, S=256,
+                   name="CodeLlama-13b attention shape (40 q / 40 kv heads, d=128), B=1024, prefix 16384, suffix 256"),
+    "c3_1k": dict(B=1024, Hq=40, Hkv=40, d=128, P=1024, S=256,
+                  name="CodeLlama-13b attention shape (40 q / 40 kv heads, d=128), B=1024, prefix 1024, suffix 256"),
+    "c2": dict(B=256, Hq=32, Hkv=32, d=128, P=2048, S=128,
+               name="CodeLlama-7b attention shape (32 q / 32 kv heads, d=128), B=256, prefix 2048, suffix 128"),
+    "c4_1gpu": dict(B=512, Hq=32, Hkv=8, d=128, P=32768, S=128,
+                    name="Llama-3-8B GQA attention shape (32 q / 8 kv, d=128), B=512, prefix 32768, suffix 128"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="c3_16k", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="hydra", choices=["hydra", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU time of the oracle sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, busy_floor=0.0):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import paper_2402_05099_b200 as hydra
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        args.gpus = world
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg = dict(CONFIGS[args.config])
+    B, Hq, Hkv, d, P, S = cfg["B"], cfg["Hq"], cfg["Hkv"], cfg["d"], cfg["P"], cfg["S"]
+    if Hkv % world:
+        raise SystemExit(f"Hkv={Hkv} is not divisible by {world} GPUs (head sharding)")
+    Hq_r, Hkv_r = Hq // world, Hkv // world
+
+    t_gen = time.time()
+    pb = synth.make_problem(B, Hq_r, Hkv_r, d, P, S, dtype="bf16", dist="mixed", seed=args.seed + rank)
+    t_gen = time.time() - t_gen
+
+    def host(a):
+        return torch.from_numpy(a).view(torch.bfloat16)
+
+    hq, hpk, hpv, hsk, hsv = (host(pb.q), host(pb.pk), host(pb.pv), host(pb.sk), host(pb.sv))
+    hlens = torch.from_numpy(pb.lens.astype(np.int32))
+    q, pk, pv, sk, sv = (t.to(dev) for t in (hq, hpk, hpv, hsk, hsv))
+    lens = hlens.to(dev)
+    ws = torch.empty(hydra.attn_workspace_bytes(q, P, S, Hkv_r), dtype=torch.uint8, device=dev)
+    out = torch.empty(B, Hq_r, d, dtype=torch.bfloat16, device=dev)
+    aux = torch.cuda.Stream(device=dev, priority=-1)
+
+    def step(overlap: bool):
+        hydra.hydragen_attention(q, pk, pv, sk, sv, lens, out=out, workspace=ws, aux_stream=aux if overlap else None)
+
+    def capture(fn):
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):
+            fn()  # eager warm-up outside capture
+        torch.cuda.current_stream(dev).wait_stream(s)
+        torch.cuda.synchronize(dev)
+        with torch.cuda.graph(g):
+            fn()
+        torch.cuda.synchronize(dev)
+        return g
+
+    def time_graph(g, k, w):
+        for _ in range(w):
+            g.replay()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(k):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        ms = e0.elapsed_time(e1) / k
+        if world > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    # pick the step variant (prefix || suffix on two streams, or sequential) on a short probe
+    g_over = capture(lambda: step(True))
+    g_seq = capture(lambda: step(False))
+    probe = max(3, min(20, args.steps // 5))
+    ms_over = time_graph(g_over, probe, 2)
+    ms_seq = time_graph(g_seq, probe, 2)
+    overlap = ms_over <= ms_seq
+    g_main = g_over if overlap else g_seq
+
+    with ClockSampler(local) as clk:
+        ms = time_graph(g_main, args.steps, args.warmup)
+    clocks = clk.summary()
+
+    # per-kernel timing on their own (roofline of the dominant kernel and the prefix phase)
+    # (the composite's workspace holds (prefix + suffix) split partials, enough for either alone)
+    g_pre = capture(lambda: hydra.prefix_attn(q, pk, pv, workspace=ws))
+    g_suf = capture(lambda: hydra.suffix_attn(q, sk, sv, lens, workspace=ws))
+    kk = max(5, args.steps // 4)
+    ms_pre = time_graph(g_pre, kk, 3)
+    ms_suf = time_graph(g_suf, kk, 3)
+
+    pk_meas = peaks()
+    hbm = float(pk_meas.get("hbm_gbs", 6650.0))
+    tc_burst = float(pk_meas.get("bf16_tflops", 1590.0))
+    tc_sust = float(pk_meas.get("bf16_tflops_sustained", 1400.0))
+    peak_src = "MEASURED_PEAKS.json" if pk_meas else "fallback (B200_PROFILING.md)"
+
+    lens_sum = int(pb.lens.sum())
+    suffix_bytes = 2 * lens_sum * Hkv_r * d * 2 + B * Hq_r * d * 2  # K+V valid rows + q (bf16)
+    prefix_flops = 4.0 * B * Hq_r * P * d
+    prefix_bytes = 2 * P * Hkv_r * d * 2
+    total_bytes = suffix_bytes + prefix_bytes + B * Hq_r * d * 2  # + bf16 output
+    suf_gbs = suffix_bytes / (ms_suf * 1e-3) / 1e9
+    pre_tflops = prefix_flops / (ms_pre * 1e-3) / 1e12
+    t_roof = max(prefix_flops / (tc_burst * 1e12), total_bytes / (hbm * 1e9))
+
+    value = B / (ms * 1e-3)
+    line = {
+        "metric": "decode-attn queries/s and % of bf16 TC peak; prefix 16K, batch 1024, 1/2/4/8 GPU",
+        "value": round(value, 1),
+        "unit": "queries/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms, 5),
+        "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (seeded PCG64 N(0,1) K/V rounded to bf16, 'mixed' needle queries)",
+        "config": {"workload": args.config, "description": cfg["name"], "B": B, "Hq": Hq, "Hkv": Hkv, "d": d,
+                   "prefix_len": P, "suffix_len": S, "parallelism": f"kv-head shard x{world}" if world > 1 else "1 GPU",
+                   "heads_per_gpu": Hq_r, "overlap_prefix_suffix": overlap,
+                   "l2": f"no flush: {total_bytes / 1e9:.2f} GB of inputs per step > 126 MB L2",
+                   "timing": "CUDA graph of one step, CUDA events over K replays, max over ranks"},
+        "roofline": {"bound": "hbm", "kernel": "suffix split-K GEMV (decode_attn_kernel)",
+                     "achieved": round(suf_gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(suf_gbs / hbm, 4),
+                     "traffic": None, "algorithmic_bytes_per_launch": suffix_bytes,
+                     "launch_ms": round(ms_suf, 5), "peak_source": peak_src},
+        "prefix_phase": {"bound": "tensor", "kernel": "prefix_tc_kernel (tcgen05)", "achieved": round(pre_tflops, 1),
+                         "unit": "TFLOP/s", "peak_burst": tc_burst, "frac_of_measured": round(pre_tflops / tc_burst, 4),
+                         "frac_of_spec_2250": round(pre_tflops / 2250.0, 4), "flops_per_launch": prefix_flops,
+                         "launch_ms": round(ms_pre, 5)},
+        "step_roofline": {"t_roof_ms": round(t_roof * 1e3, 5), "frac": round(t_roof * 1e3 / ms, 4),
+                          "ms_sequential": round(ms_seq, 5), "ms_overlap": round(ms_over, 5)},
+        "clocks": clocks,
+        "gpu_launches": args.steps * 3,
+    }
+
+    if not args.no_e2e:
+        line["e2e"] = e2e_leg(args, hydra, torch, dev, world, (hq, hpk, hpv, hsk, hsv, hlens),
+                              (q, pk, pv, sk, sv, lens), ws, out, B)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(pb, args.cpu_seconds)
+    line["gen_seconds"] = round(t_gen, 1)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def e2e_leg(args, hydra, torch, dev, world, host_t, dev_t, ws, out, B):
+    """Same metric through the public API with HOST inputs: H2D of every input + compute + D2H of out."""
+    import torch.distributed as dist
+
+    pinned = [t.pin_memory() for t in host_t]
+    h2d = sum(t.numel() * t.element_size() for t in pinned)
+    hout = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+    d2h = hout.numel() * hout.element_size()
+    q, pk, pv, sk, sv, lens = dev_t
+
+    def one():
+        for src, dst in zip(pinned, dev_t):
+            dst.copy_(src, non_blocking=True)
+        hydra.hydragen_attention(q, pk, pv, sk, sv, lens, out=out, workspace=ws)
+        hout.copy_(out, non_blocking=True)
+
+    one()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.e2e_steps):
+        one()
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = e0.elapsed_time(e1) / args.e2e_steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return {"value": round(B / (ms * 1e-3), 1), "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(ms, 3), "steps": args.e2e_steps}
+
+
+def cpu_baseline(pb, target_s: float):
+    """The fp64 oracle (oracle/), as it stands, on a bounded sample of the same workload."""
+    import numpy as np
+
+    import oracle
+
+    cores = oracle.max_threads()
+    Hq = pb.Hq
+
+    def rows_for(nseq):
+        bb, hh = np.meshgrid(np.arange(nseq), np.arange(Hq), indexing="ij")
+        return np.stack([bb.ravel(), hh.ravel()], 1)
+
+    n = 2
+    t0 = time.time()
+    oracle.flat_attention(pb, rows=rows_for(n))
+    dt = time.time() - t0
+    n2 = int(max(1, min(pb.B, math.floor(n * target_s / max(dt, 1e-3)))))
+    t0 = time.time()
+    oracle.flat_attention(pb, rows=rows_for(n2))
+    dt2 = time.time() - t0
+    return {"value": round(n2 / dt2, 3), "unit": "queries/s", "cores": cores, "kind": "oracle",
+            "sample": f"first {n2} of {pb.B} sequences x all {Hq} heads (prefix {pb.P} + suffix {pb.S_cap} tokens), "
+                      f"fp64 two-pass, {dt2:.1f} s",
+            "cpu_model": cpu_model()}
+
+
+def reference_arm(args):
+    """--impl reference: the fp64 CPU oracle timed on this box's host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+    import synth
+
+    cfg = dict(CONFIGS[args.config])
+    B, Hq, Hkv, d, P, S = cfg["B"], cfg["Hq"], cfg["Hkv"], cfg["d"], cfg["P"], cfg["S"]
+    budget = 150.0  # seconds for the whole --steps K --warmup W run
+    per_step = budget / max(1, args.steps + args.warmup)
+    # calibrate the sample size on a 2-sequence problem of the same shape
+    cal = synth.make_problem(2, Hq, Hkv, d, P, S, dtype="bf16", dist="mixed", seed=args.seed)
+    t0 = time.time()
+    oracle.flat_attention(cal)
+    per_seq = (time.time() - t0) / 2
+    nseq = int(max(1, min(B, per_step / max(per_seq, 1e-6))))
+    pb = synth.make_problem(nseq, Hq, Hkv, d, P, S, dtype="bf16", dist="mixed", seed=args.seed)
+    for _ in range(args.warmup):
+        oracle.flat_attention(pb)
+    t0 = time.time()
+    for _ in range(args.steps):
+        oracle.flat_attention(pb)
+    dt = (time.time() - t0) / max(1, args.steps)
+    value = nseq / dt
+    cores = oracle.max_threads()
+    line = {
+        "metric": "decode-attn queries/s and % of bf16 TC peak; prefix 16K, batch 1024, 1/2/4/8 GPU",
+        "value": round(value, 3), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded PCG64 N(0,1) K/V rounded to bf16, 'mixed' needle queries)",
+        "config": {"workload": args.config, "description": cfg["name"], "B": B, "Hq": Hq, "Hkv": Hkv, "d": d,
+                   "prefix_len": P, "suffix_len": S},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(value, 3), "unit": "queries/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{nseq} of {B} sequences x all {Hq} heads per step, fp64 two-pass",
+                         "cpu_model": cpu_model()},
+        "e2e": {"value": round(value, 3), "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

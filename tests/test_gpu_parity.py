@@ -235,9 +235,10 @@ def test_combine_f16_parts_and_identity():
     lt = torch.tensor(l, dtype=torch.float32, device=DEV)
     out, lse = hydra.combine(ot, lt, out_dtype=torch.float32)
     torch.cuda.synchronize()
-    ref16 = o.astype(np.float16).astype(np.float64)
-    ro, rl = ref16[0], l[0]
+    ref16 = ot.cpu().double().numpy()  # the exact fp16 values the kernel read
+    l32 = lt.cpu().double().numpy()
+    ro, rl = ref16[0], l32[0]
     for i in range(1, n):
-        ro, rl = oracle.combine(ro, rl, ref16[i], l[i])
+        ro, rl = oracle.combine(ro, rl, ref16[i], l32[i])
     np.testing.assert_allclose(out.cpu().numpy(), ro, atol=2e-6)
     np.testing.assert_allclose(lse.cpu().numpy(), rl, atol=2e-6)
