@@ -39,7 +39,8 @@ static hydra_status cuda_fail(const char *what) {
   return fail(HYDRA_ECUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
-static std::atomic<int64_t> g_prefix_impl{0}, g_prefix_splits{0}, g_suffix_splits{0}, g_tc_debug{0};
+static std::atomic<int64_t> g_prefix_impl{0}, g_prefix_splits{0}, g_suffix_splits{0}, g_tc_debug{0},
+    g_prefix_stages{3}, g_suffix_unroll{4};
 
 extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
   if (!key) return fail(HYDRA_EINVAL, "null key");
@@ -47,6 +48,8 @@ extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
   else if (!strcmp(key, "prefix_splits")) g_prefix_splits = value;
   else if (!strcmp(key, "suffix_splits")) g_suffix_splits = value;
   else if (!strcmp(key, "tc_debug_variant")) g_tc_debug = value;
+  else if (!strcmp(key, "prefix_stages")) g_prefix_stages = (value == 2 ? 2 : 3);
+  else if (!strcmp(key, "suffix_unroll")) g_suffix_unroll = (value >= 8 ? 8 : value >= 4 ? 4 : 2);
   else return fail(HYDRA_EINVAL, "unknown config key '%s'", key);
   return HYDRA_OK;
 }
@@ -57,6 +60,8 @@ extern "C" int64_t hydra_get_config(const char *key) {
   if (!strcmp(key, "prefix_splits")) return g_prefix_splits;
   if (!strcmp(key, "suffix_splits")) return g_suffix_splits;
   if (!strcmp(key, "tc_debug_variant")) return g_tc_debug;
+  if (!strcmp(key, "prefix_stages")) return g_prefix_stages;
+  if (!strcmp(key, "suffix_unroll")) return g_suffix_unroll;
   return -1;
 }
 
@@ -210,6 +215,7 @@ static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, i
     a.o_slot_stride = dst.o_stride;
     a.lse_slot_stride = dst.lse_stride;
     a.debug_variant = (int32_t)g_tc_debug;
+    a.stages = (int32_t)g_prefix_stages;
     hydra_status st = launch_prefix_tc(a, s);
     return st == HYDRA_OK ? st : cuda_fail("prefix tcgen05 launch");
   }
@@ -264,6 +270,7 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
   p.n_splits = splits;
   p.split_len = (S_cap + splits - 1) / splits;
   p.heads_per_cta = heads_per_cta(g);
+  p.unroll = (int32_t)g_suffix_unroll;
   p.o = dst.o;
   p.lse = dst.lse;
   p.o_split_stride = dst.o_stride;
@@ -686,6 +693,7 @@ extern "C" hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra
       a.o_slot_stride = all.o_stride;
       a.lse_slot_stride = all.lse_stride;
       a.debug_variant = (int32_t)g_tc_debug;
+    a.stages = (int32_t)g_prefix_stages;
       st = launch_prefix_tc(a, s);
       if (st) return cuda_fail("tree prefix tcgen05 launch");
     }

@@ -164,15 +164,23 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeParams p) 
   }
 }
 
-template <typename T, int D, int GQ>
-static cudaError_t launch_t(const DecodeParams &p, cudaStream_t s) {
+template <typename T, int D, int GQ, int U>
+static cudaError_t launch_u(const DecodeParams &p, cudaStream_t s) {
   const dim3 grid(p.n_splits, p.Hkv * (p.g / GQ), p.n_seq);
-  constexpr int U = (sizeof(T) == 2) ? 4 : 4;
   if (p.kv_sb == 0)  // shared KV (prefix in SIMT mode): let L1 keep it
     decode_attn_kernel<T, D, GQ, U, false><<<grid, 128, 0, s>>>(p);
   else
     decode_attn_kernel<T, D, GQ, U, true><<<grid, 128, 0, s>>>(p);
   return cudaGetLastError();
+}
+
+template <typename T, int D, int GQ>
+static cudaError_t launch_t(const DecodeParams &p, cudaStream_t s) {
+  // more tokens in flight per thread only where registers allow (one query head per CTA)
+  if constexpr (GQ == 1) {
+    if (p.unroll >= 8) return launch_u<T, D, GQ, 8>(p, s);
+  }
+  return launch_u<T, D, GQ, 4>(p, s);
 }
 
 template <typename T, int D>

@@ -24,6 +24,7 @@ struct DecodeParams {
   int32_t n_splits;
   int64_t split_len;            // tokens per split
   int32_t heads_per_cta;        // GQ: query heads of one KV group handled per CTA
+  int32_t unroll;               // tokens in flight per row group (4 or 8; 0 -> 4)
   float *o;                     // [split][B][Hq][d] partial outputs (fp32, normalised)
   float *lse;                   // [split][B][Hq] natural-log LSE
   int64_t o_split_stride, lse_split_stride;
@@ -79,6 +80,7 @@ struct PrefixTcArgs {
   float *o, *lse;
   int64_t o_slot_stride, lse_slot_stride;
   int32_t debug_variant;
+  int32_t stages;  // K/V pipeline stages: 2 (160 KB smem, leaves room for co-resident suffix CTAs) or 3
 };
 bool prefix_tc_supported(const hydra_heads *h);
 hydra_status launch_prefix_tc(const PrefixTcArgs &a, cudaStream_t s);

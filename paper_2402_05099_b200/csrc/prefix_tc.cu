@@ -38,19 +38,22 @@ namespace tc {
 constexpr int BM = 128;  // stacked query rows per tile (UMMA M)
 constexpr int BN = 128;  // KV tokens per block (UMMA N of S, K of PV)
 constexpr int HD = 128;  // head dim (UMMA K of S, N of PV)
-constexpr int NS = 3;    // pipeline stages
 constexpr int kThreads = 192;
 constexpr int PANEL = BN * 128;          // one 64-column SWIZZLE_128B panel: 128 rows x 128 B
 constexpr int TILE = 2 * PANEL;          // 128 rows x 128 dims bf16 = 32 KB
-constexpr int OFF_Q = 0;
-constexpr int OFF_K = OFF_Q + TILE;
-constexpr int OFF_V = OFF_K + NS * TILE;
-constexpr int OFF_BAR = OFF_V + NS * TILE;
-constexpr int N_BARS = 4 * NS + 2 + 2 + 1;
-constexpr int SMEM_BYTES = OFF_BAR + N_BARS * 8 + 16;
-constexpr int SMEM_ALLOC = SMEM_BYTES + 1024;  // slack for 1024-B alignment (SWIZZLE_128B atoms)
 constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t COL_O = 256;
+// Shared-memory carve-up for NS pipeline stages (K and V slots per stage).
+template <int NS>
+struct Smem {
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + TILE;
+  static constexpr int OFF_V = OFF_K + NS * TILE;
+  static constexpr int OFF_BAR = OFF_V + NS * TILE;
+  static constexpr int N_BARS = 4 * NS + 2 + 2 + 1;
+  static constexpr int BYTES = OFF_BAR + N_BARS * 8 + 16;
+  static constexpr int ALLOC = BYTES + 1024;  // slack for 1024-B alignment (SWIZZLE_128B atoms)
+};
 }  // namespace tc
 
 struct __align__(64) PrefixTcKernelParams {
@@ -70,8 +73,11 @@ struct __align__(64) PrefixTcKernelParams {
   int32_t debug_variant;  // bring-up switch: bit0 swaps the V descriptor LBO/SBO
 };
 
+template <int NS>
 __global__ void __launch_bounds__(tc::kThreads, 1) prefix_tc_kernel(const __grid_constant__ PrefixTcKernelParams P) {
   using namespace tc;
+  using L = Smem<NS>;
+  constexpr int OFF_Q = L::OFF_Q, OFF_K = L::OFF_K, OFF_V = L::OFF_V, OFF_BAR = L::OFF_BAR, N_BARS = L::N_BARS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sQ = smem + OFF_Q;
@@ -242,17 +248,25 @@ __global__ void __launch_bounds__(tc::kThreads, 1) prefix_tc_kernel(const __grid
       for (int c = 0; c < 4; ++c) ptx::tmem_ld32(sbuf + c * 32, sr[c]);
       ptx::tmem_ld_wait();
       const int64_t rem = task.kv_len - (int64_t)(blk_begin + n) * BN;
-      const int valid = rem < BN ? (int)rem : BN;
-      float mx = -INFINITY;
+      if (rem < BN) {  // partial last block only (CTA-uniform): mask columns >= rem
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < 4; ++c)
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          float s = __uint_as_float(sr[c][i]);
-          if (c * 32 + i >= valid) s = -INFINITY;
-          sr[c][i] = __float_as_uint(s);
-          mx = fmaxf(mx, s);
-        }
+          for (int i = 0; i < 32; ++i)
+            if (c * 32 + i >= rem) sr[c][i] = 0xff800000u;  // -inf
+      }
+      // row max: 8 independent FMNMX3 chains of depth 8, then a short tree
+      float acc[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] = fmaxf(__uint_as_float(sr[0][2 * k]), __uint_as_float(sr[0][2 * k + 1]));
+#pragma unroll
+      for (int i = 16; i < BN; i += 16)
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          acc[k] = ptx::fmax3(acc[k], __uint_as_float(sr[(i + 2 * k) / 32][(i + 2 * k) % 32]),
+                              __uint_as_float(sr[(i + 2 * k + 1) / 32][(i + 2 * k + 1) % 32]));
+      const float mx = fmaxf(ptx::fmax3(acc[0], acc[1], acc[2]),
+                             fmaxf(ptx::fmax3(acc[3], acc[4], acc[5]), fmaxf(acc[6], acc[7])));
       const float mnew = mx * c2;
       const bool need = mnew > m2 + 8.0f;
       const bool any = __any_sync(0xffffffffu, need);
@@ -262,18 +276,27 @@ __global__ void __launch_bounds__(tc::kThreads, 1) prefix_tc_kernel(const __grid
         alpha = fast_exp2(m2 - mt);  // m2 = -inf on the first block -> 0
         m2 = mt;
       }
-      float sum = 0.f;
+      // p = 2^(s*c2 - m2): packed FFMA2 for the argument, MUFU.EX2 per element,
+      // packed FADD2 into 4 independent row-sum chains, bf16x2 pack for the PV MMA
+      const uint64_t cc = ptx::pack2(c2, c2), nm = ptx::pack2(-m2, -m2);
+      uint64_t sacc[4] = {0, 0, 0, 0};
       uint32_t pk[4][16];
 #pragma unroll
       for (int c = 0; c < 4; ++c)
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float p0 = fast_exp2(fmaf(__uint_as_float(sr[c][2 * i]), c2, -m2));
-          const float p1 = fast_exp2(fmaf(__uint_as_float(sr[c][2 * i + 1]), c2, -m2));
-          sum += p0 + p1;
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);  // low half = even column
-          pk[c][i] = *reinterpret_cast<uint32_t *>(&b2);
+          float x0, x1;
+          ptx::unpack2(ptx::fma2(ptx::pack2(__uint_as_float(sr[c][2 * i]), __uint_as_float(sr[c][2 * i + 1])), cc, nm),
+                       x0, x1);
+          const float p0 = fast_exp2(x0), p1 = fast_exp2(x1);
+          sacc[i % 4] = ptx::add2(sacc[i % 4], ptx::pack2(p0, p1));
+          pk[c][i] = ptx::cvt_bf16x2(p0, p1);  // low half = even column
         }
+      float s0, s1, s2, s3, s4, s5, s6, s7;
+      ptx::unpack2(ptx::add2(sacc[0], sacc[1]), s0, s1);
+      ptx::unpack2(ptx::add2(sacc[2], sacc[3]), s2, s3);
+      (void)s4; (void)s5; (void)s6; (void)s7;
+      const float sum = (s0 + s1) + (s2 + s3);
       l = l * alpha + sum;
       if (n >= 1) {
         ptx::mbar_wait(pv_done, (n - 1) & 1);  // PV(n-1) has landed in O
@@ -341,7 +364,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) prefix_tc_kernel(const __grid
   if (warp == 1) {
     __syncwarp();
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<tc::TMEM_COLS>(tmem);
+    ptx::tmem_dealloc<TMEM_COLS>(tmem);
   }
 }
 
@@ -375,13 +398,19 @@ bool prefix_tc_supported(const hydra_heads *h) {
   return h->dtype == HYDRA_BF16 && h->head_dim == 128 && encode_fn() != nullptr;
 }
 
-hydra_status launch_prefix_tc(const PrefixTcArgs &a, cudaStream_t s) {
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [] {
-    attr_err = cudaFuncSetAttribute(prefix_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_ALLOC);
+template <int NS>
+static cudaError_t set_smem_attr() {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    err = cudaFuncSetAttribute(prefix_tc_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Smem<NS>::ALLOC);
   });
-  if (attr_err != cudaSuccess) return HYDRA_ECUDA;
+  return err;
+}
+
+hydra_status launch_prefix_tc(const PrefixTcArgs &a, cudaStream_t s) {
+  const int stages = a.stages == 2 ? 2 : 3;
+  if ((stages == 2 ? set_smem_attr<2>() : set_smem_attr<3>()) != cudaSuccess) return HYDRA_ECUDA;
   PrefixTcKernelParams P;
   memset(&P, 0, sizeof(P));
   if (a.kv_total > 0) {
@@ -408,7 +437,10 @@ hydra_status launch_prefix_tc(const PrefixTcArgs &a, cudaStream_t s) {
   const int n_x = a.tasks ? a.n_tasks : (int)(((int64_t)a.B * a.g + tc::BM - 1) / tc::BM);
   if (n_x == 0) return HYDRA_OK;
   const dim3 grid(n_x, a.Hkv, a.n_splits);
-  prefix_tc_kernel<<<grid, tc::kThreads, tc::SMEM_ALLOC, s>>>(P);
+  if (stages == 2)
+    prefix_tc_kernel<2><<<grid, tc::kThreads, tc::Smem<2>::ALLOC, s>>>(P);
+  else
+    prefix_tc_kernel<3><<<grid, tc::kThreads, tc::Smem<3>::ALLOC, s>>>(P);
   return cudaGetLastError() == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
 }
 
