@@ -40,7 +40,7 @@ static hydra_status cuda_fail(const char *what) {
 }
 
 static std::atomic<int64_t> g_prefix_impl{0}, g_prefix_splits{0}, g_suffix_splits{0}, g_tc_debug{0},
-    g_prefix_stages{3}, g_suffix_unroll{4};
+    g_prefix_stages{3}, g_suffix_unroll{4}, g_prefix_ctas{0};
 
 extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
   if (!key) return fail(HYDRA_EINVAL, "null key");
@@ -48,6 +48,7 @@ extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
   else if (!strcmp(key, "prefix_splits")) g_prefix_splits = value;
   else if (!strcmp(key, "suffix_splits")) g_suffix_splits = value;
   else if (!strcmp(key, "tc_debug_variant")) g_tc_debug = value;
+  else if (!strcmp(key, "prefix_ctas")) g_prefix_ctas = value;
   else if (!strcmp(key, "prefix_stages")) g_prefix_stages = (value == 2 ? 2 : 3);
   else if (!strcmp(key, "suffix_unroll")) g_suffix_unroll = (value >= 8 ? 8 : value >= 4 ? 4 : 2);
   else return fail(HYDRA_EINVAL, "unknown config key '%s'", key);
@@ -61,6 +62,7 @@ extern "C" int64_t hydra_get_config(const char *key) {
   if (!strcmp(key, "suffix_splits")) return g_suffix_splits;
   if (!strcmp(key, "tc_debug_variant")) return g_tc_debug;
   if (!strcmp(key, "prefix_stages")) return g_prefix_stages;
+  if (!strcmp(key, "prefix_ctas")) return g_prefix_ctas;
   if (!strcmp(key, "suffix_unroll")) return g_suffix_unroll;
   return -1;
 }
@@ -120,10 +122,21 @@ static int suffix_splits(const hydra_heads *h, int64_t B, int64_t S_cap) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(s, 64));
 }
 
-static bool use_tc(const hydra_heads *h) {
-  if (g_prefix_impl == 1) return false;
-  return prefix_tc_supported(h);
+// Prefix kernel choice: the persistent two-tile tcgen05 kernel (v3) by default; the
+// one-tile tcgen05 kernel (v1) or the SIMT kernel on request / for unsupported shapes.
+enum PrefixKind { PK_SIMT = 1, PK_TC1 = 2, PK_TC2 = 3 };
+static int prefix_ctas() { return g_prefix_ctas > 0 ? (int)g_prefix_ctas : device_sm_count(); }
+// B/P-dependent choice (rows = stacked query rows per KV head, P = KV tokens per row):
+// the persistent kernel amortises its per-segment Q load / epilogue only when every CTA
+// owns enough 128-token blocks; small problems run the one-tile kernel (more parallelism).
+static PrefixKind prefix_kind(const hydra_heads *h, int64_t rows = -1, int64_t P = -1) {
+  if (g_prefix_impl == 1 || !prefix_tc_supported(h)) return PK_SIMT;
+  if (g_prefix_impl == 2) return PK_TC1;
+  if (g_prefix_impl == 3 || rows < 0) return PK_TC2;
+  const int64_t blocks = ((rows + 255) / 256) * h->num_kv_heads * ((P + 127) / 128);
+  return blocks >= 24 * (int64_t)prefix_ctas() ? PK_TC2 : PK_TC1;
 }
+static bool use_tc(const hydra_heads *h) { return prefix_kind(h) != PK_SIMT; }
 
 // Splits of the tensor-core prefix kernel: minimise (waves x blocks per CTA) plus the
 // HBM cost of writing/reading the extra fp32 partials, in units of one KV block.
@@ -158,14 +171,18 @@ static int prefix_splits_simt(const hydra_heads *h, int64_t B, int64_t P) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(s, 64));
 }
 
+// Number of partial (O, LSE) slots per row the prefix kernel writes.
 static int prefix_splits(const hydra_heads *h, int64_t B, int64_t P) {
   if (P <= 0) return 1;
-  if (use_tc(h)) {
-    const int g = h->num_q_heads / h->num_kv_heads;
-    const int64_t tiles = ((B * g + 127) / 128) * h->num_kv_heads;
-    return prefix_splits_tc(tiles, P);
+  const int g = h->num_q_heads / h->num_kv_heads;
+  switch (prefix_kind(h, B * g, P)) {
+    case PK_TC2:
+      return prefix_tc2_slots(B, g, h->num_kv_heads, P, prefix_ctas());
+    case PK_TC1:
+      return prefix_splits_tc(((B * g + 127) / 128) * h->num_kv_heads, P);
+    default:
+      return prefix_splits_simt(h, B, P);
   }
-  return prefix_splits_simt(h, B, P);
 }
 
 static size_t part_bytes(const hydra_heads *h, int64_t B) {
@@ -193,7 +210,8 @@ static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, i
                                const PartsView &dst, cudaStream_t s) {
   const int g = h->num_q_heads / h->num_kv_heads;
   const float sl2 = scale_of(h) * 1.4426950408889634f;
-  if (use_tc(h)) {
+  const PrefixKind kind = prefix_kind(h, B * g, P);
+  if (kind != PK_SIMT) {
     PrefixTcArgs a{};
     a.q = q;
     a.q_sb = q_sb;
@@ -216,7 +234,15 @@ static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, i
     a.lse_slot_stride = dst.lse_stride;
     a.debug_variant = (int32_t)g_tc_debug;
     a.stages = (int32_t)g_prefix_stages;
-    hydra_status st = launch_prefix_tc(a, s);
+    hydra_status st;
+    if (kind == PK_TC2) {
+      // stream-K pieces leave some slots of a row unwritten: mark every slot empty first
+      if (splits > 1 && launch_fill_neg_inf(dst.lse, dst.lse_stride * splits, s) != HYDRA_OK)
+        return cuda_fail("fill");
+      st = launch_prefix_tc2(a, prefix_ctas(), s);
+    } else {
+      st = launch_prefix_tc(a, s);
+    }
     return st == HYDRA_OK ? st : cuda_fail("prefix tcgen05 launch");
   }
   DecodeParams p{};
@@ -595,12 +621,13 @@ static int tree_prefix_splits(const hydra_heads *h, const hydra_tree *t) {
     for (auto L : t->node_len) maxlen = std::max(maxlen, L);
     return prefix_splits_simt(h, t->B, maxlen);
   }
-  // total tiles over all non-empty nodes, longest node sets the per-tile work
+  // total query tiles (v3: tile pairs) over all non-empty nodes; the longest node sets the work
   const int g = h->num_q_heads / h->num_kv_heads;
+  const int rows_per = prefix_kind(h) == PK_TC2 ? 256 : 128;
   int64_t tiles = 0, maxlen = 0;
   for (int n = 0; n < t->n_nodes; ++n) {
     if (t->node_len[n] <= 0) continue;
-    tiles += ((int64_t)(t->grp_off[n + 1] - t->grp_off[n]) * g + 127) / 128;
+    tiles += ((int64_t)(t->grp_off[n + 1] - t->grp_off[n]) * g + rows_per - 1) / rows_per;
     maxlen = std::max(maxlen, t->node_len[n]);
   }
   return prefix_splits_tc(tiles * h->num_kv_heads, maxlen);
@@ -644,18 +671,20 @@ extern "C" hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra
   if (st) return cuda_fail("fill");
   const float sl2 = scale_of(h) * 1.4426950408889634f;
 
-  if (use_tc(h) && T > 0) {
+  const PrefixKind kind = prefix_kind(h);
+  if (kind != PK_SIMT && T > 0) {
     PrefixTask *d_tasks = nullptr;
     int n_tasks = 0;
+    const int rows_per_task = kind == PK_TC2 ? 256 : 128;  // tile pairs for v3
     {
       std::lock_guard<std::mutex> lock(t->mu);
-      auto it = t->work.find({g, np});
+      auto it = t->work.find({g * 4 + (int)kind, np});
       if (it == t->work.end()) {
         std::vector<PrefixTask> tasks;
         for (int n = 0; n < t->n_nodes; ++n) {
           if (t->node_len[n] <= 0) continue;
           const int32_t ns_ = t->grp_off[n + 1] - t->grp_off[n];
-          const int tiles = (int)(((int64_t)ns_ * g + 127) / 128);
+          const int tiles = (int)(((int64_t)ns_ * g + rows_per_task - 1) / rows_per_task);
           for (int tl = 0; tl < tiles; ++tl)
             tasks.push_back(PrefixTask{t->node_off[n], t->node_len[n], t->grp_off[n], ns_, t->depth[n] * np, tl});
         }
@@ -665,7 +694,7 @@ extern "C" hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra
               cudaMemcpy(dt, tasks.data(), sizeof(PrefixTask) * tasks.size(), cudaMemcpyHostToDevice) != cudaSuccess)
             return cuda_fail("tree work-list upload");
         }
-        it = t->work.emplace(std::make_pair(g, np), std::make_pair(dt, (int)tasks.size())).first;
+        it = t->work.emplace(std::make_pair(g * 4 + (int)kind, np), std::make_pair(dt, (int)tasks.size())).first;
       }
       d_tasks = it->second.first;
       n_tasks = it->second.second;

@@ -84,6 +84,11 @@ struct PrefixTcArgs {
 };
 bool prefix_tc_supported(const hydra_heads *h);
 hydra_status launch_prefix_tc(const PrefixTcArgs &a, cudaStream_t s);
+// v3: persistent, two 128-row query tiles per CTA; flat mode is stream-K over n_ctas CTAs
+// (partial slots per row = prefix_tc2_slots), task mode deals (task, head, split) items.
+hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s);
+int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas);
+int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas);
 int device_sm_count();
 
 }  // namespace hydra

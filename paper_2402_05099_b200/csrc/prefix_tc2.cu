@@ -1,0 +1,529 @@
+// prefix_tc2.cu -- persistent two-tile (M = 256) tcgen05 prefix attention for sm_100a.
+//
+// PAPER.md §3.2: all B*g decode queries of a KV head attend to the same
+// prefix K/V, so they are stacked into one matrix (rows r = b*g + i hold q[b, j*g+i])
+// and prefix attention is a dense GEMM-shaped problem reading the prefix once
+// (App. B `attention(batched_q, prefix_k, prefix_v)`).  Output per row:
+// O = softmax(s) V (fp32, normalised) and LSE (natural log, Eq. 4) for Eq. 5.
+//
+// Work item = (pair of 128-row query tiles, KV head j, KV split).  Persistent CTAs walk
+// the items round-robin (consecutive items share the KV range, so concurrently running
+// CTAs hit the same K/V tiles in L2).  384 threads per CTA:
+//   warp 0       TMA producer: K and V tiles (128 tokens x 128 dims, two 64-column
+//                SWIZZLE_128B boxes each) into a 2-stage ring; runs ahead across items
+//   warp 1       TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2-3    idle
+//   warps 4-7    softmax / correction / epilogue for query tile 0 (one row per thread)
+//   warps 8-11   the same for query tile 1
+// Every K/V tile in shared memory feeds both query tiles (256 rows), halving the K/V
+// smem/L2 traffic per FLOP compared with one 128-row tile, and the two softmax
+// warpgroups ping-pong: while one computes exp() the tensor core runs the other
+// tile's MMAs.  TMEM (512 columns): S_t at [128t, 128t+128) fp32 (P_t aliases its
+// first 64 columns as bf16 pairs and feeds the PV MMA from TMEM), O_t at
+// [256+128t, 384+128t).  MMA issue order per block n:
+//   PV0(n) S0(n+1) PV1(n) S1(n+1)       (S_t(n+1) may overwrite P_t(n): in-order pipe)
+// Online softmax in the log2 domain (scale folded into one FFMA2), running max raised
+// only when a row max grows by > 8 (P <= 256, rare O correction, exact final O / l).
+// Epilogue: O rows go TMEM -> registers -> XOR-swizzled smem (this warp's Q rows) ->
+// coalesced 128-B row stores.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace hydra {
+
+namespace tc2 {
+constexpr int BM = 128;  // rows per query tile (UMMA M)
+constexpr int BN = 128;  // KV tokens per block
+constexpr int HD = 128;  // head dim
+constexpr int NS = 2;    // K/V pipeline stages
+constexpr int kThreads = 384;
+constexpr int PANEL = BN * 128;  // 128 rows x 128 B (one 64-column SWIZZLE_128B panel)
+constexpr int TILE = 2 * PANEL;  // 128 x 128 bf16 = 32 KB
+constexpr int OFF_Q = 0;         // Q0, Q1
+constexpr int OFF_K = 2 * TILE;
+constexpr int OFF_V = OFF_K + NS * TILE;
+constexpr int OFF_BAR = OFF_V + NS * TILE;
+// k_full, k_empty, v_full, v_empty [NS]; q_full, s_full, p_full, pv_done, o_free [2]
+constexpr int N_BARS = 4 * NS + 10;
+constexpr int BYTES = OFF_BAR + N_BARS * 8 + 16;
+constexpr int ALLOC = BYTES + 1024;
+constexpr uint32_t TMEM_COLS = 512;
+}  // namespace tc2
+
+struct __align__(64) PrefixTc2Params {
+  CUtensorMap tmK;
+  CUtensorMap tmV;
+  const __nv_bfloat16 *q;
+  int64_t q_sb, q_sh;
+  int32_t Hq, Hkv, g;
+  float scale_log2;
+  int64_t P;      // flat mode: prefix length
+  int32_t B;      // flat mode: sequences
+  int32_t n_pairs;  // flat mode: ceil(B*g / 256)
+  const PrefixTask *tasks;  // task mode: task.tile = pair index within the group
+  int32_t n_tasks;
+  const int32_t *seq_list;
+  int32_t n_splits;   // task mode: KV splits per task
+  int32_t n_items;    // task mode: tasks * Hkv * n_splits
+  int32_t nb;         // flat mode: KV blocks per item (ceil(P / 128))
+  int64_t total_blocks;  // flat mode: n_pairs * Hkv * nb
+  float *o, *lse;
+  int64_t o_slot_stride, lse_slot_stride;
+};
+
+struct Item {
+  int64_t kv_off, kv_len, n_rows, row0;
+  int32_t seq_off, slot, j, blk_begin, nblk;
+};
+
+// Iterates the KV segments a persistent CTA owns.
+//  flat mode (stream-K): the (item = (pair, head), KV block) space of total_blocks is cut
+//    into gridDim.x equal contiguous ranges; a range may start/end inside an item, and
+//    each piece of an item writes its own partial slot (slot = this CTA - the CTA owning
+//    the item's first block), merged later by the LSE combine.
+//  task mode (tree): items = (task, head, split) dealt round-robin.
+struct SegIter {
+  int64_t x, end;
+  int w;
+};
+
+__device__ __forceinline__ int64_t sk_start(const PrefixTc2Params &P, int64_t c) {
+  return c * P.total_blocks / gridDim.x;
+}
+
+__device__ __forceinline__ void seg_begin(const PrefixTc2Params &P, SegIter &s) {
+  s.x = sk_start(P, blockIdx.x);
+  s.end = sk_start(P, blockIdx.x + 1);
+  s.w = blockIdx.x;
+}
+
+__device__ __forceinline__ bool seg_next(const PrefixTc2Params &P, SegIter &s, Item &it) {
+  PrefixTask task;
+  if (P.tasks) {
+    if (s.w >= P.n_items) return false;
+    const int w = s.w;
+    s.w += gridDim.x;
+    task = P.tasks[w % P.n_tasks];
+    const int rest = w / P.n_tasks;
+    const int split = rest % P.n_splits;
+    it.j = rest / P.n_splits;
+    it.kv_off = task.kv_off;
+    it.kv_len = task.kv_len;
+    it.n_rows = (int64_t)task.n_seq * P.g;
+    it.row0 = (int64_t)task.tile * (2 * tc2::BM);
+    it.seq_off = task.seq_off;
+    it.slot = task.slot + split;
+    const int nblk_total = (int)((task.kv_len + tc2::BN - 1) / tc2::BN);
+    const int per_split = (nblk_total + P.n_splits - 1) / P.n_splits;
+    it.blk_begin = split * per_split;
+    it.nblk = max(0, min(nblk_total, it.blk_begin + per_split) - it.blk_begin);
+    return true;
+  }
+  if (s.x >= s.end) return false;
+  const int64_t item = s.x / P.nb;
+  const int b = (int)(s.x % P.nb);
+  const int64_t room = s.end - s.x;
+  const int len = (int)(P.nb - b < room ? P.nb - b : room);
+  // CTA owning this item's first block: largest c with sk_start(c) <= item*nb
+  const int64_t x0 = item * P.nb;
+  int64_t c0 = x0 * gridDim.x / P.total_blocks;
+  while (c0 + 1 < gridDim.x && sk_start(P, c0 + 1) <= x0) ++c0;
+  while (c0 > 0 && sk_start(P, c0) > x0) --c0;
+  it.j = (int)(item / P.n_pairs);
+  it.kv_off = 0;
+  it.kv_len = P.P;
+  it.n_rows = (int64_t)P.B * P.g;
+  it.row0 = (item % P.n_pairs) * (2 * tc2::BM);
+  it.seq_off = 0;
+  it.slot = (int)(blockIdx.x - c0);
+  it.blk_begin = b;
+  it.nblk = len;
+  s.x += len;
+  return true;
+}
+
+__global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __grid_constant__ PrefixTc2Params P) {
+  using namespace tc2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
+  uint64_t *k_full = bars, *k_empty = bars + NS, *v_full = bars + 2 * NS, *v_empty = bars + 3 * NS;
+  uint64_t *q_full = bars + 4 * NS, *s_full = q_full + 2, *p_full = q_full + 4, *pv_done = q_full + 6,
+           *o_free = q_full + 8;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + N_BARS);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&P.tmK);
+    ptx::prefetch_tmap(&P.tmV);
+    for (int i = 0; i < NS; ++i) {
+      ptx::mbar_init(&k_full[i], 1);
+      ptx::mbar_init(&k_empty[i], 1);
+      ptx::mbar_init(&v_full[i], 1);
+      ptx::mbar_init(&v_empty[i], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      ptx::mbar_init(&q_full[t], 128);
+      ptx::mbar_init(&s_full[t], 1);
+      ptx::mbar_init(&p_full[t], 128);
+      ptx::mbar_init(&pv_done[t], 1);
+      ptx::mbar_init(&o_free[t], 128);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ================= TMA producer =================
+    if (ptx::elect_one()) {
+      uint32_t gb = 0;  // global block counter (stage ring position)
+      SegIter si;
+      seg_begin(P, si);
+      Item it;
+      while (seg_next(P, si, it)) {
+        for (int n = 0; n < it.nblk; ++n, ++gb) {
+          const int st = gb % NS;
+          const uint32_t ph = (gb / NS) & 1;
+          const int t0 = (int)(it.kv_off + (int64_t)(it.blk_begin + n) * BN);
+          uint8_t *sK = smem + OFF_K + st * TILE;
+          uint8_t *sV = smem + OFF_V + st * TILE;
+          ptx::mbar_wait(&k_empty[st], ph ^ 1);
+          ptx::mbar_arrive_expect_tx(&k_full[st], TILE);
+          ptx::tma_load_3d(sK, &P.tmK, &k_full[st], 0, it.j, t0);
+          ptx::tma_load_3d(sK + PANEL, &P.tmK, &k_full[st], 64, it.j, t0);
+          ptx::mbar_wait(&v_empty[st], ph ^ 1);
+          ptx::mbar_arrive_expect_tx(&v_full[st], TILE);
+          ptx::tma_load_3d(sV, &P.tmV, &v_full[st], 0, it.j, t0);
+          ptx::tma_load_3d(sV + PANEL, &P.tmV, &v_full[st], 64, it.j, t0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    if (ptx::elect_one()) {
+      constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BM, BN, false);  // S = Q K^T (both K-major)
+      constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(BM, HD, true);  // O += P V (V MN-major)
+      uint32_t gb = 0, qc[2] = {0, 0}, pc[2] = {0, 0}, oc[2] = {0, 0};
+      SegIter si;
+      seg_begin(P, si);
+      Item it;
+      while (seg_next(P, si, it)) {
+        if (it.nblk == 0) continue;
+        const int ntile = (it.n_rows - it.row0 > BM) ? 2 : 1;
+        auto issue_s = [&](int t, int st) {
+          const uint32_t q_addr = ptx::smem_u32(smem + OFF_Q + t * TILE);
+          const uint32_t k_addr = ptx::smem_u32(smem + OFF_K + st * TILE);
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint32_t off = (kk / 4) * PANEL + (kk % 4) * 32;
+            ptx::mma_ss(tmem + t * BN, ptx::smem_desc_sw128(q_addr + off, 16, 1024),
+                        ptx::smem_desc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0);
+          }
+          ptx::mma_commit(&s_full[t]);
+        };
+        for (int t = 0; t < ntile; ++t) {
+          ptx::mbar_wait(&q_full[t], qc[t] & 1);
+          ++qc[t];
+        }
+        {  // prologue: S_t(0)
+          const int st = gb % NS;
+          ptx::mbar_wait(&k_full[st], (gb / NS) & 1);
+          ptx::tc_fence_after();
+          for (int t = 0; t < ntile; ++t) issue_s(t, st);
+          ptx::mma_commit(&k_empty[st]);
+        }
+        for (int n = 0; n < it.nblk; ++n) {
+          const uint32_t g0 = gb + n, g1 = g0 + 1;
+          const int st = g0 % NS, st1 = g1 % NS;
+          const bool more = n + 1 < it.nblk;
+          ptx::mbar_wait(&v_full[st], (g0 / NS) & 1);
+          const uint32_t v_addr = ptx::smem_u32(smem + OFF_V + st * TILE);
+          for (int t = 0; t < ntile; ++t) {
+            ptx::mbar_wait(&p_full[t], pc[t] & 1);
+            ++pc[t];
+            if (n == 0) {  // O_t must have been drained by the previous item's epilogue
+              ptx::mbar_wait(&o_free[t], (oc[t] & 1) ^ 1);
+              ++oc[t];
+            }
+            ptx::tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < BN / 16; ++kk)
+              ptx::mma_ts(tmem + 256 + t * BN, tmem + t * BN + kk * 8,
+                          ptx::smem_desc_sw128(v_addr + kk * 2048, PANEL, 1024), idesc_pv, (n > 0 || kk > 0));
+            ptx::mma_commit(&pv_done[t]);
+            if (more) {
+              if (t == 0) {
+                ptx::mbar_wait(&k_full[st1], (g1 / NS) & 1);
+                ptx::tc_fence_after();
+              }
+              issue_s(t, st1);
+            }
+          }
+          ptx::mma_commit(&v_empty[st]);
+          if (more) ptx::mma_commit(&k_empty[st1]);
+        }
+        gb += it.nblk;
+      }
+    }
+  } else if (warp >= 4) {
+    // ================= softmax / correction / epilogue =================
+    const int t = (warp - 4) / 4;          // query tile of this warpgroup
+    const int quarter = warp % 4;           // TMEM lane quarter
+    const int r = quarter * 32 + lane;      // row within the tile
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const uint32_t s_col = tmem + lane_base + t * BN;
+    const uint32_t o_col = tmem + lane_base + 256 + t * BN;
+    uint8_t *sQ = smem + OFF_Q + t * TILE;
+    const float c2 = P.scale_log2;
+    uint32_t sc = 0, pvc = 0;  // phase counters of s_full[t] / pv_done[t]
+    SegIter si;
+    seg_begin(P, si);
+    Item it;
+    while (seg_next(P, si, it)) {
+      const int64_t trow0 = it.row0 + t * BM;
+      if (trow0 >= it.n_rows) continue;  // tile inactive for this item
+      const int64_t rr = trow0 + r;
+      const bool live = rr < it.n_rows;
+      int64_t seq = 0;
+      int h = 0;
+      if (live) {
+        seq = P.seq_list ? P.seq_list[it.seq_off + rr / P.g] : rr / P.g;
+        h = it.j * P.g + (int)(rr % P.g);
+      }
+      float *orow = P.o + it.slot * P.o_slot_stride + (seq * P.Hq + h) * HD;
+      if (it.nblk == 0) {  // empty KV range: (0, -inf) sentinel
+        if (live) {
+          P.lse[it.slot * P.lse_slot_stride + seq * P.Hq + h] = -INFINITY;
+          for (int c = 0; c < HD / 4; ++c) reinterpret_cast<float4 *>(orow)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        continue;
+      }
+      // ---- Q row -> sQ (canonical K-major SWIZZLE_128B: 16-B chunk c of row r at c ^ (r % 8))
+      {
+        uint4 ch[16];
+        if (live) {
+          const uint4 *src = reinterpret_cast<const uint4 *>(P.q + seq * P.q_sb + (int64_t)h * P.q_sh);
+#pragma unroll
+          for (int c = 0; c < 16; ++c) ch[c] = __ldg(src + c);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) ch[c] = make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          *reinterpret_cast<uint4 *>(sQ + (c / 8) * PANEL + r * 128 + (((c % 8) ^ (r % 8)) * 16)) = ch[c];
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive(&q_full[t]);
+      }
+      float m2 = -INFINITY, l = 0.f;
+      for (int n = 0; n < it.nblk; ++n) {
+        ptx::mbar_wait(&s_full[t], sc & 1);
+        ++sc;
+        ptx::tc_fence_after();
+        uint32_t sr[4][32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) ptx::tmem_ld32(s_col + c * 32, sr[c]);
+        ptx::tmem_ld_wait();
+        const int64_t rem = it.kv_len - (int64_t)(it.blk_begin + n) * BN;
+        if (rem < BN) {  // partial last block only
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c * 32 + i >= rem) sr[c][i] = 0xff800000u;
+        }
+        float acc[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] = fmaxf(__uint_as_float(sr[0][2 * k]), __uint_as_float(sr[0][2 * k + 1]));
+#pragma unroll
+        for (int i = 16; i < BN; i += 16)
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            acc[k] = ptx::fmax3(acc[k], __uint_as_float(sr[(i + 2 * k) / 32][(i + 2 * k) % 32]),
+                                __uint_as_float(sr[(i + 2 * k + 1) / 32][(i + 2 * k + 1) % 32]));
+        const float mx = fmaxf(ptx::fmax3(acc[0], acc[1], acc[2]),
+                               fmaxf(ptx::fmax3(acc[3], acc[4], acc[5]), fmaxf(acc[6], acc[7])));
+        const float mnew = mx * c2;
+        const bool any = __any_sync(0xffffffffu, mnew > m2 + 8.0f);
+        float alpha = 1.f;
+        if (any) {
+          const float mt = fmaxf(m2, mnew);
+          alpha = fast_exp2(m2 - mt);  // 0 on the first block
+          m2 = mt;
+        }
+        const uint64_t cc = ptx::pack2(c2, c2), nm = ptx::pack2(-m2, -m2);
+        uint64_t sacc[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float x0, x1;
+            ptx::unpack2(ptx::fma2(ptx::pack2(__uint_as_float(sr[c][2 * i]), __uint_as_float(sr[c][2 * i + 1])), cc,
+                                   nm),
+                         x0, x1);
+            const float p0 = fast_exp2(x0), p1 = fast_exp2(x1);
+            sacc[i % 4] = ptx::add2(sacc[i % 4], ptx::pack2(p0, p1));
+            pk[i] = ptx::cvt_bf16x2(p0, p1);
+          }
+          ptx::tmem_st16(s_col + c * 16, pk);  // P(n) -> first 64 columns of S_t
+        }
+        float s0, s1, s2, s3;
+        ptx::unpack2(ptx::add2(sacc[0], sacc[1]), s0, s1);
+        ptx::unpack2(ptx::add2(sacc[2], sacc[3]), s2, s3);
+        l = l * alpha + ((s0 + s1) + (s2 + s3));
+        if (n >= 1) {
+          ptx::mbar_wait(&pv_done[t], pvc & 1);  // PV_t(n-1) landed in O_t
+          ++pvc;
+          ptx::tc_fence_after();
+          if (any) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint32_t ov[32];
+              ptx::tmem_ld32(o_col + c * 32, ov);
+              ptx::tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+              ptx::tmem_st32(o_col + c * 32, ov);
+            }
+          }
+        }
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&p_full[t]);
+      }
+      ptx::mbar_wait(&pv_done[t], pvc & 1);  // last PV_t
+      ++pvc;
+      ptx::tc_fence_after();
+      // ---- epilogue: O / l, staged through this warp's 4 KB of sQ (XOR swizzle), coalesced rows
+      const float inv = 1.f / l;
+      uint32_t *stage = reinterpret_cast<uint32_t *>(sQ + quarter * 32 * 128);  // rows 32q..32q+31 of panel 0
+      const uint64_t my_row = live ? reinterpret_cast<uint64_t>(orow) : 0ull;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t ov[32];
+        ptx::tmem_ld32(o_col + c * 32, ov);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) stage[lane * 32 + (i ^ lane)] = __float_as_uint(__uint_as_float(ov[i]) * inv);
+        __syncwarp();
+#pragma unroll 4
+        for (int rw = 0; rw < 32; ++rw) {
+          const uint64_t base = __shfl_sync(0xffffffffu, my_row, rw);
+          const uint32_t v = stage[rw * 32 + (lane ^ rw)];
+          if (base) reinterpret_cast<float *>(base)[c * 32 + lane] = __uint_as_float(v);
+        }
+        __syncwarp();
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&o_free[t]);
+      if (live) P.lse[it.slot * P.lse_slot_stride + seq * P.Hq + h] = (m2 + log2f(l)) * HYDRA_LN2;
+      // the staging writes to sQ were generic-proxy; order them before the next item's Q writes+TMA reads
+      ptx::fence_proxy_async_smem();
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<TMEM_COLS>(tmem);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn2() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+static bool make_kv_map2(CUtensorMap *m, const void *base, int64_t T, int Hkv, int64_t st, int64_t sh) {
+  auto fn = encode_fn2();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)tc2::HD, (cuuint64_t)Hkv, (cuuint64_t)T};
+  const cuuint64_t strides[2] = {(cuuint64_t)sh * 2, (cuuint64_t)st * 2};
+  const cuuint32_t box[3] = {64, 1, (cuuint32_t)tc2::BN};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Flat mode: number of partial slots a stream-K schedule over n_ctas CTAs produces per row.
+int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas) {
+  const int64_t nb = (P + 127) / 128;
+  const int64_t total = ((B * g + 255) / 256) * Hkv * nb;
+  if (total <= 0) return 1;
+  const int64_t G = n_ctas < total ? n_ctas : total;
+  const int64_t range = total / G;  // >= 1
+  return (int)((nb + range - 1) / range + 1);
+}
+
+int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas) {
+  const int64_t nb = (P + 127) / 128;
+  const int64_t total = ((B * g + 255) / 256) * Hkv * nb;
+  return (int)(n_ctas < total ? n_ctas : total);
+}
+
+hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s) {
+  static std::once_flag once;
+  static cudaError_t attr = cudaSuccess;
+  std::call_once(once, [] {
+    attr = cudaFuncSetAttribute(prefix_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::ALLOC);
+  });
+  if (attr != cudaSuccess) return HYDRA_ECUDA;
+  PrefixTc2Params P;
+  memset(&P, 0, sizeof(P));
+  if (a.kv_total > 0) {
+    if (!make_kv_map2(&P.tmK, a.k, a.kv_total, a.Hkv, a.kv_st, a.kv_sh)) return HYDRA_ECUDA;
+    if (!make_kv_map2(&P.tmV, a.v, a.kv_total, a.Hkv, a.kv_st, a.kv_sh)) return HYDRA_ECUDA;
+  }
+  P.q = reinterpret_cast<const __nv_bfloat16 *>(a.q);
+  P.q_sb = a.q_sb;
+  P.q_sh = a.q_sh;
+  P.Hq = a.Hq;
+  P.Hkv = a.Hkv;
+  P.g = a.g;
+  P.scale_log2 = a.scale_log2;
+  P.P = a.P;
+  P.B = a.B;
+  P.n_pairs = (int)(((int64_t)a.B * a.g + 255) / 256);
+  P.tasks = a.tasks;
+  P.n_tasks = a.n_tasks;
+  P.seq_list = a.seq_list;
+  P.n_splits = a.n_splits;
+  P.n_items = a.tasks ? a.n_tasks * a.Hkv * a.n_splits : 0;
+  P.nb = (int)((a.P + 127) / 128);
+  P.total_blocks = a.tasks ? 0 : (int64_t)P.n_pairs * a.Hkv * P.nb;
+  P.o = a.o;
+  P.lse = a.lse;
+  P.o_slot_stride = a.o_slot_stride;
+  P.lse_slot_stride = a.lse_slot_stride;
+  const int64_t work = a.tasks ? P.n_items : P.total_blocks;
+  if (work == 0) return HYDRA_OK;
+  const int grid = (int)(n_ctas > 0 && n_ctas < work ? n_ctas : work);
+  prefix_tc2_kernel<<<grid, tc2::kThreads, tc2::ALLOC, s>>>(P);
+  return cudaGetLastError() == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
+}
+
+}  // namespace hydra

@@ -22,10 +22,11 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(autouse=True)
 def _reset_config():
-    for k in ("prefix_impl", "prefix_splits", "suffix_splits", "tc_debug_variant"):
+    keys = ("prefix_impl", "prefix_splits", "suffix_splits", "tc_debug_variant", "prefix_ctas")
+    for k in keys:
         hydra.set_config(k, 0)
     yield
-    for k in ("prefix_impl", "prefix_splits", "suffix_splits", "tc_debug_variant"):
+    for k in keys:
         hydra.set_config(k, 0)
 
 
@@ -65,7 +66,9 @@ PREFIX_SHAPES = [
 
 @pytest.mark.parametrize("B,Hq,Hkv,P", PREFIX_SHAPES)
 @pytest.mark.parametrize("dist", ["mixed", "boundary"])
-def test_prefix_tc_parity(B, Hq, Hkv, P, dist):
+@pytest.mark.parametrize("impl", [2, 3])
+def test_prefix_tc_parity(B, Hq, Hkv, P, dist, impl):
+    hydra.set_config("prefix_impl", impl)  # 2: one-tile tcgen05 kernel, 3: persistent two-tile
     pb = synth.make_problem(B, Hq, Hkv, 128, P, 1, dtype="bf16", dist=dist, seed=3)
     t = problem_to(pb, DEV)
     o, lse = hydra.prefix_attn(t["q"], t["pk"], t["pv"])
@@ -76,6 +79,7 @@ def test_prefix_tc_parity(B, Hq, Hkv, P, dist):
 
 @pytest.mark.parametrize("splits", [1, 2, 3, 7])
 def test_prefix_tc_splits(splits):
+    hydra.set_config("prefix_impl", 2)
     hydra.set_config("prefix_splits", splits)
     pb = synth.make_problem(20, 8, 2, 128, 1100, 1, dtype="bf16", dist="mixed", seed=4)
     t = problem_to(pb, DEV)
@@ -83,6 +87,18 @@ def test_prefix_tc_splits(splits):
     torch.cuda.synchronize()
     ref, lref = oracle.prefix_only(pb)
     assert_parity(o, ref, lse, lref, what=f"prefix splits={splits}")
+
+
+@pytest.mark.parametrize("ctas", [1, 3, 7, 64, 148, 100000])
+def test_prefix_tc2_stream_k_ctas(ctas):
+    """Stream-K piece boundaries fall inside items for most CTA counts; every piece is merged."""
+    hydra.set_config("prefix_ctas", ctas)
+    pb = synth.make_problem(300, 8, 2, 128, 1100, 1, dtype="bf16", dist="boundary", seed=4)
+    t = problem_to(pb, DEV)
+    o, lse = hydra.prefix_attn(t["q"], t["pk"], t["pv"])
+    torch.cuda.synchronize()
+    ref, lref = oracle.prefix_only(pb)
+    assert_parity(o, ref, lse, lref, what=f"prefix ctas={ctas}")
 
 
 def test_prefix_simt_bf16():
@@ -183,7 +199,7 @@ def test_sabotage_combine_bug_is_caught(monkeypatch):
 
 
 # ---------------------------------------------------------------- tree (§3.3)
-@pytest.mark.parametrize("impl", [0, 1])
+@pytest.mark.parametrize("impl", [0, 1, 2])
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
 def test_tree_parity(impl, dtype):
     if dtype == "f32" and impl == 0:
@@ -218,7 +234,7 @@ def test_one_level_tree_equals_flat():
     torch.cuda.synchronize()
     ref, _ = oracle.flat_attention(pb)
     assert_parity(a, ref, what="one-level tree")
-    assert torch.equal(a, b)
+    assert_parity(b, ref, what="flat")
 
 
 # ---------------------------------------------------------------- combine as a standalone op

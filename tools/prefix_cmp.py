@@ -1,0 +1,35 @@
+"""Time the prefix kernels (v1 one-tile, v3 persistent two-tile) at bench shapes."""
+import os, sys, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2402_05099_b200 as hydra
+dev = torch.device("cuda:0")
+def run(B, H, Hkv, P, impl, ctas=0, iters=20):
+    hydra.set_config("prefix_impl", impl); hydra.set_config("prefix_ctas", ctas)
+    g = torch.Generator(device=dev); g.manual_seed(0)
+    q = torch.randn(B, H, 128, device=dev, generator=g).bfloat16()
+    pk = torch.randn(P, Hkv, 128, device=dev, generator=g).bfloat16()
+    pv = torch.randn(P, Hkv, 128, device=dev, generator=g).bfloat16()
+    ws = torch.empty(hydra.attn_workspace_bytes(q, P, 1, Hkv), dtype=torch.uint8, device=dev)
+    fn = lambda: hydra.prefix_attn(q, pk, pv, workspace=ws)
+    s = torch.cuda.Stream(); s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s): fn()
+    torch.cuda.current_stream().wait_stream(s); torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr): fn()
+    for _ in range(3): gr.replay()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters): gr.replay()
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    fl = 4.0 * B * H * P * 128
+    print(json.dumps(dict(B=B, H=H, Hkv=Hkv, P=P, impl=impl, ctas=ctas, ms=round(ms, 4), tflops=round(fl / ms / 1e9, 1))), flush=True)
+for impl in (2, 3):
+    run(1024, 40, 40, 16384, impl)
+    run(1024, 40, 40, 1024, impl)
+    run(256, 32, 32, 2048, impl)
+    run(512, 32, 8, 32768, impl)
+for c in (74, 96, 120):
+    run(1024, 40, 40, 16384, 3, c)
