@@ -128,7 +128,8 @@ HYDRA_API hydra_status hydra_suffix_attn(const hydra_heads *h, int64_t B,
  * Parts whose lse is -inf are skipped (their O is never read).  Part p row r is at
  * o_parts + p*o_part_stride + r*d (elements of o_dtype = F32 or F16) and
  * lse_parts[p*lse_part_stride + r]; strides let it read an all-gathered
- * [rank][O|LSE] buffer in place.  out_dtype BF16 or F32; lse_out may be NULL.
+ * [rank][O|LSE] buffer in place.  out_dtype BF16 or F32 (or F16 from F32 parts: packing
+ * partials for a cross-GPU exchange, n_parts may be 1); lse_out may be NULL.
  * Setting the environment variable HYDRA_INJECT_COMBINE_BUG=1 drops the
  * rescaling (w_p = 1): a sabotage switch the parity suite must catch.
  */

@@ -97,7 +97,8 @@ def prefix_attn(q: torch.Tensor, prefix_k: torch.Tensor, prefix_v: torch.Tensor,
 
 
 def suffix_attn(q: torch.Tensor, suffix_k: torch.Tensor, suffix_v: torch.Tensor, suffix_lens: torch.Tensor,
-                scale: Optional[float] = None, workspace: Optional[torch.Tensor] = None, stream=None):
+                scale: Optional[float] = None, workspace: Optional[torch.Tensor] = None, stream=None,
+                out: Optional[torch.Tensor] = None, lse_out: Optional[torch.Tensor] = None):
     """Per-sequence suffix attention (§3.2): -> (O_s [B,Hq,d] f32, LSE_s [B,Hq] f32)."""
     q = _squeeze_q(q)
     suffix_k, suffix_v = _kv4(suffix_k, "suffix_k"), _kv4(suffix_v, "suffix_v")
@@ -110,8 +111,10 @@ def suffix_attn(q: torch.Tensor, suffix_k: torch.Tensor, suffix_v: torch.Tensor,
     S_cap, Hkv = suffix_k.shape[1], suffix_k.shape[2]
     h = _heads(q, Hkv, scale)
     lib = _lib.load()
-    o = torch.empty(B, Hq, d, dtype=torch.float32, device=q.device)
-    lse = torch.empty(B, Hq, dtype=torch.float32, device=q.device)
+    o = out if out is not None else torch.empty(B, Hq, d, dtype=torch.float32, device=q.device)
+    lse = lse_out if lse_out is not None else torch.empty(B, Hq, dtype=torch.float32, device=q.device)
+    if o.dtype != torch.float32 or not o.is_contiguous() or o.numel() != B * Hq * d or not lse.is_contiguous():
+        raise ValueError("out must be contiguous f32 [B, Hq, d], lse_out contiguous f32 [B, Hq]")
     ws = _workspace(lib.hydra_workspace_size(_lib.HYDRA_OP_SUFFIX, ctypes.byref(h), B, 0, S_cap, 0), q.device,
                     workspace)
     st = suffix_k.stride()
@@ -123,11 +126,13 @@ def suffix_attn(q: torch.Tensor, suffix_k: torch.Tensor, suffix_v: torch.Tensor,
 
 
 def combine(o_parts: torch.Tensor, lse_parts: torch.Tensor, out_dtype=torch.bfloat16, return_lse: bool = True,
-            stream=None):
+            out: Optional[torch.Tensor] = None, lse_out: Optional[torch.Tensor] = None, stream=None):
     """n-ary LSE combine (Eq. 5 / App. B combine_lse).
 
-    o_parts: [n, rows, d] (f32 or f16, rows may be any leading shape flattened),
-    lse_parts: [n, rows] f32.  Returns (out [rows, d] in out_dtype, lse [rows] f32).
+    o_parts: [n, rows, d] (f32 or f16, rows may be any leading shape flattened; parts may
+    sit at any stride, e.g. slices of an all-gathered exchange buffer), lse_parts: [n, rows]
+    f32.  Returns (out [rows, d] in out_dtype, lse [rows] f32).  out_dtype float16 (from f32
+    parts) packs partials for a cross-GPU exchange.
     """
     _require_cuda(o_parts, lse_parts)
     n = o_parts.shape[0]
@@ -137,10 +142,15 @@ def combine(o_parts: torch.Tensor, lse_parts: torch.Tensor, out_dtype=torch.bflo
     rows = o2.shape[1]
     if l2.shape[1] != rows or l2.dtype != torch.float32:
         raise ValueError("lse_parts must be f32 with one value per row of each part")
-    if o2.stride(2) != 1 or o2.stride(1) != d or l2.stride(1) != 1:
+    if o2.stride(2) != 1 or (rows > 1 and o2.stride(1) != d) or (rows > 1 and l2.stride(1) != 1):
         raise ValueError("parts must be row-contiguous")
-    out = torch.empty(rows, d, dtype=out_dtype, device=o_parts.device)
-    lse = torch.empty(rows, dtype=torch.float32, device=o_parts.device) if return_lse else None
+    if out is None:
+        out = torch.empty(rows, d, dtype=out_dtype, device=o_parts.device)
+    out_dtype = out.dtype
+    if out.numel() != rows * d or not out.is_contiguous():
+        raise ValueError("out must be a contiguous [rows, d] tensor")
+    lse = lse_out if lse_out is not None else (
+        torch.empty(rows, dtype=torch.float32, device=o_parts.device) if return_lse else None)
     check(_lib.load().hydra_combine(rows, d, n, o2.data_ptr(), _DT[o2.dtype], o2.stride(0), l2.data_ptr(),
                                     l2.stride(0), out.data_ptr(), _DT[out_dtype], _ptr(lse),
                                     _stream_ptr(stream, o_parts.device)), "hydra_combine")

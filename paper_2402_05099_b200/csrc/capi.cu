@@ -414,7 +414,8 @@ extern "C" hydra_status hydra_combine(int64_t rows, int32_t d, int32_t n_parts, 
   if (rows < 0 || d <= 0 || n_parts <= 0) return fail(HYDRA_ESHAPE, "rows >= 0, d > 0, n_parts > 0 required");
   if (!o_parts || !lse_parts || !out) return fail(HYDRA_EINVAL, "null pointer argument");
   if (o_dtype != HYDRA_F32 && o_dtype != HYDRA_F16) return fail(HYDRA_EUNSUPPORTED, "o_dtype must be F32 or F16");
-  if (out_dtype != HYDRA_F32 && out_dtype != HYDRA_BF16) return fail(HYDRA_EUNSUPPORTED, "out_dtype must be F32 or BF16");
+  if (out_dtype != HYDRA_F32 && out_dtype != HYDRA_BF16 && !(out_dtype == HYDRA_F16 && o_dtype == HYDRA_F32))
+    return fail(HYDRA_EUNSUPPORTED, "out_dtype must be F32 or BF16 (F16 only from F32 parts)");
   if (n_parts > 1 && (o_part_stride < rows * d || lse_part_stride < rows))
     return fail(HYDRA_ESHAPE, "part strides overlap the rows of a part");
   if ((d == 128 || d == 256) && (reinterpret_cast<uintptr_t>(o_parts) % 16 ||

@@ -113,6 +113,7 @@ hydra_status launch_combine(const CombineParams &p, hydra_dtype o_dtype, hydra_d
   else if (o_dtype == HYDRA_F32 && out_dtype == HYDRA_F32) e = launch_c<float, float>(p, s);
   else if (o_dtype == HYDRA_F16 && out_dtype == HYDRA_BF16) e = launch_c<__half, __nv_bfloat16>(p, s);
   else if (o_dtype == HYDRA_F16 && out_dtype == HYDRA_F32) e = launch_c<__half, float>(p, s);
+  else if (o_dtype == HYDRA_F32 && out_dtype == HYDRA_F16) e = launch_c<float, __half>(p, s);  // exchange packing
   else return HYDRA_EUNSUPPORTED;
   return e == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
 }

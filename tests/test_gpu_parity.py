@@ -258,3 +258,30 @@ def test_combine_f16_parts_and_identity():
         ro, rl = oracle.combine(ro, rl, ref16[i], l32[i])
     np.testing.assert_allclose(out.cpu().numpy(), ro, atol=2e-6)
     np.testing.assert_allclose(lse.cpu().numpy(), rl, atol=2e-6)
+
+
+# ---------------------------------------------------------------- multi-GPU layer, kernel side
+def test_seqsplit_single_rank_nccl():
+    """dist.seqsplit_attention on a 1-rank NCCL group: f16 packing of the prefix partials,
+    all-gather, strided combine of the gathered parts, suffix, final combine."""
+    import socket
+
+    import torch.distributed as tdist
+    from paper_2402_05099_b200 import dist as hdist
+
+    if not tdist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        tdist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        pb = synth.make_problem(24, 32, 8, 128, 700, 40, dtype="bf16", dist="mixed", seed=31)
+        t = problem_to(pb, DEV)
+        for ex in (torch.float16, torch.float32):
+            out, lse = hdist.seqsplit_attention(t["q"], t["pk"], t["pv"], t["sk"], t["sv"], t["lens"],
+                                                exchange_dtype=ex, return_lse=True)
+            torch.cuda.synchronize()
+            ref, lref = oracle.flat_attention(pb)
+            assert_parity(out, ref, lse, lref, what=f"seqsplit {ex}")
+    finally:
+        tdist.destroy_process_group()
