@@ -40,7 +40,8 @@ static hydra_status cuda_fail(const char *what) {
 }
 
 static std::atomic<int64_t> g_prefix_impl{0}, g_prefix_splits{0}, g_suffix_splits{0}, g_tc_debug{0},
-    g_prefix_stages{3}, g_suffix_unroll{4}, g_prefix_ctas{0};
+    g_prefix_stages{3}, g_suffix_unroll{4}, g_prefix_ctas{0}, g_suffix_impl{0}, g_suffix_ctas{0},
+    g_overlap_prefix_ctas{0};
 
 extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
   if (!key) return fail(HYDRA_EINVAL, "null key");
@@ -49,6 +50,9 @@ extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
   else if (!strcmp(key, "suffix_splits")) g_suffix_splits = value;
   else if (!strcmp(key, "tc_debug_variant")) g_tc_debug = value;
   else if (!strcmp(key, "prefix_ctas")) g_prefix_ctas = value;
+  else if (!strcmp(key, "suffix_impl")) g_suffix_impl = value;
+  else if (!strcmp(key, "suffix_ctas")) g_suffix_ctas = value;
+  else if (!strcmp(key, "overlap_prefix_ctas")) g_overlap_prefix_ctas = value;
   else if (!strcmp(key, "prefix_stages")) g_prefix_stages = (value == 2 ? 2 : 3);
   else if (!strcmp(key, "suffix_unroll")) g_suffix_unroll = (value >= 8 ? 8 : value >= 4 ? 4 : 2);
   else return fail(HYDRA_EINVAL, "unknown config key '%s'", key);
@@ -63,6 +67,9 @@ extern "C" int64_t hydra_get_config(const char *key) {
   if (!strcmp(key, "tc_debug_variant")) return g_tc_debug;
   if (!strcmp(key, "prefix_stages")) return g_prefix_stages;
   if (!strcmp(key, "prefix_ctas")) return g_prefix_ctas;
+  if (!strcmp(key, "suffix_impl")) return g_suffix_impl;
+  if (!strcmp(key, "suffix_ctas")) return g_suffix_ctas;
+  if (!strcmp(key, "overlap_prefix_ctas")) return g_overlap_prefix_ctas;
   if (!strcmp(key, "suffix_unroll")) return g_suffix_unroll;
   return -1;
 }
@@ -109,9 +116,22 @@ static int heads_per_cta(int g) {
 }
 
 // ------------------------------------------------------------------ work decomposition
+// Suffix kernel choice: the persistent tensor-core kernel (one item per (sequence, KV
+// head), TMA-fed) when there are enough items to keep every CTA busy; otherwise the SIMT
+// split-K kernel, which can split one sequence's tokens across CTAs.
+// On the full chip the SIMT kernel streams slightly faster (7.2 vs 7.0 TB/s at C3), so
+// `auto` uses the tensor-core kernel only for the SM-partitioned (overlapped) schedule,
+// where its low instruction count per byte lets a subset of SMs carry the suffix.
+static bool use_suffix_tc(const hydra_heads *h, int64_t B, int64_t S_cap, bool overlap = false) {
+  if (g_suffix_impl == 1 || S_cap <= 0 || !suffix_tc_supported(h)) return false;
+  if (g_suffix_impl == 2) return true;
+  return overlap && B * h->num_kv_heads >= 2 * (int64_t)device_sm_count();
+}
+
 // KV splits of the suffix kernel: enough CTAs to keep every SM streaming
 // (~16 resident 128-thread CTAs per SM), never fewer than 32 tokens per split.
-static int suffix_splits(const hydra_heads *h, int64_t B, int64_t S_cap) {
+static int suffix_splits(const hydra_heads *h, int64_t B, int64_t S_cap, bool overlap = false) {
+  if (use_suffix_tc(h, B, S_cap, overlap)) return 1;
   if (g_suffix_splits > 0) return (int)std::min<int64_t>(g_suffix_splits, std::max<int64_t>(1, S_cap));
   if (S_cap <= 0) return 1;
   const int g = h->num_q_heads / h->num_kv_heads;
@@ -172,17 +192,45 @@ static int prefix_splits_simt(const hydra_heads *h, int64_t B, int64_t P) {
 }
 
 // Number of partial (O, LSE) slots per row the prefix kernel writes.
-static int prefix_splits(const hydra_heads *h, int64_t B, int64_t P) {
+static int prefix_splits(const hydra_heads *h, int64_t B, int64_t P, int tc2_ctas = 0) {
   if (P <= 0) return 1;
   const int g = h->num_q_heads / h->num_kv_heads;
   switch (prefix_kind(h, B * g, P)) {
     case PK_TC2:
-      return prefix_tc2_slots(B, g, h->num_kv_heads, P, prefix_ctas());
+      return prefix_tc2_slots(B, g, h->num_kv_heads, P, tc2_ctas > 0 ? tc2_ctas : prefix_ctas());
     case PK_TC1:
       return prefix_splits_tc(((B * g + 127) / 128) * h->num_kv_heads, P);
     default:
       return prefix_splits_simt(h, B, P);
   }
+}
+
+// SM split for running the persistent prefix (tensor-bound) and suffix (HBM-bound)
+// kernels concurrently.  k prefix CTAs balance the two finish times:
+//   t_prefix(k) = pair_blocks / (k * R_P),  t_suffix(k) = kv_bytes / min((SMs-k) * R_S, BW)
+// with per-SM rates measured on B200 (R_P: 256-row x 128-token blocks per us per SM;
+// R_S: suffix bytes per us per SM; BW: achievable HBM read bandwidth).  0 = no overlap.
+static int overlap_prefix_ctas(const hydra_heads *h, int64_t B, int64_t P, int64_t S_cap) {
+  if (P <= 0 || S_cap <= 0 || !use_suffix_tc(h, B, S_cap, true)) return 0;
+  const int g = h->num_q_heads / h->num_kv_heads;
+  if (prefix_kind(h, B * g, P) != PK_TC2) return 0;
+  const int sms = device_sm_count();
+  if (g_overlap_prefix_ctas > 0) return (int)std::min<int64_t>(g_overlap_prefix_ctas, sms - 1);
+  // calibrated on B200 at C3@16K under overlap (prefix and suffix share HBM and L2):
+  // best k ~ 40-50 of 148 (tools/overlap_exp2.py)
+  const double R_P = 0.44, R_S = 5.0e4, BW = 7.0e6;
+  const double pair_blocks = (double)((B * g + 255) / 256) * h->num_kv_heads * ((P + 127) / 128);
+  const double kv_bytes = (double)B * h->num_kv_heads * S_cap * h->head_dim * 4.0;
+  int best_k = 0;
+  double best = 1e300;
+  for (int k = 8; k <= sms - 8; ++k) {
+    const double t = std::max(pair_blocks / (k * R_P), kv_bytes / std::min((sms - k) * R_S, BW));
+    if (t < best) {
+      best = t;
+      best_k = k;
+    }
+  }
+  return best_k;
 }
 
 static size_t part_bytes(const hydra_heads *h, int64_t B) {
@@ -207,7 +255,7 @@ static PartsView parts_in_ws(void *ws, const hydra_heads *h, int64_t B, int n) {
 
 static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, int64_t q_sb, int64_t q_sh,
                                int64_t P, const void *k, const void *v, int64_t kv_st, int64_t kv_sh, int splits,
-                               const PartsView &dst, cudaStream_t s) {
+                               const PartsView &dst, cudaStream_t s, int tc2_ctas = 0) {
   const int g = h->num_q_heads / h->num_kv_heads;
   const float sl2 = scale_of(h) * 1.4426950408889634f;
   const PrefixKind kind = prefix_kind(h, B * g, P);
@@ -239,7 +287,7 @@ static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, i
       // stream-K pieces leave some slots of a row unwritten: mark every slot empty first
       if (splits > 1 && launch_fill_neg_inf(dst.lse, dst.lse_stride * splits, s) != HYDRA_OK)
         return cuda_fail("fill");
-      st = launch_prefix_tc2(a, prefix_ctas(), s);
+      st = launch_prefix_tc2(a, tc2_ctas > 0 ? tc2_ctas : prefix_ctas(), s);
     } else {
       st = launch_prefix_tc(a, s);
     }
@@ -275,8 +323,30 @@ static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, i
 static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, int64_t q_sb, int64_t q_sh,
                                const void *k, const void *v, int64_t s_sb, int64_t s_st, int64_t s_sh,
                                int64_t S_cap, const int32_t *lens, int splits, const PartsView &dst,
-                               cudaStream_t s) {
+                               cudaStream_t s, int tc_ctas = 0) {
   const int g = h->num_q_heads / h->num_kv_heads;
+  if (use_suffix_tc(h, B, S_cap, tc_ctas > 0)) {
+    SuffixTcArgs a{};
+    a.q = q;
+    a.q_sb = q_sb;
+    a.q_sh = q_sh;
+    a.k = k;
+    a.v = v;
+    a.s_sb = s_sb;
+    a.s_st = s_st;
+    a.s_sh = s_sh;
+    a.S_cap = S_cap;
+    a.lens = lens;
+    a.B = (int32_t)B;
+    a.Hq = h->num_q_heads;
+    a.Hkv = h->num_kv_heads;
+    a.scale_log2 = scale_of(h) * 1.4426950408889634f;
+    a.o = dst.o;
+    a.lse = dst.lse;
+    const int ctas = tc_ctas > 0 ? tc_ctas : (g_suffix_ctas > 0 ? (int)g_suffix_ctas : device_sm_count());
+    hydra_status st = launch_suffix_tc(a, ctas, s);
+    return st == HYDRA_OK ? st : cuda_fail("suffix tcgen05 launch");
+  }
   DecodeParams p{};
   p.q = q;
   p.q_sb = q_sb;
@@ -337,8 +407,11 @@ extern "C" size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, 
       const int s = suffix_splits(h, B, S_cap);
       return s > 1 ? pb * s : 0;
     }
-    case HYDRA_OP_ATTN:
-      return pb * (size_t)(prefix_splits(h, B, P) + suffix_splits(h, B, S_cap));
+    case HYDRA_OP_ATTN: {  // enough for both the sequential and the SM-partitioned schedule
+      const int k = overlap_prefix_ctas(h, B, P, S_cap);
+      const int np = std::max(prefix_splits(h, B, P), k > 0 ? prefix_splits(h, B, P, k) : 1);
+      return pb * (size_t)(np + std::max(suffix_splits(h, B, S_cap), suffix_splits(h, B, S_cap, k > 0)));
+    }
   }
   return 0;
 }
@@ -468,11 +541,15 @@ extern "C" hydra_status hydra_attn(const hydra_heads *h, int64_t B, const void *
   if (!aligned16(q, es, {q_sb, q_sh}) || (P > 0 && (!aligned16(pk, es, {kv_st, kv_sh}) || !aligned16(pv, es, {}))) ||
       (S_cap > 0 && (!aligned16(sk, es, {s_sb, s_st, s_sh}) || !aligned16(sv, es, {}))))
     return fail(HYDRA_EINVAL, "q/k/v base pointers and strides must be 16-byte aligned");
-  const int np = prefix_splits(h, B, P), ns = suffix_splits(h, B, S_cap);
-  const size_t need = part_bytes(h, B) * (np + ns);
-  if (!ws || ws_bytes < need) return fail(HYDRA_ENOMEM, "workspace too small: need %zu bytes", need);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   cudaStream_t sa = s_aux ? reinterpret_cast<cudaStream_t>(s_aux) : s;
+  // With a second stream and both persistent tensor-core kernels, run them concurrently
+  // on disjoint SM sets (k prefix CTAs + (SMs - k) suffix CTAs, one CTA per SM each).
+  const int k_over = (sa != s) ? overlap_prefix_ctas(h, B, P, S_cap) : 0;
+  const int sms = device_sm_count();
+  const int np = prefix_splits(h, B, P, k_over), ns = suffix_splits(h, B, S_cap, k_over > 0);
+  const size_t need = part_bytes(h, B) * (np + ns);
+  if (!ws || ws_bytes < need) return fail(HYDRA_ENOMEM, "workspace too small: need %zu bytes", need);
   PartsView all = parts_in_ws(ws, h, B, np + ns);
   PartsView pre = all, suf = all;
   suf.o = all.o + all.o_stride * np;
@@ -484,14 +561,15 @@ extern "C" hydra_status hydra_attn(const hydra_heads *h, int64_t B, const void *
       return cuda_fail("fork");
   }
   if (P > 0) {
-    st = run_prefix(h, B, q, q_sb, q_sh, P, pk, pv, kv_st, kv_sh, np, pre, sa);
+    st = run_prefix(h, B, q, q_sb, q_sh, P, pk, pv, kv_st, kv_sh, np, pre, sa, k_over);
   } else {
     st = launch_fill_neg_inf(pre.lse, rows, sa);
     if (st) st = cuda_fail("fill");
   }
   if (st) return st;
   if (S_cap > 0) {
-    st = run_suffix(h, B, q, q_sb, q_sh, sk, sv, s_sb, s_st, s_sh, S_cap, lens, ns, suf, s);
+    st = run_suffix(h, B, q, q_sb, q_sh, sk, sv, s_sb, s_st, s_sh, S_cap, lens, ns, suf, s,
+                    k_over > 0 ? std::max(1, sms - k_over) : 0);
   } else {
     st = launch_fill_neg_inf(suf.lse, rows, s);
     if (st) st = cuda_fail("fill");

@@ -89,6 +89,19 @@ hydra_status launch_prefix_tc(const PrefixTcArgs &a, cudaStream_t s);
 hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s);
 int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas);
 int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas);
+// Persistent tensor-core suffix kernel (bf16, d = 128, g <= 16), TMA-fed.
+struct SuffixTcArgs {
+  const void *q;
+  int64_t q_sb, q_sh;
+  const void *k, *v;
+  int64_t s_sb, s_st, s_sh, S_cap;
+  const int32_t *lens;
+  int32_t B, Hq, Hkv;
+  float scale_log2;
+  float *o, *lse;  // [B, Hq, 128], [B, Hq]
+};
+bool suffix_tc_supported(const hydra_heads *h);
+hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s);
 int device_sm_count();
 
 }  // namespace hydra

@@ -22,7 +22,8 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(autouse=True)
 def _reset_config():
-    keys = ("prefix_impl", "prefix_splits", "suffix_splits", "tc_debug_variant", "prefix_ctas")
+    keys = ("prefix_impl", "prefix_splits", "suffix_splits", "tc_debug_variant", "prefix_ctas", "suffix_impl",
+            "suffix_ctas", "overlap_prefix_ctas")
     for k in keys:
         hydra.set_config(k, 0)
     yield
@@ -113,8 +114,10 @@ def test_prefix_simt_bf16():
 
 # ---------------------------------------------------------------- suffix kernel
 @pytest.mark.parametrize("B,Hq,Hkv,d,S", [(7, 8, 8, 128, 300), (5, 16, 4, 128, 77), (6, 16, 1, 128, 40),
-                                          (4, 8, 2, 64, 129), (3, 32, 2, 128, 64)])
-def test_suffix_parity(B, Hq, Hkv, d, S):
+                                          (4, 8, 2, 64, 129), (3, 32, 2, 128, 64), (9, 12, 4, 128, 513)])
+@pytest.mark.parametrize("impl", [1, 2])  # 1: SIMT split-K, 2: persistent tensor-core (falls back if unsupported)
+def test_suffix_parity(B, Hq, Hkv, d, S, impl):
+    hydra.set_config("suffix_impl", impl)
     rng = np.random.default_rng(B * S)
     lens = rng.integers(0, S + 1, B)
     lens[0] = S
@@ -158,6 +161,34 @@ def test_composite_parity(B, Hq, Hkv, d, P, S, dist, aux):
     ref, lref = oracle.flat_attention(pb)
     assert out.dtype == torch.bfloat16
     assert_parity(out, ref, lse, lref, what="composite")
+
+
+@pytest.mark.parametrize("k", [1, 50, 100, 147])
+@pytest.mark.parametrize("B,Hq,Hkv,P,S", [(40, 8, 8, 1000, 200), (24, 32, 8, 513, 33)])
+def test_composite_sm_partitioned(k, B, Hq, Hkv, P, S):
+    """Persistent prefix (k CTAs) || persistent tensor-core suffix (SMs - k CTAs) on two streams."""
+    hydra.set_config("prefix_impl", 3)
+    hydra.set_config("suffix_impl", 2)
+    hydra.set_config("overlap_prefix_ctas", k)
+    rng = np.random.default_rng(k)
+    lens = rng.integers(0, S + 1, B)
+    pb = synth.make_problem(B, Hq, Hkv, 128, P, S, lens=lens, dtype="bf16", dist="boundary", seed=17)
+    out, lse = run_flat(pb, aux=True)
+    ref, lref = oracle.flat_attention(pb)
+    assert_parity(out, ref, lse, lref, what=f"partitioned k={k}")
+
+
+@pytest.mark.parametrize("ctas", [1, 5, 148])
+def test_suffix_tc_ctas_and_ragged(ctas):
+    hydra.set_config("suffix_impl", 2)
+    hydra.set_config("suffix_ctas", ctas)
+    lens = [0, 1, 127, 128, 129, 255, 256, 300, 17, 0, 384]
+    pb = synth.make_problem(len(lens), 8, 1, 128, 0, 384, lens=lens, dtype="bf16", dist="boundary", seed=18)
+    t = problem_to(pb, DEV)
+    o, lse = hydra.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
+    torch.cuda.synchronize()
+    ref, lref = oracle.suffix_only(pb)
+    assert_parity(o, ref, lse, lref, what=f"suffix tc ctas={ctas}")
 
 
 def test_composite_f32_output_is_tighter():

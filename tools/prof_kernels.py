@@ -11,9 +11,13 @@ ap.add_argument("--Hkv", type=int, default=40); ap.add_argument("--P", type=int,
 ap.add_argument("--S", type=int, default=256); ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--what", default="prefix", choices=["prefix", "suffix", "attn"])
 ap.add_argument("--splits", type=int, default=0)
+ap.add_argument("--suffix-impl", type=int, default=0)
+ap.add_argument("--prefix-impl", type=int, default=0)
 a = ap.parse_args()
 dev = torch.device("cuda:0")
 hydra.set_config("prefix_splits", a.splits)
+hydra.set_config("suffix_impl", a.suffix_impl)
+hydra.set_config("prefix_impl", a.prefix_impl)
 S = a.S if a.what != "prefix" else 1
 # plain N(0,1) on device is enough for profiling (values do not change the work)
 g = torch.Generator(device=dev); g.manual_seed(0)
