@@ -29,6 +29,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -73,7 +74,8 @@ struct __align__(64) PrefixTc2Params {
   int32_t n_splits;   // task mode: KV splits per task
   int32_t n_items;    // task mode: tasks * Hkv * n_splits
   int32_t nb;         // flat mode: KV blocks per item (ceil(P / 128))
-  int64_t total_blocks;  // flat mode: n_pairs * Hkv * nb
+  int64_t total_blocks;  // flat mode: units in the stream-K space (Hkv*nb grouped, n_pairs*Hkv*nb not)
+  int32_t group;         // flat mode: CTAs per group (= n_pairs when grouped, else 1)
   float *o, *lse;
   int64_t o_slot_stride, lse_slot_stride;
 };
@@ -84,23 +86,35 @@ struct Item {
 };
 
 // Iterates the KV segments a persistent CTA owns.
-//  flat mode (stream-K): the (item = (pair, head), KV block) space of total_blocks is cut
-//    into gridDim.x equal contiguous ranges; a range may start/end inside an item, and
-//    each piece of an item writes its own partial slot (slot = this CTA - the CTA owning
-//    the item's first block), merged later by the LSE combine.
+//  flat mode, grouped stream-K: CTAs form groups of `group` members; member m of a group
+//    owns query-tile pair m (rows 256m .. 256m+255) of every head, and the group walks a
+//    contiguous range of the (head, 128-token KV block) space -- the space of
+//    Hkv * nb units is cut into G = gridDim.x / group equal ranges.  All members of a
+//    group read the same K/V tiles at about the same time, so each tile comes from DRAM
+//    once and from L2 for the other members.  With group == 1 the unit space is
+//    (pair, head, block) instead.  A range may start or end inside a head; every piece
+//    writes its own partial slot (slot = this group - the group owning the head's first
+//    block), merged later by the LSE combine.
 //  task mode (tree): items = (task, head, split) dealt round-robin.
 struct SegIter {
   int64_t x, end;
   int w;
 };
 
+__device__ __forceinline__ int n_groups(const PrefixTc2Params &P) { return gridDim.x / P.group; }
+
 __device__ __forceinline__ int64_t sk_start(const PrefixTc2Params &P, int64_t c) {
-  return c * P.total_blocks / gridDim.x;
+  return c * P.total_blocks / n_groups(P);
 }
 
 __device__ __forceinline__ void seg_begin(const PrefixTc2Params &P, SegIter &s) {
-  s.x = sk_start(P, blockIdx.x);
-  s.end = sk_start(P, blockIdx.x + 1);
+  const int grp = blockIdx.x / P.group;
+  if (grp >= n_groups(P)) {  // leftover CTAs when gridDim.x % group != 0
+    s.x = s.end = 0;
+  } else {
+    s.x = sk_start(P, grp);
+    s.end = sk_start(P, grp + 1);
+  }
   s.w = blockIdx.x;
 }
 
@@ -127,22 +141,24 @@ __device__ __forceinline__ bool seg_next(const PrefixTc2Params &P, SegIter &s, I
     return true;
   }
   if (s.x >= s.end) return false;
-  const int64_t item = s.x / P.nb;
+  const int64_t unit = s.x / P.nb;  // head (grouped) or (pair, head)
   const int b = (int)(s.x % P.nb);
   const int64_t room = s.end - s.x;
   const int len = (int)(P.nb - b < room ? P.nb - b : room);
-  // CTA owning this item's first block: largest c with sk_start(c) <= item*nb
-  const int64_t x0 = item * P.nb;
-  int64_t c0 = x0 * gridDim.x / P.total_blocks;
-  while (c0 + 1 < gridDim.x && sk_start(P, c0 + 1) <= x0) ++c0;
+  // group owning this unit's first block: largest c with sk_start(c) <= unit*nb
+  const int G = n_groups(P);
+  const int64_t x0 = unit * P.nb;
+  int64_t c0 = x0 * G / P.total_blocks;
+  while (c0 + 1 < G && sk_start(P, c0 + 1) <= x0) ++c0;
   while (c0 > 0 && sk_start(P, c0) > x0) --c0;
-  it.j = (int)(item / P.n_pairs);
+  const int64_t pair = P.group > 1 ? (int64_t)(blockIdx.x % P.group) : unit % P.n_pairs;
+  it.j = (int)(P.group > 1 ? unit : unit / P.n_pairs);
   it.kv_off = 0;
   it.kv_len = P.P;
   it.n_rows = (int64_t)P.B * P.g;
-  it.row0 = (item % P.n_pairs) * (2 * tc2::BM);
+  it.row0 = pair * (2 * tc2::BM);
   it.seq_off = 0;
-  it.slot = (int)(blockIdx.x - c0);
+  it.slot = (int)(blockIdx.x / P.group - c0);
   it.blk_begin = b;
   it.nblk = len;
   s.x += len;
@@ -469,20 +485,33 @@ static bool make_kv_map2(CUtensorMap *m, const void *base, int64_t T, int Hkv, i
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Flat mode: number of partial slots a stream-K schedule over n_ctas CTAs produces per row.
-int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas) {
+// Flat-mode schedule: grouped stream-K when there are at least two groups' worth of CTAs.
+struct Tc2Plan {
+  int group, ctas;
+  int64_t total;  // stream-K units
+};
+static Tc2Plan tc2_plan(int64_t B, int g, int Hkv, int64_t P, int n_ctas) {
   const int64_t nb = (P + 127) / 128;
-  const int64_t total = ((B * g + 255) / 256) * Hkv * nb;
-  if (total <= 0) return 1;
-  const int64_t G = n_ctas < total ? n_ctas : total;
-  const int64_t range = total / G;  // >= 1
+  const int64_t n_pairs = (B * g + 255) / 256;
+  Tc2Plan pl;
+  pl.group = (n_pairs > 1 && 2 * n_pairs <= n_ctas) ? (int)n_pairs : 1;
+  pl.total = pl.group > 1 ? (int64_t)Hkv * nb : n_pairs * Hkv * nb;
+  const int64_t G = std::min<int64_t>(n_ctas / pl.group, pl.total);
+  pl.ctas = (int)(std::max<int64_t>(G, 1) * pl.group);
+  return pl;
+}
+
+// Flat mode: number of partial slots per row the schedule over n_ctas CTAs produces.
+int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas) {
+  const Tc2Plan pl = tc2_plan(B, g, Hkv, P, n_ctas);
+  if (pl.total <= 0) return 1;
+  const int64_t nb = (P + 127) / 128;
+  const int64_t range = pl.total / (pl.ctas / pl.group);  // >= 1
   return (int)((nb + range - 1) / range + 1);
 }
 
 int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas) {
-  const int64_t nb = (P + 127) / 128;
-  const int64_t total = ((B * g + 255) / 256) * Hkv * nb;
-  return (int)(n_ctas < total ? n_ctas : total);
+  return tc2_plan(B, g, Hkv, P, n_ctas).ctas;
 }
 
 hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s) {
@@ -514,14 +543,17 @@ hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s
   P.n_splits = a.n_splits;
   P.n_items = a.tasks ? a.n_tasks * a.Hkv * a.n_splits : 0;
   P.nb = (int)((a.P + 127) / 128);
-  P.total_blocks = a.tasks ? 0 : (int64_t)P.n_pairs * a.Hkv * P.nb;
+  Tc2Plan pl{1, n_ctas, 0};
+  if (!a.tasks) pl = tc2_plan(a.B, a.g, a.Hkv, a.P, n_ctas > 0 ? n_ctas : 1 << 30);
+  P.total_blocks = a.tasks ? 0 : pl.total;
+  P.group = pl.group;
   P.o = a.o;
   P.lse = a.lse;
   P.o_slot_stride = a.o_slot_stride;
   P.lse_slot_stride = a.lse_slot_stride;
   const int64_t work = a.tasks ? P.n_items : P.total_blocks;
   if (work == 0) return HYDRA_OK;
-  const int grid = (int)(n_ctas > 0 && n_ctas < work ? n_ctas : work);
+  const int grid = a.tasks ? (int)(n_ctas > 0 && n_ctas < work ? n_ctas : work) : pl.ctas;
   prefix_tc2_kernel<<<grid, tc2::kThreads, tc2::ALLOC, s>>>(P);
   return cudaGetLastError() == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
 }
