@@ -232,6 +232,25 @@ def main():
         ms = time_graph(g_main, args.steps, args.warmup)
     clocks = clk.summary()
 
+    # Flatness (north_star: total time at B=1024 should drop < 15% when the prefix grows
+    # from 1K to 16K): the same suffixes with the prefix cut to its first 1024 tokens,
+    # timed the same way (best of the two schedules).
+    flat = None
+    if P > 1024:
+        P1 = 1024
+        pk1, pv1 = pk[:P1], pv[:P1]
+        ws1 = torch.empty(hydra.attn_workspace_bytes(q, P1, S, Hkv_r), dtype=torch.uint8, device=dev)
+
+        def step1(overlap: bool):
+            hydra.hydragen_attention(q, pk1, pv1, sk, sv, lens, out=out, workspace=ws1,
+                                     aux_stream=aux if overlap else None)
+
+        ms1 = min(time_graph(capture(lambda: step1(True)), args.steps, args.warmup),
+                  time_graph(capture(lambda: step1(False)), args.steps, args.warmup))
+        q1, q16 = B / (ms1 * 1e-3), B / (ms * 1e-3)
+        flat = {"prefix_1k_queries_per_s": round(q1, 1), "prefix_%d_queries_per_s" % P: round(q16, 1),
+                "drop": round(1.0 - q16 / q1, 4), "target_drop": 0.15, "ms_prefix_1k": round(ms1, 5)}
+
     # per-kernel timing on their own (roofline of the dominant kernel and the prefix phase)
     # (the composite's workspace holds (prefix + suffix) split partials, enough for either alone)
     g_pre = capture(lambda: hydra.prefix_attn(q, pk, pv, workspace=ws))
@@ -285,8 +304,10 @@ def main():
         "step_roofline": {"t_roof_ms": round(t_roof * 1e3, 5), "frac": round(t_roof * 1e3 / ms, 4),
                           "ms_sequential": round(ms_seq, 5), "ms_overlap": round(ms_over, 5)},
         "clocks": clocks,
-        "gpu_launches": args.steps * 3,
+        "gpu_launches": args.steps * (4 if overlap else 3),
     }
+    if flat:
+        line["flatness"] = flat
 
     if not args.no_e2e:
         line["e2e"] = e2e_leg(args, hydra, torch, dev, world, (hq, hpk, hpv, hsk, hsv, hlens),

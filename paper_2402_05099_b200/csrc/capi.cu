@@ -545,7 +545,9 @@ extern "C" hydra_status hydra_attn(const hydra_heads *h, int64_t B, const void *
   cudaStream_t sa = s_aux ? reinterpret_cast<cudaStream_t>(s_aux) : s;
   // With a second stream and both persistent tensor-core kernels, run them concurrently
   // on disjoint SM sets (k prefix CTAs + (SMs - k) suffix CTAs, one CTA per SM each).
+  // Without an SM split (k = 0) two full grids would only contend: run sequentially.
   const int k_over = (sa != s) ? overlap_prefix_ctas(h, B, P, S_cap) : 0;
+  if (k_over == 0) sa = s;
   const int sms = device_sm_count();
   const int np = prefix_splits(h, B, P, k_over), ns = suffix_splits(h, B, S_cap, k_over > 0);
   const size_t need = part_bytes(h, B) * (np + ns);
