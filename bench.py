@@ -43,6 +43,14 @@ CONFIGS = {
                name="CodeLlama-7b attention shape (32 q / 32 kv heads, d=128), B=256, prefix 2048, suffix 128"),
     "c4_1gpu": dict(B=512, Hq=32, Hkv=8, d=128, P=32768, S=128,
                     name="Llama-3-8B GQA attention shape (32 q / 8 kv, d=128), B=512, prefix 32768, suffix 128"),
+    # prefix sequence split across ranks + NCCL all-gather of (O fp16, LSE) (dist.seqsplit_attention)
+    "c4": dict(B=512, Hq=32, Hkv=8, d=128, P=32768, S=128, kind="seqsplit",
+               name="Llama-3-8B GQA attention shape (32 q / 8 kv, d=128), B=512, prefix 32768 split along the "
+                    "sequence across ranks with an NCCL (O, LSE) all-gather, suffix 128"),
+    # two-level sharing tree (tree_attention)
+    "c5": dict(B=1024, Hq=32, Hkv=32, d=128, P=4096, S=512, kind="tree", branches=16, branch_len=1024,
+               name="tree sharing: 4096-token root -> 16 branches x 1024 tokens -> 64 sequences each with 512-token "
+                    "suffixes, CodeLlama-7b attention shape (32 MHA heads, d=128)"),
 }
 
 
@@ -139,10 +147,215 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def make_timer(torch, dist, dev, world):
+    """CUDA-graph capture and device timing (CUDA events, barrier, max over ranks)."""
+
+    def capture(fn):
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):
+            fn()  # eager warm-up outside capture
+        torch.cuda.current_stream(dev).wait_stream(s)
+        torch.cuda.synchronize(dev)
+        with torch.cuda.graph(g):
+            fn()
+        torch.cuda.synchronize(dev)
+        return g
+
+    def time_fn(run, k, w):
+        for _ in range(w):
+            run()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(k):
+            run()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        ms = e0.elapsed_time(e1) / k
+        if world > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    return capture, time_fn
+
+
+def base_line(args, cfg, world, ms, B, dtype="bf16"):
+    return {
+        "metric": "decode-attn queries/s and % of bf16 TC peak; prefix 16K, batch 1024, 1/2/4/8 GPU",
+        "value": round(B / (ms * 1e-3), 1), "unit": "queries/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": dtype,
+        "data": "synthetic (seeded PCG64 N(0,1) K/V rounded to bf16, 'mixed' needle queries)",
+    }
+
+
+def run_tree(args, cfg):
+    """C5: two-level sharing tree through hydra.tree_attention (one GPU; replicas for N > 1)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import paper_2402_05099_b200 as hydra
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    B, Hq, Hkv, d, S = cfg["B"], cfg["Hq"], cfg["Hkv"], cfg["d"], cfg["S"]
+    nbr, blen = cfg["branches"], cfg["branch_len"]
+    if Hkv % world:
+        raise SystemExit("Hkv not divisible by world")
+    Hq_r, Hkv_r = Hq // world, Hkv // world
+    parent, node_len, leaf = synth.two_level_tree(cfg["P"], nbr, blen, B // nbr)
+    tp = synth.make_tree_problem(parent, node_len, leaf, Hq_r, Hkv_r, d, S, dtype="bf16", dist="mixed",
+                                 seed=args.seed + rank)
+    t = lambda a: torch.from_numpy(a).view(torch.bfloat16).to(dev)
+    q, nk, nv, sk, sv = t(tp.q), t(tp.node_k), t(tp.node_v), t(tp.sk), t(tp.sv)
+    lens = torch.from_numpy(tp.lens.astype(np.int32)).to(dev)
+    tree = hydra.Tree(tp.parent, tp.node_off, tp.node_len, tp.leaf_of_seq)
+    capture, time_fn = make_timer(torch, dist, dev, world)
+    g = capture(lambda: hydra.tree_attention(q, tree, nk, nv, sk, sv, lens))
+    with ClockSampler(local) as clk:
+        ms = time_fn(g.replay, args.steps, args.warmup)
+    g_suf = capture(lambda: hydra.suffix_attn(q, sk, sv, lens))
+    ms_suf = time_fn(g_suf.replay, max(5, args.steps // 4), 3)
+    pk = peaks()
+    hbm = float(pk.get("hbm_gbs", 6650.0))
+    suffix_bytes = 2 * int(tp.lens.sum()) * Hkv_r * d * 2 + B * Hq_r * d * 2
+    # every node's K/V attended by the stacked queries of its group (§3.3): 4 d per (row, token)
+    flops = 4.0 * Hq_r * d * sum(int(node_len[n]) * tree.group_size(n) for n in range(len(node_len)))
+    line = base_line(args, cfg, world, ms, B)
+    line["config"] = {"workload": args.config, "description": cfg["name"], "B": B, "Hq": Hq, "Hkv": Hkv, "d": d,
+                      "root_len": cfg["P"], "branches": nbr, "branch_len": blen, "suffix_len": S,
+                      "parallelism": f"kv-head shard x{world}" if world > 1 else "1 GPU",
+                      "l2": "no flush: %.2f GB of inputs per step > 126 MB L2" % (suffix_bytes / 1e9)}
+    line["roofline"] = {"bound": "hbm", "kernel": "suffix split-K GEMV (decode_attn_kernel)",
+                        "achieved": round(suffix_bytes / (ms_suf * 1e-3) / 1e9, 1), "peak": hbm, "unit": "GB/s",
+                        "frac": round(suffix_bytes / (ms_suf * 1e-3) / 1e9 / hbm, 4), "traffic": None,
+                        "algorithmic_bytes_per_launch": suffix_bytes, "launch_ms": round(ms_suf, 5)}
+    line["tree_prefix_flops_per_step"] = flops
+    line["clocks"] = clk.summary()
+    line["gpu_launches"] = args.steps * 4
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+
+        n = 2
+        bb, hh = np.meshgrid(np.arange(n), np.arange(Hq_r), indexing="ij")
+        t0 = time.time()
+        oracle.tree_attention(tp, rows=np.stack([bb.ravel(), hh.ravel()], 1))
+        dt = time.time() - t0
+        n2 = int(max(1, min(B, n * args.cpu_seconds / max(dt, 1e-3))))
+        bb, hh = np.meshgrid(np.arange(n2), np.arange(Hq_r), indexing="ij")
+        t0 = time.time()
+        oracle.tree_attention(tp, rows=np.stack([bb.ravel(), hh.ravel()], 1))
+        dt2 = time.time() - t0
+        line["cpu_baseline"] = {"value": round(n2 / dt2, 3), "unit": "queries/s", "cores": oracle.max_threads(),
+                                "kind": "oracle", "sample": f"first {n2} of {B} sequences x all heads, {dt2:.1f} s"}
+    if not args.no_e2e:
+        pinned = [x.pin_memory() for x in (torch.from_numpy(tp.q).view(torch.bfloat16),
+                                             torch.from_numpy(tp.sk).view(torch.bfloat16),
+                                             torch.from_numpy(tp.sv).view(torch.bfloat16))]
+        h2d = sum(x.numel() * x.element_size() for x in pinned)
+        hout = torch.empty(B, Hq_r, d, dtype=torch.bfloat16).pin_memory()
+
+        def one():
+            for src, dst in zip(pinned, (q, sk, sv)):
+                dst.copy_(src, non_blocking=True)
+            hout.copy_(hydra.tree_attention(q, tree, nk, nv, sk, sv, lens), non_blocking=True)
+
+        ms_e = time_fn(one, args.e2e_steps, 1)
+        line["e2e"] = {"value": round(B / (ms_e * 1e-3), 1), "unit": "queries/s", "h2d_bytes_per_step": int(h2d),
+                       "d2h_bytes_per_step": int(hout.numel() * 2), "ms_per_step": round(ms_e, 3),
+                       "note": "tree node K/V stay resident (shared across steps); q and suffix K/V copied per step"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_seqsplit(args, cfg):
+    """C4: prefix split along the sequence across ranks, NCCL all-gather of (O fp16, LSE) + combine."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import paper_2402_05099_b200 as hydra
+    from paper_2402_05099_b200 import dist as hdist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=dev, init_method=None if world > 1 else "tcp://127.0.0.1:%d"
+                                % (29500 + os.getpid() % 1000), rank=rank, world_size=world)
+    B, Hq, Hkv, d, P, S = cfg["B"], cfg["Hq"], cfg["Hkv"], cfg["d"], cfg["P"], cfg["S"]
+    p0, p1 = hdist.shard_range(P, world, rank)
+    b0, b1 = hdist.shard_range(B, world, rank)
+    # every rank draws the same q; its own prefix shard and batch-shard suffixes (seeded per rank)
+    pq = synth.make_problem(B, Hq, Hkv, d, 0, 0, dtype="bf16", seed=args.seed)
+    pr = synth.make_problem(b1 - b0, Hq, Hkv, d, p1 - p0, S, dtype="bf16", seed=args.seed + 1 + rank)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).view(torch.bfloat16).to(dev)
+    q, pk, pv, sk, sv = t(pq.q), t(pr.pk), t(pr.pv), t(pr.sk), t(pr.sv)
+    lens = torch.from_numpy(pr.lens.astype(np.int32)).to(dev)
+    capture, time_fn = make_timer(torch, dist, dev, world)
+    fn = lambda: hdist.seqsplit_attention(q, pk, pv, sk, sv, lens)
+    try:
+        g = capture(fn)
+        run = g.replay
+        graphed = True
+    except Exception:  # NCCL capture unsupported here: time eagerly
+        run, graphed = fn, False
+    with ClockSampler(local) as clk:
+        ms = time_fn(run, args.steps, args.warmup)
+    pk_ = peaks()
+    flops = 4.0 * B * Hq * (p1 - p0) * d
+    g_pre = capture(lambda: hydra.prefix_attn(q, pk, pv))
+    ms_pre = time_fn(g_pre.replay, max(5, args.steps // 4), 3)
+    tc = float(pk_.get("bf16_tflops", 1590.0))
+    line = base_line(args, cfg, world, ms, B)
+    line["config"] = {"workload": args.config, "description": cfg["name"], "B": B, "Hq": Hq, "Hkv": Hkv, "d": d,
+                      "prefix_len": P, "suffix_len": S, "parallelism": f"prefix sequence split x{world}",
+                      "prefix_tokens_per_rank": p1 - p0, "exchange": "NCCL all_gather_into_tensor of fp16 O + fp32 LSE",
+                      "exchange_bytes_per_rank": sum(hdist.exchange_layout(B, Hq, d)), "cuda_graph": graphed,
+                      "l2": "no flush: %.2f GB of prefix K/V per rank > 126 MB L2" % (2 * (p1 - p0) * Hkv * d * 2 / 1e9)}
+    line["roofline"] = {"bound": "tensor", "kernel": "prefix_tc2_kernel (tcgen05)",
+                        "achieved": round(flops / (ms_pre * 1e-3) / 1e12, 1), "peak": tc, "unit": "TFLOP/s",
+                        "frac": round(flops / (ms_pre * 1e-3) / 1e12 / tc, 4), "traffic": None,
+                        "algorithmic_flops_per_launch": flops, "launch_ms": round(ms_pre, 5)}
+    line["clocks"] = clk.summary()
+    line["gpu_launches"] = args.steps * 6
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return reference_arm(args)
+    kind = CONFIGS[args.config].get("kind")
+    if kind == "tree":
+        return run_tree(args, dict(CONFIGS[args.config]))
+    if kind == "seqsplit":
+        return run_seqsplit(args, dict(CONFIGS[args.config]))
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -399,18 +612,30 @@ def reference_arm(args):
     B, Hq, Hkv, d, P, S = cfg["B"], cfg["Hq"], cfg["Hkv"], cfg["d"], cfg["P"], cfg["S"]
     budget = 150.0  # seconds for the whole --steps K --warmup W run
     per_step = budget / max(1, args.steps + args.warmup)
-    # calibrate the sample size on a 2-sequence problem of the same shape
-    cal = synth.make_problem(2, Hq, Hkv, d, P, S, dtype="bf16", dist="mixed", seed=args.seed)
+    tree = cfg.get("kind") == "tree"
+
+    def problem(n):
+        if tree:  # same root / branch lengths, n sequences spread over the branches
+            per = max(1, -(-n // cfg["branches"]))
+            parent, node_len, leaf = synth.two_level_tree(P, cfg["branches"], cfg["branch_len"], per)
+            return synth.make_tree_problem(parent, node_len, leaf, Hq, Hkv, d, S, dtype="bf16", dist="mixed",
+                                           seed=args.seed)
+        return synth.make_problem(n, Hq, Hkv, d, P, S, dtype="bf16", dist="mixed", seed=args.seed)
+
+    run_oracle = oracle.tree_attention if tree else oracle.flat_attention
+    # calibrate the sample size on a small problem of the same shape
+    cal = problem(2)
     t0 = time.time()
-    oracle.flat_attention(cal)
-    per_seq = (time.time() - t0) / 2
+    run_oracle(cal)
+    per_seq = (time.time() - t0) / cal.B
     nseq = int(max(1, min(B, per_step / max(per_seq, 1e-6))))
-    pb = synth.make_problem(nseq, Hq, Hkv, d, P, S, dtype="bf16", dist="mixed", seed=args.seed)
+    pb = problem(nseq)
+    nseq = pb.B
     for _ in range(args.warmup):
-        oracle.flat_attention(pb)
+        run_oracle(pb)
     t0 = time.time()
     for _ in range(args.steps):
-        oracle.flat_attention(pb)
+        run_oracle(pb)
     dt = (time.time() - t0) / max(1, args.steps)
     value = nseq / dt
     cores = oracle.max_threads()
