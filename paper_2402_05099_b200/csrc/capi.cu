@@ -780,6 +780,15 @@ extern "C" hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra
       d_tasks = it->second.first;
       n_tasks = it->second.second;
     }
+    if (getenv("HYDRA_DEBUG_TREE")) {
+      std::vector<PrefixTask> hv(n_tasks);
+      cudaMemcpy(hv.data(), d_tasks, sizeof(PrefixTask) * n_tasks, cudaMemcpyDeviceToHost);
+      fprintf(stderr, "[hydra] tree kind=%d g=%d np=%d n_tasks=%d sizeof(task)=%zu\n", (int)kind, g, np, n_tasks,
+              sizeof(PrefixTask));
+      for (auto &x : hv)
+        fprintf(stderr, "  task kv_off=%lld kv_len=%lld seq_off=%d n_seq=%d slot=%d tile=%d\n", (long long)x.kv_off,
+                (long long)x.kv_len, x.seq_off, x.n_seq, x.slot, x.tile);
+    }
     if (n_tasks > 0) {
       PrefixTcArgs a{};
       a.q = q;
@@ -803,8 +812,9 @@ extern "C" hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra
       a.o_slot_stride = all.o_stride;
       a.lse_slot_stride = all.lse_stride;
       a.debug_variant = (int32_t)g_tc_debug;
-    a.stages = (int32_t)g_prefix_stages;
-      st = launch_prefix_tc(a, s);
+      a.stages = (int32_t)g_prefix_stages;
+      // the work list holds 256-row tile pairs for v3 and 128-row tiles for v1
+      st = kind == PK_TC2 ? launch_prefix_tc2(a, prefix_ctas(), s) : launch_prefix_tc(a, s);
       if (st) return cuda_fail("tree prefix tcgen05 launch");
     }
   } else {

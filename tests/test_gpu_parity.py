@@ -316,3 +316,21 @@ def test_seqsplit_single_rank_nccl():
             assert_parity(out, ref, lse, lref, what=f"seqsplit {ex}")
     finally:
         tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("impl", [0, 2, 3])
+@pytest.mark.parametrize("per,g", [(300, 1), (100, 4)])
+def test_tree_large_groups(impl, per, g):
+    """Groups with > 128 and > 256 stacked rows: both query tiles of a pair and several pairs
+    per node (the persistent kernel's task mode), on root and branch nodes."""
+    hydra.set_config("prefix_impl", impl)
+    parent, node_len, leaf = synth.two_level_tree(300, 2, 200, per)
+    tp = synth.make_tree_problem(parent, node_len, leaf, 4 * g, 4, 128, 24, dtype="bf16", dist="boundary", seed=19)
+    t = tree_to(tp, DEV)
+    tree = hydra.Tree(tp.parent, tp.node_off, tp.node_len, tp.leaf_of_seq)
+    out, lse = hydra.tree_attention(t["q"], tree, t["node_k"], t["node_v"], t["sk"], t["sv"], t["lens"],
+                                    return_lse=True)
+    torch.cuda.synchronize()
+    ref, lref = oracle.tree_attention(tp)
+    assert_parity(out, ref, lse, lref, what=f"tree large groups impl={impl} per={per} g={g}")
+    tree.destroy()
