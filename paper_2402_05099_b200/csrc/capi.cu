@@ -41,7 +41,7 @@ static hydra_status cuda_fail(const char *what) {
 
 static std::atomic<int64_t> g_prefix_impl{0}, g_prefix_splits{0}, g_suffix_splits{0}, g_tc_debug{0},
     g_prefix_stages{3}, g_suffix_unroll{4}, g_prefix_ctas{0}, g_suffix_impl{0}, g_suffix_ctas{0},
-    g_overlap_prefix_ctas{0};
+    g_overlap_prefix_ctas{0}, g_prefix_poly{0};
 
 extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
   if (!key) return fail(HYDRA_EINVAL, "null key");
@@ -53,6 +53,7 @@ extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
   else if (!strcmp(key, "suffix_impl")) g_suffix_impl = value;
   else if (!strcmp(key, "suffix_ctas")) g_suffix_ctas = value;
   else if (!strcmp(key, "overlap_prefix_ctas")) g_overlap_prefix_ctas = value;
+  else if (!strcmp(key, "prefix_poly")) g_prefix_poly = (value == 0 || value == 2 || value == 3) ? value : 4;
   else if (!strcmp(key, "prefix_stages")) g_prefix_stages = (value == 2 ? 2 : 3);
   else if (!strcmp(key, "suffix_unroll")) g_suffix_unroll = (value >= 8 ? 8 : value >= 4 ? 4 : 2);
   else return fail(HYDRA_EINVAL, "unknown config key '%s'", key);
@@ -70,6 +71,7 @@ extern "C" int64_t hydra_get_config(const char *key) {
   if (!strcmp(key, "suffix_impl")) return g_suffix_impl;
   if (!strcmp(key, "suffix_ctas")) return g_suffix_ctas;
   if (!strcmp(key, "overlap_prefix_ctas")) return g_overlap_prefix_ctas;
+  if (!strcmp(key, "prefix_poly")) return g_prefix_poly;
   if (!strcmp(key, "suffix_unroll")) return g_suffix_unroll;
   return -1;
 }
@@ -282,6 +284,7 @@ static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, i
     a.lse_slot_stride = dst.lse_stride;
     a.debug_variant = (int32_t)g_tc_debug;
     a.stages = (int32_t)g_prefix_stages;
+    a.poly_every = (int32_t)g_prefix_poly;
     hydra_status st;
     if (kind == PK_TC2) {
       // stream-K pieces leave some slots of a row unwritten: mark every slot empty first
@@ -813,6 +816,7 @@ extern "C" hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra
       a.lse_slot_stride = all.lse_stride;
       a.debug_variant = (int32_t)g_tc_debug;
       a.stages = (int32_t)g_prefix_stages;
+    a.poly_every = (int32_t)g_prefix_poly;
       // the work list holds 256-row tile pairs for v3 and 128-row tiles for v1
       st = kind == PK_TC2 ? launch_prefix_tc2(a, prefix_ctas(), s) : launch_prefix_tc(a, s);
       if (st) return cuda_fail("tree prefix tcgen05 launch");

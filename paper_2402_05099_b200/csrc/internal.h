@@ -80,6 +80,7 @@ struct PrefixTcArgs {
   float *o, *lse;
   int64_t o_slot_stride, lse_slot_stride;
   int32_t debug_variant;
+  int32_t poly_every = 0;  // v3: every k-th exp2 column pair on the FMA pipe (0 = all MUFU)
   int32_t stages;  // K/V pipeline stages: 2 (160 KB smem, leaves room for co-resident suffix CTAs) or 3
 };
 bool prefix_tc_supported(const hydra_heads *h);

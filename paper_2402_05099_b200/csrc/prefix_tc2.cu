@@ -165,6 +165,7 @@ __device__ __forceinline__ bool seg_next(const PrefixTc2Params &P, SegIter &s, I
   return true;
 }
 
+template <int kPolyEvery>  // 0: all exp2 on MUFU; k: every k-th column pair on the FMA pipe
 __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __grid_constant__ PrefixTc2Params P) {
   using namespace tc2;
   extern __shared__ uint8_t smem_raw[];
@@ -200,6 +201,11 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  // Register rebalancing per warpgroup (inside disjoint role branches so ptxas allocates each
+  // region separately): producer / MMA / idle warps need few registers, the two softmax
+  // warpgroups hold a 128-column score row each (128*80 + 256*208 <= 64K).
+  if (warp < 4) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 80;" ::: "memory");
   if (warp == 0) {
     // ================= TMA producer =================
     if (ptx::elect_one()) {
@@ -292,7 +298,9 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
         gb += it.nblk;
       }
     }
-  } else if (warp >= 4) {
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
     // ================= softmax / correction / epilogue =================
     const int t = (warp - 4) / 4;          // query tile of this warpgroup
     const int quarter = warp % 4;           // TMEM lane quarter
@@ -389,7 +397,13 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
             ptx::unpack2(ptx::fma2(ptx::pack2(__uint_as_float(sr[c][2 * i]), __uint_as_float(sr[c][2 * i + 1])), cc,
                                    nm),
                          x0, x1);
-            const float p0 = fast_exp2(x0), p1 = fast_exp2(x1);
+            float p0, p1;
+            if (kPolyEvery > 0 && (i % kPolyEvery) == kPolyEvery - 1) {
+              ptx::exp2_poly2(x0, x1, p0, p1);  // FMA-pipe exp2 for 1/kPolyEvery of the pairs
+            } else {
+              p0 = fast_exp2(x0);
+              p1 = fast_exp2(x1);
+            }
             sacc[i % 4] = ptx::add2(sacc[i % 4], ptx::pack2(p0, p1));
             pk[i] = ptx::cvt_bf16x2(p0, p1);
           }
@@ -514,13 +528,21 @@ int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas) {
   return tc2_plan(B, g, Hkv, P, n_ctas).ctas;
 }
 
-hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s) {
+template <int kPoly>
+static cudaError_t tc2_attr() {
   static std::once_flag once;
   static cudaError_t attr = cudaSuccess;
   std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(prefix_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::ALLOC);
+    attr = cudaFuncSetAttribute(prefix_tc2_kernel<kPoly>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::ALLOC);
   });
-  if (attr != cudaSuccess) return HYDRA_ECUDA;
+  return attr;
+}
+
+hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s) {
+  const int poly = a.poly_every;
+  if ((poly == 0 ? tc2_attr<0>() : poly == 3 ? tc2_attr<3>() : poly == 2 ? tc2_attr<2>() : tc2_attr<4>()) !=
+      cudaSuccess)
+    return HYDRA_ECUDA;
   PrefixTc2Params P;
   memset(&P, 0, sizeof(P));
   if (a.kv_total > 0) {
@@ -554,7 +576,14 @@ hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s
   const int64_t work = a.tasks ? P.n_items : P.total_blocks;
   if (work == 0) return HYDRA_OK;
   const int grid = a.tasks ? (int)(n_ctas > 0 && n_ctas < work ? n_ctas : work) : pl.ctas;
-  prefix_tc2_kernel<<<grid, tc2::kThreads, tc2::ALLOC, s>>>(P);
+  if (poly == 0)
+    prefix_tc2_kernel<0><<<grid, tc2::kThreads, tc2::ALLOC, s>>>(P);
+  else if (poly == 2)
+    prefix_tc2_kernel<2><<<grid, tc2::kThreads, tc2::ALLOC, s>>>(P);
+  else if (poly == 3)
+    prefix_tc2_kernel<3><<<grid, tc2::kThreads, tc2::ALLOC, s>>>(P);
+  else
+    prefix_tc2_kernel<4><<<grid, tc2::kThreads, tc2::ALLOC, s>>>(P);
   return cudaGetLastError() == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
 }
 

@@ -216,6 +216,27 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {  // FMNMX3
   asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
   return d;
 }
+// 2^x for a pair on the FMA/ALU pipes (offloads MUFU.EX2):  x = n + f, n = rint(x) via the
+// 1.5*2^23 magic add, f in [-0.5, 0.5]; 2^f by a degree-3 relative-error fit (max rel err
+// 7.5e-5, far below bf16's 2^-9); 2^n added to the exponent field.  x is clamped at -126
+// (result >= 2^-126, i.e. a masked score contributes ~1e-38 instead of exactly 0).
+__device__ __forceinline__ void exp2_poly2(float x0, float x1, float &y0, float &y1) {
+  x0 = fmaxf(x0, -126.f);
+  x1 = fmaxf(x1, -126.f);
+  const uint64_t magic = pack2(12582912.f, 12582912.f), nmagic = pack2(-12582912.f, -12582912.f);
+  const uint64_t x = pack2(x0, x1);
+  const uint64_t t = add2(x, magic);                                      // low mantissa bits = n
+  const uint64_t f = add2(x, add2(t, nmagic) ^ 0x8000000080000000ull);  // x - n  (negate via sign bits)
+  uint64_t p = fma2(f, pack2(0.0551716685f, 0.0551716685f), pack2(0.242611155f, 0.242611155f));
+  p = fma2(f, p, pack2(0.693260968f, 0.693260968f));
+  p = fma2(f, p, pack2(0.999928057f, 0.999928057f));
+  float p0, p1, t0, t1;
+  unpack2(p, p0, p1);
+  unpack2(t, t0, t1);
+  y0 = __uint_as_float(__float_as_uint(p0) + (__float_as_uint(t0) << 23));
+  y1 = __uint_as_float(__float_as_uint(p1) + (__float_as_uint(t1) << 23));
+}
+
 // two fp32 -> packed bf16x2 (round to nearest even); `lo` lands in the low 16 bits
 __device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
   uint32_t d;

@@ -4,8 +4,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2402_05099_b200 as hydra
 dev = torch.device("cuda:0")
-def run(B, H, Hkv, P, impl, ctas=0, iters=20):
-    hydra.set_config("prefix_impl", impl); hydra.set_config("prefix_ctas", ctas)
+def run(B, H, Hkv, P, impl, ctas=0, iters=20, poly=4):
+    hydra.set_config("prefix_impl", impl); hydra.set_config("prefix_ctas", ctas); hydra.set_config("prefix_poly", poly)
     g = torch.Generator(device=dev); g.manual_seed(0)
     q = torch.randn(B, H, 128, device=dev, generator=g).bfloat16()
     pk = torch.randn(P, Hkv, 128, device=dev, generator=g).bfloat16()
@@ -25,11 +25,7 @@ def run(B, H, Hkv, P, impl, ctas=0, iters=20):
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / iters
     fl = 4.0 * B * H * P * 128
-    print(json.dumps(dict(B=B, H=H, Hkv=Hkv, P=P, impl=impl, ctas=ctas, ms=round(ms, 4), tflops=round(fl / ms / 1e9, 1))), flush=True)
-for impl in (2, 3):
-    run(1024, 40, 40, 16384, impl)
-    run(1024, 40, 40, 1024, impl)
-    run(256, 32, 32, 2048, impl)
-    run(512, 32, 8, 32768, impl)
-for c in (74, 96, 120):
-    run(1024, 40, 40, 16384, 3, c)
+    print(json.dumps(dict(B=B, H=H, Hkv=Hkv, P=P, impl=impl, ctas=ctas, poly=poly, ms=round(ms, 4), tflops=round(fl / ms / 1e9, 1))), flush=True)
+for poly in (0, 4, 3, 2):
+    run(1024, 40, 40, 16384, 3, poly=poly)
+    run(512, 32, 8, 32768, 3, poly=poly)
