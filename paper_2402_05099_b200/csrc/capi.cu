@@ -41,7 +41,7 @@ static hydra_status cuda_fail(const char *what) {
 
 static std::atomic<int64_t> g_prefix_impl{0}, g_prefix_splits{0}, g_suffix_splits{0}, g_tc_debug{0},
     g_prefix_stages{3}, g_suffix_unroll{4}, g_prefix_ctas{0}, g_suffix_impl{0}, g_suffix_ctas{0},
-    g_overlap_prefix_ctas{0}, g_prefix_poly{0};
+    g_overlap_prefix_ctas{0}, g_prefix_poly{0}, g_prefix_variant{3};
 
 extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
   if (!key) return fail(HYDRA_EINVAL, "null key");
@@ -54,6 +54,7 @@ extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
   else if (!strcmp(key, "suffix_ctas")) g_suffix_ctas = value;
   else if (!strcmp(key, "overlap_prefix_ctas")) g_overlap_prefix_ctas = value;
   else if (!strcmp(key, "prefix_poly")) g_prefix_poly = (value == 0 || value == 2 || value == 3) ? value : 4;
+  else if (!strcmp(key, "prefix_variant")) g_prefix_variant = (value == 4 ? 4 : 3);
   else if (!strcmp(key, "prefix_stages")) g_prefix_stages = (value == 2 ? 2 : 3);
   else if (!strcmp(key, "suffix_unroll")) g_suffix_unroll = (value >= 8 ? 8 : value >= 4 ? 4 : 2);
   else return fail(HYDRA_EINVAL, "unknown config key '%s'", key);
@@ -72,6 +73,7 @@ extern "C" int64_t hydra_get_config(const char *key) {
   if (!strcmp(key, "suffix_ctas")) return g_suffix_ctas;
   if (!strcmp(key, "overlap_prefix_ctas")) return g_overlap_prefix_ctas;
   if (!strcmp(key, "prefix_poly")) return g_prefix_poly;
+  if (!strcmp(key, "prefix_variant")) return g_prefix_variant;
   if (!strcmp(key, "suffix_unroll")) return g_suffix_unroll;
   return -1;
 }
@@ -148,6 +150,7 @@ static int suffix_splits(const hydra_heads *h, int64_t B, int64_t S_cap, bool ov
 // one-tile tcgen05 kernel (v1) or the SIMT kernel on request / for unsupported shapes.
 enum PrefixKind { PK_SIMT = 1, PK_TC1 = 2, PK_TC2 = 3 };
 static int prefix_ctas() { return g_prefix_ctas > 0 ? (int)g_prefix_ctas : device_sm_count(); }
+static int prefix_bn() { return g_prefix_variant == 4 ? 64 : 128; }  // KV tokens per persistent-kernel block
 // B/P-dependent choice (rows = stacked query rows per KV head, P = KV tokens per row):
 // the persistent kernel amortises its per-segment Q load / epilogue only when every CTA
 // owns enough 128-token blocks; small problems run the one-tile kernel (more parallelism).
@@ -199,7 +202,7 @@ static int prefix_splits(const hydra_heads *h, int64_t B, int64_t P, int tc2_cta
   const int g = h->num_q_heads / h->num_kv_heads;
   switch (prefix_kind(h, B * g, P)) {
     case PK_TC2:
-      return prefix_tc2_slots(B, g, h->num_kv_heads, P, tc2_ctas > 0 ? tc2_ctas : prefix_ctas());
+      return prefix_tc2_slots(B, g, h->num_kv_heads, P, tc2_ctas > 0 ? tc2_ctas : prefix_ctas(), prefix_bn());
     case PK_TC1:
       return prefix_splits_tc(((B * g + 127) / 128) * h->num_kv_heads, P);
     default:
@@ -285,6 +288,7 @@ static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, i
     a.debug_variant = (int32_t)g_tc_debug;
     a.stages = (int32_t)g_prefix_stages;
     a.poly_every = (int32_t)g_prefix_poly;
+    a.variant = (int32_t)g_prefix_variant;
     hydra_status st;
     if (kind == PK_TC2) {
       // stream-K pieces leave some slots of a row unwritten: mark every slot empty first
@@ -817,6 +821,7 @@ extern "C" hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra
       a.debug_variant = (int32_t)g_tc_debug;
       a.stages = (int32_t)g_prefix_stages;
     a.poly_every = (int32_t)g_prefix_poly;
+    a.variant = (int32_t)g_prefix_variant;
       // the work list holds 256-row tile pairs for v3 and 128-row tiles for v1
       st = kind == PK_TC2 ? launch_prefix_tc2(a, prefix_ctas(), s) : launch_prefix_tc(a, s);
       if (st) return cuda_fail("tree prefix tcgen05 launch");

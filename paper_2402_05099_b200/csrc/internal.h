@@ -81,6 +81,7 @@ struct PrefixTcArgs {
   int64_t o_slot_stride, lse_slot_stride;
   int32_t debug_variant;
   int32_t poly_every = 0;  // v3: every k-th exp2 column pair on the FMA pipe (0 = all MUFU)
+  int32_t variant = 3;     // persistent kernel: 3 (128-token blocks) or 4 (64-token, double-buffered S)
   int32_t stages;  // K/V pipeline stages: 2 (160 KB smem, leaves room for co-resident suffix CTAs) or 3
 };
 bool prefix_tc_supported(const hydra_heads *h);
@@ -88,8 +89,8 @@ hydra_status launch_prefix_tc(const PrefixTcArgs &a, cudaStream_t s);
 // v3: persistent, two 128-row query tiles per CTA; flat mode is stream-K over n_ctas CTAs
 // (partial slots per row = prefix_tc2_slots), task mode deals (task, head, split) items.
 hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s);
-int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas);
-int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas);
+int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn);
+int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn);
 // Persistent tensor-core suffix kernel (bf16, d = 128, g <= 16), TMA-fed.
 struct SuffixTcArgs {
   const void *q;

@@ -76,6 +76,7 @@ struct __align__(64) PrefixTc2Params {
   int32_t nb;         // flat mode: KV blocks per item (ceil(P / 128))
   int64_t total_blocks;  // flat mode: units in the stream-K space (Hkv*nb grouped, n_pairs*Hkv*nb not)
   int32_t group;         // flat mode: CTAs per group (= n_pairs when grouped, else 1)
+  int32_t bn;            // KV tokens per block (128: v3, 64: v4)
   float *o, *lse;
   int64_t o_slot_stride, lse_slot_stride;
 };
@@ -134,7 +135,7 @@ __device__ __forceinline__ bool seg_next(const PrefixTc2Params &P, SegIter &s, I
     it.row0 = (int64_t)task.tile * (2 * tc2::BM);
     it.seq_off = task.seq_off;
     it.slot = task.slot + split;
-    const int nblk_total = (int)((task.kv_len + tc2::BN - 1) / tc2::BN);
+    const int nblk_total = (int)((task.kv_len + P.bn - 1) / P.bn);
     const int per_split = (nblk_total + P.n_splits - 1) / P.n_splits;
     it.blk_begin = split * per_split;
     it.nblk = max(0, min(nblk_total, it.blk_begin + per_split) - it.blk_begin);
@@ -473,6 +474,345 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
   }
 }
 
+// ===================================================================================
+// v4: 64-token KV blocks with two score buffers per query tile.
+// TMEM per tile t (256 columns): S_t[0] at [256t, 256t+64), S_t[1] at [256t+64, 256t+128),
+// O_t at [256t+128, 256t+256).  P_t(n) aliases the first 32 columns of S_t[n & 1].
+// Because S_t(n+2) lands in the other buffer than S_t(n+1), the MMA thread issues
+//   prologue: S_0(0) S_1(0) S_0(1) S_1(1);   block n: PV_0(n) S_0(n+2) PV_1(n) S_1(n+2)
+// and the score MMA of the next block is always done before the softmax of the current
+// block ends, so the softmax warpgroups run back to back instead of waiting a full
+// PV + S round trip per block (the v3 limiter).  The commit after S_t(n+2) also covers
+// PV_t(n), so the P write of block n+2 into the same buffer is ordered; the rare O
+// correction of block n waits for PV_t(n-1) explicitly.
+namespace tc4 {
+constexpr int BM = 128;
+constexpr int BN = 64;
+constexpr int HD = 128;
+constexpr int NS = 4;
+constexpr int kThreads = 384;
+constexpr int QPANEL = BM * 128;  // 16 KB
+constexpr int QTILE = 2 * QPANEL;  // 32 KB
+constexpr int KPANEL = BN * 128;   // 8 KB: 64 rows x 128 B
+constexpr int KTILE = 2 * KPANEL;  // 16 KB
+constexpr int OFF_Q = 0;
+constexpr int OFF_K = 2 * QTILE;
+constexpr int OFF_V = OFF_K + NS * KTILE;
+constexpr int OFF_BAR = OFF_V + NS * KTILE;
+// k_full, k_empty, v_full, v_empty [NS]; q_full[2]; s_full[2][2]; p_full[2][2]; pv_done[2]; o_free[2];
+// o_ready[2] (one completion per item: the last PV of the item has landed)
+constexpr int N_BARS = 4 * NS + 2 + 4 + 4 + 2 + 2 + 2;
+constexpr int BYTES = OFF_BAR + N_BARS * 8 + 16;
+constexpr int ALLOC = BYTES + 1024;
+constexpr uint32_t TMEM_COLS = 512;
+}  // namespace tc4
+
+__global__ void __launch_bounds__(tc4::kThreads, 1) prefix_tc4_kernel(const __grid_constant__ PrefixTc2Params P) {
+  using namespace tc4;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
+  uint64_t *k_full = bars, *k_empty = bars + NS, *v_full = bars + 2 * NS, *v_empty = bars + 3 * NS;
+  uint64_t *q_full = bars + 4 * NS;      // [2]
+  uint64_t *s_full = q_full + 2;         // [tile][buf]
+  uint64_t *p_full = s_full + 4;         // [tile][buf]
+  uint64_t *pv_done = p_full + 4;        // [tile]
+  uint64_t *o_free = pv_done + 2;        // [tile]
+  uint64_t *o_ready = o_free + 2;        // [tile]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + N_BARS);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&P.tmK);
+    ptx::prefetch_tmap(&P.tmV);
+    for (int i = 0; i < NS; ++i) {
+      ptx::mbar_init(&k_full[i], 1);
+      ptx::mbar_init(&k_empty[i], 1);
+      ptx::mbar_init(&v_full[i], 1);
+      ptx::mbar_init(&v_empty[i], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      ptx::mbar_init(&q_full[t], 128);
+      ptx::mbar_init(&pv_done[t], 1);
+      ptx::mbar_init(&o_free[t], 128);
+      ptx::mbar_init(&o_ready[t], 1);
+      for (int b = 0; b < 2; ++b) {
+        ptx::mbar_init(&s_full[2 * t + b], 1);
+        ptx::mbar_init(&p_full[2 * t + b], 128);
+      }
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;" ::: "memory");
+    if (warp == 0) {
+      // ================= TMA producer =================
+      if (ptx::elect_one()) {
+        uint32_t gb = 0;
+        SegIter si;
+        seg_begin(P, si);
+        Item it;
+        while (seg_next(P, si, it)) {
+          for (int n = 0; n < it.nblk; ++n, ++gb) {
+            const int st = gb % NS;
+            const uint32_t ph = (gb / NS) & 1;
+            const int t0 = (int)(it.kv_off + (int64_t)(it.blk_begin + n) * BN);
+            uint8_t *sK = smem + OFF_K + st * KTILE;
+            uint8_t *sV = smem + OFF_V + st * KTILE;
+            ptx::mbar_wait(&k_empty[st], ph ^ 1);
+            ptx::mbar_arrive_expect_tx(&k_full[st], KTILE);
+            ptx::tma_load_3d(sK, &P.tmK, &k_full[st], 0, it.j, t0);
+            ptx::tma_load_3d(sK + KPANEL, &P.tmK, &k_full[st], 64, it.j, t0);
+            ptx::mbar_wait(&v_empty[st], ph ^ 1);
+            ptx::mbar_arrive_expect_tx(&v_full[st], KTILE);
+            ptx::tma_load_3d(sV, &P.tmV, &v_full[st], 0, it.j, t0);
+            ptx::tma_load_3d(sV + KPANEL, &P.tmV, &v_full[st], 64, it.j, t0);
+          }
+        }
+      }
+    } else if (warp == 1) {
+      // ================= MMA issuer =================
+      if (ptx::elect_one()) {
+        constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BM, BN, false);
+        constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(BM, HD, true);
+        uint32_t gb = 0, qc[2] = {0, 0}, pc[4] = {0, 0, 0, 0}, oc[2] = {0, 0};
+        SegIter si;
+        seg_begin(P, si);
+        Item it;
+        while (seg_next(P, si, it)) {
+          if (it.nblk == 0) continue;
+          const int ntile = (it.n_rows - it.row0 > BM) ? 2 : 1;
+          auto issue_s = [&](int t, int n) {  // S_t(n) into buffer n & 1
+            const uint32_t st = (gb + n) % NS;
+            const uint32_t q_addr = ptx::smem_u32(smem + OFF_Q + t * QTILE);
+            const uint32_t k_addr = ptx::smem_u32(smem + OFF_K + st * KTILE);
+#pragma unroll
+            for (int kk = 0; kk < HD / 16; ++kk)
+              ptx::mma_ss(tmem + t * 256 + (n & 1) * BN,
+                          ptx::smem_desc_sw128(q_addr + (kk / 4) * QPANEL + (kk % 4) * 32, 16, 1024),
+                          ptx::smem_desc_sw128(k_addr + (kk / 4) * KPANEL + (kk % 4) * 32, 16, 1024), idesc_s,
+                          kk > 0);
+            ptx::mma_commit(&s_full[2 * t + (n & 1)]);
+          };
+          auto wait_k = [&](int n) {
+            const uint32_t g0 = gb + n;
+            ptx::mbar_wait(&k_full[g0 % NS], (g0 / NS) & 1);
+            ptx::tc_fence_after();
+          };
+          for (int t = 0; t < ntile; ++t) {
+            ptx::mbar_wait(&q_full[t], qc[t] & 1);
+            ++qc[t];
+          }
+          for (int n = 0; n < 2 && n < it.nblk; ++n) {  // prologue: S_t(0), S_t(1)
+            wait_k(n);
+            for (int t = 0; t < ntile; ++t) issue_s(t, n);
+            ptx::mma_commit(&k_empty[(gb + n) % NS]);
+          }
+          for (int n = 0; n < it.nblk; ++n) {
+            const uint32_t g0 = gb + n;
+            const int st = g0 % NS;
+            const bool more = n + 2 < it.nblk;
+            ptx::mbar_wait(&v_full[st], (g0 / NS) & 1);
+            const uint32_t v_addr = ptx::smem_u32(smem + OFF_V + st * KTILE);
+            for (int t = 0; t < ntile; ++t) {
+              const int pb = 2 * t + (n & 1);
+              ptx::mbar_wait(&p_full[pb], pc[pb] & 1);
+              ++pc[pb];
+              if (n == 0) {
+                ptx::mbar_wait(&o_free[t], (oc[t] & 1) ^ 1);
+                ++oc[t];
+              }
+              ptx::tc_fence_after();
+#pragma unroll
+              for (int kk = 0; kk < BN / 16; ++kk)
+                ptx::mma_ts(tmem + t * 256 + 128, tmem + t * 256 + (n & 1) * BN + kk * 8,
+                            ptx::smem_desc_sw128(v_addr + kk * 2048, KPANEL, 1024), idesc_pv, (n > 0 || kk > 0));
+              ptx::mma_commit(&pv_done[t]);
+              if (n == it.nblk - 1) ptx::mma_commit(&o_ready[t]);
+              if (more) {
+                if (t == 0) wait_k(n + 2);
+                issue_s(t, n + 2);
+              }
+            }
+            ptx::mma_commit(&v_empty[st]);
+            if (more) ptx::mma_commit(&k_empty[(g0 + 2) % NS]);
+          }
+          gb += it.nblk;
+        }
+      }
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
+    // ================= softmax / correction / epilogue =================
+    const int t = (warp - 4) / 4;
+    const int quarter = warp % 4;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const uint32_t o_col = tmem + lane_base + t * 256 + 128;
+    uint8_t *sQ = smem + OFF_Q + t * QTILE;
+    const float c2 = P.scale_log2;
+    uint32_t sc[2] = {0, 0}, pvn = 0, orc = 0;  // s_full phase per buffer; PV_t count; items done
+    SegIter si;
+    seg_begin(P, si);
+    Item it;
+    while (seg_next(P, si, it)) {
+      const int64_t trow0 = it.row0 + t * BM;
+      if (trow0 >= it.n_rows) continue;
+      const int64_t rr = trow0 + r;
+      const bool live = rr < it.n_rows;
+      int64_t seq = 0;
+      int h = 0;
+      if (live) {
+        seq = P.seq_list ? P.seq_list[it.seq_off + rr / P.g] : rr / P.g;
+        h = it.j * P.g + (int)(rr % P.g);
+      }
+      float *orow = P.o + it.slot * P.o_slot_stride + (seq * P.Hq + h) * HD;
+      if (it.nblk == 0) {
+        if (live) {
+          P.lse[it.slot * P.lse_slot_stride + seq * P.Hq + h] = -INFINITY;
+          for (int c = 0; c < HD / 4; ++c) reinterpret_cast<float4 *>(orow)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        continue;
+      }
+      {
+        uint4 ch[16];
+        if (live) {
+          const uint4 *src = reinterpret_cast<const uint4 *>(P.q + seq * P.q_sb + (int64_t)h * P.q_sh);
+#pragma unroll
+          for (int c = 0; c < 16; ++c) ch[c] = __ldg(src + c);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) ch[c] = make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          *reinterpret_cast<uint4 *>(sQ + (c / 8) * QPANEL + r * 128 + (((c % 8) ^ (r % 8)) * 16)) = ch[c];
+        ptx::fence_proxy_async_smem();
+        ptx::mbar_arrive(&q_full[t]);
+      }
+      float m2 = -INFINITY, l = 0.f;
+      for (int n = 0; n < it.nblk; ++n) {
+        const int b = n & 1;
+        const uint32_t s_col = tmem + lane_base + t * 256 + b * BN;
+        ptx::mbar_wait(&s_full[2 * t + b], sc[b] & 1);
+        ++sc[b];
+        ptx::tc_fence_after();
+        uint32_t sr[2][32];
+        ptx::tmem_ld32(s_col, sr[0]);
+        ptx::tmem_ld32(s_col + 32, sr[1]);
+        ptx::tmem_ld_wait();
+        const int64_t rem = it.kv_len - (int64_t)(it.blk_begin + n) * BN;
+        if (rem < BN) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c * 32 + i >= rem) sr[c][i] = 0xff800000u;
+        }
+        float acc[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] = fmaxf(__uint_as_float(sr[0][2 * k]), __uint_as_float(sr[0][2 * k + 1]));
+#pragma unroll
+        for (int i = 16; i < BN; i += 16)
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            acc[k] = ptx::fmax3(acc[k], __uint_as_float(sr[(i + 2 * k) / 32][(i + 2 * k) % 32]),
+                                __uint_as_float(sr[(i + 2 * k + 1) / 32][(i + 2 * k + 1) % 32]));
+        const float mx = fmaxf(ptx::fmax3(acc[0], acc[1], acc[2]),
+                               fmaxf(ptx::fmax3(acc[3], acc[4], acc[5]), fmaxf(acc[6], acc[7])));
+        const float mnew = mx * c2;
+        const bool any = __any_sync(0xffffffffu, mnew > m2 + 8.0f);
+        float alpha = 1.f;
+        if (any) {
+          const float mt = fmaxf(m2, mnew);
+          alpha = fast_exp2(m2 - mt);
+          m2 = mt;
+        }
+        const uint64_t cc = ptx::pack2(c2, c2), nm = ptx::pack2(-m2, -m2);
+        uint64_t sacc[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float x0, x1;
+            ptx::unpack2(ptx::fma2(ptx::pack2(__uint_as_float(sr[c][2 * i]), __uint_as_float(sr[c][2 * i + 1])), cc,
+                                   nm),
+                         x0, x1);
+            const float p0 = fast_exp2(x0), p1 = fast_exp2(x1);
+            sacc[i % 4] = ptx::add2(sacc[i % 4], ptx::pack2(p0, p1));
+            pk[i] = ptx::cvt_bf16x2(p0, p1);
+          }
+          ptx::tmem_st16(s_col + c * 16, pk);  // P(n) -> first 32 columns of S_t[n & 1]
+        }
+        float s0, s1, s2, s3;
+        ptx::unpack2(ptx::add2(sacc[0], sacc[1]), s0, s1);
+        ptx::unpack2(ptx::add2(sacc[2], sacc[3]), s2, s3);
+        l = l * alpha + ((s0 + s1) + (s2 + s3));
+        if (any && n >= 1) {  // rare O correction: needs PV_t(n-1) (completion index pvn-1) landed
+          ptx::mbar_wait(&pv_done[t], (pvn - 1) & 1);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t ov[32];
+            ptx::tmem_ld32(o_col + c * 32, ov);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+            ptx::tmem_st32(o_col + c * 32, ov);
+          }
+        }
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(&p_full[2 * t + b]);
+        ++pvn;
+      }
+      // All PVs of this item landed.  (pv_done cannot be used here: up to two PVs may be in
+      // flight, and a parity wait cannot tell "one phase behind" from "two phases behind".)
+      ptx::mbar_wait(&o_ready[t], orc & 1);
+      ++orc;
+      ptx::tc_fence_after();
+      const float inv = 1.f / l;
+      uint32_t *stage = reinterpret_cast<uint32_t *>(sQ + quarter * 32 * 128);
+      const uint64_t my_row = live ? reinterpret_cast<uint64_t>(orow) : 0ull;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t ov[32];
+        ptx::tmem_ld32(o_col + c * 32, ov);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) stage[lane * 32 + (i ^ lane)] = __float_as_uint(__uint_as_float(ov[i]) * inv);
+        __syncwarp();
+#pragma unroll 4
+        for (int rw = 0; rw < 32; ++rw) {
+          const uint64_t base = __shfl_sync(0xffffffffu, my_row, rw);
+          const uint32_t v = stage[rw * 32 + (lane ^ rw)];
+          if (base) reinterpret_cast<float *>(base)[c * 32 + lane] = __uint_as_float(v);
+        }
+        __syncwarp();
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(&o_free[t]);
+      if (live) P.lse[it.slot * P.lse_slot_stride + seq * P.Hq + h] = (m2 + log2f(l)) * HYDRA_LN2;
+      ptx::fence_proxy_async_smem();
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<tc4::TMEM_COLS>(tmem);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn2() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -487,12 +827,13 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn2() {
   return fn;
 }
 
-static bool make_kv_map2(CUtensorMap *m, const void *base, int64_t T, int Hkv, int64_t st, int64_t sh) {
+static bool make_kv_map2(CUtensorMap *m, const void *base, int64_t T, int Hkv, int64_t st, int64_t sh,
+                         int box_rows = tc2::BN) {
   auto fn = encode_fn2();
   if (!fn) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)tc2::HD, (cuuint64_t)Hkv, (cuuint64_t)T};
   const cuuint64_t strides[2] = {(cuuint64_t)sh * 2, (cuuint64_t)st * 2};
-  const cuuint32_t box[3] = {64, 1, (cuuint32_t)tc2::BN};
+  const cuuint32_t box[3] = {64, 1, (cuuint32_t)box_rows};
   const cuuint32_t estr[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -504,8 +845,8 @@ struct Tc2Plan {
   int group, ctas;
   int64_t total;  // stream-K units
 };
-static Tc2Plan tc2_plan(int64_t B, int g, int Hkv, int64_t P, int n_ctas) {
-  const int64_t nb = (P + 127) / 128;
+static Tc2Plan tc2_plan(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn = 128) {
+  const int64_t nb = (P + bn - 1) / bn;
   const int64_t n_pairs = (B * g + 255) / 256;
   Tc2Plan pl;
   pl.group = (n_pairs > 1 && 2 * n_pairs <= n_ctas) ? (int)n_pairs : 1;
@@ -516,16 +857,16 @@ static Tc2Plan tc2_plan(int64_t B, int g, int Hkv, int64_t P, int n_ctas) {
 }
 
 // Flat mode: number of partial slots per row the schedule over n_ctas CTAs produces.
-int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas) {
-  const Tc2Plan pl = tc2_plan(B, g, Hkv, P, n_ctas);
+int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn) {
+  const Tc2Plan pl = tc2_plan(B, g, Hkv, P, n_ctas, bn);
   if (pl.total <= 0) return 1;
-  const int64_t nb = (P + 127) / 128;
+  const int64_t nb = (P + bn - 1) / bn;
   const int64_t range = pl.total / (pl.ctas / pl.group);  // >= 1
   return (int)((nb + range - 1) / range + 1);
 }
 
-int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas) {
-  return tc2_plan(B, g, Hkv, P, n_ctas).ctas;
+int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn) {
+  return tc2_plan(B, g, Hkv, P, n_ctas, bn).ctas;
 }
 
 template <int kPoly>
@@ -538,17 +879,30 @@ static cudaError_t tc2_attr() {
   return attr;
 }
 
+static cudaError_t tc4_attr() {
+  static std::once_flag once;
+  static cudaError_t attr = cudaSuccess;
+  std::call_once(once, [] {
+    attr = cudaFuncSetAttribute(prefix_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc4::ALLOC);
+  });
+  return attr;
+}
+
 hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s) {
   const int poly = a.poly_every;
-  if ((poly == 0 ? tc2_attr<0>() : poly == 3 ? tc2_attr<3>() : poly == 2 ? tc2_attr<2>() : tc2_attr<4>()) !=
-      cudaSuccess)
+  const bool v4 = a.variant == 4;
+  const int bn = v4 ? tc4::BN : tc2::BN;
+  if (v4 ? tc4_attr() != cudaSuccess
+         : (poly == 0 ? tc2_attr<0>() : poly == 3 ? tc2_attr<3>() : poly == 2 ? tc2_attr<2>() : tc2_attr<4>()) !=
+               cudaSuccess)
     return HYDRA_ECUDA;
   PrefixTc2Params P;
   memset(&P, 0, sizeof(P));
   if (a.kv_total > 0) {
-    if (!make_kv_map2(&P.tmK, a.k, a.kv_total, a.Hkv, a.kv_st, a.kv_sh)) return HYDRA_ECUDA;
-    if (!make_kv_map2(&P.tmV, a.v, a.kv_total, a.Hkv, a.kv_st, a.kv_sh)) return HYDRA_ECUDA;
+    if (!make_kv_map2(&P.tmK, a.k, a.kv_total, a.Hkv, a.kv_st, a.kv_sh, bn)) return HYDRA_ECUDA;
+    if (!make_kv_map2(&P.tmV, a.v, a.kv_total, a.Hkv, a.kv_st, a.kv_sh, bn)) return HYDRA_ECUDA;
   }
+  P.bn = bn;
   P.q = reinterpret_cast<const __nv_bfloat16 *>(a.q);
   P.q_sb = a.q_sb;
   P.q_sh = a.q_sh;
@@ -564,9 +918,9 @@ hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s
   P.seq_list = a.seq_list;
   P.n_splits = a.n_splits;
   P.n_items = a.tasks ? a.n_tasks * a.Hkv * a.n_splits : 0;
-  P.nb = (int)((a.P + 127) / 128);
+  P.nb = (int)((a.P + bn - 1) / bn);
   Tc2Plan pl{1, n_ctas, 0};
-  if (!a.tasks) pl = tc2_plan(a.B, a.g, a.Hkv, a.P, n_ctas > 0 ? n_ctas : 1 << 30);
+  if (!a.tasks) pl = tc2_plan(a.B, a.g, a.Hkv, a.P, n_ctas > 0 ? n_ctas : 1 << 30, bn);
   P.total_blocks = a.tasks ? 0 : pl.total;
   P.group = pl.group;
   P.o = a.o;
@@ -576,7 +930,9 @@ hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s
   const int64_t work = a.tasks ? P.n_items : P.total_blocks;
   if (work == 0) return HYDRA_OK;
   const int grid = a.tasks ? (int)(n_ctas > 0 && n_ctas < work ? n_ctas : work) : pl.ctas;
-  if (poly == 0)
+  if (v4)
+    prefix_tc4_kernel<<<grid, tc4::kThreads, tc4::ALLOC, s>>>(P);
+  else if (poly == 0)
     prefix_tc2_kernel<0><<<grid, tc2::kThreads, tc2::ALLOC, s>>>(P);
   else if (poly == 2)
     prefix_tc2_kernel<2><<<grid, tc2::kThreads, tc2::ALLOC, s>>>(P);

@@ -26,7 +26,9 @@ def _reset_config():
             "suffix_ctas", "overlap_prefix_ctas")
     for k in keys:
         hydra.set_config(k, 0)
+    hydra.set_config("prefix_variant", 3)
     yield
+    hydra.set_config("prefix_variant", 3)
     for k in keys:
         hydra.set_config(k, 0)
 
@@ -67,9 +69,12 @@ PREFIX_SHAPES = [
 
 @pytest.mark.parametrize("B,Hq,Hkv,P", PREFIX_SHAPES)
 @pytest.mark.parametrize("dist", ["mixed", "boundary"])
-@pytest.mark.parametrize("impl", [2, 3])
+@pytest.mark.parametrize("impl", [2, 3, 4])
 def test_prefix_tc_parity(B, Hq, Hkv, P, dist, impl):
-    hydra.set_config("prefix_impl", impl)  # 2: one-tile tcgen05 kernel, 3: persistent two-tile
+    # 2: one-tile tcgen05 kernel, 3: persistent two-tile (128-token blocks), 4: same with 64-token
+    # blocks and double-buffered scores
+    hydra.set_config("prefix_impl", min(impl, 3))
+    hydra.set_config("prefix_variant", 4 if impl == 4 else 3)
     pb = synth.make_problem(B, Hq, Hkv, 128, P, 1, dtype="bf16", dist=dist, seed=3)
     t = problem_to(pb, DEV)
     o, lse = hydra.prefix_attn(t["q"], t["pk"], t["pv"])
@@ -91,9 +96,11 @@ def test_prefix_tc_splits(splits):
 
 
 @pytest.mark.parametrize("ctas", [1, 3, 7, 64, 148, 100000])
-def test_prefix_tc2_stream_k_ctas(ctas):
+@pytest.mark.parametrize("variant", [3, 4])
+def test_prefix_tc2_stream_k_ctas(ctas, variant):
     """Stream-K piece boundaries fall inside items for most CTA counts; every piece is merged."""
     hydra.set_config("prefix_ctas", ctas)
+    hydra.set_config("prefix_variant", variant)
     pb = synth.make_problem(300, 8, 2, 128, 1100, 1, dtype="bf16", dist="boundary", seed=4)
     t = problem_to(pb, DEV)
     o, lse = hydra.prefix_attn(t["q"], t["pk"], t["pv"])
@@ -318,12 +325,13 @@ def test_seqsplit_single_rank_nccl():
         tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("impl", [0, 2, 3])
+@pytest.mark.parametrize("impl", [0, 2, 3, 4])
 @pytest.mark.parametrize("per,g", [(300, 1), (100, 4)])
 def test_tree_large_groups(impl, per, g):
     """Groups with > 128 and > 256 stacked rows: both query tiles of a pair and several pairs
     per node (the persistent kernel's task mode), on root and branch nodes."""
-    hydra.set_config("prefix_impl", impl)
+    hydra.set_config("prefix_impl", min(impl, 3))
+    hydra.set_config("prefix_variant", 4 if impl == 4 else 3)
     parent, node_len, leaf = synth.two_level_tree(300, 2, 200, per)
     tp = synth.make_tree_problem(parent, node_len, leaf, 4 * g, 4, 128, 24, dtype="bf16", dist="boundary", seed=19)
     t = tree_to(tp, DEV)

@@ -4,8 +4,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2402_05099_b200 as hydra
 dev = torch.device("cuda:0")
-def run(B, H, Hkv, P, impl, ctas=0, iters=20, poly=4):
+def run(B, H, Hkv, P, impl, ctas=0, iters=20, poly=0, variant=3):
     hydra.set_config("prefix_impl", impl); hydra.set_config("prefix_ctas", ctas); hydra.set_config("prefix_poly", poly)
+    hydra.set_config("prefix_variant", variant)
     g = torch.Generator(device=dev); g.manual_seed(0)
     q = torch.randn(B, H, 128, device=dev, generator=g).bfloat16()
     pk = torch.randn(P, Hkv, 128, device=dev, generator=g).bfloat16()
@@ -25,7 +26,8 @@ def run(B, H, Hkv, P, impl, ctas=0, iters=20, poly=4):
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / iters
     fl = 4.0 * B * H * P * 128
-    print(json.dumps(dict(B=B, H=H, Hkv=Hkv, P=P, impl=impl, ctas=ctas, poly=poly, ms=round(ms, 4), tflops=round(fl / ms / 1e9, 1))), flush=True)
-for poly in (0, 4, 3, 2):
-    run(1024, 40, 40, 16384, 3, poly=poly)
-    run(512, 32, 8, 32768, 3, poly=poly)
+    print(json.dumps(dict(B=B, H=H, Hkv=Hkv, P=P, impl=impl, ctas=ctas, poly=poly, variant=variant, ms=round(ms, 4), tflops=round(fl / ms / 1e9, 1))), flush=True)
+for variant in (3, 4):
+    run(1024, 40, 40, 16384, 3, variant=variant)
+    run(512, 32, 8, 32768, 3, variant=variant)
+    run(1024, 40, 40, 4096, 3, variant=variant)
