@@ -41,7 +41,7 @@ static hydra_status cuda_fail(const char *what) {
 
 static std::atomic<int64_t> g_prefix_impl{0}, g_prefix_splits{0}, g_suffix_splits{0}, g_tc_debug{0},
     g_prefix_stages{3}, g_suffix_unroll{4}, g_prefix_ctas{0}, g_suffix_impl{0}, g_suffix_ctas{0},
-    g_overlap_prefix_ctas{0}, g_prefix_poly{0}, g_prefix_variant{3};
+    g_overlap_prefix_ctas{0}, g_prefix_poly{0}, g_prefix_variant{3}, g_prefix_trace{0};
 
 extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
   if (!key) return fail(HYDRA_EINVAL, "null key");
@@ -49,12 +49,13 @@ extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
   else if (!strcmp(key, "prefix_splits")) g_prefix_splits = value;
   else if (!strcmp(key, "suffix_splits")) g_suffix_splits = value;
   else if (!strcmp(key, "tc_debug_variant")) g_tc_debug = value;
+  else if (!strcmp(key, "prefix_trace")) g_prefix_trace = value;
   else if (!strcmp(key, "prefix_ctas")) g_prefix_ctas = value;
   else if (!strcmp(key, "suffix_impl")) g_suffix_impl = value;
   else if (!strcmp(key, "suffix_ctas")) g_suffix_ctas = value;
   else if (!strcmp(key, "overlap_prefix_ctas")) g_overlap_prefix_ctas = value;
-  else if (!strcmp(key, "prefix_poly")) g_prefix_poly = (value == 0 || value == 2 || value == 3) ? value : 4;
-  else if (!strcmp(key, "prefix_variant")) g_prefix_variant = (value == 4 ? 4 : 3);
+  else if (!strcmp(key, "prefix_poly")) g_prefix_poly = (value == 0 || value == 3 || value == 8 || value == -1) ? value : 4;
+  else if (!strcmp(key, "prefix_variant")) g_prefix_variant = (value == 4 || value == 5) ? value : 3;
   else if (!strcmp(key, "prefix_stages")) g_prefix_stages = (value == 2 ? 2 : 3);
   else if (!strcmp(key, "suffix_unroll")) g_suffix_unroll = (value >= 8 ? 8 : value >= 4 ? 4 : 2);
   else return fail(HYDRA_EINVAL, "unknown config key '%s'", key);
@@ -67,6 +68,7 @@ extern "C" int64_t hydra_get_config(const char *key) {
   if (!strcmp(key, "prefix_splits")) return g_prefix_splits;
   if (!strcmp(key, "suffix_splits")) return g_suffix_splits;
   if (!strcmp(key, "tc_debug_variant")) return g_tc_debug;
+  if (!strcmp(key, "prefix_trace")) return g_prefix_trace;
   if (!strcmp(key, "prefix_stages")) return g_prefix_stages;
   if (!strcmp(key, "prefix_ctas")) return g_prefix_ctas;
   if (!strcmp(key, "suffix_impl")) return g_suffix_impl;
@@ -286,6 +288,7 @@ static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, i
     a.o_slot_stride = dst.o_stride;
     a.lse_slot_stride = dst.lse_stride;
     a.debug_variant = (int32_t)g_tc_debug;
+    a.trace = reinterpret_cast<void *>((intptr_t)g_prefix_trace.load());
     a.stages = (int32_t)g_prefix_stages;
     a.poly_every = (int32_t)g_prefix_poly;
     a.variant = (int32_t)g_prefix_variant;
@@ -819,6 +822,7 @@ extern "C" hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra
       a.o_slot_stride = all.o_stride;
       a.lse_slot_stride = all.lse_stride;
       a.debug_variant = (int32_t)g_tc_debug;
+      a.trace = reinterpret_cast<void *>((intptr_t)g_prefix_trace.load());
       a.stages = (int32_t)g_prefix_stages;
     a.poly_every = (int32_t)g_prefix_poly;
     a.variant = (int32_t)g_prefix_variant;

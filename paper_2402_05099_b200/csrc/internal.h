@@ -80,6 +80,7 @@ struct PrefixTcArgs {
   float *o, *lse;
   int64_t o_slot_stride, lse_slot_stride;
   int32_t debug_variant;
+  void *trace = nullptr;  // diagnostics only (config key prefix_trace): device buffer for CTA-0 timestamps
   int32_t poly_every = 0;  // v3: every k-th exp2 column pair on the FMA pipe (0 = all MUFU)
   int32_t variant = 3;     // persistent kernel: 3 (128-token blocks) or 4 (64-token, double-buffered S)
   int32_t stages;  // K/V pipeline stages: 2 (160 KB smem, leaves room for co-resident suffix CTAs) or 3

@@ -56,6 +56,7 @@ constexpr int N_BARS = 4 * NS + 10;
 constexpr int BYTES = OFF_BAR + N_BARS * 8 + 16;
 constexpr int ALLOC = BYTES + 1024;
 constexpr uint32_t TMEM_COLS = 512;
+constexpr int kTraceN = 1024;  // diagnostics: events per trace row
 }  // namespace tc2
 
 struct __align__(64) PrefixTc2Params {
@@ -77,6 +78,8 @@ struct __align__(64) PrefixTc2Params {
   int64_t total_blocks;  // flat mode: units in the stream-K space (Hkv*nb grouped, n_pairs*Hkv*nb not)
   int32_t group;         // flat mode: CTAs per group (= n_pairs when grouped, else 1)
   int32_t bn;            // KV tokens per block (128: v3, 64: v4)
+  int32_t debug;         // timing experiments only (invalid results): bit 1 no softmax math, bit 2 no K/V TMA
+  long long *trace;      // diagnostics: CTA 0 event timestamps (clock64), see tools/prefix_trace.py; null = off
   float *o, *lse;
   int64_t o_slot_stride, lse_slot_stride;
 };
@@ -166,7 +169,9 @@ __device__ __forceinline__ bool seg_next(const PrefixTc2Params &P, SegIter &s, I
   return true;
 }
 
-template <int kPolyEvery>  // 0: all exp2 on MUFU; k: every k-th column pair on the FMA pipe
+// kPolyEvery -- 0: all exp2 on MUFU; k: every k-th column pair on the FMA pipe.
+// kPingPong -- alternate the two tiles' exp phases per SM sub-partition (see the loop).
+template <int kPolyEvery, bool kPingPong>
 __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __grid_constant__ PrefixTc2Params P) {
   using namespace tc2;
   extern __shared__ uint8_t smem_raw[];
@@ -204,9 +209,11 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
 
   // Register rebalancing per warpgroup (inside disjoint role branches so ptxas allocates each
   // region separately): producer / MMA / idle warps need few registers, the two softmax
-  // warpgroups hold a 128-column score row each (128*80 + 256*208 <= 64K).
+  // warpgroups hold a 128-column score row each.  The launch grants 168 per thread (384 threads,
+  // 64K / 384 rounded down to 8): 128 x (168 - 88) released = 256 x (208 - 168) acquired --
+  // an increase not covered by the decrease would block setmaxnreg.inc forever.
   if (warp < 4) {
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 80;" ::: "memory");
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
   if (warp == 0) {
     // ================= TMA producer =================
     if (ptx::elect_one()) {
@@ -221,6 +228,13 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
           const int t0 = (int)(it.kv_off + (int64_t)(it.blk_begin + n) * BN);
           uint8_t *sK = smem + OFF_K + st * TILE;
           uint8_t *sV = smem + OFF_V + st * TILE;
+          if ((P.debug & 4) && gb >= (uint32_t)NS) {  // timing experiment only: no K/V traffic after the fill
+            ptx::mbar_wait(&k_empty[st], ph ^ 1);
+            ptx::mbar_arrive(&k_full[st]);
+            ptx::mbar_wait(&v_empty[st], ph ^ 1);
+            ptx::mbar_arrive(&v_full[st]);
+            continue;
+          }
           ptx::mbar_wait(&k_empty[st], ph ^ 1);
           ptx::mbar_arrive_expect_tx(&k_full[st], TILE);
           ptx::tma_load_3d(sK, &P.tmK, &k_full[st], 0, it.j, t0);
@@ -238,6 +252,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
       constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BM, BN, false);  // S = Q K^T (both K-major)
       constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(BM, HD, true);  // O += P V (V MN-major)
       uint32_t gb = 0, qc[2] = {0, 0}, pc[2] = {0, 0}, oc[2] = {0, 0};
+      long long *tr = (P.trace && blockIdx.x == 0) ? P.trace : nullptr;
       SegIter si;
       seg_begin(P, si);
       Item it;
@@ -275,6 +290,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
           for (int t = 0; t < ntile; ++t) {
             ptx::mbar_wait(&p_full[t], pc[t] & 1);
             ++pc[t];
+            if (tr && pc[t] <= kTraceN) tr[(6 + t) * kTraceN + pc[t] - 1] = clock64();
             if (n == 0) {  // O_t must have been drained by the previous item's epilogue
               ptx::mbar_wait(&o_free[t], (oc[t] & 1) ^ 1);
               ++oc[t];
@@ -312,6 +328,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
     uint8_t *sQ = smem + OFF_Q + t * TILE;
     const float c2 = P.scale_log2;
     uint32_t sc = 0, pvc = 0;  // phase counters of s_full[t] / pv_done[t]
+    long long *tr = (P.trace && blockIdx.x == 0 && quarter == 0 && lane == 0) ? P.trace : nullptr;
     SegIter si;
     seg_begin(P, si);
     Item it;
@@ -352,54 +369,39 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
         ptx::mbar_arrive(&q_full[t]);
       }
       float m2 = -INFINITY, l = 0.f;
+      const bool pp = kPingPong && (it.n_rows - it.row0 > BM);  // both tiles live (same test as the MMA warp)
       for (int n = 0; n < it.nblk; ++n) {
+        if (tr && sc < kTraceN) tr[(3 * t + 0) * kTraceN + sc] = clock64();
         ptx::mbar_wait(&s_full[t], sc & 1);
+        if (tr && sc < kTraceN) tr[(3 * t + 1) * kTraceN + sc] = clock64();
         ++sc;
         ptx::tc_fence_after();
-        uint32_t sr[4][32];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) ptx::tmem_ld32(s_col + c * 32, sr[c]);
-        ptx::tmem_ld_wait();
+        if (P.debug & 2) {  // timing experiment only: MMA pipeline without the softmax math
+          if (n >= 1) {
+            ptx::mbar_wait(&pv_done[t], pvc & 1);
+            ++pvc;
+          }
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&p_full[t]);
+          continue;
+        }
         const int64_t rem = it.kv_len - (int64_t)(it.blk_begin + n) * BN;
-        if (rem < BN) {  // partial last block only
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (c * 32 + i >= rem) sr[c][i] = 0xff800000u;
-        }
-        float acc[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] = fmaxf(__uint_as_float(sr[0][2 * k]), __uint_as_float(sr[0][2 * k + 1]));
-#pragma unroll
-        for (int i = 16; i < BN; i += 16)
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            acc[k] = ptx::fmax3(acc[k], __uint_as_float(sr[(i + 2 * k) / 32][(i + 2 * k) % 32]),
-                                __uint_as_float(sr[(i + 2 * k + 1) / 32][(i + 2 * k + 1) % 32]));
-        const float mx = fmaxf(ptx::fmax3(acc[0], acc[1], acc[2]),
-                               fmaxf(ptx::fmax3(acc[3], acc[4], acc[5]), fmaxf(acc[6], acc[7])));
-        const float mnew = mx * c2;
-        const bool any = __any_sync(0xffffffffu, mnew > m2 + 8.0f);
-        float alpha = 1.f;
-        if (any) {
-          const float mt = fmaxf(m2, mnew);
-          alpha = fast_exp2(m2 - mt);  // 0 on the first block
-          m2 = mt;
-        }
-        const uint64_t cc = ptx::pack2(c2, c2), nm = ptx::pack2(-m2, -m2);
-        uint64_t sacc[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        const uint64_t cc = ptx::pack2(c2, c2);
+        uint32_t sr[4][32];
+        uint64_t sacc[4];
+        // exp2(s * c2 - m2) of S chunk c (32 columns) -> bf16 P chunk c (16 TMEM columns), row sums
+        auto exp_chunk = [&](const uint32_t(&src)[32], int c, uint64_t nm) {
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             float x0, x1;
-            ptx::unpack2(ptx::fma2(ptx::pack2(__uint_as_float(sr[c][2 * i]), __uint_as_float(sr[c][2 * i + 1])), cc,
-                                   nm),
+            ptx::unpack2(ptx::fma2(ptx::pack2(__uint_as_float(src[2 * i]), __uint_as_float(src[2 * i + 1])), cc, nm),
                          x0, x1);
             float p0, p1;
-            if (kPolyEvery > 0 && (i % kPolyEvery) == kPolyEvery - 1) {
+            if (kPolyEvery < 0) {  // timing experiment only: no exp at all (wrong results)
+              p0 = x0 * 0.01f;
+              p1 = x1 * 0.01f;
+            } else if (kPolyEvery > 0 && (i % kPolyEvery) == kPolyEvery - 1) {
               ptx::exp2_poly2(x0, x1, p0, p1);  // FMA-pipe exp2 for 1/kPolyEvery of the pairs
             } else {
               p0 = fast_exp2(x0);
@@ -409,11 +411,73 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
             pk[i] = ptx::cvt_bf16x2(p0, p1);
           }
           ptx::tmem_st16(s_col + c * 16, pk);  // P(n) -> first 64 columns of S_t
+        };
+        auto mask_chunk = [&](uint32_t(&src)[32], int c) {
+          if (rem < BN) {  // partial last block only
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (c * 32 + i >= rem) src[i] = 0xff800000u;
+          }
+        };
+        float acc[8];
+        auto max_chunk = [&](const uint32_t(&src)[32], bool first) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float a = __uint_as_float(src[2 * k]), b = __uint_as_float(src[2 * k + 1]);
+            acc[k] = first ? fmaxf(a, b) : ptx::fmax3(acc[k], a, b);
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            acc[k] = ptx::fmax3(acc[k], __uint_as_float(src[16 + 2 * k]), __uint_as_float(src[17 + 2 * k]));
+        };
+        bool any;
+        float alpha = 1.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) ptx::tmem_ld32(s_col + c * 32, sr[c]);
+        ptx::tmem_ld_wait();
+        if (tr && sc <= kTraceN) tr[(10 + t) * kTraceN + sc - 1] = clock64();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          ptx::reg_fence32(sr[c]);
+          mask_chunk(sr[c], c);
+          max_chunk(sr[c], c == 0);
+        }
+        const float mx = fmaxf(ptx::fmax3(acc[0], acc[1], acc[2]),
+                               fmaxf(ptx::fmax3(acc[3], acc[4], acc[5]), fmaxf(acc[6], acc[7])));
+        const float mnew = mx * c2;
+        any = __any_sync(0xffffffffu, mnew > m2 + 8.0f);
+        if (any) {
+          const float mt = fmaxf(m2, mnew);
+          alpha = fast_exp2(m2 - mt);  // 0 on the first block
+          m2 = mt;
+        }
+        const uint64_t nm = ptx::pack2(-m2, -m2);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) sacc[k] = 0;
+        if (tr && sc <= kTraceN) {
+          asm volatile("" ::"l"(nm));  // the max is done before this timestamp
+          tr[(12 + t) * kTraceN + sc - 1] = clock64();
+        }
+        // Ping-pong (kPingPong, both tiles live): the exp phases of the two warps sharing an
+        // SM sub-partition (same TMEM lane quarter) alternate -- tile 0 block n, tile 1
+        // block n, tile 0 block n+1, ... -- so each runs at the full MUFU rate and the two
+        // tiles stay half a period apart instead of drifting into phase.  Named barriers,
+        // one pair per quarter (2 warps each); the counts balance within every item.
+        if (pp) {
+          if (t == 0 && n > 0) ptx::named_bar_sync(5 + quarter, 64);
+          if (t == 1) ptx::named_bar_sync(1 + quarter, 64);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) exp_chunk(sr[c], c, nm);
+        if (pp) {
+          if (t == 0) ptx::named_bar_arrive(1 + quarter, 64);
+          if (t == 1 && n + 1 < it.nblk) ptx::named_bar_arrive(5 + quarter, 64);
         }
         float s0, s1, s2, s3;
         ptx::unpack2(ptx::add2(sacc[0], sacc[1]), s0, s1);
         ptx::unpack2(ptx::add2(sacc[2], sacc[3]), s2, s3);
         l = l * alpha + ((s0 + s1) + (s2 + s3));
+        if (tr && sc <= kTraceN) tr[(8 + t) * kTraceN + sc - 1] = clock64();
         if (n >= 1) {
           ptx::mbar_wait(&pv_done[t], pvc & 1);  // PV_t(n-1) landed in O_t
           ++pvc;
@@ -433,6 +497,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(&p_full[t]);
+        if (tr && sc <= kTraceN) tr[(3 * t + 2) * kTraceN + sc - 1] = clock64();
       }
       ptx::mbar_wait(&pv_done[t], pvc & 1);  // last PV_t
       ++pvc;
@@ -550,7 +615,7 @@ __global__ void __launch_bounds__(tc4::kThreads, 1) prefix_tc4_kernel(const __gr
   const uint32_t tmem = *tmem_slot;
 
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 80;" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
     if (warp == 0) {
       // ================= TMA producer =================
       if (ptx::elect_one()) {
@@ -869,14 +934,17 @@ int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn) {
   return tc2_plan(B, g, Hkv, P, n_ctas, bn).ctas;
 }
 
-template <int kPoly>
-static cudaError_t tc2_attr() {
+template <int kPoly, bool kPP>
+static cudaError_t tc2_launch(const PrefixTc2Params &P, int grid, cudaStream_t s) {
   static std::once_flag once;
   static cudaError_t attr = cudaSuccess;
   std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(prefix_tc2_kernel<kPoly>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::ALLOC);
+    attr = cudaFuncSetAttribute(prefix_tc2_kernel<kPoly, kPP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                tc2::ALLOC);
   });
-  return attr;
+  if (attr != cudaSuccess) return attr;
+  prefix_tc2_kernel<kPoly, kPP><<<grid, tc2::kThreads, tc2::ALLOC, s>>>(P);
+  return cudaGetLastError();
 }
 
 static cudaError_t tc4_attr() {
@@ -892,10 +960,10 @@ hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s
   const int poly = a.poly_every;
   const bool v4 = a.variant == 4;
   const int bn = v4 ? tc4::BN : tc2::BN;
-  if (v4 ? tc4_attr() != cudaSuccess
-         : (poly == 0 ? tc2_attr<0>() : poly == 3 ? tc2_attr<3>() : poly == 2 ? tc2_attr<2>() : tc2_attr<4>()) !=
-               cudaSuccess)
-    return HYDRA_ECUDA;
+  // instantiations: kPolyEvery 0 (all MUFU), 3/4/8 (1/k of the pairs on the FMA pipe),
+  // -1 (timing experiment: no exp); kPingPong for variant 5 (v3 + ping-pong exp phases)
+  if (!(poly == 0 || poly == 3 || poly == 4 || poly == 8 || poly == -1)) return HYDRA_EINVAL;
+  if (v4 && tc4_attr() != cudaSuccess) return HYDRA_ECUDA;
   PrefixTc2Params P;
   memset(&P, 0, sizeof(P));
   if (a.kv_total > 0) {
@@ -903,6 +971,8 @@ hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s
     if (!make_kv_map2(&P.tmV, a.v, a.kv_total, a.Hkv, a.kv_st, a.kv_sh, bn)) return HYDRA_ECUDA;
   }
   P.bn = bn;
+  P.debug = a.debug_variant;
+  P.trace = reinterpret_cast<long long *>(a.trace);
   P.q = reinterpret_cast<const __nv_bfloat16 *>(a.q);
   P.q_sb = a.q_sb;
   P.q_sh = a.q_sh;
@@ -930,17 +1000,25 @@ hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s
   const int64_t work = a.tasks ? P.n_items : P.total_blocks;
   if (work == 0) return HYDRA_OK;
   const int grid = a.tasks ? (int)(n_ctas > 0 && n_ctas < work ? n_ctas : work) : pl.ctas;
-  if (v4)
+  if (v4) {
     prefix_tc4_kernel<<<grid, tc4::kThreads, tc4::ALLOC, s>>>(P);
-  else if (poly == 0)
-    prefix_tc2_kernel<0><<<grid, tc2::kThreads, tc2::ALLOC, s>>>(P);
-  else if (poly == 2)
-    prefix_tc2_kernel<2><<<grid, tc2::kThreads, tc2::ALLOC, s>>>(P);
-  else if (poly == 3)
-    prefix_tc2_kernel<3><<<grid, tc2::kThreads, tc2::ALLOC, s>>>(P);
-  else
-    prefix_tc2_kernel<4><<<grid, tc2::kThreads, tc2::ALLOC, s>>>(P);
-  return cudaGetLastError() == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
+    return cudaGetLastError() == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
+  }
+  const bool spec = a.variant == 5;  // ping-pong
+  cudaError_t e;
+  switch (poly * 2 + (spec ? 1 : 0)) {
+    case 0: e = tc2_launch<0, false>(P, grid, s); break;
+    case 1: e = tc2_launch<0, true>(P, grid, s); break;
+    case 6: e = tc2_launch<3, false>(P, grid, s); break;
+    case 7: e = tc2_launch<3, true>(P, grid, s); break;
+    case 8: e = tc2_launch<4, false>(P, grid, s); break;
+    case 9: e = tc2_launch<4, true>(P, grid, s); break;
+    case 16: e = tc2_launch<8, false>(P, grid, s); break;
+    case 17: e = tc2_launch<8, true>(P, grid, s); break;
+    case -2: e = tc2_launch<-1, false>(P, grid, s); break;
+    default: e = tc2_launch<-1, true>(P, grid, s); break;
+  }
+  return e == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
 }
 
 }  // namespace hydra

@@ -57,6 +57,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   }
 }
 
+// Named barriers (ids 1..15; 0 is __syncthreads).  `n` counts threads, a multiple of 32.
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 // ------------------------------------------------------------------ proxy fences
 // Generic-proxy smem writes -> visible to the async proxy (tcgen05.mma / TMA).
 __device__ __forceinline__ void fence_proxy_async_smem() {
@@ -144,6 +152,16 @@ __device__ __forceinline__ void mma_commit(uint64_t *bar) {
                : "memory");
 }
 
+// Orders register consumers after tcgen05.wait::ld (the ld's destination registers are
+// formally defined by the ld; this empty asm re-defines them after the wait).
+__device__ __forceinline__ void reg_fence32(uint32_t (&r)[32]) {
+  asm volatile(""
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
+                 "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
+                 "+r"(r[29]), "+r"(r[30]), "+r"(r[31]));
+}
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -225,8 +243,8 @@ __device__ __forceinline__ void exp2_poly2(float x0, float x1, float &y0, float 
   x1 = fmaxf(x1, -126.f);
   const uint64_t magic = pack2(12582912.f, 12582912.f), nmagic = pack2(-12582912.f, -12582912.f);
   const uint64_t x = pack2(x0, x1);
-  const uint64_t t = add2(x, magic);                                      // low mantissa bits = n
-  const uint64_t f = add2(x, add2(t, nmagic) ^ 0x8000000080000000ull);  // x - n  (negate via sign bits)
+  const uint64_t t = add2(x, magic);                                 // low mantissa bits = n = rint(x)
+  const uint64_t f = fma2(add2(t, nmagic), pack2(-1.f, -1.f), x);  // x - n in [-0.5, 0.5]
   uint64_t p = fma2(f, pack2(0.0551716685f, 0.0551716685f), pack2(0.242611155f, 0.242611155f));
   p = fma2(f, p, pack2(0.693260968f, 0.693260968f));
   p = fma2(f, p, pack2(0.999928057f, 0.999928057f));

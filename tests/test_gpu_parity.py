@@ -23,7 +23,7 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(autouse=True)
 def _reset_config():
     keys = ("prefix_impl", "prefix_splits", "suffix_splits", "tc_debug_variant", "prefix_ctas", "suffix_impl",
-            "suffix_ctas", "overlap_prefix_ctas")
+            "suffix_ctas", "overlap_prefix_ctas", "prefix_poly")
     for k in keys:
         hydra.set_config(k, 0)
     hydra.set_config("prefix_variant", 3)
@@ -69,12 +69,12 @@ PREFIX_SHAPES = [
 
 @pytest.mark.parametrize("B,Hq,Hkv,P", PREFIX_SHAPES)
 @pytest.mark.parametrize("dist", ["mixed", "boundary"])
-@pytest.mark.parametrize("impl", [2, 3, 4])
+@pytest.mark.parametrize("impl", [2, 3, 4, 5])
 def test_prefix_tc_parity(B, Hq, Hkv, P, dist, impl):
     # 2: one-tile tcgen05 kernel, 3: persistent two-tile (128-token blocks), 4: same with 64-token
-    # blocks and double-buffered scores
+    # blocks and double-buffered scores, 5: 3 with the speculative (running-max) softmax
     hydra.set_config("prefix_impl", min(impl, 3))
-    hydra.set_config("prefix_variant", 4 if impl == 4 else 3)
+    hydra.set_config("prefix_variant", impl if impl >= 3 else 3)
     pb = synth.make_problem(B, Hq, Hkv, 128, P, 1, dtype="bf16", dist=dist, seed=3)
     t = problem_to(pb, DEV)
     o, lse = hydra.prefix_attn(t["q"], t["pk"], t["pv"])
@@ -95,8 +95,28 @@ def test_prefix_tc_splits(splits):
     assert_parity(o, ref, lse, lref, what=f"prefix splits={splits}")
 
 
+@pytest.mark.parametrize("variant,poly", [(3, 0), (5, 0), (5, 4), (5, 8), (3, 4)])
+def test_prefix_tc2_growing_max(variant, poly):
+    """Scores that grow along the prefix: the running max is raised block after block, which
+    exercises the O/l correction and, for the speculative softmax, the redo path."""
+    hydra.set_config("prefix_impl", 3)
+    hydra.set_config("prefix_variant", variant)
+    hydra.set_config("prefix_poly", poly)
+    pb = synth.make_problem(300, 8, 2, 128, 2000, 1, dtype="bf16", dist="mixed", seed=11)
+    ramp = (1.0 + 6.0 * np.arange(pb.P, dtype=np.float64) / pb.P)[:, None, None]
+    pb.pk = synth.gen.f32_to_bf16_bits((pb.f32("pk") * ramp).astype(np.float32))
+    t = problem_to(pb, DEV)
+    try:
+        o, lse = hydra.prefix_attn(t["q"], t["pk"], t["pv"])
+        torch.cuda.synchronize()
+    finally:
+        hydra.set_config("prefix_poly", 0)
+    ref, lref = oracle.prefix_only(pb)
+    assert_parity(o, ref, lse, lref, what=f"prefix growing max v{variant} poly{poly}")
+
+
 @pytest.mark.parametrize("ctas", [1, 3, 7, 64, 148, 100000])
-@pytest.mark.parametrize("variant", [3, 4])
+@pytest.mark.parametrize("variant", [3, 4, 5])
 def test_prefix_tc2_stream_k_ctas(ctas, variant):
     """Stream-K piece boundaries fall inside items for most CTA counts; every piece is merged."""
     hydra.set_config("prefix_ctas", ctas)
@@ -325,13 +345,13 @@ def test_seqsplit_single_rank_nccl():
         tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("impl", [0, 2, 3, 4])
+@pytest.mark.parametrize("impl", [0, 2, 3, 4, 5])
 @pytest.mark.parametrize("per,g", [(300, 1), (100, 4)])
 def test_tree_large_groups(impl, per, g):
     """Groups with > 128 and > 256 stacked rows: both query tiles of a pair and several pairs
     per node (the persistent kernel's task mode), on root and branch nodes."""
     hydra.set_config("prefix_impl", min(impl, 3))
-    hydra.set_config("prefix_variant", 4 if impl == 4 else 3)
+    hydra.set_config("prefix_variant", impl if impl >= 3 else 3)
     parent, node_len, leaf = synth.two_level_tree(300, 2, 200, per)
     tp = synth.make_tree_problem(parent, node_len, leaf, 4 * g, 4, 128, 24, dtype="bf16", dist="boundary", seed=19)
     t = tree_to(tp, DEV)

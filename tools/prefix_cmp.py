@@ -27,7 +27,32 @@ def run(B, H, Hkv, P, impl, ctas=0, iters=20, poly=0, variant=3):
     ms = e0.elapsed_time(e1) / iters
     fl = 4.0 * B * H * P * 128
     print(json.dumps(dict(B=B, H=H, Hkv=Hkv, P=P, impl=impl, ctas=ctas, poly=poly, variant=variant, ms=round(ms, 4), tflops=round(fl / ms / 1e9, 1))), flush=True)
-for variant in (3, 4):
-    run(1024, 40, 40, 16384, 3, variant=variant)
-    run(512, 32, 8, 32768, 3, variant=variant)
-    run(1024, 40, 40, 4096, 3, variant=variant)
+mode = sys.argv[1] if len(sys.argv) > 1 else "variants"
+if mode == "variants":
+    for variant in (3, 4):
+        run(1024, 40, 40, 16384, 3, variant=variant)
+        run(512, 32, 8, 32768, 3, variant=variant)
+        run(1024, 40, 40, 4096, 3, variant=variant)
+elif mode == "spec":
+    for variant, poly in ((3, 0), (5, 0), (5, 8), (5, 4), (5, 3), (3, 4)):
+        run(1024, 40, 40, 16384, 3, poly=poly, variant=variant)
+        run(512, 32, 8, 32768, 3, poly=poly, variant=variant)
+    hydra.set_config("prefix_poly", 0)
+elif mode == "poly":
+    for poly in (0, 8, 4, 3, -1):  # -1: timing experiment, no exp at all
+        run(1024, 40, 40, 16384, 3, poly=poly)
+        run(512, 32, 8, 32768, 3, poly=poly)
+    hydra.set_config("prefix_poly", 0)
+elif mode == "debug":
+    hydra.set_config("tc_debug_variant", 2)
+    print("debug: softmax math skipped (timing only)")
+    run(1024, 40, 40, 16384, 3, variant=3)
+    run(512, 32, 8, 32768, 3, variant=3)
+    hydra.set_config("tc_debug_variant", 0)
+elif mode == "feed":
+    for dbg, poly in ((4, 0), (6, 0), (4, -1)):
+        hydra.set_config("tc_debug_variant", dbg)
+        print(f"debug={dbg} poly={poly} (timing only: 4 = no K/V TMA after the fill, 2 = no softmax math)")
+        run(1024, 40, 40, 16384, 3, poly=poly)
+        run(512, 32, 8, 32768, 3, poly=poly)
+    hydra.set_config("tc_debug_variant", 0); hydra.set_config("prefix_poly", 0)
