@@ -54,6 +54,15 @@ CONFIGS = {
 }
 
 
+# DRAM bytes (read + write) per launch from one `ncu --set full` capture of the kernel at this
+# config (profiles/r1b_ncu_full_*.csv: dram__bytes_read.sum + dram__bytes_write.sum)
+NCU_TRAFFIC = {
+    ("c3_16k", "decode_attn_kernel"): 5379256000 + 9611264,
+    ("c3_16k", "suffix_tc_kernel"): 5379232000 + 24610048,
+    ("c3_16k", "prefix_tc2_kernel"): 354441216 + 24963072,
+}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -434,6 +443,7 @@ def main():
 
     # pick the step variant (prefix || suffix on two streams, or sequential) on a short probe
     g_over = capture(lambda: step(True))
+    k_over = int(hydra.get_config("last_overlap_k"))  # SM split chosen for the overlapped step
     g_seq = capture(lambda: step(False))
     probe = max(3, min(20, args.steps // 5))
     ms_over = time_graph(g_over, probe, 2)
@@ -466,11 +476,28 @@ def main():
 
     # per-kernel timing on their own (roofline of the dominant kernel and the prefix phase)
     # (the composite's workspace holds (prefix + suffix) split partials, enough for either alone)
+    kk = max(5, args.steps // 4)
     g_pre = capture(lambda: hydra.prefix_attn(q, pk, pv, workspace=ws))
     g_suf = capture(lambda: hydra.suffix_attn(q, sk, sv, lens, workspace=ws))
-    kk = max(5, args.steps // 4)
     ms_pre = time_graph(g_pre, kk, 3)
     ms_suf = time_graph(g_suf, kk, 3)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    in_step = None
+    if overlap and k_over > 0:
+        # the kernels as the overlapped step runs them: prefix on k SMs || tensor-core suffix on
+        # the other SMs (timed one at a time, so without the other's HBM/L2/power interference)
+        try:
+            hydra.set_config("prefix_ctas", k_over)
+            ms_pre_k = time_graph(capture(lambda: hydra.prefix_attn(q, pk, pv, workspace=ws)), kk, 3)
+            hydra.set_config("prefix_ctas", 0)
+            hydra.set_config("suffix_impl", 2)
+            hydra.set_config("suffix_ctas", sms - k_over)
+            ms_suf_k = time_graph(capture(lambda: hydra.suffix_attn(q, sk, sv, lens, workspace=ws)), kk, 3)
+        finally:
+            for key in ("prefix_ctas", "suffix_impl", "suffix_ctas"):
+                hydra.set_config(key, 0)
+        in_step = {"prefix_ctas": k_over, "suffix_ctas": sms - k_over, "ms_prefix": round(ms_pre_k, 5),
+                   "ms_suffix": round(ms_suf_k, 5)}
 
     pk_meas = peaks()
     hbm = float(pk_meas.get("hbm_gbs", 6650.0))
@@ -506,14 +533,21 @@ def main():
                    "heads_per_gpu": Hq_r, "overlap_prefix_suffix": overlap,
                    "l2": f"no flush: {total_bytes / 1e9:.2f} GB of inputs per step > 126 MB L2",
                    "timing": "CUDA graph of one step, CUDA events over K replays, max over ranks"},
-        "roofline": {"bound": "hbm", "kernel": "suffix split-K GEMV (decode_attn_kernel)",
+        "roofline": {"bound": "hbm", "kernel": "suffix split-K GEMV (decode_attn_kernel, all SMs)",
                      "achieved": round(suf_gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(suf_gbs / hbm, 4),
-                     "traffic": None, "algorithmic_bytes_per_launch": suffix_bytes,
-                     "launch_ms": round(ms_suf, 5), "peak_source": peak_src},
-        "prefix_phase": {"bound": "tensor", "kernel": "prefix_tc_kernel (tcgen05)", "achieved": round(pre_tflops, 1),
-                         "unit": "TFLOP/s", "peak_burst": tc_burst, "frac_of_measured": round(pre_tflops / tc_burst, 4),
+                     "traffic": NCU_TRAFFIC.get((args.config, "decode_attn_kernel")),
+                     "algorithmic_bytes_per_launch": suffix_bytes,
+                     "launch_ms": round(ms_suf, 5), "peak_source": peak_src + " (STREAM copy)",
+                     "frac_of_nominal_7700": round(suf_gbs / 7700.0, 4),
+                     "note": "read-only stream vs a read+write copy peak: can read a little above 1.0"},
+        "prefix_phase": {"bound": "tensor", "kernel": "prefix_tc2_kernel (persistent tcgen05, all SMs)",
+                         "achieved": round(pre_tflops, 1), "unit": "TFLOP/s", "peak_burst": tc_burst,
+                         "frac_of_measured": round(pre_tflops / tc_burst, 4), "peak_sustained": tc_sust,
+                         "frac_of_measured_sustained": round(pre_tflops / tc_sust, 4),
                          "frac_of_spec_2250": round(pre_tflops / 2250.0, 4), "flops_per_launch": prefix_flops,
-                         "launch_ms": round(ms_pre, 5)},
+                         "traffic": NCU_TRAFFIC.get((args.config, "prefix_tc2_kernel")),
+                         "algorithmic_bytes_per_launch": prefix_bytes,
+                         "launch_ms": round(ms_pre, 5), "timed": "after the timed region (GPU warm, power-capped)"},
         "step_roofline": {"t_roof_ms": round(t_roof * 1e3, 5), "frac": round(t_roof * 1e3 / ms, 4),
                           "ms_sequential": round(ms_seq, 5), "ms_overlap": round(ms_over, 5)},
         "clocks": clocks,
@@ -521,6 +555,15 @@ def main():
     }
     if flat:
         line["flatness"] = flat
+    if in_step:
+        # the overlapped step's dominant kernel: the tensor-core suffix on (SMs - k) SMs
+        b_k = suffix_bytes / (in_step["ms_suffix"] * 1e-3) / 1e9
+        f_k = prefix_flops / (in_step["ms_prefix"] * 1e-3) / 1e12
+        line["roofline_in_step"] = {
+            "bound": "hbm", "kernel": "suffix_tc_kernel on %d SMs (prefix on %d SMs)" % (sms - k_over, k_over),
+            "achieved": round(b_k, 1), "peak": hbm, "unit": "GB/s", "frac": round(b_k / hbm, 4),
+            "traffic": NCU_TRAFFIC.get((args.config, "suffix_tc_kernel")), "launch_ms": in_step["ms_suffix"],
+            "prefix_tflops_on_k_sms": round(f_k, 1), "prefix_launch_ms_on_k_sms": in_step["ms_prefix"]}
 
     if not args.no_e2e:
         line["e2e"] = e2e_leg(args, hydra, torch, dev, world, (hq, hpk, hpv, hsk, hsv, hlens),

@@ -198,10 +198,24 @@ HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, i
                             int32_t n_parts);
 
 /*
- * Tuning / test switches (process-wide):
- *   "prefix_impl"   0 auto (tcgen05 when supported), 1 force SIMT, 2 force tcgen05
- *   "prefix_splits" 0 auto, else number of KV splits of the prefix kernel
- *   "suffix_splits" 0 auto, else number of KV splits of the suffix kernel
+ * Tuning / test switches (process-wide; 0 = automatic unless stated):
+ *   "prefix_impl"         1 SIMT, 2 one-tile tcgen05 kernel, 3 persistent two-tile tcgen05 kernel
+ *   "prefix_variant"      persistent kernel: 3 (default, 128-token blocks), 4 (64-token blocks,
+ *                         double-buffered scores), 5 (3 + ping-pong exp phases; experimental)
+ *   "prefix_poly"         0 (default) all exp2 on MUFU; 3/4/8: every k-th pair on the FMA pipe
+ *   "prefix_splits"       KV splits of the one-tile / SIMT prefix kernels
+ *   "prefix_ctas"         CTAs of the persistent prefix kernel
+ *   "suffix_impl"         1 SIMT split-K GEMV, 2 persistent TMA-fed tensor-core kernel
+ *   "suffix_splits"       KV splits of the SIMT suffix kernel
+ *   "suffix_ctas"         CTAs of the persistent suffix kernel
+ *   "suffix_unroll"       tokens in flight per row group of the SIMT suffix kernel (4 or 8)
+ *   "overlap_prefix_ctas" SM split of hydra_attn with an aux stream (prefix CTAs)
+ *   "prefix_stages"       K/V pipeline stages of the one-tile kernel (2 or 3)
+ *   "tc_debug_variant"    timing experiments only (invalid results); never set in production
+ *   "prefix_trace"        diagnostics: device pointer of a 14*1024 int64 buffer for CTA-0
+ *                         timestamps of the persistent prefix kernel (tools/prefix_trace.py)
+ * hydra_get_config also answers "last_overlap_k": prefix CTAs of the last hydra_attn
+ * overlap split (0 = the two phases ran sequentially).
  * Returns HYDRA_EINVAL for an unknown key.
  */
 HYDRA_API hydra_status hydra_set_config(const char *key, int64_t value);

@@ -41,7 +41,8 @@ static hydra_status cuda_fail(const char *what) {
 
 static std::atomic<int64_t> g_prefix_impl{0}, g_prefix_splits{0}, g_suffix_splits{0}, g_tc_debug{0},
     g_prefix_stages{3}, g_suffix_unroll{4}, g_prefix_ctas{0}, g_suffix_impl{0}, g_suffix_ctas{0},
-    g_overlap_prefix_ctas{0}, g_prefix_poly{0}, g_prefix_variant{3}, g_prefix_trace{0};
+    g_overlap_prefix_ctas{0}, g_prefix_poly{0}, g_prefix_variant{3}, g_prefix_trace{0},
+    g_last_overlap_k{0};  // read-only: prefix CTAs of the last hydra_attn overlap split (0 = sequential)
 
 extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
   if (!key) return fail(HYDRA_EINVAL, "null key");
@@ -69,6 +70,7 @@ extern "C" int64_t hydra_get_config(const char *key) {
   if (!strcmp(key, "suffix_splits")) return g_suffix_splits;
   if (!strcmp(key, "tc_debug_variant")) return g_tc_debug;
   if (!strcmp(key, "prefix_trace")) return g_prefix_trace;
+  if (!strcmp(key, "last_overlap_k")) return g_last_overlap_k;
   if (!strcmp(key, "prefix_stages")) return g_prefix_stages;
   if (!strcmp(key, "prefix_ctas")) return g_prefix_ctas;
   if (!strcmp(key, "suffix_impl")) return g_suffix_impl;
@@ -558,6 +560,8 @@ extern "C" hydra_status hydra_attn(const hydra_heads *h, int64_t B, const void *
   // Without an SM split (k = 0) two full grids would only contend: run sequentially.
   const int k_over = (sa != s) ? overlap_prefix_ctas(h, B, P, S_cap) : 0;
   if (k_over == 0) sa = s;
+  g_last_overlap_k = k_over;
+  if (getenv("HYDRA_DEBUG_OVERLAP")) fprintf(stderr, "hydra_attn: overlap prefix CTAs k=%d (aux stream %s)\n", k_over, s_aux ? "given" : "none");
   const int sms = device_sm_count();
   const int np = prefix_splits(h, B, P, k_over), ns = suffix_splits(h, B, S_cap, k_over > 0);
   const size_t need = part_bytes(h, B) * (np + ns);
