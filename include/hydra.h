@@ -201,7 +201,7 @@ HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, i
  * Tuning / test switches (process-wide; 0 = automatic unless stated):
  *   "prefix_impl"         1 SIMT, 2 one-tile tcgen05 kernel, 3 persistent two-tile tcgen05 kernel
  *   "prefix_variant"      persistent kernel: 3 (default, 128-token blocks), 4 (64-token blocks,
- *                         double-buffered scores), 5 (3 + ping-pong exp phases; experimental)
+ *                         double-buffered scores), 5 (3 + speculative running-max softmax)
  *   "prefix_poly"         0 (default) all exp2 on MUFU; 3/4/8: every k-th pair on the FMA pipe
  *   "prefix_splits"       KV splits of the one-tile / SIMT prefix kernels
  *   "prefix_ctas"         CTAs of the persistent prefix kernel

@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) prefix_tc_kernel(const __grid
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&s_full[i], 1);
-      ptx::mbar_init(&p_full[i], 128);
+      ptx::mbar_init(&p_full[i], 4);  // one elected arrival per softmax warp
     }
     ptx::mbar_init(pv_done, 1);
     ptx::fence_mbar_init();
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) prefix_tc_kernel(const __grid
       }
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&p_full[n & 1]);
+      ptx::warp_arrive(&p_full[n & 1]);
     }
     // ---- epilogue: O / l and LSE = (m2 + log2 l) ln 2
     ptx::mbar_wait(pv_done, (nblk - 1) & 1);

@@ -170,8 +170,8 @@ __device__ __forceinline__ bool seg_next(const PrefixTc2Params &P, SegIter &s, I
 }
 
 // kPolyEvery -- 0: all exp2 on MUFU; k: every k-th column pair on the FMA pipe.
-// kPingPong -- alternate the two tiles' exp phases per SM sub-partition (see the loop).
-template <int kPolyEvery, bool kPingPong>
+// kSpec -- speculative softmax with the running max (variant 5, see the loop).
+template <int kPolyEvery, bool kSpec>
 __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __grid_constant__ PrefixTc2Params P) {
   using namespace tc2;
   extern __shared__ uint8_t smem_raw[];
@@ -193,11 +193,11 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
       ptx::mbar_init(&v_empty[i], 1);
     }
     for (int t = 0; t < 2; ++t) {
-      ptx::mbar_init(&q_full[t], 128);
+      ptx::mbar_init(&q_full[t], 4);  // one elected arrival per softmax warp
       ptx::mbar_init(&s_full[t], 1);
-      ptx::mbar_init(&p_full[t], 128);
+      ptx::mbar_init(&p_full[t], 4);  // one elected arrival per softmax warp
       ptx::mbar_init(&pv_done[t], 1);
-      ptx::mbar_init(&o_free[t], 128);
+      ptx::mbar_init(&o_free[t], 4);  // one elected arrival per softmax warp
     }
     ptx::fence_mbar_init();
   }
@@ -366,10 +366,9 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
         for (int c = 0; c < 16; ++c)
           *reinterpret_cast<uint4 *>(sQ + (c / 8) * PANEL + r * 128 + (((c % 8) ^ (r % 8)) * 16)) = ch[c];
         ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&q_full[t]);
+        ptx::warp_arrive(&q_full[t]);
       }
       float m2 = -INFINITY, l = 0.f;
-      const bool pp = kPingPong && (it.n_rows - it.row0 > BM);  // both tiles live (same test as the MMA warp)
       for (int n = 0; n < it.nblk; ++n) {
         if (tr && sc < kTraceN) tr[(3 * t + 0) * kTraceN + sc] = clock64();
         ptx::mbar_wait(&s_full[t], sc & 1);
@@ -382,7 +381,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
             ++pvc;
           }
           ptx::tc_fence_before();
-          ptx::mbar_arrive(&p_full[t]);
+          ptx::warp_arrive(&p_full[t]);
           continue;
         }
         const int64_t rem = it.kv_len - (int64_t)(it.blk_begin + n) * BN;
@@ -437,41 +436,58 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
         ptx::tmem_ld_wait();
         if (tr && sc <= kTraceN) tr[(10 + t) * kTraceN + sc - 1] = clock64();
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          ptx::reg_fence32(sr[c]);
-          mask_chunk(sr[c], c);
-          max_chunk(sr[c], c == 0);
-        }
-        const float mx = fmaxf(ptx::fmax3(acc[0], acc[1], acc[2]),
-                               fmaxf(ptx::fmax3(acc[3], acc[4], acc[5]), fmaxf(acc[6], acc[7])));
-        const float mnew = mx * c2;
-        any = __any_sync(0xffffffffu, mnew > m2 + 8.0f);
-        if (any) {
-          const float mt = fmaxf(m2, mnew);
-          alpha = fast_exp2(m2 - mt);  // 0 on the first block
-          m2 = mt;
-        }
-        const uint64_t nm = ptx::pack2(-m2, -m2);
+        for (int c = 0; c < 4; ++c) ptx::reg_fence32(sr[c]);
 #pragma unroll
         for (int k = 0; k < 4; ++k) sacc[k] = 0;
-        if (tr && sc <= kTraceN) {
-          asm volatile("" ::"l"(nm));  // the max is done before this timestamp
-          tr[(12 + t) * kTraceN + sc - 1] = clock64();
-        }
-        // Ping-pong (kPingPong, both tiles live): the exp phases of the two warps sharing an
-        // SM sub-partition (same TMEM lane quarter) alternate -- tile 0 block n, tile 1
-        // block n, tile 0 block n+1, ... -- so each runs at the full MUFU rate and the two
-        // tiles stay half a period apart instead of drifting into phase.  Named barriers,
-        // one pair per quarter (2 warps each); the counts balance within every item.
-        if (pp) {
-          if (t == 0 && n > 0) ptx::named_bar_sync(5 + quarter, 64);
-          if (t == 1) ptx::named_bar_sync(1 + quarter, 64);
-        }
+        if (kSpec && n > 0) {
+          // Speculative (variant 5): P = exp2(s*c2 - m2) with the running max of the previous
+          // blocks, chunk by chunk as each TMEM load lands (the four loads are in flight
+          // together), the block max reduced alongside -- the row max leaves the critical
+          // path.  If some row's max grew by > 8 (p could exceed 2^8) the block is redone
+          // with the raised max: the same rule as the exact path.
+          const uint64_t nm = ptx::pack2(-m2, -m2);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) exp_chunk(sr[c], c, nm);
-        if (pp) {
-          if (t == 0) ptx::named_bar_arrive(1 + quarter, 64);
-          if (t == 1 && n + 1 < it.nblk) ptx::named_bar_arrive(5 + quarter, 64);
+          for (int c = 0; c < 4; ++c) {
+            mask_chunk(sr[c], c);
+            max_chunk(sr[c], c == 0);
+            exp_chunk(sr[c], c, nm);
+          }
+          const float mx = fmaxf(ptx::fmax3(acc[0], acc[1], acc[2]),
+                                 fmaxf(ptx::fmax3(acc[3], acc[4], acc[5]), fmaxf(acc[6], acc[7])));
+          const float mnew = mx * c2;
+          any = __any_sync(0xffffffffu, mnew > m2 + 8.0f);
+          if (any) {  // rare
+            const float mt = fmaxf(m2, mnew);
+            alpha = fast_exp2(m2 - mt);
+            m2 = mt;
+            const uint64_t nm2 = ptx::pack2(-m2, -m2);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) sacc[k] = 0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) exp_chunk(sr[c], c, nm2);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            mask_chunk(sr[c], c);
+            max_chunk(sr[c], c == 0);
+          }
+          const float mx = fmaxf(ptx::fmax3(acc[0], acc[1], acc[2]),
+                                 fmaxf(ptx::fmax3(acc[3], acc[4], acc[5]), fmaxf(acc[6], acc[7])));
+          const float mnew = mx * c2;
+          any = __any_sync(0xffffffffu, mnew > m2 + 8.0f);
+          if (any) {
+            const float mt = fmaxf(m2, mnew);
+            alpha = fast_exp2(m2 - mt);  // 0 on the first block
+            m2 = mt;
+          }
+          const uint64_t nm = ptx::pack2(-m2, -m2);
+          if (tr && sc <= kTraceN) {
+            asm volatile("" ::"l"(nm));  // the max is done before this timestamp
+            tr[(12 + t) * kTraceN + sc - 1] = clock64();
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c) exp_chunk(sr[c], c, nm);
         }
         float s0, s1, s2, s3;
         ptx::unpack2(ptx::add2(sacc[0], sacc[1]), s0, s1);
@@ -496,7 +512,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
         }
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(&p_full[t]);
+        ptx::warp_arrive(&p_full[t]);
         if (tr && sc <= kTraceN) tr[(3 * t + 2) * kTraceN + sc - 1] = clock64();
       }
       ptx::mbar_wait(&pv_done[t], pvc & 1);  // last PV_t
@@ -523,7 +539,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
         __syncwarp();
       }
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&o_free[t]);
+      ptx::warp_arrive(&o_free[t]);
       if (live) P.lse[it.slot * P.lse_slot_stride + seq * P.Hq + h] = (m2 + log2f(l)) * HYDRA_LN2;
       // the staging writes to sQ were generic-proxy; order them before the next item's Q writes+TMA reads
       ptx::fence_proxy_async_smem();
@@ -597,13 +613,13 @@ __global__ void __launch_bounds__(tc4::kThreads, 1) prefix_tc4_kernel(const __gr
       ptx::mbar_init(&v_empty[i], 1);
     }
     for (int t = 0; t < 2; ++t) {
-      ptx::mbar_init(&q_full[t], 128);
+      ptx::mbar_init(&q_full[t], 4);  // one elected arrival per softmax warp
       ptx::mbar_init(&pv_done[t], 1);
-      ptx::mbar_init(&o_free[t], 128);
+      ptx::mbar_init(&o_free[t], 4);  // one elected arrival per softmax warp
       ptx::mbar_init(&o_ready[t], 1);
       for (int b = 0; b < 2; ++b) {
         ptx::mbar_init(&s_full[2 * t + b], 1);
-        ptx::mbar_init(&p_full[2 * t + b], 128);
+        ptx::mbar_init(&p_full[2 * t + b], 4);  // one elected arrival per softmax warp
       }
     }
     ptx::fence_mbar_init();
@@ -647,6 +663,8 @@ __global__ void __launch_bounds__(tc4::kThreads, 1) prefix_tc4_kernel(const __gr
         constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BM, BN, false);
         constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(BM, HD, true);
         uint32_t gb = 0, qc[2] = {0, 0}, pc[4] = {0, 0, 0, 0}, oc[2] = {0, 0};
+        long long *tr = (P.trace && blockIdx.x == 0) ? P.trace : nullptr;
+        uint32_t trn[2] = {0, 0};
         SegIter si;
         seg_begin(P, si);
         Item it;
@@ -689,6 +707,7 @@ __global__ void __launch_bounds__(tc4::kThreads, 1) prefix_tc4_kernel(const __gr
               const int pb = 2 * t + (n & 1);
               ptx::mbar_wait(&p_full[pb], pc[pb] & 1);
               ++pc[pb];
+              if (tr && trn[t] < tc2::kTraceN) tr[(6 + t) * tc2::kTraceN + trn[t]++] = clock64();
               if (n == 0) {
                 ptx::mbar_wait(&o_free[t], (oc[t] & 1) ^ 1);
                 ++oc[t];
@@ -723,6 +742,8 @@ __global__ void __launch_bounds__(tc4::kThreads, 1) prefix_tc4_kernel(const __gr
     uint8_t *sQ = smem + OFF_Q + t * QTILE;
     const float c2 = P.scale_log2;
     uint32_t sc[2] = {0, 0}, pvn = 0, orc = 0;  // s_full phase per buffer; PV_t count; items done
+    long long *tr = (P.trace && blockIdx.x == 0 && quarter == 0 && lane == 0) ? P.trace : nullptr;
+    constexpr int kTN = tc2::kTraceN;
     SegIter si;
     seg_begin(P, si);
     Item it;
@@ -759,19 +780,23 @@ __global__ void __launch_bounds__(tc4::kThreads, 1) prefix_tc4_kernel(const __gr
         for (int c = 0; c < 16; ++c)
           *reinterpret_cast<uint4 *>(sQ + (c / 8) * QPANEL + r * 128 + (((c % 8) ^ (r % 8)) * 16)) = ch[c];
         ptx::fence_proxy_async_smem();
-        ptx::mbar_arrive(&q_full[t]);
+        ptx::warp_arrive(&q_full[t]);
       }
       float m2 = -INFINITY, l = 0.f;
       for (int n = 0; n < it.nblk; ++n) {
         const int b = n & 1;
         const uint32_t s_col = tmem + lane_base + t * 256 + b * BN;
+        const uint32_t trk = pvn;  // block counter of this tile
+        if (tr && trk < kTN) tr[(3 * t + 0) * kTN + trk] = clock64();
         ptx::mbar_wait(&s_full[2 * t + b], sc[b] & 1);
+        if (tr && trk < kTN) tr[(3 * t + 1) * kTN + trk] = clock64();
         ++sc[b];
         ptx::tc_fence_after();
         uint32_t sr[2][32];
         ptx::tmem_ld32(s_col, sr[0]);
         ptx::tmem_ld32(s_col + 32, sr[1]);
         ptx::tmem_ld_wait();
+        if (tr && trk < kTN) tr[(10 + t) * kTN + trk] = clock64();
         const int64_t rem = it.kv_len - (int64_t)(it.blk_begin + n) * BN;
         if (rem < BN) {
 #pragma unroll
@@ -801,6 +826,10 @@ __global__ void __launch_bounds__(tc4::kThreads, 1) prefix_tc4_kernel(const __gr
         }
         const uint64_t cc = ptx::pack2(c2, c2), nm = ptx::pack2(-m2, -m2);
         uint64_t sacc[4] = {0, 0, 0, 0};
+        if (tr && trk < kTN) {
+          asm volatile("" ::"l"(nm));
+          tr[(12 + t) * kTN + trk] = clock64();
+        }
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           uint32_t pk[16];
@@ -820,6 +849,7 @@ __global__ void __launch_bounds__(tc4::kThreads, 1) prefix_tc4_kernel(const __gr
         ptx::unpack2(ptx::add2(sacc[0], sacc[1]), s0, s1);
         ptx::unpack2(ptx::add2(sacc[2], sacc[3]), s2, s3);
         l = l * alpha + ((s0 + s1) + (s2 + s3));
+        if (tr && trk < kTN) tr[(8 + t) * kTN + trk] = clock64();
         if (any && n >= 1) {  // rare O correction: needs PV_t(n-1) (completion index pvn-1) landed
           ptx::mbar_wait(&pv_done[t], (pvn - 1) & 1);
           ptx::tc_fence_after();
@@ -835,7 +865,8 @@ __global__ void __launch_bounds__(tc4::kThreads, 1) prefix_tc4_kernel(const __gr
         }
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(&p_full[2 * t + b]);
+        ptx::warp_arrive(&p_full[2 * t + b]);
+        if (tr && trk < kTN) tr[(3 * t + 2) * kTN + trk] = clock64();
         ++pvn;
       }
       // All PVs of this item landed.  (pv_done cannot be used here: up to two PVs may be in
@@ -863,7 +894,7 @@ __global__ void __launch_bounds__(tc4::kThreads, 1) prefix_tc4_kernel(const __gr
         __syncwarp();
       }
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&o_free[t]);
+      ptx::warp_arrive(&o_free[t]);
       if (live) P.lse[it.slot * P.lse_slot_stride + seq * P.Hq + h] = (m2 + log2f(l)) * HYDRA_LN2;
       ptx::fence_proxy_async_smem();
     }
@@ -961,7 +992,7 @@ hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s
   const bool v4 = a.variant == 4;
   const int bn = v4 ? tc4::BN : tc2::BN;
   // instantiations: kPolyEvery 0 (all MUFU), 3/4/8 (1/k of the pairs on the FMA pipe),
-  // -1 (timing experiment: no exp); kPingPong for variant 5 (v3 + ping-pong exp phases)
+  // -1 (timing experiment: no exp); kSpec for variant 5 (v3 + speculative softmax)
   if (!(poly == 0 || poly == 3 || poly == 4 || poly == 8 || poly == -1)) return HYDRA_EINVAL;
   if (v4 && tc4_attr() != cudaSuccess) return HYDRA_ECUDA;
   PrefixTc2Params P;
@@ -1004,7 +1035,7 @@ hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s
     prefix_tc4_kernel<<<grid, tc4::kThreads, tc4::ALLOC, s>>>(P);
     return cudaGetLastError() == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
   }
-  const bool spec = a.variant == 5;  // ping-pong
+  const bool spec = a.variant == 5;
   cudaError_t e;
   switch (poly * 2 + (spec ? 1 : 0)) {
     case 0: e = tc2_launch<0, false>(P, grid, s); break;

@@ -104,8 +104,8 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
       ptx::mbar_init(&q_full[i], 1);
       ptx::mbar_init(&q_empty[i], 1);
       ptx::mbar_init(&s_full[i], 1);
-      ptx::mbar_init(&p_full[i], 128);
-      ptx::mbar_init(&o_free[i], 128);
+      ptx::mbar_init(&p_full[i], 4);  // one elected arrival per softmax warp
+      ptx::mbar_init(&o_free[i], 4);
       ptx::mbar_init(&pv_done[i], 1);
     }
     ptx::fence_mbar_init();
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
       ptx::tmem_ld16(tmem + lane_base + 2 * NQ + pend_ob * NQ, ov);
       ptx::tmem_ld_wait();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(&o_free[pend_ob]);
+      ptx::warp_arrive(&o_free[pend_ob]);
 #pragma unroll
       for (int h = 0; h < G; ++h) {
           const float L = rs[h] + rs[NQ + h] + rs[2 * NQ + h] + rs[3 * NQ + h];
@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
         }
         ptx::fence_proxy_async_smem();
         ptx::tc_fence_before();
-        ptx::mbar_arrive(&p_full[buf]);
+        ptx::warp_arrive(&p_full[buf]);
         if (n == 0 && pend) epilogue();  // previous item's epilogue, off the critical path
       }
       pend = true;

@@ -34,7 +34,7 @@ if mode == "variants":
         run(512, 32, 8, 32768, 3, variant=variant)
         run(1024, 40, 40, 4096, 3, variant=variant)
 elif mode == "spec":
-    for variant, poly in ((3, 0), (5, 0), (5, 8), (5, 4), (5, 3), (3, 4)):
+    for variant, poly in ((3, 0), (5, 0), (5, 8), (5, 4), (3, 4)):
         run(1024, 40, 40, 16384, 3, poly=poly, variant=variant)
         run(512, 32, 8, 32768, 3, poly=poly, variant=variant)
     hydra.set_config("prefix_poly", 0)

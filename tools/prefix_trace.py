@@ -40,7 +40,7 @@ for t in (0, 1):
     sm = T[8 + t, lo:hi] - T[3 * t + 1, lo:hi]              # ld + max + exps
     pvw = T[3 * t + 2, lo:hi] - T[8 + t, lo:hi]             # PV wait + correction + st + arrive
     per = np.diff(T[3 * t + 1, lo:hi])                       # S ready -> next S ready
-    mma = T[3 * t + 1, lo + 1:hi + 1] - T[6 + t, lo:hi]     # MMA saw P(n) -> S(n+1) ready
+    mma = T[3 * t + 1, lo + 1:hi + 1] - T[6 + t, lo:hi]     # MMA saw P(n) -> S(n+1) ready (v3)
     rx = T[6 + t, lo:hi] - T[3 * t + 2, lo:hi]               # P published -> MMA thread saw it
     ldw = T[10 + t, lo:hi] - T[3 * t + 1, lo:hi]
     mxw = T[12 + t, lo:hi] - T[10 + t, lo:hi]
