@@ -441,6 +441,17 @@ def main():
             ms = float(t.item())
         return ms
 
+    # Prefix phase (north_star: >= 60% of bf16 tensor peak), measured before the step loop:
+    # burst = 20 replays on a cool GPU (against the burst cuBLAS figure); sustained = replays
+    # back to back for ~1 s (against the sustained cuBLAS figure, itself a seconds-long loop
+    # under the 1 kW power cap).
+    g_pre = capture(lambda: hydra.prefix_attn(q, pk, pv, workspace=ws))
+    ms_pre_burst = time_graph(g_pre, 20, 3)
+    n_sus = max(20, int(1000.0 / max(ms_pre_burst, 1e-3)))
+    with ClockSampler(local) as clk_pre:
+        ms_pre_sus = time_graph(g_pre, n_sus, 0)
+    clocks_pre = clk_pre.summary()
+
     # pick the step variant (prefix || suffix on two streams, or sequential) on a short probe
     g_over = capture(lambda: step(True))
     k_over = int(hydra.get_config("last_overlap_k"))  # SM split chosen for the overlapped step
@@ -477,9 +488,8 @@ def main():
     # per-kernel timing on their own (roofline of the dominant kernel and the prefix phase)
     # (the composite's workspace holds (prefix + suffix) split partials, enough for either alone)
     kk = max(5, args.steps // 4)
-    g_pre = capture(lambda: hydra.prefix_attn(q, pk, pv, workspace=ws))
     g_suf = capture(lambda: hydra.suffix_attn(q, sk, sv, lens, workspace=ws))
-    ms_pre = time_graph(g_pre, kk, 3)
+    ms_pre = time_graph(g_pre, kk, 3)  # after the step loop: GPU warm, power-capped
     ms_suf = time_graph(g_suf, kk, 3)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     in_step = None
@@ -512,6 +522,8 @@ def main():
     total_bytes = suffix_bytes + prefix_bytes + B * Hq_r * d * 2  # + bf16 output
     suf_gbs = suffix_bytes / (ms_suf * 1e-3) / 1e9
     pre_tflops = prefix_flops / (ms_pre * 1e-3) / 1e12
+    pre_burst = prefix_flops / (ms_pre_burst * 1e-3) / 1e12
+    pre_sus = prefix_flops / (ms_pre_sus * 1e-3) / 1e12
     t_roof = max(prefix_flops / (tc_burst * 1e12), total_bytes / (hbm * 1e9))
 
     value = B / (ms * 1e-3)
@@ -541,17 +553,21 @@ def main():
                      "frac_of_nominal_7700": round(suf_gbs / 7700.0, 4),
                      "note": "read-only stream vs a read+write copy peak: can read a little above 1.0"},
         "prefix_phase": {"bound": "tensor", "kernel": "prefix_tc2_kernel (persistent tcgen05, all SMs)",
-                         "achieved": round(pre_tflops, 1), "unit": "TFLOP/s", "peak_burst": tc_burst,
-                         "frac_of_measured": round(pre_tflops / tc_burst, 4), "peak_sustained": tc_sust,
-                         "frac_of_measured_sustained": round(pre_tflops / tc_sust, 4),
-                         "frac_of_spec_2250": round(pre_tflops / 2250.0, 4), "flops_per_launch": prefix_flops,
+                         "achieved": round(pre_burst, 1), "unit": "TFLOP/s", "peak": tc_burst,
+                         "frac": round(pre_burst / tc_burst, 4), "launch_ms": round(ms_pre_burst, 5),
+                         "timed": "burst: 20 graph replays on a cool GPU, before the step loop",
+                         "sustained": {"achieved": round(pre_sus, 1), "peak": tc_sust,
+                                       "frac": round(pre_sus / tc_sust, 4), "launch_ms": round(ms_pre_sus, 5),
+                                       "replays": n_sus, "clocks": clocks_pre,
+                                       "timed": "back-to-back replays for ~1 s vs the sustained cuBLAS loop"},
+                         "after_step_loop": {"achieved": round(pre_tflops, 1), "launch_ms": round(ms_pre, 5)},
+                         "frac_of_spec_2250": round(pre_burst / 2250.0, 4), "flops_per_launch": prefix_flops,
                          "traffic": NCU_TRAFFIC.get((args.config, "prefix_tc2_kernel")),
-                         "algorithmic_bytes_per_launch": prefix_bytes,
-                         "launch_ms": round(ms_pre, 5), "timed": "after the timed region (GPU warm, power-capped)"},
+                         "algorithmic_bytes_per_launch": prefix_bytes},
         "step_roofline": {"t_roof_ms": round(t_roof * 1e3, 5), "frac": round(t_roof * 1e3 / ms, 4),
                           "ms_sequential": round(ms_seq, 5), "ms_overlap": round(ms_over, 5)},
         "clocks": clocks,
-        "gpu_launches": args.steps * (4 if overlap else 3),
+        "gpu_launches": args.steps * 4,  # fill (-inf partial slots), prefix, suffix, combine
     }
     if flat:
         line["flatness"] = flat

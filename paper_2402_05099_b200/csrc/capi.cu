@@ -217,22 +217,26 @@ static int prefix_splits(const hydra_heads *h, int64_t B, int64_t P, int tc2_cta
 // SM split for running the persistent prefix (tensor-bound) and suffix (HBM-bound)
 // kernels concurrently.  k prefix CTAs balance the two finish times:
 //   t_prefix(k) = pair_blocks / (k * R_P),  t_suffix(k) = kv_bytes / min((SMs-k) * R_S, BW)
-// with per-SM rates measured on B200 (R_P: 256-row x 128-token blocks per us per SM;
-// R_S: suffix bytes per us per SM; BW: achievable HBM read bandwidth).  0 = no overlap.
+// with per-SM rates measured on B200 at C3@16K, each kernel alone on its SM share
+// (tools/overlap_var.py): R_P = 256-row x 128-token blocks per us per SM (0.46 at 48-56
+// SMs), R_S = suffix bytes per us per SM (64-72 KB/us at 92-100 SMs), BW = HBM read
+// ceiling.  Running together they interfere (HBM, L2, the 1 kW power cap), which favours
+// the prefix side: R_S is taken at the top of its range.  Candidates are multiples of the
+// prefix plan's group size so no SM is left idle.  0 = no overlap.
 static int overlap_prefix_ctas(const hydra_heads *h, int64_t B, int64_t P, int64_t S_cap) {
   if (P <= 0 || S_cap <= 0 || !use_suffix_tc(h, B, S_cap, true)) return 0;
   const int g = h->num_q_heads / h->num_kv_heads;
   if (prefix_kind(h, B * g, P) != PK_TC2) return 0;
   const int sms = device_sm_count();
   if (g_overlap_prefix_ctas > 0) return (int)std::min<int64_t>(g_overlap_prefix_ctas, sms - 1);
-  // calibrated on B200 at C3@16K under overlap (prefix and suffix share HBM and L2):
-  // best k ~ 40-50 of 148 (tools/overlap_exp2.py)
-  const double R_P = 0.44, R_S = 5.0e4, BW = 7.0e6;
-  const double pair_blocks = (double)((B * g + 255) / 256) * h->num_kv_heads * ((P + 127) / 128);
+  const double R_P = 0.46, R_S = 7.2e4, BW = 7.0e6;
+  const int64_t pairs = (B * g + 255) / 256;
+  const double pair_blocks = (double)pairs * h->num_kv_heads * ((P + 127) / 128);
   const double kv_bytes = (double)B * h->num_kv_heads * S_cap * h->head_dim * 4.0;
   int best_k = 0;
   double best = 1e300;
   for (int k = 8; k <= sms - 8; ++k) {
+    if (prefix_tc2_ctas(B, g, h->num_kv_heads, P, k, prefix_bn()) != k) continue;  // plan would idle SMs
     const double t = std::max(pair_blocks / (k * R_P), kv_bytes / std::min((sms - k) * R_S, BW));
     if (t < best) {
       best = t;
@@ -584,8 +588,12 @@ extern "C" hydra_status hydra_attn(const hydra_heads *h, int64_t B, const void *
   }
   if (st) return st;
   if (S_cap > 0) {
+    // the suffix takes every SM the prefix plan leaves free (the plan may round k down)
+    const int k_eff = k_over > 0 ? prefix_tc2_ctas(B, h->num_q_heads / h->num_kv_heads, h->num_kv_heads, P, k_over,
+                                                   prefix_bn())
+                                 : 0;
     st = run_suffix(h, B, q, q_sb, q_sh, sk, sv, s_sb, s_st, s_sh, S_cap, lens, ns, suf, s,
-                    k_over > 0 ? std::max(1, sms - k_over) : 0);
+                    k_over > 0 ? std::max(1, sms - k_eff) : 0);
   } else {
     st = launch_fill_neg_inf(suf.lse, rows, s);
     if (st) st = cuda_fail("fill");
