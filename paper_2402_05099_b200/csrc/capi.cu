@@ -41,7 +41,7 @@ static hydra_status cuda_fail(const char *what) {
 
 static std::atomic<int64_t> g_prefix_impl{0}, g_prefix_splits{0}, g_suffix_splits{0}, g_tc_debug{0},
     g_prefix_stages{3}, g_suffix_unroll{4}, g_prefix_ctas{0}, g_suffix_impl{0}, g_suffix_ctas{0},
-    g_overlap_prefix_ctas{0}, g_prefix_poly{0}, g_prefix_variant{3}, g_prefix_trace{0},
+    g_overlap_prefix_ctas{0}, g_prefix_poly{0}, g_prefix_variant{3}, g_prefix_trace{0}, g_suffix_cb{2}, g_suffix_trace{0},
     g_last_overlap_k{0};  // read-only: prefix CTAs of the last hydra_attn overlap split (0 = sequential)
 
 extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
@@ -58,6 +58,8 @@ extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
   else if (!strcmp(key, "prefix_poly")) g_prefix_poly = (value == 0 || value == 3 || value == 8 || value == -1) ? value : 4;
   else if (!strcmp(key, "prefix_variant")) g_prefix_variant = (value == 4 || value == 5) ? value : 3;
   else if (!strcmp(key, "prefix_stages")) g_prefix_stages = (value == 2 ? 2 : 3);
+  else if (!strcmp(key, "suffix_trace")) g_suffix_trace = value;
+  else if (!strcmp(key, "suffix_cb")) g_suffix_cb = (value == 1 ? 1 : 2);
   else if (!strcmp(key, "suffix_unroll")) g_suffix_unroll = (value >= 8 ? 8 : value >= 4 ? 4 : 2);
   else return fail(HYDRA_EINVAL, "unknown config key '%s'", key);
   return HYDRA_OK;
@@ -79,6 +81,8 @@ extern "C" int64_t hydra_get_config(const char *key) {
   if (!strcmp(key, "prefix_poly")) return g_prefix_poly;
   if (!strcmp(key, "prefix_variant")) return g_prefix_variant;
   if (!strcmp(key, "suffix_unroll")) return g_suffix_unroll;
+  if (!strcmp(key, "suffix_cb")) return g_suffix_cb;
+  if (!strcmp(key, "suffix_trace")) return g_suffix_trace;
   return -1;
 }
 
@@ -359,6 +363,9 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
     a.scale_log2 = scale_of(h) * 1.4426950408889634f;
     a.o = dst.o;
     a.lse = dst.lse;
+    a.cb = (int32_t)g_suffix_cb;
+    a.trace = reinterpret_cast<void *>((intptr_t)g_suffix_trace.load());
+    a.debug = (int32_t)g_tc_debug;
     const int ctas = tc_ctas > 0 ? tc_ctas : (g_suffix_ctas > 0 ? (int)g_suffix_ctas : device_sm_count());
     hydra_status st = launch_suffix_tc(a, ctas, s);
     return st == HYDRA_OK ? st : cuda_fail("suffix tcgen05 launch");

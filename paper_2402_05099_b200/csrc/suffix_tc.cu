@@ -38,24 +38,32 @@ constexpr int BT = 128;   // tokens per block (UMMA M of S^T, K of PV)
 constexpr int HD = 128;   // head dim (UMMA K of S^T, M of PV)
 constexpr int NQ = 16;    // padded query heads per KV group (UMMA N)
 constexpr int NS = 3;     // K stages and V stages (separate rings: K frees after S, V after PV)
-constexpr int kThreads = 192;
+constexpr int kThreads = 256;  // warp 0 K producer, 1 MMA, 2-5 softmax, 6 V producer, 7 Q producer
 constexpr int PANEL = BT * 128;      // 128 rows x 128 B
 constexpr int TILE = 2 * PANEL;      // 32 KB
 constexpr int QPANEL = NQ * 128;     // 2 KB: 16 rows x 64 dims
 constexpr int QTILE = 2 * QPANEL;    // 4 KB
 constexpr int PPANEL = NQ * 128;     // P^T: 16 rows x 64 tokens
-constexpr int PTILE = 2 * PPANEL;    // 4 KB
+constexpr int PTILE = 2 * PPANEL;    // 4 KB per 128-token block
 constexpr int OFF_K = 0;
 constexpr int OFF_V = OFF_K + NS * TILE;
 constexpr int OFF_Q = OFF_V + NS * TILE;     // 2 slots
-constexpr int OFF_P = OFF_Q + 2 * QTILE;     // 2 slots
-constexpr int OFF_RED = OFF_P + 2 * PTILE;   // [2 block parity][4 warps][16] max + [2 item parity][4][16] sums
-constexpr int OFF_BAR = OFF_RED + (2 * 4 * NQ + 2 * 4 * NQ) * 4;
-// k_full, k_empty, v_full, v_empty [NS]; q_full, q_empty, s_full, p_full, o_free, pv_done [2]
-constexpr int N_BARS = 4 * NS + 12;
-constexpr int BYTES = OFF_BAR + N_BARS * 8 + 16;
-constexpr int ALLOC = BYTES + 1024;
-constexpr uint32_t TMEM_COLS = 64;  // S^T x2 (16 cols each), O^T x2
+// Round slots (S^T in TMEM, P^T in smem): the score MMA may run nsp rounds ahead of the PV
+// MMA, so a round's softmax is done long before its V tile lands and a V slot is held for
+// little more than the load latency (SM-budget measurements, tools/suffix_trace.py).
+// Q slots: items the score MMA may be ahead of the PV MMA, plus one.
+__host__ __device__ constexpr int nsp(int cb) { return cb == 1 ? 4 : 2; }
+__host__ __device__ constexpr int nqs(int cb) { return cb == 1 ? 3 : 2; }
+__host__ __device__ constexpr int off_p(int cb) { return OFF_Q + nqs(cb) * QTILE; }
+__host__ __device__ constexpr int off_red(int cb) { return off_p(cb) + nsp(cb) * cb * PTILE; }
+// [2 round parity][4 warps][16] max + [2 item parity][4][16] sums
+__host__ __device__ constexpr int off_bar(int cb) { return off_red(cb) + (2 * 4 * NQ + 2 * 4 * NQ) * 4; }
+// k_full, k_empty, v_full, v_empty [NS]; q_full, q_empty [4]; s_full, p_full, pv_done [4]; o_free [2]
+constexpr int N_BARS = 4 * NS + 8 + 12 + 2;
+__host__ __device__ constexpr int alloc_bytes(int cb) { return off_bar(cb) + N_BARS * 8 + 16 + 1024; }
+static_assert(alloc_bytes(1) <= 232448 && alloc_bytes(2) <= 232448, "suffix_tc smem over the 227 KB opt-in limit");
+// S^T x 2 round slots x CB blocks (16 columns each), O^T x 2; rounded up to a power of two
+__host__ __device__ constexpr uint32_t tmem_cols(int cb) { return 128u; }  // nsp*cb*16 + 2*16 <= 96
 }  // namespace stc
 
 struct __align__(64) SuffixTcParams {
@@ -65,21 +73,93 @@ struct __align__(64) SuffixTcParams {
   float scale_log2;
   int32_t n_items;
   float *o, *lse;
+  int32_t debug;     // timing experiments only (invalid results): 256 = consume K/V tiles without math,
+                     // 512 = MMAs without softmax work, 1024 = no proxy fence before publishing P^T
+  long long *trace;  // diagnostics: CTA 0 event timestamps [kTraceRows][kTraceN] (tools/suffix_trace.py); null = off
 };
+namespace stc {
+constexpr int kTraceN = 1024;
+// trace rows: 0 softmax s_full wait begin, 1 s_full acquired, 2 scores loaded, 3 block max done,
+// 4 P^T published (p_full arrive), 5 epilogue begin, 6 epilogue end, 7 MMA S round committed,
+// 8 MMA PV round committed, 9 K TMA issued (block), 10 V TMA issued (block), 11 / 12 MMA thread
+// sees K / V landed (block)
+__device__ __forceinline__ void trace(long long *tr, int row, uint32_t i) {
+  if (tr && i < (uint32_t)kTraceN) tr[row * kTraceN + i] = clock64();
+}
+}  // namespace stc
 
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <int G>  // query heads per KV group (compile-time: no per-head predicates)
+// lens[b] of the item this CTA handles `k` steps ahead (0 when past the end): every role
+// fetches the next item's length one item early so the load is off the critical path.
+__device__ __forceinline__ int item_len(const SuffixTcParams &P, int item) {
+  return item < P.n_items ? __ldg(P.lens + item / P.Hkv) : 0;
+}
+
+// Walks the rounds (up to CB consecutive 128-token blocks of one item) a CTA processes, in
+// order, with the ring positions the producers use: gb = first block's ring index, gr =
+// round index, qi / item_no = index of the item among this CTA's non-empty items.
+template <int CB>
+struct RoundCursor {
+  int item, len, len_next, nblk, n0, nb;
+  uint32_t gb, gr, qi, item_no;
+  bool valid;
+  __device__ __forceinline__ void seek(const SuffixTcParams &P) {  // first round of the next non-empty item
+    while (item < P.n_items) {
+      len = len_next;
+      len_next = item_len(P, item + gridDim.x);
+      nblk = (len + stc::BT - 1) / stc::BT;
+      if (nblk > 0) {
+        n0 = 0;
+        nb = min(CB, nblk);
+        valid = true;
+        return;
+      }
+      item += gridDim.x;
+    }
+    valid = false;
+  }
+  __device__ __forceinline__ void init(const SuffixTcParams &P) {
+    item = blockIdx.x;
+    len_next = item_len(P, item);
+    gb = gr = qi = item_no = 0;
+    seek(P);
+  }
+  __device__ __forceinline__ void next(const SuffixTcParams &P) {
+    gb += nb;
+    ++gr;
+    n0 += nb;
+    if (n0 < nblk) {
+      nb = min(CB, nblk - n0);
+      return;
+    }
+    ++qi;
+    ++item_no;
+    item += gridDim.x;
+    seek(P);
+  }
+};
+
+// G = query heads per KV group (compile-time: no per-head predicates).
+// CB = 128-token blocks per softmax round: the softmax warps take one block max / barrier /
+// P^T write per round of up to CB blocks (thread r owns tokens r, 128 + r, ...), so the
+// per-round latency chain (S MMA -> TMEM load -> cross-warp max -> exp -> P^T -> PV MMA)
+// is paid once per CB blocks.  Online softmax across the rounds of an item.
+template <int G, int CB>
 __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __grid_constant__ SuffixTcParams P) {
   using namespace stc;
+  constexpr int OFF_P = off_p(CB), OFF_RED = off_red(CB), OFF_BAR = off_bar(CB);
+  constexpr int NSP = nsp(CB), NQS = nqs(CB);
+  constexpr uint32_t TMEM_COLS = tmem_cols(CB);
+  constexpr uint32_t O_COL = NSP * CB * NQ;  // O^T buffers start after the S^T round slots
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
   uint64_t *k_full = bars, *k_empty = bars + NS, *v_full = bars + 2 * NS, *v_empty = bars + 3 * NS;
-  uint64_t *q_full = bars + 4 * NS, *q_empty = q_full + 2, *s_full = q_full + 4, *p_full = q_full + 6,
-           *o_free = q_full + 8, *pv_done = q_full + 10;
+  uint64_t *q_full = bars + 4 * NS, *q_empty = q_full + 4, *s_full = q_full + 8, *p_full = q_full + 12,
+           *pv_done = q_full + 16, *o_free = q_full + 20;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + N_BARS);
   float *red_max = reinterpret_cast<float *>(smem + OFF_RED);  // [2][4][NQ]
   float *red_sum = red_max + 2 * 4 * NQ;                        // [2][4][NQ]
@@ -87,7 +167,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
   constexpr int g = G;
 
   // zero Q^T / P^T slots once: rows >= g (padding heads) must stay 0 forever
-  for (int i = threadIdx.x; i < (2 * QTILE + 2 * PTILE) / 16; i += kThreads)
+  for (int i = threadIdx.x; i < (NQS * QTILE + NSP * CB * PTILE) / 16; i += kThreads)
     reinterpret_cast<uint4 *>(smem + OFF_Q)[i] = make_uint4(0, 0, 0, 0);
   ptx::fence_proxy_async_smem();
   if (warp == 0 && lane == 0) {
@@ -100,14 +180,14 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
       ptx::mbar_init(&v_full[i], 1);
       ptx::mbar_init(&v_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       ptx::mbar_init(&q_full[i], 1);
       ptx::mbar_init(&q_empty[i], 1);
       ptx::mbar_init(&s_full[i], 1);
       ptx::mbar_init(&p_full[i], 4);  // one elected arrival per softmax warp
-      ptx::mbar_init(&o_free[i], 4);
       ptx::mbar_init(&pv_done[i], 1);
     }
+    for (int i = 0; i < 2; ++i) ptx::mbar_init(&o_free[i], 4);
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
@@ -116,109 +196,186 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    // ================= TMA producer =================
+  if (warp == 0 || warp == 6 || warp == 7) {
+    // ================= TMA producers: warp 0 K ring, warp 6 V ring, warp 7 Q slots =================
+    // Separate threads so no load waits behind another kind of slot (V slots free only after
+    // the PV MMA, K slots right after the score MMA, Q slots after an item's last PV).
     if (ptx::elect_one()) {
+      long long *tr = blockIdx.x == 0 ? P.trace : nullptr;
       uint32_t gb = 0, qi = 0;
+      int len_next = item_len(P, blockIdx.x);
       for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
         const int b = item / P.Hkv, j = item % P.Hkv;
-        const int len = P.lens[b];
+        const int len = len_next;
+        len_next = item_len(P, item + gridDim.x);
         const int nblk = (len + BT - 1) / BT;
         if (nblk == 0) continue;
-        const int qs = qi & 1;
-        ptx::mbar_wait(&q_empty[qs], ((qi >> 1) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&q_full[qs], 2 * 64 * g * 2);
-        uint8_t *sQ = smem + OFF_Q + qs * QTILE;
-        ptx::tma_load_3d(sQ, &P.tmQ, &q_full[qs], 0, j * g, b);
-        ptx::tma_load_3d(sQ + QPANEL, &P.tmQ, &q_full[qs], 64, j * g, b);
-        ++qi;
+        if (warp == 7) {
+          const int qs = qi % NQS;
+          ptx::mbar_wait(&q_empty[qs], ((qi / NQS) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&q_full[qs], 2 * 64 * g * 2);
+          uint8_t *sQ = smem + OFF_Q + qs * QTILE;
+          ptx::tma_load_3d(sQ, &P.tmQ, &q_full[qs], 0, j * g, b);
+          ptx::tma_load_3d(sQ + QPANEL, &P.tmQ, &q_full[qs], 64, j * g, b);
+          ++qi;
+          continue;
+        }
         for (int n = 0; n < nblk; ++n, ++gb) {
           const int st = gb % NS;
           const uint32_t ph = ((gb / NS) & 1) ^ 1;
-          uint8_t *sK = smem + OFF_K + st * TILE, *sV = smem + OFF_V + st * TILE;
           const int t0 = n * BT;
-          ptx::mbar_wait(&k_empty[st], ph);
-          ptx::mbar_arrive_expect_tx(&k_full[st], TILE);
-          ptx::tma_load_4d(sK, &P.tmK, &k_full[st], 0, j, t0, b);
-          ptx::tma_load_4d(sK + PANEL, &P.tmK, &k_full[st], 64, j, t0, b);
-          ptx::mbar_wait(&v_empty[st], ph);
-          ptx::mbar_arrive_expect_tx(&v_full[st], TILE);
-          ptx::tma_load_4d(sV, &P.tmV, &v_full[st], 0, j, t0, b);
-          ptx::tma_load_4d(sV + PANEL, &P.tmV, &v_full[st], 64, j, t0, b);
+          if (warp == 0) {
+            uint8_t *sK = smem + OFF_K + st * TILE;
+            ptx::mbar_wait(&k_empty[st], ph);
+            if (P.debug & 524288) ptx::mbar_wait(&v_empty[st], ph);  // timing experiment: K issued with V
+            ptx::mbar_arrive_expect_tx(&k_full[st], TILE);
+            ptx::tma_load_4d(sK, &P.tmK, &k_full[st], 0, j, t0, b);
+            ptx::tma_load_4d(sK + PANEL, &P.tmK, &k_full[st], 64, j, t0, b);
+            trace(tr, 9, gb);
+          } else {
+            uint8_t *sV = smem + OFF_V + st * TILE;
+            ptx::mbar_wait(&v_empty[st], ph);
+            ptx::mbar_arrive_expect_tx(&v_full[st], TILE);
+            ptx::tma_load_4d(sV, &P.tmV, &v_full[st], 0, j, t0, b);
+            ptx::tma_load_4d(sV + PANEL, &P.tmV, &v_full[st], 64, j, t0, b);
+            trace(tr, 10, gb);
+          }
         }
       }
     }
   } else if (warp == 1) {
-    // ================= MMA issuer (flat block sequence across items, one-block lookahead) =================
-    if (ptx::elect_one()) {
+    // ================= MMA issuer (event-driven) =================
+    // Two cursors over the same flat round sequence: the S cursor issues score MMAs as soon
+    // as a round's K tiles land (at most two rounds ahead of the PV cursor: two S^T slots),
+    // the PV cursor issues a round's PV MMAs as soon as its P^T and V tiles are ready.
+    // Neither waits behind the other, so a V slot is held only for load + softmax + PV.
+    const bool leader = ptx::elect_one();
+    if (leader && (P.debug & 256)) {  // drain only: release each tile as soon as it lands
+      RoundCursor<CB> c;
+      c.init(P);
+      while (c.valid) {
+        if (c.n0 == 0) ptx::mbar_wait(&q_full[c.qi % NQS], (c.qi / NQS) & 1);
+        for (int i = 0; i < c.nb; ++i) {
+          const uint32_t gbc = c.gb + i, st = gbc % NS;
+          ptx::mbar_wait(&k_full[st], (gbc / NS) & 1);
+          trace(blockIdx.x == 0 ? P.trace : nullptr, 11, gbc);
+          ptx::mbar_arrive(&k_empty[st]);
+          ptx::mbar_wait(&v_full[st], (gbc / NS) & 1);
+          trace(blockIdx.x == 0 ? P.trace : nullptr, 12, gbc);
+          ptx::mbar_arrive(&v_empty[st]);
+        }
+        if (c.n0 + c.nb >= c.nblk) ptx::mbar_arrive(&q_empty[c.qi % NQS]);
+        c.next(P);
+      }
+    } else if (leader) {
       constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BT, NQ, false);                 // A=K, B=Q^T (K-major)
       constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(HD, NQ, false) | (1u << 15);  // A=V^T (MN-major), B=P^T
-      struct Blk {
-        uint32_t gbi, st, ob, qs, item_no;
-        bool first, last;
-      } prev{};
-      bool have_prev = false;
-      uint32_t gbi = 0, qi = 0, item_no = 0;
-      auto do_pv = [&](const Blk &x) {
-        const uint32_t slot = x.gbi & 1;
-        ptx::mbar_wait(&p_full[slot], (x.gbi >> 1) & 1);
-        if (x.first) ptx::mbar_wait(&o_free[x.ob], ((x.item_no >> 1) & 1) ^ 1);
-        ptx::mbar_wait(&v_full[x.st], (x.gbi / NS) & 1);
-        ptx::tc_fence_after();
-        const uint32_t v_addr = ptx::smem_u32(smem + OFF_V + x.st * TILE);
-        const uint32_t p_addr = ptx::smem_u32(smem + OFF_P + slot * PTILE);
-#pragma unroll
-        for (int kk = 0; kk < BT / 16; ++kk)
-          ptx::mma_ss(tmem + 2 * NQ + x.ob * NQ, ptx::smem_desc_sw128(v_addr + kk * 2048, PANEL, 1024),
-                      ptx::smem_desc_sw128(p_addr + (kk / 4) * PPANEL + (kk % 4) * 32, 16, 1024), idesc_pv,
-                      (!x.first || kk > 0));
-        ptx::mma_commit(&pv_done[slot]);
-        ptx::mma_commit(&v_empty[x.st]);
-        if (x.last) ptx::mma_commit(&q_empty[x.qs]);
+      long long *tr = blockIdx.x == 0 ? P.trace : nullptr;
+      // timing experiment 32768 (only with the MMAs skipped): plain arrivals instead of commits
+      auto commit_ = [&](uint64_t *bar) {
+        if (P.debug & 32768) ptx::mbar_arrive(bar);
+        else ptx::mma_commit(bar);
       };
-      for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
-        const int b = item / P.Hkv;
-        const int nblk = (P.lens[b] + BT - 1) / BT;
-        if (nblk == 0) continue;
-        const uint32_t qs = qi & 1;
-        ptx::mbar_wait(&q_full[qs], (qi >> 1) & 1);
-        const uint32_t q_addr = ptx::smem_u32(smem + OFF_Q + qs * QTILE);
-        for (int n = 0; n < nblk; ++n, ++gbi) {
-          const uint32_t st = gbi % NS;
-          ptx::mbar_wait(&k_full[st], (gbi / NS) & 1);
-          ptx::tc_fence_after();
-          const uint32_t k_addr = ptx::smem_u32(smem + OFF_K + st * TILE);
+      auto poll_ = [&](uint64_t *bar, uint32_t ph) {  // 131072: suspending try_wait (timing experiment)
+        return (P.debug & 131072) ? ptx::mbar_try_wait(bar, ph) : ptx::mbar_test_wait(bar, ph);
+      };
+      RoundCursor<CB> sc, pc;
+      sc.init(P);
+      pc.init(P);
+      uint32_t s_c = 0, p_c = 0;  // blocks of the current round already issued (S / PV cursor)
+      bool p_ready = false;       // PV cursor: P^T (and O^T) of the current round available
+      while (pc.valid) {
+        const uint32_t mark = sc.gr * 8 + s_c + pc.gr * 4096 + p_c * 512;
+        // ---- S cursor
+        if (sc.valid && sc.gr < pc.gr + NSP) {
+          const uint32_t qs = sc.qi % NQS;
+          if (s_c < (uint32_t)sc.nb && poll_(&q_full[qs], (sc.qi / NQS) & 1)) {
+            const uint32_t q_addr = ptx::smem_u32(smem + OFF_Q + qs * QTILE);
+            while (s_c < (uint32_t)sc.nb) {
+              const uint32_t gbc = sc.gb + s_c, st = gbc % NS;
+              if (!poll_(&k_full[st], (gbc / NS) & 1)) break;
+              trace(tr, 11, gbc);
+              if (!(P.debug & (1 << 20))) ptx::tc_fence_after();
+              const uint32_t k_addr = ptx::smem_u32(smem + OFF_K + st * TILE);
 #pragma unroll
-          for (int kk = 0; kk < HD / 16; ++kk) {
-            const uint32_t off = (kk / 4) * PANEL + (kk % 4) * 32, qoff = (kk / 4) * QPANEL + (kk % 4) * 32;
-            ptx::mma_ss(tmem + (gbi & 1) * NQ, ptx::smem_desc_sw128(k_addr + off, 16, 1024),
-                        ptx::smem_desc_sw128(q_addr + qoff, 16, 1024), idesc_s, kk > 0);
+              for (int kk = 0; kk < HD / 16; ++kk) {
+                if (P.debug & 4096) break;  // timing experiment only: no score MMAs
+                const uint32_t off = (kk / 4) * PANEL + (kk % 4) * 32, qoff = (kk / 4) * QPANEL + (kk % 4) * 32;
+                ptx::mma_ss(tmem + ((sc.gr % NSP) * CB + s_c) * NQ, ptx::smem_desc_sw128(k_addr + off, 16, 1024),
+                            ptx::smem_desc_sw128(q_addr + qoff, 16, 1024), idesc_s, kk > 0);
+              }
+              commit_(&k_empty[st]);
+              ++s_c;
+            }
           }
-          ptx::mma_commit(&s_full[gbi & 1]);
-          ptx::mma_commit(&k_empty[st]);
-          if (have_prev) do_pv(prev);  // PV of the previous block after S of this one
-          prev = Blk{gbi, st, item_no & 1, qs, item_no, n == 0, n == nblk - 1};
-          have_prev = true;
+          if (s_c == (uint32_t)sc.nb) {
+            commit_(&s_full[sc.gr % NSP]);
+            if (P.debug & 65536)  // timing experiment only: no softmax warps; stand in for their arrivals
+              for (int w = 0; w < 4; ++w) ptx::mbar_arrive(&p_full[sc.gr % NSP]);
+            trace(tr, 7, sc.gr);
+            sc.next(P);
+            s_c = 0;
+          }
         }
-        ++qi;
-        ++item_no;
+        // ---- PV cursor (only rounds whose S was issued)
+        if (pc.gr < sc.gr || !sc.valid) {
+          const uint32_t slot = pc.gr % NSP;
+          if (!p_ready) {
+            p_ready = poll_(&p_full[slot], (pc.gr / NSP) & 1) &&
+                      (pc.n0 > 0 || poll_(&o_free[pc.item_no & 1], ((pc.item_no >> 1) & 1) ^ 1));
+          }
+          if (p_ready) {
+            const uint32_t p_base = ptx::smem_u32(smem + OFF_P + slot * CB * PTILE);
+            const uint32_t ob = pc.item_no & 1;
+            while (p_c < (uint32_t)pc.nb) {
+              const uint32_t gbc = pc.gb + p_c, st = gbc % NS;
+              if (!poll_(&v_full[st], (gbc / NS) & 1)) break;
+              trace(tr, 12, gbc);
+              if (!(P.debug & (1 << 20))) ptx::tc_fence_after();
+              const uint32_t v_addr = ptx::smem_u32(smem + OFF_V + st * TILE);
+              const uint32_t p_addr = p_base + p_c * PTILE;
+#pragma unroll
+              for (int kk = 0; kk < BT / 16; ++kk)
+                if (!(P.debug & 8192))  // timing experiment only: no PV MMAs
+                ptx::mma_ss(tmem + O_COL + ob * NQ, ptx::smem_desc_sw128(v_addr + kk * 2048, PANEL, 1024),
+                            ptx::smem_desc_sw128(p_addr + (kk / 4) * PPANEL + (kk % 4) * 32, 16, 1024), idesc_pv,
+                            (pc.n0 > 0 || p_c > 0 || kk > 0));
+              commit_(&v_empty[st]);
+              ++p_c;
+            }
+            if (p_c == (uint32_t)pc.nb) {
+              commit_(&pv_done[slot]);
+              trace(tr, 8, pc.gr);
+              if (pc.n0 + pc.nb >= pc.nblk) {
+                commit_(&q_empty[pc.qi % NQS]);
+                if (P.debug & 65536)
+                  for (int w = 0; w < 4; ++w) ptx::mbar_arrive(&o_free[pc.item_no & 1]);
+              }
+              pc.next(P);
+              p_c = 0;
+              p_ready = false;
+            }
+          }
+        }
+        if ((P.debug & 16384) && mark == sc.gr * 8 + s_c + pc.gr * 4096 + p_c * 512) __nanosleep((P.debug & 262144) ? 1000 : 64);
       }
-      if (have_prev) do_pv(prev);
     }
-  } else {
+  } else if (!(P.debug & (256 | 65536))) {
     // ================= softmax (thread = token lane) / lagged epilogue (thread = head dim) =================
     const int quarter = warp % 4;
     const int r = quarter * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const float c2 = P.scale_log2;
-    uint32_t gbi = 0, item_no = 0;
-    // state of the item whose epilogue is pending (run after the next item's first block)
+    uint32_t gr = 0, gb = 0, item_no = 0, n_epi = 0;
+    long long *tr = (blockIdx.x == 0 && quarter == 0 && lane == 0) ? P.trace : nullptr;
+    // state of the item whose epilogue is pending (run after the next item's first round)
     bool pend = false;
     int64_t pend_row0 = 0;
     uint32_t pend_ob = 0, pend_last = 0;
     float pm[G], pl[G];
     auto epilogue = [&]() {
-      ptx::mbar_wait(&pv_done[pend_last & 1], (pend_last >> 1) & 1);
+      trace(tr, 5, n_epi);
+      ptx::mbar_wait(&pv_done[pend_last % NSP], (pend_last / NSP) & 1);
       ptx::tc_fence_after();
       // two epilogues can run back to back (the lagged one and the final one): alternate
       // the reduction buffer by item parity so a fast warp never overwrites sums a slow
@@ -226,28 +383,31 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
       float *rs = red_sum + pend_ob * 4 * NQ;
 #pragma unroll
       for (int h = 0; h < G; ++h) {
-          float x = pl[h];
+        float x = pl[h];
 #pragma unroll
-          for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-          if (lane == 0) rs[quarter * NQ + h] = x;
-        }
+        for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) rs[quarter * NQ + h] = x;
+      }
       named_bar_sync(1, 128);
       uint32_t ov[NQ];
-      ptx::tmem_ld16(tmem + lane_base + 2 * NQ + pend_ob * NQ, ov);
+      ptx::tmem_ld16(tmem + lane_base + O_COL + pend_ob * NQ, ov);
       ptx::tmem_ld_wait();
       ptx::tc_fence_before();
       ptx::warp_arrive(&o_free[pend_ob]);
 #pragma unroll
       for (int h = 0; h < G; ++h) {
-          const float L = rs[h] + rs[NQ + h] + rs[2 * NQ + h] + rs[3 * NQ + h];
-          P.o[(pend_row0 + h) * HD + r] = __uint_as_float(ov[h]) / L;
-          if (r == h) P.lse[pend_row0 + h] = (pm[h] + log2f(L)) * HYDRA_LN2;
-        }
+        const float L = rs[h] + rs[NQ + h] + rs[2 * NQ + h] + rs[3 * NQ + h];
+        P.o[(pend_row0 + h) * HD + r] = __uint_as_float(ov[h]) / L;
+        if (r == h) P.lse[pend_row0 + h] = (pm[h] + log2f(L)) * HYDRA_LN2;
+      }
+      trace(tr, 6, n_epi++);
       pend = false;
     };
+    int len_next = item_len(P, blockIdx.x);
     for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
       const int b = item / P.Hkv, j = item % P.Hkv;
-      const int len = P.lens[b];
+      const int len = len_next;
+      len_next = item_len(P, item + gridDim.x);
       const int nblk = (len + BT - 1) / BT;
       const int64_t row0 = (int64_t)b * P.Hq + (int64_t)j * g;
       if (nblk == 0) {  // empty suffix: (0, -inf) sentinel
@@ -258,33 +418,52 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
         continue;
       }
       const uint32_t ob = item_no & 1;
-      const uint32_t o_tmem = tmem + lane_base + 2 * NQ + ob * NQ;
+      const uint32_t o_tmem = tmem + lane_base + O_COL + ob * NQ;
       float m[G], l[G];
 #pragma unroll
       for (int h = 0; h < G; ++h) {
         m[h] = -INFINITY;
         l[h] = 0.f;
       }
-      for (int n = 0; n < nblk; ++n, ++gbi) {
-        const uint32_t buf = gbi & 1;
-        ptx::mbar_wait(&s_full[buf], (gbi >> 1) & 1);
+      for (int n0 = 0; n0 < nblk; n0 += CB, ++gr) {
+        const int nb = min(CB, nblk - n0);
+        const uint32_t buf = gr % NSP;
+        trace(tr, 0, gr);
+        ptx::mbar_wait(&s_full[buf], (gr / NSP) & 1);
+        trace(tr, 1, gr);
         ptx::tc_fence_after();
-        uint32_t sv[NQ];
-        ptx::tmem_ld16(tmem + lane_base + buf * NQ, sv);
+        if (P.debug & 512) {  // timing experiment only: no softmax work
+          if (gr >= (uint32_t)NSP) ptx::mbar_wait(&pv_done[buf], ((gr - NSP) / NSP) & 1);
+          ptx::warp_arrive(&p_full[buf]);
+          gb += nb;
+          if (n0 == 0 && pend) epilogue();
+          continue;
+        }
+        uint32_t sv[CB][NQ];
+#pragma unroll
+        for (int c = 0; c < CB; ++c)
+          if (c < nb) ptx::tmem_ld16(tmem + lane_base + (buf * CB + c) * NQ, sv[c]);
         ptx::tmem_ld_wait();
-        const int valid = min(BT, len - n * BT);
-        const bool tok = r < valid;
-        float s[G];
-        float *rm = red_max + buf * 4 * NQ;
+        trace(tr, 2, gr);
+        float s[CB][G];
+        bool tok[CB];
+        float *rm = red_max + (gr & 1) * 4 * NQ;
+#pragma unroll
+        for (int c = 0; c < CB; ++c) tok[c] = c < nb && (n0 + c) * BT + r < len;
 #pragma unroll
         for (int h = 0; h < G; ++h) {
-          s[h] = tok ? __uint_as_float(sv[h]) : -INFINITY;
-          float x = s[h];
+          float x = -INFINITY;
+#pragma unroll
+          for (int c = 0; c < CB; ++c) {
+            s[c][h] = tok[c] ? __uint_as_float(sv[c][h]) : -INFINITY;
+            x = fmaxf(x, s[c][h]);
+          }
 #pragma unroll
           for (int o = 16; o >= 1; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
           if (lane == 0) rm[quarter * NQ + h] = x;
         }
         named_bar_sync(1, 128);
+        trace(tr, 3, gr);
         float alpha[NQ];
         bool resc = false;
 #pragma unroll
@@ -293,23 +472,28 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
         for (int h = 0; h < G; ++h) {
           const float bm = fmaxf(fmaxf(rm[h], rm[NQ + h]), fmaxf(rm[2 * NQ + h], rm[3 * NQ + h]));
           const float mnew = bm * c2;
-          if (mnew > m[h] + 8.0f) {  // block-uniform decision
+          if (mnew > m[h] + 8.0f) {  // round-uniform decision
             const float mt = fmaxf(m[h], mnew);
             alpha[h] = fast_exp2(m[h] - mt);
             m[h] = mt;
             resc = true;
           }
         }
-        float p[G];
+        float p[CB][G];
 #pragma unroll
         for (int h = 0; h < G; ++h) {
-          p[h] = tok ? fast_exp2(fmaf(s[h], c2, -m[h])) : 0.f;
-          l[h] = l[h] * alpha[h] + p[h];
+          float acc = 0.f;
+#pragma unroll
+          for (int c = 0; c < CB; ++c) {
+            p[c][h] = tok[c] ? fast_exp2(fmaf(s[c][h], c2, -m[h])) : 0.f;
+            acc += p[c][h];
+          }
+          l[h] = l[h] * alpha[h] + acc;
         }
-        // P slot `buf` was last read by PV(gbi - 2)
-        if (gbi >= 2) ptx::mbar_wait(&pv_done[buf], ((gbi - 2) >> 1) & 1);
-        if (resc && n >= 1) {  // rare: O^T column h *= alpha[h] once PV(gbi - 1) has landed
-          ptx::mbar_wait(&pv_done[buf ^ 1], ((gbi - 1) >> 1) & 1);
+        // P slot `buf` was last read by PV(gr - NSP)
+        if (gr >= (uint32_t)NSP) ptx::mbar_wait(&pv_done[buf], ((gr - NSP) / NSP) & 1);
+        if (resc && n0 > 0) {  // rare: O^T column h *= alpha[h] once PV(gr - 1) has landed
+          ptx::mbar_wait(&pv_done[(gr - 1) % NSP], ((gr - 1) / NSP) & 1);
           ptx::tc_fence_after();
           uint32_t ov[NQ];
           ptx::tmem_ld16(o_tmem, ov);
@@ -319,29 +503,39 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
           ptx::tmem_st16(o_tmem, ov);
           ptx::tmem_st_wait();
         }
-        uint8_t *sp = smem + OFF_P + buf * PTILE + (r / 64) * PPANEL;
-        const int c = (r % 64) / 8, e = r % 8;
+        const int cc = (r % 64) / 8, e = r % 8;
 #pragma unroll
-        for (int h = 0; h < G; ++h)
-          *reinterpret_cast<__nv_bfloat16 *>(sp + h * 128 + ((c ^ (h % 8)) * 16) + e * 2) = __float2bfloat16_rn(p[h]);
-        if (valid < BT) ptx::mbar_wait(&v_full[gbi % NS], (gbi / NS) & 1);  // V tile landed
-        if (!tok) {  // rows past lens[b] in the last block: zero the V row (0 * NaN would poison O)
-          uint8_t *vrow = smem + OFF_V + (gbi % NS) * TILE + r * 128;
+        for (int c = 0; c < CB; ++c) {
+          if (c >= nb) break;
+          uint8_t *sp = smem + OFF_P + (buf * CB + c) * PTILE + (r / 64) * PPANEL;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            *reinterpret_cast<uint4 *>(vrow + q * 16) = make_uint4(0, 0, 0, 0);
-            *reinterpret_cast<uint4 *>(vrow + PANEL + q * 16) = make_uint4(0, 0, 0, 0);
+          for (int h = 0; h < G; ++h)
+            *reinterpret_cast<__nv_bfloat16 *>(sp + h * 128 + ((cc ^ (h % 8)) * 16) + e * 2) =
+                __float2bfloat16_rn(p[c][h]);
+        }
+        if ((n0 + nb) * BT > len) {  // ragged last block of the item (always the round's last)
+          const uint32_t gl = gb + nb - 1;
+          ptx::mbar_wait(&v_full[gl % NS], (gl / NS) & 1);  // V tile landed
+          if (!tok[nb - 1]) {  // rows past lens[b]: zero the V row (0 * NaN would poison O)
+            uint8_t *vrow = smem + OFF_V + (gl % NS) * TILE + r * 128;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              *reinterpret_cast<uint4 *>(vrow + q * 16) = make_uint4(0, 0, 0, 0);
+              *reinterpret_cast<uint4 *>(vrow + PANEL + q * 16) = make_uint4(0, 0, 0, 0);
+            }
           }
         }
-        ptx::fence_proxy_async_smem();
+        if (!(P.debug & 1024)) ptx::fence_proxy_async_smem();
         ptx::tc_fence_before();
         ptx::warp_arrive(&p_full[buf]);
-        if (n == 0 && pend) epilogue();  // previous item's epilogue, off the critical path
+        trace(tr, 4, gr);
+        gb += nb;
+        if (n0 == 0 && pend) epilogue();  // previous item's epilogue, off the critical path
       }
       pend = true;
       pend_row0 = row0;
       pend_ob = ob;
-      pend_last = gbi - 1;
+      pend_last = gr - 1;
 #pragma unroll
       for (int h = 0; h < G; ++h) {
         pm[h] = m[h];
@@ -381,16 +575,21 @@ bool suffix_tc_supported(const hydra_heads *h) {
   return h->dtype == HYDRA_BF16 && h->head_dim == 128 && g_ok && encode_fn3() != nullptr;
 }
 
-template <int G>
-static cudaError_t launch_g(const SuffixTcParams &P, int grid, cudaStream_t s) {
+template <int G, int CB>
+static cudaError_t launch_gc(const SuffixTcParams &P, int grid, cudaStream_t s) {
   static std::once_flag once;
   static cudaError_t attr = cudaSuccess;
+  constexpr int alloc = stc::alloc_bytes(CB);
   std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(suffix_tc_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, stc::ALLOC);
+    attr = cudaFuncSetAttribute(suffix_tc_kernel<G, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, alloc);
   });
   if (attr != cudaSuccess) return attr;
-  suffix_tc_kernel<G><<<grid, stc::kThreads, stc::ALLOC, s>>>(P);
+  suffix_tc_kernel<G, CB><<<grid, stc::kThreads, alloc, s>>>(P);
   return cudaGetLastError();
+}
+template <int G>
+static cudaError_t launch_g(const SuffixTcParams &P, int cb, int grid, cudaStream_t s) {
+  return cb == 1 ? launch_gc<G, 1>(P, grid, s) : launch_gc<G, 2>(P, grid, s);
 }
 
 hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s) {
@@ -432,15 +631,17 @@ hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s)
   P.n_items = a.B * a.Hkv;
   P.o = a.o;
   P.lse = a.lse;
+  P.trace = reinterpret_cast<long long *>(a.trace);
+  P.debug = a.debug;
   if (P.n_items == 0) return HYDRA_OK;
   const int grid = n_ctas > 0 && n_ctas < P.n_items ? n_ctas : P.n_items;
   cudaError_t e = cudaErrorInvalidValue;
   switch (g) {
-    case 1: e = launch_g<1>(P, grid, s); break;
-    case 2: e = launch_g<2>(P, grid, s); break;
-    case 4: e = launch_g<4>(P, grid, s); break;
-    case 8: e = launch_g<8>(P, grid, s); break;
-    case 16: e = launch_g<16>(P, grid, s); break;
+    case 1: e = launch_g<1>(P, a.cb, grid, s); break;
+    case 2: e = launch_g<2>(P, a.cb, grid, s); break;
+    case 4: e = launch_g<4>(P, a.cb, grid, s); break;
+    case 8: e = launch_g<8>(P, a.cb, grid, s); break;
+    case 16: e = launch_g<16>(P, a.cb, grid, s); break;
   }
   return e == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
 }
