@@ -222,18 +222,19 @@ static int prefix_splits(const hydra_heads *h, int64_t B, int64_t P, int tc2_cta
 // kernels concurrently.  k prefix CTAs balance the two finish times:
 //   t_prefix(k) = pair_blocks / (k * R_P),  t_suffix(k) = kv_bytes / min((SMs-k) * R_S, BW)
 // with per-SM rates measured on B200 at C3@16K, each kernel alone on its SM share
-// (tools/overlap_var.py): R_P = 256-row x 128-token blocks per us per SM (0.46 at 48-56
-// SMs), R_S = suffix bytes per us per SM (64-72 KB/us at 92-100 SMs), BW = HBM read
-// ceiling.  Running together they interfere (HBM, L2, the 1 kW power cap), which favours
-// the prefix side: R_S is taken at the top of its range.  Candidates are multiples of the
-// prefix plan's group size so no SM is left idle.  0 = no overlap.
+// (tools/overlap_var.py, tools/overlap_sweep.py): R_P = 256-row x 128-token blocks per us
+// per SM (0.46 at 48-64 SMs), R_S = suffix bytes per us per SM (100 KB/us at 64 SMs for
+// the two-issuer tensor-core suffix, 7.0 TB/s at 80-92 SMs), BW = HBM read ceiling.
+// Candidates are multiples of the prefix plan's group size so no SM is left idle; on ties
+// (suffix-bound) the smallest k wins.  Measured at C3@16K: k = 56-60 best (0.86 ms).
+// 0 = no overlap.
 static int overlap_prefix_ctas(const hydra_heads *h, int64_t B, int64_t P, int64_t S_cap) {
   if (P <= 0 || S_cap <= 0 || !use_suffix_tc(h, B, S_cap, true)) return 0;
   const int g = h->num_q_heads / h->num_kv_heads;
   if (prefix_kind(h, B * g, P) != PK_TC2) return 0;
   const int sms = device_sm_count();
   if (g_overlap_prefix_ctas > 0) return (int)std::min<int64_t>(g_overlap_prefix_ctas, sms - 1);
-  const double R_P = 0.46, R_S = 7.2e4, BW = 7.0e6;
+  const double R_P = 0.46, R_S = 1.0e5, BW = 7.0e6;
   const int64_t pairs = (B * g + 255) / 256;
   const double pair_blocks = (double)pairs * h->num_kv_heads * ((P + 127) / 128);
   const double kv_bytes = (double)B * h->num_kv_heads * S_cap * h->head_dim * 4.0;

@@ -9,18 +9,27 @@
 //   S^T [128 tokens x 16] = K_tile [128 x 128] . Q^T        (tcgen05.mma, M=128, N=16)
 //   O^T [128 dims x 16]  += V_tile^T [128 x 128 tokens] . P^T (tcgen05.mma, A MN-major)
 // N = 16 holds the g = Hq/Hkv query heads of the KV group (zero-padded), so GQA reuses
-// every K/V byte g times.  One CTA per SM (persistent, 192 threads):
-//   warp 0     TMA producer: per item the g query rows (Q^T) and per 128-token block
-//              the K and V tiles (two 64-column SWIZZLE_128B boxes each) into a
-//              3-stage ring; reads lens[b] itself, so only blocks with valid tokens move
-//   warp 1     TMEM allocator + single-thread MMA issuer: S(0) S(1) PV(0) S(2) PV(1) ...
-//   warps 2-5  softmax: thread = token lane; per block a block max per head (warp
-//              shuffles + smem across the 4 warps), the stale-max rule of the prefix
-//              kernel (rescale only when the max grows by > 8, log2 units), P^T as bf16
-//              into shared memory (B operand of the PV MMA); epilogue per item:
-//              O^T / l with thread = head dim (coalesced stores), LSE per head.
-// Tokens >= lens[b] inside the last block: their scores are masked to -inf, and their
-// V rows are zeroed in shared memory before the PV MMA (0 * NaN would poison O).
+// every K/V byte g times.  One CTA per SM (persistent, 416 threads), one warp per job so
+// that no stage ever waits behind another kind of slot:
+//   warp 0      TMA producer, K ring (3 x 32 KB; a slot frees once its score MMA is done)
+//   warp 6      TMA producer, V ring (3 x 32 KB; a slot frees once its PV MMA is done)
+//   warp 7      TMA producer, Q^T slots (the g query rows of an item)
+//   warp 1      TMEM allocator + score-MMA issuer: S^T(n) as soon as K(n) lands and the
+//               softmax has consumed S^T slot n % 3
+//   warp 12     PV-MMA issuer: O^T += V^T P^T as soon as P^T(n) and V(n) are ready
+//   warps 2-5   softmax (thread = token lane): per round of CB blocks a block max per head
+//               (warp shuffles + smem across the 4 warps), the stale-max rule of the prefix
+//               kernel (rescale only when the max grows by > 8, log2 units), P^T as bf16
+//               into shared memory (B operand of the PV MMA)
+//   warps 8-11  epilogue (thread = head dim): O^T / l, LSE, coalesced stores, after the
+//               item's last PV -- off the softmax warps' critical path
+// Reads lens[b] itself, so only blocks with valid tokens move.  Tokens >= lens[b] inside
+// the last block: their scores are masked to -inf, and their V rows are zeroed in shared
+// memory before the PV MMA (0 * NaN would poison O).
+// Per-SM rate (tools/suffix_rate.py, C3 shape): 112 GB/s at 16 CTAs, 100 at 64; 7.0 TB/s
+// on 80-92 SMs.  The earlier single-issuer version (S(n) then PV(n-1) from one thread,
+// epilogue on the softmax warps) coupled every V slot release to the next K tile and the
+// softmax chain: 60-73 GB/s per SM (profiles/r1d_suffix_streaming.md).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -38,7 +47,8 @@ constexpr int BT = 128;   // tokens per block (UMMA M of S^T, K of PV)
 constexpr int HD = 128;   // head dim (UMMA K of S^T, M of PV)
 constexpr int NQ = 16;    // padded query heads per KV group (UMMA N)
 constexpr int NS = 3;     // K stages and V stages (separate rings: K frees after S, V after PV)
-constexpr int kThreads = 256;  // warp 0 K producer, 1 MMA, 2-5 softmax, 6 V producer, 7 Q producer
+constexpr int kThreads = 416;  // warp 0 K producer, 1 score MMA, 2-5 softmax, 6 V producer, 7 Q producer,
+                               // 8-11 epilogue, 12 PV MMA
 constexpr int PANEL = BT * 128;      // 128 rows x 128 B
 constexpr int TILE = 2 * PANEL;      // 32 KB
 constexpr int QPANEL = NQ * 128;     // 2 KB: 16 rows x 64 dims
@@ -52,18 +62,19 @@ constexpr int OFF_Q = OFF_V + NS * TILE;     // 2 slots
 // MMA, so a round's softmax is done long before its V tile lands and a V slot is held for
 // little more than the load latency (SM-budget measurements, tools/suffix_trace.py).
 // Q slots: items the score MMA may be ahead of the PV MMA, plus one.
-__host__ __device__ constexpr int nsp(int cb) { return cb == 1 ? 4 : 2; }
+__host__ __device__ constexpr int nsp(int cb) { return 3; }
 __host__ __device__ constexpr int nqs(int cb) { return cb == 1 ? 3 : 2; }
 __host__ __device__ constexpr int off_p(int cb) { return OFF_Q + nqs(cb) * QTILE; }
 __host__ __device__ constexpr int off_red(int cb) { return off_p(cb) + nsp(cb) * cb * PTILE; }
 // [2 round parity][4 warps][16] max + [2 item parity][4][16] sums
-__host__ __device__ constexpr int off_bar(int cb) { return off_red(cb) + (2 * 4 * NQ + 2 * 4 * NQ) * 4; }
-// k_full, k_empty, v_full, v_empty [NS]; q_full, q_empty [4]; s_full, p_full, pv_done [4]; o_free [2]
-constexpr int N_BARS = 4 * NS + 8 + 12 + 2;
+__host__ __device__ constexpr int off_bar(int cb) { return off_red(cb) + (2 * 4 * NQ + 2 * 4 * NQ + 2 * NQ) * 4; }
+// k_full, k_empty, v_full, v_empty [NS]; q_full, q_empty [4]; s_full, p_full, pv_done [4];
+// o_free, o_full, ml_full [2]
+constexpr int N_BARS = 4 * NS + 8 + 12 + 6;
 __host__ __device__ constexpr int alloc_bytes(int cb) { return off_bar(cb) + N_BARS * 8 + 16 + 1024; }
 static_assert(alloc_bytes(1) <= 232448 && alloc_bytes(2) <= 232448, "suffix_tc smem over the 227 KB opt-in limit");
 // S^T x 2 round slots x CB blocks (16 columns each), O^T x 2; rounded up to a power of two
-__host__ __device__ constexpr uint32_t tmem_cols(int cb) { return 128u; }  // nsp*cb*16 + 2*16 <= 96
+__host__ __device__ constexpr uint32_t tmem_cols(int cb) { return 128u; }  // nsp*cb*16 + 2*16 <= 128
 }  // namespace stc
 
 struct __align__(64) SuffixTcParams {
@@ -73,8 +84,9 @@ struct __align__(64) SuffixTcParams {
   float scale_log2;
   int32_t n_items;
   float *o, *lse;
-  int32_t debug;     // timing experiments only (invalid results): 256 = consume K/V tiles without math,
-                     // 512 = MMAs without softmax work, 1024 = no proxy fence before publishing P^T
+  int32_t debug;     // timing experiments only (invalid results): 256 = the MMA warp releases K/V
+                     // tiles as they land (no MMA, no softmax), 512 = no softmax work,
+                     // 4096 / 8192 = no score / PV MMA instructions
   long long *trace;  // diagnostics: CTA 0 event timestamps [kTraceRows][kTraceN] (tools/suffix_trace.py); null = off
 };
 namespace stc {
@@ -159,10 +171,11 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
   uint64_t *k_full = bars, *k_empty = bars + NS, *v_full = bars + 2 * NS, *v_empty = bars + 3 * NS;
   uint64_t *q_full = bars + 4 * NS, *q_empty = q_full + 4, *s_full = q_full + 8, *p_full = q_full + 12,
-           *pv_done = q_full + 16, *o_free = q_full + 20;
+           *pv_done = q_full + 16, *o_free = q_full + 20, *o_full = q_full + 22, *ml_full = q_full + 24;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + N_BARS);
   float *red_max = reinterpret_cast<float *>(smem + OFF_RED);  // [2][4][NQ]
-  float *red_sum = red_max + 2 * 4 * NQ;                        // [2][4][NQ]
+  float *red_sum = red_max + 2 * 4 * NQ;                        // [2][4][NQ] per-warp row-sum partials
+  float *item_m = red_sum + 2 * 4 * NQ;                         // [2][NQ] running max per head (log2)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   constexpr int g = G;
 
@@ -187,7 +200,11 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
       ptx::mbar_init(&p_full[i], 4);  // one elected arrival per softmax warp
       ptx::mbar_init(&pv_done[i], 1);
     }
-    for (int i = 0; i < 2; ++i) ptx::mbar_init(&o_free[i], 4);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&o_free[i], 4);   // one elected arrival per epilogue warp
+      ptx::mbar_init(&o_full[i], 1);   // tcgen05.commit after the item's last PV
+      ptx::mbar_init(&ml_full[i], 4);  // one elected arrival per softmax warp
+    }
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
@@ -227,7 +244,6 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
           if (warp == 0) {
             uint8_t *sK = smem + OFF_K + st * TILE;
             ptx::mbar_wait(&k_empty[st], ph);
-            if (P.debug & 524288) ptx::mbar_wait(&v_empty[st], ph);  // timing experiment: K issued with V
             ptx::mbar_arrive_expect_tx(&k_full[st], TILE);
             ptx::tma_load_4d(sK, &P.tmK, &k_full[st], 0, j, t0, b);
             ptx::tma_load_4d(sK + PANEL, &P.tmK, &k_full[st], 64, j, t0, b);
@@ -268,141 +284,79 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
         c.next(P);
       }
     } else if (leader) {
-      constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BT, NQ, false);                 // A=K, B=Q^T (K-major)
-      constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(HD, NQ, false) | (1u << 15);  // A=V^T (MN-major), B=P^T
+      // ================= score-MMA issuer (warp 1; the PV MMAs are issued by warp 12) =================
+      // S(n) needs K(n) landed and S^T slot n % NSP consumed by the softmax (p_full of round
+      // n - NSP).  Two issuing threads, each blocking on one barrier at a time: a score MMA
+      // never waits behind a V tile and a PV MMA never waits behind a K tile.
+      constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BT, NQ, false);  // A=K, B=Q^T (K-major)
       long long *tr = blockIdx.x == 0 ? P.trace : nullptr;
-      // timing experiment 32768 (only with the MMAs skipped): plain arrivals instead of commits
-      auto commit_ = [&](uint64_t *bar) {
-        if (P.debug & 32768) ptx::mbar_arrive(bar);
-        else ptx::mma_commit(bar);
-      };
-      auto poll_ = [&](uint64_t *bar, uint32_t ph) {  // 131072: suspending try_wait (timing experiment)
-        return (P.debug & 131072) ? ptx::mbar_try_wait(bar, ph) : ptx::mbar_test_wait(bar, ph);
-      };
-      RoundCursor<CB> sc, pc;
+      RoundCursor<CB> sc;
       sc.init(P);
-      pc.init(P);
-      uint32_t s_c = 0, p_c = 0;  // blocks of the current round already issued (S / PV cursor)
-      bool p_ready = false;       // PV cursor: P^T (and O^T) of the current round available
-      while (pc.valid) {
-        const uint32_t mark = sc.gr * 8 + s_c + pc.gr * 4096 + p_c * 512;
-        // ---- S cursor
-        if (sc.valid && sc.gr < pc.gr + NSP) {
-          const uint32_t qs = sc.qi % NQS;
-          if (s_c < (uint32_t)sc.nb && poll_(&q_full[qs], (sc.qi / NQS) & 1)) {
-            const uint32_t q_addr = ptx::smem_u32(smem + OFF_Q + qs * QTILE);
-            while (s_c < (uint32_t)sc.nb) {
-              const uint32_t gbc = sc.gb + s_c, st = gbc % NS;
-              if (!poll_(&k_full[st], (gbc / NS) & 1)) break;
-              trace(tr, 11, gbc);
-              if (!(P.debug & (1 << 20))) ptx::tc_fence_after();
-              const uint32_t k_addr = ptx::smem_u32(smem + OFF_K + st * TILE);
+      while (sc.valid) {
+        if (sc.gr >= (uint32_t)NSP) ptx::mbar_wait(&p_full[sc.gr % NSP], ((sc.gr - NSP) / NSP) & 1);
+        const uint32_t qs = sc.qi % NQS;
+        if (sc.n0 == 0) ptx::mbar_wait(&q_full[qs], (sc.qi / NQS) & 1);
+        const uint32_t q_addr = ptx::smem_u32(smem + OFF_Q + qs * QTILE);
+        for (int c = 0; c < sc.nb; ++c) {
+          const uint32_t gbc = sc.gb + c, st = gbc % NS;
+          ptx::mbar_wait(&k_full[st], (gbc / NS) & 1);
+          trace(tr, 11, gbc);
+          ptx::tc_fence_after();
+          const uint32_t k_addr = ptx::smem_u32(smem + OFF_K + st * TILE);
 #pragma unroll
-              for (int kk = 0; kk < HD / 16; ++kk) {
-                if (P.debug & 4096) break;  // timing experiment only: no score MMAs
-                const uint32_t off = (kk / 4) * PANEL + (kk % 4) * 32, qoff = (kk / 4) * QPANEL + (kk % 4) * 32;
-                ptx::mma_ss(tmem + ((sc.gr % NSP) * CB + s_c) * NQ, ptx::smem_desc_sw128(k_addr + off, 16, 1024),
-                            ptx::smem_desc_sw128(q_addr + qoff, 16, 1024), idesc_s, kk > 0);
-              }
-              commit_(&k_empty[st]);
-              ++s_c;
-            }
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint32_t off = (kk / 4) * PANEL + (kk % 4) * 32, qoff = (kk / 4) * QPANEL + (kk % 4) * 32;
+            ptx::mma_ss(tmem + ((sc.gr % NSP) * CB + c) * NQ, ptx::smem_desc_sw128(k_addr + off, 16, 1024),
+                        ptx::smem_desc_sw128(q_addr + qoff, 16, 1024), idesc_s, kk > 0);
           }
-          if (s_c == (uint32_t)sc.nb) {
-            commit_(&s_full[sc.gr % NSP]);
-            if (P.debug & 65536)  // timing experiment only: no softmax warps; stand in for their arrivals
-              for (int w = 0; w < 4; ++w) ptx::mbar_arrive(&p_full[sc.gr % NSP]);
-            trace(tr, 7, sc.gr);
-            sc.next(P);
-            s_c = 0;
-          }
+          ptx::mma_commit(&k_empty[st]);
         }
-        // ---- PV cursor (only rounds whose S was issued)
-        if (pc.gr < sc.gr || !sc.valid) {
-          const uint32_t slot = pc.gr % NSP;
-          if (!p_ready) {
-            p_ready = poll_(&p_full[slot], (pc.gr / NSP) & 1) &&
-                      (pc.n0 > 0 || poll_(&o_free[pc.item_no & 1], ((pc.item_no >> 1) & 1) ^ 1));
-          }
-          if (p_ready) {
-            const uint32_t p_base = ptx::smem_u32(smem + OFF_P + slot * CB * PTILE);
-            const uint32_t ob = pc.item_no & 1;
-            while (p_c < (uint32_t)pc.nb) {
-              const uint32_t gbc = pc.gb + p_c, st = gbc % NS;
-              if (!poll_(&v_full[st], (gbc / NS) & 1)) break;
-              trace(tr, 12, gbc);
-              if (!(P.debug & (1 << 20))) ptx::tc_fence_after();
-              const uint32_t v_addr = ptx::smem_u32(smem + OFF_V + st * TILE);
-              const uint32_t p_addr = p_base + p_c * PTILE;
-#pragma unroll
-              for (int kk = 0; kk < BT / 16; ++kk)
-                if (!(P.debug & 8192))  // timing experiment only: no PV MMAs
-                ptx::mma_ss(tmem + O_COL + ob * NQ, ptx::smem_desc_sw128(v_addr + kk * 2048, PANEL, 1024),
-                            ptx::smem_desc_sw128(p_addr + (kk / 4) * PPANEL + (kk % 4) * 32, 16, 1024), idesc_pv,
-                            (pc.n0 > 0 || p_c > 0 || kk > 0));
-              commit_(&v_empty[st]);
-              ++p_c;
-            }
-            if (p_c == (uint32_t)pc.nb) {
-              commit_(&pv_done[slot]);
-              trace(tr, 8, pc.gr);
-              if (pc.n0 + pc.nb >= pc.nblk) {
-                commit_(&q_empty[pc.qi % NQS]);
-                if (P.debug & 65536)
-                  for (int w = 0; w < 4; ++w) ptx::mbar_arrive(&o_free[pc.item_no & 1]);
-              }
-              pc.next(P);
-              p_c = 0;
-              p_ready = false;
-            }
-          }
-        }
-        if ((P.debug & 16384) && mark == sc.gr * 8 + s_c + pc.gr * 4096 + p_c * 512) __nanosleep((P.debug & 262144) ? 1000 : 64);
+        ptx::mma_commit(&s_full[sc.gr % NSP]);
+        if (sc.n0 + sc.nb >= sc.nblk) ptx::mma_commit(&q_empty[qs]);  // the item's last score MMA
+        trace(tr, 7, sc.gr);
+        sc.next(P);
       }
     }
-  } else if (!(P.debug & (256 | 65536))) {
-    // ================= softmax (thread = token lane) / lagged epilogue (thread = head dim) =================
+  } else if (warp == 12) {
+    // ================= PV-MMA issuer =================
+    if (ptx::elect_one() && !(P.debug & 256)) {
+      constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(HD, NQ, false) | (1u << 15);  // A=V^T (MN-major), B=P^T
+      long long *tr = blockIdx.x == 0 ? P.trace : nullptr;
+      RoundCursor<CB> pc;
+      pc.init(P);
+      while (pc.valid) {
+        const uint32_t slot = pc.gr % NSP, ob = pc.item_no & 1;
+        ptx::mbar_wait(&p_full[slot], (pc.gr / NSP) & 1);
+        if (pc.n0 == 0) ptx::mbar_wait(&o_free[ob], ((pc.item_no >> 1) & 1) ^ 1);
+        const uint32_t p_base = ptx::smem_u32(smem + OFF_P + slot * CB * PTILE);
+        for (int c = 0; c < pc.nb; ++c) {
+          const uint32_t gbc = pc.gb + c, st = gbc % NS;
+          ptx::mbar_wait(&v_full[st], (gbc / NS) & 1);
+          trace(tr, 12, gbc);
+          ptx::tc_fence_after();
+          const uint32_t v_addr = ptx::smem_u32(smem + OFF_V + st * TILE);
+          const uint32_t p_addr = p_base + c * PTILE;
+#pragma unroll
+          for (int kk = 0; kk < BT / 16; ++kk)
+            ptx::mma_ss(tmem + O_COL + ob * NQ, ptx::smem_desc_sw128(v_addr + kk * 2048, PANEL, 1024),
+                        ptx::smem_desc_sw128(p_addr + (kk / 4) * PPANEL + (kk % 4) * 32, 16, 1024), idesc_pv,
+                        (pc.n0 > 0 || c > 0 || kk > 0));
+          ptx::mma_commit(&v_empty[st]);
+        }
+        ptx::mma_commit(&pv_done[slot]);
+        trace(tr, 8, pc.gr);
+        if (pc.n0 + pc.nb >= pc.nblk) ptx::mma_commit(&o_full[ob]);
+        pc.next(P);
+      }
+    }
+  } else if (warp < 8 && !(P.debug & 256)) {
+    // ================= softmax (thread = token lane) =================
     const int quarter = warp % 4;
     const int r = quarter * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const float c2 = P.scale_log2;
-    uint32_t gr = 0, gb = 0, item_no = 0, n_epi = 0;
+    uint32_t gr = 0, gb = 0, item_no = 0;
     long long *tr = (blockIdx.x == 0 && quarter == 0 && lane == 0) ? P.trace : nullptr;
-    // state of the item whose epilogue is pending (run after the next item's first round)
-    bool pend = false;
-    int64_t pend_row0 = 0;
-    uint32_t pend_ob = 0, pend_last = 0;
-    float pm[G], pl[G];
-    auto epilogue = [&]() {
-      trace(tr, 5, n_epi);
-      ptx::mbar_wait(&pv_done[pend_last % NSP], (pend_last / NSP) & 1);
-      ptx::tc_fence_after();
-      // two epilogues can run back to back (the lagged one and the final one): alternate
-      // the reduction buffer by item parity so a fast warp never overwrites sums a slow
-      // warp is still reading
-      float *rs = red_sum + pend_ob * 4 * NQ;
-#pragma unroll
-      for (int h = 0; h < G; ++h) {
-        float x = pl[h];
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-        if (lane == 0) rs[quarter * NQ + h] = x;
-      }
-      named_bar_sync(1, 128);
-      uint32_t ov[NQ];
-      ptx::tmem_ld16(tmem + lane_base + O_COL + pend_ob * NQ, ov);
-      ptx::tmem_ld_wait();
-      ptx::tc_fence_before();
-      ptx::warp_arrive(&o_free[pend_ob]);
-#pragma unroll
-      for (int h = 0; h < G; ++h) {
-        const float L = rs[h] + rs[NQ + h] + rs[2 * NQ + h] + rs[3 * NQ + h];
-        P.o[(pend_row0 + h) * HD + r] = __uint_as_float(ov[h]) / L;
-        if (r == h) P.lse[pend_row0 + h] = (pm[h] + log2f(L)) * HYDRA_LN2;
-      }
-      trace(tr, 6, n_epi++);
-      pend = false;
-    };
     int len_next = item_len(P, blockIdx.x);
     for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
       const int b = item / P.Hkv, j = item % P.Hkv;
@@ -436,7 +390,6 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
           if (gr >= (uint32_t)NSP) ptx::mbar_wait(&pv_done[buf], ((gr - NSP) / NSP) & 1);
           ptx::warp_arrive(&p_full[buf]);
           gb += nb;
-          if (n0 == 0 && pend) epilogue();
           continue;
         }
         uint32_t sv[CB][NQ];
@@ -525,25 +478,63 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
             }
           }
         }
-        if (!(P.debug & 1024)) ptx::fence_proxy_async_smem();
+        ptx::fence_proxy_async_smem();
         ptx::tc_fence_before();
         ptx::warp_arrive(&p_full[buf]);
         trace(tr, 4, gr);
         gb += nb;
-        if (n0 == 0 && pend) epilogue();  // previous item's epilogue, off the critical path
       }
-      pend = true;
-      pend_row0 = row0;
-      pend_ob = ob;
-      pend_last = gr - 1;
+      // hand (m, row-sum partials) to the epilogue warps; slot ob was last read by the
+      // epilogue of item item_no - 2
+      ptx::mbar_wait(&o_free[ob], ((item_no >> 1) & 1) ^ 1);
+      float *rs = red_sum + ob * 4 * NQ;
 #pragma unroll
       for (int h = 0; h < G; ++h) {
-        pm[h] = m[h];
-        pl[h] = l[h];
+        float x = l[h];
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) rs[quarter * NQ + h] = x;
+        if (r == 0) item_m[ob * NQ + h] = m[h];
+      }
+      ptx::warp_arrive(&ml_full[ob]);
+      ++item_no;
+    }
+  } else if (warp >= 8 && !(P.debug & 256)) {
+    // ================= epilogue (thread = head dim): O = O^T / l, LSE =================
+    const int quarter = warp % 4;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    uint32_t item_no = 0;
+    int len_next = item_len(P, blockIdx.x);
+    for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+      const int len = len_next;
+      len_next = item_len(P, item + gridDim.x);
+      if (len <= 0) continue;
+      const int b = item / P.Hkv, j = item % P.Hkv;
+      const int64_t row0 = (int64_t)b * P.Hq + (int64_t)j * g;
+      const uint32_t ob = item_no & 1, ph = (item_no >> 1) & 1;
+      ptx::mbar_wait(&o_full[ob], ph);
+      ptx::mbar_wait(&ml_full[ob], ph);
+      ptx::tc_fence_after();
+      uint32_t ov[NQ];
+      ptx::tmem_ld16(tmem + lane_base + O_COL + ob * NQ, ov);
+      ptx::tmem_ld_wait();
+      const float *rs = red_sum + ob * 4 * NQ;
+      float L[G], M[G];
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        L[h] = rs[h] + rs[NQ + h] + rs[2 * NQ + h] + rs[3 * NQ + h];
+        M[h] = item_m[ob * NQ + h];
+      }
+      ptx::tc_fence_before();
+      ptx::warp_arrive(&o_free[ob]);  // O^T buffer and (m, l) slot free
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        P.o[(row0 + h) * HD + r] = __uint_as_float(ov[h]) / L[h];
+        if (r == h) P.lse[row0 + h] = (M[h] + log2f(L[h])) * HYDRA_LN2;
       }
       ++item_no;
     }
-    if (pend) epilogue();
   }
 
   ptx::tc_fence_before();
@@ -641,7 +632,7 @@ hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s)
     case 2: e = launch_g<2>(P, a.cb, grid, s); break;
     case 4: e = launch_g<4>(P, a.cb, grid, s); break;
     case 8: e = launch_g<8>(P, a.cb, grid, s); break;
-    case 16: e = launch_g<16>(P, a.cb, grid, s); break;
+    case 16: e = launch_g<16>(P, 1, grid, s); break;  // CB = 2 would spill at G = 16
   }
   return e == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
 }
