@@ -41,7 +41,7 @@ static hydra_status cuda_fail(const char *what) {
 
 static std::atomic<int64_t> g_prefix_impl{0}, g_prefix_splits{0}, g_suffix_splits{0}, g_tc_debug{0},
     g_prefix_stages{3}, g_suffix_unroll{4}, g_prefix_ctas{0}, g_suffix_impl{0}, g_suffix_ctas{0},
-    g_overlap_prefix_ctas{0}, g_prefix_poly{0}, g_prefix_variant{3}, g_prefix_trace{0},
+    g_overlap_prefix_ctas{0}, g_prefix_poly{0}, g_prefix_variant{3}, g_prefix_trace{0}, g_suffix_cb{2}, g_suffix_trace{0},
     g_last_overlap_k{0};  // read-only: prefix CTAs of the last hydra_attn overlap split (0 = sequential)
 
 extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
@@ -58,6 +58,8 @@ extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
   else if (!strcmp(key, "prefix_poly")) g_prefix_poly = (value == 0 || value == 3 || value == 8 || value == -1) ? value : 4;
   else if (!strcmp(key, "prefix_variant")) g_prefix_variant = (value == 4 || value == 5) ? value : 3;
   else if (!strcmp(key, "prefix_stages")) g_prefix_stages = (value == 2 ? 2 : 3);
+  else if (!strcmp(key, "suffix_trace")) g_suffix_trace = value;
+  else if (!strcmp(key, "suffix_cb")) g_suffix_cb = (value == 1 ? 1 : 2);
   else if (!strcmp(key, "suffix_unroll")) g_suffix_unroll = (value >= 8 ? 8 : value >= 4 ? 4 : 2);
   else return fail(HYDRA_EINVAL, "unknown config key '%s'", key);
   return HYDRA_OK;
@@ -79,6 +81,8 @@ extern "C" int64_t hydra_get_config(const char *key) {
   if (!strcmp(key, "prefix_poly")) return g_prefix_poly;
   if (!strcmp(key, "prefix_variant")) return g_prefix_variant;
   if (!strcmp(key, "suffix_unroll")) return g_suffix_unroll;
+  if (!strcmp(key, "suffix_cb")) return g_suffix_cb;
+  if (!strcmp(key, "suffix_trace")) return g_suffix_trace;
   return -1;
 }
 
@@ -218,18 +222,19 @@ static int prefix_splits(const hydra_heads *h, int64_t B, int64_t P, int tc2_cta
 // kernels concurrently.  k prefix CTAs balance the two finish times:
 //   t_prefix(k) = pair_blocks / (k * R_P),  t_suffix(k) = kv_bytes / min((SMs-k) * R_S, BW)
 // with per-SM rates measured on B200 at C3@16K, each kernel alone on its SM share
-// (tools/overlap_var.py): R_P = 256-row x 128-token blocks per us per SM (0.46 at 48-56
-// SMs), R_S = suffix bytes per us per SM (64-72 KB/us at 92-100 SMs), BW = HBM read
-// ceiling.  Running together they interfere (HBM, L2, the 1 kW power cap), which favours
-// the prefix side: R_S is taken at the top of its range.  Candidates are multiples of the
-// prefix plan's group size so no SM is left idle.  0 = no overlap.
+// (tools/overlap_var.py, tools/overlap_sweep.py): R_P = 256-row x 128-token blocks per us
+// per SM (0.46 at 48-64 SMs), R_S = suffix bytes per us per SM (100 KB/us at 64 SMs for
+// the two-issuer tensor-core suffix, 7.0 TB/s at 80-92 SMs), BW = HBM read ceiling.
+// Candidates are multiples of the prefix plan's group size so no SM is left idle; on ties
+// (suffix-bound) the smallest k wins.  Measured at C3@16K: k = 56-60 best (0.86 ms).
+// 0 = no overlap.
 static int overlap_prefix_ctas(const hydra_heads *h, int64_t B, int64_t P, int64_t S_cap) {
   if (P <= 0 || S_cap <= 0 || !use_suffix_tc(h, B, S_cap, true)) return 0;
   const int g = h->num_q_heads / h->num_kv_heads;
   if (prefix_kind(h, B * g, P) != PK_TC2) return 0;
   const int sms = device_sm_count();
   if (g_overlap_prefix_ctas > 0) return (int)std::min<int64_t>(g_overlap_prefix_ctas, sms - 1);
-  const double R_P = 0.46, R_S = 7.2e4, BW = 7.0e6;
+  const double R_P = 0.46, R_S = 1.0e5, BW = 7.0e6;
   const int64_t pairs = (B * g + 255) / 256;
   const double pair_blocks = (double)pairs * h->num_kv_heads * ((P + 127) / 128);
   const double kv_bytes = (double)B * h->num_kv_heads * S_cap * h->head_dim * 4.0;
@@ -359,6 +364,9 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
     a.scale_log2 = scale_of(h) * 1.4426950408889634f;
     a.o = dst.o;
     a.lse = dst.lse;
+    a.cb = (int32_t)g_suffix_cb;
+    a.trace = reinterpret_cast<void *>((intptr_t)g_suffix_trace.load());
+    a.debug = (int32_t)g_tc_debug;
     const int ctas = tc_ctas > 0 ? tc_ctas : (g_suffix_ctas > 0 ? (int)g_suffix_ctas : device_sm_count());
     hydra_status st = launch_suffix_tc(a, ctas, s);
     return st == HYDRA_OK ? st : cuda_fail("suffix tcgen05 launch");

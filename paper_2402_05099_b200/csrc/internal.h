@@ -102,6 +102,9 @@ struct SuffixTcArgs {
   int32_t B, Hq, Hkv;
   float scale_log2;
   float *o, *lse;  // [B, Hq, 128], [B, Hq]
+  int32_t cb;      // 128-token blocks per softmax round (1 or 2)
+  void *trace;     // diagnostics (suffix_trace config key); null = off
+  int32_t debug;   // tc_debug_variant (timing experiments only)
 };
 bool suffix_tc_supported(const hydra_heads *h);
 hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s);

@@ -9,18 +9,27 @@
 //   S^T [128 tokens x 16] = K_tile [128 x 128] . Q^T        (tcgen05.mma, M=128, N=16)
 //   O^T [128 dims x 16]  += V_tile^T [128 x 128 tokens] . P^T (tcgen05.mma, A MN-major)
 // N = 16 holds the g = Hq/Hkv query heads of the KV group (zero-padded), so GQA reuses
-// every K/V byte g times.  One CTA per SM (persistent, 192 threads):
-//   warp 0     TMA producer: per item the g query rows (Q^T) and per 128-token block
-//              the K and V tiles (two 64-column SWIZZLE_128B boxes each) into a
-//              3-stage ring; reads lens[b] itself, so only blocks with valid tokens move
-//   warp 1     TMEM allocator + single-thread MMA issuer: S(0) S(1) PV(0) S(2) PV(1) ...
-//   warps 2-5  softmax: thread = token lane; per block a block max per head (warp
-//              shuffles + smem across the 4 warps), the stale-max rule of the prefix
-//              kernel (rescale only when the max grows by > 8, log2 units), P^T as bf16
-//              into shared memory (B operand of the PV MMA); epilogue per item:
-//              O^T / l with thread = head dim (coalesced stores), LSE per head.
-// Tokens >= lens[b] inside the last block: their scores are masked to -inf, and their
-// V rows are zeroed in shared memory before the PV MMA (0 * NaN would poison O).
+// every K/V byte g times.  One CTA per SM (persistent, 416 threads), one warp per job so
+// that no stage ever waits behind another kind of slot:
+//   warp 0      TMA producer, K ring (3 x 32 KB; a slot frees once its score MMA is done)
+//   warp 6      TMA producer, V ring (3 x 32 KB; a slot frees once its PV MMA is done)
+//   warp 7      TMA producer, Q^T slots (the g query rows of an item)
+//   warp 1      TMEM allocator + score-MMA issuer: S^T(n) as soon as K(n) lands and the
+//               softmax has consumed S^T slot n % 3
+//   warp 12     PV-MMA issuer: O^T += V^T P^T as soon as P^T(n) and V(n) are ready
+//   warps 2-5   softmax (thread = token lane): per round of CB blocks a block max per head
+//               (warp shuffles + smem across the 4 warps), the stale-max rule of the prefix
+//               kernel (rescale only when the max grows by > 8, log2 units), P^T as bf16
+//               into shared memory (B operand of the PV MMA)
+//   warps 8-11  epilogue (thread = head dim): O^T / l, LSE, coalesced stores, after the
+//               item's last PV -- off the softmax warps' critical path
+// Reads lens[b] itself, so only blocks with valid tokens move.  Tokens >= lens[b] inside
+// the last block: their scores are masked to -inf, and their V rows are zeroed in shared
+// memory before the PV MMA (0 * NaN would poison O).
+// Per-SM rate (tools/suffix_rate.py, C3 shape): 112 GB/s at 16 CTAs, 100 at 64; 7.0 TB/s
+// on 80-92 SMs.  The earlier single-issuer version (S(n) then PV(n-1) from one thread,
+// epilogue on the softmax warps) coupled every V slot release to the next K tile and the
+// softmax chain: 60-73 GB/s per SM (profiles/r1d_suffix_streaming.md).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -38,24 +47,34 @@ constexpr int BT = 128;   // tokens per block (UMMA M of S^T, K of PV)
 constexpr int HD = 128;   // head dim (UMMA K of S^T, M of PV)
 constexpr int NQ = 16;    // padded query heads per KV group (UMMA N)
 constexpr int NS = 3;     // K stages and V stages (separate rings: K frees after S, V after PV)
-constexpr int kThreads = 192;
+constexpr int kThreads = 416;  // warp 0 K producer, 1 score MMA, 2-5 softmax, 6 V producer, 7 Q producer,
+                               // 8-11 epilogue, 12 PV MMA
 constexpr int PANEL = BT * 128;      // 128 rows x 128 B
 constexpr int TILE = 2 * PANEL;      // 32 KB
 constexpr int QPANEL = NQ * 128;     // 2 KB: 16 rows x 64 dims
 constexpr int QTILE = 2 * QPANEL;    // 4 KB
 constexpr int PPANEL = NQ * 128;     // P^T: 16 rows x 64 tokens
-constexpr int PTILE = 2 * PPANEL;    // 4 KB
+constexpr int PTILE = 2 * PPANEL;    // 4 KB per 128-token block
 constexpr int OFF_K = 0;
 constexpr int OFF_V = OFF_K + NS * TILE;
 constexpr int OFF_Q = OFF_V + NS * TILE;     // 2 slots
-constexpr int OFF_P = OFF_Q + 2 * QTILE;     // 2 slots
-constexpr int OFF_RED = OFF_P + 2 * PTILE;   // [2 block parity][4 warps][16] max + [2 item parity][4][16] sums
-constexpr int OFF_BAR = OFF_RED + (2 * 4 * NQ + 2 * 4 * NQ) * 4;
-// k_full, k_empty, v_full, v_empty [NS]; q_full, q_empty, s_full, p_full, o_free, pv_done [2]
-constexpr int N_BARS = 4 * NS + 12;
-constexpr int BYTES = OFF_BAR + N_BARS * 8 + 16;
-constexpr int ALLOC = BYTES + 1024;
-constexpr uint32_t TMEM_COLS = 64;  // S^T x2 (16 cols each), O^T x2
+// Round slots (S^T in TMEM, P^T in smem): the score MMA may run nsp rounds ahead of the PV
+// MMA, so a round's softmax is done long before its V tile lands and a V slot is held for
+// little more than the load latency (SM-budget measurements, tools/suffix_trace.py).
+// Q slots: items the score MMA may be ahead of the PV MMA, plus one.
+__host__ __device__ constexpr int nsp(int cb) { return 3; }
+__host__ __device__ constexpr int nqs(int cb) { return cb == 1 ? 3 : 2; }
+__host__ __device__ constexpr int off_p(int cb) { return OFF_Q + nqs(cb) * QTILE; }
+__host__ __device__ constexpr int off_red(int cb) { return off_p(cb) + nsp(cb) * cb * PTILE; }
+// [2 round parity][4 warps][16] max + [2 item parity][4][16] sums
+__host__ __device__ constexpr int off_bar(int cb) { return off_red(cb) + (2 * 4 * NQ + 2 * 4 * NQ + 2 * NQ) * 4; }
+// k_full, k_empty, v_full, v_empty [NS]; q_full, q_empty [4]; s_full, p_full, pv_done [4];
+// o_free, o_full, ml_full [2]
+constexpr int N_BARS = 4 * NS + 8 + 12 + 6;
+__host__ __device__ constexpr int alloc_bytes(int cb) { return off_bar(cb) + N_BARS * 8 + 16 + 1024; }
+static_assert(alloc_bytes(1) <= 232448 && alloc_bytes(2) <= 232448, "suffix_tc smem over the 227 KB opt-in limit");
+// S^T x 2 round slots x CB blocks (16 columns each), O^T x 2; rounded up to a power of two
+__host__ __device__ constexpr uint32_t tmem_cols(int cb) { return 128u; }  // nsp*cb*16 + 2*16 <= 128
 }  // namespace stc
 
 struct __align__(64) SuffixTcParams {
@@ -65,29 +84,103 @@ struct __align__(64) SuffixTcParams {
   float scale_log2;
   int32_t n_items;
   float *o, *lse;
+  int32_t debug;     // timing experiments only (invalid results): 256 = the MMA warp releases K/V
+                     // tiles as they land (no MMA, no softmax), 512 = no softmax work,
+                     // 4096 / 8192 = no score / PV MMA instructions
+  long long *trace;  // diagnostics: CTA 0 event timestamps [kTraceRows][kTraceN] (tools/suffix_trace.py); null = off
 };
+namespace stc {
+constexpr int kTraceN = 1024;
+// trace rows: 0 softmax s_full wait begin, 1 s_full acquired, 2 scores loaded, 3 block max done,
+// 4 P^T published (p_full arrive), 5 epilogue begin, 6 epilogue end, 7 MMA S round committed,
+// 8 MMA PV round committed, 9 K TMA issued (block), 10 V TMA issued (block), 11 / 12 MMA thread
+// sees K / V landed (block)
+__device__ __forceinline__ void trace(long long *tr, int row, uint32_t i) {
+  if (tr && i < (uint32_t)kTraceN) tr[row * kTraceN + i] = clock64();
+}
+}  // namespace stc
 
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <int G>  // query heads per KV group (compile-time: no per-head predicates)
+// lens[b] of the item this CTA handles `k` steps ahead (0 when past the end): every role
+// fetches the next item's length one item early so the load is off the critical path.
+__device__ __forceinline__ int item_len(const SuffixTcParams &P, int item) {
+  return item < P.n_items ? __ldg(P.lens + item / P.Hkv) : 0;
+}
+
+// Walks the rounds (up to CB consecutive 128-token blocks of one item) a CTA processes, in
+// order, with the ring positions the producers use: gb = first block's ring index, gr =
+// round index, qi / item_no = index of the item among this CTA's non-empty items.
+template <int CB>
+struct RoundCursor {
+  int item, len, len_next, nblk, n0, nb;
+  uint32_t gb, gr, qi, item_no;
+  bool valid;
+  __device__ __forceinline__ void seek(const SuffixTcParams &P) {  // first round of the next non-empty item
+    while (item < P.n_items) {
+      len = len_next;
+      len_next = item_len(P, item + gridDim.x);
+      nblk = (len + stc::BT - 1) / stc::BT;
+      if (nblk > 0) {
+        n0 = 0;
+        nb = min(CB, nblk);
+        valid = true;
+        return;
+      }
+      item += gridDim.x;
+    }
+    valid = false;
+  }
+  __device__ __forceinline__ void init(const SuffixTcParams &P) {
+    item = blockIdx.x;
+    len_next = item_len(P, item);
+    gb = gr = qi = item_no = 0;
+    seek(P);
+  }
+  __device__ __forceinline__ void next(const SuffixTcParams &P) {
+    gb += nb;
+    ++gr;
+    n0 += nb;
+    if (n0 < nblk) {
+      nb = min(CB, nblk - n0);
+      return;
+    }
+    ++qi;
+    ++item_no;
+    item += gridDim.x;
+    seek(P);
+  }
+};
+
+// G = query heads per KV group (compile-time: no per-head predicates).
+// CB = 128-token blocks per softmax round: the softmax warps take one block max / barrier /
+// P^T write per round of up to CB blocks (thread r owns tokens r, 128 + r, ...), so the
+// per-round latency chain (S MMA -> TMEM load -> cross-warp max -> exp -> P^T -> PV MMA)
+// is paid once per CB blocks.  Online softmax across the rounds of an item.
+template <int G, int CB>
 __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __grid_constant__ SuffixTcParams P) {
   using namespace stc;
+  constexpr int OFF_P = off_p(CB), OFF_RED = off_red(CB), OFF_BAR = off_bar(CB);
+  constexpr int NSP = nsp(CB), NQS = nqs(CB);
+  constexpr uint32_t TMEM_COLS = tmem_cols(CB);
+  constexpr uint32_t O_COL = NSP * CB * NQ;  // O^T buffers start after the S^T round slots
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
   uint64_t *k_full = bars, *k_empty = bars + NS, *v_full = bars + 2 * NS, *v_empty = bars + 3 * NS;
-  uint64_t *q_full = bars + 4 * NS, *q_empty = q_full + 2, *s_full = q_full + 4, *p_full = q_full + 6,
-           *o_free = q_full + 8, *pv_done = q_full + 10;
+  uint64_t *q_full = bars + 4 * NS, *q_empty = q_full + 4, *s_full = q_full + 8, *p_full = q_full + 12,
+           *pv_done = q_full + 16, *o_free = q_full + 20, *o_full = q_full + 22, *ml_full = q_full + 24;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + N_BARS);
   float *red_max = reinterpret_cast<float *>(smem + OFF_RED);  // [2][4][NQ]
-  float *red_sum = red_max + 2 * 4 * NQ;                        // [2][4][NQ]
+  float *red_sum = red_max + 2 * 4 * NQ;                        // [2][4][NQ] per-warp row-sum partials
+  float *item_m = red_sum + 2 * 4 * NQ;                         // [2][NQ] running max per head (log2)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   constexpr int g = G;
 
   // zero Q^T / P^T slots once: rows >= g (padding heads) must stay 0 forever
-  for (int i = threadIdx.x; i < (2 * QTILE + 2 * PTILE) / 16; i += kThreads)
+  for (int i = threadIdx.x; i < (NQS * QTILE + NSP * CB * PTILE) / 16; i += kThreads)
     reinterpret_cast<uint4 *>(smem + OFF_Q)[i] = make_uint4(0, 0, 0, 0);
   ptx::fence_proxy_async_smem();
   if (warp == 0 && lane == 0) {
@@ -100,13 +193,17 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
       ptx::mbar_init(&v_full[i], 1);
       ptx::mbar_init(&v_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 4; ++i) {
       ptx::mbar_init(&q_full[i], 1);
       ptx::mbar_init(&q_empty[i], 1);
       ptx::mbar_init(&s_full[i], 1);
       ptx::mbar_init(&p_full[i], 4);  // one elected arrival per softmax warp
-      ptx::mbar_init(&o_free[i], 4);
       ptx::mbar_init(&pv_done[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&o_free[i], 4);   // one elected arrival per epilogue warp
+      ptx::mbar_init(&o_full[i], 1);   // tcgen05.commit after the item's last PV
+      ptx::mbar_init(&ml_full[i], 4);  // one elected arrival per softmax warp
     }
     ptx::fence_mbar_init();
   }
@@ -116,138 +213,155 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    // ================= TMA producer =================
+  if (warp == 0 || warp == 6 || warp == 7) {
+    // ================= TMA producers: warp 0 K ring, warp 6 V ring, warp 7 Q slots =================
+    // Separate threads so no load waits behind another kind of slot (V slots free only after
+    // the PV MMA, K slots right after the score MMA, Q slots after an item's last PV).
     if (ptx::elect_one()) {
+      long long *tr = blockIdx.x == 0 ? P.trace : nullptr;
       uint32_t gb = 0, qi = 0;
+      int len_next = item_len(P, blockIdx.x);
       for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
         const int b = item / P.Hkv, j = item % P.Hkv;
-        const int len = P.lens[b];
+        const int len = len_next;
+        len_next = item_len(P, item + gridDim.x);
         const int nblk = (len + BT - 1) / BT;
         if (nblk == 0) continue;
-        const int qs = qi & 1;
-        ptx::mbar_wait(&q_empty[qs], ((qi >> 1) & 1) ^ 1);
-        ptx::mbar_arrive_expect_tx(&q_full[qs], 2 * 64 * g * 2);
-        uint8_t *sQ = smem + OFF_Q + qs * QTILE;
-        ptx::tma_load_3d(sQ, &P.tmQ, &q_full[qs], 0, j * g, b);
-        ptx::tma_load_3d(sQ + QPANEL, &P.tmQ, &q_full[qs], 64, j * g, b);
-        ++qi;
+        if (warp == 7) {
+          const int qs = qi % NQS;
+          ptx::mbar_wait(&q_empty[qs], ((qi / NQS) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&q_full[qs], 2 * 64 * g * 2);
+          uint8_t *sQ = smem + OFF_Q + qs * QTILE;
+          ptx::tma_load_3d(sQ, &P.tmQ, &q_full[qs], 0, j * g, b);
+          ptx::tma_load_3d(sQ + QPANEL, &P.tmQ, &q_full[qs], 64, j * g, b);
+          ++qi;
+          continue;
+        }
         for (int n = 0; n < nblk; ++n, ++gb) {
           const int st = gb % NS;
           const uint32_t ph = ((gb / NS) & 1) ^ 1;
-          uint8_t *sK = smem + OFF_K + st * TILE, *sV = smem + OFF_V + st * TILE;
           const int t0 = n * BT;
-          ptx::mbar_wait(&k_empty[st], ph);
-          ptx::mbar_arrive_expect_tx(&k_full[st], TILE);
-          ptx::tma_load_4d(sK, &P.tmK, &k_full[st], 0, j, t0, b);
-          ptx::tma_load_4d(sK + PANEL, &P.tmK, &k_full[st], 64, j, t0, b);
-          ptx::mbar_wait(&v_empty[st], ph);
-          ptx::mbar_arrive_expect_tx(&v_full[st], TILE);
-          ptx::tma_load_4d(sV, &P.tmV, &v_full[st], 0, j, t0, b);
-          ptx::tma_load_4d(sV + PANEL, &P.tmV, &v_full[st], 64, j, t0, b);
+          if (warp == 0) {
+            uint8_t *sK = smem + OFF_K + st * TILE;
+            ptx::mbar_wait(&k_empty[st], ph);
+            ptx::mbar_arrive_expect_tx(&k_full[st], TILE);
+            ptx::tma_load_4d(sK, &P.tmK, &k_full[st], 0, j, t0, b);
+            ptx::tma_load_4d(sK + PANEL, &P.tmK, &k_full[st], 64, j, t0, b);
+            trace(tr, 9, gb);
+          } else {
+            uint8_t *sV = smem + OFF_V + st * TILE;
+            ptx::mbar_wait(&v_empty[st], ph);
+            ptx::mbar_arrive_expect_tx(&v_full[st], TILE);
+            ptx::tma_load_4d(sV, &P.tmV, &v_full[st], 0, j, t0, b);
+            ptx::tma_load_4d(sV + PANEL, &P.tmV, &v_full[st], 64, j, t0, b);
+            trace(tr, 10, gb);
+          }
         }
       }
     }
   } else if (warp == 1) {
-    // ================= MMA issuer (flat block sequence across items, one-block lookahead) =================
-    if (ptx::elect_one()) {
-      constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BT, NQ, false);                 // A=K, B=Q^T (K-major)
-      constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(HD, NQ, false) | (1u << 15);  // A=V^T (MN-major), B=P^T
-      struct Blk {
-        uint32_t gbi, st, ob, qs, item_no;
-        bool first, last;
-      } prev{};
-      bool have_prev = false;
-      uint32_t gbi = 0, qi = 0, item_no = 0;
-      auto do_pv = [&](const Blk &x) {
-        const uint32_t slot = x.gbi & 1;
-        ptx::mbar_wait(&p_full[slot], (x.gbi >> 1) & 1);
-        if (x.first) ptx::mbar_wait(&o_free[x.ob], ((x.item_no >> 1) & 1) ^ 1);
-        ptx::mbar_wait(&v_full[x.st], (x.gbi / NS) & 1);
-        ptx::tc_fence_after();
-        const uint32_t v_addr = ptx::smem_u32(smem + OFF_V + x.st * TILE);
-        const uint32_t p_addr = ptx::smem_u32(smem + OFF_P + slot * PTILE);
-#pragma unroll
-        for (int kk = 0; kk < BT / 16; ++kk)
-          ptx::mma_ss(tmem + 2 * NQ + x.ob * NQ, ptx::smem_desc_sw128(v_addr + kk * 2048, PANEL, 1024),
-                      ptx::smem_desc_sw128(p_addr + (kk / 4) * PPANEL + (kk % 4) * 32, 16, 1024), idesc_pv,
-                      (!x.first || kk > 0));
-        ptx::mma_commit(&pv_done[slot]);
-        ptx::mma_commit(&v_empty[x.st]);
-        if (x.last) ptx::mma_commit(&q_empty[x.qs]);
-      };
-      for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
-        const int b = item / P.Hkv;
-        const int nblk = (P.lens[b] + BT - 1) / BT;
-        if (nblk == 0) continue;
-        const uint32_t qs = qi & 1;
-        ptx::mbar_wait(&q_full[qs], (qi >> 1) & 1);
+    // ================= MMA issuer (event-driven) =================
+    // Two cursors over the same flat round sequence: the S cursor issues score MMAs as soon
+    // as a round's K tiles land (at most two rounds ahead of the PV cursor: two S^T slots),
+    // the PV cursor issues a round's PV MMAs as soon as its P^T and V tiles are ready.
+    // Neither waits behind the other, so a V slot is held only for load + softmax + PV.
+    const bool leader = ptx::elect_one();
+    if (leader && (P.debug & 256)) {  // drain only: release each tile as soon as it lands
+      RoundCursor<CB> c;
+      c.init(P);
+      while (c.valid) {
+        if (c.n0 == 0) ptx::mbar_wait(&q_full[c.qi % NQS], (c.qi / NQS) & 1);
+        for (int i = 0; i < c.nb; ++i) {
+          const uint32_t gbc = c.gb + i, st = gbc % NS;
+          ptx::mbar_wait(&k_full[st], (gbc / NS) & 1);
+          trace(blockIdx.x == 0 ? P.trace : nullptr, 11, gbc);
+          ptx::mbar_arrive(&k_empty[st]);
+          ptx::mbar_wait(&v_full[st], (gbc / NS) & 1);
+          trace(blockIdx.x == 0 ? P.trace : nullptr, 12, gbc);
+          ptx::mbar_arrive(&v_empty[st]);
+        }
+        if (c.n0 + c.nb >= c.nblk) ptx::mbar_arrive(&q_empty[c.qi % NQS]);
+        c.next(P);
+      }
+    } else if (leader) {
+      // ================= score-MMA issuer (warp 1; the PV MMAs are issued by warp 12) =================
+      // S(n) needs K(n) landed and S^T slot n % NSP consumed by the softmax (p_full of round
+      // n - NSP).  Two issuing threads, each blocking on one barrier at a time: a score MMA
+      // never waits behind a V tile and a PV MMA never waits behind a K tile.
+      constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BT, NQ, false);  // A=K, B=Q^T (K-major)
+      long long *tr = blockIdx.x == 0 ? P.trace : nullptr;
+      RoundCursor<CB> sc;
+      sc.init(P);
+      while (sc.valid) {
+        if (sc.gr >= (uint32_t)NSP) ptx::mbar_wait(&p_full[sc.gr % NSP], ((sc.gr - NSP) / NSP) & 1);
+        const uint32_t qs = sc.qi % NQS;
+        if (sc.n0 == 0) ptx::mbar_wait(&q_full[qs], (sc.qi / NQS) & 1);
         const uint32_t q_addr = ptx::smem_u32(smem + OFF_Q + qs * QTILE);
-        for (int n = 0; n < nblk; ++n, ++gbi) {
-          const uint32_t st = gbi % NS;
-          ptx::mbar_wait(&k_full[st], (gbi / NS) & 1);
+        for (int c = 0; c < sc.nb; ++c) {
+          const uint32_t gbc = sc.gb + c, st = gbc % NS;
+          ptx::mbar_wait(&k_full[st], (gbc / NS) & 1);
+          trace(tr, 11, gbc);
           ptx::tc_fence_after();
           const uint32_t k_addr = ptx::smem_u32(smem + OFF_K + st * TILE);
 #pragma unroll
           for (int kk = 0; kk < HD / 16; ++kk) {
             const uint32_t off = (kk / 4) * PANEL + (kk % 4) * 32, qoff = (kk / 4) * QPANEL + (kk % 4) * 32;
-            ptx::mma_ss(tmem + (gbi & 1) * NQ, ptx::smem_desc_sw128(k_addr + off, 16, 1024),
+            ptx::mma_ss(tmem + ((sc.gr % NSP) * CB + c) * NQ, ptx::smem_desc_sw128(k_addr + off, 16, 1024),
                         ptx::smem_desc_sw128(q_addr + qoff, 16, 1024), idesc_s, kk > 0);
           }
-          ptx::mma_commit(&s_full[gbi & 1]);
           ptx::mma_commit(&k_empty[st]);
-          if (have_prev) do_pv(prev);  // PV of the previous block after S of this one
-          prev = Blk{gbi, st, item_no & 1, qs, item_no, n == 0, n == nblk - 1};
-          have_prev = true;
         }
-        ++qi;
-        ++item_no;
+        ptx::mma_commit(&s_full[sc.gr % NSP]);
+        if (sc.n0 + sc.nb >= sc.nblk) ptx::mma_commit(&q_empty[qs]);  // the item's last score MMA
+        trace(tr, 7, sc.gr);
+        sc.next(P);
       }
-      if (have_prev) do_pv(prev);
     }
-  } else {
-    // ================= softmax (thread = token lane) / lagged epilogue (thread = head dim) =================
+  } else if (warp == 12) {
+    // ================= PV-MMA issuer =================
+    if (ptx::elect_one() && !(P.debug & 256)) {
+      constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(HD, NQ, false) | (1u << 15);  // A=V^T (MN-major), B=P^T
+      long long *tr = blockIdx.x == 0 ? P.trace : nullptr;
+      RoundCursor<CB> pc;
+      pc.init(P);
+      while (pc.valid) {
+        const uint32_t slot = pc.gr % NSP, ob = pc.item_no & 1;
+        ptx::mbar_wait(&p_full[slot], (pc.gr / NSP) & 1);
+        if (pc.n0 == 0) ptx::mbar_wait(&o_free[ob], ((pc.item_no >> 1) & 1) ^ 1);
+        const uint32_t p_base = ptx::smem_u32(smem + OFF_P + slot * CB * PTILE);
+        for (int c = 0; c < pc.nb; ++c) {
+          const uint32_t gbc = pc.gb + c, st = gbc % NS;
+          ptx::mbar_wait(&v_full[st], (gbc / NS) & 1);
+          trace(tr, 12, gbc);
+          ptx::tc_fence_after();
+          const uint32_t v_addr = ptx::smem_u32(smem + OFF_V + st * TILE);
+          const uint32_t p_addr = p_base + c * PTILE;
+#pragma unroll
+          for (int kk = 0; kk < BT / 16; ++kk)
+            ptx::mma_ss(tmem + O_COL + ob * NQ, ptx::smem_desc_sw128(v_addr + kk * 2048, PANEL, 1024),
+                        ptx::smem_desc_sw128(p_addr + (kk / 4) * PPANEL + (kk % 4) * 32, 16, 1024), idesc_pv,
+                        (pc.n0 > 0 || c > 0 || kk > 0));
+          ptx::mma_commit(&v_empty[st]);
+        }
+        ptx::mma_commit(&pv_done[slot]);
+        trace(tr, 8, pc.gr);
+        if (pc.n0 + pc.nb >= pc.nblk) ptx::mma_commit(&o_full[ob]);
+        pc.next(P);
+      }
+    }
+  } else if (warp < 8 && !(P.debug & 256)) {
+    // ================= softmax (thread = token lane) =================
     const int quarter = warp % 4;
     const int r = quarter * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const float c2 = P.scale_log2;
-    uint32_t gbi = 0, item_no = 0;
-    // state of the item whose epilogue is pending (run after the next item's first block)
-    bool pend = false;
-    int64_t pend_row0 = 0;
-    uint32_t pend_ob = 0, pend_last = 0;
-    float pm[G], pl[G];
-    auto epilogue = [&]() {
-      ptx::mbar_wait(&pv_done[pend_last & 1], (pend_last >> 1) & 1);
-      ptx::tc_fence_after();
-      // two epilogues can run back to back (the lagged one and the final one): alternate
-      // the reduction buffer by item parity so a fast warp never overwrites sums a slow
-      // warp is still reading
-      float *rs = red_sum + pend_ob * 4 * NQ;
-#pragma unroll
-      for (int h = 0; h < G; ++h) {
-          float x = pl[h];
-#pragma unroll
-          for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-          if (lane == 0) rs[quarter * NQ + h] = x;
-        }
-      named_bar_sync(1, 128);
-      uint32_t ov[NQ];
-      ptx::tmem_ld16(tmem + lane_base + 2 * NQ + pend_ob * NQ, ov);
-      ptx::tmem_ld_wait();
-      ptx::tc_fence_before();
-      ptx::warp_arrive(&o_free[pend_ob]);
-#pragma unroll
-      for (int h = 0; h < G; ++h) {
-          const float L = rs[h] + rs[NQ + h] + rs[2 * NQ + h] + rs[3 * NQ + h];
-          P.o[(pend_row0 + h) * HD + r] = __uint_as_float(ov[h]) / L;
-          if (r == h) P.lse[pend_row0 + h] = (pm[h] + log2f(L)) * HYDRA_LN2;
-        }
-      pend = false;
-    };
+    uint32_t gr = 0, gb = 0, item_no = 0;
+    long long *tr = (blockIdx.x == 0 && quarter == 0 && lane == 0) ? P.trace : nullptr;
+    int len_next = item_len(P, blockIdx.x);
     for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
       const int b = item / P.Hkv, j = item % P.Hkv;
-      const int len = P.lens[b];
+      const int len = len_next;
+      len_next = item_len(P, item + gridDim.x);
       const int nblk = (len + BT - 1) / BT;
       const int64_t row0 = (int64_t)b * P.Hq + (int64_t)j * g;
       if (nblk == 0) {  // empty suffix: (0, -inf) sentinel
@@ -258,33 +372,51 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
         continue;
       }
       const uint32_t ob = item_no & 1;
-      const uint32_t o_tmem = tmem + lane_base + 2 * NQ + ob * NQ;
+      const uint32_t o_tmem = tmem + lane_base + O_COL + ob * NQ;
       float m[G], l[G];
 #pragma unroll
       for (int h = 0; h < G; ++h) {
         m[h] = -INFINITY;
         l[h] = 0.f;
       }
-      for (int n = 0; n < nblk; ++n, ++gbi) {
-        const uint32_t buf = gbi & 1;
-        ptx::mbar_wait(&s_full[buf], (gbi >> 1) & 1);
+      for (int n0 = 0; n0 < nblk; n0 += CB, ++gr) {
+        const int nb = min(CB, nblk - n0);
+        const uint32_t buf = gr % NSP;
+        trace(tr, 0, gr);
+        ptx::mbar_wait(&s_full[buf], (gr / NSP) & 1);
+        trace(tr, 1, gr);
         ptx::tc_fence_after();
-        uint32_t sv[NQ];
-        ptx::tmem_ld16(tmem + lane_base + buf * NQ, sv);
+        if (P.debug & 512) {  // timing experiment only: no softmax work
+          if (gr >= (uint32_t)NSP) ptx::mbar_wait(&pv_done[buf], ((gr - NSP) / NSP) & 1);
+          ptx::warp_arrive(&p_full[buf]);
+          gb += nb;
+          continue;
+        }
+        uint32_t sv[CB][NQ];
+#pragma unroll
+        for (int c = 0; c < CB; ++c)
+          if (c < nb) ptx::tmem_ld16(tmem + lane_base + (buf * CB + c) * NQ, sv[c]);
         ptx::tmem_ld_wait();
-        const int valid = min(BT, len - n * BT);
-        const bool tok = r < valid;
-        float s[G];
-        float *rm = red_max + buf * 4 * NQ;
+        trace(tr, 2, gr);
+        float s[CB][G];
+        bool tok[CB];
+        float *rm = red_max + (gr & 1) * 4 * NQ;
+#pragma unroll
+        for (int c = 0; c < CB; ++c) tok[c] = c < nb && (n0 + c) * BT + r < len;
 #pragma unroll
         for (int h = 0; h < G; ++h) {
-          s[h] = tok ? __uint_as_float(sv[h]) : -INFINITY;
-          float x = s[h];
+          float x = -INFINITY;
+#pragma unroll
+          for (int c = 0; c < CB; ++c) {
+            s[c][h] = tok[c] ? __uint_as_float(sv[c][h]) : -INFINITY;
+            x = fmaxf(x, s[c][h]);
+          }
 #pragma unroll
           for (int o = 16; o >= 1; o >>= 1) x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, o));
           if (lane == 0) rm[quarter * NQ + h] = x;
         }
         named_bar_sync(1, 128);
+        trace(tr, 3, gr);
         float alpha[NQ];
         bool resc = false;
 #pragma unroll
@@ -293,23 +425,28 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
         for (int h = 0; h < G; ++h) {
           const float bm = fmaxf(fmaxf(rm[h], rm[NQ + h]), fmaxf(rm[2 * NQ + h], rm[3 * NQ + h]));
           const float mnew = bm * c2;
-          if (mnew > m[h] + 8.0f) {  // block-uniform decision
+          if (mnew > m[h] + 8.0f) {  // round-uniform decision
             const float mt = fmaxf(m[h], mnew);
             alpha[h] = fast_exp2(m[h] - mt);
             m[h] = mt;
             resc = true;
           }
         }
-        float p[G];
+        float p[CB][G];
 #pragma unroll
         for (int h = 0; h < G; ++h) {
-          p[h] = tok ? fast_exp2(fmaf(s[h], c2, -m[h])) : 0.f;
-          l[h] = l[h] * alpha[h] + p[h];
+          float acc = 0.f;
+#pragma unroll
+          for (int c = 0; c < CB; ++c) {
+            p[c][h] = tok[c] ? fast_exp2(fmaf(s[c][h], c2, -m[h])) : 0.f;
+            acc += p[c][h];
+          }
+          l[h] = l[h] * alpha[h] + acc;
         }
-        // P slot `buf` was last read by PV(gbi - 2)
-        if (gbi >= 2) ptx::mbar_wait(&pv_done[buf], ((gbi - 2) >> 1) & 1);
-        if (resc && n >= 1) {  // rare: O^T column h *= alpha[h] once PV(gbi - 1) has landed
-          ptx::mbar_wait(&pv_done[buf ^ 1], ((gbi - 1) >> 1) & 1);
+        // P slot `buf` was last read by PV(gr - NSP)
+        if (gr >= (uint32_t)NSP) ptx::mbar_wait(&pv_done[buf], ((gr - NSP) / NSP) & 1);
+        if (resc && n0 > 0) {  // rare: O^T column h *= alpha[h] once PV(gr - 1) has landed
+          ptx::mbar_wait(&pv_done[(gr - 1) % NSP], ((gr - 1) / NSP) & 1);
           ptx::tc_fence_after();
           uint32_t ov[NQ];
           ptx::tmem_ld16(o_tmem, ov);
@@ -319,37 +456,85 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
           ptx::tmem_st16(o_tmem, ov);
           ptx::tmem_st_wait();
         }
-        uint8_t *sp = smem + OFF_P + buf * PTILE + (r / 64) * PPANEL;
-        const int c = (r % 64) / 8, e = r % 8;
+        const int cc = (r % 64) / 8, e = r % 8;
 #pragma unroll
-        for (int h = 0; h < G; ++h)
-          *reinterpret_cast<__nv_bfloat16 *>(sp + h * 128 + ((c ^ (h % 8)) * 16) + e * 2) = __float2bfloat16_rn(p[h]);
-        if (valid < BT) ptx::mbar_wait(&v_full[gbi % NS], (gbi / NS) & 1);  // V tile landed
-        if (!tok) {  // rows past lens[b] in the last block: zero the V row (0 * NaN would poison O)
-          uint8_t *vrow = smem + OFF_V + (gbi % NS) * TILE + r * 128;
+        for (int c = 0; c < CB; ++c) {
+          if (c >= nb) break;
+          uint8_t *sp = smem + OFF_P + (buf * CB + c) * PTILE + (r / 64) * PPANEL;
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            *reinterpret_cast<uint4 *>(vrow + q * 16) = make_uint4(0, 0, 0, 0);
-            *reinterpret_cast<uint4 *>(vrow + PANEL + q * 16) = make_uint4(0, 0, 0, 0);
+          for (int h = 0; h < G; ++h)
+            *reinterpret_cast<__nv_bfloat16 *>(sp + h * 128 + ((cc ^ (h % 8)) * 16) + e * 2) =
+                __float2bfloat16_rn(p[c][h]);
+        }
+        if ((n0 + nb) * BT > len) {  // ragged last block of the item (always the round's last)
+          const uint32_t gl = gb + nb - 1;
+          ptx::mbar_wait(&v_full[gl % NS], (gl / NS) & 1);  // V tile landed
+          if (!tok[nb - 1]) {  // rows past lens[b]: zero the V row (0 * NaN would poison O)
+            uint8_t *vrow = smem + OFF_V + (gl % NS) * TILE + r * 128;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              *reinterpret_cast<uint4 *>(vrow + q * 16) = make_uint4(0, 0, 0, 0);
+              *reinterpret_cast<uint4 *>(vrow + PANEL + q * 16) = make_uint4(0, 0, 0, 0);
+            }
           }
         }
         ptx::fence_proxy_async_smem();
         ptx::tc_fence_before();
         ptx::warp_arrive(&p_full[buf]);
-        if (n == 0 && pend) epilogue();  // previous item's epilogue, off the critical path
+        trace(tr, 4, gr);
+        gb += nb;
       }
-      pend = true;
-      pend_row0 = row0;
-      pend_ob = ob;
-      pend_last = gbi - 1;
+      // hand (m, row-sum partials) to the epilogue warps; slot ob was last read by the
+      // epilogue of item item_no - 2
+      ptx::mbar_wait(&o_free[ob], ((item_no >> 1) & 1) ^ 1);
+      float *rs = red_sum + ob * 4 * NQ;
 #pragma unroll
       for (int h = 0; h < G; ++h) {
-        pm[h] = m[h];
-        pl[h] = l[h];
+        float x = l[h];
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) rs[quarter * NQ + h] = x;
+        if (r == 0) item_m[ob * NQ + h] = m[h];
+      }
+      ptx::warp_arrive(&ml_full[ob]);
+      ++item_no;
+    }
+  } else if (warp >= 8 && !(P.debug & 256)) {
+    // ================= epilogue (thread = head dim): O = O^T / l, LSE =================
+    const int quarter = warp % 4;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    uint32_t item_no = 0;
+    int len_next = item_len(P, blockIdx.x);
+    for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+      const int len = len_next;
+      len_next = item_len(P, item + gridDim.x);
+      if (len <= 0) continue;
+      const int b = item / P.Hkv, j = item % P.Hkv;
+      const int64_t row0 = (int64_t)b * P.Hq + (int64_t)j * g;
+      const uint32_t ob = item_no & 1, ph = (item_no >> 1) & 1;
+      ptx::mbar_wait(&o_full[ob], ph);
+      ptx::mbar_wait(&ml_full[ob], ph);
+      ptx::tc_fence_after();
+      uint32_t ov[NQ];
+      ptx::tmem_ld16(tmem + lane_base + O_COL + ob * NQ, ov);
+      ptx::tmem_ld_wait();
+      const float *rs = red_sum + ob * 4 * NQ;
+      float L[G], M[G];
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        L[h] = rs[h] + rs[NQ + h] + rs[2 * NQ + h] + rs[3 * NQ + h];
+        M[h] = item_m[ob * NQ + h];
+      }
+      ptx::tc_fence_before();
+      ptx::warp_arrive(&o_free[ob]);  // O^T buffer and (m, l) slot free
+#pragma unroll
+      for (int h = 0; h < G; ++h) {
+        P.o[(row0 + h) * HD + r] = __uint_as_float(ov[h]) / L[h];
+        if (r == h) P.lse[row0 + h] = (M[h] + log2f(L[h])) * HYDRA_LN2;
       }
       ++item_no;
     }
-    if (pend) epilogue();
   }
 
   ptx::tc_fence_before();
@@ -381,16 +566,21 @@ bool suffix_tc_supported(const hydra_heads *h) {
   return h->dtype == HYDRA_BF16 && h->head_dim == 128 && g_ok && encode_fn3() != nullptr;
 }
 
-template <int G>
-static cudaError_t launch_g(const SuffixTcParams &P, int grid, cudaStream_t s) {
+template <int G, int CB>
+static cudaError_t launch_gc(const SuffixTcParams &P, int grid, cudaStream_t s) {
   static std::once_flag once;
   static cudaError_t attr = cudaSuccess;
+  constexpr int alloc = stc::alloc_bytes(CB);
   std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(suffix_tc_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, stc::ALLOC);
+    attr = cudaFuncSetAttribute(suffix_tc_kernel<G, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, alloc);
   });
   if (attr != cudaSuccess) return attr;
-  suffix_tc_kernel<G><<<grid, stc::kThreads, stc::ALLOC, s>>>(P);
+  suffix_tc_kernel<G, CB><<<grid, stc::kThreads, alloc, s>>>(P);
   return cudaGetLastError();
+}
+template <int G>
+static cudaError_t launch_g(const SuffixTcParams &P, int cb, int grid, cudaStream_t s) {
+  return cb == 1 ? launch_gc<G, 1>(P, grid, s) : launch_gc<G, 2>(P, grid, s);
 }
 
 hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s) {
@@ -432,15 +622,17 @@ hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s)
   P.n_items = a.B * a.Hkv;
   P.o = a.o;
   P.lse = a.lse;
+  P.trace = reinterpret_cast<long long *>(a.trace);
+  P.debug = a.debug;
   if (P.n_items == 0) return HYDRA_OK;
   const int grid = n_ctas > 0 && n_ctas < P.n_items ? n_ctas : P.n_items;
   cudaError_t e = cudaErrorInvalidValue;
   switch (g) {
-    case 1: e = launch_g<1>(P, grid, s); break;
-    case 2: e = launch_g<2>(P, grid, s); break;
-    case 4: e = launch_g<4>(P, grid, s); break;
-    case 8: e = launch_g<8>(P, grid, s); break;
-    case 16: e = launch_g<16>(P, grid, s); break;
+    case 1: e = launch_g<1>(P, a.cb, grid, s); break;
+    case 2: e = launch_g<2>(P, a.cb, grid, s); break;
+    case 4: e = launch_g<4>(P, a.cb, grid, s); break;
+    case 8: e = launch_g<8>(P, a.cb, grid, s); break;
+    case 16: e = launch_g<16>(P, 1, grid, s); break;  // CB = 2 would spill at G = 16
   }
   return e == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
 }

@@ -27,8 +27,10 @@ def _reset_config():
     for k in keys:
         hydra.set_config(k, 0)
     hydra.set_config("prefix_variant", 3)
+    hydra.set_config("suffix_cb", 2)
     yield
     hydra.set_config("prefix_variant", 3)
+    hydra.set_config("suffix_cb", 2)
     for k in keys:
         hydra.set_config(k, 0)
 
@@ -142,9 +144,10 @@ def test_prefix_simt_bf16():
 # ---------------------------------------------------------------- suffix kernel
 @pytest.mark.parametrize("B,Hq,Hkv,d,S", [(7, 8, 8, 128, 300), (5, 16, 4, 128, 77), (6, 16, 1, 128, 40),
                                           (4, 8, 2, 64, 129), (3, 32, 2, 128, 64), (9, 12, 4, 128, 513)])
-@pytest.mark.parametrize("impl", [1, 2])  # 1: SIMT split-K, 2: persistent tensor-core (falls back if unsupported)
+@pytest.mark.parametrize("impl", [1, 2, 3])  # 1: SIMT split-K, 2/3: persistent tensor-core, 2 / 1 blocks per round
 def test_suffix_parity(B, Hq, Hkv, d, S, impl):
-    hydra.set_config("suffix_impl", impl)
+    hydra.set_config("suffix_impl", min(impl, 2))
+    hydra.set_config("suffix_cb", 1 if impl == 3 else 2)
     rng = np.random.default_rng(B * S)
     lens = rng.integers(0, S + 1, B)
     lens[0] = S
@@ -206,8 +209,10 @@ def test_composite_sm_partitioned(k, B, Hq, Hkv, P, S):
 
 
 @pytest.mark.parametrize("ctas", [1, 5, 148])
-def test_suffix_tc_ctas_and_ragged(ctas):
+@pytest.mark.parametrize("cb", [1, 2])
+def test_suffix_tc_ctas_and_ragged(ctas, cb):
     hydra.set_config("suffix_impl", 2)
+    hydra.set_config("suffix_cb", cb)
     hydra.set_config("suffix_ctas", ctas)
     lens = [0, 1, 127, 128, 129, 255, 256, 300, 17, 0, 384]
     pb = synth.make_problem(len(lens), 8, 1, 128, 0, 384, lens=lens, dtype="bf16", dist="boundary", seed=18)
@@ -215,7 +220,7 @@ def test_suffix_tc_ctas_and_ragged(ctas):
     o, lse = hydra.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
     torch.cuda.synchronize()
     ref, lref = oracle.suffix_only(pb)
-    assert_parity(o, ref, lse, lref, what=f"suffix tc ctas={ctas}")
+    assert_parity(o, ref, lse, lref, what=f"suffix tc ctas={ctas} cb={cb}")
 
 
 def test_composite_f32_output_is_tighter():
