@@ -41,7 +41,7 @@ static hydra_status cuda_fail(const char *what) {
 
 static std::atomic<int64_t> g_prefix_impl{0}, g_prefix_splits{0}, g_suffix_splits{0}, g_tc_debug{0},
     g_prefix_stages{3}, g_suffix_unroll{4}, g_prefix_ctas{0}, g_suffix_impl{0}, g_suffix_ctas{0},
-    g_overlap_prefix_ctas{0}, g_prefix_poly{0}, g_prefix_variant{3}, g_prefix_trace{0}, g_suffix_cb{2}, g_suffix_trace{0},
+    g_overlap_prefix_ctas{0}, g_prefix_poly{0}, g_prefix_variant{6}, g_prefix_trace{0}, g_suffix_cb{2}, g_suffix_trace{0},
     g_last_overlap_k{0};  // read-only: prefix CTAs of the last hydra_attn overlap split (0 = sequential)
 
 extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
@@ -56,7 +56,7 @@ extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
   else if (!strcmp(key, "suffix_ctas")) g_suffix_ctas = value;
   else if (!strcmp(key, "overlap_prefix_ctas")) g_overlap_prefix_ctas = value;
   else if (!strcmp(key, "prefix_poly")) g_prefix_poly = (value == 0 || value == 3 || value == 8 || value == -1) ? value : 4;
-  else if (!strcmp(key, "prefix_variant")) g_prefix_variant = (value == 4 || value == 5) ? value : 3;
+  else if (!strcmp(key, "prefix_variant")) g_prefix_variant = (value == 3 || value == 4 || value == 5) ? value : 6;
   else if (!strcmp(key, "prefix_stages")) g_prefix_stages = (value == 2 ? 2 : 3);
   else if (!strcmp(key, "suffix_trace")) g_suffix_trace = value;
   else if (!strcmp(key, "suffix_cb")) g_suffix_cb = (value == 1 ? 1 : 2);

@@ -51,8 +51,8 @@ constexpr int OFF_Q = 0;         // Q0, Q1
 constexpr int OFF_K = 2 * TILE;
 constexpr int OFF_V = OFF_K + NS * TILE;
 constexpr int OFF_BAR = OFF_V + NS * TILE;
-// k_full, k_empty, v_full, v_empty [NS]; q_full, s_full, p_full, pv_done, o_free [2]
-constexpr int N_BARS = 4 * NS + 10;
+// k_full, k_empty, v_full, v_empty [NS]; q_full, s_full, p_full, pv_done, o_free, p_half [2]
+constexpr int N_BARS = 4 * NS + 12;
 constexpr int BYTES = OFF_BAR + N_BARS * 8 + 16;
 constexpr int ALLOC = BYTES + 1024;
 constexpr uint32_t TMEM_COLS = 512;
@@ -171,7 +171,9 @@ __device__ __forceinline__ bool seg_next(const PrefixTc2Params &P, SegIter &s, I
 
 // kPolyEvery -- 0: all exp2 on MUFU; k: every k-th column pair on the FMA pipe.
 // kSpec -- speculative softmax with the running max (variant 5, see the loop).
-template <int kPolyEvery, bool kSpec>
+// kSplit -- P published in two 64-token halves (variant 6): the PV MMAs of the first half
+//   run while the softmax still computes exp() of the second half.
+template <int kPolyEvery, bool kSpec, bool kSplit = false>
 __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __grid_constant__ PrefixTc2Params P) {
   using namespace tc2;
   extern __shared__ uint8_t smem_raw[];
@@ -179,7 +181,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
   uint64_t *k_full = bars, *k_empty = bars + NS, *v_full = bars + 2 * NS, *v_empty = bars + 3 * NS;
   uint64_t *q_full = bars + 4 * NS, *s_full = q_full + 2, *p_full = q_full + 4, *pv_done = q_full + 6,
-           *o_free = q_full + 8;
+           *o_free = q_full + 8, *p_half = q_full + 10;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + N_BARS);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
@@ -198,6 +200,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
       ptx::mbar_init(&p_full[t], 4);  // one elected arrival per softmax warp
       ptx::mbar_init(&pv_done[t], 1);
       ptx::mbar_init(&o_free[t], 4);  // one elected arrival per softmax warp
+      ptx::mbar_init(&p_half[t], 4);  // one elected arrival per softmax warp
     }
     ptx::fence_mbar_init();
   }
@@ -288,16 +291,28 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
           ptx::mbar_wait(&v_full[st], (g0 / NS) & 1);
           const uint32_t v_addr = ptx::smem_u32(smem + OFF_V + st * TILE);
           for (int t = 0; t < ntile; ++t) {
+            if (kSplit) {  // first half of P(n): tokens 0-63 (P columns 0-31)
+              ptx::mbar_wait(&p_half[t], pc[t] & 1);
+              if (n == 0) {
+                ptx::mbar_wait(&o_free[t], (oc[t] & 1) ^ 1);
+                ++oc[t];
+              }
+              ptx::tc_fence_after();
+#pragma unroll
+              for (int kk = 0; kk < BN / 32; ++kk)
+                ptx::mma_ts(tmem + 256 + t * BN, tmem + t * BN + kk * 8,
+                            ptx::smem_desc_sw128(v_addr + kk * 2048, PANEL, 1024), idesc_pv, (n > 0 || kk > 0));
+            }
             ptx::mbar_wait(&p_full[t], pc[t] & 1);
             ++pc[t];
             if (tr && pc[t] <= kTraceN) tr[(6 + t) * kTraceN + pc[t] - 1] = clock64();
-            if (n == 0) {  // O_t must have been drained by the previous item's epilogue
+            if (!kSplit && n == 0) {  // O_t must have been drained by the previous item's epilogue
               ptx::mbar_wait(&o_free[t], (oc[t] & 1) ^ 1);
               ++oc[t];
             }
             ptx::tc_fence_after();
 #pragma unroll
-            for (int kk = 0; kk < BN / 16; ++kk)
+            for (int kk = kSplit ? BN / 32 : 0; kk < BN / 16; ++kk)
               ptx::mma_ts(tmem + 256 + t * BN, tmem + t * BN + kk * 8,
                           ptx::smem_desc_sw128(v_addr + kk * 2048, PANEL, 1024), idesc_pv, (n > 0 || kk > 0));
             ptx::mma_commit(&pv_done[t]);
@@ -486,15 +501,44 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
             asm volatile("" ::"l"(nm));  // the max is done before this timestamp
             tr[(12 + t) * kTraceN + sc - 1] = clock64();
           }
+          if (kSplit) {
+            // first half of P, then the O correction (PV_t(n-1) landed: S_t(n) was issued after
+            // it; done here so the first half's scores are dead), then the first half is
+            // published so its PV MMAs overlap the exp() of the second half
+            exp_chunk(sr[0], 0, nm);
+            exp_chunk(sr[1], 1, nm);
+            if (n >= 1) {
+              ptx::mbar_wait(&pv_done[t], pvc & 1);
+              ++pvc;
+              ptx::tc_fence_after();
+              if (any) {
 #pragma unroll
-          for (int c = 0; c < 4; ++c) exp_chunk(sr[c], c, nm);
+                for (int c = 0; c < 4; ++c) {
+                  uint32_t ov[32];
+                  ptx::tmem_ld32(o_col + c * 32, ov);
+                  ptx::tmem_ld_wait();
+#pragma unroll
+                  for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+                  ptx::tmem_st32(o_col + c * 32, ov);
+                }
+              }
+            }
+            ptx::tmem_st_wait();
+            ptx::tc_fence_before();
+            ptx::warp_arrive(&p_half[t]);
+            exp_chunk(sr[2], 2, nm);
+            exp_chunk(sr[3], 3, nm);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) exp_chunk(sr[c], c, nm);
+          }
         }
         float s0, s1, s2, s3;
         ptx::unpack2(ptx::add2(sacc[0], sacc[1]), s0, s1);
         ptx::unpack2(ptx::add2(sacc[2], sacc[3]), s2, s3);
         l = l * alpha + ((s0 + s1) + (s2 + s3));
         if (tr && sc <= kTraceN) tr[(8 + t) * kTraceN + sc - 1] = clock64();
-        if (n >= 1) {
+        if (!kSplit && n >= 1) {
           ptx::mbar_wait(&pv_done[t], pvc & 1);  // PV_t(n-1) landed in O_t
           ++pvc;
           ptx::tc_fence_after();
@@ -965,16 +1009,16 @@ int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn) {
   return tc2_plan(B, g, Hkv, P, n_ctas, bn).ctas;
 }
 
-template <int kPoly, bool kPP>
+template <int kPoly, bool kPP, bool kSplit = false>
 static cudaError_t tc2_launch(const PrefixTc2Params &P, int grid, cudaStream_t s) {
   static std::once_flag once;
   static cudaError_t attr = cudaSuccess;
   std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(prefix_tc2_kernel<kPoly, kPP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr = cudaFuncSetAttribute(prefix_tc2_kernel<kPoly, kPP, kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 tc2::ALLOC);
   });
   if (attr != cudaSuccess) return attr;
-  prefix_tc2_kernel<kPoly, kPP><<<grid, tc2::kThreads, tc2::ALLOC, s>>>(P);
+  prefix_tc2_kernel<kPoly, kPP, kSplit><<<grid, tc2::kThreads, tc2::ALLOC, s>>>(P);
   return cudaGetLastError();
 }
 
@@ -1037,6 +1081,10 @@ hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s
   }
   const bool spec = a.variant == 5;
   cudaError_t e;
+  if (a.variant == 6) {  // split P publication
+    e = poly == 4 ? tc2_launch<4, false, true>(P, grid, s) : tc2_launch<0, false, true>(P, grid, s);
+    return e == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
+  }
   switch (poly * 2 + (spec ? 1 : 0)) {
     case 0: e = tc2_launch<0, false>(P, grid, s); break;
     case 1: e = tc2_launch<0, true>(P, grid, s); break;

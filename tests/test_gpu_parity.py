@@ -26,10 +26,10 @@ def _reset_config():
             "suffix_ctas", "overlap_prefix_ctas", "prefix_poly")
     for k in keys:
         hydra.set_config(k, 0)
-    hydra.set_config("prefix_variant", 3)
+    hydra.set_config("prefix_variant", 6)
     hydra.set_config("suffix_cb", 2)
     yield
-    hydra.set_config("prefix_variant", 3)
+    hydra.set_config("prefix_variant", 6)
     hydra.set_config("suffix_cb", 2)
     for k in keys:
         hydra.set_config(k, 0)
@@ -71,10 +71,11 @@ PREFIX_SHAPES = [
 
 @pytest.mark.parametrize("B,Hq,Hkv,P", PREFIX_SHAPES)
 @pytest.mark.parametrize("dist", ["mixed", "boundary"])
-@pytest.mark.parametrize("impl", [2, 3, 4, 5])
+@pytest.mark.parametrize("impl", [2, 3, 4, 5, 6])
 def test_prefix_tc_parity(B, Hq, Hkv, P, dist, impl):
     # 2: one-tile tcgen05 kernel, 3: persistent two-tile (128-token blocks), 4: same with 64-token
-    # blocks and double-buffered scores, 5: 3 with the speculative (running-max) softmax
+    # blocks and double-buffered scores, 5: 3 with the speculative (running-max) softmax,
+    # 6: 3 with P published in two halves (default)
     hydra.set_config("prefix_impl", min(impl, 3))
     hydra.set_config("prefix_variant", impl if impl >= 3 else 3)
     pb = synth.make_problem(B, Hq, Hkv, 128, P, 1, dtype="bf16", dist=dist, seed=3)
@@ -97,7 +98,7 @@ def test_prefix_tc_splits(splits):
     assert_parity(o, ref, lse, lref, what=f"prefix splits={splits}")
 
 
-@pytest.mark.parametrize("variant,poly", [(3, 0), (5, 0), (5, 4), (5, 8), (3, 4)])
+@pytest.mark.parametrize("variant,poly", [(3, 0), (5, 0), (5, 4), (5, 8), (3, 4), (6, 0), (6, 4)])
 def test_prefix_tc2_growing_max(variant, poly):
     """Scores that grow along the prefix: the running max is raised block after block, which
     exercises the O/l correction and, for the speculative softmax, the redo path."""
@@ -118,7 +119,7 @@ def test_prefix_tc2_growing_max(variant, poly):
 
 
 @pytest.mark.parametrize("ctas", [1, 3, 7, 64, 148, 100000])
-@pytest.mark.parametrize("variant", [3, 4, 5])
+@pytest.mark.parametrize("variant", [3, 4, 5, 6])
 def test_prefix_tc2_stream_k_ctas(ctas, variant):
     """Stream-K piece boundaries fall inside items for most CTA counts; every piece is merged."""
     hydra.set_config("prefix_ctas", ctas)
@@ -350,7 +351,7 @@ def test_seqsplit_single_rank_nccl():
         tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("impl", [0, 2, 3, 4, 5])
+@pytest.mark.parametrize("impl", [0, 2, 3, 4, 5, 6])
 @pytest.mark.parametrize("per,g", [(300, 1), (100, 4)])
 def test_tree_large_groups(impl, per, g):
     """Groups with > 128 and > 256 stacked rows: both query tiles of a pair and several pairs

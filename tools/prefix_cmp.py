@@ -33,6 +33,11 @@ if mode == "variants":
         run(1024, 40, 40, 16384, 3, variant=variant)
         run(512, 32, 8, 32768, 3, variant=variant)
         run(1024, 40, 40, 4096, 3, variant=variant)
+elif mode == "split":
+    for variant, poly in ((3, 0), (6, 0), (6, 4), (3, 0), (6, 0)):
+        run(1024, 40, 40, 16384, 3, poly=poly, variant=variant)
+        run(512, 32, 8, 32768, 3, poly=poly, variant=variant)
+    hydra.set_config("prefix_poly", 0); hydra.set_config("prefix_variant", 3)
 elif mode == "spec":
     for variant, poly in ((3, 0), (5, 0), (5, 8), (5, 4), (3, 4)):
         run(1024, 40, 40, 16384, 3, poly=poly, variant=variant)
