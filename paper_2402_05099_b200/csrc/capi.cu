@@ -234,7 +234,10 @@ static int overlap_prefix_ctas(const hydra_heads *h, int64_t B, int64_t P, int64
   if (prefix_kind(h, B * g, P) != PK_TC2) return 0;
   const int sms = device_sm_count();
   if (g_overlap_prefix_ctas > 0) return (int)std::min<int64_t>(g_overlap_prefix_ctas, sms - 1);
-  const double R_P = 0.46, R_S = 1.0e5, BW = 7.0e6;
+  // R_P derated from 0.46 (full clock) for the ~1.45-1.7 GHz the 1 kW cap holds the SMs at in a
+  // sustained overlapped step: the tensor-bound prefix slows with the clock, the HBM-bound
+  // suffix does not (tools/power_profile.py, tools/overlap_sustained.py)
+  const double R_P = 0.38, R_S = 1.0e5, BW = 7.0e6;
   const int64_t pairs = (B * g + 255) / 256;
   const double pair_blocks = (double)pairs * h->num_kv_heads * ((P + 127) / 128);
   const double kv_bytes = (double)B * h->num_kv_heads * S_cap * h->head_dim * 4.0;

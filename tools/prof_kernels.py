@@ -13,11 +13,15 @@ ap.add_argument("--what", default="prefix", choices=["prefix", "suffix", "attn"]
 ap.add_argument("--splits", type=int, default=0)
 ap.add_argument("--suffix-impl", type=int, default=0)
 ap.add_argument("--prefix-impl", type=int, default=0)
+ap.add_argument("--suffix-ctas", type=int, default=0)
+ap.add_argument("--prefix-ctas", type=int, default=0)
 a = ap.parse_args()
 dev = torch.device("cuda:0")
 hydra.set_config("prefix_splits", a.splits)
 hydra.set_config("suffix_impl", a.suffix_impl)
 hydra.set_config("prefix_impl", a.prefix_impl)
+hydra.set_config("suffix_ctas", a.suffix_ctas)
+hydra.set_config("prefix_ctas", a.prefix_ctas)
 S = a.S if a.what != "prefix" else 1
 # plain N(0,1) on device is enough for profiling (values do not change the work)
 g = torch.Generator(device=dev); g.manual_seed(0)
