@@ -236,7 +236,15 @@ def run_tree(args, cfg):
     lens = torch.from_numpy(tp.lens.astype(np.int32)).to(dev)
     tree = hydra.Tree(tp.parent, tp.node_off, tp.node_len, tp.leaf_of_seq)
     capture, time_fn = make_timer(torch, dist, dev, world)
-    g = capture(lambda: hydra.tree_attention(q, tree, nk, nv, sk, sv, lens))
+    aux = torch.cuda.Stream(priority=-1)
+    # node attention on k SMs || tensor-core suffix on the rest (aux stream), or sequential:
+    # whichever is faster on a short probe
+    g_over = capture(lambda: hydra.tree_attention(q, tree, nk, nv, sk, sv, lens, aux_stream=aux))
+    k_over = int(hydra.get_config("last_overlap_k"))
+    g_seq = capture(lambda: hydra.tree_attention(q, tree, nk, nv, sk, sv, lens))
+    probe = max(3, min(20, args.steps // 5))
+    ms_over, ms_seq = time_fn(g_over.replay, probe, 2), time_fn(g_seq.replay, probe, 2)
+    g = g_over if ms_over <= ms_seq else g_seq
     with ClockSampler(local) as clk:
         ms = time_fn(g.replay, args.steps, args.warmup)
     g_suf = capture(lambda: hydra.suffix_attn(q, sk, sv, lens))
@@ -256,6 +264,8 @@ def run_tree(args, cfg):
                         "frac": round(suffix_bytes / (ms_suf * 1e-3) / 1e9 / hbm, 4), "traffic": None,
                         "algorithmic_bytes_per_launch": suffix_bytes, "launch_ms": round(ms_suf, 5)}
     line["tree_prefix_flops_per_step"] = flops
+    line["schedule"] = {"overlap": bool(ms_over <= ms_seq), "prefix_ctas": k_over, "ms_overlap_probe": round(ms_over, 5),
+                        "ms_sequential_probe": round(ms_seq, 5)}
     line["clocks"] = clk.summary()
     line["gpu_launches"] = args.steps * 4
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

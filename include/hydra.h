@@ -184,6 +184,10 @@ HYDRA_API size_t hydra_tree_workspace_size(const hydra_heads *h, const struct hy
  * §3.3).  Output as hydra_attn.  The first call for a given Hq/Hkv grouping
  * uploads a small work list to the device synchronously (not capturable); later
  * calls are pure launches.
+ * stream_aux: nullable second stream.  When given (and both the node attention and the
+ * suffix take their persistent tensor-core kernels), the node attention runs on k SMs
+ * on stream_aux while the suffix runs on the other SMs on `stream`, as in hydra_attn;
+ * stream_aux is forked from and joined back into `stream` inside the call.
  */
 HYDRA_API hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra_tree *t,
                              const void *q, int64_t q_sb, int64_t q_sh,
@@ -191,7 +195,7 @@ HYDRA_API hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra_
                              const void *sk, const void *sv, int64_t s_sb, int64_t s_st, int64_t s_sh,
                              int64_t S_cap, const int32_t *lens,
                              void *out, hydra_dtype out_dtype, float *lse_out,
-                             void *ws, size_t ws_bytes, void *stream);
+                             void *ws, size_t ws_bytes, void *stream, void *stream_aux);
 
 /* Bytes of device workspace the op needs for these sizes (0 if none). */
 HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, int64_t P, int64_t S_cap,

@@ -62,7 +62,7 @@ def load():
         "hydra_tree_group_size": (_i64, [_vp, _i32]),
         "hydra_tree_workspace_size": (_sz, [_HP, _vp, _i64]),
         "hydra_tree_attn": (st, [_HP, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _i64,
-                                 _i64, _vp, _vp, _i32, _vp, _vp, _sz, _vp]),
+                                 _i64, _vp, _vp, _i32, _vp, _vp, _sz, _vp, _vp]),
         "hydra_workspace_size": (_sz, [ctypes.c_int, _HP, _i64, _i64, _i64, _i32]),
         "hydra_set_config": (st, [ctypes.c_char_p, _i64]),
         "hydra_get_config": (_i64, [ctypes.c_char_p]),

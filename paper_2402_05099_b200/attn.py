@@ -255,8 +255,9 @@ class Tree:
 def tree_attention(q: torch.Tensor, tree: Tree, node_k: torch.Tensor, node_v: torch.Tensor,
                    suffix_k: torch.Tensor, suffix_v: torch.Tensor, suffix_lens: torch.Tensor,
                    scale: Optional[float] = None, out_dtype=None, return_lse: bool = False,
-                   workspace: Optional[torch.Tensor] = None, stream=None):
-    """Decomposition at every tree vertex (§3.3) + suffix + n-ary combine."""
+                   workspace: Optional[torch.Tensor] = None, stream=None, aux_stream=None):
+    """Decomposition at every tree vertex (§3.3) + suffix + n-ary combine.  With
+    `aux_stream` the node attention and the suffix run concurrently on disjoint SM sets."""
     q = _squeeze_q(q)
     node_k, node_v = _kv3(node_k, "node_k"), _kv3(node_v, "node_v")
     suffix_k, suffix_v = _kv4(suffix_k, "suffix_k"), _kv4(suffix_v, "suffix_v")
@@ -277,5 +278,7 @@ def tree_attention(q: torch.Tensor, tree: Tree, node_k: torch.Tensor, node_v: to
                               node_k.data_ptr(), node_v.data_ptr(), node_k.stride(0), node_k.stride(1),
                               suffix_k.data_ptr(), suffix_v.data_ptr(), ss[0], ss[1], ss[2], S_cap,
                               suffix_lens.data_ptr(), out.data_ptr(), _DT[out_dtype], _ptr(lse), _ptr(ws),
-                              ws.numel(), _stream_ptr(stream, q.device)), "hydra_tree_attn")
+                              ws.numel(), _stream_ptr(stream, q.device),
+                              _stream_ptr(aux_stream, q.device) if aux_stream is not None else None),
+          "hydra_tree_attn")
     return (out, lse) if return_lse else out

@@ -747,6 +747,43 @@ static int tree_prefix_splits(const hydra_heads *h, const hydra_tree *t) {
   return prefix_splits_tc(tiles * h->num_kv_heads, maxlen);
 }
 
+// SM split for the tree: node attention (persistent tcgen05 kernel in task mode) on k SMs
+// || tensor-core suffix on the rest.  Work units are
+// 256-row x 128-token blocks; a node group whose last tile pair holds <= 128 rows runs one
+// M=128 tile for it (half a unit).  Items are dealt whole, so a 10 % imbalance is allowed for.
+static int tree_overlap_ctas(const hydra_heads *h, const struct hydra_tree *t, int64_t S_cap) {
+  if (S_cap <= 0 || !use_suffix_tc(h, t->B, S_cap, true) || prefix_kind(h) != PK_TC2) return 0;
+  const int sms = device_sm_count();
+  if (g_overlap_prefix_ctas > 0) return (int)std::min<int64_t>(g_overlap_prefix_ctas, sms - 1);
+  const int g = h->num_q_heads / h->num_kv_heads;
+  double units = 0.0;
+  for (int n = 0; n < t->n_nodes; ++n) {
+    if (t->node_len[n] <= 0) continue;
+    const int64_t r = (int64_t)(t->grp_off[n + 1] - t->grp_off[n]) * g;
+    const double pairs = (double)(r / 256) + (r % 256 == 0 ? 0.0 : (r % 256 <= 128 ? 0.5 : 1.0));
+    units += pairs * h->num_kv_heads * (double)((t->node_len[n] + 127) / 128);
+  }
+  // R_P measured for the task-mode kernel on C5 (tools/tree_overlap_sweep.py: 0.26-0.28 units
+  // per us per SM on 15-64 SMs, below the flat kernel's 0.46: half-filled branch tiles,
+  // per-item prologue/epilogue); the node side is kept at <= 1/1.6 of the suffix time so
+  // the power-capped clock does not make it the critical path.  Measured at C5: overlap
+  // 1.32-1.34 ms at k = 32-64 vs 1.35 ms sequential (the suffix streams at ~6.5 TB/s on
+  // 84-116 SMs against 7.36 TB/s for the SIMT kernel on all SMs), so the bench keeps
+  // whichever schedule is faster.
+  const double R_P = 0.27, R_S = 1.0e5, BW = 7.0e6;
+  const double kv_bytes = (double)t->B * h->num_kv_heads * S_cap * h->head_dim * 4.0;
+  int best_k = 0;
+  double best = 1e300;
+  for (int k = 4; k <= sms - 8; ++k) {
+    const double tt = std::max(1.6 * 1.1 * units / (k * R_P), kv_bytes / std::min((sms - k) * R_S, BW));
+    if (tt < best) {
+      best = tt;
+      best_k = k;
+    }
+  }
+  return best_k;
+}
+
 extern "C" size_t hydra_tree_workspace_size(const hydra_heads *h, const struct hydra_tree *t, int64_t S_cap) {
   if (!t || check_heads(h) != HYDRA_OK) return 0;
   return part_bytes(h, t->B) * (size_t)(t->max_depth * tree_prefix_splits(h, t) + suffix_splits(h, t->B, S_cap));
@@ -757,7 +794,7 @@ extern "C" hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra
                                         int64_t kv_sh, const void *sk, const void *sv, int64_t s_sb, int64_t s_st,
                                         int64_t s_sh, int64_t S_cap, const int32_t *lens, void *out,
                                         hydra_dtype out_dtype, float *lse_out, void *ws, size_t ws_bytes,
-                                        void *stream) {
+                                        void *stream, void *stream_aux) {
   hydra_status st = check_heads(h);
   if (st) return st;
   if (!t) return fail(HYDRA_EINVAL, "tree is NULL");
@@ -771,18 +808,27 @@ extern "C" hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra
   if (!aligned16(q, es, {q_sb, q_sh}) || (T > 0 && (!aligned16(node_k, es, {kv_st, kv_sh}) || !aligned16(node_v, es, {}))) ||
       (S_cap > 0 && (!aligned16(sk, es, {s_sb, s_st, s_sh}) || !aligned16(sv, es, {}))))
     return fail(HYDRA_EINVAL, "q/k/v base pointers and strides must be 16-byte aligned");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cudaStream_t sa = stream_aux ? reinterpret_cast<cudaStream_t>(stream_aux) : s;
+  const int k_over = (sa != s && T > 0) ? tree_overlap_ctas(h, t, S_cap) : 0;
+  if (k_over == 0) sa = s;
+  g_last_overlap_k = k_over;
+  const int sms = device_sm_count();
   const int np = tree_prefix_splits(h, t);
-  const int ns = suffix_splits(h, B, S_cap);
+  const int ns = suffix_splits(h, B, S_cap, k_over > 0);
   const int n_parts = t->max_depth * np + ns;
   const size_t need = part_bytes(h, B) * n_parts;
   if (!ws || ws_bytes < need) return fail(HYDRA_ENOMEM, "workspace too small: need %zu bytes", need);
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int g = h->num_q_heads / h->num_kv_heads;
   const int64_t rows = B * h->num_q_heads;
   PartsView all = parts_in_ws(ws, h, B, n_parts);
   // Sequences whose path is shorter than max_depth leave slots empty: mark all node slots -inf.
   st = launch_fill_neg_inf(all.lse, all.lse_stride * (int64_t)(t->max_depth * np), s);
   if (st) return cuda_fail("fill");
+  if (sa != s) {
+    if (cudaEventRecord(events().fork, s) != cudaSuccess || cudaStreamWaitEvent(sa, events().fork, 0) != cudaSuccess)
+      return cuda_fail("fork");
+  }
   const float sl2 = scale_of(h) * 1.4426950408889634f;
 
   const PrefixKind kind = prefix_kind(h);
@@ -850,7 +896,7 @@ extern "C" hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra
     a.poly_every = (int32_t)g_prefix_poly;
     a.variant = (int32_t)g_prefix_variant;
       // the work list holds 256-row tile pairs for v3 and 128-row tiles for v1
-      st = kind == PK_TC2 ? launch_prefix_tc2(a, prefix_ctas(), s) : launch_prefix_tc(a, s);
+      st = kind == PK_TC2 ? launch_prefix_tc2(a, k_over > 0 ? k_over : prefix_ctas(), sa) : launch_prefix_tc(a, sa);
       if (st) return cuda_fail("tree prefix tcgen05 launch");
     }
   } else {
@@ -881,7 +927,7 @@ extern "C" hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra
       p.lse = all.lse + all.lse_stride * (int64_t)(t->depth[n] * np);
       p.o_split_stride = all.o_stride;
       p.lse_split_stride = all.lse_stride;
-      st = launch_decode(p, h->dtype, h->head_dim, s);
+      st = launch_decode(p, h->dtype, h->head_dim, sa);
       if (st) return st == HYDRA_ECUDA ? cuda_fail("tree node SIMT launch") : fail(st, "tree node SIMT");
     }
   }
@@ -889,11 +935,16 @@ extern "C" hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra
   suf.o = all.o + all.o_stride * (int64_t)(t->max_depth * np);
   suf.lse = all.lse + all.lse_stride * (int64_t)(t->max_depth * np);
   if (S_cap > 0) {
-    st = run_suffix(h, B, q, q_sb, q_sh, sk, sv, s_sb, s_st, s_sh, S_cap, lens, ns, suf, s);
+    st = run_suffix(h, B, q, q_sb, q_sh, sk, sv, s_sb, s_st, s_sh, S_cap, lens, ns, suf, s,
+                    k_over > 0 ? std::max(1, sms - k_over) : 0);
     if (st) return st;
   } else {
     st = launch_fill_neg_inf(suf.lse, rows, s);
     if (st) return cuda_fail("fill");
+  }
+  if (sa != s) {
+    if (cudaEventRecord(events().join, sa) != cudaSuccess || cudaStreamWaitEvent(s, events().join, 0) != cudaSuccess)
+      return cuda_fail("join");
   }
   return run_combine(rows, h->head_dim, n_parts, all, out, out_dtype, lse_out, s);
 }

@@ -24,8 +24,8 @@
 //   warps 8-11  epilogue (thread = head dim): O^T / l, LSE, coalesced stores, after the
 //               item's last PV -- off the softmax warps' critical path
 // Reads lens[b] itself, so only blocks with valid tokens move.  Tokens >= lens[b] inside
-// the last block: their scores are masked to -inf, and their V rows are zeroed in shared
-// memory before the PV MMA (0 * NaN would poison O).
+// the last block: their scores are masked to -inf, and the PV warp zeroes their V rows in
+// shared memory before the PV MMA (0 * NaN would poison O).
 // Per-SM rate (tools/suffix_rate.py, C3 shape): 112 GB/s at 16 CTAs, 100 at 64; 7.0 TB/s
 // on 80-92 SMs.  The earlier single-issuer version (S(n) then PV(n-1) from one thread,
 // epilogue on the softmax warps) coupled every V slot release to the next K tile and the
@@ -318,10 +318,15 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
       }
     }
   } else if (warp == 12) {
-    // ================= PV-MMA issuer =================
-    if (ptx::elect_one() && !(P.debug & 256)) {
+    // ================= PV-MMA issuer (one elected lane issues; the warp zeroes ragged V rows) =================
+    // V rows past lens[b] in an item's last block are zeroed here, after the tile landed and
+    // before the PV MMA reads it (0 * NaN would poison O).  The softmax warps cannot do it:
+    // they may run up to three rounds ahead of the V ring, where a parity wait on v_full
+    // could not tell the tile's phase from the one two loads earlier.
+    if (!(P.debug & 256)) {
+      const bool leader = ptx::elect_one();
       constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(HD, NQ, false) | (1u << 15);  // A=V^T (MN-major), B=P^T
-      long long *tr = blockIdx.x == 0 ? P.trace : nullptr;
+      long long *tr = (blockIdx.x == 0 && leader) ? P.trace : nullptr;
       RoundCursor<CB> pc;
       pc.init(P);
       while (pc.valid) {
@@ -333,19 +338,35 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
           const uint32_t gbc = pc.gb + c, st = gbc % NS;
           ptx::mbar_wait(&v_full[st], (gbc / NS) & 1);
           trace(tr, 12, gbc);
-          ptx::tc_fence_after();
-          const uint32_t v_addr = ptx::smem_u32(smem + OFF_V + st * TILE);
-          const uint32_t p_addr = p_base + c * PTILE;
+          const int valid = pc.len - (pc.n0 + c) * BT;
+          if (valid < BT) {  // ragged last block: zero rows valid..127 of both 64-column panels
+            uint8_t *sV = smem + OFF_V + st * TILE;
+            for (int i = lane; i < (BT - valid) * 16; i += 32) {
+              const int row = valid + i / 16, ch = i % 16;
+              *reinterpret_cast<uint4 *>(sV + (ch / 8) * PANEL + row * 128 + (ch % 8) * 16) = make_uint4(0, 0, 0, 0);
+            }
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+          }
+          if (leader) {
+            ptx::tc_fence_after();
+            const uint32_t v_addr = ptx::smem_u32(smem + OFF_V + st * TILE);
+            const uint32_t p_addr = p_base + c * PTILE;
 #pragma unroll
-          for (int kk = 0; kk < BT / 16; ++kk)
-            ptx::mma_ss(tmem + O_COL + ob * NQ, ptx::smem_desc_sw128(v_addr + kk * 2048, PANEL, 1024),
-                        ptx::smem_desc_sw128(p_addr + (kk / 4) * PPANEL + (kk % 4) * 32, 16, 1024), idesc_pv,
-                        (pc.n0 > 0 || c > 0 || kk > 0));
-          ptx::mma_commit(&v_empty[st]);
+            for (int kk = 0; kk < BT / 16; ++kk)
+              ptx::mma_ss(tmem + O_COL + ob * NQ, ptx::smem_desc_sw128(v_addr + kk * 2048, PANEL, 1024),
+                          ptx::smem_desc_sw128(p_addr + (kk / 4) * PPANEL + (kk % 4) * 32, 16, 1024), idesc_pv,
+                          (pc.n0 > 0 || c > 0 || kk > 0));
+            ptx::mma_commit(&v_empty[st]);
+          }
+          __syncwarp();
         }
-        ptx::mma_commit(&pv_done[slot]);
-        trace(tr, 8, pc.gr);
-        if (pc.n0 + pc.nb >= pc.nblk) ptx::mma_commit(&o_full[ob]);
+        if (leader) {
+          ptx::mma_commit(&pv_done[slot]);
+          trace(tr, 8, pc.gr);
+          if (pc.n0 + pc.nb >= pc.nblk) ptx::mma_commit(&o_full[ob]);
+        }
+        __syncwarp();
         pc.next(P);
       }
     }
@@ -465,18 +486,6 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
           for (int h = 0; h < G; ++h)
             *reinterpret_cast<__nv_bfloat16 *>(sp + h * 128 + ((cc ^ (h % 8)) * 16) + e * 2) =
                 __float2bfloat16_rn(p[c][h]);
-        }
-        if ((n0 + nb) * BT > len) {  // ragged last block of the item (always the round's last)
-          const uint32_t gl = gb + nb - 1;
-          ptx::mbar_wait(&v_full[gl % NS], (gl / NS) & 1);  // V tile landed
-          if (!tok[nb - 1]) {  // rows past lens[b]: zero the V row (0 * NaN would poison O)
-            uint8_t *vrow = smem + OFF_V + (gl % NS) * TILE + r * 128;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              *reinterpret_cast<uint4 *>(vrow + q * 16) = make_uint4(0, 0, 0, 0);
-              *reinterpret_cast<uint4 *>(vrow + PANEL + q * 16) = make_uint4(0, 0, 0, 0);
-            }
-          }
         }
         ptx::fence_proxy_async_smem();
         ptx::tc_fence_before();

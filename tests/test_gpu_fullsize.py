@@ -93,15 +93,18 @@ def test_c4_full_size_single_rank_seqsplit():
     check_rows(out, lse, ref, lref, rows, "C4 seq-split")
 
 
-def test_c5_tree_full_size():
-    """Tree: 4096-token root -> 16 x 1024-token branches -> 64 sequences each, 512-token suffixes."""
+@pytest.mark.parametrize("overlap", [False, True])
+def test_c5_tree_full_size(overlap):
+    """Tree: 4096-token root -> 16 x 1024-token branches -> 64 sequences each, 512-token suffixes
+    (overlap: node attention on k SMs || tensor-core suffix, the bench's schedule)."""
     parent, node_len, leaf = synth.two_level_tree(4096, 16, 1024, 64)
     tp = synth.make_tree_problem(parent, node_len, leaf, 32, 32, 128, 512, dtype="bf16", dist="mixed", seed=5)
     t = tree_to(tp, DEV)
     tree = hydra.Tree(tp.parent, tp.node_off, tp.node_len, tp.leaf_of_seq)
     out, lse = hydra.tree_attention(t["q"], tree, t["node_k"], t["node_v"], t["sk"], t["sv"], t["lens"],
-                                    return_lse=True)
+                                    return_lse=True, aux_stream=torch.cuda.Stream() if overlap else None)
     torch.cuda.synchronize()
+    assert (hydra.get_config("last_overlap_k") > 0) == overlap
     rows = sample_rows(1024, 32)
     ref, lref = oracle.tree_attention(tp, rows=rows)
     check_rows(out, lse, ref, lref, rows, "C5 tree")

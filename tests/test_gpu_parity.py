@@ -224,6 +224,21 @@ def test_suffix_tc_ctas_and_ragged(ctas, cb):
     assert_parity(o, ref, lse, lref, what=f"suffix tc ctas={ctas} cb={cb}")
 
 
+def test_suffix_tc_ragged_repeat():
+    """Many ragged items with NaN-poisoned padding, repeated: the PV warp must zero the padded V
+    rows of exactly the landed tile (a parity wait run ahead of the V ring once zeroed the wrong
+    phase's tile and let NaN through, intermittently)."""
+    hydra.set_config("suffix_impl", 2)
+    lens = np.arange(600) % 301
+    pb = synth.make_problem(600, 4, 4, 128, 0, 300, lens=lens, dtype="bf16", dist="boundary", seed=18)
+    t = problem_to(pb, DEV)
+    ref, lref = oracle.suffix_only(pb)
+    for _ in range(8):
+        o, lse = hydra.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
+        torch.cuda.synchronize()
+        assert_parity(o, ref, lse, lref, what="suffix tc ragged repeat")
+
+
 def test_composite_f32_output_is_tighter():
     pb = synth.make_problem(16, 8, 2, 128, 600, 50, dtype="bf16", dist="mixed", seed=9)
     out, lse = run_flat(pb, out_dtype=torch.float32)
@@ -286,6 +301,27 @@ def test_tree_parity(impl, dtype):
     torch.cuda.synchronize()
     ref, lref = oracle.tree_attention(tp)
     assert_parity(out, ref, lse, lref, dtype=dtype, what=f"tree impl={impl}")
+    tree.destroy()
+
+
+@pytest.mark.parametrize("k", [1, 37, 147])
+@pytest.mark.parametrize("per,g", [(300, 1), (100, 4)])
+def test_tree_sm_partitioned(k, per, g):
+    """Tree node attention on k SMs (aux stream) || tensor-core suffix on the other SMs."""
+    hydra.set_config("prefix_impl", 3)
+    hydra.set_config("suffix_impl", 2)
+    hydra.set_config("overlap_prefix_ctas", k)
+    parent, node_len, leaf = synth.two_level_tree(300, 2, 200, per)
+    tp = synth.make_tree_problem(parent, node_len, leaf, 4 * g, 4, 128, 300, dtype="bf16", dist="boundary",
+                                 seed=23, lens=np.arange(2 * per) % 301)
+    t = tree_to(tp, DEV)
+    tree = hydra.Tree(tp.parent, tp.node_off, tp.node_len, tp.leaf_of_seq)
+    out, lse = hydra.tree_attention(t["q"], tree, t["node_k"], t["node_v"], t["sk"], t["sv"], t["lens"],
+                                    return_lse=True, aux_stream=torch.cuda.Stream())
+    torch.cuda.synchronize()
+    assert hydra.get_config("last_overlap_k") == k
+    ref, lref = oracle.tree_attention(tp)
+    assert_parity(out, ref, lse, lref, what=f"tree partitioned k={k}")
     tree.destroy()
 
 
