@@ -162,12 +162,13 @@ static int prefix_bn() { return g_prefix_variant == 4 ? 64 : 128; }  // KV token
 // B/P-dependent choice (rows = stacked query rows per KV head, P = KV tokens per row):
 // the persistent kernel amortises its per-segment Q load / epilogue only when every CTA
 // owns enough 128-token blocks; small problems run the one-tile kernel (more parallelism).
-static PrefixKind prefix_kind(const hydra_heads *h, int64_t rows = -1, int64_t P = -1) {
+// ctas: the persistent kernel's CTA count (0 = all SMs, or the prefix_ctas override).
+static PrefixKind prefix_kind(const hydra_heads *h, int64_t rows = -1, int64_t P = -1, int ctas = 0) {
   if (g_prefix_impl == 1 || !prefix_tc_supported(h)) return PK_SIMT;
   if (g_prefix_impl == 2) return PK_TC1;
   if (g_prefix_impl == 3 || rows < 0) return PK_TC2;
   const int64_t blocks = ((rows + 255) / 256) * h->num_kv_heads * ((P + 127) / 128);
-  return blocks >= 24 * (int64_t)prefix_ctas() ? PK_TC2 : PK_TC1;
+  return blocks >= 24 * (int64_t)(ctas > 0 ? ctas : prefix_ctas()) ? PK_TC2 : PK_TC1;
 }
 static bool use_tc(const hydra_heads *h) { return prefix_kind(h) != PK_SIMT; }
 
@@ -208,7 +209,7 @@ static int prefix_splits_simt(const hydra_heads *h, int64_t B, int64_t P) {
 static int prefix_splits(const hydra_heads *h, int64_t B, int64_t P, int tc2_ctas = 0) {
   if (P <= 0) return 1;
   const int g = h->num_q_heads / h->num_kv_heads;
-  switch (prefix_kind(h, B * g, P)) {
+  switch (prefix_kind(h, B * g, P, tc2_ctas)) {
     case PK_TC2:
       return prefix_tc2_slots(B, g, h->num_kv_heads, P, tc2_ctas > 0 ? tc2_ctas : prefix_ctas(), prefix_bn());
     case PK_TC1:
@@ -231,7 +232,7 @@ static int prefix_splits(const hydra_heads *h, int64_t B, int64_t P, int tc2_cta
 static int overlap_prefix_ctas(const hydra_heads *h, int64_t B, int64_t P, int64_t S_cap) {
   if (P <= 0 || S_cap <= 0 || !use_suffix_tc(h, B, S_cap, true)) return 0;
   const int g = h->num_q_heads / h->num_kv_heads;
-  if (prefix_kind(h, B * g, P) != PK_TC2) return 0;
+  if (prefix_kind(h, B * g, P, 8) != PK_TC2) return 0;  // not even 8 persistent CTAs' worth of blocks
   const int sms = device_sm_count();
   if (g_overlap_prefix_ctas > 0) return (int)std::min<int64_t>(g_overlap_prefix_ctas, sms - 1);
   // R_P derated from 0.46 (full clock) for the ~1.45-1.7 GHz the 1 kW cap holds the SMs at in a
@@ -244,6 +245,7 @@ static int overlap_prefix_ctas(const hydra_heads *h, int64_t B, int64_t P, int64
   int best_k = 0;
   double best = 1e300;
   for (int k = 8; k <= sms - 8; ++k) {
+    if (prefix_kind(h, B * g, P, k) != PK_TC2) break;  // too few blocks per CTA beyond this k
     if (prefix_tc2_ctas(B, g, h->num_kv_heads, P, k, prefix_bn()) != k) continue;  // plan would idle SMs
     const double t = std::max(pair_blocks / (k * R_P), kv_bytes / std::min((sms - k) * R_S, BW));
     if (t < best) {
@@ -279,7 +281,7 @@ static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, i
                                const PartsView &dst, cudaStream_t s, int tc2_ctas = 0) {
   const int g = h->num_q_heads / h->num_kv_heads;
   const float sl2 = scale_of(h) * 1.4426950408889634f;
-  const PrefixKind kind = prefix_kind(h, B * g, P);
+  const PrefixKind kind = prefix_kind(h, B * g, P, tc2_ctas);
   if (kind != PK_SIMT) {
     PrefixTcArgs a{};
     a.q = q;
