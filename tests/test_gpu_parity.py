@@ -144,7 +144,8 @@ def test_prefix_simt_bf16():
 
 # ---------------------------------------------------------------- suffix kernel
 @pytest.mark.parametrize("B,Hq,Hkv,d,S", [(7, 8, 8, 128, 300), (5, 16, 4, 128, 77), (6, 16, 1, 128, 40),
-                                          (4, 8, 2, 64, 129), (3, 32, 2, 128, 64), (9, 12, 4, 128, 513)])
+                                          (4, 8, 2, 64, 129), (3, 32, 2, 128, 64), (9, 12, 4, 128, 513),
+                                          (8, 16, 8, 128, 200), (4, 32, 4, 128, 300)])  # g = 2, g = 8
 @pytest.mark.parametrize("impl", [1, 2, 3])  # 1: SIMT split-K, 2/3: persistent tensor-core, 2 / 1 blocks per round
 def test_suffix_parity(B, Hq, Hkv, d, S, impl):
     hydra.set_config("suffix_impl", min(impl, 2))
@@ -207,6 +208,19 @@ def test_composite_sm_partitioned(k, B, Hq, Hkv, P, S):
     out, lse = run_flat(pb, aux=True)
     ref, lref = oracle.flat_attention(pb)
     assert_parity(out, ref, lse, lref, what=f"partitioned k={k}")
+
+
+def test_composite_auto_overlap_small_shard():
+    """A 5-KV-head shard (C3 on 8 GPUs, scaled down): too few prefix blocks for 148 persistent
+    CTAs but enough for the automatic SM split, which must pick the persistent kernel for its
+    own CTA count."""
+    rng = np.random.default_rng(31)
+    lens = rng.integers(64, 129, 256)
+    pb = synth.make_problem(256, 5, 5, 128, 8192, 128, lens=lens, dtype="bf16", dist="mixed", seed=31)
+    out, lse = run_flat(pb, aux=True)
+    assert hydra.get_config("last_overlap_k") > 0
+    ref, lref = oracle.flat_attention(pb)
+    assert_parity(out, ref, lse, lref, what="auto overlap, 5-head shard")
 
 
 @pytest.mark.parametrize("ctas", [1, 5, 148])
