@@ -1,3 +1,5 @@
+"""Stress: repeated tree (SM-partitioned) and ragged tensor-core suffix runs with NaN-poisoned
+padding, counting parity failures (caught an intermittent V-ring race; diagnostics)."""
 import sys, numpy as np, torch
 sys.path.insert(0, '.')
 import oracle, synth
