@@ -41,7 +41,7 @@ static hydra_status cuda_fail(const char *what) {
 
 static std::atomic<int64_t> g_prefix_impl{0}, g_prefix_splits{0}, g_suffix_splits{0}, g_tc_debug{0},
     g_prefix_stages{3}, g_suffix_unroll{4}, g_prefix_ctas{0}, g_suffix_impl{0}, g_suffix_ctas{0},
-    g_overlap_prefix_ctas{0}, g_prefix_poly{0}, g_prefix_variant{6}, g_prefix_trace{0}, g_suffix_cb{2}, g_suffix_trace{0},
+    g_overlap_prefix_ctas{0}, g_prefix_poly{4}, g_prefix_variant{6}, g_prefix_trace{0}, g_suffix_cb{2}, g_suffix_trace{0},
     g_last_overlap_k{0};  // read-only: prefix CTAs of the last hydra_attn overlap split (0 = sequential)
 
 extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {

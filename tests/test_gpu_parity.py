@@ -23,14 +23,15 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(autouse=True)
 def _reset_config():
     keys = ("prefix_impl", "prefix_splits", "suffix_splits", "tc_debug_variant", "prefix_ctas", "suffix_impl",
-            "suffix_ctas", "overlap_prefix_ctas", "prefix_poly")
+            "suffix_ctas", "overlap_prefix_ctas")
     for k in keys:
         hydra.set_config(k, 0)
-    hydra.set_config("prefix_variant", 6)
-    hydra.set_config("suffix_cb", 2)
+    defaults = {"prefix_variant": 6, "suffix_cb": 2, "prefix_poly": 4}  # the library defaults
+    for k, v in defaults.items():
+        hydra.set_config(k, v)
     yield
-    hydra.set_config("prefix_variant", 6)
-    hydra.set_config("suffix_cb", 2)
+    for k, v in defaults.items():
+        hydra.set_config(k, v)
     for k in keys:
         hydra.set_config(k, 0)
 
@@ -113,7 +114,7 @@ def test_prefix_tc2_growing_max(variant, poly):
         o, lse = hydra.prefix_attn(t["q"], t["pk"], t["pv"])
         torch.cuda.synchronize()
     finally:
-        hydra.set_config("prefix_poly", 0)
+        hydra.set_config("prefix_poly", 4)
     ref, lref = oracle.prefix_only(pb)
     assert_parity(o, ref, lse, lref, what=f"prefix growing max v{variant} poly{poly}")
 

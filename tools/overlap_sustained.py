@@ -27,6 +27,8 @@ def graph(fn):
     with torch.cuda.graph(gr): fn()
     return gr
 graphs = {}
+if os.environ.get("POLY") is not None:
+    hydra.set_config("prefix_poly", int(os.environ["POLY"]))
 for k in ks:
     hydra.set_config("overlap_prefix_ctas", k)
     graphs[k] = graph(lambda: hydra.hydragen_attention(q, pk, pv, sk, sv, lens, out=out, workspace=ws, aux_stream=aux))

@@ -38,6 +38,12 @@ elif mode == "split":
         run(1024, 40, 40, 16384, 3, poly=poly, variant=variant)
         run(512, 32, 8, 32768, 3, poly=poly, variant=variant)
     hydra.set_config("prefix_poly", 0); hydra.set_config("prefix_variant", 3)
+elif mode == "v8":
+    for variant, poly in ((6, 0), (8, 0), (8, 8), (8, 4), (8, 3), (6, 4)):
+        run(1024, 40, 40, 16384, 3, variant=variant, poly=poly)
+        run(512, 32, 8, 32768, 3, variant=variant, poly=poly)
+    hydra.set_config("prefix_poly", 0)
+    hydra.set_config("prefix_variant", 6)
 elif mode == "spec":
     for variant, poly in ((3, 0), (5, 0), (5, 8), (5, 4), (3, 4)):
         run(1024, 40, 40, 16384, 3, poly=poly, variant=variant)
