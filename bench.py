@@ -47,6 +47,11 @@ CONFIGS = {
     "c4": dict(B=512, Hq=32, Hkv=8, d=128, P=32768, S=128, kind="seqsplit",
                name="Llama-3-8B GQA attention shape (32 q / 8 kv, d=128), B=512, prefix 32768 split along the "
                     "sequence across ranks with an NCCL (O, LSE) all-gather, suffix 128"),
+    # the paper's long-document shape (P:198, 19,947-token document,
+    # Yi-6B-200k-like heads 32 q / 4 kv); suffix length assumed 128 (the paper gives none)
+    "c6_longdoc": dict(B=256, Hq=32, Hkv=4, d=128, P=19947, S=128,
+                       name="long-document shape (Yi-6B-like 32 q / 4 kv heads, d=128), B=256, prefix 19947, "
+                            "suffix 128 (assumed)"),
     # two-level sharing tree (tree_attention)
     "c5": dict(B=1024, Hq=32, Hkv=32, d=128, P=4096, S=512, kind="tree", branches=16, branch_len=1024,
                name="tree sharing: 4096-token root -> 16 branches x 1024 tokens -> 64 sequences each with 512-token "

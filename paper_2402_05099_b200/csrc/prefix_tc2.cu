@@ -39,6 +39,12 @@
 
 namespace hydra {
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 namespace tc2 {
 constexpr int BM = 128;  // rows per query tile (UMMA M)
 constexpr int BN = 128;  // KV tokens per block
@@ -184,6 +190,9 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
            *o_free = q_full + 8, *p_half = q_full + 10;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + N_BARS);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // diagnostics: every CTA's globaltimer at entry / setup done / first S / last P / exit
+  long long *cta_tr = (P.trace && blockIdx.x < 256) ? P.trace + 14 * kTraceN + blockIdx.x * 8 : nullptr;
+  if (cta_tr && threadIdx.x == 0) cta_tr[0] = (long long)gtimer();
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&P.tmK);
@@ -209,6 +218,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (cta_tr && threadIdx.x == 0) cta_tr[1] = (long long)gtimer();
 
   // Register rebalancing per warpgroup (inside disjoint role branches so ptxas allocates each
   // region separately): producer / MMA / idle warps need few registers, the two softmax
@@ -388,6 +398,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
         if (tr && sc < kTraceN) tr[(3 * t + 0) * kTraceN + sc] = clock64();
         ptx::mbar_wait(&s_full[t], sc & 1);
         if (tr && sc < kTraceN) tr[(3 * t + 1) * kTraceN + sc] = clock64();
+        if (cta_tr && sc == 0 && t == 0 && quarter == 0 && lane == 0) cta_tr[2] = (long long)gtimer();
         ++sc;
         ptx::tc_fence_after();
         if (P.debug & 2) {  // timing experiment only: MMA pipeline without the softmax math
@@ -590,6 +601,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
     }
   }
 
+  if (cta_tr && warp == 4 && lane == 0) cta_tr[3] = (long long)gtimer();  // tile-0 softmax/epilogue done
   ptx::tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -597,6 +609,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
     ptx::tc_fence_after();
     ptx::tmem_dealloc<TMEM_COLS>(tmem);
   }
+  if (cta_tr && threadIdx.x == 0) cta_tr[4] = (long long)gtimer();
 }
 
 // ===================================================================================

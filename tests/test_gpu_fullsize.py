@@ -69,6 +69,22 @@ def test_c2_full_size_ragged():
     check_rows(out, lse, ref, lref, rows, "C2")
 
 
+@pytest.mark.parametrize("overlap", [False, True])
+def test_c6_longdoc_full_size(overlap):
+    """Long-document shape: 19,947-token prefix (not a multiple of the 128-token tile),
+    32 q / 4 kv heads (g = 8), B = 256, ragged suffixes up to 128."""
+    lens = np.random.default_rng(6).integers(1, 129, 256)
+    pb = synth.make_problem(256, 32, 4, 128, 19947, 128, lens=lens, dtype="bf16", dist="boundary", seed=6)
+    t = problem_to(pb, DEV)
+    aux = torch.cuda.Stream(priority=-1) if overlap else None
+    out, lse = hydra.hydragen_attention(t["q"], t["pk"], t["pv"], t["sk"], t["sv"], t["lens"], return_lse=True,
+                                        aux_stream=aux)
+    torch.cuda.synchronize()
+    rows = sample_rows(256, 32)
+    ref, lref = oracle.flat_attention(pb, rows=rows)
+    check_rows(out, lse, ref, lref, rows, f"long-doc overlap={overlap}")
+
+
 def test_c4_full_size_single_rank_seqsplit():
     """Llama-3-8B GQA shape, B=512, prefix 32768, suffix 128, through dist.seqsplit_attention (1 rank)."""
     import socket

@@ -7,7 +7,7 @@ import torch
 import paper_2402_05099_b200 as hydra
 ks = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "48,56,60,64,68,72,76").split(",")]
 variant = int(sys.argv[2]) if len(sys.argv) > 2 else 3
-B, H, P, S = 1024, int(os.environ.get("H", 40)), int(os.environ.get("P", 16384)), 256
+B, H, P, S = int(os.environ.get("B", 1024)), int(os.environ.get("H", 40)), int(os.environ.get("P", 16384)), int(os.environ.get("S", 256))
 dev = torch.device("cuda:0")
 g = torch.Generator(device=dev); g.manual_seed(0)
 q = torch.randn(B, H, 128, device=dev, generator=g).bfloat16()

@@ -44,6 +44,13 @@ elif mode == "v8":
         run(512, 32, 8, 32768, 3, variant=variant, poly=poly)
     hydra.set_config("prefix_poly", 0)
     hydra.set_config("prefix_variant", 6)
+elif mode == "longdoc":
+    for P in (19947, 39894, 79788):
+        run(256, 32, 4, P, 3, variant=6, poly=4)
+    run(512, 32, 8, 32768, 3, variant=6, poly=4)
+    run(256, 32, 8, 32768, 3, variant=6, poly=4)
+    run(1024, 5, 5, 16384, 3, variant=6, poly=4)
+    run(1024, 40, 40, 16384, 3, variant=6, poly=4)
 elif mode == "spec":
     for variant, poly in ((3, 0), (5, 0), (5, 8), (5, 4), (3, 4)):
         run(1024, 40, 40, 16384, 3, poly=poly, variant=variant)
