@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhydra.so")
+# HYDRA_LIB_PATH: load another build of the library (A/B timing of two builds on one box)
+LIB_PATH = os.environ.get("HYDRA_LIB_PATH") or os.path.join(_HERE, "libhydra.so")
 
 HYDRA_OK, HYDRA_EINVAL, HYDRA_ESHAPE, HYDRA_EUNSUPPORTED, HYDRA_ECUDA, HYDRA_ENCCL, HYDRA_ENOMEM = range(7)
 HYDRA_BF16, HYDRA_F32, HYDRA_F16 = 0, 1, 2
