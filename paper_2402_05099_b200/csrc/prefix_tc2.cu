@@ -283,15 +283,15 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
           }
           ptx::mma_commit(&s_full[t]);
         };
-        for (int t = 0; t < ntile; ++t) {
-          ptx::mbar_wait(&q_full[t], qc[t] & 1);
-          ++qc[t];
-        }
-        {  // prologue: S_t(0)
+        {  // prologue: S_t(0), each tile as soon as its Q is in shared memory
           const int st = gb % NS;
           ptx::mbar_wait(&k_full[st], (gb / NS) & 1);
-          ptx::tc_fence_after();
-          for (int t = 0; t < ntile; ++t) issue_s(t, st);
+          for (int t = 0; t < ntile; ++t) {
+            ptx::mbar_wait(&q_full[t], qc[t] & 1);
+            ++qc[t];
+            ptx::tc_fence_after();
+            issue_s(t, st);
+          }
           ptx::mma_commit(&k_empty[st]);
         }
         for (int n = 0; n < it.nblk; ++n) {
@@ -585,11 +585,19 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
 #pragma unroll
         for (int i = 0; i < 32; ++i) stage[lane * 32 + (i ^ lane)] = __float_as_uint(__uint_as_float(ov[i]) * inv);
         __syncwarp();
-#pragma unroll 4
-        for (int rw = 0; rw < 32; ++rw) {
+        // 4 rows per step, 16 B per lane: lane = 8 * (row % 4) + column group (4 floats);
+        // conflict-free: (4 cg + k) ^ rw spans 32 banks over the 8 column groups x 4 rows
+        const int cg = lane % 8;
+#pragma unroll
+        for (int rw4 = 0; rw4 < 8; ++rw4) {
+          const int rw = rw4 * 4 + lane / 8;
           const uint64_t base = __shfl_sync(0xffffffffu, my_row, rw);
-          const uint32_t v = stage[rw * 32 + (lane ^ rw)];
-          if (base) reinterpret_cast<float *>(base)[c * 32 + lane] = __uint_as_float(v);
+          float4 v;
+          v.x = __uint_as_float(stage[rw * 32 + ((cg * 4 + 0) ^ rw)]);
+          v.y = __uint_as_float(stage[rw * 32 + ((cg * 4 + 1) ^ rw)]);
+          v.z = __uint_as_float(stage[rw * 32 + ((cg * 4 + 2) ^ rw)]);
+          v.w = __uint_as_float(stage[rw * 32 + ((cg * 4 + 3) ^ rw)]);
+          if (base) reinterpret_cast<float4 *>(base)[c * 8 + cg] = v;
         }
         __syncwarp();
       }
