@@ -63,8 +63,8 @@ CONFIGS = {
 # config (profiles/r1b_ncu_full_*.csv: dram__bytes_read.sum + dram__bytes_write.sum)
 NCU_TRAFFIC = {
     ("c3_16k", "decode_attn_kernel"): 5379256000 + 9611264,
-    ("c3_16k", "suffix_tc_kernel"): 5379289000 + 24782080,   # profiles/r1h_suffix_tc_76_raw.csv (76 CTAs, k = 72)
-    ("c3_16k", "prefix_tc2_kernel"): 354299904 + 21155328,   # profiles/r1h_prefix_tc2_raw.csv (variant 6)
+    ("c3_16k", "suffix_tc_kernel"): 5379763000 + 25173504,   # profiles/r1j_suffix_tc_76_raw.csv (76 CTAs, k = 72)
+    ("c3_16k", "prefix_tc2_kernel"): 355116288 + 23960320,   # profiles/r1j_prefix_tc2_raw.csv (variant 6, poly 4)
 }
 
 
