@@ -767,17 +767,16 @@ static int tree_overlap_ctas(const hydra_heads *h, const struct hydra_tree *t, i
   }
   // R_P measured for the task-mode kernel on C5 (tools/tree_overlap_sweep.py: 0.26-0.28 units
   // per us per SM on 15-64 SMs, below the flat kernel's 0.46: half-filled branch tiles,
-  // per-item prologue/epilogue); the node side is kept at <= 1/1.6 of the suffix time so
-  // the power-capped clock does not make it the critical path.  Measured at C5: overlap
-  // 1.32-1.34 ms at k = 32-64 vs 1.35 ms sequential (the suffix streams at ~6.5 TB/s on
-  // 84-116 SMs against 7.36 TB/s for the SIMT kernel on all SMs), so the bench keeps
-  // whichever schedule is faster.
+  // per-item prologue/epilogue); the node side is kept at <= 1/2.3 of the suffix time
+  // (interference and the power-capped clock slow it further when both run).  Measured at
+  // C5 (tools/tree_overlap_sweep.py): 1.344 / 1.312 / 1.322 / 1.379 ms at k = 32 / 48 / 64 /
+  // 80 vs 1.372 ms sequential; this picks k = 48.
   const double R_P = 0.27, R_S = 1.0e5, BW = 7.0e6;
   const double kv_bytes = (double)t->B * h->num_kv_heads * S_cap * h->head_dim * 4.0;
   int best_k = 0;
   double best = 1e300;
   for (int k = 4; k <= sms - 8; ++k) {
-    const double tt = std::max(1.6 * 1.1 * units / (k * R_P), kv_bytes / std::min((sms - k) * R_S, BW));
+    const double tt = std::max(2.3 * 1.1 * units / (k * R_P), kv_bytes / std::min((sms - k) * R_S, BW));
     if (tt < best) {
       best = tt;
       best_k = k;
