@@ -12,11 +12,13 @@ Two ways the shared-prefix decode attention shards (SURVEY §8(e)
   prefix tokens [r*P/N, (r+1)*P/N) for all heads and the batch shard
   [r*B/N, (r+1)*B/N) of the suffixes.  Each rank
     1. attends all B*g stacked queries to its prefix shard (tcgen05 prefix kernel),
-    2. packs (O fp16, LSE fp32) into one contiguous block (the combine kernel doing a
-       1-part combine with an f16 output),
-    3. all-gathers the blocks over NCCL (NVLink / NVSwitch),
+    2. packs (O fp16, LSE fp32) of all rows (the combine kernel doing a 1-part combine with
+       an f16 output); the rows of each destination rank's batch shard are contiguous,
+    3. exchanges them all-to-all over NCCL (NVLink / NVSwitch): every rank receives only the
+       N pieces of its own batch shard's rows -- 1/N of what an all-gather moves
+       (`exchange="allgather"` keeps the all-gather of whole blocks for comparison),
     4. runs suffix attention for its batch shard,
-    5. merges the N prefix pieces of its rows straight out of the gathered buffer
+    5. merges the N prefix pieces of its rows straight out of the received buffer
        (strided parts), then merges that with its suffix part -- both with the Eq. 5
        combine kernel, exactly as the single-GPU decomposition.
   fp16 (not bf16) is used for exchanged O: |O_r| <= max|V|, and fp16's 11-bit mantissa
@@ -88,7 +90,8 @@ def exchange_layout(B: int, Hq: int, d: int, exchange_dtype=torch.float16):
 def seqsplit_attention(q: torch.Tensor, pk_shard: torch.Tensor, pv_shard: torch.Tensor,
                        sk_local: torch.Tensor, sv_local: torch.Tensor, lens_local: torch.Tensor,
                        group: Optional[dist.ProcessGroup] = None, scale: Optional[float] = None,
-                       exchange_dtype=torch.float16, out_dtype=None, ops=None, return_lse: bool = False):
+                       exchange_dtype=torch.float16, out_dtype=None, ops=None, return_lse: bool = False,
+                       exchange: str = "alltoall"):
     """Prefix sequence split across the ranks of `group` (see module docstring).
 
     q: [B, Hq, d] replicated on every rank; pk/pv_shard: this rank's prefix tokens
@@ -107,6 +110,21 @@ def seqsplit_attention(q: torch.Tensor, pk_shard: torch.Tensor, pv_shard: torch.
 
     # 1-2. prefix pieces of all B*Hq rows over the local prefix shard, packed for the exchange
     o_p, l_p = ops.prefix(q, pk_shard, pv_shard, scale=scale)
+    if exchange == "alltoall":
+        # rows of rank c's batch shard are contiguous in [B, Hq, d]: split sizes by shard
+        o_send = torch.empty(B * Hq, d, dtype=exchange_dtype, device=dev)
+        l_send = torch.empty(B * Hq, dtype=torch.float32, device=dev)
+        ops.combine(o_p.view(1, B * Hq, d), l_p.view(1, B * Hq), out=o_send, lse_out=l_send)
+        rows_by_rank = [(lambda r: (r[1] - r[0]) * Hq)(shard_range(B, world, c)) for c in range(world)]
+        # split sizes count dim-0 entries: rows of [rows, d] / [rows]
+        o_all = torch.empty(world * nb * Hq, d, dtype=exchange_dtype, device=dev)
+        l_all = torch.empty(world * nb * Hq, dtype=torch.float32, device=dev)
+        dist.all_to_all_single(o_all, o_send, output_split_sizes=[nb * Hq] * world,
+                               input_split_sizes=rows_by_rank, group=group)
+        dist.all_to_all_single(l_all, l_send, output_split_sizes=[nb * Hq] * world,
+                               input_split_sizes=rows_by_rank, group=group)
+        return _finish(q, sk_local, sv_local, lens_local, o_all.view(world, nb * Hq, d),
+                       l_all.view(world, nb * Hq), b0, b1, scale, out_dtype, ops, return_lse)
     o_bytes, l_bytes = exchange_layout(B, Hq, d, exchange_dtype)
     block = o_bytes + l_bytes
     send = torch.empty(block, dtype=torch.uint8, device=dev)
@@ -121,16 +139,24 @@ def seqsplit_attention(q: torch.Tensor, pk_shard: torch.Tensor, pv_shard: torch.
     esz = torch.empty((), dtype=exchange_dtype).element_size()
     o_all = blocks[:, : B * Hq * d * esz].view(exchange_dtype).view(world, B, Hq, d)
     l_all = blocks[:, o_bytes:].view(torch.float32).view(world, B, Hq)
+    return _finish(q, sk_local, sv_local, lens_local, o_all[:, b0:b1].reshape(world, nb * Hq, d),
+                   l_all[:, b0:b1].reshape(world, nb * Hq), b0, b1, scale, out_dtype, ops, return_lse)
 
+
+def _finish(q, sk_local, sv_local, lens_local, o_parts, l_parts, b0, b1, scale, out_dtype, ops, return_lse):
+    """Steps 4-5: suffix of the batch shard, merge of the N exchanged prefix pieces of its
+    rows (o_parts [N, rows, d], l_parts [N, rows], strided parts allowed), final merge."""
+    B, Hq, d = q.shape
+    nb = b1 - b0
+    dev = q.device
     # 4. suffix of the local batch shard, written straight into part 1
     parts = torch.empty(2, nb * Hq, d, dtype=torch.float32, device=dev)
     lparts = torch.empty(2, nb * Hq, dtype=torch.float32, device=dev)
     if nb > 0:
         ops.suffix(q[b0:b1], sk_local, sv_local, lens_local, scale=scale, out=parts[1].view(nb, Hq, d),
                    lse_out=lparts[1].view(nb, Hq))
-        # 5a. merge the world prefix pieces of these rows (strided parts of the gathered buffer)
-        ops.combine(o_all[:, b0:b1].reshape(world, nb * Hq, d), l_all[:, b0:b1].reshape(world, nb * Hq),
-                    out=parts[0], lse_out=lparts[0])
+        # 5a. merge the world prefix pieces of these rows (strided parts of the exchanged buffer)
+        ops.combine(o_parts, l_parts, out=parts[0], lse_out=lparts[0])
         # 5b. prefix (+) suffix
         out, lse = ops.combine(parts, lparts, out_dtype=out_dtype)
     else:

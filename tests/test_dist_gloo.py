@@ -76,19 +76,22 @@ def _worker(rank, world, port, mode, exchange, outdir):
     from paper_2402_05099_b200 import dist as hdist
 
     try:
-        B, Hq, Hkv, d, P, S = 6, 8, 2, 32, 90, 12
-        pb = synth.make_problem(B, Hq, Hkv, d, P, S, lens=[12, 0, 5, 12, 1, 7], dtype="bf16", dist="mixed", seed=21)
+        lens_all = [12, 0, 5, 12, 1, 7, 3]
+        B = 6 if world == 2 else 7  # world 3: unequal batch shards (3, 2, 2 rows) for the all-to-all splits
+        Hq, Hkv, d, P, S = 8, 2, 32, 90, 12
+        pb = synth.make_problem(B, Hq, Hkv, d, P, S, lens=lens_all[:B], dtype="bf16", dist="mixed", seed=21)
         tt = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16)
         q, pk, pv, sk, sv = tt(pb.q), tt(pb.pk), tt(pb.pv), tt(pb.sk), tt(pb.sv)
         lens = torch.from_numpy(pb.lens.astype(np.int32))
         ref, lref = oracle.flat_attention(pb)
         ops = OracleOps()
-        if mode == "seqsplit":
+        if mode.startswith("seqsplit"):
             p0, p1 = hdist.shard_range(P, world, rank)
             b0, b1 = hdist.shard_range(B, world, rank)
             out, lse = hdist.seqsplit_attention(q, pk[p0:p1], pv[p0:p1], sk[b0:b1], sv[b0:b1], lens[b0:b1],
                                                 exchange_dtype=exchange, out_dtype=torch.float32, ops=ops,
-                                                return_lse=True)
+                                                return_lse=True,
+                                                exchange="allgather" if mode.endswith("ag") else "alltoall")
             err = float(np.abs(out.double().numpy() - ref[b0:b1]).max())
             lerr = float(np.abs(lse.double().numpy() - lref[b0:b1]).max())
             tol = 1e-6 if exchange == torch.float32 else 4e-3
@@ -111,10 +114,10 @@ def _worker(rank, world, port, mode, exchange, outdir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode,exchange", [("seqsplit", torch.float32), ("seqsplit", torch.float16),
-                                           ("heads", torch.float16)])
-def test_world2_gloo(mode, exchange):
-    world = 2
+@pytest.mark.parametrize("mode,exchange,world", [("seqsplit-a2a", torch.float32, 2), ("seqsplit-a2a", torch.float16, 2),
+                                                 ("seqsplit-a2a", torch.float16, 3), ("seqsplit-ag", torch.float16, 2),
+                                                 ("heads", torch.float16, 2)])
+def test_world_gloo(mode, exchange, world):
     with tempfile.TemporaryDirectory() as td:
         mp.spawn(_worker, args=(world, _free_port(), mode, exchange, td), nprocs=world, join=True)
         for r in range(world):
