@@ -111,20 +111,28 @@ def seqsplit_attention(q: torch.Tensor, pk_shard: torch.Tensor, pv_shard: torch.
     # 1-2. prefix pieces of all B*Hq rows over the local prefix shard, packed for the exchange
     o_p, l_p = ops.prefix(q, pk_shard, pv_shard, scale=scale)
     if exchange == "alltoall":
-        # rows of rank c's batch shard are contiguous in [B, Hq, d]: split sizes by shard
-        o_send = torch.empty(B * Hq, d, dtype=exchange_dtype, device=dev)
-        l_send = torch.empty(B * Hq, dtype=torch.float32, device=dev)
-        ops.combine(o_p.view(1, B * Hq, d), l_p.view(1, B * Hq), out=o_send, lse_out=l_send)
-        rows_by_rank = [(lambda r: (r[1] - r[0]) * Hq)(shard_range(B, world, c)) for c in range(world)]
-        # split sizes count dim-0 entries: rows of [rows, d] / [rows]
-        o_all = torch.empty(world * nb * Hq, d, dtype=exchange_dtype, device=dev)
-        l_all = torch.empty(world * nb * Hq, dtype=torch.float32, device=dev)
-        dist.all_to_all_single(o_all, o_send, output_split_sizes=[nb * Hq] * world,
-                               input_split_sizes=rows_by_rank, group=group)
-        dist.all_to_all_single(l_all, l_send, output_split_sizes=[nb * Hq] * world,
-                               input_split_sizes=rows_by_rank, group=group)
-        return _finish(q, sk_local, sv_local, lens_local, o_all.view(world, nb * Hq, d),
-                       l_all.view(world, nb * Hq), b0, b1, scale, out_dtype, ops, return_lse)
+        # One slot of ceil(B/N) rows per destination rank; rank c's batch-shard rows are
+        # packed at the start of slot c (pad rows are sent but never read).  Equal slots:
+        # all_to_all_single without split sizes (the split-size form hangs process-group
+        # teardown after CUDA-graph capture with this NCCL build).
+        mb = -(-B // world)
+        o_send = torch.empty(world * mb * Hq, d, dtype=exchange_dtype, device=dev)
+        l_send = torch.empty(world * mb * Hq, dtype=torch.float32, device=dev)
+        if B % world == 0:  # slots are exactly the shards: one pack for all rows
+            ops.combine(o_p.view(1, B * Hq, d), l_p.view(1, B * Hq), out=o_send, lse_out=l_send)
+        else:
+            for c in range(world):
+                c0, c1 = shard_range(B, world, c)
+                if c1 > c0:
+                    ops.combine(o_p[c0:c1].reshape(1, (c1 - c0) * Hq, d), l_p[c0:c1].reshape(1, (c1 - c0) * Hq),
+                                out=o_send[c * mb * Hq:(c * mb + c1 - c0) * Hq],
+                                lse_out=l_send[c * mb * Hq:(c * mb + c1 - c0) * Hq])
+        o_all = torch.empty(world * mb * Hq, d, dtype=exchange_dtype, device=dev)
+        l_all = torch.empty(world * mb * Hq, dtype=torch.float32, device=dev)
+        dist.all_to_all_single(o_all, o_send, group=group)
+        dist.all_to_all_single(l_all, l_send, group=group)
+        return _finish(q, sk_local, sv_local, lens_local, o_all.view(world, mb * Hq, d)[:, : nb * Hq],
+                       l_all.view(world, mb * Hq)[:, : nb * Hq], b0, b1, scale, out_dtype, ops, return_lse)
     o_bytes, l_bytes = exchange_layout(B, Hq, d, exchange_dtype)
     block = o_bytes + l_bytes
     send = torch.empty(block, dtype=torch.uint8, device=dev)
