@@ -155,6 +155,21 @@ HYDRA_API hydra_status hydra_attn(const hydra_heads *h, int64_t B,
                         void *ws, size_t ws_bytes, void *stream, void *s_aux);
 
 /*
+ * hydra_append_kv -- decode-loop KV append: for every sequence b,
+ * write its new token's rows k_new[b, :, :] / v_new[b, :, :] ([B, Hkv, d], strides nb / nh
+ * in elements, d contiguous) into the suffix caches at position lens[b]
+ * (suffix_k/v[B, S_cap, Hkv, d], strides s_sb / s_st / s_sh), then increment lens[b] -- on
+ * the device, so "attend, then append" (the order of SPEC's toy model) replays
+ * from one CUDA graph step after step.  Precondition: lens[b] < S_cap; a sequence whose
+ * cache is full is left unchanged (no write, no increment).  Same dtype as h->dtype;
+ * every pointer and stride 16-byte aligned (EINVAL otherwise).  Asynchronous on `stream`.
+ */
+HYDRA_API hydra_status hydra_append_kv(const hydra_heads *h, int64_t B,
+                             const void *k_new, const void *v_new, int64_t nb, int64_t nh,
+                             void *sk, void *sv, int64_t s_sb, int64_t s_st, int64_t s_sh, int64_t S_cap,
+                             int32_t *lens, void *stream);
+
+/*
  * Sharing tree (§3.3, Fig. 2; SPEC SharingTree S:182-193).
  * Host arrays: parent[n_nodes] (root = -1, exactly one root), node_off/node_len
  * [n_nodes] (node n owns tokens node_off[n] .. node_off[n]+node_len[n]-1 of the

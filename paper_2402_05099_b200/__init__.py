@@ -7,6 +7,7 @@ torch tensors into the C ABI declared in include/hydra.h.
 from ._lib import HydraError, get_config, load, set_config, version  # noqa: F401
 from .attn import (  # noqa: F401
     Tree,
+    append_kv,
     attn_workspace_bytes,
     combine,
     hydragen_attention,

@@ -21,7 +21,7 @@ _STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ESHAPE", 3: "EUNSUPPORTED", 4: "ECUDA
 EXPORTED = ["hydra_prefix_attn", "hydra_suffix_attn", "hydra_combine", "hydra_attn", "hydra_tree_create",
             "hydra_tree_destroy", "hydra_tree_depth", "hydra_tree_group_size", "hydra_tree_workspace_size",
             "hydra_tree_attn", "hydra_workspace_size", "hydra_set_config", "hydra_get_config",
-            "hydra_last_error", "hydra_version"]
+            "hydra_last_error", "hydra_version", "hydra_append_kv"]
 
 
 class HydraError(RuntimeError):
@@ -65,6 +65,7 @@ def load():
         "hydra_tree_attn": (st, [_HP, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _i64,
                                  _i64, _vp, _vp, _i32, _vp, _vp, _sz, _vp, _vp]),
         "hydra_workspace_size": (_sz, [ctypes.c_int, _HP, _i64, _i64, _i64, _i32]),
+        "hydra_append_kv": (st, [_HP, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp]),
         "hydra_set_config": (st, [ctypes.c_char_p, _i64]),
         "hydra_get_config": (_i64, [ctypes.c_char_p]),
         "hydra_last_error": (ctypes.c_char_p, []),

@@ -125,6 +125,31 @@ def suffix_attn(q: torch.Tensor, suffix_k: torch.Tensor, suffix_v: torch.Tensor,
     return o, lse
 
 
+def append_kv(k_new: torch.Tensor, v_new: torch.Tensor, suffix_k: torch.Tensor, suffix_v: torch.Tensor,
+              suffix_lens: torch.Tensor, stream=None):
+    """Decode-loop KV append: suffix_k/v[b, lens[b]] = k/v_new[b]; lens[b] += 1,
+    on the device (graph-capturable).  k_new/v_new: [B, Hkv, d] (or [B, 1, Hkv, d])."""
+    if k_new.dim() == 4:
+        k_new, v_new = k_new[:, 0], v_new[:, 0]
+    suffix_k, suffix_v = _kv4(suffix_k, "suffix_k"), _kv4(suffix_v, "suffix_v")
+    _require_cuda(k_new, v_new, suffix_k, suffix_v, suffix_lens)
+    B, S_cap, Hkv, d = suffix_k.shape
+    if k_new.shape != (B, Hkv, d) or v_new.shape != k_new.shape or k_new.stride() != v_new.stride():
+        raise ValueError("k_new / v_new must be [B, Hkv, d] with equal strides")
+    if suffix_k.stride() != suffix_v.stride():
+        raise ValueError("suffix_k and suffix_v must have equal strides")
+    if suffix_lens.dtype != torch.int32 or suffix_lens.shape != (B,):
+        raise ValueError("suffix_lens must be int32 [B]")
+    if k_new.dtype != suffix_k.dtype or v_new.dtype != suffix_v.dtype:
+        raise TypeError("k_new / v_new must have the cache dtype")
+    h = Heads(Hkv, Hkv, d, 0.0, _DT[suffix_k.dtype])
+    st = suffix_k.stride()
+    check(_lib.load().hydra_append_kv(ctypes.byref(h), B, k_new.data_ptr(), v_new.data_ptr(), k_new.stride(0),
+                                      k_new.stride(1), suffix_k.data_ptr(), suffix_v.data_ptr(), st[0], st[1], st[2],
+                                      S_cap, suffix_lens.data_ptr(), _stream_ptr(stream, k_new.device)),
+          "hydra_append_kv")
+
+
 def combine(o_parts: torch.Tensor, lse_parts: torch.Tensor, out_dtype=torch.bfloat16, return_lse: bool = True,
             out: Optional[torch.Tensor] = None, lse_out: Optional[torch.Tensor] = None, stream=None):
     """n-ary LSE combine (Eq. 5 / App. B combine_lse).

@@ -619,6 +619,24 @@ extern "C" hydra_status hydra_attn(const hydra_heads *h, int64_t B, const void *
   return run_combine(rows, h->head_dim, np + ns, all, out, out_dtype, lse_out, s);
 }
 
+// ------------------------------------------------------------------ decode-loop KV append
+extern "C" hydra_status hydra_append_kv(const hydra_heads *h, int64_t B, const void *k_new, const void *v_new,
+                                        int64_t nb, int64_t nh, void *sk, void *sv, int64_t s_sb, int64_t s_st,
+                                        int64_t s_sh, int64_t S_cap, int32_t *lens, void *stream) {
+  hydra_status st = check_heads(h);
+  if (st) return st;
+  if (B <= 0) return fail(HYDRA_ESHAPE, "B must be > 0");
+  if (S_cap <= 0) return fail(HYDRA_ESHAPE, "S_cap must be > 0");
+  if (!k_new || !v_new || !sk || !sv || !lens) return fail(HYDRA_EINVAL, "null pointer argument");
+  const size_t es = elem_size(h->dtype);
+  if (!aligned16(k_new, es, {nb, nh}) || !aligned16(v_new, es, {}) || !aligned16(sk, es, {s_sb, s_st, s_sh}) ||
+      !aligned16(sv, es, {}))
+    return fail(HYDRA_EINVAL, "k/v pointers and strides must be 16-byte aligned");
+  st = launch_append_kv(k_new, v_new, nb, nh, sk, sv, s_sb, s_st, s_sh, S_cap, h->num_kv_heads, h->head_dim, es, B,
+                        lens, reinterpret_cast<cudaStream_t>(stream));
+  return st == HYDRA_OK ? st : cuda_fail("append_kv launch");
+}
+
 // ------------------------------------------------------------------ sharing tree
 struct hydra_tree {
   int32_t n_nodes = 0;
