@@ -170,6 +170,57 @@ HYDRA_API hydra_status hydra_append_kv(const hydra_heads *h, int64_t B,
                              int32_t *lens, void *stream);
 
 /*
+ * Paged suffix cache ("per-step suffix KV append into a growable or
+ * paged cache").  The paper keeps each sequence's suffix K/V in its own contiguous tensor
+ * (App. B, suffix_k/v [B, Nq+S, Hkv, d]); a serving engine instead allocates
+ * the suffixes from a pool of fixed-size pages so sequences can grow without a
+ * worst-case reservation.  The attention is unchanged -- only where token t of sequence
+ * b is read from (reading R14):
+ *     suffix row (b, t)  ==  pool row (block_table[b * bt_stride + t / page_size], t % page_size)
+ * Pools: k_pool / v_pool [n_pages, page_size, Hkv, d], element (p, r, j, i) at
+ * pool[p*p_sp + r*p_st + j*p_sh + i] (same dtype as h->dtype, 16-byte aligned strides).
+ * block_table: DEVICE int32 [B, bt_stride], owned by the caller; entries for the pages
+ * that cover tokens 0 .. lens[b]-1 must be in [0, n_pages) (a documented precondition
+ * like lens, not checked); entries past them are never read.  Pages may be shared or
+ * listed in any order.  S_cap (capacity, tokens per sequence) must be
+ * <= bt_stride * page_size and bounds lens[b] as in the contiguous calls.
+ */
+typedef struct {
+  const int32_t *block_table; /* device [B, bt_stride]                             */
+  int64_t bt_stride;          /* row stride of block_table (pages per sequence)    */
+  int32_t page_size;          /* tokens per page: a power of two >= 8 (ESHAPE)     */
+  int64_t n_pages;            /* pages in each pool, in [1, 2^31)                  */
+} hydra_paging;
+
+/* hydra_suffix_attn over a paged cache; otherwise identical (same kernels, same
+ * workspace size as hydra_workspace_size(HYDRA_OP_SUFFIX, h, B, 0, S_cap, 0)). */
+HYDRA_API hydra_status hydra_suffix_attn_paged(const hydra_heads *h, int64_t B,
+                                     const void *q, int64_t q_sb, int64_t q_sh,
+                                     const void *k_pool, const void *v_pool, int64_t p_sp, int64_t p_st, int64_t p_sh,
+                                     const hydra_paging *pg, int64_t S_cap, const int32_t *lens,
+                                     float *o_part, float *lse_part,
+                                     void *ws, size_t ws_bytes, void *stream);
+
+/* hydra_attn with the suffix in a paged cache (prefix stays a dense [P, Hkv, d] tensor:
+ * it is read once per step by the stacked-query GEMM, §3.2).  Workspace as hydra_attn. */
+HYDRA_API hydra_status hydra_attn_paged(const hydra_heads *h, int64_t B,
+                              const void *q, int64_t q_sb, int64_t q_sh,
+                              int64_t P, const void *pk, const void *pv, int64_t kv_st, int64_t kv_sh,
+                              const void *k_pool, const void *v_pool, int64_t p_sp, int64_t p_st, int64_t p_sh,
+                              const hydra_paging *pg, int64_t S_cap, const int32_t *lens,
+                              void *out, hydra_dtype out_dtype, float *lse_out,
+                              void *ws, size_t ws_bytes, void *stream, void *s_aux);
+
+/* hydra_append_kv into a paged cache: sequence b's new row goes to row lens[b] % page_size
+ * of page block_table[b][lens[b] / page_size] (the caller has mapped that page before the
+ * call, e.g. when lens[b] % page_size == 0), then lens[b] += 1 on the device.  A sequence
+ * with lens[b] >= S_cap is left unchanged. */
+HYDRA_API hydra_status hydra_append_kv_paged(const hydra_heads *h, int64_t B,
+                                   const void *k_new, const void *v_new, int64_t nb, int64_t nh,
+                                   void *k_pool, void *v_pool, int64_t p_sp, int64_t p_st, int64_t p_sh,
+                                   const hydra_paging *pg, int64_t S_cap, int32_t *lens, void *stream);
+
+/*
  * Sharing tree (§3.3, Fig. 2; SPEC SharingTree S:182-193).
  * Host arrays: parent[n_nodes] (root = -1, exactly one root), node_off/node_len
  * [n_nodes] (node n owns tokens node_off[n] .. node_off[n]+node_len[n]-1 of the

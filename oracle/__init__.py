@@ -155,6 +155,34 @@ def suffix_only(pb, rows=None, threads: int = 0):
     return attention_segments(pb.q, segs, pb.Hkv, pb.scale, rows, threads)
 
 
+def paged_rows(pool: np.ndarray, table_row: np.ndarray, page_size: int, n: int) -> np.ndarray:
+    """Tokens 0..n-1 of one sequence of a paged cache, in order (reading R14):
+    token t is row t % page_size of page table_row[t // page_size].  Pure indexing."""
+    out = [pool[int(table_row[t // page_size]), t % page_size] for t in range(n)]
+    return np.stack(out) if out else pool[:0, 0]
+
+
+def suffix_only_paged(q, k_pool, v_pool, block_table, page_size, lens, Hkv, scale=None, rows=None,
+                      threads: int = 0):
+    """suffix_only over a paged cache: gather each suffix (paged_rows), then the definition."""
+    segs = []
+    for b in range(q.shape[0]):
+        n = int(lens[b])
+        segs.append([(paged_rows(k_pool, block_table[b], page_size, n),
+                      paged_rows(v_pool, block_table[b], page_size, n))])
+    return attention_segments(q, segs, Hkv, scale, rows, threads)
+
+
+def flat_attention_paged(pb, pc, rows=None, threads: int = 0):
+    """flat_attention with the suffixes read from a paged cache pc (synth.PagedCache)."""
+    segs = []
+    for b in range(pb.B):
+        n = int(pb.lens[b])
+        segs.append([(pb.pk, pb.pv), (paged_rows(pc.k_pool, pc.block_table[b], pc.page_size, n),
+                                      paged_rows(pc.v_pool, pc.block_table[b], pc.page_size, n))])
+    return attention_segments(pb.q, segs, pb.Hkv, pb.scale, rows, threads)
+
+
 def tree_path(parent: np.ndarray, leaf: int) -> list:
     """Root->leaf node list by walking parent pointers (S:242-250 flatten order)."""
     out, n = [], int(leaf)

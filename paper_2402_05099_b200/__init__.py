@@ -8,10 +8,13 @@ from ._lib import HydraError, get_config, load, set_config, version  # noqa: F40
 from .attn import (  # noqa: F401
     Tree,
     append_kv,
+    append_kv_paged,
     attn_workspace_bytes,
     combine,
     hydragen_attention,
+    hydragen_attention_paged,
     prefix_attn,
     suffix_attn,
+    suffix_attn_paged,
     tree_attention,
 )

@@ -21,7 +21,8 @@ _STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ESHAPE", 3: "EUNSUPPORTED", 4: "ECUDA
 EXPORTED = ["hydra_prefix_attn", "hydra_suffix_attn", "hydra_combine", "hydra_attn", "hydra_tree_create",
             "hydra_tree_destroy", "hydra_tree_depth", "hydra_tree_group_size", "hydra_tree_workspace_size",
             "hydra_tree_attn", "hydra_workspace_size", "hydra_set_config", "hydra_get_config",
-            "hydra_last_error", "hydra_version", "hydra_append_kv"]
+            "hydra_last_error", "hydra_version", "hydra_append_kv", "hydra_suffix_attn_paged", "hydra_attn_paged",
+            "hydra_append_kv_paged"]
 
 
 class HydraError(RuntimeError):
@@ -35,9 +36,16 @@ class Heads(ctypes.Structure):
                 ("scale", ctypes.c_float), ("dtype", ctypes.c_int32)]
 
 
+class Paging(ctypes.Structure):
+    """hydra_paging (include/hydra.h): block table [B, bt_stride] of a paged suffix cache."""
+    _fields_ = [("block_table", ctypes.c_void_p), ("bt_stride", ctypes.c_int64), ("page_size", ctypes.c_int32),
+                ("n_pages", ctypes.c_int64)]
+
+
 _lib = None
 _i64, _i32, _vp, _sz = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_size_t
 _HP = ctypes.POINTER(Heads)
+_PP = ctypes.POINTER(Paging)
 
 
 def load():
@@ -66,6 +74,12 @@ def load():
                                  _i64, _vp, _vp, _i32, _vp, _vp, _sz, _vp, _vp]),
         "hydra_workspace_size": (_sz, [ctypes.c_int, _HP, _i64, _i64, _i64, _i32]),
         "hydra_append_kv": (st, [_HP, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp]),
+        "hydra_suffix_attn_paged": (st, [_HP, _i64, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _PP, _i64, _vp,
+                                         _vp, _vp, _vp, _sz, _vp]),
+        "hydra_attn_paged": (st, [_HP, _i64, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64,
+                                  _i64, _PP, _i64, _vp, _vp, _i32, _vp, _vp, _sz, _vp, _vp]),
+        "hydra_append_kv_paged": (st, [_HP, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _PP, _i64, _vp,
+                                       _vp]),
         "hydra_set_config": (st, [ctypes.c_char_p, _i64]),
         "hydra_get_config": (_i64, [ctypes.c_char_p]),
         "hydra_last_error": (ctypes.c_char_p, []),

@@ -150,6 +150,117 @@ def append_kv(k_new: torch.Tensor, v_new: torch.Tensor, suffix_k: torch.Tensor, 
           "hydra_append_kv")
 
 
+# ------------------------------------------------------------------ paged suffix cache (hydra.h hydra_paging)
+def _paging(k_pool: torch.Tensor, v_pool: torch.Tensor, block_table: torch.Tensor, B: int,
+            S_cap: Optional[int]):
+    """Validates pools [n_pages, page_size, Hkv, d] and block_table int32 [B, max_pages];
+    returns (Paging, S_cap).  S_cap defaults to max_pages * page_size."""
+    if k_pool.dim() != 4 or k_pool.stride(-1) != 1:
+        raise ValueError("k_pool must be [n_pages, page_size, Hkv, d] with a contiguous last dim")
+    if k_pool.shape != v_pool.shape or k_pool.stride() != v_pool.stride():
+        raise ValueError("k_pool and v_pool must have equal shapes and strides")
+    if block_table.dtype != torch.int32 or block_table.dim() != 2 or block_table.shape[0] != B \
+            or block_table.stride(1) != 1:
+        raise ValueError("block_table must be int32 [B, max_pages] with contiguous rows")
+    _require_cuda(k_pool, v_pool, block_table)
+    n_pages, page_size = k_pool.shape[0], k_pool.shape[1]
+    cap = block_table.shape[1] * page_size
+    S_cap = cap if S_cap is None else int(S_cap)
+    pg = _lib.Paging(block_table.data_ptr(), block_table.stride(0), page_size, n_pages)
+    return pg, S_cap
+
+
+def suffix_attn_paged(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor, block_table: torch.Tensor,
+                      suffix_lens: torch.Tensor, S_cap: Optional[int] = None, scale: Optional[float] = None,
+                      workspace: Optional[torch.Tensor] = None, stream=None):
+    """suffix_attn over a paged cache: token t of sequence b is k_pool[block_table[b, t // page_size],
+    t % page_size] (reading R14).  -> (O_s [B,Hq,d] f32, LSE_s [B,Hq] f32)."""
+    q = _squeeze_q(q)
+    _require_cuda(q, suffix_lens)
+    B, Hq, d = q.shape
+    if suffix_lens.dtype != torch.int32 or suffix_lens.shape != (B,):
+        raise ValueError("suffix_lens must be int32 [B]")
+    pg, S_cap = _paging(k_pool, v_pool, block_table, B, S_cap)
+    h = _heads(q, k_pool.shape[2], scale)
+    lib = _lib.load()
+    o = torch.empty(B, Hq, d, dtype=torch.float32, device=q.device)
+    lse = torch.empty(B, Hq, dtype=torch.float32, device=q.device)
+    ws = _workspace(lib.hydra_workspace_size(_lib.HYDRA_OP_SUFFIX, ctypes.byref(h), B, 0, S_cap, 0), q.device,
+                    workspace)
+    st = k_pool.stride()
+    check(lib.hydra_suffix_attn_paged(ctypes.byref(h), B, q.data_ptr(), q.stride(0), q.stride(1),
+                                      k_pool.data_ptr(), v_pool.data_ptr(), st[0], st[1], st[2], ctypes.byref(pg),
+                                      S_cap, suffix_lens.data_ptr(), o.data_ptr(), lse.data_ptr(), _ptr(ws),
+                                      ws.numel(), _stream_ptr(stream, q.device)),
+          "hydra_suffix_attn_paged")
+    return o, lse
+
+
+def append_kv_paged(k_new: torch.Tensor, v_new: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
+                    block_table: torch.Tensor, suffix_lens: torch.Tensor, S_cap: Optional[int] = None, stream=None):
+    """append_kv into a paged cache: row lens[b] % page_size of page block_table[b, lens[b] // page_size]
+    receives k/v_new[b]; lens[b] += 1 on the device (graph-capturable)."""
+    if k_new.dim() == 4:
+        k_new, v_new = k_new[:, 0], v_new[:, 0]
+    B = k_new.shape[0]
+    pg, S_cap = _paging(k_pool, v_pool, block_table, B, S_cap)
+    _require_cuda(k_new, v_new, suffix_lens)
+    Hkv, d = k_pool.shape[2], k_pool.shape[3]
+    if k_new.shape != (B, Hkv, d) or v_new.shape != k_new.shape or k_new.stride() != v_new.stride():
+        raise ValueError("k_new / v_new must be [B, Hkv, d] with equal strides")
+    if suffix_lens.dtype != torch.int32 or suffix_lens.shape != (B,):
+        raise ValueError("suffix_lens must be int32 [B]")
+    if k_new.dtype != k_pool.dtype or v_new.dtype != v_pool.dtype:
+        raise TypeError("k_new / v_new must have the cache dtype")
+    h = Heads(Hkv, Hkv, d, 0.0, _DT[k_pool.dtype])
+    st = k_pool.stride()
+    check(_lib.load().hydra_append_kv_paged(ctypes.byref(h), B, k_new.data_ptr(), v_new.data_ptr(),
+                                            k_new.stride(0), k_new.stride(1), k_pool.data_ptr(), v_pool.data_ptr(),
+                                            st[0], st[1], st[2], ctypes.byref(pg), S_cap, suffix_lens.data_ptr(),
+                                            _stream_ptr(stream, k_new.device)),
+          "hydra_append_kv_paged")
+
+
+def hydragen_attention_paged(q: torch.Tensor, prefix_k: torch.Tensor, prefix_v: torch.Tensor,
+                             k_pool: torch.Tensor, v_pool: torch.Tensor, block_table: torch.Tensor,
+                             suffix_lens: torch.Tensor, S_cap: Optional[int] = None, scale: Optional[float] = None,
+                             out_dtype=None, return_lse: bool = False, workspace: Optional[torch.Tensor] = None,
+                             out: Optional[torch.Tensor] = None, lse_out: Optional[torch.Tensor] = None,
+                             stream=None, aux_stream=None):
+    """hydragen_attention with the suffixes in a paged cache (pools [n_pages, page_size, Hkv, d],
+    block_table int32 [B, max_pages]); the prefix stays a dense [P, Hkv, d] tensor."""
+    q = _squeeze_q(q)
+    prefix_k, prefix_v = _kv3(prefix_k, "prefix_k"), _kv3(prefix_v, "prefix_v")
+    _require_cuda(q, prefix_k, prefix_v, suffix_lens)
+    if prefix_k.stride() != prefix_v.stride():
+        raise ValueError("K and V must share strides")
+    B, Hq, d = q.shape
+    P, Hkv = prefix_k.shape[0], prefix_k.shape[1]
+    if k_pool.dim() != 4 or k_pool.shape[2] != Hkv:
+        raise ValueError("k_pool must be [n_pages, page_size, Hkv, d]")
+    if suffix_lens.dtype != torch.int32 or suffix_lens.shape != (B,):
+        raise ValueError("suffix_lens must be int32 [B]")
+    pg, S_cap = _paging(k_pool, v_pool, block_table, B, S_cap)
+    h = _heads(q, Hkv, scale)
+    lib = _lib.load()
+    out_dtype = out_dtype or (torch.bfloat16 if q.dtype == torch.bfloat16 else torch.float32)
+    if out is None:
+        out = torch.empty(B, Hq, d, dtype=out_dtype, device=q.device)
+    if return_lse and lse_out is None:
+        lse_out = torch.empty(B, Hq, dtype=torch.float32, device=q.device)
+    ws = _workspace(lib.hydra_workspace_size(_lib.HYDRA_OP_ATTN, ctypes.byref(h), B, P, S_cap, 0), q.device,
+                    workspace)
+    ss = k_pool.stride()
+    aux = None if aux_stream is None else aux_stream.cuda_stream
+    check(lib.hydra_attn_paged(ctypes.byref(h), B, q.data_ptr(), q.stride(0), q.stride(1), P, prefix_k.data_ptr(),
+                               prefix_v.data_ptr(), prefix_k.stride(0), prefix_k.stride(1), k_pool.data_ptr(),
+                               v_pool.data_ptr(), ss[0], ss[1], ss[2], ctypes.byref(pg), S_cap,
+                               suffix_lens.data_ptr(), out.data_ptr(), _DT[out.dtype], _ptr(lse_out), _ptr(ws),
+                               ws.numel(), _stream_ptr(stream, q.device), aux),
+          "hydra_attn_paged")
+    return (out, lse_out) if return_lse else out
+
+
 def combine(o_parts: torch.Tensor, lse_parts: torch.Tensor, out_dtype=torch.bfloat16, return_lse: bool = True,
             out: Optional[torch.Tensor] = None, lse_out: Optional[torch.Tensor] = None, stream=None):
     """n-ary LSE combine (Eq. 5 / App. B combine_lse).

@@ -349,7 +349,7 @@ static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, i
 static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, int64_t q_sb, int64_t q_sh,
                                const void *k, const void *v, int64_t s_sb, int64_t s_st, int64_t s_sh,
                                int64_t S_cap, const int32_t *lens, int splits, const PartsView &dst,
-                               cudaStream_t s, int tc_ctas = 0) {
+                               cudaStream_t s, int tc_ctas = 0, const hydra_paging *pg = nullptr) {
   const int g = h->num_q_heads / h->num_kv_heads;
   if (use_suffix_tc(h, B, S_cap, tc_ctas > 0)) {
     SuffixTcArgs a{};
@@ -372,6 +372,12 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
     a.cb = (int32_t)g_suffix_cb;
     a.trace = reinterpret_cast<void *>((intptr_t)g_suffix_trace.load());
     a.debug = (int32_t)g_tc_debug;
+    if (pg) {
+      a.block_table = pg->block_table;
+      a.bt_stride = pg->bt_stride;
+      a.n_pages = pg->n_pages;
+      a.page_size = pg->page_size;
+    }
     const int ctas = tc_ctas > 0 ? tc_ctas : (g_suffix_ctas > 0 ? (int)g_suffix_ctas : device_sm_count());
     hydra_status st = launch_suffix_tc(a, ctas, s);
     return st == HYDRA_OK ? st : cuda_fail("suffix tcgen05 launch");
@@ -400,6 +406,11 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
   p.lse = dst.lse;
   p.o_split_stride = dst.o_stride;
   p.lse_split_stride = dst.lse_stride;
+  if (pg) {
+    p.block_table = pg->block_table;
+    p.bt_stride = pg->bt_stride;
+    p.page_shift = __builtin_ctz((unsigned)pg->page_size);
+  }
   hydra_status st = launch_decode(p, h->dtype, h->head_dim, s);
   return st == HYDRA_OK ? st : (st == HYDRA_ECUDA ? cuda_fail("suffix launch") : fail(st, "suffix"));
 }
@@ -477,10 +488,21 @@ extern "C" hydra_status hydra_prefix_attn(const hydra_heads *h, int64_t B, const
   return run_combine(B * h->num_q_heads, d, splits, parts, o_part, HYDRA_F32, lse_part, s);
 }
 
-extern "C" hydra_status hydra_suffix_attn(const hydra_heads *h, int64_t B, const void *q, int64_t q_sb,
-                                          int64_t q_sh, const void *k, const void *v, int64_t s_sb, int64_t s_st,
-                                          int64_t s_sh, int64_t S_cap, const int32_t *lens, float *o_part,
-                                          float *lse_part, void *ws, size_t ws_bytes, void *stream) {
+// Paging descriptor checks shared by the *_paged entry points (hydra.h, hydra_paging).
+static hydra_status check_paging(const hydra_paging *pg, int64_t S_cap) {
+  if (!pg || !pg->block_table) return fail(HYDRA_EINVAL, "null paging descriptor / block table");
+  if (pg->page_size < 8 || (pg->page_size & (pg->page_size - 1)))
+    return fail(HYDRA_ESHAPE, "page_size must be a power of two >= 8 (got %d)", pg->page_size);
+  if (pg->n_pages <= 0 || pg->n_pages > INT32_MAX) return fail(HYDRA_ESHAPE, "n_pages must be in [1, 2^31)");
+  if (pg->bt_stride <= 0 || S_cap > pg->bt_stride * (int64_t)pg->page_size)
+    return fail(HYDRA_ESHAPE, "S_cap (%lld) exceeds bt_stride * page_size", (long long)S_cap);
+  return HYDRA_OK;
+}
+
+static hydra_status suffix_impl(const hydra_heads *h, int64_t B, const void *q, int64_t q_sb, int64_t q_sh,
+                                const void *k, const void *v, int64_t s_sb, int64_t s_st, int64_t s_sh,
+                                int64_t S_cap, const int32_t *lens, float *o_part, float *lse_part, void *ws,
+                                size_t ws_bytes, void *stream, const hydra_paging *pg) {
   hydra_status st = check_heads(h);
   if (st) return st;
   if (B <= 0) return fail(HYDRA_ESHAPE, "B must be > 0 (S:291)");
@@ -500,13 +522,34 @@ extern "C" hydra_status hydra_suffix_attn(const hydra_heads *h, int64_t B, const
     return st ? cuda_fail("fill") : HYDRA_OK;
   }
   const int splits = suffix_splits(h, B, S_cap);
-  if (splits == 1) return run_suffix(h, B, q, q_sb, q_sh, k, v, s_sb, s_st, s_sh, S_cap, lens, 1, out, s);
+  if (splits == 1) return run_suffix(h, B, q, q_sb, q_sh, k, v, s_sb, s_st, s_sh, S_cap, lens, 1, out, s, 0, pg);
   const size_t need = part_bytes(h, B) * splits;
   if (!ws || ws_bytes < need) return fail(HYDRA_ENOMEM, "workspace too small: need %zu bytes", need);
   PartsView parts = parts_in_ws(ws, h, B, splits);
-  st = run_suffix(h, B, q, q_sb, q_sh, k, v, s_sb, s_st, s_sh, S_cap, lens, splits, parts, s);
+  st = run_suffix(h, B, q, q_sb, q_sh, k, v, s_sb, s_st, s_sh, S_cap, lens, splits, parts, s, 0, pg);
   if (st) return st;
   return run_combine(B * h->num_q_heads, d, splits, parts, o_part, HYDRA_F32, lse_part, s);
+}
+
+extern "C" hydra_status hydra_suffix_attn(const hydra_heads *h, int64_t B, const void *q, int64_t q_sb,
+                                          int64_t q_sh, const void *k, const void *v, int64_t s_sb, int64_t s_st,
+                                          int64_t s_sh, int64_t S_cap, const int32_t *lens, float *o_part,
+                                          float *lse_part, void *ws, size_t ws_bytes, void *stream) {
+  return suffix_impl(h, B, q, q_sb, q_sh, k, v, s_sb, s_st, s_sh, S_cap, lens, o_part, lse_part, ws, ws_bytes,
+                     stream, nullptr);
+}
+
+extern "C" hydra_status hydra_suffix_attn_paged(const hydra_heads *h, int64_t B, const void *q, int64_t q_sb,
+                                                int64_t q_sh, const void *k_pool, const void *v_pool, int64_t p_sp,
+                                                int64_t p_st, int64_t p_sh, const hydra_paging *pg, int64_t S_cap,
+                                                const int32_t *lens, float *o_part, float *lse_part, void *ws,
+                                                size_t ws_bytes, void *stream) {
+  if (S_cap > 0) {
+    hydra_status st = check_paging(pg, S_cap);
+    if (st) return st;
+  }
+  return suffix_impl(h, B, q, q_sb, q_sh, k_pool, v_pool, p_sp, p_st, p_sh, S_cap, lens, o_part, lse_part, ws,
+                     ws_bytes, stream, S_cap > 0 ? pg : nullptr);
 }
 
 extern "C" hydra_status hydra_combine(int64_t rows, int32_t d, int32_t n_parts, const void *o_parts,
@@ -554,11 +597,12 @@ StreamEvents &events() {
 }
 }  // namespace
 
-extern "C" hydra_status hydra_attn(const hydra_heads *h, int64_t B, const void *q, int64_t q_sb, int64_t q_sh,
-                                   int64_t P, const void *pk, const void *pv, int64_t kv_st, int64_t kv_sh,
-                                   const void *sk, const void *sv, int64_t s_sb, int64_t s_st, int64_t s_sh,
-                                   int64_t S_cap, const int32_t *lens, void *out, hydra_dtype out_dtype,
-                                   float *lse_out, void *ws, size_t ws_bytes, void *stream, void *s_aux) {
+static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, int64_t q_sb, int64_t q_sh,
+                              int64_t P, const void *pk, const void *pv, int64_t kv_st, int64_t kv_sh,
+                              const void *sk, const void *sv, int64_t s_sb, int64_t s_st, int64_t s_sh,
+                              int64_t S_cap, const int32_t *lens, void *out, hydra_dtype out_dtype,
+                              float *lse_out, void *ws, size_t ws_bytes, void *stream, void *s_aux,
+                              const hydra_paging *pg) {
   hydra_status st = check_heads(h);
   if (st) return st;
   if (B <= 0) return fail(HYDRA_ESHAPE, "B must be > 0 (S:291)");
@@ -606,7 +650,7 @@ extern "C" hydra_status hydra_attn(const hydra_heads *h, int64_t B, const void *
                                                    prefix_bn())
                                  : 0;
     st = run_suffix(h, B, q, q_sb, q_sh, sk, sv, s_sb, s_st, s_sh, S_cap, lens, ns, suf, s,
-                    k_over > 0 ? std::max(1, sms - k_eff) : 0);
+                    k_over > 0 ? std::max(1, sms - k_eff) : 0, pg);
   } else {
     st = launch_fill_neg_inf(suf.lse, rows, s);
     if (st) st = cuda_fail("fill");
@@ -619,10 +663,33 @@ extern "C" hydra_status hydra_attn(const hydra_heads *h, int64_t B, const void *
   return run_combine(rows, h->head_dim, np + ns, all, out, out_dtype, lse_out, s);
 }
 
+extern "C" hydra_status hydra_attn(const hydra_heads *h, int64_t B, const void *q, int64_t q_sb, int64_t q_sh,
+                                   int64_t P, const void *pk, const void *pv, int64_t kv_st, int64_t kv_sh,
+                                   const void *sk, const void *sv, int64_t s_sb, int64_t s_st, int64_t s_sh,
+                                   int64_t S_cap, const int32_t *lens, void *out, hydra_dtype out_dtype,
+                                   float *lse_out, void *ws, size_t ws_bytes, void *stream, void *s_aux) {
+  return attn_impl(h, B, q, q_sb, q_sh, P, pk, pv, kv_st, kv_sh, sk, sv, s_sb, s_st, s_sh, S_cap, lens, out,
+                   out_dtype, lse_out, ws, ws_bytes, stream, s_aux, nullptr);
+}
+
+extern "C" hydra_status hydra_attn_paged(const hydra_heads *h, int64_t B, const void *q, int64_t q_sb,
+                                         int64_t q_sh, int64_t P, const void *pk, const void *pv, int64_t kv_st,
+                                         int64_t kv_sh, const void *k_pool, const void *v_pool, int64_t p_sp,
+                                         int64_t p_st, int64_t p_sh, const hydra_paging *pg, int64_t S_cap,
+                                         const int32_t *lens, void *out, hydra_dtype out_dtype, float *lse_out,
+                                         void *ws, size_t ws_bytes, void *stream, void *s_aux) {
+  if (S_cap > 0) {
+    hydra_status st = check_paging(pg, S_cap);
+    if (st) return st;
+  }
+  return attn_impl(h, B, q, q_sb, q_sh, P, pk, pv, kv_st, kv_sh, k_pool, v_pool, p_sp, p_st, p_sh, S_cap, lens,
+                   out, out_dtype, lse_out, ws, ws_bytes, stream, s_aux, S_cap > 0 ? pg : nullptr);
+}
+
 // ------------------------------------------------------------------ decode-loop KV append
-extern "C" hydra_status hydra_append_kv(const hydra_heads *h, int64_t B, const void *k_new, const void *v_new,
-                                        int64_t nb, int64_t nh, void *sk, void *sv, int64_t s_sb, int64_t s_st,
-                                        int64_t s_sh, int64_t S_cap, int32_t *lens, void *stream) {
+static hydra_status append_impl(const hydra_heads *h, int64_t B, const void *k_new, const void *v_new, int64_t nb,
+                                int64_t nh, void *sk, void *sv, int64_t s_sb, int64_t s_st, int64_t s_sh,
+                                int64_t S_cap, int32_t *lens, void *stream, const hydra_paging *pg) {
   hydra_status st = check_heads(h);
   if (st) return st;
   if (B <= 0) return fail(HYDRA_ESHAPE, "B must be > 0");
@@ -632,9 +699,28 @@ extern "C" hydra_status hydra_append_kv(const hydra_heads *h, int64_t B, const v
   if (!aligned16(k_new, es, {nb, nh}) || !aligned16(v_new, es, {}) || !aligned16(sk, es, {s_sb, s_st, s_sh}) ||
       !aligned16(sv, es, {}))
     return fail(HYDRA_EINVAL, "k/v pointers and strides must be 16-byte aligned");
+  if (pg) {
+    st = check_paging(pg, S_cap);
+    if (st) return st;
+  }
   st = launch_append_kv(k_new, v_new, nb, nh, sk, sv, s_sb, s_st, s_sh, S_cap, h->num_kv_heads, h->head_dim, es, B,
-                        lens, reinterpret_cast<cudaStream_t>(stream));
+                        lens, reinterpret_cast<cudaStream_t>(stream), pg ? pg->block_table : nullptr,
+                        pg ? pg->bt_stride : 0, pg ? pg->page_size : 0);
   return st == HYDRA_OK ? st : cuda_fail("append_kv launch");
+}
+
+extern "C" hydra_status hydra_append_kv(const hydra_heads *h, int64_t B, const void *k_new, const void *v_new,
+                                        int64_t nb, int64_t nh, void *sk, void *sv, int64_t s_sb, int64_t s_st,
+                                        int64_t s_sh, int64_t S_cap, int32_t *lens, void *stream) {
+  return append_impl(h, B, k_new, v_new, nb, nh, sk, sv, s_sb, s_st, s_sh, S_cap, lens, stream, nullptr);
+}
+
+extern "C" hydra_status hydra_append_kv_paged(const hydra_heads *h, int64_t B, const void *k_new, const void *v_new,
+                                              int64_t nb, int64_t nh, void *k_pool, void *v_pool, int64_t p_sp,
+                                              int64_t p_st, int64_t p_sh, const hydra_paging *pg, int64_t S_cap,
+                                              int32_t *lens, void *stream) {
+  if (!pg) return fail(HYDRA_EINVAL, "null paging descriptor");
+  return append_impl(h, B, k_new, v_new, nb, nh, k_pool, v_pool, p_sp, p_st, p_sh, S_cap, lens, stream, pg);
 }
 
 // ------------------------------------------------------------------ sharing tree

@@ -20,7 +20,7 @@
 
 namespace hydra {
 
-template <typename T, int D, int GQ, int U, bool kStream>
+template <typename T, int D, int GQ, int U, bool kStream, bool kPaged>
 __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeParams p) {
   constexpr int EPT = Vec16<T>::N;          // elements per thread per row
   constexpr int TPR = D / EPT;              // threads per token row
@@ -65,8 +65,11 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeParams p) 
     for (int e = 0; e < EPT; ++e) acc[i][e] = 0.f;
   }
 
-  const T *kb = reinterpret_cast<const T *>(p.k) + (int64_t)b * p.kv_sb + (int64_t)j * p.kv_sh + lane * EPT;
-  const T *vb = reinterpret_cast<const T *>(p.v) + (int64_t)b * p.kv_sb + (int64_t)j * p.kv_sh + lane * EPT;
+  // paged: kv_sb is the page stride and the block table gives each token's page
+  const int64_t seq_off = kPaged ? 0 : (int64_t)b * p.kv_sb;
+  const T *kb = reinterpret_cast<const T *>(p.k) + seq_off + (int64_t)j * p.kv_sh + lane * EPT;
+  const T *vb = reinterpret_cast<const T *>(p.v) + seq_off + (int64_t)j * p.kv_sh + lane * EPT;
+  const int32_t *btab = kPaged ? p.block_table + (int64_t)b * p.bt_stride : nullptr;
 
   // Trip count is uniform across the CTA (shuffles below need converged warps).
   for (int64_t tb = t_begin; tb < t_end; tb += (int64_t)NG * U) {
@@ -76,8 +79,10 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeParams p) 
     for (int u = 0; u < U; ++u) {
       const int64_t t = tb + grp + (int64_t)u * NG;
       valid[u] = t < t_end;
-      const int64_t off = (p.kv_tok_off + t) * p.kv_st;
       if (valid[u]) {
+        const int64_t off = kPaged ? (int64_t)__ldg(btab + (t >> p.page_shift)) * p.kv_sb +
+                                         (t & ((1 << p.page_shift) - 1)) * p.kv_st
+                                   : (p.kv_tok_off + t) * p.kv_st;
         kr[u] = ld_v4<kStream>(kb + off);
         vr[u] = ld_v4<kStream>(vb + off);
       } else {
@@ -167,10 +172,12 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeParams p) 
 template <typename T, int D, int GQ, int U>
 static cudaError_t launch_u(const DecodeParams &p, cudaStream_t s) {
   const dim3 grid(p.n_splits, p.Hkv * (p.g / GQ), p.n_seq);
-  if (p.kv_sb == 0)  // shared KV (prefix in SIMT mode): let L1 keep it
-    decode_attn_kernel<T, D, GQ, U, false><<<grid, 128, 0, s>>>(p);
+  if (p.block_table)  // paged suffix cache
+    decode_attn_kernel<T, D, GQ, U, true, true><<<grid, 128, 0, s>>>(p);
+  else if (p.kv_sb == 0)  // shared KV (prefix in SIMT mode): let L1 keep it
+    decode_attn_kernel<T, D, GQ, U, false, false><<<grid, 128, 0, s>>>(p);
   else
-    decode_attn_kernel<T, D, GQ, U, true><<<grid, 128, 0, s>>>(p);
+    decode_attn_kernel<T, D, GQ, U, true, false><<<grid, 128, 0, s>>>(p);
   return cudaGetLastError();
 }
 

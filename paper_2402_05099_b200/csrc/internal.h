@@ -28,6 +28,12 @@ struct DecodeParams {
   float *o;                     // [split][B][Hq][d] partial outputs (fp32, normalised)
   float *lse;                   // [split][B][Hq] natural-log LSE
   int64_t o_split_stride, lse_split_stride;
+  // Paged suffix cache (hydra_paging): when block_table != nullptr, token t of sequence b is
+  // at k + block_table[b * bt_stride + (t >> page_shift)] * kv_sb + (t & page_mask) * kv_st
+  // (kv_sb is then the page stride of the pool).
+  const int32_t *block_table;
+  int64_t bt_stride;
+  int32_t page_shift;
 };
 
 hydra_status launch_decode(const DecodeParams &p, hydra_dtype dt, int d, cudaStream_t s);
@@ -105,12 +111,18 @@ struct SuffixTcArgs {
   int32_t cb;      // 128-token blocks per softmax round (1 or 2)
   void *trace;     // diagnostics (suffix_trace config key); null = off
   int32_t debug;   // tc_debug_variant (timing experiments only)
+  // paged cache (block_table != nullptr): k/v are page pools [n_pages, page_size, Hkv, 128]
+  // with s_sb = page stride; S_cap = bt_stride * page_size
+  const int32_t *block_table;
+  int64_t bt_stride, n_pages;
+  int32_t page_size;
 };
 bool suffix_tc_supported(const hydra_heads *h);
 hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s);
 int device_sm_count();
 hydra_status launch_append_kv(const void *k_new, const void *v_new, int64_t nb, int64_t nh, void *sk, void *sv,
                               int64_t s_sb, int64_t s_st, int64_t s_sh, int64_t S_cap, int32_t Hkv, int32_t d,
-                              size_t es, int64_t B, int32_t *lens, cudaStream_t s);
+                              size_t es, int64_t B, int32_t *lens, cudaStream_t s,
+                              const int32_t *block_table = nullptr, int64_t bt_stride = 0, int32_t page_size = 0);
 
 }  // namespace hydra

@@ -33,6 +33,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -88,6 +89,12 @@ struct __align__(64) SuffixTcParams {
                      // tiles as they land (no MMA, no softmax), 512 = no softmax work,
                      // 4096 / 8192 = no score / PV MMA instructions
   long long *trace;  // diagnostics: CTA 0 event timestamps [kTraceRows][kTraceN] (tools/suffix_trace.py); null = off
+  // Paged cache (null = contiguous [B, S_cap, Hkv, d]): tmK / tmV then map the page pools
+  // [n_pages, page_size, Hkv, d] with a box of pbox = min(page_size, BT) tokens, and token t of
+  // sequence b is row t % page_size of page block_table[b * bt_stride + t / page_size].
+  const int32_t *block_table;
+  int64_t bt_stride;
+  int32_t page_shift, pbox_shift;  // log2(page_size), log2(pbox)
 };
 namespace stc {
 constexpr int kTraceN = 1024;
@@ -241,21 +248,44 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
           const int st = gb % NS;
           const uint32_t ph = ((gb / NS) & 1) ^ 1;
           const int t0 = n * BT;
-          if (warp == 0) {
-            uint8_t *sK = smem + OFF_K + st * TILE;
-            ptx::mbar_wait(&k_empty[st], ph);
-            ptx::mbar_arrive_expect_tx(&k_full[st], TILE);
-            ptx::tma_load_4d(sK, &P.tmK, &k_full[st], 0, j, t0, b);
-            ptx::tma_load_4d(sK + PANEL, &P.tmK, &k_full[st], 64, j, t0, b);
-            trace(tr, 9, gb);
+          const CUtensorMap *tm = warp == 0 ? &P.tmK : &P.tmV;
+          uint64_t *full = warp == 0 ? &k_full[st] : &v_full[st];
+          uint8_t *dst = smem + (warp == 0 ? OFF_K : OFF_V) + st * TILE;
+          if (P.block_table == nullptr) {
+            ptx::mbar_wait(warp == 0 ? &k_empty[st] : &v_empty[st], ph);
+            ptx::mbar_arrive_expect_tx(full, TILE);
+            ptx::tma_load_4d(dst, tm, full, 0, j, t0, b);
+            ptx::tma_load_4d(dst + PANEL, tm, full, 64, j, t0, b);
           } else {
-            uint8_t *sV = smem + OFF_V + st * TILE;
-            ptx::mbar_wait(&v_empty[st], ph);
-            ptx::mbar_arrive_expect_tx(&v_full[st], TILE);
-            ptx::tma_load_4d(sV, &P.tmV, &v_full[st], 0, j, t0, b);
-            ptx::tma_load_4d(sV + PANEL, &P.tmV, &v_full[st], 64, j, t0, b);
-            trace(tr, 10, gb);
+            // Paged: BT / pbox sub-tiles of pbox tokens, each inside one page.  Sub-tiles past
+            // lens[b] are not loaded (their block-table entries need not be valid); the rows
+            // they leave stale are masked like every row >= lens[b] (scores -> -inf, V rows
+            // zeroed by the PV warp).  Each sub-tile lands at a multiple of pbox * 128 B
+            // >= 1024 B, so the 128-B swizzle pattern equals that of one whole-tile load.
+            const int pbox = 1 << P.pbox_shift;
+            const int nsub = min(BT >> P.pbox_shift, (len - t0 + pbox - 1) >> P.pbox_shift);
+            const int32_t *bt = P.block_table + (int64_t)b * P.bt_stride;
+            int pg[BT / 8], row[BT / 8];  // page-table lookups issued before the slot wait
+#pragma unroll
+            for (int c = 0; c < BT / 8; ++c) {
+              const int t = t0 + (c << P.pbox_shift);
+              if (c < nsub) {
+                pg[c] = __ldg(bt + (t >> P.page_shift));
+                row[c] = t & ((1 << P.page_shift) - 1);
+              }
+            }
+            ptx::mbar_wait(warp == 0 ? &k_empty[st] : &v_empty[st], ph);
+            ptx::mbar_arrive_expect_tx(full, (uint32_t)nsub * pbox * 256);
+#pragma unroll
+            for (int c = 0; c < BT / 8; ++c) {
+              if (c < nsub) {
+                uint8_t *d = dst + (c << P.pbox_shift) * 128;
+                ptx::tma_load_4d(d, tm, full, 0, j, row[c], pg[c]);
+                ptx::tma_load_4d(d + PANEL, tm, full, 64, j, row[c], pg[c]);
+              }
+            }
           }
+          trace(tr, warp == 0 ? 9 : 10, gb);
         }
       }
     }
@@ -598,10 +628,16 @@ hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s)
   SuffixTcParams P;
   memset(&P, 0, sizeof(P));
   const int g = a.Hq / a.Hkv;
+  const bool paged = a.block_table != nullptr;
+  if (paged && (a.page_size < 8 || (a.page_size & (a.page_size - 1)) || a.n_pages <= 0)) return HYDRA_EUNSUPPORTED;
   {
-    const cuuint64_t dims[4] = {(cuuint64_t)stc::HD, (cuuint64_t)a.Hkv, (cuuint64_t)a.S_cap, (cuuint64_t)a.B};
+    // contiguous: [B, S_cap, Hkv, d], one 128-token box per panel; paged: the page pools
+    // [n_pages, page_size, Hkv, d] with min(page_size, 128)-token boxes
+    const int pbox = paged ? std::min(a.page_size, stc::BT) : stc::BT;
+    const cuuint64_t dims[4] = {(cuuint64_t)stc::HD, (cuuint64_t)a.Hkv,
+                                (cuuint64_t)(paged ? a.page_size : a.S_cap), (cuuint64_t)(paged ? a.n_pages : a.B)};
     const cuuint64_t strides[3] = {(cuuint64_t)a.s_sh * 2, (cuuint64_t)a.s_st * 2, (cuuint64_t)a.s_sb * 2};
-    const cuuint32_t box[4] = {64, 1, (cuuint32_t)stc::BT, 1};
+    const cuuint32_t box[4] = {64, 1, (cuuint32_t)pbox, 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     if (fn(&P.tmK, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(a.k), dims, strides, box, estr,
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -633,6 +669,12 @@ hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s)
   P.lse = a.lse;
   P.trace = reinterpret_cast<long long *>(a.trace);
   P.debug = a.debug;
+  P.block_table = a.block_table;
+  P.bt_stride = a.bt_stride;
+  if (paged) {
+    P.page_shift = __builtin_ctz((unsigned)a.page_size);
+    P.pbox_shift = __builtin_ctz((unsigned)std::min(a.page_size, stc::BT));
+  }
   if (P.n_items == 0) return HYDRA_OK;
   const int grid = n_ctas > 0 && n_ctas < P.n_items ? n_ctas : P.n_items;
   cudaError_t e = cudaErrorInvalidValue;

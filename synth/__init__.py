@@ -5,6 +5,7 @@ CUDA path (`paper_2402_05099_b200/`).  It draws random numbers and lays them out
 it contains none of the method's arithmetic (no scores, softmax, LSE or combine).
 """
 from .gen import (  # noqa: F401
+    PagedCache,
     Problem,
     TreeProblem,
     bf16_bits_to_f32,
@@ -13,6 +14,7 @@ from .gen import (  # noqa: F401
     make_tree_problem,
     normal_f32,
     normal_bf16_bits,
+    paginate,
     BF16_NAN,
     two_level_tree,
 )

@@ -337,3 +337,49 @@ def two_level_tree(root_len, n_branches, branch_len, seqs_per_branch):
     node_len = [root_len] + [branch_len] * n_branches
     leaf = np.repeat(np.arange(1, n_branches + 1, dtype=np.int32), seqs_per_branch)
     return parent, node_len, leaf
+
+
+@dataclass
+class PagedCache:
+    """A paged copy of a Problem's suffix caches (reading R14): token t of
+    sequence b is row t % page_size of page block_table[b, t // page_size] of the pools."""
+
+    page_size: int
+    k_pool: np.ndarray  # [n_pages, page_size, Hkv, d]
+    v_pool: np.ndarray
+    block_table: np.ndarray  # int32 [B, max_pages]
+
+    @property
+    def n_pages(self) -> int:
+        return self.k_pool.shape[0]
+
+
+def paginate(pb: Problem, page_size: int, seed: int = 0, spare_pages: int = 3, map_tail: bool = True,
+             unmapped: int = 2**30) -> PagedCache:
+    """Scatter pb.sk/sv into page pools in a seeded random page order.
+
+    Every sequence gets ceil(S_cap / page_size) table entries.  With map_tail=False only the
+    pages covering tokens < lens[b] are mapped and the remaining entries hold `unmapped`
+    (an out-of-range page id the kernels must never read).  Spare pages and page rows past
+    S_cap are poisoned with NaN, as the suffix padding already is (layout only, no arithmetic).
+    """
+    rng = np.random.default_rng(seed)
+    max_pages = -(-pb.S_cap // page_size)
+    used = [max_pages if map_tail else -(-int(pb.lens[b]) // page_size) for b in range(pb.B)]
+    n_pages = sum(used) + spare_pages
+    perm = rng.permutation(n_pages).astype(np.int32)
+    nan = BF16_NAN if pb.dtype == "bf16" else F32_NAN
+    shape = (n_pages, page_size, pb.Hkv, pb.d)
+    k_pool = np.full(shape, nan, dtype=pb.sk.dtype)
+    v_pool = np.full(shape, nan, dtype=pb.sv.dtype)
+    table = np.full((pb.B, max(1, max_pages)), unmapped, np.int32)
+    nxt = 0
+    for b in range(pb.B):
+        for i in range(used[b]):
+            page = perm[nxt]
+            nxt += 1
+            table[b, i] = page
+            lo, hi = i * page_size, min(pb.S_cap, (i + 1) * page_size)
+            k_pool[page, :hi - lo] = pb.sk[b, lo:hi]
+            v_pool[page, :hi - lo] = pb.sv[b, lo:hi]
+    return PagedCache(page_size, k_pool, v_pool, table)

@@ -130,3 +130,31 @@ def test_python_api_refuses_cpu_tensors():
     k = torch.zeros(8, 2, 128, dtype=torch.bfloat16)
     with pytest.raises(ValueError, match="CUDA"):
         hydra.prefix_attn(q, k, k)
+
+
+def test_paged_validation_errors(lib):
+    """hydra_paging checks (include/hydra.h): page_size a power of two >= 8, n_pages >= 1,
+    S_cap <= bt_stride * page_size, non-null table -- all rejected before any launch."""
+    h = H()
+
+    def suffix(pg, S_cap=64):
+        return lib.hydra_suffix_attn_paged(ctypes.byref(h), 2, FAKE, 512, 128, FAKE, FAKE, 16 * 2 * 128, 2 * 128,
+                                           128, ctypes.byref(pg) if pg is not None else None, S_cap, FAKE, FAKE,
+                                           FAKE, None, 0, None)
+
+    P = _lib.Paging
+    assert suffix(None) == _lib.HYDRA_EINVAL
+    assert suffix(P(None, 4, 16, 8)) == _lib.HYDRA_EINVAL  # null block table
+    assert suffix(P(FAKE, 4, 12, 8)) == _lib.HYDRA_ESHAPE  # not a power of two
+    assert suffix(P(FAKE, 8, 4, 8)) == _lib.HYDRA_ESHAPE  # below 8 tokens
+    assert suffix(P(FAKE, 4, 16, 0)) == _lib.HYDRA_ESHAPE  # empty pool
+    assert suffix(P(FAKE, 3, 16, 8)) == _lib.HYDRA_ESHAPE  # 3 * 16 < S_cap = 64
+    assert "bt_stride" in lib.hydra_last_error().decode()
+    assert lib.hydra_append_kv_paged(ctypes.byref(h), 2, FAKE, FAKE, 256, 128, FAKE, FAKE, 4096, 256, 128, None, 64,
+                                     FAKE, None) == _lib.HYDRA_EINVAL
+    assert lib.hydra_append_kv_paged(ctypes.byref(h), 2, FAKE, FAKE, 256, 128, FAKE, FAKE, 4096, 256, 128,
+                                     ctypes.byref(P(FAKE, 2, 16, 8)), 64, FAKE, None) == _lib.HYDRA_ESHAPE
+    need = lib.hydra_workspace_size(_lib.HYDRA_OP_ATTN, ctypes.byref(h), 2, 256, 64, 0)
+    assert lib.hydra_attn_paged(ctypes.byref(h), 2, FAKE, 512, 128, 256, FAKE, FAKE, 256, 128, FAKE, FAKE, 4096, 256,
+                                128, ctypes.byref(P(FAKE, 4, 24, 8)), 64, FAKE, FAKE, 0, None, FAKE, need, None,
+                                None) == _lib.HYDRA_ESHAPE

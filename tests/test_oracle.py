@@ -332,3 +332,48 @@ def test_tree_equals_explicit_flattening_and_path_lengths():
         ob, lb = oracle.attention_segments(tp.q[b:b + 1], [[(K, V)]], 2)
         np.testing.assert_allclose(ob[0], o[b], atol=1e-14)
         np.testing.assert_allclose(lb[0], l[b], atol=1e-14)
+
+
+# ---------------------------------------------------------------- paged suffix cache (reading R14)
+def test_paged_rows_hand_example():
+    """Hand-laid pool: page_size 2, sequence table [2, 0] -> tokens are (page 2, row 0),
+    (page 2, row 1), (page 0, row 0) -- the expected rows are written out, not computed."""
+    pool = np.arange(3 * 2 * 1 * 2, dtype=np.float32).reshape(3, 2, 1, 2)  # value = 4*page + 2*row + i
+    got = oracle.paged_rows(pool, np.array([2, 0], np.int32), 2, 3)
+    want = np.array([[[8, 9]], [[10, 11]], [[0, 1]]], np.float32)
+    assert np.array_equal(got, want)
+    assert oracle.paged_rows(pool, np.array([1], np.int32), 2, 0).shape == (0, 1, 2)
+
+
+@pytest.mark.parametrize("page_size,map_tail", [(8, True), (16, False), (64, True), (256, False)])
+def test_paged_suffix_equals_contiguous(page_size, map_tail):
+    """Reading R14: paging only moves rows, so the paged oracle reproduces the contiguous
+    suffix result bit for bit (same rows, same order, same fp64 arithmetic), with unmapped
+    table entries past lens[b] and NaN-poisoned spare pages never read."""
+    pb = synth.make_problem(5, 4, 2, 32, 0, 70, lens=[0, 1, 8, 69, 70], dtype="bf16", dist="mixed", seed=7)
+    pc = synth.paginate(pb, page_size, seed=3, map_tail=map_tail)
+    o_ref, l_ref = oracle.suffix_only(pb)
+    o, l = oracle.suffix_only_paged(pb.q, pc.k_pool, pc.v_pool, pc.block_table, page_size, pb.lens, pb.Hkv,
+                                    pb.scale)
+    assert np.array_equal(o, o_ref) and np.array_equal(l, l_ref)
+    assert np.isneginf(l[0]).all() and (o[0] == 0).all()  # empty suffix sentinel (R6)
+
+
+def test_paged_flat_attention_equals_contiguous():
+    pb = synth.make_problem(3, 8, 2, 16, 40, 33, lens=[33, 5, 17], dtype="f32", dist="mixed", seed=9)
+    pc = synth.paginate(pb, 8, seed=1)
+    o_ref, l_ref = oracle.flat_attention(pb)
+    o, l = oracle.flat_attention_paged(pb, pc)
+    assert np.array_equal(o, o_ref) and np.array_equal(l, l_ref)
+
+
+def test_paginate_is_a_permutation_of_the_suffix_rows():
+    """The synthetic paged layout holds every suffix row exactly once (layout check of synth)."""
+    pb = synth.make_problem(4, 2, 2, 16, 0, 20, lens=[20, 3, 0, 11], dtype="bf16", seed=2)
+    pc = synth.paginate(pb, 8, seed=5, spare_pages=2)
+    ids = pc.block_table[pc.block_table < pc.n_pages]
+    assert len(set(ids.tolist())) == ids.size == 4 * 3 and pc.n_pages == 14
+    for b in range(pb.B):
+        for t in range(pb.S_cap):
+            assert np.array_equal(pc.k_pool[pc.block_table[b, t // 8], t % 8], pb.sk[b, t], equal_nan=False) \
+                or np.isnan(synth.bf16_bits_to_f32(pb.sk[b, t])).all()
