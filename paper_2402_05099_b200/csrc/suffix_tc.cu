@@ -48,8 +48,8 @@ constexpr int BT = 128;   // tokens per block (UMMA M of S^T, K of PV)
 constexpr int HD = 128;   // head dim (UMMA K of S^T, M of PV)
 constexpr int NQ = 16;    // padded query heads per KV group (UMMA N)
 constexpr int NS = 3;     // K stages and V stages (separate rings: K frees after S, V after PV)
-constexpr int kThreads = 416;  // warp 0 K producer, 1 score MMA, 2-5 softmax, 6 V producer, 7 Q producer,
-                               // 8-11 epilogue, 12 PV MMA
+constexpr int kThreads = 448;  // warp 0 K producer, 1 score MMA, 2-5 softmax, 6 V producer, 7 Q producer,
+                               // 8-11 epilogue, 12 PV MMA, 13 paged-cache block-table loader
 constexpr int PANEL = BT * 128;      // 128 rows x 128 B
 constexpr int TILE = 2 * PANEL;      // 32 KB
 constexpr int QPANEL = NQ * 128;     // 2 KB: 16 rows x 64 dims
@@ -72,7 +72,11 @@ __host__ __device__ constexpr int off_bar(int cb) { return off_red(cb) + (2 * 4 
 // k_full, k_empty, v_full, v_empty [NS]; q_full, q_empty [4]; s_full, p_full, pv_done [4];
 // o_free, o_full, ml_full [2]
 constexpr int N_BARS = 4 * NS + 8 + 12 + 6;
-__host__ __device__ constexpr int alloc_bytes(int cb) { return off_bar(cb) + N_BARS * 8 + 16 + 1024; }
+// Paged cache: a ring of PR tiles' page ids (16 sub-tiles max) shared by the K and V
+// producers, filled with cp.async by warp 13 (tab_full / tab_empty barriers).
+constexpr int PR = 6;
+__host__ __device__ constexpr int off_tab(int cb) { return off_bar(cb) + N_BARS * 8 + 16; }
+__host__ __device__ constexpr int alloc_bytes(int cb) { return off_tab(cb) + PR * (16 * 4 + 16) + 1024; }
 static_assert(alloc_bytes(1) <= 232448 && alloc_bytes(2) <= 232448, "suffix_tc smem over the 227 KB opt-in limit");
 // S^T x 2 round slots x CB blocks (16 columns each), O^T x 2; rounded up to a power of two
 __host__ __device__ constexpr uint32_t tmem_cols(int cb) { return 128u; }  // nsp*cb*16 + 2*16 <= 128
@@ -115,6 +119,36 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 // fetches the next item's length one item early so the load is off the critical path.
 __device__ __forceinline__ int item_len(const SuffixTcParams &P, int item) {
   return item < P.n_items ? __ldg(P.lens + item / P.Hkv) : 0;
+}
+
+// Paged cache: one lane of warp 13 walks the CTA's tile sequence (the one the K / V
+// producers walk) up to PR tiles ahead of them and copies each tile's block-table entries into
+// ring slot (tile % PR) with cp.async, tracked by tab_full[slot] (cp.async.mbarrier.arrive).
+// The producers' own threads do not load the entries: a global load issued by a TMA-issuing
+// thread returned only after that thread's in-flight tiles had landed (measured: the ring
+// collapsed to about one tile in flight, 3.6 of 7.2 TB/s at 76 SMs).
+__device__ __forceinline__ void page_table_lane(const SuffixTcParams &P, int32_t *ring, uint64_t *tab_full,
+                                                uint64_t *tab_empty) {
+  uint32_t k = 0;
+  for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
+    const int len = item_len(P, item);
+    const int nblk = (len + stc::BT - 1) / stc::BT;
+    const int32_t *bt = P.block_table + (int64_t)(item / P.Hkv) * P.bt_stride;
+    for (int n = 0; n < nblk; ++n, ++k) {
+      const int slot = k % stc::PR;
+      ptx::mbar_wait(&tab_empty[slot], ((k / stc::PR) & 1) ^ 1);
+      const int t0 = n * stc::BT;
+      const int nsub = min(stc::BT >> P.pbox_shift, (len - t0 + (1 << P.pbox_shift) - 1) >> P.pbox_shift);
+      const uint32_t dst = ptx::smem_u32(ring + slot * 16);
+      for (int c = 0; c < nsub; ++c)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + 4 * c),
+                     "l"(bt + ((t0 + (c << P.pbox_shift)) >> P.page_shift))
+                     : "memory");
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(ptx::smem_u32(&tab_full[slot]))
+                   : "memory");
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // Walks the rounds (up to CB consecutive 128-token blocks of one item) a CTA processes, in
@@ -180,6 +214,9 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
   uint64_t *q_full = bars + 4 * NS, *q_empty = q_full + 4, *s_full = q_full + 8, *p_full = q_full + 12,
            *pv_done = q_full + 16, *o_free = q_full + 20, *o_full = q_full + 22, *ml_full = q_full + 24;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + N_BARS);
+  int32_t *tab_ring = reinterpret_cast<int32_t *>(smem + off_tab(CB));                  // [PR][16] page ids
+  uint64_t *tab_full = reinterpret_cast<uint64_t *>(smem + off_tab(CB) + PR * 16 * 4);  // [PR]
+  uint64_t *tab_empty = tab_full + PR;                                                   // [PR]
   float *red_max = reinterpret_cast<float *>(smem + OFF_RED);  // [2][4][NQ]
   float *red_sum = red_max + 2 * 4 * NQ;                        // [2][4][NQ] per-warp row-sum partials
   float *item_m = red_sum + 2 * 4 * NQ;                         // [2][NQ] running max per head (log2)
@@ -194,6 +231,10 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
     ptx::prefetch_tmap(&P.tmK);
     ptx::prefetch_tmap(&P.tmV);
     ptx::prefetch_tmap(&P.tmQ);
+    for (int i = 0; i < PR; ++i) {
+      ptx::mbar_init(&tab_full[i], 1);   // the table lane's cp.async arrival (noinc)
+      ptx::mbar_init(&tab_empty[i], 2);  // K and V producers
+    }
     for (int i = 0; i < NS; ++i) {
       ptx::mbar_init(&k_full[i], 1);
       ptx::mbar_init(&k_empty[i], 1);
@@ -220,7 +261,11 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 || warp == 6 || warp == 7) {
+  if (warp == 13) {
+    // ================= paged cache: block-table entries into the page-id ring =================
+    if (P.block_table != nullptr && !(P.debug & 131072) && ptx::elect_one())
+      page_table_lane(P, tab_ring, tab_full, tab_empty);
+  } else if (warp == 0 || warp == 6 || warp == 7) {
     // ================= TMA producers: warp 0 K ring, warp 6 V ring, warp 7 Q slots =================
     // Separate threads so no load waits behind another kind of slot (V slots free only after
     // the PV MMA, K slots right after the score MMA, Q slots after an item's last PV).
@@ -251,7 +296,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
           const CUtensorMap *tm = warp == 0 ? &P.tmK : &P.tmV;
           uint64_t *full = warp == 0 ? &k_full[st] : &v_full[st];
           uint8_t *dst = smem + (warp == 0 ? OFF_K : OFF_V) + st * TILE;
-          if (P.block_table == nullptr) {
+          if (P.block_table == nullptr || (P.debug & 131072)) {  // 131072: timing experiment
             ptx::mbar_wait(warp == 0 ? &k_empty[st] : &v_empty[st], ph);
             ptx::mbar_arrive_expect_tx(full, TILE);
             ptx::tma_load_4d(dst, tm, full, 0, j, t0, b);
@@ -262,28 +307,20 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
             // they leave stale are masked like every row >= lens[b] (scores -> -inf, V rows
             // zeroed by the PV warp).  Each sub-tile lands at a multiple of pbox * 128 B
             // >= 1024 B, so the 128-B swizzle pattern equals that of one whole-tile load.
-            const int pbox = 1 << P.pbox_shift;
-            const int nsub = min(BT >> P.pbox_shift, (len - t0 + pbox - 1) >> P.pbox_shift);
-            const int32_t *bt = P.block_table + (int64_t)b * P.bt_stride;
-            int pg[BT / 8], row[BT / 8];  // page-table lookups issued before the slot wait
-#pragma unroll
-            for (int c = 0; c < BT / 8; ++c) {
-              const int t = t0 + (c << P.pbox_shift);
-              if (c < nsub) {
-                pg[c] = __ldg(bt + (t >> P.page_shift));
-                row[c] = t & ((1 << P.page_shift) - 1);
-              }
-            }
+            const int ts = gb % PR;
+            ptx::mbar_wait(&tab_full[ts], (gb / PR) & 1);  // this tile's page ids have landed
+            const int nsub = min(BT >> P.pbox_shift, (len - t0 + (1 << P.pbox_shift) - 1) >> P.pbox_shift);
             ptx::mbar_wait(warp == 0 ? &k_empty[st] : &v_empty[st], ph);
-            ptx::mbar_arrive_expect_tx(full, (uint32_t)nsub * pbox * 256);
-#pragma unroll
-            for (int c = 0; c < BT / 8; ++c) {
-              if (c < nsub) {
-                uint8_t *d = dst + (c << P.pbox_shift) * 128;
-                ptx::tma_load_4d(d, tm, full, 0, j, row[c], pg[c]);
-                ptx::tma_load_4d(d + PANEL, tm, full, 64, j, row[c], pg[c]);
-              }
+            ptx::mbar_arrive_expect_tx(full, (uint32_t)nsub * (256u << P.pbox_shift));
+#pragma unroll 1
+            for (int c = 0; c < nsub; ++c) {
+              const int pg = tab_ring[ts * 16 + c];
+              const int row = (t0 + (c << P.pbox_shift)) & ((1 << P.page_shift) - 1);
+              uint8_t *d = dst + (c << P.pbox_shift) * 128;
+              ptx::tma_load_4d(d, tm, full, 0, j, row, pg);
+              ptx::tma_load_4d(d + PANEL, tm, full, 64, j, row, pg);
             }
+            ptx::mbar_arrive(&tab_empty[ts]);
           }
           trace(tr, warp == 0 ? 9 : 10, gb);
         }

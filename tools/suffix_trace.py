@@ -15,16 +15,23 @@ q = torch.randn(B, H, 128, device=dev, generator=g).bfloat16()
 sk = torch.randn(B, S, H, 128, device=dev, generator=g).bfloat16()
 sv = torch.randn(B, S, H, 128, device=dev, generator=g).bfloat16()
 lens = torch.full((B,), S, dtype=torch.int32, device=dev)
+PAGED = int(os.environ.get("PAGED", 0))  # page size: the same caches through the paged path (identity table)
+if PAGED:
+    tab = torch.arange(B * (S // PAGED), device=dev, dtype=torch.int32).view(B, S // PAGED)
+    kp, vp = sk.view(-1, PAGED, H, 128), sv.view(-1, PAGED, H, 128)
+    call = lambda: hydra.suffix_attn_paged(q, kp, vp, tab, lens)
+else:
+    call = lambda: hydra.suffix_attn(q, sk, sv, lens)
 N = 1024
 tr = torch.zeros(13, N, dtype=torch.int64, device=dev)
 hydra.set_config("suffix_impl", 2); hydra.set_config("suffix_ctas", ctas); hydra.set_config("suffix_cb", cb)
 hydra.set_config("tc_debug_variant", int(os.environ.get("DEBUG", 0)))
 for _ in range(2):
-    hydra.suffix_attn(q, sk, sv, lens)
+    call()
 torch.cuda.synchronize()
 hydra.set_config("suffix_trace", tr.data_ptr())
 e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-e0.record(); hydra.suffix_attn(q, sk, sv, lens); e1.record()
+e0.record(); call(); e1.record()
 torch.cuda.synchronize()
 hydra.set_config("suffix_trace", 0); hydra.set_config("tc_debug_variant", 0); hydra.set_config("suffix_impl", 0); hydra.set_config("suffix_ctas", 0); hydra.set_config("suffix_cb", 2)
 ms = e0.elapsed_time(e1)
