@@ -124,9 +124,9 @@ __device__ __forceinline__ int item_len(const SuffixTcParams &P, int item) {
 // Paged cache: one lane of warp 13 walks the CTA's tile sequence (the one the K / V
 // producers walk) up to PR tiles ahead of them and copies each tile's block-table entries into
 // ring slot (tile % PR) with cp.async, tracked by tab_full[slot] (cp.async.mbarrier.arrive).
-// The producers' own threads do not load the entries: a global load issued by a TMA-issuing
-// thread returned only after that thread's in-flight tiles had landed (measured: the ring
-// collapsed to about one tile in flight, 3.6 of 7.2 TB/s at 76 SMs).
+// Measured (tools/paged_rate.py, C3 suffix on 76 SMs): block-table loads in the producer
+// thread, or this loop on a second lane of the producer warp, held the paged kernel at
+// 3.6-4.0 TB/s even with identity pages; on its own warp 6.4-6.6 TB/s (pages >= 16).
 __device__ __forceinline__ void page_table_lane(const SuffixTcParams &P, int32_t *ring, uint64_t *tab_full,
                                                 uint64_t *tab_empty) {
   uint32_t k = 0;
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
 
   if (warp == 13) {
     // ================= paged cache: block-table entries into the page-id ring =================
-    if (P.block_table != nullptr && !(P.debug & 131072) && ptx::elect_one())
+    if (P.block_table != nullptr && ptx::elect_one())
       page_table_lane(P, tab_ring, tab_full, tab_empty);
   } else if (warp == 0 || warp == 6 || warp == 7) {
     // ================= TMA producers: warp 0 K ring, warp 6 V ring, warp 7 Q slots =================
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
           const CUtensorMap *tm = warp == 0 ? &P.tmK : &P.tmV;
           uint64_t *full = warp == 0 ? &k_full[st] : &v_full[st];
           uint8_t *dst = smem + (warp == 0 ? OFF_K : OFF_V) + st * TILE;
-          if (P.block_table == nullptr || (P.debug & 131072)) {  // 131072: timing experiment
+          if (P.block_table == nullptr) {
             ptx::mbar_wait(warp == 0 ? &k_empty[st] : &v_empty[st], ph);
             ptx::mbar_arrive_expect_tx(full, TILE);
             ptx::tma_load_4d(dst, tm, full, 0, j, t0, b);
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
             const int nsub = min(BT >> P.pbox_shift, (len - t0 + (1 << P.pbox_shift) - 1) >> P.pbox_shift);
             ptx::mbar_wait(warp == 0 ? &k_empty[st] : &v_empty[st], ph);
             ptx::mbar_arrive_expect_tx(full, (uint32_t)nsub * (256u << P.pbox_shift));
-#pragma unroll 1
+#pragma unroll 8
             for (int c = 0; c < nsub; ++c) {
               const int pg = tab_ring[ts * 16 + c];
               const int row = (t0 + (c << P.pbox_shift)) & ((1 << P.page_shift) - 1);
