@@ -15,6 +15,7 @@ ap.add_argument("--suffix-impl", type=int, default=0)
 ap.add_argument("--prefix-impl", type=int, default=0)
 ap.add_argument("--suffix-ctas", type=int, default=0)
 ap.add_argument("--prefix-ctas", type=int, default=0)
+ap.add_argument("--paged", type=int, default=0, help="suffix in a shuffled page pool of this page size")
 a = ap.parse_args()
 dev = torch.device("cuda:0")
 hydra.set_config("prefix_splits", a.splits)
@@ -32,9 +33,19 @@ sk = torch.randn(a.B, S, a.Hkv, 128, device=dev, generator=g).bfloat16()
 sv = torch.randn(a.B, S, a.Hkv, 128, device=dev, generator=g).bfloat16()
 lens = torch.full((a.B,), S, dtype=torch.int32, device=dev)
 ws = torch.empty(hydra.attn_workspace_bytes(q, a.P, S, a.Hkv), dtype=torch.uint8, device=dev)
+if a.paged:
+    npg = S // a.paged
+    perm = torch.randperm(a.B * npg, device=dev, generator=g)
+    kp = torch.empty(a.B * npg, a.paged, a.Hkv, 128, dtype=torch.bfloat16, device=dev)
+    vp = torch.empty_like(kp)
+    kp[perm] = sk.view(-1, a.paged, a.Hkv, 128)
+    vp[perm] = sv.view(-1, a.paged, a.Hkv, 128)
+    tab = perm.view(a.B, npg).to(torch.int32)
 for _ in range(a.iters):
     if a.what == "prefix":
         hydra.prefix_attn(q, pk, pv, workspace=ws)
+    elif a.what == "suffix" and a.paged:
+        hydra.suffix_attn_paged(q, kp, vp, tab, lens, workspace=ws)
     elif a.what == "suffix":
         hydra.suffix_attn(q, sk, sv, lens, workspace=ws)
     else:
