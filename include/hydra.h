@@ -263,6 +263,16 @@ HYDRA_API hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra_
                              void *out, hydra_dtype out_dtype, float *lse_out,
                              void *ws, size_t ws_bytes, void *stream, void *stream_aux);
 
+/* hydra_tree_attn with the sequences' suffixes in a paged cache (hydra_paging above); the
+ * node K/V stay pooled [T_nodes, Hkv, d].  Workspace as hydra_tree_attn. */
+HYDRA_API hydra_status hydra_tree_attn_paged(const hydra_heads *h, const struct hydra_tree *t,
+                                   const void *q, int64_t q_sb, int64_t q_sh,
+                                   const void *node_k, const void *node_v, int64_t kv_st, int64_t kv_sh,
+                                   const void *k_pool, const void *v_pool, int64_t p_sp, int64_t p_st, int64_t p_sh,
+                                   const hydra_paging *pg, int64_t S_cap, const int32_t *lens,
+                                   void *out, hydra_dtype out_dtype, float *lse_out,
+                                   void *ws, size_t ws_bytes, void *stream, void *stream_aux);
+
 /* Bytes of device workspace the op needs for these sizes (0 if none). */
 HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, int64_t P, int64_t S_cap,
                             int32_t n_parts);

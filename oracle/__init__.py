@@ -205,6 +205,21 @@ def tree_attention(tp, rows=None, threads: int = 0):
     return attention_segments(tp.q, segs, tp.Hkv, tp.scale, rows, threads)
 
 
+def tree_attention_paged(tp, pc, rows=None, threads: int = 0):
+    """tree_attention with each sequence's suffix read from a paged cache pc (reading R14)."""
+    segs = []
+    for b in range(tp.B):
+        lst = []
+        for n in tree_path(tp.parent, tp.leaf_of_seq[b]):
+            lo, L = int(tp.node_off[n]), int(tp.node_len[n])
+            lst.append((tp.node_k[lo:lo + L], tp.node_v[lo:lo + L]))
+        n_suf = int(tp.lens[b])
+        lst.append((paged_rows(pc.k_pool, pc.block_table[b], pc.page_size, n_suf),
+                    paged_rows(pc.v_pool, pc.block_table[b], pc.page_size, n_suf)))
+        segs.append(lst)
+    return attention_segments(tp.q, segs, tp.Hkv, tp.scale, rows, threads)
+
+
 def combine(o1, lse1, o2, lse2):
     """App. B `combine_lse`, fp64, plus the merged LSE (reading R5).
 

@@ -17,4 +17,5 @@ from .attn import (  # noqa: F401
     suffix_attn,
     suffix_attn_paged,
     tree_attention,
+    tree_attention_paged,
 )

@@ -22,7 +22,7 @@ EXPORTED = ["hydra_prefix_attn", "hydra_suffix_attn", "hydra_combine", "hydra_at
             "hydra_tree_destroy", "hydra_tree_depth", "hydra_tree_group_size", "hydra_tree_workspace_size",
             "hydra_tree_attn", "hydra_workspace_size", "hydra_set_config", "hydra_get_config",
             "hydra_last_error", "hydra_version", "hydra_append_kv", "hydra_suffix_attn_paged", "hydra_attn_paged",
-            "hydra_append_kv_paged"]
+            "hydra_append_kv_paged", "hydra_tree_attn_paged"]
 
 
 class HydraError(RuntimeError):
@@ -80,6 +80,8 @@ def load():
                                   _i64, _PP, _i64, _vp, _vp, _i32, _vp, _vp, _sz, _vp, _vp]),
         "hydra_append_kv_paged": (st, [_HP, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _PP, _i64, _vp,
                                        _vp]),
+        "hydra_tree_attn_paged": (st, [_HP, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64,
+                                       _i64, _PP, _i64, _vp, _vp, _i32, _vp, _vp, _sz, _vp, _vp]),
         "hydra_set_config": (st, [ctypes.c_char_p, _i64]),
         "hydra_get_config": (_i64, [ctypes.c_char_p]),
         "hydra_last_error": (ctypes.c_char_p, []),

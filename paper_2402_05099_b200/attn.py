@@ -418,3 +418,39 @@ def tree_attention(q: torch.Tensor, tree: Tree, node_k: torch.Tensor, node_v: to
                               _stream_ptr(aux_stream, q.device) if aux_stream is not None else None),
           "hydra_tree_attn")
     return (out, lse) if return_lse else out
+
+
+def tree_attention_paged(q: torch.Tensor, tree: Tree, node_k: torch.Tensor, node_v: torch.Tensor,
+                         k_pool: torch.Tensor, v_pool: torch.Tensor, block_table: torch.Tensor,
+                         suffix_lens: torch.Tensor, S_cap: Optional[int] = None, scale: Optional[float] = None,
+                         out_dtype=None, return_lse: bool = False, workspace: Optional[torch.Tensor] = None,
+                         stream=None, aux_stream=None):
+    """tree_attention with the suffixes in a paged cache (pools [n_pages, page_size, Hkv, d],
+    block_table int32 [B, max_pages]; reading R14)."""
+    q = _squeeze_q(q)
+    node_k, node_v = _kv3(node_k, "node_k"), _kv3(node_v, "node_v")
+    _require_cuda(q, node_k, node_v, suffix_lens)
+    B, Hq, d = q.shape
+    if B != tree.B:
+        raise ValueError("q batch does not match the tree's sequence count")
+    Hkv = node_k.shape[1]
+    if k_pool.dim() != 4 or k_pool.shape[2] != Hkv:
+        raise ValueError("k_pool must be [n_pages, page_size, Hkv, d]")
+    if suffix_lens.dtype != torch.int32 or suffix_lens.shape != (B,):
+        raise ValueError("suffix_lens must be int32 [B]")
+    pg, S_cap = _paging(k_pool, v_pool, block_table, B, S_cap)
+    h = _heads(q, Hkv, scale)
+    lib = _lib.load()
+    out_dtype = out_dtype or (torch.bfloat16 if q.dtype == torch.bfloat16 else torch.float32)
+    out = torch.empty(B, Hq, d, dtype=out_dtype, device=q.device)
+    lse = torch.empty(B, Hq, dtype=torch.float32, device=q.device) if return_lse else None
+    ws = _workspace(lib.hydra_tree_workspace_size(ctypes.byref(h), tree.handle, S_cap), q.device, workspace)
+    ss = k_pool.stride()
+    check(lib.hydra_tree_attn_paged(ctypes.byref(h), tree.handle, q.data_ptr(), q.stride(0), q.stride(1),
+                                    node_k.data_ptr(), node_v.data_ptr(), node_k.stride(0), node_k.stride(1),
+                                    k_pool.data_ptr(), v_pool.data_ptr(), ss[0], ss[1], ss[2], ctypes.byref(pg),
+                                    S_cap, suffix_lens.data_ptr(), out.data_ptr(), _DT[out_dtype], _ptr(lse),
+                                    _ptr(ws), ws.numel(), _stream_ptr(stream, q.device),
+                                    _stream_ptr(aux_stream, q.device) if aux_stream is not None else None),
+          "hydra_tree_attn_paged")
+    return (out, lse) if return_lse else out

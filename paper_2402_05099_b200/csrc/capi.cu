@@ -894,12 +894,11 @@ extern "C" size_t hydra_tree_workspace_size(const hydra_heads *h, const struct h
   return part_bytes(h, t->B) * (size_t)(t->max_depth * tree_prefix_splits(h, t) + suffix_splits(h, t->B, S_cap));
 }
 
-extern "C" hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra_tree *t, const void *q, int64_t q_sb,
-                                        int64_t q_sh, const void *node_k, const void *node_v, int64_t kv_st,
-                                        int64_t kv_sh, const void *sk, const void *sv, int64_t s_sb, int64_t s_st,
-                                        int64_t s_sh, int64_t S_cap, const int32_t *lens, void *out,
-                                        hydra_dtype out_dtype, float *lse_out, void *ws, size_t ws_bytes,
-                                        void *stream, void *stream_aux) {
+static hydra_status tree_impl(const hydra_heads *h, const struct hydra_tree *t, const void *q, int64_t q_sb,
+                              int64_t q_sh, const void *node_k, const void *node_v, int64_t kv_st, int64_t kv_sh,
+                              const void *sk, const void *sv, int64_t s_sb, int64_t s_st, int64_t s_sh,
+                              int64_t S_cap, const int32_t *lens, void *out, hydra_dtype out_dtype, float *lse_out,
+                              void *ws, size_t ws_bytes, void *stream, void *stream_aux, const hydra_paging *pg) {
   hydra_status st = check_heads(h);
   if (st) return st;
   if (!t) return fail(HYDRA_EINVAL, "tree is NULL");
@@ -1041,7 +1040,7 @@ extern "C" hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra
   suf.lse = all.lse + all.lse_stride * (int64_t)(t->max_depth * np);
   if (S_cap > 0) {
     st = run_suffix(h, B, q, q_sb, q_sh, sk, sv, s_sb, s_st, s_sh, S_cap, lens, ns, suf, s,
-                    k_over > 0 ? std::max(1, sms - k_over) : 0);
+                    k_over > 0 ? std::max(1, sms - k_over) : 0, pg);
     if (st) return st;
   } else {
     st = launch_fill_neg_inf(suf.lse, rows, s);
@@ -1052,4 +1051,29 @@ extern "C" hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra
       return cuda_fail("join");
   }
   return run_combine(rows, h->head_dim, n_parts, all, out, out_dtype, lse_out, s);
+}
+
+extern "C" hydra_status hydra_tree_attn(const hydra_heads *h, const struct hydra_tree *t, const void *q, int64_t q_sb,
+                                        int64_t q_sh, const void *node_k, const void *node_v, int64_t kv_st,
+                                        int64_t kv_sh, const void *sk, const void *sv, int64_t s_sb, int64_t s_st,
+                                        int64_t s_sh, int64_t S_cap, const int32_t *lens, void *out,
+                                        hydra_dtype out_dtype, float *lse_out, void *ws, size_t ws_bytes,
+                                        void *stream, void *stream_aux) {
+  return tree_impl(h, t, q, q_sb, q_sh, node_k, node_v, kv_st, kv_sh, sk, sv, s_sb, s_st, s_sh, S_cap, lens, out,
+                   out_dtype, lse_out, ws, ws_bytes, stream, stream_aux, nullptr);
+}
+
+extern "C" hydra_status hydra_tree_attn_paged(const hydra_heads *h, const struct hydra_tree *t, const void *q,
+                                              int64_t q_sb, int64_t q_sh, const void *node_k, const void *node_v,
+                                              int64_t kv_st, int64_t kv_sh, const void *k_pool, const void *v_pool,
+                                              int64_t p_sp, int64_t p_st, int64_t p_sh, const hydra_paging *pg,
+                                              int64_t S_cap, const int32_t *lens, void *out, hydra_dtype out_dtype,
+                                              float *lse_out, void *ws, size_t ws_bytes, void *stream,
+                                              void *stream_aux) {
+  if (S_cap > 0) {
+    hydra_status st = check_paging(pg, S_cap);
+    if (st) return st;
+  }
+  return tree_impl(h, t, q, q_sb, q_sh, node_k, node_v, kv_st, kv_sh, k_pool, v_pool, p_sp, p_st, p_sh, S_cap, lens,
+                   out, out_dtype, lse_out, ws, ws_bytes, stream, stream_aux, S_cap > 0 ? pg : nullptr);
 }

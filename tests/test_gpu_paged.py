@@ -189,3 +189,32 @@ def test_c3_16k_paged_full_size():
     rows = sample_rows(B, Hq, seed=3)
     ref, lref = oracle.flat_attention(pb, rows=rows)
     check_rows(out, lse, ref, lref, rows, "C3@16K paged(16)")
+
+
+@pytest.mark.parametrize("aux", [False, True])
+def test_tree_paged_parity(aux):
+    """Tree attention (§3.3) with the suffixes in 16-token pages; with aux the node attention and
+    the tensor-core suffix run on disjoint SM sets."""
+    from tests.util import tree_to
+
+    parent, node_len, leaf = synth.two_level_tree(300, 2, 200, 40)
+    tp = synth.make_tree_problem(parent, node_len, leaf, 16, 4, 128, 200, dtype="bf16", dist="mixed", seed=31,
+                                 lens=np.arange(80) * 7 % 201)
+    pc = synth.paginate(tp, 16, seed=8, map_tail=False)
+    t = tree_to(tp, DEV)
+    kp, vp, tab = paged_to(pc, "bf16")
+    tree = hydra.Tree(tp.parent, tp.node_off, tp.node_len, tp.leaf_of_seq)
+    if aux:
+        hydra.set_config("suffix_impl", 2)
+        hydra.set_config("overlap_prefix_ctas", 32)
+    out, lse = hydra.tree_attention_paged(t["q"], tree, t["node_k"], t["node_v"], kp, vp, tab, t["lens"],
+                                          S_cap=tp.S_cap, return_lse=True,
+                                          aux_stream=torch.cuda.Stream() if aux else None)
+    torch.cuda.synchronize()
+    ref, lref = oracle.tree_attention_paged(tp, pc)
+    assert_parity(out, ref, lse, lref, what=f"tree paged aux={aux}")
+    out2, lse2 = hydra.tree_attention(t["q"], tree, t["node_k"], t["node_v"], t["sk"], t["sv"], t["lens"],
+                                      return_lse=True, aux_stream=torch.cuda.Stream() if aux else None)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out2) and torch.equal(lse, lse2)
+    tree.destroy()

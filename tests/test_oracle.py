@@ -377,3 +377,13 @@ def test_paginate_is_a_permutation_of_the_suffix_rows():
         for t in range(pb.S_cap):
             assert np.array_equal(pc.k_pool[pc.block_table[b, t // 8], t % 8], pb.sk[b, t], equal_nan=False) \
                 or np.isnan(synth.bf16_bits_to_f32(pb.sk[b, t])).all()
+
+
+def test_paged_tree_equals_contiguous_tree():
+    parent, node_len, leaf = synth.two_level_tree(20, 2, 9, 2)
+    tp = synth.make_tree_problem(parent, node_len, leaf, 4, 2, 16, 24, lens=[24, 0, 7, 16], dtype="bf16",
+                                 dist="mixed", seed=4)
+    pc = synth.paginate(tp, 8, seed=6, map_tail=False)
+    o_ref, l_ref = oracle.tree_attention(tp)
+    o, l = oracle.tree_attention_paged(tp, pc)
+    assert np.array_equal(o, o_ref) and np.array_equal(l, l_ref)
