@@ -80,6 +80,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--paged-page-size", type=int, default=16,
+                    help="also time the step with the suffix in a paged cache of this page size (0 = skip)")
     return ap.parse_args()
 
 
@@ -143,7 +145,7 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self, busy_floor=0.0):
-        sm, mx, reasons = [], None, set()
+        sm, pw, mx, reasons = [], [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -154,11 +156,15 @@ class ClockSampler:
                 mx = float(parts[1])
             except ValueError:
                 continue
+            try:
+                pw.append(float(parts[2]))
+            except ValueError:
+                pass
             for n, v in zip(names, parts[3:7]):
                 if v.lower() == "active":
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w": statistics.median(pw) if pw else None}
 
 
 L2_BYTES = 126 * 1024 * 1024  # B200 L2
@@ -529,6 +535,28 @@ def main():
         flat = {"prefix_1k_queries_per_s": round(q1, 1), "prefix_%d_queries_per_s" % P: round(q16, 1),
                 "drop": round(1.0 - q16 / q1, 4), "target_drop": 0.15, "ms_prefix_1k": round(ms1, 5)}
 
+    # The same step with the suffixes in a paged cache (hydra_attn_paged, R14): the
+    # contiguous caches scattered into a shuffled page pool, the same schedule as g_main.
+    paged = None
+    if args.paged_page_size > 0 and S % args.paged_page_size == 0:
+        ps = args.paged_page_size
+        npg = S // ps
+        perm = torch.from_numpy(np.random.default_rng(args.seed + 7).permutation(B * npg).astype(np.int64)).to(dev)
+        kp = torch.empty(B * npg, ps, Hkv_r, d, dtype=torch.bfloat16, device=dev)
+        vp = torch.empty_like(kp)
+        kp[perm] = sk.view(B * npg, ps, Hkv_r, d)
+        vp[perm] = sv.view(B * npg, ps, Hkv_r, d)
+        tab = perm.view(B, npg).to(torch.int32)
+        del perm
+        g_pg = capture(lambda: hydra.hydragen_attention_paged(q, pk, pv, kp, vp, tab, lens, out=out, workspace=ws,
+                                                              aux_stream=aux if overlap else None))
+        ms_pg = time_graph(g_pg, args.steps, args.warmup)
+        paged = {"page_size": ps, "pages": B * npg, "layout": "shuffled page pool, block table [B, %d]" % npg,
+                 "queries_per_s": round(B / (ms_pg * 1e-3), 1), "ms_per_step": round(ms_pg, 5),
+                 "vs_contiguous": round(ms / ms_pg, 4)}
+        del g_pg, kp, vp, tab
+        torch.cuda.empty_cache()
+
     # per-kernel timing on their own (roofline of the dominant kernel and the prefix phase)
     # (the composite's workspace holds (prefix + suffix) split partials, enough for either alone)
     kk = max(5, args.steps // 4)
@@ -616,6 +644,13 @@ def main():
     }
     if flat:
         line["flatness"] = flat
+    if paged:
+        line["paged_suffix"] = paged
+    if clocks.get("power_w"):
+        # board power (nvidia-smi power.draw, median over the timed region) x step time
+        j = clocks["power_w"] * ms * 1e-3
+        line["energy"] = {"board_power_w": clocks["power_w"], "joules_per_step": round(j, 5),
+                          "queries_per_joule": round(B / j, 1), "samples": clocks["samples"]}
     if in_step:
         # the overlapped step's dominant kernel: the tensor-core suffix on (SMs - k) SMs
         b_k = suffix_bytes / (in_step["ms_suffix"] * 1e-3) / 1e9

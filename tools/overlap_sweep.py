@@ -19,6 +19,17 @@ lens = torch.full((B,), S, dtype=torch.int32, device=dev)
 ws = torch.empty(hydra.attn_workspace_bytes(q, P, S, H) * 2, dtype=torch.uint8, device=dev)
 out = torch.empty(B, H, 128, dtype=torch.bfloat16, device=dev)
 aux = torch.cuda.Stream(priority=-1)
+PAGED = int(os.environ.get("PAGED", 0))  # page size: the suffix in a shuffled page pool
+if PAGED:
+    perm = torch.randperm(B * (S // PAGED), device=dev, generator=g)
+    kp = torch.empty(B * (S // PAGED), PAGED, H, 128, dtype=torch.bfloat16, device=dev); vp = torch.empty_like(kp)
+    kp[perm] = sk.view(-1, PAGED, H, 128); vp[perm] = sv.view(-1, PAGED, H, 128)
+    tab = perm.view(B, -1).to(torch.int32)
+    suffix_call = lambda: hydra.suffix_attn_paged(q, kp, vp, tab, lens, workspace=ws)
+    attn_call = lambda **kw: hydra.hydragen_attention_paged(q, pk, pv, kp, vp, tab, lens, out=out, workspace=ws, **kw)
+else:
+    suffix_call = lambda: hydra.suffix_attn(q, sk, sv, lens, workspace=ws)
+    attn_call = lambda **kw: hydra.hydragen_attention(q, pk, pv, sk, sv, lens, out=out, workspace=ws, **kw)
 hydra.set_config("prefix_variant", variant)
 def graph(fn):
     s = torch.cuda.Stream(); s.wait_stream(torch.cuda.current_stream())
@@ -40,15 +51,15 @@ for k in ks:
     tp = t(graph(lambda: hydra.prefix_attn(q, pk, pv, workspace=ws)))
     hydra.set_config("prefix_ctas", 0)
     hydra.set_config("suffix_impl", 2); hydra.set_config("suffix_ctas", 148 - k)
-    ts = t(graph(lambda: hydra.suffix_attn(q, sk, sv, lens, workspace=ws)))
+    ts = t(graph(suffix_call))
     hydra.set_config("suffix_impl", 0); hydra.set_config("suffix_ctas", 0)
     hydra.set_config("overlap_prefix_ctas", k)
-    to = t(graph(lambda: hydra.hydragen_attention(q, pk, pv, sk, sv, lens, out=out, workspace=ws, aux_stream=aux)))
+    to = t(graph(lambda: attn_call(aux_stream=aux)))
     hydra.set_config("overlap_prefix_ctas", 0)
     print(json.dumps(dict(k=k, variant=variant, prefix_alone=tp, suffix_alone=ts, overlap=to)), flush=True)
 hydra.set_config("overlap_prefix_ctas", 0)
-ts = t(graph(lambda: hydra.hydragen_attention(q, pk, pv, sk, sv, lens, out=out, workspace=ws)))
+ts = t(graph(lambda: attn_call()))
 print(json.dumps(dict(what="sequential", ms=ts)))
-to = t(graph(lambda: hydra.hydragen_attention(q, pk, pv, sk, sv, lens, out=out, workspace=ws, aux_stream=aux)))
+to = t(graph(lambda: attn_call(aux_stream=aux)))
 print(json.dumps(dict(what="auto", k=hydra.get_config("last_overlap_k"), ms=to)))
 hydra.set_config("prefix_variant", 6)
