@@ -218,3 +218,37 @@ def test_tree_paged_parity(aux):
     torch.cuda.synchronize()
     assert torch.equal(out, out2) and torch.equal(lse, lse2)
     tree.destroy()
+
+
+@pytest.mark.parametrize("impl", [1, 2])
+@pytest.mark.parametrize("edge", ["one_seq", "all_empty", "page_gt_cap", "ragged_cap", "wide_table", "shared_pages"])
+def test_suffix_paged_edges(impl, edge):
+    """Degenerate paged layouts: a single sequence, every suffix empty, one page larger than the
+    whole capacity, S_cap not a multiple of the page size, a block table wider than needed, and
+    two sequences mapping the same physical pages (prefix-sharing caches do this)."""
+    B, Hq, Hkv, d, S, ps = 4, 8, 2, 128, 150, 16
+    lens = [150, 3, 77, 128]
+    if edge == "one_seq":
+        B, lens = 1, [150]
+    elif edge == "all_empty":
+        lens = [0, 0, 0, 0]
+    elif edge == "page_gt_cap":
+        ps = 256
+    elif edge == "ragged_cap":
+        S, lens = 150, [150, 149, 1, 145]
+    pb = synth.make_problem(B, Hq, Hkv, d, 0, S, lens=lens, dtype="bf16", dist="mixed", seed=5)
+    pc = synth.paginate(pb, ps, seed=3)
+    table = pc.block_table
+    if edge == "wide_table":
+        table = np.concatenate([table, np.full((B, 5), 2**30, np.int32)], axis=1)
+    if edge == "shared_pages":  # sequence 1 reads sequence 0's pages (and therefore its rows)
+        table = table.copy()
+        table[1] = table[0]
+    t = problem_to(pb, DEV)
+    kp, vp, _ = paged_to(pc, "bf16")
+    tab = torch.from_numpy(np.ascontiguousarray(table)).to(DEV)
+    hydra.set_config("suffix_impl", impl)
+    o, l = hydra.suffix_attn_paged(t["q"], kp, vp, tab, t["lens"], S_cap=S)
+    torch.cuda.synchronize()
+    ref, lref = oracle.suffix_only_paged(pb.q, pc.k_pool, pc.v_pool, table, ps, pb.lens, Hkv, pb.scale)
+    assert_parity(o, ref, l, lref, what=f"paged edge {edge} impl={impl}")
