@@ -134,10 +134,30 @@ static int heads_per_cta(int g) {
 // On the full chip the SIMT kernel streams slightly faster (7.2 vs 7.0 TB/s at C3), so
 // `auto` uses the tensor-core kernel only for the SM-partitioned (overlapped) schedule,
 // where its low instruction count per byte lets a subset of SMs carry the suffix.
+// With GQA (g >= 2) the tensor-core kernel is also the faster one on the full chip: it reads
+// each K/V row once for all g heads of the group (N = 16 MMA), where the SIMT kernel holds g
+// query heads and accumulators in registers (2 CTAs/SM at g = 8).  Measured on B200
+// (tools/suffix_shapes.py, L2 flushed): g = 8, B = 256, S = 128: 28 vs 66-117 us; g = 4,
+// B = 512: 67 vs 96 us; g = 16: 108 vs 357-410 us; MHA (g = 1): 0.83 vs 0.79 ms at C3.
 static bool use_suffix_tc(const hydra_heads *h, int64_t B, int64_t S_cap, bool overlap = false) {
   if (g_suffix_impl == 1 || S_cap <= 0 || !suffix_tc_supported(h)) return false;
   if (g_suffix_impl == 2) return true;
-  return overlap && B * h->num_kv_heads >= 2 * (int64_t)device_sm_count();
+  const int64_t items = B * h->num_kv_heads, sms = device_sm_count();
+  if (overlap) return items >= 2 * sms;
+  return h->num_q_heads / h->num_kv_heads >= 2 && items >= sms;
+}
+
+// Tensor-core suffix time model (us) on n SMs: HBM streaming at R_S bytes/us per SM (capped
+// by BW), or the per-item floor -- pipeline fill plus a per-item cost that grows with the
+// tiles and the heads of an item (tools/suffix_shapes.py: g = 8 one-tile items ~2.5 us at
+// 7 items per CTA; the floor stays below the streaming term for C3's MHA two-tile items, so
+// C3's split is the streaming model's).
+static double suffix_tc_us(const hydra_heads *h, int64_t B, int64_t S_cap, int n, double R_S, double BW) {
+  const int g = h->num_q_heads / h->num_kv_heads;
+  const int64_t items = B * h->num_kv_heads;
+  const double bytes = (double)items * S_cap * h->head_dim * 4.0;
+  const double per_item = 0.45 * (double)((S_cap + 127) / 128) + 0.25 * g;
+  return std::max(bytes / std::min(n * R_S, BW), 10.0 + (double)((items + n - 1) / n) * per_item);
 }
 
 // KV splits of the suffix kernel: enough CTAs to keep every SM streaming
@@ -241,17 +261,24 @@ static int overlap_prefix_ctas(const hydra_heads *h, int64_t B, int64_t P, int64
   const double R_P = 0.38, R_S = 1.0e5, BW = 7.0e6;
   const int64_t pairs = (B * g + 255) / 256;
   const double pair_blocks = (double)pairs * h->num_kv_heads * ((P + 127) / 128);
-  const double kv_bytes = (double)B * h->num_kv_heads * S_cap * h->head_dim * 4.0;
   int best_k = 0;
   double best = 1e300;
   for (int k = 8; k <= sms - 8; ++k) {
     if (prefix_kind(h, B * g, P, k) != PK_TC2) break;  // too few blocks per CTA beyond this k
     if (prefix_tc2_ctas(B, g, h->num_kv_heads, P, k, prefix_bn()) != k) continue;  // plan would idle SMs
-    const double t = std::max(pair_blocks / (k * R_P), kv_bytes / std::min((sms - k) * R_S, BW));
+    const double t = std::max(pair_blocks / (k * R_P), suffix_tc_us(h, B, S_cap, sms - k, R_S, BW));
     if (t < best) {
       best = t;
       best_k = k;
     }
+  }
+  // GQA: the sequential schedule runs the tensor-core suffix on every SM, which the split
+  // starves of SMs when the suffix is short (C6: 146 us on 12 SMs against 29 us on 148).
+  // Overlap only when the model says it is clearly (> 10 %) faster than prefix-then-suffix.
+  // (MHA keeps the split: there the measured overlap wins at every shard size.)
+  if (use_suffix_tc(h, B, S_cap, false)) {
+    const double t_seq = pair_blocks / (sms * R_P) + suffix_tc_us(h, B, S_cap, sms, R_S, BW);
+    if (best * 1.1 >= t_seq) return 0;
   }
   return best_k;
 }
