@@ -62,9 +62,9 @@ CONFIGS = {
 # DRAM bytes (read + write) per launch from one `ncu --set full` capture of the kernel at this
 # config (profiles/r1b_ncu_full_*.csv: dram__bytes_read.sum + dram__bytes_write.sum)
 NCU_TRAFFIC = {
-    ("c3_16k", "decode_attn_kernel"): 5379256000 + 9611264,
-    ("c3_16k", "suffix_tc_kernel"): 5379763000 + 25173504,   # profiles/r1j_suffix_tc_76_raw.csv (76 CTAs, k = 72)
-    ("c3_16k", "prefix_tc2_kernel"): 355116288 + 23960320,   # profiles/r1j_prefix_tc2_raw.csv (variant 6, poly 4)
+    ("c3_16k", "decode_attn_kernel"): 5379352000 + 8595712,   # profiles/r1l_suffix_decode_raw.csv
+    ("c3_16k", "suffix_tc_kernel"): 5379254000 + 24337664,   # profiles/r1l_suffix_tc_76_raw.csv (76 CTAs, k = 72)
+    ("c3_16k", "prefix_tc2_kernel"): 355146496 + 22375168,   # profiles/r1l_prefix_tc2_raw.csv (variant 6, poly 4)
 }
 
 
@@ -618,9 +618,11 @@ def main():
                    "l2": (f"no flush: {in_bytes / 1e9:.2f} GB of inputs per step > 2 x 126 MB L2" if flush is None else
                           f"L2 flushed (256 MB write) before every timed step: {in_bytes / 1e9:.3f} GB of inputs per rank"),
                    "timing": "CUDA graph of one step, CUDA events over K replays, max over ranks"},
-        "roofline": {"bound": "hbm", "kernel": "suffix split-K GEMV (decode_attn_kernel, all SMs; the sequential schedule's dominant kernel)",
+        "roofline": {"bound": "hbm", "kernel": ("suffix_tc_kernel (tensor-core GEMV, all SMs; GQA g = %d; the sequential schedule's suffix)" % (Hq // Hkv)
+                                                if Hq // Hkv >= 2 else
+                                                "suffix split-K GEMV (decode_attn_kernel, all SMs; the sequential schedule's dominant kernel)"),
                      "achieved": round(suf_gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(suf_gbs / hbm, 4),
-                     "traffic": NCU_TRAFFIC.get((args.config, "decode_attn_kernel")),
+                     "traffic": NCU_TRAFFIC.get((args.config, "suffix_tc_kernel" if Hq // Hkv >= 2 else "decode_attn_kernel")),
                      "algorithmic_bytes_per_launch": suffix_bytes,
                      "launch_ms": round(ms_suf, 5), "peak_source": peak_src + " (STREAM copy)",
                      "frac_of_nominal_7700": round(suf_gbs / 7700.0, 4),

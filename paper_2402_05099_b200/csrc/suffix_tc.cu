@@ -9,7 +9,7 @@
 //   S^T [128 tokens x 16] = K_tile [128 x 128] . Q^T        (tcgen05.mma, M=128, N=16)
 //   O^T [128 dims x 16]  += V_tile^T [128 x 128 tokens] . P^T (tcgen05.mma, A MN-major)
 // N = 16 holds the g = Hq/Hkv query heads of the KV group (zero-padded), so GQA reuses
-// every K/V byte g times.  One CTA per SM (persistent, 416 threads), one warp per job so
+// every K/V byte g times.  One CTA per SM (persistent, 448 threads), one warp per job so
 // that no stage ever waits behind another kind of slot:
 //   warp 0      TMA producer, K ring (3 x 32 KB; a slot frees once its score MMA is done)
 //   warp 6      TMA producer, V ring (3 x 32 KB; a slot frees once its PV MMA is done)
@@ -17,6 +17,7 @@
 //   warp 1      TMEM allocator + score-MMA issuer: S^T(n) as soon as K(n) lands and the
 //               softmax has consumed S^T slot n % 3
 //   warp 12     PV-MMA issuer: O^T += V^T P^T as soon as P^T(n) and V(n) are ready
+//   warp 13     paged cache only: block-table entries of upcoming tiles -> smem ring (cp.async)
 //   warps 2-5   softmax (thread = token lane): per round of CB blocks a block max per head
 //               (warp shuffles + smem across the 4 warps), the stale-max rule of the prefix
 //               kernel (rescale only when the max grows by > 8, log2 units), P^T as bf16
