@@ -286,7 +286,8 @@ HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, i
  *   "prefix_splits"       KV splits of the one-tile / SIMT prefix kernels
  *   "prefix_ctas"         CTAs of the persistent prefix kernel
  *   "suffix_impl"         1 SIMT split-K GEMV, 2 persistent TMA-fed tensor-core kernel
- *   "suffix_splits"       KV splits of the SIMT suffix kernel
+ *   "suffix_splits"       KV splits of the suffix kernels (tensor-core kernel: split-K over
+ *                         tokens, only when set; SIMT kernel: automatic when 0)
  *   "suffix_ctas"         CTAs of the persistent suffix kernel
  *   "suffix_unroll"       tokens in flight per row group of the SIMT suffix kernel (4 or 8)
  *   "overlap_prefix_ctas" SM split of hydra_attn with an aux stream (prefix CTAs)

@@ -163,7 +163,15 @@ static double suffix_tc_us(const hydra_heads *h, int64_t B, int64_t S_cap, int n
 // KV splits of the suffix kernel: enough CTAs to keep every SM streaming
 // (~16 resident 128-thread CTAs per SM), never fewer than 32 tokens per split.
 static int suffix_splits(const hydra_heads *h, int64_t B, int64_t S_cap, bool overlap = false) {
-  if (use_suffix_tc(h, B, S_cap, overlap)) return 1;
+  if (use_suffix_tc(h, B, S_cap, overlap)) {
+    // Tensor-core kernel: split-K over tokens only on request (config key suffix_splits).
+    // Measured (tools/suffix_shapes.py): an automatic split that fills the last wave (512
+    // items on 148 SMs, 2048-token suffixes -> 2 splits) was 11 % slower (114 vs 103 us;
+    // 64 x 8 heads x 1024 tokens: 68 vs 60 us) -- the kernel streams ~40 GB/s per SM there,
+    // so the extra items' fill / epilogue and the partial combine cost more than the tail.
+    if (overlap || g_suffix_splits <= 0) return 1;
+    return (int)std::min<int64_t>(g_suffix_splits, std::max<int64_t>(1, (S_cap + 127) / 128));
+  }
   if (g_suffix_splits > 0) return (int)std::min<int64_t>(g_suffix_splits, std::max<int64_t>(1, S_cap));
   if (S_cap <= 0) return 1;
   const int g = h->num_q_heads / h->num_kv_heads;
@@ -399,6 +407,10 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
     a.cb = (int32_t)g_suffix_cb;
     a.trace = reinterpret_cast<void *>((intptr_t)g_suffix_trace.load());
     a.debug = (int32_t)g_tc_debug;
+    a.n_split = splits;
+    a.split_len = (int32_t)(((S_cap + splits - 1) / splits + 127) / 128 * 128);
+    a.o_split_stride = dst.o_stride;
+    a.lse_split_stride = dst.lse_stride;
     if (pg) {
       a.block_table = pg->block_table;
       a.bt_stride = pg->bt_stride;

@@ -116,6 +116,11 @@ struct SuffixTcArgs {
   const int32_t *block_table;
   int64_t bt_stride, n_pages;
   int32_t page_size;
+  // split-K over tokens (0 / 1 = none): split sp of a sequence covers tokens
+  // [sp * split_len, (sp + 1) * split_len) (split_len a multiple of 128) and writes its
+  // (O, LSE) partial at o + sp * o_split_stride, lse + sp * lse_split_stride
+  int32_t n_split, split_len;
+  int64_t o_split_stride, lse_split_stride;
 };
 bool suffix_tc_supported(const hydra_heads *h);
 hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s);

@@ -100,6 +100,10 @@ struct __align__(64) SuffixTcParams {
   const int32_t *block_table;
   int64_t bt_stride;
   int32_t page_shift, pbox_shift;  // log2(page_size), log2(pbox)
+  // split-K over tokens: item = (b * Hkv + j) * n_split + sp covers tokens
+  // [sp * split_len, (sp + 1) * split_len) of sequence b; its (O, LSE) go to slot sp
+  int32_t n_split, split_len;
+  int64_t o_split_stride, lse_split_stride;
 };
 namespace stc {
 constexpr int kTraceN = 1024;
@@ -119,7 +123,18 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 // lens[b] of the item this CTA handles `k` steps ahead (0 when past the end): every role
 // fetches the next item's length one item early so the load is off the critical path.
 __device__ __forceinline__ int item_len(const SuffixTcParams &P, int item) {
-  return item < P.n_items ? __ldg(P.lens + item / P.Hkv) : 0;
+  if (item >= P.n_items) return 0;
+  const int bj = item / P.n_split, sp = item - bj * P.n_split;
+  return max(0, min(P.split_len, __ldg(P.lens + bj / P.Hkv) - sp * P.split_len));
+}
+// (sequence, KV head, first token, output offset in elements of o / lse) of an item
+struct ItemRef {
+  int b, j, t_base;
+  int64_t o_off, lse_off;
+};
+__device__ __forceinline__ ItemRef item_ref(const SuffixTcParams &P, int item) {
+  const int bj = item / P.n_split, sp = item - bj * P.n_split;
+  return {bj / P.Hkv, bj % P.Hkv, sp * P.split_len, sp * P.o_split_stride, sp * P.lse_split_stride};
 }
 
 // Paged cache: one lane of warp 13 walks the CTA's tile sequence (the one the K / V
@@ -134,12 +149,13 @@ __device__ __forceinline__ void page_table_lane(const SuffixTcParams &P, int32_t
   for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
     const int len = item_len(P, item);
     const int nblk = (len + stc::BT - 1) / stc::BT;
-    const int32_t *bt = P.block_table + (int64_t)(item / P.Hkv) * P.bt_stride;
+    const ItemRef ir = item_ref(P, item);
+    const int32_t *bt = P.block_table + (int64_t)ir.b * P.bt_stride;
     for (int n = 0; n < nblk; ++n, ++k) {
       const int slot = k % stc::PR;
       ptx::mbar_wait(&tab_empty[slot], ((k / stc::PR) & 1) ^ 1);
-      const int t0 = n * stc::BT;
-      const int nsub = min(stc::BT >> P.pbox_shift, (len - t0 + (1 << P.pbox_shift) - 1) >> P.pbox_shift);
+      const int t0 = ir.t_base + n * stc::BT;
+      const int nsub = min(stc::BT >> P.pbox_shift, (ir.t_base + len - t0 + (1 << P.pbox_shift) - 1) >> P.pbox_shift);
       const uint32_t dst = ptx::smem_u32(ring + slot * 16);
       for (int c = 0; c < nsub; ++c)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + 4 * c),
@@ -275,7 +291,8 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
       uint32_t gb = 0, qi = 0;
       int len_next = item_len(P, blockIdx.x);
       for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
-        const int b = item / P.Hkv, j = item % P.Hkv;
+        const ItemRef ir = item_ref(P, item);
+        const int b = ir.b, j = ir.j;
         const int len = len_next;
         len_next = item_len(P, item + gridDim.x);
         const int nblk = (len + BT - 1) / BT;
@@ -293,7 +310,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
         for (int n = 0; n < nblk; ++n, ++gb) {
           const int st = gb % NS;
           const uint32_t ph = ((gb / NS) & 1) ^ 1;
-          const int t0 = n * BT;
+          const int t0 = ir.t_base + n * BT;  // first token of the tile in the sequence
           const CUtensorMap *tm = warp == 0 ? &P.tmK : &P.tmV;
           uint64_t *full = warp == 0 ? &k_full[st] : &v_full[st];
           uint8_t *dst = smem + (warp == 0 ? OFF_K : OFF_V) + st * TILE;
@@ -310,7 +327,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
             // >= 1024 B, so the 128-B swizzle pattern equals that of one whole-tile load.
             const int ts = gb % PR;
             ptx::mbar_wait(&tab_full[ts], (gb / PR) & 1);  // this tile's page ids have landed
-            const int nsub = min(BT >> P.pbox_shift, (len - t0 + (1 << P.pbox_shift) - 1) >> P.pbox_shift);
+            const int nsub = min(BT >> P.pbox_shift, (ir.t_base + len - t0 + (1 << P.pbox_shift) - 1) >> P.pbox_shift);
             ptx::mbar_wait(warp == 0 ? &k_empty[st] : &v_empty[st], ph);
             ptx::mbar_arrive_expect_tx(full, (uint32_t)nsub * (256u << P.pbox_shift));
 #pragma unroll 8
@@ -448,15 +465,15 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
     long long *tr = (blockIdx.x == 0 && quarter == 0 && lane == 0) ? P.trace : nullptr;
     int len_next = item_len(P, blockIdx.x);
     for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
-      const int b = item / P.Hkv, j = item % P.Hkv;
+      const ItemRef ir = item_ref(P, item);
       const int len = len_next;
       len_next = item_len(P, item + gridDim.x);
       const int nblk = (len + BT - 1) / BT;
-      const int64_t row0 = (int64_t)b * P.Hq + (int64_t)j * g;
-      if (nblk == 0) {  // empty suffix: (0, -inf) sentinel
+      const int64_t row0 = (int64_t)ir.b * P.Hq + (int64_t)ir.j * g;
+      if (nblk == 0) {  // empty suffix (or split): (0, -inf) sentinel
         for (int h = 0; h < g; ++h) {
-          P.o[(row0 + h) * HD + r] = 0.f;
-          if (r == 0) P.lse[row0 + h] = -INFINITY;
+          P.o[ir.o_off + (row0 + h) * HD + r] = 0.f;
+          if (r == 0) P.lse[ir.lse_off + row0 + h] = -INFINITY;
         }
         continue;
       }
@@ -587,8 +604,8 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
       const int len = len_next;
       len_next = item_len(P, item + gridDim.x);
       if (len <= 0) continue;
-      const int b = item / P.Hkv, j = item % P.Hkv;
-      const int64_t row0 = (int64_t)b * P.Hq + (int64_t)j * g;
+      const ItemRef ir = item_ref(P, item);
+      const int64_t row0 = (int64_t)ir.b * P.Hq + (int64_t)ir.j * g;
       const uint32_t ob = item_no & 1, ph = (item_no >> 1) & 1;
       ptx::mbar_wait(&o_full[ob], ph);
       ptx::mbar_wait(&ml_full[ob], ph);
@@ -607,8 +624,8 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
       ptx::warp_arrive(&o_free[ob]);  // O^T buffer and (m, l) slot free
 #pragma unroll
       for (int h = 0; h < G; ++h) {
-        P.o[(row0 + h) * HD + r] = __uint_as_float(ov[h]) / L[h];
-        if (r == h) P.lse[row0 + h] = (M[h] + log2f(L[h])) * HYDRA_LN2;
+        P.o[ir.o_off + (row0 + h) * HD + r] = __uint_as_float(ov[h]) / L[h];
+        if (r == h) P.lse[ir.lse_off + row0 + h] = (M[h] + log2f(L[h])) * HYDRA_LN2;
       }
       ++item_no;
     }
@@ -702,7 +719,11 @@ hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s)
   P.Hkv = a.Hkv;
   P.g = g;
   P.scale_log2 = a.scale_log2;
-  P.n_items = a.B * a.Hkv;
+  P.n_split = a.n_split > 0 ? a.n_split : 1;
+  P.split_len = P.n_split > 1 ? a.split_len : (int32_t)std::min<int64_t>(a.S_cap, INT32_MAX);
+  P.o_split_stride = a.o_split_stride;
+  P.lse_split_stride = a.lse_split_stride;
+  P.n_items = a.B * a.Hkv * P.n_split;
   P.o = a.o;
   P.lse = a.lse;
   P.trace = reinterpret_cast<long long *>(a.trace);

@@ -419,3 +419,45 @@ def test_tree_large_groups(impl, per, g):
     ref, lref = oracle.tree_attention(tp)
     assert_parity(out, ref, lse, lref, what=f"tree large groups impl={impl} per={per} g={g}")
     tree.destroy()
+
+
+@pytest.mark.parametrize("splits", [2, 3, 5])
+@pytest.mark.parametrize("g", [1, 4, 8])
+def test_suffix_tc_split_k(splits, g):
+    """Tensor-core suffix with split-K over tokens (512-token-or-longer suffixes on few items):
+    ragged lengths that end inside, at, and before split boundaries, empty splits, empty
+    sequences; partials combined by the library."""
+    hydra.set_config("suffix_impl", 2)
+    hydra.set_config("suffix_splits", splits)
+    try:
+        B, Hkv, S = 6, 2, 700
+        lens = [700, 0, 1, 128, 256 + 5, 511]
+        pb = synth.make_problem(B, Hkv * g, Hkv, 128, 0, S, lens=lens, dtype="bf16", dist="mixed", seed=40 + g)
+        t = problem_to(pb, DEV)
+        o, l = hydra.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
+        torch.cuda.synchronize()
+        ref, lref = oracle.suffix_only(pb)
+        assert_parity(o, ref, l, lref, what=f"suffix_tc split-K s={splits} g={g}")
+    finally:
+        hydra.set_config("suffix_splits", 0)
+        hydra.set_config("suffix_impl", 0)
+
+
+def test_suffix_gqa_long_suffix_auto():
+    """Auto policy: GQA, 512 items on 148 SMs, 2048-token suffixes -> the tensor-core kernel on
+    the full chip; sampled rows vs the oracle, and the paged call gives the same bits."""
+    B, Hq, Hkv, S = 128, 32, 4, 2048
+    rng = np.random.default_rng(3)
+    lens = rng.integers(1500, S + 1, B).astype(np.int32)
+    pb = synth.make_problem(B, Hq, Hkv, 128, 0, S, lens=lens, dtype="bf16", dist="mixed", seed=77)
+    t = problem_to(pb, DEV)
+    o, l = hydra.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
+    torch.cuda.synchronize()
+    rows = np.array([(b, h) for b in (0, 1, 63, 127) for h in (0, 7, 8, 31)])
+    ref, lref = oracle.suffix_only(pb, rows=rows)
+    assert_parity(o[rows[:, 0], rows[:, 1]], ref, l[rows[:, 0], rows[:, 1]], lref, what="auto split long suffix")
+    pc = synth.paginate(pb, 64, seed=2)
+    kp, vp = (torch.from_numpy(x).view(torch.bfloat16).to(DEV) for x in (pc.k_pool, pc.v_pool))
+    o2, l2 = hydra.suffix_attn_paged(t["q"], kp, vp, torch.from_numpy(pc.block_table).to(DEV), t["lens"], S_cap=S)
+    torch.cuda.synchronize()
+    assert torch.equal(o, o2) and torch.equal(l, l2)

@@ -5,7 +5,7 @@ import paper_2402_05099_b200 as hydra
 sys.path.insert(0, "/root/repo/tools")
 dev = torch.device("cuda:0")
 g = torch.Generator(device=dev); g.manual_seed(0)
-for (B, Hq, Hkv, S) in [(512, 32, 16, 256), (1024, 16, 8, 256), (256, 32, 4, 128), (512, 32, 8, 128)]:
+for (B, Hq, Hkv, S) in [(128, 32, 4, 2048), (64, 32, 8, 1024), (256, 64, 8, 512), (256, 32, 4, 128)]:
     q = torch.randn(B, Hq, 128, device=dev, generator=g).bfloat16()
     sk = torch.randn(B, S, Hkv, 128, device=dev, generator=g).bfloat16()
     sv = torch.randn(B, S, Hkv, 128, device=dev, generator=g).bfloat16()
