@@ -144,7 +144,9 @@ static bool use_suffix_tc(const hydra_heads *h, int64_t B, int64_t S_cap, bool o
   if (g_suffix_impl == 2) return true;
   const int64_t items = B * h->num_kv_heads, sms = device_sm_count();
   if (overlap) return items >= 2 * sms;
-  return h->num_q_heads / h->num_kv_heads >= 2 && items >= sms;
+  // (also with fewer items than SMs: 64-128 items of 1-8K-token suffixes, 62-64 us against
+  // 106-210 us for the SIMT kernel's best split)
+  return h->num_q_heads / h->num_kv_heads >= 2;
 }
 
 // Tensor-core suffix time model (us) on n SMs: HBM streaming at R_S bytes/us per SM (capped
@@ -169,8 +171,14 @@ static int suffix_splits(const hydra_heads *h, int64_t B, int64_t S_cap, bool ov
     // items on 148 SMs, 2048-token suffixes -> 2 splits) was 11 % slower (114 vs 103 us;
     // 64 x 8 heads x 1024 tokens: 68 vs 60 us) -- the kernel streams ~40 GB/s per SM there,
     // so the extra items' fill / epilogue and the partial combine cost more than the tail.
-    if (overlap || g_suffix_splits <= 0) return 1;
-    return (int)std::min<int64_t>(g_suffix_splits, std::max<int64_t>(1, (S_cap + 127) / 128));
+    if (overlap) return 1;
+    if (g_suffix_splits > 0) return (int)std::min<int64_t>(g_suffix_splits, std::max<int64_t>(1, (S_cap + 127) / 128));
+    // Very few items (< SMs / 4, e.g. 4 sequences x 8 KV heads): split into one wave of
+    // items x splits <= SMs (32 items x 16K tokens: 64.5 us with 4 splits, 74 with 5 = two
+    // waves, 91 unsplit); at 64+ items the split measured slower.
+    const int64_t items = B * h->num_kv_heads, sms = device_sm_count();
+    if (items * 4 >= sms) return 1;
+    return (int)std::max<int64_t>(1, std::min<int64_t>({sms / items, S_cap / 512, 16}));  // one wave
   }
   if (g_suffix_splits > 0) return (int)std::min<int64_t>(g_suffix_splits, std::max<int64_t>(1, S_cap));
   if (S_cap <= 0) return 1;

@@ -5,7 +5,7 @@ import paper_2402_05099_b200 as hydra
 sys.path.insert(0, "/root/repo/tools")
 dev = torch.device("cuda:0")
 g = torch.Generator(device=dev); g.manual_seed(0)
-for (B, Hq, Hkv, S) in [(128, 32, 4, 2048), (64, 32, 8, 1024), (256, 64, 8, 512), (256, 32, 4, 128)]:
+for (B, Hq, Hkv, S) in [(16, 32, 8, 4096), (8, 64, 8, 8192), (32, 32, 4, 2048), (4, 32, 8, 16384), (2, 32, 8, 32768), (256, 32, 4, 128), (1024, 40, 40, 256)]:
     q = torch.randn(B, Hq, 128, device=dev, generator=g).bfloat16()
     sk = torch.randn(B, S, Hkv, 128, device=dev, generator=g).bfloat16()
     sv = torch.randn(B, S, Hkv, 128, device=dev, generator=g).bfloat16()
@@ -23,7 +23,7 @@ for (B, Hq, Hkv, S) in [(128, 32, 4, 2048), (64, 32, 8, 1024), (256, 64, 8, 512)
         return tot / iters
     kvb = 2 * B * S * Hkv * 256
     res = {}
-    for impl, sp, ctas in [(1, 0, 0), (1, 1, 0), (1, 2, 0), (1, 4, 0), (2, 0, 148), (2, 0, 76)]:
+    for impl, sp, ctas in [(0, 0, 0), (1, 0, 0), (1, 1, 0), (1, 2, 0), (1, 4, 0), (2, 0, 148), (2, 0, 76), (2, 2, 148), (2, 4, 148), (2, 8, 148)]:
         hydra.set_config("suffix_impl", impl); hydra.set_config("suffix_splits", sp); hydra.set_config("suffix_ctas", ctas)
         ms = t(lambda: hydra.suffix_attn(q, sk, sv, lens, workspace=ws))
         res[f"impl{impl}_sp{sp}_c{ctas}"] = (round(ms * 1000, 1), round(kvb / ms / 1e6))
