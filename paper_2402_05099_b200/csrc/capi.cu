@@ -184,9 +184,12 @@ static int suffix_splits(const hydra_heads *h, int64_t B, int64_t S_cap, bool ov
   if (S_cap <= 0) return 1;
   const int g = h->num_q_heads / h->num_kv_heads;
   const int64_t items = B * h->num_kv_heads * (g / heads_per_cta(g));
-  const int64_t target = (int64_t)device_sm_count() * 16;
+  // ~6 resident 128-thread CTAs per SM and >= 256 tokens per split (tools/suffix_shapes.py:
+  // MHA 2-16 sequences x 32-40 heads x 0.5-16K tokens; 16 per SM and 32-token splits were
+  // 10-18 % slower through the extra partials and the combine)
+  const int64_t target = (int64_t)device_sm_count() * 6;
   int64_t s = (target + items - 1) / items;
-  s = std::min<int64_t>(s, std::max<int64_t>(1, S_cap / 32));
+  s = std::min<int64_t>(s, std::max<int64_t>(1, S_cap / 256));
   return (int)std::max<int64_t>(1, std::min<int64_t>(s, 64));
 }
 

@@ -5,7 +5,7 @@ import paper_2402_05099_b200 as hydra
 sys.path.insert(0, "/root/repo/tools")
 dev = torch.device("cuda:0")
 g = torch.Generator(device=dev); g.manual_seed(0)
-for (B, Hq, Hkv, S) in [(16, 32, 8, 4096), (8, 64, 8, 8192), (32, 32, 4, 2048), (4, 32, 8, 16384), (2, 32, 8, 32768), (256, 32, 4, 128), (1024, 40, 40, 256)]:
+for (B, Hq, Hkv, S) in [(8, 32, 32, 4096), (4, 40, 40, 8192), (64, 32, 32, 1024), (2, 32, 32, 16384), (16, 32, 32, 512), (256, 32, 32, 128), (1024, 40, 40, 256), (128, 40, 40, 128)]:
     q = torch.randn(B, Hq, 128, device=dev, generator=g).bfloat16()
     sk = torch.randn(B, S, Hkv, 128, device=dev, generator=g).bfloat16()
     sv = torch.randn(B, S, Hkv, 128, device=dev, generator=g).bfloat16()
