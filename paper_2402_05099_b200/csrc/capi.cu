@@ -206,8 +206,12 @@ static PrefixKind prefix_kind(const hydra_heads *h, int64_t rows = -1, int64_t P
   if (g_prefix_impl == 1 || !prefix_tc_supported(h)) return PK_SIMT;
   if (g_prefix_impl == 2) return PK_TC1;
   if (g_prefix_impl == 3 || rows < 0) return PK_TC2;
+  // Persistent kernel when each CTA owns enough 256-row x 128-token blocks to amortise its
+  // pipeline fill: 24 on an SM share (the overlap split needs the persistent kernel), 40 on
+  // the full chip (tools/prefix_shapes.py: C6 at 34 blocks per CTA, one-tile kernel 104 us vs
+  // 108 us; C4 at 110 blocks, persistent 266 vs 312 us).
   const int64_t blocks = ((rows + 255) / 256) * h->num_kv_heads * ((P + 127) / 128);
-  return blocks >= 24 * (int64_t)(ctas > 0 ? ctas : prefix_ctas()) ? PK_TC2 : PK_TC1;
+  return blocks >= (ctas > 0 ? 24 : 40) * (int64_t)(ctas > 0 ? ctas : prefix_ctas()) ? PK_TC2 : PK_TC1;
 }
 static bool use_tc(const hydra_heads *h) { return prefix_kind(h) != PK_SIMT; }
 
