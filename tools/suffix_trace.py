@@ -9,16 +9,17 @@ import paper_2402_05099_b200 as hydra
 cb = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 ctas = int(sys.argv[2]) if len(sys.argv) > 2 else 16
 B, H, S = int(os.environ.get("B", 1024)), int(os.environ.get("H", 40)), int(os.environ.get("S", 256))
+HKV = int(os.environ.get("HKV", H))  # KV heads (GQA when < H)
 dev = torch.device("cuda:0")
 g = torch.Generator(device=dev); g.manual_seed(0)
 q = torch.randn(B, H, 128, device=dev, generator=g).bfloat16()
-sk = torch.randn(B, S, H, 128, device=dev, generator=g).bfloat16()
-sv = torch.randn(B, S, H, 128, device=dev, generator=g).bfloat16()
+sk = torch.randn(B, S, HKV, 128, device=dev, generator=g).bfloat16()
+sv = torch.randn(B, S, HKV, 128, device=dev, generator=g).bfloat16()
 lens = torch.full((B,), S, dtype=torch.int32, device=dev)
 PAGED = int(os.environ.get("PAGED", 0))  # page size: the same caches through the paged path (identity table)
 if PAGED:
     tab = torch.arange(B * (S // PAGED), device=dev, dtype=torch.int32).view(B, S // PAGED)
-    kp, vp = sk.view(-1, PAGED, H, 128), sv.view(-1, PAGED, H, 128)
+    kp, vp = sk.view(-1, PAGED, HKV, 128), sv.view(-1, PAGED, HKV, 128)
     call = lambda: hydra.suffix_attn_paged(q, kp, vp, tab, lens)
 else:
     call = lambda: hydra.suffix_attn(q, sk, sv, lens)
@@ -35,7 +36,7 @@ e0.record(); call(); e1.record()
 torch.cuda.synchronize()
 hydra.set_config("suffix_trace", 0); hydra.set_config("tc_debug_variant", 0); hydra.set_config("suffix_impl", 0); hydra.set_config("suffix_ctas", 0); hydra.set_config("suffix_cb", 2)
 ms = e0.elapsed_time(e1)
-print(f"cb={cb} ctas={ctas} ms={ms:.3f} GB/s/SM={2*B*S*H*256/ms/1e6/ctas:.1f}")
+print(f"cb={cb} ctas={ctas} ms={ms:.3f} GB/s/SM={2*B*S*HKV*256/ms/1e6/ctas:.1f}")
 t = tr.cpu().numpy().astype(np.float64)
 names = ["sm_wait0", "s_full", "ld", "max", "p_arrive", "epi0", "epi1", "mma_S", "mma_PV", "tma_K", "tma_V"]
 lo, hi = 50, 400  # steady-state window (rounds / blocks)
@@ -66,3 +67,11 @@ if os.environ.get("RAW"):
     for rr in range(100, 116):
         b0 = rr * bpr
         print(f"{rr:4d}: " + " ".join(f"{x - base:8.0f}" for x in (t[9, b0], t[10, b0], t[11, b0], t[12, b0], t[7, rr], t[1, rr], t[4, rr], t[8, rr])))
+if os.environ.get("FIRST"):
+    n = int(os.environ["FIRST"])
+    base = t[9, 0]
+    print(f"first {n} rounds/blocks/items of CTA 0 (cycles rel. to the first K TMA):")
+    print("idx:  Ktma  Vtma Kseen Vseen Scommit sm_wait0 s_full ld  max  p_arrive PVcommit")
+    for i in range(n):
+        print(f"{i:3d}: " + " ".join(f"{x - base:6.0f}" for x in (t[9, i], t[10, i], t[11, i], t[12, i], t[7, i], t[0, i], t[1, i],
+                                                              t[2, i], t[3, i], t[4, i], t[8, i])))
