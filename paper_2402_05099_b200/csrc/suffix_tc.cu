@@ -108,7 +108,8 @@ struct __align__(64) SuffixTcParams {
 namespace stc {
 constexpr int kTraceN = 1024;
 // trace rows: 0 softmax s_full wait begin, 1 s_full acquired, 2 scores loaded, 3 block max done,
-// 4 P^T published (p_full arrive), 5 epilogue begin, 6 epilogue end, 7 MMA S round committed,
+// 4 P^T published (p_full arrive), 5 / 6 softmax item end before / after its o_free wait
+// (indexed by item), 7 MMA S round committed,
 // 8 MMA PV round committed, 9 K TMA issued (block), 10 V TMA issued (block), 11 / 12 MMA thread
 // sees K / V landed (block)
 __device__ __forceinline__ void trace(long long *tr, int row, uint32_t i) {
@@ -122,10 +123,21 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 
 // lens[b] of the item this CTA handles `k` steps ahead (0 when past the end): every role
 // fetches the next item's length one item early so the load is off the critical path.
+// The roles keep the raw lens[b] of their next item (item_len_raw, a bare load whose value is
+// first used one item later) and derive the item's token count at use (item_len_of): clamping
+// right after the load could make an item transition wait for it.  (The softmax warps still
+// spend ~1000 cycles between an item's end and the next item's first wait on one-tile GQA
+// items, tools/suffix_trace.py FIRST=7 -- not this load; unresolved.)
+__device__ __forceinline__ int item_len_raw(const SuffixTcParams &P, int item) {
+  return item < P.n_items ? __ldg(P.lens + (item / P.n_split) / P.Hkv) : 0;
+}
+__device__ __forceinline__ int item_len_of(const SuffixTcParams &P, int item, int raw) {
+  if (P.n_split == 1) return raw;
+  const int sp = item % P.n_split;
+  return max(0, min(P.split_len, raw - sp * P.split_len));
+}
 __device__ __forceinline__ int item_len(const SuffixTcParams &P, int item) {
-  if (item >= P.n_items) return 0;
-  const int bj = item / P.n_split, sp = item - bj * P.n_split;
-  return max(0, min(P.split_len, __ldg(P.lens + bj / P.Hkv) - sp * P.split_len));
+  return item_len_of(P, item, item_len_raw(P, item));
 }
 // (sequence, KV head, first token, output offset in elements of o / lse) of an item
 struct ItemRef {
@@ -178,8 +190,8 @@ struct RoundCursor {
   bool valid;
   __device__ __forceinline__ void seek(const SuffixTcParams &P) {  // first round of the next non-empty item
     while (item < P.n_items) {
-      len = len_next;
-      len_next = item_len(P, item + gridDim.x);
+      len = item_len_of(P, item, len_next);
+      len_next = item_len_raw(P, item + gridDim.x);
       nblk = (len + stc::BT - 1) / stc::BT;
       if (nblk > 0) {
         n0 = 0;
@@ -193,7 +205,7 @@ struct RoundCursor {
   }
   __device__ __forceinline__ void init(const SuffixTcParams &P) {
     item = blockIdx.x;
-    len_next = item_len(P, item);
+    len_next = item_len_raw(P, item);
     gb = gr = qi = item_no = 0;
     seek(P);
   }
@@ -289,12 +301,12 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
     if (ptx::elect_one()) {
       long long *tr = blockIdx.x == 0 ? P.trace : nullptr;
       uint32_t gb = 0, qi = 0;
-      int len_next = item_len(P, blockIdx.x);
+      int len_next = item_len_raw(P, blockIdx.x);
       for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
         const ItemRef ir = item_ref(P, item);
         const int b = ir.b, j = ir.j;
-        const int len = len_next;
-        len_next = item_len(P, item + gridDim.x);
+        const int len = item_len_of(P, item, len_next);
+        len_next = item_len_raw(P, item + gridDim.x);
         const int nblk = (len + BT - 1) / BT;
         if (nblk == 0) continue;
         if (warp == 7) {
@@ -463,11 +475,11 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
     const float c2 = P.scale_log2;
     uint32_t gr = 0, gb = 0, item_no = 0;
     long long *tr = (blockIdx.x == 0 && quarter == 0 && lane == 0) ? P.trace : nullptr;
-    int len_next = item_len(P, blockIdx.x);
+    int len_next = item_len_raw(P, blockIdx.x);
     for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
       const ItemRef ir = item_ref(P, item);
-      const int len = len_next;
-      len_next = item_len(P, item + gridDim.x);
+      const int len = item_len_of(P, item, len_next);
+      len_next = item_len_raw(P, item + gridDim.x);
       const int nblk = (len + BT - 1) / BT;
       const int64_t row0 = (int64_t)ir.b * P.Hq + (int64_t)ir.j * g;
       if (nblk == 0) {  // empty suffix (or split): (0, -inf) sentinel
@@ -580,7 +592,9 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
       }
       // hand (m, row-sum partials) to the epilogue warps; slot ob was last read by the
       // epilogue of item item_no - 2
+      trace(tr, 5, item_no);
       ptx::mbar_wait(&o_free[ob], ((item_no >> 1) & 1) ^ 1);
+      trace(tr, 6, item_no);
       float *rs = red_sum + ob * 4 * NQ;
 #pragma unroll
       for (int h = 0; h < G; ++h) {
@@ -599,10 +613,10 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
     const int r = quarter * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     uint32_t item_no = 0;
-    int len_next = item_len(P, blockIdx.x);
+    int len_next = item_len_raw(P, blockIdx.x);
     for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
-      const int len = len_next;
-      len_next = item_len(P, item + gridDim.x);
+      const int len = item_len_of(P, item, len_next);
+      len_next = item_len_raw(P, item + gridDim.x);
       if (len <= 0) continue;
       const ItemRef ir = item_ref(P, item);
       const int64_t row0 = (int64_t)ir.b * P.Hq + (int64_t)ir.j * g;

@@ -71,7 +71,7 @@ if os.environ.get("FIRST"):
     n = int(os.environ["FIRST"])
     base = t[9, 0]
     print(f"first {n} rounds/blocks/items of CTA 0 (cycles rel. to the first K TMA):")
-    print("idx:  Ktma  Vtma Kseen Vseen Scommit sm_wait0 s_full ld  max  p_arrive PVcommit")
+    print("idx:  Ktma  Vtma Kseen Vseen Scommit sm_wait0 s_full ld  max  p_arrive PVcommit ofree0 ofree1")
     for i in range(n):
         print(f"{i:3d}: " + " ".join(f"{x - base:6.0f}" for x in (t[9, i], t[10, i], t[11, i], t[12, i], t[7, i], t[0, i], t[1, i],
-                                                              t[2, i], t[3, i], t[4, i], t[8, i])))
+                                                              t[2, i], t[3, i], t[4, i], t[8, i], t[5, i], t[6, i])))
