@@ -127,7 +127,10 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 // first used one item later) and derive the item's token count at use (item_len_of): clamping
 // right after the load could make an item transition wait for it.  (The softmax warps still
 // spend ~1000 cycles between an item's end and the next item's first wait on one-tile GQA
-// items, tools/suffix_trace.py FIRST=7 -- not this load; unresolved.)
+// items, tools/suffix_trace.py FIRST=7 -- not this load.  ncu at that shape
+// (profiles/r1n_suffix_tc_c6shape_raw.csv): 3.05 warps stalled on no_instruction per issue,
+// next to 3.8 on barriers -- instruction-fetch misses: 5.1 K SASS instructions for G = 8,
+// every role's per-item path executed once per ~2 us.  Unresolved.)
 __device__ __forceinline__ int item_len_raw(const SuffixTcParams &P, int item) {
   return item < P.n_items ? __ldg(P.lens + (item / P.n_split) / P.Hkv) : 0;
 }
