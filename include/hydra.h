@@ -295,6 +295,10 @@ HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, i
  *   "tc_debug_variant"    timing experiments only (invalid results); never set in production
  *   "prefix_trace"        diagnostics: device pointer of a 14*1024 int64 buffer for CTA-0
  *                         timestamps of the persistent prefix kernel (tools/prefix_trace.py)
+ *   "ev_prefix_begin" / "ev_prefix_end" / "ev_suffix_begin" / "ev_suffix_end"
+ *                         measurement: a cudaEvent_t (as an integer) that hydra_attn records
+ *                         right before / after its prefix (on the prefix's stream) or suffix
+ *                         launches, also inside graph capture; 0 = off
  * hydra_get_config also answers "last_overlap_k": prefix CTAs of the last hydra_attn
  * overlap split (0 = the two phases ran sequentially).
  * Returns HYDRA_EINVAL for an unknown key.

@@ -43,6 +43,26 @@ static std::atomic<int64_t> g_prefix_impl{0}, g_prefix_splits{0}, g_suffix_split
     g_prefix_stages{3}, g_suffix_unroll{4}, g_prefix_ctas{0}, g_suffix_impl{0}, g_suffix_ctas{0},
     g_overlap_prefix_ctas{0}, g_prefix_poly{4}, g_prefix_variant{6}, g_prefix_trace{0}, g_suffix_cb{2}, g_suffix_trace{0},
     g_last_overlap_k{0};  // read-only: prefix CTAs of the last hydra_attn overlap split (0 = sequential)
+// Measurement: cudaEvent_t handles recorded around the prefix (on its stream) and the suffix
+// inside hydra_attn / hydra_attn_paged, so a benchmark can time each kernel within the step
+// (also inside a captured graph); 0 = off.  [0] prefix begin, [1] prefix end, [2] suffix
+// begin, [3] suffix end.
+static std::atomic<int64_t> g_step_ev[4] = {{0}, {0}, {0}, {0}};
+static const char *kStepEvKeys[4] = {"ev_prefix_begin", "ev_prefix_end", "ev_suffix_begin", "ev_suffix_end"};
+static void record_step_ev(int i, cudaStream_t s) {
+  const int64_t e = g_step_ev[i].load();
+  // External: under stream capture the record becomes an observable event-record node (an
+  // internal record would only be a capture dependency and could not be timed)
+  if (!e) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  cudaEvent_t ev = reinterpret_cast<cudaEvent_t>((intptr_t)e);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(ev, s);
+  (void)cudaGetLastError();  // a failed measurement record must not surface as a launch error
+}
 
 extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
   if (!key) return fail(HYDRA_EINVAL, "null key");
@@ -61,7 +81,14 @@ extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
   else if (!strcmp(key, "suffix_trace")) g_suffix_trace = value;
   else if (!strcmp(key, "suffix_cb")) g_suffix_cb = (value == 1 ? 1 : 2);
   else if (!strcmp(key, "suffix_unroll")) g_suffix_unroll = (value >= 8 ? 8 : value >= 4 ? 4 : 2);
-  else return fail(HYDRA_EINVAL, "unknown config key '%s'", key);
+  else {
+    for (int i = 0; i < 4; ++i)
+      if (!strcmp(key, kStepEvKeys[i])) {
+        g_step_ev[i] = value;
+        return HYDRA_OK;
+      }
+    return fail(HYDRA_EINVAL, "unknown config key '%s'", key);
+  }
   return HYDRA_OK;
 }
 
@@ -692,7 +719,9 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
       return cuda_fail("fork");
   }
   if (P > 0) {
+    record_step_ev(0, sa);
     st = run_prefix(h, B, q, q_sb, q_sh, P, pk, pv, kv_st, kv_sh, np, pre, sa, k_over);
+    record_step_ev(1, sa);
   } else {
     st = launch_fill_neg_inf(pre.lse, rows, sa);
     if (st) st = cuda_fail("fill");
@@ -703,8 +732,10 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
     const int k_eff = k_over > 0 ? prefix_tc2_ctas(B, h->num_q_heads / h->num_kv_heads, h->num_kv_heads, P, k_over,
                                                    prefix_bn())
                                  : 0;
+    record_step_ev(2, s);
     st = run_suffix(h, B, q, q_sb, q_sh, sk, sv, s_sb, s_st, s_sh, S_cap, lens, ns, suf, s,
                     k_over > 0 ? std::max(1, sms - k_eff) : 0, pg);
+    record_step_ev(3, s);
   } else {
     st = launch_fill_neg_inf(suf.lse, rows, s);
     if (st) st = cuda_fail("fill");
