@@ -131,23 +131,30 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
 // (profiles/r1n_suffix_tc_c6shape_raw.csv): 3.05 warps stalled on no_instruction per issue,
 // next to 3.8 on barriers -- instruction-fetch misses: 5.1 K SASS instructions for G = 8,
 // every role's per-item path executed once per ~2 us.  Unresolved.)
+// SPLIT (compile time): split-K over tokens.  The unsplit instantiation keeps the plain
+// item = b * Hkv + j arithmetic (the general form cost ~2 % of the C3 step, measured A/B).
+template <bool SPLIT>
 __device__ __forceinline__ int item_len_raw(const SuffixTcParams &P, int item) {
-  return item < P.n_items ? __ldg(P.lens + (item / P.n_split) / P.Hkv) : 0;
+  return item < P.n_items ? __ldg(P.lens + (SPLIT ? item / P.n_split : item) / P.Hkv) : 0;
 }
+template <bool SPLIT>
 __device__ __forceinline__ int item_len_of(const SuffixTcParams &P, int item, int raw) {
-  if (P.n_split == 1) return raw;
+  if (!SPLIT) return raw;
   const int sp = item % P.n_split;
   return max(0, min(P.split_len, raw - sp * P.split_len));
 }
+template <bool SPLIT>
 __device__ __forceinline__ int item_len(const SuffixTcParams &P, int item) {
-  return item_len_of(P, item, item_len_raw(P, item));
+  return item_len_of<SPLIT>(P, item, item_len_raw<SPLIT>(P, item));
 }
 // (sequence, KV head, first token, output offset in elements of o / lse) of an item
 struct ItemRef {
   int b, j, t_base;
   int64_t o_off, lse_off;
 };
+template <bool SPLIT>
 __device__ __forceinline__ ItemRef item_ref(const SuffixTcParams &P, int item) {
+  if (!SPLIT) return {item / P.Hkv, item % P.Hkv, 0, 0, 0};
   const int bj = item / P.n_split, sp = item - bj * P.n_split;
   return {bj / P.Hkv, bj % P.Hkv, sp * P.split_len, sp * P.o_split_stride, sp * P.lse_split_stride};
 }
@@ -158,13 +165,14 @@ __device__ __forceinline__ ItemRef item_ref(const SuffixTcParams &P, int item) {
 // Measured (tools/paged_rate.py, C3 suffix on 76 SMs): block-table loads in the producer
 // thread, or this loop on a second lane of the producer warp, held the paged kernel at
 // 3.6-4.0 TB/s even with identity pages; on its own warp 6.4-6.6 TB/s (pages >= 16).
+template <bool SPLIT>
 __device__ __forceinline__ void page_table_lane(const SuffixTcParams &P, int32_t *ring, uint64_t *tab_full,
                                                 uint64_t *tab_empty) {
   uint32_t k = 0;
   for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
-    const int len = item_len(P, item);
+    const int len = item_len<SPLIT>(P, item);
     const int nblk = (len + stc::BT - 1) / stc::BT;
-    const ItemRef ir = item_ref(P, item);
+    const ItemRef ir = item_ref<SPLIT>(P, item);
     const int32_t *bt = P.block_table + (int64_t)ir.b * P.bt_stride;
     for (int n = 0; n < nblk; ++n, ++k) {
       const int slot = k % stc::PR;
@@ -186,15 +194,15 @@ __device__ __forceinline__ void page_table_lane(const SuffixTcParams &P, int32_t
 // Walks the rounds (up to CB consecutive 128-token blocks of one item) a CTA processes, in
 // order, with the ring positions the producers use: gb = first block's ring index, gr =
 // round index, qi / item_no = index of the item among this CTA's non-empty items.
-template <int CB>
+template <int CB, bool SPLIT>
 struct RoundCursor {
   int item, len, len_next, nblk, n0, nb;
   uint32_t gb, gr, qi, item_no;
   bool valid;
   __device__ __forceinline__ void seek(const SuffixTcParams &P) {  // first round of the next non-empty item
     while (item < P.n_items) {
-      len = item_len_of(P, item, len_next);
-      len_next = item_len_raw(P, item + gridDim.x);
+      len = item_len_of<SPLIT>(P, item, len_next);
+      len_next = item_len_raw<SPLIT>(P, item + gridDim.x);
       nblk = (len + stc::BT - 1) / stc::BT;
       if (nblk > 0) {
         n0 = 0;
@@ -208,7 +216,7 @@ struct RoundCursor {
   }
   __device__ __forceinline__ void init(const SuffixTcParams &P) {
     item = blockIdx.x;
-    len_next = item_len_raw(P, item);
+    len_next = item_len_raw<SPLIT>(P, item);
     gb = gr = qi = item_no = 0;
     seek(P);
   }
@@ -232,7 +240,7 @@ struct RoundCursor {
 // P^T write per round of up to CB blocks (thread r owns tokens r, 128 + r, ...), so the
 // per-round latency chain (S MMA -> TMEM load -> cross-warp max -> exp -> P^T -> PV MMA)
 // is paid once per CB blocks.  Online softmax across the rounds of an item.
-template <int G, int CB>
+template <int G, int CB, bool SPLIT>
 __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __grid_constant__ SuffixTcParams P) {
   using namespace stc;
   constexpr int OFF_P = off_p(CB), OFF_RED = off_red(CB), OFF_BAR = off_bar(CB);
@@ -296,7 +304,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
   if (warp == 13) {
     // ================= paged cache: block-table entries into the page-id ring =================
     if (P.block_table != nullptr && ptx::elect_one())
-      page_table_lane(P, tab_ring, tab_full, tab_empty);
+      page_table_lane<SPLIT>(P, tab_ring, tab_full, tab_empty);
   } else if (warp == 0 || warp == 6 || warp == 7) {
     // ================= TMA producers: warp 0 K ring, warp 6 V ring, warp 7 Q slots =================
     // Separate threads so no load waits behind another kind of slot (V slots free only after
@@ -304,12 +312,12 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
     if (ptx::elect_one()) {
       long long *tr = blockIdx.x == 0 ? P.trace : nullptr;
       uint32_t gb = 0, qi = 0;
-      int len_next = item_len_raw(P, blockIdx.x);
+      int len_next = item_len_raw<SPLIT>(P, blockIdx.x);
       for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
-        const ItemRef ir = item_ref(P, item);
+        const ItemRef ir = item_ref<SPLIT>(P, item);
         const int b = ir.b, j = ir.j;
-        const int len = item_len_of(P, item, len_next);
-        len_next = item_len_raw(P, item + gridDim.x);
+        const int len = item_len_of<SPLIT>(P, item, len_next);
+        len_next = item_len_raw<SPLIT>(P, item + gridDim.x);
         const int nblk = (len + BT - 1) / BT;
         if (nblk == 0) continue;
         if (warp == 7) {
@@ -367,7 +375,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
     // Neither waits behind the other, so a V slot is held only for load + softmax + PV.
     const bool leader = ptx::elect_one();
     if (leader && (P.debug & 256)) {  // drain only: release each tile as soon as it lands
-      RoundCursor<CB> c;
+      RoundCursor<CB, SPLIT> c;
       c.init(P);
       while (c.valid) {
         if (c.n0 == 0) ptx::mbar_wait(&q_full[c.qi % NQS], (c.qi / NQS) & 1);
@@ -390,7 +398,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
       // never waits behind a V tile and a PV MMA never waits behind a K tile.
       constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BT, NQ, false);  // A=K, B=Q^T (K-major)
       long long *tr = blockIdx.x == 0 ? P.trace : nullptr;
-      RoundCursor<CB> sc;
+      RoundCursor<CB, SPLIT> sc;
       sc.init(P);
       while (sc.valid) {
         if (sc.gr >= (uint32_t)NSP) ptx::mbar_wait(&p_full[sc.gr % NSP], ((sc.gr - NSP) / NSP) & 1);
@@ -427,7 +435,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
       const bool leader = ptx::elect_one();
       constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(HD, NQ, false) | (1u << 15);  // A=V^T (MN-major), B=P^T
       long long *tr = (blockIdx.x == 0 && leader) ? P.trace : nullptr;
-      RoundCursor<CB> pc;
+      RoundCursor<CB, SPLIT> pc;
       pc.init(P);
       while (pc.valid) {
         const uint32_t slot = pc.gr % NSP, ob = pc.item_no & 1;
@@ -478,11 +486,11 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
     const float c2 = P.scale_log2;
     uint32_t gr = 0, gb = 0, item_no = 0;
     long long *tr = (blockIdx.x == 0 && quarter == 0 && lane == 0) ? P.trace : nullptr;
-    int len_next = item_len_raw(P, blockIdx.x);
+    int len_next = item_len_raw<SPLIT>(P, blockIdx.x);
     for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
-      const ItemRef ir = item_ref(P, item);
-      const int len = item_len_of(P, item, len_next);
-      len_next = item_len_raw(P, item + gridDim.x);
+      const ItemRef ir = item_ref<SPLIT>(P, item);
+      const int len = item_len_of<SPLIT>(P, item, len_next);
+      len_next = item_len_raw<SPLIT>(P, item + gridDim.x);
       const int nblk = (len + BT - 1) / BT;
       const int64_t row0 = (int64_t)ir.b * P.Hq + (int64_t)ir.j * g;
       if (nblk == 0) {  // empty suffix (or split): (0, -inf) sentinel
@@ -616,12 +624,12 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
     const int r = quarter * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     uint32_t item_no = 0;
-    int len_next = item_len_raw(P, blockIdx.x);
+    int len_next = item_len_raw<SPLIT>(P, blockIdx.x);
     for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
-      const int len = item_len_of(P, item, len_next);
-      len_next = item_len_raw(P, item + gridDim.x);
+      const int len = item_len_of<SPLIT>(P, item, len_next);
+      len_next = item_len_raw<SPLIT>(P, item + gridDim.x);
       if (len <= 0) continue;
-      const ItemRef ir = item_ref(P, item);
+      const ItemRef ir = item_ref<SPLIT>(P, item);
       const int64_t row0 = (int64_t)ir.b * P.Hq + (int64_t)ir.j * g;
       const uint32_t ob = item_no & 1, ph = (item_no >> 1) & 1;
       ptx::mbar_wait(&o_full[ob], ph);
@@ -677,17 +685,21 @@ bool suffix_tc_supported(const hydra_heads *h) {
   return h->dtype == HYDRA_BF16 && h->head_dim == 128 && g_ok && encode_fn3() != nullptr;
 }
 
-template <int G, int CB>
-static cudaError_t launch_gc(const SuffixTcParams &P, int grid, cudaStream_t s) {
+template <int G, int CB, bool SPLIT>
+static cudaError_t launch_gcs(const SuffixTcParams &P, int grid, cudaStream_t s) {
   static std::once_flag once;
   static cudaError_t attr = cudaSuccess;
   constexpr int alloc = stc::alloc_bytes(CB);
   std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(suffix_tc_kernel<G, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, alloc);
+    attr = cudaFuncSetAttribute(suffix_tc_kernel<G, CB, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, alloc);
   });
   if (attr != cudaSuccess) return attr;
-  suffix_tc_kernel<G, CB><<<grid, stc::kThreads, alloc, s>>>(P);
+  suffix_tc_kernel<G, CB, SPLIT><<<grid, stc::kThreads, alloc, s>>>(P);
   return cudaGetLastError();
+}
+template <int G, int CB>
+static cudaError_t launch_gc(const SuffixTcParams &P, int grid, cudaStream_t s) {
+  return P.n_split > 1 ? launch_gcs<G, CB, true>(P, grid, s) : launch_gcs<G, CB, false>(P, grid, s);
 }
 template <int G>
 static cudaError_t launch_g(const SuffixTcParams &P, int cb, int grid, cudaStream_t s) {
