@@ -104,23 +104,16 @@ __global__ void __launch_bounds__(256) combine_kernel_p8(const CombineParams p) 
   const int lane = threadIdx.x % 32;
   if (row >= p.rows) return;
   const OT *o_parts = reinterpret_cast<const OT *>(p.o_parts);
-  float lq[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) lq[q] = q < p.n_parts ? __ldg(p.lse_parts + q * p.lse_part_stride + row) : -INFINITY;
-  float m = -INFINITY;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) m = fmaxf(m, lq[q]);
-  OutT *out = reinterpret_cast<OutT *>(p.out) + row * p.d;
-  if (m == -INFINITY) {  // every part empty: sentinel (0, -inf)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) out[lane * 4 + i] = OutT(0.f);
-    if (p.lse_out && lane == 0) p.lse_out[row] = -INFINITY;
-    return;
-  }
-  float f[8][4];
+  // Every part's LSE and O loads are issued together, before any decision on their values
+  // (one memory round trip per row, not two).  An empty part's O slot may be unwritten
+  // workspace: it is loaded but never used (skipped below, not multiplied by 0, so garbage
+  // or NaN cannot leak in).
+  float lq[8], f[8][4];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    if (lq[q] != -INFINITY) {  // empty parts are never read (their O slot may be unwritten)
+    lq[q] = -INFINITY;
+    if (q < p.n_parts) {
+      lq[q] = __ldg(p.lse_parts + q * p.lse_part_stride + row);
       const OT *src = o_parts + q * p.o_part_stride + row * p.d + lane * 4;
       if constexpr (sizeof(OT) == 4) {
         const float4 v = __ldg(reinterpret_cast<const float4 *>(src));
@@ -132,6 +125,16 @@ __global__ void __launch_bounds__(256) combine_kernel_p8(const CombineParams p) 
         f[q][0] = __low2float(a); f[q][1] = __high2float(a); f[q][2] = __low2float(b); f[q][3] = __high2float(b);
       }
     }
+  }
+  float m = -INFINITY;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) m = fmaxf(m, lq[q]);
+  OutT *out = reinterpret_cast<OutT *>(p.out) + row * p.d;
+  if (m == -INFINITY) {  // every part empty: sentinel (0, -inf)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[lane * 4 + i] = OutT(0.f);
+    if (p.lse_out && lane == 0) p.lse_out[row] = -INFINITY;
+    return;
   }
   float acc[4] = {0.f, 0.f, 0.f, 0.f}, den = 0.f;
 #pragma unroll
