@@ -98,64 +98,79 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
 // rows together (16 B per lane), then the weighted sum.  The part loop of combine_kernel
 // serialises a dependent LSE load and O load per part, so with 3-8 parts it ran at 30-50 %
 // of HBM bandwidth (e.g. 22 us instead of ~12 at C3).
-template <typename OT, typename OutT>
+template <typename OT, typename OutT, int NP, int RPW>
 __global__ void __launch_bounds__(256) combine_kernel_p8(const CombineParams p) {
-  const int64_t row = (int64_t)blockIdx.x * 8 + threadIdx.x / 32;
+  // NP: parts rounded up (2, 4 or 8); RPW rows per warp.  Every part's LSE and O loads of all
+  // RPW rows are issued together, before any decision on their values (one memory round trip
+  // per RPW rows).  An empty part's O slot may be unwritten workspace: it is loaded but never
+  // used (skipped below, not multiplied by 0, so garbage or NaN cannot leak in).
+  const int64_t row0 = ((int64_t)blockIdx.x * 8 + threadIdx.x / 32) * RPW;
   const int lane = threadIdx.x % 32;
-  if (row >= p.rows) return;
+  if (row0 >= p.rows) return;
   const OT *o_parts = reinterpret_cast<const OT *>(p.o_parts);
-  // Every part's LSE and O loads are issued together, before any decision on their values
-  // (one memory round trip per row, not two).  An empty part's O slot may be unwritten
-  // workspace: it is loaded but never used (skipped below, not multiplied by 0, so garbage
-  // or NaN cannot leak in).
-  float lq[8], f[8][4];
+  float lq[RPW][NP], f[RPW][NP][4];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    lq[q] = -INFINITY;
-    if (q < p.n_parts) {
-      lq[q] = __ldg(p.lse_parts + q * p.lse_part_stride + row);
-      const OT *src = o_parts + q * p.o_part_stride + row * p.d + lane * 4;
-      if constexpr (sizeof(OT) == 4) {
-        const float4 v = __ldg(reinterpret_cast<const float4 *>(src));
-        f[q][0] = v.x; f[q][1] = v.y; f[q][2] = v.z; f[q][3] = v.w;
-      } else {
-        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(src));
-        const __half2 a = *reinterpret_cast<const __half2 *>(&v.x);
-        const __half2 b = *reinterpret_cast<const __half2 *>(&v.y);
-        f[q][0] = __low2float(a); f[q][1] = __high2float(a); f[q][2] = __low2float(b); f[q][3] = __high2float(b);
+  for (int k = 0; k < RPW; ++k) {
+    const int64_t row = row0 + k;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      lq[k][q] = -INFINITY;
+      if (q < p.n_parts && row < p.rows) {
+        lq[k][q] = __ldg(p.lse_parts + q * p.lse_part_stride + row);
+        const OT *src = o_parts + q * p.o_part_stride + row * p.d + lane * 4;
+        if constexpr (sizeof(OT) == 4) {
+          const float4 v = __ldg(reinterpret_cast<const float4 *>(src));
+          f[k][q][0] = v.x; f[k][q][1] = v.y; f[k][q][2] = v.z; f[k][q][3] = v.w;
+        } else {
+          const uint2 v = __ldg(reinterpret_cast<const uint2 *>(src));
+          const __half2 a = *reinterpret_cast<const __half2 *>(&v.x);
+          const __half2 b = *reinterpret_cast<const __half2 *>(&v.y);
+          f[k][q][0] = __low2float(a); f[k][q][1] = __high2float(a);
+          f[k][q][2] = __low2float(b); f[k][q][3] = __high2float(b);
+        }
       }
     }
   }
-  float m = -INFINITY;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) m = fmaxf(m, lq[q]);
-  OutT *out = reinterpret_cast<OutT *>(p.out) + row * p.d;
-  if (m == -INFINITY) {  // every part empty: sentinel (0, -inf)
+  for (int k = 0; k < RPW; ++k) {
+    const int64_t row = row0 + k;
+    if (row >= p.rows) break;
+    float m = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) out[lane * 4 + i] = OutT(0.f);
-    if (p.lse_out && lane == 0) p.lse_out[row] = -INFINITY;
-    return;
+    for (int q = 0; q < NP; ++q) m = fmaxf(m, lq[k][q]);
+    OutT *out = reinterpret_cast<OutT *>(p.out) + row * p.d;
+    if (m == -INFINITY) {  // every part empty: sentinel (0, -inf)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) out[lane * 4 + i] = OutT(0.f);
+      if (p.lse_out && lane == 0) p.lse_out[row] = -INFINITY;
+      continue;
+    }
+    float acc[4] = {0.f, 0.f, 0.f, 0.f}, den = 0.f;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      if (lq[k][q] == -INFINITY) continue;
+      const float w = p.inject_bug ? 1.f : expf(lq[k][q] - m);
+      den += w;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) acc[i] = fmaf(w, f[k][q][i], acc[i]);
+    }
+    const float inv = 1.f / den;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) out[lane * 4 + i] = OutT(acc[i] * inv);
+    if (p.lse_out && lane == 0) p.lse_out[row] = m + logf(den);
   }
-  float acc[4] = {0.f, 0.f, 0.f, 0.f}, den = 0.f;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    if (lq[q] == -INFINITY) continue;
-    const float w = p.inject_bug ? 1.f : expf(lq[q] - m);
-    den += w;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) acc[i] = fmaf(w, f[q][i], acc[i]);
-  }
-  const float inv = 1.f / den;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) out[lane * 4 + i] = OutT(acc[i] * inv);
-  if (p.lse_out && lane == 0) p.lse_out[row] = m + logf(den);
 }
 
 template <typename OT, typename OutT>
 static cudaError_t launch_c(const CombineParams &p, cudaStream_t s) {
   const dim3 grid((unsigned)((p.rows + 7) / 8));
-  if (p.d == 128 && p.n_parts <= 8)
-    combine_kernel_p8<OT, OutT><<<grid, 256, 0, s>>>(p);
+  const dim3 grid2((unsigned)((p.rows + 15) / 16));  // two rows per warp
+  if (p.d == 128 && p.n_parts <= 2)
+    combine_kernel_p8<OT, OutT, 2, 2><<<grid2, 256, 0, s>>>(p);
+  else if (p.d == 128 && p.n_parts <= 4)
+    combine_kernel_p8<OT, OutT, 4, 2><<<grid2, 256, 0, s>>>(p);
+  else if (p.d == 128 && p.n_parts <= 8)
+    combine_kernel_p8<OT, OutT, 8, 2><<<grid2, 256, 0, s>>>(p);
   else if (p.d == 128)
     combine_kernel<OT, OutT, 4><<<grid, 256, 0, s>>>(p);
   else if (p.d == 256)
