@@ -62,9 +62,9 @@ CONFIGS = {
 # DRAM bytes (read + write) per launch from one `ncu --set full` capture of the kernel at this
 # config (profiles/r1b_ncu_full_*.csv: dram__bytes_read.sum + dram__bytes_write.sum)
 NCU_TRAFFIC = {
-    ("c3_16k", "decode_attn_kernel"): 5379352000 + 8595712,   # profiles/r1l_suffix_decode_raw.csv
-    ("c3_16k", "suffix_tc_kernel"): 5379254000 + 24337664,   # profiles/r1l_suffix_tc_76_raw.csv (76 CTAs, k = 72)
-    ("c3_16k", "prefix_tc2_kernel"): 355146496 + 22375168,   # profiles/r1l_prefix_tc2_raw.csv (variant 6, poly 4)
+    ("c3_16k", "decode_attn_kernel"): 5379746000 + 6668800,    # profiles/r1o_suffix_decode_raw.csv
+    ("c3_16k", "suffix_tc_kernel"): 5379274000 + 25441024,     # profiles/r1o_suffix_tc_76_raw.csv (76 CTAs, k = 72)
+    ("c3_16k", "prefix_tc2_kernel"): 355092736 + 21645312,     # profiles/r1o_prefix_tc2_raw.csv (variant 6, poly 4)
 }
 
 
