@@ -461,3 +461,33 @@ def test_suffix_gqa_long_suffix_auto():
     o2, l2 = hydra.suffix_attn_paged(t["q"], kp, vp, torch.from_numpy(pc.block_table).to(DEV), t["lens"], S_cap=S)
     torch.cuda.synchronize()
     assert torch.equal(o, o2) and torch.equal(l, l2)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("rows", [1, 7, 33, 1001])
+def test_combine_part_counts_and_odd_rows(n, rows):
+    """The combine kernels for 2 / 4 / 8 parts at two rows per warp: odd row counts (a warp's
+    second row past the end), all-empty rows, NaN in an empty part's unwritten slot."""
+    rng = np.random.default_rng(n * 1000 + rows)
+    o = rng.standard_normal((n, rows, 128))
+    l = rng.uniform(-6, 6, (n, rows))
+    l[0, ::3] = -np.inf
+    if n > 1:
+        l[:, rows // 2] = -np.inf  # every part empty for this row
+        o[1, l[1] == -np.inf] = np.nan  # garbage in slots the combine must not read
+        l[1, ::2] = -np.inf
+        o[1, l[1] == -np.inf] = np.nan
+    o_ref = np.where(np.isneginf(l)[..., None], 0.0, o)  # an empty part is the (0, -inf) sentinel (R6)
+    ref_o, ref_l = o_ref[0], l[0]
+    for i in range(1, n):
+        ref_o, ref_l = oracle.combine(ref_o, ref_l, o_ref[i], l[i])
+    ot = torch.tensor(o, dtype=torch.float32, device=DEV)
+    lt = torch.tensor(l, dtype=torch.float32, device=DEV)
+    out, lse = hydra.combine(ot, lt, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    assert np.isfinite(got).all()
+    np.testing.assert_allclose(got, ref_o, atol=2e-5)
+    np.testing.assert_array_equal(np.isneginf(lse.cpu().numpy()), np.isneginf(ref_l))
+    fin = np.isfinite(ref_l)
+    np.testing.assert_allclose(lse.cpu().numpy()[fin], ref_l[fin], atol=2e-5)
