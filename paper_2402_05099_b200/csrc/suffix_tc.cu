@@ -240,7 +240,7 @@ struct RoundCursor {
 // P^T write per round of up to CB blocks (thread r owns tokens r, 128 + r, ...), so the
 // per-round latency chain (S MMA -> TMEM load -> cross-warp max -> exp -> P^T -> PV MMA)
 // is paid once per CB blocks.  Online softmax across the rounds of an item.
-template <int G, int CB, bool SPLIT>
+template <int G, int CB, bool SPLIT, bool PAGED>
 __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __grid_constant__ SuffixTcParams P) {
   using namespace stc;
   constexpr int OFF_P = off_p(CB), OFF_RED = off_red(CB), OFF_BAR = off_bar(CB);
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
 
   if (warp == 13) {
     // ================= paged cache: block-table entries into the page-id ring =================
-    if (P.block_table != nullptr && ptx::elect_one())
+    if (PAGED && ptx::elect_one())
       page_table_lane<SPLIT>(P, tab_ring, tab_full, tab_empty);
   } else if (warp == 0 || warp == 6 || warp == 7) {
     // ================= TMA producers: warp 0 K ring, warp 6 V ring, warp 7 Q slots =================
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
           const CUtensorMap *tm = warp == 0 ? &P.tmK : &P.tmV;
           uint64_t *full = warp == 0 ? &k_full[st] : &v_full[st];
           uint8_t *dst = smem + (warp == 0 ? OFF_K : OFF_V) + st * TILE;
-          if (P.block_table == nullptr) {
+          if constexpr (!PAGED) {
             ptx::mbar_wait(warp == 0 ? &k_empty[st] : &v_empty[st], ph);
             ptx::mbar_arrive_expect_tx(full, TILE);
             ptx::tma_load_4d(dst, tm, full, 0, j, t0, b);
@@ -685,17 +685,23 @@ bool suffix_tc_supported(const hydra_heads *h) {
   return h->dtype == HYDRA_BF16 && h->head_dim == 128 && g_ok && encode_fn3() != nullptr;
 }
 
-template <int G, int CB, bool SPLIT>
-static cudaError_t launch_gcs(const SuffixTcParams &P, int grid, cudaStream_t s) {
+template <int G, int CB, bool SPLIT, bool PAGED>
+static cudaError_t launch_gcsp(const SuffixTcParams &P, int grid, cudaStream_t s) {
   static std::once_flag once;
   static cudaError_t attr = cudaSuccess;
   constexpr int alloc = stc::alloc_bytes(CB);
   std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(suffix_tc_kernel<G, CB, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, alloc);
+    attr = cudaFuncSetAttribute(suffix_tc_kernel<G, CB, SPLIT, PAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                alloc);
   });
   if (attr != cudaSuccess) return attr;
-  suffix_tc_kernel<G, CB, SPLIT><<<grid, stc::kThreads, alloc, s>>>(P);
+  suffix_tc_kernel<G, CB, SPLIT, PAGED><<<grid, stc::kThreads, alloc, s>>>(P);
   return cudaGetLastError();
+}
+// PAGED (compile time): the contiguous kernel carries no paging branch in its producers
+template <int G, int CB, bool SPLIT>
+static cudaError_t launch_gcs(const SuffixTcParams &P, int grid, cudaStream_t s) {
+  return P.block_table ? launch_gcsp<G, CB, SPLIT, true>(P, grid, s) : launch_gcsp<G, CB, SPLIT, false>(P, grid, s);
 }
 template <int G, int CB>
 static cudaError_t launch_gc(const SuffixTcParams &P, int grid, cudaStream_t s) {
