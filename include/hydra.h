@@ -31,17 +31,27 @@
  *  - Every call is asynchronous and stream-ordered on `stream` (a cudaStream_t
  *    passed as void*), never synchronises the host and never reads device data
  *    on the host, so it can be captured in a CUDA graph (the paper's requirement,
- *    P:149).  Exception: the first hydra_tree_attn call for a given head grouping
- *    uploads the tree's work list (see hydra_tree_attn).
+ *    P:149).  Tree attention is capturable once its tree is prepared for the head
+ *    grouping (hydra_tree_prepare; an unprepared tree is prepared by the first call
+ *    made outside capture, and a captured call on it fails with HYDRA_EINVAL).
  *  - Errors: host-visible arguments are validated synchronously; on a non-OK
  *    status nothing has been launched and hydra_last_error() describes why.
  *    Launch failures return HYDRA_ECUDA.  Device-resident lens values are a
- *    documented precondition (0 <= lens[b] <= S_cap), not checked.
- *  - Thread safety: all entry points are reentrant; hydra_last_error is
- *    thread-local.
+ *    documented precondition (0 <= lens[b] <= S_cap): the kernels clamp an
+ *    out-of-range value into [0, S_cap] (never reading past the cache), and the
+ *    testing build (libhydra_test.so) also counts violations on the device
+ *    (hydra_debug_lens_violations).
+ *  - Thread safety: all entry points are reentrant.  hydra_last_error and the
+ *    settings of hydra_set_config are thread-local: one thread's switches and
+ *    measurement events never affect another thread's calls.
  *  - Precision: HYDRA_BF16 inputs use fp32 accumulation, fp32 partials and a
  *    bf16 (round-to-nearest-even) final output; HYDRA_F32 inputs run an all-fp32
  *    reference mode (SIMT kernels, accurate exp).
+ *  - Kernels: BF16 with head_dim 128 runs the tcgen05/TMEM/TMA kernels (the stacked
+ *    prefix GEMM of §3.2 and the tensor-core suffix GEMV).  Other head dims and F32
+ *    run SIMT kernels: the suffix kernel, and for the prefix the same kernel with a
+ *    batch stride of 0 (every sequence reads the one prefix copy through L2, but the
+ *    queries are not stacked into a tensor-core GEMM).
  */
 #ifndef HYDRA_H_
 #define HYDRA_H_
@@ -87,6 +97,7 @@ typedef struct {
 #define HYDRA_OP_PREFIX 0
 #define HYDRA_OP_SUFFIX 1
 #define HYDRA_OP_ATTN 2
+#define HYDRA_OP_PARTS 3 /* n_parts caller-staged partial slots (O f32 [B,Hq,d] + LSE f32 [B,Hq] each) */
 
 /*
  * hydra_prefix_attn -- inter-sequence batched attention over the shared prefix
@@ -130,8 +141,8 @@ HYDRA_API hydra_status hydra_suffix_attn(const hydra_heads *h, int64_t B,
  * lse_parts[p*lse_part_stride + r]; strides let it read an all-gathered
  * [rank][O|LSE] buffer in place.  out_dtype BF16 or F32 (or F16 from F32 parts: packing
  * partials for a cross-GPU exchange, n_parts may be 1); lse_out may be NULL.
- * Setting the environment variable HYDRA_INJECT_COMBINE_BUG=1 drops the
- * rescaling (w_p = 1): a sabotage switch the parity suite must catch.
+ * (The testing build's config key "inject_combine_bug" drops the rescaling, w_p = 1:
+ * a sabotage switch the parity suite must catch.  The release build has none.)
  */
 HYDRA_API hydra_status hydra_combine(int64_t rows, int32_t d, int32_t n_parts,
                            const void *o_parts, hydra_dtype o_dtype, int64_t o_part_stride,
@@ -231,11 +242,16 @@ HYDRA_API hydra_status hydra_append_kv_paged(const hydra_heads *h, int64_t B,
  * hydra_tree_create builds the per-node query groups (ascending sequence ids of
  * every sequence whose root->leaf path passes through the node) and
  * copies them to the device (synchronous; call outside graph capture).
+ * hydra_tree_prepare uploads the node-attention work list for the head grouping of `h`
+ * (synchronous, outside capture; idempotent).  After it, every hydra_tree_attn /
+ * hydra_tree_attn_paged call with that grouping is a pure, capturable launch sequence.
+ * A tree may be prepared for several groupings.
  */
 struct hydra_tree;
 HYDRA_API hydra_status hydra_tree_create(const int32_t *parent, const int64_t *node_off, const int64_t *node_len,
                                int32_t n_nodes, const int32_t *leaf_of_seq, int64_t B,
                                struct hydra_tree **out);
+HYDRA_API hydra_status hydra_tree_prepare(struct hydra_tree *t, const hydra_heads *h);
 HYDRA_API void hydra_tree_destroy(struct hydra_tree *t);
 /* Depth (number of nodes on the longest root->leaf path) and group sizes, for tooling. */
 HYDRA_API int32_t hydra_tree_depth(const struct hydra_tree *t);
@@ -247,9 +263,10 @@ HYDRA_API size_t hydra_tree_workspace_size(const hydra_heads *h, const struct hy
  * sequences in its group attend to the node's K/V (one grouped launch over
  * (node, KV head, query tile)); each sequence's suffix attention; then an n-ary
  * combine over the path partials and the suffix (decomposition at every vertex,
- * §3.3).  Output as hydra_attn.  The first call for a given Hq/Hkv grouping
- * uploads a small work list to the device synchronously (not capturable); later
- * calls are pure launches.
+ * §3.3).  Output as hydra_attn.  Capturable once the tree is prepared for
+ * this Hq/Hkv grouping (hydra_tree_prepare); an unprepared tree is prepared
+ * synchronously by the first call made outside capture, and a captured call on an
+ * unprepared tree returns HYDRA_EINVAL with nothing launched.
  * stream_aux: nullable second stream.  When given (and both the node attention and the
  * suffix take their persistent tensor-core kernels), the node attention runs on k SMs
  * on stream_aux while the suffix runs on the other SMs on `stream`, as in hydra_attn;
@@ -273,38 +290,51 @@ HYDRA_API hydra_status hydra_tree_attn_paged(const hydra_heads *h, const struct 
                                    void *out, hydra_dtype out_dtype, float *lse_out,
                                    void *ws, size_t ws_bytes, void *stream, void *stream_aux);
 
-/* Bytes of device workspace the op needs for these sizes (0 if none). */
+/* Bytes of device workspace the op needs for these sizes (0 if none).  n_parts is read by
+ * HYDRA_OP_PARTS only: n_parts partial slots of B*Hq rows (for callers that stage their
+ * own partials for hydra_combine, e.g. a cross-GPU exchange); the other ops ignore it. */
 HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, int64_t P, int64_t S_cap,
                             int32_t n_parts);
 
 /*
- * Tuning / test switches (process-wide; 0 = automatic unless stated):
+ * Tuning switches, per calling thread (thread-local; 0 = automatic unless stated):
  *   "prefix_impl"         1 SIMT, 2 one-tile tcgen05 kernel, 3 persistent two-tile tcgen05 kernel
- *   "prefix_variant"      persistent kernel: 3 (default, 128-token blocks), 4 (64-token blocks,
+ *   "prefix_variant"      persistent kernel: 6 (default: 128-token blocks, P published in two
+ *                         64-token halves), 3 (128-token blocks), 4 (64-token blocks,
  *                         double-buffered scores), 5 (3 + speculative running-max softmax)
- *   "prefix_poly"         0 (default) all exp2 on MUFU; 3/4/8: every k-th pair on the FMA pipe
+ *   "prefix_poly"         4 (default): every 4th exp2 pair on the FMA pipe; 0 all exp2 on MUFU; 3 / 8
  *   "prefix_splits"       KV splits of the one-tile / SIMT prefix kernels
  *   "prefix_ctas"         CTAs of the persistent prefix kernel
  *   "suffix_impl"         1 SIMT split-K GEMV, 2 persistent TMA-fed tensor-core kernel
  *   "suffix_splits"       KV splits of the suffix kernels (tensor-core kernel: split-K over
  *                         tokens, only when set; SIMT kernel: automatic when 0)
  *   "suffix_ctas"         CTAs of the persistent suffix kernel
+ *   "suffix_cb"           tensor-core suffix: 128-token blocks per softmax round, 2 (default) or 1
  *   "suffix_unroll"       tokens in flight per row group of the SIMT suffix kernel (4 or 8)
  *   "overlap_prefix_ctas" SM split of hydra_attn with an aux stream (prefix CTAs)
  *   "prefix_stages"       K/V pipeline stages of the one-tile kernel (2 or 3)
- *   "tc_debug_variant"    timing experiments only (invalid results); never set in production
- *   "prefix_trace"        diagnostics: device pointer of a 14*1024 int64 buffer for CTA-0
- *                         timestamps of the persistent prefix kernel (tools/prefix_trace.py)
  *   "ev_prefix_begin" / "ev_prefix_end" / "ev_suffix_begin" / "ev_suffix_end"
  *                         measurement: a cudaEvent_t (as an integer) that hydra_attn records
  *                         right before / after its prefix (on the prefix's stream) or suffix
  *                         launches, also inside graph capture; 0 = off
- * hydra_get_config also answers "last_overlap_k": prefix CTAs of the last hydra_attn
- * overlap split (0 = the two phases ran sequentially).
+ * Testing build only (libhydra_test.so; the release library returns HYDRA_EINVAL for these):
+ *   "tc_debug_variant"    timing experiments (invalid results)
+ *   "prefix_trace" / "suffix_trace"  device buffer for CTA-0 timestamps (tools/)
+ *   "inject_combine_bug"  1: the combine drops its rescaling (w_p = 1) -- the sabotage of S:522
+ *   "mutate"              1: the persistent prefix kernel's CTA 0 skips one 4-row store group of
+ *                         its epilogues; 2: the tensor-core suffix's CTA 0 skips head 0's output
+ *                         row of its first item (unwritten rows the parity suite must catch)
+ * hydra_get_config also answers "last_overlap_k" (prefix CTAs of this thread's last hydra_attn /
+ * hydra_tree_attn overlap split, 0 = sequential) and "testing_build" (1 in libhydra_test.so).
  * Returns HYDRA_EINVAL for an unknown key.
  */
 HYDRA_API hydra_status hydra_set_config(const char *key, int64_t value);
 HYDRA_API int64_t hydra_get_config(const char *key);
+
+/* Testing build: number of lens[b] values outside [0, S_cap] the suffix launches have seen
+ * since the last reset (synchronises the device; reset != 0 zeroes the count).  The release
+ * build returns -1 (no device check; its kernels clamp). */
+HYDRA_API int64_t hydra_debug_lens_violations(int32_t reset);
 
 /* Message for the last non-OK status on this thread ("" if none). */
 HYDRA_API const char *hydra_last_error(void);

@@ -18,4 +18,5 @@ from .attn import (  # noqa: F401
     suffix_attn_paged,
     tree_attention,
     tree_attention_paged,
+    workspace_bytes_tree,
 )

@@ -10,19 +10,23 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# HYDRA_LIB_PATH: load another build of the library (A/B timing of two builds on one box)
-LIB_PATH = os.environ.get("HYDRA_LIB_PATH") or os.path.join(_HERE, "libhydra.so")
+# HYDRA_LIB_PATH: load another build of the library (A/B timing of two builds on one box);
+# HYDRA_TESTING=1: the testing build libhydra_test.so (diagnostics and the parity suite's
+# sabotage switches, which the release libhydra.so does not contain).
+RELEASE_LIB = os.path.join(_HERE, "libhydra.so")
+TEST_LIB = os.path.join(_HERE, "libhydra_test.so")
+LIB_PATH = os.environ.get("HYDRA_LIB_PATH") or (TEST_LIB if os.environ.get("HYDRA_TESTING") == "1" else RELEASE_LIB)
 
 HYDRA_OK, HYDRA_EINVAL, HYDRA_ESHAPE, HYDRA_EUNSUPPORTED, HYDRA_ECUDA, HYDRA_ENCCL, HYDRA_ENOMEM = range(7)
 HYDRA_BF16, HYDRA_F32, HYDRA_F16 = 0, 1, 2
-HYDRA_OP_PREFIX, HYDRA_OP_SUFFIX, HYDRA_OP_ATTN = 0, 1, 2
+HYDRA_OP_PREFIX, HYDRA_OP_SUFFIX, HYDRA_OP_ATTN, HYDRA_OP_PARTS = 0, 1, 2, 3
 _STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ESHAPE", 3: "EUNSUPPORTED", 4: "ECUDA", 5: "ENCCL", 6: "ENOMEM"}
 
 EXPORTED = ["hydra_prefix_attn", "hydra_suffix_attn", "hydra_combine", "hydra_attn", "hydra_tree_create",
             "hydra_tree_destroy", "hydra_tree_depth", "hydra_tree_group_size", "hydra_tree_workspace_size",
             "hydra_tree_attn", "hydra_workspace_size", "hydra_set_config", "hydra_get_config",
             "hydra_last_error", "hydra_version", "hydra_append_kv", "hydra_suffix_attn_paged", "hydra_attn_paged",
-            "hydra_append_kv_paged", "hydra_tree_attn_paged"]
+            "hydra_append_kv_paged", "hydra_tree_attn_paged", "hydra_tree_prepare", "hydra_debug_lens_violations"]
 
 
 class HydraError(RuntimeError):
@@ -67,6 +71,8 @@ def load():
                             _i64, _vp, _vp, _i32, _vp, _vp, _sz, _vp, _vp]),
         "hydra_tree_create": (st, [_vp, _vp, _vp, _i32, _vp, _i64, ctypes.POINTER(_vp)]),
         "hydra_tree_destroy": (None, [_vp]),
+        "hydra_tree_prepare": (st, [_vp, _HP]),
+        "hydra_debug_lens_violations": (_i64, [_i32]),
         "hydra_tree_depth": (_i32, [_vp]),
         "hydra_tree_group_size": (_i64, [_vp, _i32]),
         "hydra_tree_workspace_size": (_sz, [_HP, _vp, _i64]),

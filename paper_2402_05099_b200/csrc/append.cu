@@ -20,7 +20,7 @@ __global__ void append_kv_kernel(const uint4 *__restrict__ k_new, const uint4 *_
                                  int64_t bt_stride, int32_t page_shift) {
   const int b = blockIdx.x;
   const int pos = lens[b];
-  if (pos >= S_cap) return;  // uniform across the CTA
+  if (pos >= S_cap || pos < 0) return;  // uniform across the CTA (a full or invalid entry is left unchanged)
   // contiguous: row pos of sequence b; paged (s_sb = page stride): row pos % page_size of
   // page block_table[b][pos / page_size]
   const int64_t row0 = block_table ? (int64_t)block_table[b * bt_stride + (pos >> page_shift)] * s_sb +

@@ -39,18 +39,27 @@ static hydra_status cuda_fail(const char *what) {
   return fail(HYDRA_ECUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
-static std::atomic<int64_t> g_prefix_impl{0}, g_prefix_splits{0}, g_suffix_splits{0}, g_tc_debug{0},
-    g_prefix_stages{3}, g_suffix_unroll{4}, g_prefix_ctas{0}, g_suffix_impl{0}, g_suffix_ctas{0},
-    g_overlap_prefix_ctas{0}, g_prefix_poly{4}, g_prefix_variant{6}, g_prefix_trace{0}, g_suffix_cb{2}, g_suffix_trace{0},
-    g_last_overlap_k{0};  // read-only: prefix CTAs of the last hydra_attn overlap split (0 = sequential)
-// Measurement: cudaEvent_t handles recorded around the prefix (on its stream) and the suffix
-// inside hydra_attn / hydra_attn_paged, so a benchmark can time each kernel within the step
-// (also inside a captured graph); 0 = off.  [0] prefix begin, [1] prefix end, [2] suffix
-// begin, [3] suffix end.
-static std::atomic<int64_t> g_step_ev[4] = {{0}, {0}, {0}, {0}};
+// Settings of the calling thread (hydra_set_config).  Thread-local, so calls made by
+// different threads never see each other's switches or measurement events (hydra.h:
+// "reentrant"); a thread that never calls hydra_set_config runs the automatic choices.
+struct Config {
+  int64_t prefix_impl = 0, prefix_splits = 0, prefix_ctas = 0, prefix_stages = 3, prefix_poly = 4, prefix_variant = 6;
+  int64_t suffix_impl = 0, suffix_splits = 0, suffix_ctas = 0, suffix_unroll = 4, suffix_cb = 2;
+  int64_t overlap_prefix_ctas = 0;
+  // Measurement: cudaEvent_t handles hydra_attn / hydra_attn_paged record around the prefix (on
+  // its stream) and the suffix launches, so a benchmark can time each kernel within the step
+  // (also inside a captured graph); 0 = off.  [0] prefix begin, [1] prefix end, [2] suffix
+  // begin, [3] suffix end.
+  int64_t step_ev[4] = {0, 0, 0, 0};
+  // testing build only (libhydra_test.so): timing experiments, diagnostics, sabotage
+  int64_t tc_debug = 0, prefix_trace = 0, suffix_trace = 0, inject_combine_bug = 0, mutate = 0;
+  int64_t last_overlap_k = 0;  // read-only: prefix CTAs of this thread's last overlap split (0 = sequential)
+};
+static thread_local Config g_cfg;
 static const char *kStepEvKeys[4] = {"ev_prefix_begin", "ev_prefix_end", "ev_suffix_begin", "ev_suffix_end"};
+
 static void record_step_ev(int i, cudaStream_t s) {
-  const int64_t e = g_step_ev[i].load();
+  const int64_t e = g_cfg.step_ev[i];
   // External: under stream capture the record becomes an observable event-record node (an
   // internal record would only be a capture dependency and could not be timed)
   if (!e) return;
@@ -64,62 +73,66 @@ static void record_step_ev(int i, cudaStream_t s) {
   (void)cudaGetLastError();  // a failed measurement record must not surface as a launch error
 }
 
+namespace {
+struct Key {
+  const char *name;
+  int64_t Config::*field;
+  bool testing_only;
+};
+const Key kKeys[] = {
+    {"prefix_impl", &Config::prefix_impl, false},         {"prefix_splits", &Config::prefix_splits, false},
+    {"prefix_ctas", &Config::prefix_ctas, false},         {"prefix_stages", &Config::prefix_stages, false},
+    {"prefix_poly", &Config::prefix_poly, false},         {"prefix_variant", &Config::prefix_variant, false},
+    {"suffix_impl", &Config::suffix_impl, false},         {"suffix_splits", &Config::suffix_splits, false},
+    {"suffix_ctas", &Config::suffix_ctas, false},         {"suffix_unroll", &Config::suffix_unroll, false},
+    {"suffix_cb", &Config::suffix_cb, false},             {"overlap_prefix_ctas", &Config::overlap_prefix_ctas, false},
+    {"tc_debug_variant", &Config::tc_debug, true},        {"prefix_trace", &Config::prefix_trace, true},
+    {"suffix_trace", &Config::suffix_trace, true},        {"inject_combine_bug", &Config::inject_combine_bug, true},
+    {"mutate", &Config::mutate, true},
+};
+}  // namespace
+
 extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
   if (!key) return fail(HYDRA_EINVAL, "null key");
-  if (!strcmp(key, "prefix_impl")) g_prefix_impl = value;
-  else if (!strcmp(key, "prefix_splits")) g_prefix_splits = value;
-  else if (!strcmp(key, "suffix_splits")) g_suffix_splits = value;
-  else if (!strcmp(key, "tc_debug_variant")) g_tc_debug = value;
-  else if (!strcmp(key, "prefix_trace")) g_prefix_trace = value;
-  else if (!strcmp(key, "prefix_ctas")) g_prefix_ctas = value;
-  else if (!strcmp(key, "suffix_impl")) g_suffix_impl = value;
-  else if (!strcmp(key, "suffix_ctas")) g_suffix_ctas = value;
-  else if (!strcmp(key, "overlap_prefix_ctas")) g_overlap_prefix_ctas = value;
-  else if (!strcmp(key, "prefix_poly")) g_prefix_poly = (value == 0 || value == 3 || value == 8 || value == -1) ? value : 4;
-  else if (!strcmp(key, "prefix_variant")) g_prefix_variant = (value == 3 || value == 4 || value == 5) ? value : 6;
-  else if (!strcmp(key, "prefix_stages")) g_prefix_stages = (value == 2 ? 2 : 3);
-  else if (!strcmp(key, "suffix_trace")) g_suffix_trace = value;
-  else if (!strcmp(key, "suffix_cb")) g_suffix_cb = (value == 1 ? 1 : 2);
-  else if (!strcmp(key, "suffix_unroll")) g_suffix_unroll = (value >= 8 ? 8 : value >= 4 ? 4 : 2);
-  else {
-    for (int i = 0; i < 4; ++i)
-      if (!strcmp(key, kStepEvKeys[i])) {
-        g_step_ev[i] = value;
-        return HYDRA_OK;
-      }
-    return fail(HYDRA_EINVAL, "unknown config key '%s'", key);
+  for (int i = 0; i < 4; ++i)
+    if (!strcmp(key, kStepEvKeys[i])) {
+      g_cfg.step_ev[i] = value;
+      return HYDRA_OK;
+    }
+  for (const Key &k : kKeys) {
+    if (strcmp(key, k.name)) continue;
+    if (k.testing_only && !kTesting)
+      return fail(HYDRA_EINVAL, "config key '%s' exists only in the testing build (libhydra_test.so)", key);
+    int64_t v = value;
+    if (!strcmp(key, "prefix_poly")) v = (v == 0 || v == 3 || v == 4 || v == 8 || (kTesting && v == -1)) ? v : 4;
+    if (!strcmp(key, "prefix_variant")) v = (v == 3 || v == 4 || v == 5) ? v : 6;
+    if (!strcmp(key, "prefix_stages")) v = (v == 2 ? 2 : 3);
+    if (!strcmp(key, "suffix_cb")) v = (v == 1 ? 1 : 2);
+    if (!strcmp(key, "suffix_unroll")) v = (v >= 8 ? 8 : v >= 4 ? 4 : 2);
+    g_cfg.*(k.field) = v;
+    return HYDRA_OK;
   }
-  return HYDRA_OK;
+  return fail(HYDRA_EINVAL, "unknown config key '%s'", key);
 }
 
 extern "C" int64_t hydra_get_config(const char *key) {
   if (!key) return -1;
-  if (!strcmp(key, "prefix_impl")) return g_prefix_impl;
-  if (!strcmp(key, "prefix_splits")) return g_prefix_splits;
-  if (!strcmp(key, "suffix_splits")) return g_suffix_splits;
-  if (!strcmp(key, "tc_debug_variant")) return g_tc_debug;
-  if (!strcmp(key, "prefix_trace")) return g_prefix_trace;
-  if (!strcmp(key, "last_overlap_k")) return g_last_overlap_k;
-  if (!strcmp(key, "prefix_stages")) return g_prefix_stages;
-  if (!strcmp(key, "prefix_ctas")) return g_prefix_ctas;
-  if (!strcmp(key, "suffix_impl")) return g_suffix_impl;
-  if (!strcmp(key, "suffix_ctas")) return g_suffix_ctas;
-  if (!strcmp(key, "overlap_prefix_ctas")) return g_overlap_prefix_ctas;
-  if (!strcmp(key, "prefix_poly")) return g_prefix_poly;
-  if (!strcmp(key, "prefix_variant")) return g_prefix_variant;
-  if (!strcmp(key, "suffix_unroll")) return g_suffix_unroll;
-  if (!strcmp(key, "suffix_cb")) return g_suffix_cb;
-  if (!strcmp(key, "suffix_trace")) return g_suffix_trace;
+  if (!strcmp(key, "last_overlap_k")) return g_cfg.last_overlap_k;
+  if (!strcmp(key, "testing_build")) return kTesting ? 1 : 0;
+  for (int i = 0; i < 4; ++i)
+    if (!strcmp(key, kStepEvKeys[i])) return g_cfg.step_ev[i];
+  for (const Key &k : kKeys)
+    if (!strcmp(key, k.name)) return (k.testing_only && !kTesting) ? -1 : g_cfg.*(k.field);
   return -1;
 }
 
 extern "C" const char *hydra_last_error(void) { return g_last_error.c_str(); }
-extern "C" const char *hydra_version(void) { return "hydra-b200 0.1.0 (sm_100a)"; }
-
-static bool inject_combine_bug() {
-  const char *e = getenv("HYDRA_INJECT_COMBINE_BUG");
-  return e && e[0] && strcmp(e, "0") != 0;
+extern "C" const char *hydra_version(void) {
+  return kTesting ? "hydra-b200 0.2.0 (sm_100a, testing build)" : "hydra-b200 0.2.0 (sm_100a)";
 }
+extern "C" int64_t hydra_debug_lens_violations(int32_t reset) { return read_lens_violations(reset != 0); }
+
+static bool inject_combine_bug() { return kTesting && g_cfg.inject_combine_bug != 0; }
 
 // ------------------------------------------------------------------ validation helpers
 static size_t elem_size(hydra_dtype d) { return d == HYDRA_F32 ? 4 : 2; }
@@ -167,8 +180,8 @@ static int heads_per_cta(int g) {
 // (tools/suffix_shapes.py, L2 flushed): g = 8, B = 256, S = 128: 28 vs 66-117 us; g = 4,
 // B = 512: 67 vs 96 us; g = 16: 108 vs 357-410 us; MHA (g = 1): 0.83 vs 0.79 ms at C3.
 static bool use_suffix_tc(const hydra_heads *h, int64_t B, int64_t S_cap, bool overlap = false) {
-  if (g_suffix_impl == 1 || S_cap <= 0 || !suffix_tc_supported(h)) return false;
-  if (g_suffix_impl == 2) return true;
+  if (g_cfg.suffix_impl == 1 || S_cap <= 0 || !suffix_tc_supported(h)) return false;
+  if (g_cfg.suffix_impl == 2) return true;
   const int64_t items = B * h->num_kv_heads, sms = device_sm_count();
   if (overlap) return items >= 2 * sms;
   // (also with fewer items than SMs: 64-128 items of 1-8K-token suffixes, 62-64 us against
@@ -199,7 +212,7 @@ static int suffix_splits(const hydra_heads *h, int64_t B, int64_t S_cap, bool ov
     // 64 x 8 heads x 1024 tokens: 68 vs 60 us) -- the kernel streams ~40 GB/s per SM there,
     // so the extra items' fill / epilogue and the partial combine cost more than the tail.
     if (overlap) return 1;
-    if (g_suffix_splits > 0) return (int)std::min<int64_t>(g_suffix_splits, std::max<int64_t>(1, (S_cap + 127) / 128));
+    if (g_cfg.suffix_splits > 0) return (int)std::min<int64_t>(g_cfg.suffix_splits, std::max<int64_t>(1, (S_cap + 127) / 128));
     // Very few items (< SMs / 4, e.g. 4 sequences x 8 KV heads): split into one wave of
     // items x splits <= SMs (32 items x 16K tokens: 64.5 us with 4 splits, 74 with 5 = two
     // waves, 91 unsplit); at 64+ items the split measured slower.
@@ -207,7 +220,7 @@ static int suffix_splits(const hydra_heads *h, int64_t B, int64_t S_cap, bool ov
     if (items * 4 >= sms) return 1;
     return (int)std::max<int64_t>(1, std::min<int64_t>({sms / items, S_cap / 512, 16}));  // one wave
   }
-  if (g_suffix_splits > 0) return (int)std::min<int64_t>(g_suffix_splits, std::max<int64_t>(1, S_cap));
+  if (g_cfg.suffix_splits > 0) return (int)std::min<int64_t>(g_cfg.suffix_splits, std::max<int64_t>(1, S_cap));
   if (S_cap <= 0) return 1;
   const int g = h->num_q_heads / h->num_kv_heads;
   const int64_t items = B * h->num_kv_heads * (g / heads_per_cta(g));
@@ -223,16 +236,16 @@ static int suffix_splits(const hydra_heads *h, int64_t B, int64_t S_cap, bool ov
 // Prefix kernel choice: the persistent two-tile tcgen05 kernel (v3) by default; the
 // one-tile tcgen05 kernel (v1) or the SIMT kernel on request / for unsupported shapes.
 enum PrefixKind { PK_SIMT = 1, PK_TC1 = 2, PK_TC2 = 3 };
-static int prefix_ctas() { return g_prefix_ctas > 0 ? (int)g_prefix_ctas : device_sm_count(); }
-static int prefix_bn() { return g_prefix_variant == 4 ? 64 : 128; }  // KV tokens per persistent-kernel block
+static int prefix_ctas() { return g_cfg.prefix_ctas > 0 ? (int)g_cfg.prefix_ctas : device_sm_count(); }
+static int prefix_bn() { return g_cfg.prefix_variant == 4 ? 64 : 128; }  // KV tokens per persistent-kernel block
 // B/P-dependent choice (rows = stacked query rows per KV head, P = KV tokens per row):
 // the persistent kernel amortises its per-segment Q load / epilogue only when every CTA
 // owns enough 128-token blocks; small problems run the one-tile kernel (more parallelism).
 // ctas: the persistent kernel's CTA count (0 = all SMs, or the prefix_ctas override).
 static PrefixKind prefix_kind(const hydra_heads *h, int64_t rows = -1, int64_t P = -1, int ctas = 0) {
-  if (g_prefix_impl == 1 || !prefix_tc_supported(h)) return PK_SIMT;
-  if (g_prefix_impl == 2) return PK_TC1;
-  if (g_prefix_impl == 3 || rows < 0) return PK_TC2;
+  if (g_cfg.prefix_impl == 1 || !prefix_tc_supported(h)) return PK_SIMT;
+  if (g_cfg.prefix_impl == 2) return PK_TC1;
+  if (g_cfg.prefix_impl == 3 || rows < 0) return PK_TC2;
   // Persistent kernel when each CTA owns enough 256-row x 128-token blocks to amortise its
   // pipeline fill: 24 on an SM share (the overlap split needs the persistent kernel), 40 on
   // the full chip (tools/prefix_shapes.py: C6 at 34 blocks per CTA, one-tile kernel 104 us vs
@@ -245,7 +258,7 @@ static bool use_tc(const hydra_heads *h) { return prefix_kind(h) != PK_SIMT; }
 // Splits of the tensor-core prefix kernel: minimise (waves x blocks per CTA) plus the
 // HBM cost of writing/reading the extra fp32 partials, in units of one KV block.
 static int prefix_splits_tc(int64_t tiles, int64_t P) {
-  if (g_prefix_splits > 0) return (int)g_prefix_splits;
+  if (g_cfg.prefix_splits > 0) return (int)g_cfg.prefix_splits;
   const int64_t nblk = (P + 127) / 128;
   if (nblk <= 1) return 1;
   const int64_t sms = device_sm_count();
@@ -265,7 +278,7 @@ static int prefix_splits_tc(int64_t tiles, int64_t P) {
 }
 
 static int prefix_splits_simt(const hydra_heads *h, int64_t B, int64_t P) {
-  if (g_prefix_splits > 0) return (int)g_prefix_splits;
+  if (g_cfg.prefix_splits > 0) return (int)g_cfg.prefix_splits;
   if (P <= 0) return 1;
   const int g = h->num_q_heads / h->num_kv_heads;
   const int64_t items = B * h->num_kv_heads * (g / heads_per_cta(g));
@@ -304,7 +317,7 @@ static int overlap_prefix_ctas(const hydra_heads *h, int64_t B, int64_t P, int64
   const int g = h->num_q_heads / h->num_kv_heads;
   if (prefix_kind(h, B * g, P, 8) != PK_TC2) return 0;  // not even 8 persistent CTAs' worth of blocks
   const int sms = device_sm_count();
-  if (g_overlap_prefix_ctas > 0) return (int)std::min<int64_t>(g_overlap_prefix_ctas, sms - 1);
+  if (g_cfg.overlap_prefix_ctas > 0) return (int)std::min<int64_t>(g_cfg.overlap_prefix_ctas, sms - 1);
   // R_P derated from 0.46 (full clock) for the ~1.45-1.7 GHz the 1 kW cap holds the SMs at in a
   // sustained overlapped step: the tensor-bound prefix slows with the clock, the HBM-bound
   // suffix does not (tools/power_profile.py, tools/overlap_sustained.py)
@@ -380,11 +393,12 @@ static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, i
     a.lse = dst.lse;
     a.o_slot_stride = dst.o_stride;
     a.lse_slot_stride = dst.lse_stride;
-    a.debug_variant = (int32_t)g_tc_debug;
-    a.trace = reinterpret_cast<void *>((intptr_t)g_prefix_trace.load());
-    a.stages = (int32_t)g_prefix_stages;
-    a.poly_every = (int32_t)g_prefix_poly;
-    a.variant = (int32_t)g_prefix_variant;
+    a.debug_variant = (int32_t)g_cfg.tc_debug;
+    a.trace = reinterpret_cast<void *>((intptr_t)g_cfg.prefix_trace);
+    a.stages = (int32_t)g_cfg.prefix_stages;
+    a.poly_every = (int32_t)g_cfg.prefix_poly;
+    a.variant = (int32_t)g_cfg.prefix_variant;
+    a.mutate = (int32_t)g_cfg.mutate;
     hydra_status st;
     if (kind == PK_TC2) {
       // stream-K pieces leave some slots of a row unwritten: mark every slot empty first
@@ -428,6 +442,7 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
                                int64_t S_cap, const int32_t *lens, int splits, const PartsView &dst,
                                cudaStream_t s, int tc_ctas = 0, const hydra_paging *pg = nullptr) {
   const int g = h->num_q_heads / h->num_kv_heads;
+  if (kTesting && launch_lens_check(lens, B, S_cap, s) != HYDRA_OK) return cuda_fail("lens check");
   if (use_suffix_tc(h, B, S_cap, tc_ctas > 0)) {
     SuffixTcArgs a{};
     a.q = q;
@@ -446,9 +461,10 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
     a.scale_log2 = scale_of(h) * 1.4426950408889634f;
     a.o = dst.o;
     a.lse = dst.lse;
-    a.cb = (int32_t)g_suffix_cb;
-    a.trace = reinterpret_cast<void *>((intptr_t)g_suffix_trace.load());
-    a.debug = (int32_t)g_tc_debug;
+    a.cb = (int32_t)g_cfg.suffix_cb;
+    a.trace = reinterpret_cast<void *>((intptr_t)g_cfg.suffix_trace);
+    a.debug = (int32_t)g_cfg.tc_debug;
+    a.mutate = (int32_t)g_cfg.mutate;
     a.n_split = splits;
     a.split_len = (int32_t)(((S_cap + splits - 1) / splits + 127) / 128 * 128);
     a.o_split_stride = dst.o_stride;
@@ -459,7 +475,7 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
       a.n_pages = pg->n_pages;
       a.page_size = pg->page_size;
     }
-    const int ctas = tc_ctas > 0 ? tc_ctas : (g_suffix_ctas > 0 ? (int)g_suffix_ctas : device_sm_count());
+    const int ctas = tc_ctas > 0 ? tc_ctas : (g_cfg.suffix_ctas > 0 ? (int)g_cfg.suffix_ctas : device_sm_count());
     hydra_status st = launch_suffix_tc(a, ctas, s);
     return st == HYDRA_OK ? st : cuda_fail("suffix tcgen05 launch");
   }
@@ -473,6 +489,7 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
   p.kv_st = s_st;
   p.kv_sh = s_sh;
   p.lens = lens;
+  p.len_cap = S_cap;
   p.len_uniform = 0;
   p.n_seq = (int32_t)B;
   p.Hq = h->num_q_heads;
@@ -482,7 +499,7 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
   p.n_splits = splits;
   p.split_len = (S_cap + splits - 1) / splits;
   p.heads_per_cta = heads_per_cta(g);
-  p.unroll = (int32_t)g_suffix_unroll;
+  p.unroll = (int32_t)g_cfg.suffix_unroll;
   p.o = dst.o;
   p.lse = dst.lse;
   p.o_split_stride = dst.o_stride;
@@ -516,10 +533,11 @@ static hydra_status run_combine(int64_t rows, int d, int n, const PartsView &src
 // ------------------------------------------------------------------ workspace
 extern "C" size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, int64_t P, int64_t S_cap,
                                        int32_t n_parts) {
-  (void)n_parts;
   if (check_heads(h) != HYDRA_OK || B <= 0) return 0;
   const size_t pb = part_bytes(h, B);
   switch (op) {
+    case HYDRA_OP_PARTS:  // caller-staged partials for hydra_combine: n_parts x (O f32 [B,Hq,d] + LSE f32 [B,Hq])
+      return n_parts > 0 ? pb * (size_t)n_parts : 0;
     case HYDRA_OP_PREFIX: {
       const int s = prefix_splits(h, B, P);
       return s > 1 ? pb * s : 0;
@@ -702,8 +720,7 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
   // Without an SM split (k = 0) two full grids would only contend: run sequentially.
   const int k_over = (sa != s) ? overlap_prefix_ctas(h, B, P, S_cap) : 0;
   if (k_over == 0) sa = s;
-  g_last_overlap_k = k_over;
-  if (getenv("HYDRA_DEBUG_OVERLAP")) fprintf(stderr, "hydra_attn: overlap prefix CTAs k=%d (aux stream %s)\n", k_over, s_aux ? "given" : "none");
+  g_cfg.last_overlap_k = k_over;
   const int sms = device_sm_count();
   const int np = prefix_splits(h, B, P, k_over), ns = suffix_splits(h, B, S_cap, k_over > 0);
   const size_t need = part_bytes(h, B) * (np + ns);
@@ -817,8 +834,16 @@ struct hydra_tree {
   std::vector<int32_t> grp_off, grp_seq;  // CSR: sequences of node n = grp_seq[grp_off[n]..grp_off[n+1])
   int32_t max_depth = 0;                  // nodes on the longest root->leaf path
   int32_t *d_grp_seq = nullptr;           // device copy of grp_seq
+  // Work lists of the tensor-core node attention, built by hydra_tree_prepare (off the hot
+  // path) per query-group size g: [0] 128-row tiles (one-tile kernel), [1] 256-row tile
+  // pairs (persistent kernel).  A task stores its node's depth, not a slot, so the lists do
+  // not depend on the KV split count.
+  struct Lists {
+    PrefixTask *d[2] = {nullptr, nullptr};
+    int n[2] = {0, 0};
+  };
   mutable std::mutex mu;
-  mutable std::map<std::pair<int, int>, std::pair<PrefixTask *, int>> work;  // (g, splits) -> device tasks
+  std::map<int, Lists> work;  // g -> lists
 };
 
 extern "C" hydra_status hydra_tree_create(const int32_t *parent, const int64_t *node_off, const int64_t *node_len,
@@ -907,7 +932,8 @@ extern "C" hydra_status hydra_tree_create(const int32_t *parent, const int64_t *
 
 extern "C" void hydra_tree_destroy(struct hydra_tree *t) {
   if (!t) return;
-  for (auto &kv : t->work) cudaFree(kv.second.first);
+  for (auto &kv : t->work)
+    for (int k = 0; k < 2; ++k) cudaFree(kv.second.d[k]);
   cudaFree(t->d_grp_seq);
   delete t;
 }
@@ -919,8 +945,45 @@ extern "C" int64_t hydra_tree_group_size(const struct hydra_tree *t, int32_t nod
   return t->grp_off[node + 1] - t->grp_off[node];
 }
 
+// Builds and uploads the node-attention work lists for query groups of g rows per
+// sequence (synchronous; the only device allocation of the tree path).
+static hydra_status tree_prepare_g(const hydra_tree *t, int g) {
+  std::lock_guard<std::mutex> lock(t->mu);
+  if (t->work.count(g)) return HYDRA_OK;
+  hydra_tree::Lists L;
+  for (int k = 0; k < 2; ++k) {
+    const int rows_per_task = k ? 256 : 128;
+    std::vector<PrefixTask> tasks;
+    for (int n = 0; n < t->n_nodes; ++n) {
+      if (t->node_len[n] <= 0) continue;
+      const int32_t ns_ = t->grp_off[n + 1] - t->grp_off[n];
+      const int tiles = (int)(((int64_t)ns_ * g + rows_per_task - 1) / rows_per_task);
+      for (int tl = 0; tl < tiles; ++tl)
+        tasks.push_back(PrefixTask{t->node_off[n], t->node_len[n], t->grp_off[n], ns_, t->depth[n], tl});
+    }
+    L.n[k] = (int)tasks.size();
+    if (tasks.empty()) continue;
+    if (cudaMalloc(&L.d[k], sizeof(PrefixTask) * tasks.size()) != cudaSuccess ||
+        cudaMemcpy(L.d[k], tasks.data(), sizeof(PrefixTask) * tasks.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+      hydra_status st = cuda_fail("tree work-list upload");
+      cudaFree(L.d[0]);
+      cudaFree(L.d[1]);
+      return st;
+    }
+  }
+  const_cast<hydra_tree *>(t)->work.emplace(g, L);
+  return HYDRA_OK;
+}
+
+extern "C" hydra_status hydra_tree_prepare(struct hydra_tree *t, const hydra_heads *h) {
+  if (!t) return fail(HYDRA_EINVAL, "tree is NULL");
+  hydra_status st = check_heads(h);
+  if (st) return st;
+  return tree_prepare_g(t, h->num_q_heads / h->num_kv_heads);
+}
+
 static int tree_prefix_splits(const hydra_heads *h, const hydra_tree *t) {
-  if (g_prefix_splits > 0) return (int)g_prefix_splits;
+  if (g_cfg.prefix_splits > 0) return (int)g_cfg.prefix_splits;
   if (!use_tc(h)) {
     int64_t maxlen = 0;
     for (auto L : t->node_len) maxlen = std::max(maxlen, L);
@@ -945,7 +1008,7 @@ static int tree_prefix_splits(const hydra_heads *h, const hydra_tree *t) {
 static int tree_overlap_ctas(const hydra_heads *h, const struct hydra_tree *t, int64_t S_cap) {
   if (S_cap <= 0 || !use_suffix_tc(h, t->B, S_cap, true) || prefix_kind(h) != PK_TC2) return 0;
   const int sms = device_sm_count();
-  if (g_overlap_prefix_ctas > 0) return (int)std::min<int64_t>(g_overlap_prefix_ctas, sms - 1);
+  if (g_cfg.overlap_prefix_ctas > 0) return (int)std::min<int64_t>(g_cfg.overlap_prefix_ctas, sms - 1);
   const int g = h->num_q_heads / h->num_kv_heads;
   double units = 0.0;
   for (int n = 0; n < t->n_nodes; ++n) {
@@ -1001,7 +1064,7 @@ static hydra_status tree_impl(const hydra_heads *h, const struct hydra_tree *t, 
   cudaStream_t sa = stream_aux ? reinterpret_cast<cudaStream_t>(stream_aux) : s;
   const int k_over = (sa != s && T > 0) ? tree_overlap_ctas(h, t, S_cap) : 0;
   if (k_over == 0) sa = s;
-  g_last_overlap_k = k_over;
+  g_cfg.last_overlap_k = k_over;
   const int sms = device_sm_count();
   const int np = tree_prefix_splits(h, t);
   const int ns = suffix_splits(h, B, S_cap, k_over > 0);
@@ -1011,6 +1074,30 @@ static hydra_status tree_impl(const hydra_heads *h, const struct hydra_tree *t, 
   const int g = h->num_q_heads / h->num_kv_heads;
   const int64_t rows = B * h->num_q_heads;
   PartsView all = parts_in_ws(ws, h, B, n_parts);
+  const PrefixKind kind = prefix_kind(h);
+  // the node-attention work list (looked up before anything is launched)
+  PrefixTask *d_tasks = nullptr;
+  int n_tasks = 0;
+  if (kind != PK_SIMT && T > 0) {
+    std::unique_lock<std::mutex> lock(t->mu);
+    auto it = t->work.find(g);
+    if (it == t->work.end()) {
+      lock.unlock();
+      // Not prepared for this head grouping: build the lists now unless the stream is being
+      // captured (an upload cannot be part of a graph) -- hydra_tree_prepare avoids this.
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      cudaStreamIsCapturing(s, &cs);
+      if (cs != cudaStreamCaptureStatusNone)
+        return fail(HYDRA_EINVAL, "tree not prepared for Hq/Hkv = %d: call hydra_tree_prepare before capture", g);
+      st = tree_prepare_g(t, g);
+      if (st) return st;
+      lock.lock();
+      it = t->work.find(g);
+    }
+    const int k = kind == PK_TC2 ? 1 : 0;
+    d_tasks = it->second.d[k];
+    n_tasks = it->second.n[k];
+  }
   // Sequences whose path is shorter than max_depth leave slots empty: mark all node slots -inf.
   st = launch_fill_neg_inf(all.lse, all.lse_stride * (int64_t)(t->max_depth * np), s);
   if (st) return cuda_fail("fill");
@@ -1020,43 +1107,7 @@ static hydra_status tree_impl(const hydra_heads *h, const struct hydra_tree *t, 
   }
   const float sl2 = scale_of(h) * 1.4426950408889634f;
 
-  const PrefixKind kind = prefix_kind(h);
   if (kind != PK_SIMT && T > 0) {
-    PrefixTask *d_tasks = nullptr;
-    int n_tasks = 0;
-    const int rows_per_task = kind == PK_TC2 ? 256 : 128;  // tile pairs for v3
-    {
-      std::lock_guard<std::mutex> lock(t->mu);
-      auto it = t->work.find({g * 4 + (int)kind, np});
-      if (it == t->work.end()) {
-        std::vector<PrefixTask> tasks;
-        for (int n = 0; n < t->n_nodes; ++n) {
-          if (t->node_len[n] <= 0) continue;
-          const int32_t ns_ = t->grp_off[n + 1] - t->grp_off[n];
-          const int tiles = (int)(((int64_t)ns_ * g + rows_per_task - 1) / rows_per_task);
-          for (int tl = 0; tl < tiles; ++tl)
-            tasks.push_back(PrefixTask{t->node_off[n], t->node_len[n], t->grp_off[n], ns_, t->depth[n] * np, tl});
-        }
-        PrefixTask *dt = nullptr;
-        if (!tasks.empty()) {
-          if (cudaMalloc(&dt, sizeof(PrefixTask) * tasks.size()) != cudaSuccess ||
-              cudaMemcpy(dt, tasks.data(), sizeof(PrefixTask) * tasks.size(), cudaMemcpyHostToDevice) != cudaSuccess)
-            return cuda_fail("tree work-list upload");
-        }
-        it = t->work.emplace(std::make_pair(g * 4 + (int)kind, np), std::make_pair(dt, (int)tasks.size())).first;
-      }
-      d_tasks = it->second.first;
-      n_tasks = it->second.second;
-    }
-    if (getenv("HYDRA_DEBUG_TREE")) {
-      std::vector<PrefixTask> hv(n_tasks);
-      cudaMemcpy(hv.data(), d_tasks, sizeof(PrefixTask) * n_tasks, cudaMemcpyDeviceToHost);
-      fprintf(stderr, "[hydra] tree kind=%d g=%d np=%d n_tasks=%d sizeof(task)=%zu\n", (int)kind, g, np, n_tasks,
-              sizeof(PrefixTask));
-      for (auto &x : hv)
-        fprintf(stderr, "  task kv_off=%lld kv_len=%lld seq_off=%d n_seq=%d slot=%d tile=%d\n", (long long)x.kv_off,
-                (long long)x.kv_len, x.seq_off, x.n_seq, x.slot, x.tile);
-    }
     if (n_tasks > 0) {
       PrefixTcArgs a{};
       a.q = q;
@@ -1079,11 +1130,12 @@ static hydra_status tree_impl(const hydra_heads *h, const struct hydra_tree *t, 
       a.lse = all.lse;
       a.o_slot_stride = all.o_stride;
       a.lse_slot_stride = all.lse_stride;
-      a.debug_variant = (int32_t)g_tc_debug;
-      a.trace = reinterpret_cast<void *>((intptr_t)g_prefix_trace.load());
-      a.stages = (int32_t)g_prefix_stages;
-    a.poly_every = (int32_t)g_prefix_poly;
-    a.variant = (int32_t)g_prefix_variant;
+      a.debug_variant = (int32_t)g_cfg.tc_debug;
+      a.trace = reinterpret_cast<void *>((intptr_t)g_cfg.prefix_trace);
+      a.stages = (int32_t)g_cfg.prefix_stages;
+      a.poly_every = (int32_t)g_cfg.prefix_poly;
+      a.variant = (int32_t)g_cfg.prefix_variant;
+      a.mutate = (int32_t)g_cfg.mutate;
       // the work list holds 256-row tile pairs for v3 and 128-row tiles for v1
       st = kind == PK_TC2 ? launch_prefix_tc2(a, k_over > 0 ? k_over : prefix_ctas(), sa) : launch_prefix_tc(a, sa);
       if (st) return cuda_fail("tree prefix tcgen05 launch");

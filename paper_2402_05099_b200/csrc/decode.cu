@@ -42,7 +42,8 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeParams p) 
   const int b = p.seq_map ? p.seq_map[slot] : slot;
   const int h0 = j * p.g + chunk * GQ;
 
-  const int64_t len = p.lens ? (int64_t)p.lens[b] : p.len_uniform;
+  // out-of-range lens[b] (a documented precondition violation) is clamped to [0, len_cap]
+  const int64_t len = p.lens ? min(max((int64_t)p.lens[b], (int64_t)0), p.len_cap) : p.len_uniform;
   const int64_t t_begin = (int64_t)split * p.split_len;
   const int64_t t_end = min(len, t_begin + p.split_len);
 

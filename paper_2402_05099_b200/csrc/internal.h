@@ -7,6 +7,27 @@
 
 namespace hydra {
 
+// Testing build (-DHYDRA_TESTING, libhydra_test.so): diagnostics (CTA timestamps), timing
+// experiments that produce invalid results, and the parity suite's sabotage switches.  The
+// release library compiles none of them: every use is guarded by this constant.
+#ifdef HYDRA_TESTING
+constexpr bool kTesting = true;
+#else
+constexpr bool kTesting = false;
+#endif
+
+// ---------------------------------------------------------------- host helpers (hostutil.cu)
+bool tensor_maps_available();
+// bf16 TMA tensor map, 128-B swizzle, dims innermost first; strides (bytes) of dims 1..rank-1.
+bool encode_bf16_map(void *map, int rank, const void *base, const uint64_t *dims, const uint64_t *strides_bytes,
+                     const uint32_t *box);
+// cudaFuncAttributeMaxDynamicSharedMemorySize for `func` on the current device (cached per device).
+cudaError_t ensure_smem_attr(const void *func, int bytes);
+int device_sm_count();
+// Testing build: count lens[b] outside [0, S_cap] on the device (no-op in release).
+hydra_status launch_lens_check(const int32_t *lens, int64_t B, int64_t S_cap, cudaStream_t s);
+int64_t read_lens_violations(bool reset);
+
 // ---------------------------------------------------------------- SIMT decode kernel
 // One CTA = one (sequence-slot b, KV head j, head chunk, KV split).  Used for the
 // suffix (§3.2), the fp32 reference-mode prefix / tree nodes, and odd shapes.
@@ -17,6 +38,7 @@ struct DecodeParams {
   int64_t kv_sb, kv_st, kv_sh;  // kv_sb == 0: every sequence reads the same KV (shared prefix)
   int64_t kv_tok_off;           // token offset added to every position (tree node offset)
   const int32_t *lens;          // device [n_seq]; nullptr -> len_uniform for every sequence
+  int64_t len_cap;              // lens[b] is clamped to [0, len_cap] (hydra.h precondition)
   int64_t len_uniform;
   const int32_t *seq_map;       // device [n_seq] slot -> sequence id; nullptr -> identity
   int32_t n_seq, Hq, Hkv, g;
@@ -63,7 +85,7 @@ struct PrefixTask {
   int64_t kv_len;    // tokens in the segment
   int32_t seq_off;   // offset into the sequence list
   int32_t n_seq;     // sequences in the group
-  int32_t slot;      // output slot (tree depth * splits); split index is added
+  int32_t depth;     // tree depth of the segment: its partials go to slot depth * n_splits + split
   int32_t tile;      // query tile index within the group (128 stacked rows each)
 };
 
@@ -87,6 +109,7 @@ struct PrefixTcArgs {
   int64_t o_slot_stride, lse_slot_stride;
   int32_t debug_variant;
   void *trace = nullptr;  // diagnostics only (config key prefix_trace): device buffer for CTA-0 timestamps
+  int32_t mutate = 0;     // testing build only: parity-suite mutation (prefix_tc2 epilogue store skip)
   int32_t poly_every = 0;  // v3: every k-th exp2 column pair on the FMA pipe (0 = all MUFU)
   int32_t variant = 3;     // persistent kernel: 3 (128-token blocks) or 4 (64-token, double-buffered S)
   int32_t stages;  // K/V pipeline stages: 2 (160 KB smem, leaves room for co-resident suffix CTAs) or 3
@@ -110,7 +133,8 @@ struct SuffixTcArgs {
   float *o, *lse;  // [B, Hq, 128], [B, Hq]
   int32_t cb;      // 128-token blocks per softmax round (1 or 2)
   void *trace;     // diagnostics (suffix_trace config key); null = off
-  int32_t debug;   // tc_debug_variant (timing experiments only)
+  int32_t debug;   // tc_debug_variant (timing experiments only, testing build)
+  int32_t mutate;  // testing build only: 2 = CTA 0's epilogue skips head 0's store of its first item
   // paged cache (block_table != nullptr): k/v are page pools [n_pages, page_size, Hkv, 128]
   // with s_sb = page stride; S_cap = bt_stride * page_size
   const int32_t *block_table;
@@ -124,7 +148,6 @@ struct SuffixTcArgs {
 };
 bool suffix_tc_supported(const hydra_heads *h);
 hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s);
-int device_sm_count();
 hydra_status launch_append_kv(const void *k_new, const void *v_new, int64_t nb, int64_t nh, void *sk, void *sv,
                               int64_t s_sb, int64_t s_st, int64_t s_sh, int64_t S_cap, int32_t Hkv, int32_t d,
                               size_t es, int64_t B, int32_t *lens, cudaStream_t s,

@@ -26,7 +26,6 @@
 #include <cudaTypedefs.h>
 
 #include <cstring>
-#include <mutex>
 
 #include "common.cuh"
 #include "internal.h"
@@ -98,7 +97,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) prefix_tc_kernel(const __grid
     task.kv_len = P.P;
     task.seq_off = 0;
     task.n_seq = P.B;
-    task.slot = 0;
+    task.depth = 0;
     task.tile = blockIdx.x;
   }
   const int64_t n_rows = (int64_t)task.n_seq * P.g;
@@ -107,7 +106,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) prefix_tc_kernel(const __grid
   const int per_split = (nblk_total + P.n_splits - 1) / P.n_splits;
   const int blk_begin = split * per_split;
   const int nblk = max(0, min(nblk_total, blk_begin + per_split) - blk_begin);
-  const int out_slot = task.slot + split;
+  const int out_slot = task.depth * P.n_splits + split;
 
   if (nblk == 0) {  // empty KV range for this split: the (0, -inf) sentinel
     if (warp >= 2) {
@@ -222,7 +221,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) prefix_tc_kernel(const __grid
             // B = V tile, MN-major: 16 tokens per step = 2 groups of 8 rows (SBO 1024 B);
             // the two 64-dim panels are LBO = 16 KB apart.  A = P in TMEM: 16 bf16 per row
             // = 8 packed 32-bit columns per step.
-            const uint64_t vdesc = (P.debug_variant & 1)
+            const uint64_t vdesc = (kTesting && (P.debug_variant & 1))
                                        ? ptx::smem_desc_sw128(v_addr + kk * 2048, 1024, PANEL)
                                        : ptx::smem_desc_sw128(v_addr + kk * 2048, PANEL, 1024);
             ptx::mma_ts(tmem + COL_O, p_tmem + kk * 8, vdesc, idesc_pv, (m > 0 || kk > 0));
@@ -369,43 +368,20 @@ __global__ void __launch_bounds__(tc::kThreads, 1) prefix_tc_kernel(const __grid
 }
 
 // ------------------------------------------------------------------ host side
-static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void *p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  });
-  return fn;
-}
-
 static bool make_kv_map(CUtensorMap *m, const void *base, int64_t T, int Hkv, int64_t st, int64_t sh) {
-  auto fn = encode_fn();
-  if (!fn) return false;
-  const cuuint64_t dims[3] = {(cuuint64_t)tc::HD, (cuuint64_t)Hkv, (cuuint64_t)T};
-  const cuuint64_t strides[2] = {(cuuint64_t)sh * 2, (cuuint64_t)st * 2};
-  const cuuint32_t box[3] = {64, 1, (cuuint32_t)tc::BN};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  const uint64_t dims[3] = {(uint64_t)tc::HD, (uint64_t)Hkv, (uint64_t)T};
+  const uint64_t strides[2] = {(uint64_t)sh * 2, (uint64_t)st * 2};
+  const uint32_t box[3] = {64, 1, (uint32_t)tc::BN};
+  return encode_bf16_map(m, 3, base, dims, strides, box);
 }
 
 bool prefix_tc_supported(const hydra_heads *h) {
-  return h->dtype == HYDRA_BF16 && h->head_dim == 128 && encode_fn() != nullptr;
+  return h->dtype == HYDRA_BF16 && h->head_dim == 128 && tensor_maps_available();
 }
 
 template <int NS>
 static cudaError_t set_smem_attr() {
-  static std::once_flag once;
-  static cudaError_t err = cudaSuccess;
-  std::call_once(once, [] {
-    err = cudaFuncSetAttribute(prefix_tc_kernel<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::Smem<NS>::ALLOC);
-  });
-  return err;
+  return ensure_smem_attr(reinterpret_cast<const void *>(prefix_tc_kernel<NS>), tc::Smem<NS>::ALLOC);
 }
 
 hydra_status launch_prefix_tc(const PrefixTcArgs &a, cudaStream_t s) {
@@ -442,12 +418,6 @@ hydra_status launch_prefix_tc(const PrefixTcArgs &a, cudaStream_t s) {
   else
     prefix_tc_kernel<3><<<grid, tc::kThreads, tc::Smem<3>::ALLOC, s>>>(P);
   return cudaGetLastError() == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
-}
-
-int device_sm_count() {
-  int dev = 0, n = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n;
 }
 
 }  // namespace hydra

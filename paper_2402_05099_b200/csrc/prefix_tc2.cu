@@ -31,7 +31,6 @@
 
 #include <algorithm>
 #include <cstring>
-#include <mutex>
 
 #include "common.cuh"
 #include "internal.h"
@@ -86,6 +85,7 @@ struct __align__(64) PrefixTc2Params {
   int32_t bn;            // KV tokens per block (128: v3, 64: v4)
   int32_t debug;         // timing experiments only (invalid results): bit 1 no softmax math, bit 2 no K/V TMA
   long long *trace;      // diagnostics: CTA 0 event timestamps (clock64), see tools/prefix_trace.py; null = off
+  int32_t mutate;        // testing build only: 1 = CTA 0 skips one 4-row store group of its epilogues
   float *o, *lse;
   int64_t o_slot_stride, lse_slot_stride;
 };
@@ -143,7 +143,7 @@ __device__ __forceinline__ bool seg_next(const PrefixTc2Params &P, SegIter &s, I
     it.n_rows = (int64_t)task.n_seq * P.g;
     it.row0 = (int64_t)task.tile * (2 * tc2::BM);
     it.seq_off = task.seq_off;
-    it.slot = task.slot + split;
+    it.slot = task.depth * P.n_splits + split;
     const int nblk_total = (int)((task.kv_len + P.bn - 1) / P.bn);
     const int per_split = (nblk_total + P.n_splits - 1) / P.n_splits;
     it.blk_begin = split * per_split;
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + N_BARS);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // diagnostics: every CTA's globaltimer at entry / setup done / first S / last P / exit
-  long long *cta_tr = (P.trace && blockIdx.x < 256) ? P.trace + 14 * kTraceN + blockIdx.x * 8 : nullptr;
+  long long *cta_tr = (kTesting && P.trace && blockIdx.x < 256) ? P.trace + 14 * kTraceN + blockIdx.x * 8 : nullptr;
   if (cta_tr && threadIdx.x == 0) cta_tr[0] = (long long)gtimer();
 
   if (warp == 0 && lane == 0) {
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
           const int t0 = (int)(it.kv_off + (int64_t)(it.blk_begin + n) * BN);
           uint8_t *sK = smem + OFF_K + st * TILE;
           uint8_t *sV = smem + OFF_V + st * TILE;
-          if ((P.debug & 4) && gb >= (uint32_t)NS) {  // timing experiment only: no K/V traffic after the fill
+          if (kTesting && (P.debug & 4) && gb >= (uint32_t)NS) {  // timing experiment only: no K/V traffic after the fill
             ptx::mbar_wait(&k_empty[st], ph ^ 1);
             ptx::mbar_arrive(&k_full[st]);
             ptx::mbar_wait(&v_empty[st], ph ^ 1);
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
       constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BM, BN, false);  // S = Q K^T (both K-major)
       constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(BM, HD, true);  // O += P V (V MN-major)
       uint32_t gb = 0, qc[2] = {0, 0}, pc[2] = {0, 0}, oc[2] = {0, 0};
-      long long *tr = (P.trace && blockIdx.x == 0) ? P.trace : nullptr;
+      long long *tr = (kTesting && P.trace && blockIdx.x == 0) ? P.trace : nullptr;
       SegIter si;
       seg_begin(P, si);
       Item it;
@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
     uint8_t *sQ = smem + OFF_Q + t * TILE;
     const float c2 = P.scale_log2;
     uint32_t sc = 0, pvc = 0;  // phase counters of s_full[t] / pv_done[t]
-    long long *tr = (P.trace && blockIdx.x == 0 && quarter == 0 && lane == 0) ? P.trace : nullptr;
+    long long *tr = (kTesting && P.trace && blockIdx.x == 0 && quarter == 0 && lane == 0) ? P.trace : nullptr;
     SegIter si;
     seg_begin(P, si);
     Item it;
@@ -401,7 +401,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
         if (cta_tr && sc == 0 && t == 0 && quarter == 0 && lane == 0) cta_tr[2] = (long long)gtimer();
         ++sc;
         ptx::tc_fence_after();
-        if (P.debug & 2) {  // timing experiment only: MMA pipeline without the softmax math
+        if (kTesting && (P.debug & 2)) {  // timing experiment only: MMA pipeline without the softmax math
           if (n >= 1) {
             ptx::mbar_wait(&pv_done[t], pvc & 1);
             ++pvc;
@@ -423,10 +423,10 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
             ptx::unpack2(ptx::fma2(ptx::pack2(__uint_as_float(src[2 * i]), __uint_as_float(src[2 * i + 1])), cc, nm),
                          x0, x1);
             float p0, p1;
-            if (kPolyEvery < 0) {  // timing experiment only: no exp at all (wrong results)
+            if (kTesting && kPolyEvery < 0) {  // timing experiment only (testing build): no exp at all (wrong results)
               p0 = x0 * 0.01f;
               p1 = x1 * 0.01f;
-            } else if (kPolyEvery > 0 && (i % kPolyEvery) == kPolyEvery - 1) {
+            } else if (kPolyEvery > 0 && (i % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1) {
               ptx::exp2_poly2(x0, x1, p0, p1);  // FMA-pipe exp2 for 1/kPolyEvery of the pairs
             } else {
               p0 = fast_exp2(x0);
@@ -597,7 +597,9 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
           v.y = __uint_as_float(stage[rw * 32 + ((cg * 4 + 1) ^ rw)]);
           v.z = __uint_as_float(stage[rw * 32 + ((cg * 4 + 2) ^ rw)]);
           v.w = __uint_as_float(stage[rw * 32 + ((cg * 4 + 3) ^ rw)]);
-          if (base) reinterpret_cast<float4 *>(base)[c * 8 + cg] = v;
+          // testing build: the parity suite's "unwritten rows" mutation (must fail parity)
+          const bool skip = kTesting && P.mutate == 1 && blockIdx.x == 0 && c == 0 && rw4 == 1;
+          if (base && !skip) reinterpret_cast<float4 *>(base)[c * 8 + cg] = v;
         }
         __syncwarp();
       }
@@ -728,7 +730,7 @@ __global__ void __launch_bounds__(tc4::kThreads, 1) prefix_tc4_kernel(const __gr
         constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BM, BN, false);
         constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(BM, HD, true);
         uint32_t gb = 0, qc[2] = {0, 0}, pc[4] = {0, 0, 0, 0}, oc[2] = {0, 0};
-        long long *tr = (P.trace && blockIdx.x == 0) ? P.trace : nullptr;
+        long long *tr = (kTesting && P.trace && blockIdx.x == 0) ? P.trace : nullptr;
         uint32_t trn[2] = {0, 0};
         SegIter si;
         seg_begin(P, si);
@@ -807,7 +809,7 @@ __global__ void __launch_bounds__(tc4::kThreads, 1) prefix_tc4_kernel(const __gr
     uint8_t *sQ = smem + OFF_Q + t * QTILE;
     const float c2 = P.scale_log2;
     uint32_t sc[2] = {0, 0}, pvn = 0, orc = 0;  // s_full phase per buffer; PV_t count; items done
-    long long *tr = (P.trace && blockIdx.x == 0 && quarter == 0 && lane == 0) ? P.trace : nullptr;
+    long long *tr = (kTesting && P.trace && blockIdx.x == 0 && quarter == 0 && lane == 0) ? P.trace : nullptr;
     constexpr int kTN = tc2::kTraceN;
     SegIter si;
     seg_begin(P, si);
@@ -975,30 +977,12 @@ __global__ void __launch_bounds__(tc4::kThreads, 1) prefix_tc4_kernel(const __gr
 }
 
 // ------------------------------------------------------------------ host side
-static PFN_cuTensorMapEncodeTiled_v12000 encode_fn2() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void *p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  });
-  return fn;
-}
-
 static bool make_kv_map2(CUtensorMap *m, const void *base, int64_t T, int Hkv, int64_t st, int64_t sh,
                          int box_rows = tc2::BN) {
-  auto fn = encode_fn2();
-  if (!fn) return false;
-  const cuuint64_t dims[3] = {(cuuint64_t)tc2::HD, (cuuint64_t)Hkv, (cuuint64_t)T};
-  const cuuint64_t strides[2] = {(cuuint64_t)sh * 2, (cuuint64_t)st * 2};
-  const cuuint32_t box[3] = {64, 1, (cuuint32_t)box_rows};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(base), dims, strides, box, estr,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  const uint64_t dims[3] = {(uint64_t)tc2::HD, (uint64_t)Hkv, (uint64_t)T};
+  const uint64_t strides[2] = {(uint64_t)sh * 2, (uint64_t)st * 2};
+  const uint32_t box[3] = {64, 1, (uint32_t)box_rows};
+  return encode_bf16_map(m, 3, base, dims, strides, box);
 }
 
 // Flat-mode schedule: grouped stream-K when there are at least two groups' worth of CTAs.
@@ -1032,24 +1016,15 @@ int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn) {
 
 template <int kPoly, bool kPP, bool kSplit = false>
 static cudaError_t tc2_launch(const PrefixTc2Params &P, int grid, cudaStream_t s) {
-  static std::once_flag once;
-  static cudaError_t attr = cudaSuccess;
-  std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(prefix_tc2_kernel<kPoly, kPP, kSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                tc2::ALLOC);
-  });
+  const cudaError_t attr = ensure_smem_attr(reinterpret_cast<const void *>(prefix_tc2_kernel<kPoly, kPP, kSplit>),
+                                            tc2::ALLOC);
   if (attr != cudaSuccess) return attr;
   prefix_tc2_kernel<kPoly, kPP, kSplit><<<grid, tc2::kThreads, tc2::ALLOC, s>>>(P);
   return cudaGetLastError();
 }
 
 static cudaError_t tc4_attr() {
-  static std::once_flag once;
-  static cudaError_t attr = cudaSuccess;
-  std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(prefix_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc4::ALLOC);
-  });
-  return attr;
+  return ensure_smem_attr(reinterpret_cast<const void *>(prefix_tc4_kernel), tc4::ALLOC);
 }
 
 hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s) {
@@ -1058,7 +1033,7 @@ hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s
   const int bn = v4 ? tc4::BN : tc2::BN;
   // instantiations: kPolyEvery 0 (all MUFU), 3/4/8 (1/k of the pairs on the FMA pipe),
   // -1 (timing experiment: no exp); kSpec for variant 5 (v3 + speculative softmax)
-  if (!(poly == 0 || poly == 3 || poly == 4 || poly == 8 || poly == -1)) return HYDRA_EINVAL;
+  if (!(poly == 0 || poly == 3 || poly == 4 || poly == 8 || (kTesting && poly == -1))) return HYDRA_EINVAL;
   if (v4 && tc4_attr() != cudaSuccess) return HYDRA_ECUDA;
   PrefixTc2Params P;
   memset(&P, 0, sizeof(P));
@@ -1067,8 +1042,9 @@ hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s
     if (!make_kv_map2(&P.tmV, a.v, a.kv_total, a.Hkv, a.kv_st, a.kv_sh, bn)) return HYDRA_ECUDA;
   }
   P.bn = bn;
-  P.debug = a.debug_variant;
-  P.trace = reinterpret_cast<long long *>(a.trace);
+  P.debug = kTesting ? a.debug_variant : 0;
+  P.trace = kTesting ? reinterpret_cast<long long *>(a.trace) : nullptr;
+  P.mutate = kTesting ? a.mutate : 0;
   P.q = reinterpret_cast<const __nv_bfloat16 *>(a.q);
   P.q_sb = a.q_sb;
   P.q_sh = a.q_sh;
@@ -1115,8 +1091,11 @@ hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s
     case 9: e = tc2_launch<4, true>(P, grid, s); break;
     case 16: e = tc2_launch<8, false>(P, grid, s); break;
     case 17: e = tc2_launch<8, true>(P, grid, s); break;
-    case -2: e = tc2_launch<-1, false>(P, grid, s); break;
-    default: e = tc2_launch<-1, true>(P, grid, s); break;
+#ifdef HYDRA_TESTING
+    case -2: e = tc2_launch<-1, false>(P, grid, s); break;  // timing experiment: no exp (invalid results)
+    case -1: e = tc2_launch<-1, true>(P, grid, s); break;
+#endif
+    default: return HYDRA_EINVAL;
   }
   return e == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
 }

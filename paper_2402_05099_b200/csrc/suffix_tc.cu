@@ -36,7 +36,6 @@
 
 #include <algorithm>
 #include <cstring>
-#include <mutex>
 
 #include "common.cuh"
 #include "internal.h"
@@ -90,7 +89,9 @@ struct __align__(64) SuffixTcParams {
   float scale_log2;
   int32_t n_items;
   float *o, *lse;
-  int32_t debug;     // timing experiments only (invalid results): 256 = the MMA warp releases K/V
+  int32_t S_cap;     // lens[b] is clamped to [0, S_cap] (hydra.h precondition; release and testing)
+  int32_t mutate;    // testing build only: 2 = CTA 0's epilogue skips head 0's store of its first item
+  int32_t debug;     // testing build only, timing experiments (invalid results): 256 = the MMA warp releases K/V
                      // tiles as they land (no MMA, no softmax), 512 = no softmax work,
                      // 4096 / 8192 = no score / PV MMA instructions
   long long *trace;  // diagnostics: CTA 0 event timestamps [kTraceRows][kTraceN] (tools/suffix_trace.py); null = off
@@ -113,7 +114,7 @@ constexpr int kTraceN = 1024;
 // 8 MMA PV round committed, 9 K TMA issued (block), 10 V TMA issued (block), 11 / 12 MMA thread
 // sees K / V landed (block)
 __device__ __forceinline__ void trace(long long *tr, int row, uint32_t i) {
-  if (tr && i < (uint32_t)kTraceN) tr[row * kTraceN + i] = clock64();
+  if (kTesting && tr && i < (uint32_t)kTraceN) tr[row * kTraceN + i] = clock64();
 }
 }  // namespace stc
 
@@ -139,6 +140,7 @@ __device__ __forceinline__ int item_len_raw(const SuffixTcParams &P, int item) {
 }
 template <bool SPLIT>
 __device__ __forceinline__ int item_len_of(const SuffixTcParams &P, int item, int raw) {
+  raw = min(max(raw, 0), P.S_cap);  // out-of-range lens[b] (a precondition violation) is clamped
   if (!SPLIT) return raw;
   const int sp = item % P.n_split;
   return max(0, min(P.split_len, raw - sp * P.split_len));
@@ -374,7 +376,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
     // the PV cursor issues a round's PV MMAs as soon as its P^T and V tiles are ready.
     // Neither waits behind the other, so a V slot is held only for load + softmax + PV.
     const bool leader = ptx::elect_one();
-    if (leader && (P.debug & 256)) {  // drain only: release each tile as soon as it lands
+    if (kTesting && leader && (P.debug & 256)) {  // drain only: release each tile as soon as it lands
       RoundCursor<CB, SPLIT> c;
       c.init(P);
       while (c.valid) {
@@ -431,7 +433,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
     // before the PV MMA reads it (0 * NaN would poison O).  The softmax warps cannot do it:
     // they may run up to three rounds ahead of the V ring, where a parity wait on v_full
     // could not tell the tile's phase from the one two loads earlier.
-    if (!(P.debug & 256)) {
+    if (!(kTesting && (P.debug & 256))) {
       const bool leader = ptx::elect_one();
       constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(HD, NQ, false) | (1u << 15);  // A=V^T (MN-major), B=P^T
       long long *tr = (blockIdx.x == 0 && leader) ? P.trace : nullptr;
@@ -478,7 +480,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
         pc.next(P);
       }
     }
-  } else if (warp < 8 && !(P.debug & 256)) {
+  } else if (warp < 8 && !(kTesting && (P.debug & 256))) {
     // ================= softmax (thread = token lane) =================
     const int quarter = warp % 4;
     const int r = quarter * 32 + lane;
@@ -515,7 +517,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
         ptx::mbar_wait(&s_full[buf], (gr / NSP) & 1);
         trace(tr, 1, gr);
         ptx::tc_fence_after();
-        if (P.debug & 512) {  // timing experiment only: no softmax work
+        if (kTesting && (P.debug & 512)) {  // timing experiment only: no softmax work
           if (gr >= (uint32_t)NSP) ptx::mbar_wait(&pv_done[buf], ((gr - NSP) / NSP) & 1);
           ptx::warp_arrive(&p_full[buf]);
           gb += nb;
@@ -618,7 +620,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
       ptx::warp_arrive(&ml_full[ob]);
       ++item_no;
     }
-  } else if (warp >= 8 && !(P.debug & 256)) {
+  } else if (warp >= 8 && !(kTesting && (P.debug & 256))) {
     // ================= epilogue (thread = head dim): O = O^T / l, LSE =================
     const int quarter = warp % 4;
     const int r = quarter * 32 + lane;
@@ -647,9 +649,11 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
       }
       ptx::tc_fence_before();
       ptx::warp_arrive(&o_free[ob]);  // O^T buffer and (m, l) slot free
+      // testing build: the parity suite's "unwritten rows" mutation (must fail parity)
+      const bool skip0 = kTesting && P.mutate == 2 && blockIdx.x == 0 && item_no == 0;
 #pragma unroll
       for (int h = 0; h < G; ++h) {
-        P.o[ir.o_off + (row0 + h) * HD + r] = __uint_as_float(ov[h]) / L[h];
+        if (!(skip0 && h == 0)) P.o[ir.o_off + (row0 + h) * HD + r] = __uint_as_float(ov[h]) / L[h];
         if (r == h) P.lse[ir.lse_off + row0 + h] = (M[h] + log2f(L[h])) * HYDRA_LN2;
       }
       ++item_no;
@@ -666,34 +670,16 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
 }
 
 // ------------------------------------------------------------------ host side
-static PFN_cuTensorMapEncodeTiled_v12000 encode_fn3() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void *p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  });
-  return fn;
-}
-
 bool suffix_tc_supported(const hydra_heads *h) {
   const int g = h->num_q_heads / h->num_kv_heads;
   const bool g_ok = g == 1 || g == 2 || g == 4 || g == 8 || g == 16;
-  return h->dtype == HYDRA_BF16 && h->head_dim == 128 && g_ok && encode_fn3() != nullptr;
+  return h->dtype == HYDRA_BF16 && h->head_dim == 128 && g_ok && tensor_maps_available();
 }
 
 template <int G, int CB, bool SPLIT, bool PAGED>
 static cudaError_t launch_gcsp(const SuffixTcParams &P, int grid, cudaStream_t s) {
-  static std::once_flag once;
-  static cudaError_t attr = cudaSuccess;
   constexpr int alloc = stc::alloc_bytes(CB);
-  std::call_once(once, [] {
-    attr = cudaFuncSetAttribute(suffix_tc_kernel<G, CB, SPLIT, PAGED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                alloc);
-  });
+  const cudaError_t attr = ensure_smem_attr(reinterpret_cast<const void *>(suffix_tc_kernel<G, CB, SPLIT, PAGED>), alloc);
   if (attr != cudaSuccess) return attr;
   suffix_tc_kernel<G, CB, SPLIT, PAGED><<<grid, stc::kThreads, alloc, s>>>(P);
   return cudaGetLastError();
@@ -713,8 +699,6 @@ static cudaError_t launch_g(const SuffixTcParams &P, int cb, int grid, cudaStrea
 }
 
 hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s) {
-  auto fn = encode_fn3();
-  if (!fn) return HYDRA_ECUDA;
   SuffixTcParams P;
   memset(&P, 0, sizeof(P));
   const int g = a.Hq / a.Hkv;
@@ -723,30 +707,19 @@ hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s)
   {
     // contiguous: [B, S_cap, Hkv, d], one 128-token box per panel; paged: the page pools
     // [n_pages, page_size, Hkv, d] with min(page_size, 128)-token boxes
-    const int pbox = paged ? std::min(a.page_size, stc::BT) : stc::BT;
-    const cuuint64_t dims[4] = {(cuuint64_t)stc::HD, (cuuint64_t)a.Hkv,
-                                (cuuint64_t)(paged ? a.page_size : a.S_cap), (cuuint64_t)(paged ? a.n_pages : a.B)};
-    const cuuint64_t strides[3] = {(cuuint64_t)a.s_sh * 2, (cuuint64_t)a.s_st * 2, (cuuint64_t)a.s_sb * 2};
-    const cuuint32_t box[4] = {64, 1, (cuuint32_t)pbox, 1};
-    const cuuint32_t estr[4] = {1, 1, 1, 1};
-    if (fn(&P.tmK, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(a.k), dims, strides, box, estr,
-           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return HYDRA_ECUDA;
-    if (fn(&P.tmV, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(a.v), dims, strides, box, estr,
-           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return HYDRA_ECUDA;
+    const uint32_t pbox = paged ? (uint32_t)std::min(a.page_size, stc::BT) : (uint32_t)stc::BT;
+    const uint64_t dims[4] = {(uint64_t)stc::HD, (uint64_t)a.Hkv, (uint64_t)(paged ? a.page_size : a.S_cap),
+                              (uint64_t)(paged ? a.n_pages : a.B)};
+    const uint64_t strides[3] = {(uint64_t)a.s_sh * 2, (uint64_t)a.s_st * 2, (uint64_t)a.s_sb * 2};
+    const uint32_t box[4] = {64, 1, pbox, 1};
+    if (!encode_bf16_map(&P.tmK, 4, a.k, dims, strides, box)) return HYDRA_ECUDA;
+    if (!encode_bf16_map(&P.tmV, 4, a.v, dims, strides, box)) return HYDRA_ECUDA;
   }
   {
-    const cuuint64_t dims[3] = {(cuuint64_t)stc::HD, (cuuint64_t)a.Hq, (cuuint64_t)a.B};
-    const cuuint64_t strides[2] = {(cuuint64_t)a.q_sh * 2, (cuuint64_t)a.q_sb * 2};
-    const cuuint32_t box[3] = {64, (cuuint32_t)g, 1};
-    const cuuint32_t estr[3] = {1, 1, 1};
-    if (fn(&P.tmQ, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(a.q), dims, strides, box, estr,
-           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return HYDRA_ECUDA;
+    const uint64_t dims[3] = {(uint64_t)stc::HD, (uint64_t)a.Hq, (uint64_t)a.B};
+    const uint64_t strides[2] = {(uint64_t)a.q_sh * 2, (uint64_t)a.q_sb * 2};
+    const uint32_t box[3] = {64, (uint32_t)g, 1};
+    if (!encode_bf16_map(&P.tmQ, 3, a.q, dims, strides, box)) return HYDRA_ECUDA;
   }
   P.lens = a.lens;
   P.B = a.B;
@@ -761,8 +734,10 @@ hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s)
   P.n_items = a.B * a.Hkv * P.n_split;
   P.o = a.o;
   P.lse = a.lse;
-  P.trace = reinterpret_cast<long long *>(a.trace);
-  P.debug = a.debug;
+  P.trace = kTesting ? reinterpret_cast<long long *>(a.trace) : nullptr;
+  P.debug = kTesting ? a.debug : 0;
+  P.mutate = kTesting ? a.mutate : 0;
+  P.S_cap = (int32_t)std::min<int64_t>(a.S_cap, INT32_MAX);
   P.block_table = a.block_table;
   P.bt_stride = a.bt_stride;
   if (paged) {

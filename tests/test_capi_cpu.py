@@ -158,3 +158,73 @@ def test_paged_validation_errors(lib):
     assert lib.hydra_attn_paged(ctypes.byref(h), 2, FAKE, 512, 128, 256, FAKE, FAKE, 256, 128, FAKE, FAKE, 4096, 256,
                                 128, ctypes.byref(P(FAKE, 4, 24, 8)), 64, FAKE, FAKE, 0, None, FAKE, need, None,
                                 None) == _lib.HYDRA_ESHAPE
+
+
+# ---------------------------------------------------------------- release vs testing build
+def _kernel_symbols(path):
+    out = os.popen(f"cuobjdump -elf {path} 2>/dev/null").read()
+    return set(re.findall(r"_ZN5hydra\w+", out))
+
+
+def test_release_library_has_no_wrong_result_modes(lib):
+    """The release libhydra.so carries none of the testing build's wrong-result paths: no
+    no-exp instantiation of the persistent prefix kernel (kPolyEvery = -1), and the
+    timing-experiment / sabotage / trace switches are rejected (include/hydra.h)."""
+    syms = _kernel_symbols(_lib.RELEASE_LIB)
+    if not syms:
+        pytest.skip("cuobjdump unavailable")
+    assert any("prefix_tc2_kernel" in s for s in syms)
+    assert not any("prefix_tc2_kernelILin1" in s for s in syms), "no-exp timing variant shipped in release"
+    test_syms = _kernel_symbols(_lib.TEST_LIB)
+    assert any("prefix_tc2_kernelILin1" in s for s in test_syms)  # the testing build keeps it
+    for key in (b"tc_debug_variant", b"prefix_trace", b"suffix_trace", b"inject_combine_bug", b"mutate"):
+        assert lib.hydra_set_config(key, 1) == _lib.HYDRA_EINVAL
+        assert "testing build" in lib.hydra_last_error().decode()
+    assert lib.hydra_set_config(b"prefix_poly", -1) == _lib.HYDRA_OK and hydra.get_config("prefix_poly") == 4
+    assert hydra.get_config("testing_build") == 0
+    assert lib.hydra_debug_lens_violations(0) == -1  # no device check in release (kernels clamp)
+    assert "testing" not in hydra.version()
+
+
+def test_testing_library_accepts_test_switches():
+    """libhydra_test.so in a subprocess (HYDRA_TESTING=1): the sabotage keys exist there."""
+    import subprocess
+    import sys
+
+    code = ("import paper_2402_05099_b200 as h; from paper_2402_05099_b200 import _lib;"
+            "assert _lib.LIB_PATH == _lib.TEST_LIB; assert h.get_config('testing_build') == 1;"
+            "h.set_config('inject_combine_bug', 1); h.set_config('mutate', 2); assert h.get_config('mutate') == 2;"
+            "assert 'testing' in h.version(); print('ok')")
+    env = dict(os.environ, HYDRA_TESTING="1")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr
+
+
+def test_config_is_thread_local(lib):
+    """hydra_set_config is per thread (hydra.h "Thread safety"): another thread's switch does
+    not leak into this thread's calls."""
+    import threading
+
+    hydra.set_config("prefix_splits", 5)
+    seen = {}
+
+    def other():
+        seen["before"] = hydra.get_config("prefix_splits")
+        hydra.set_config("prefix_splits", 9)
+        seen["after"] = hydra.get_config("prefix_splits")
+
+    t = threading.Thread(target=other)
+    t.start()
+    t.join()
+    assert seen == {"before": 0, "after": 9}
+    assert hydra.get_config("prefix_splits") == 5
+    hydra.set_config("prefix_splits", 0)
+
+
+def test_workspace_parts_op(lib):
+    """HYDRA_OP_PARTS sizes n_parts caller-staged partial slots (the n_parts argument)."""
+    h = H(Hq=8, Hkv=2)
+    one = 3 * 8 * (128 + 1) * 4
+    assert lib.hydra_workspace_size(_lib.HYDRA_OP_PARTS, ctypes.byref(h), 3, 0, 0, 1) == one
+    assert lib.hydra_workspace_size(_lib.HYDRA_OP_PARTS, ctypes.byref(h), 3, 0, 0, 5) == 5 * one
+    assert lib.hydra_workspace_size(_lib.HYDRA_OP_PARTS, ctypes.byref(h), 3, 0, 0, 0) == 0

@@ -9,6 +9,7 @@ import torch
 
 import oracle
 import synth
+from tests import nanfill as H
 from tests.util import assert_parity, problem_to
 
 hydra = pytest.importorskip("paper_2402_05099_b200")
@@ -77,7 +78,7 @@ def test_decode_loop_in_one_graph(aux):
 
     def step():
         hydra.append_kv(k_in, v_in, t["sk"], t["sv"], t["lens"])
-        hydra.hydragen_attention(t["q"], t["pk"], t["pv"], t["sk"], t["sv"], t["lens"], out=out, lse_out=lse,
+        H.hydragen_attention(t["q"], t["pk"], t["pv"], t["sk"], t["sv"], t["lens"], out=out, lse_out=lse,
                                  workspace=ws, aux_stream=side)
 
     # capture on a scratch copy of the state, then restore: capture runs the step once
@@ -97,6 +98,7 @@ def test_decode_loop_in_one_graph(aux):
     torch.cuda.synchronize()
     for i in range(steps):
         k_in.copy_(new_k[i]); v_in.copy_(new_v[i])
+        out.fill_(float("nan")); lse.fill_(float("nan")); ws.fill_(0xFF)  # unwritten rows fail
         g.replay()
         torch.cuda.synchronize()
         lens = t["lens"].cpu().numpy()

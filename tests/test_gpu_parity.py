@@ -13,6 +13,7 @@ import torch
 
 import oracle
 import synth
+from tests import nanfill as H
 from tests.util import assert_parity, errors, problem_to, tree_to
 
 hydra = pytest.importorskip("paper_2402_05099_b200")
@@ -42,7 +43,7 @@ DEV = "cuda:0"
 def run_flat(pb, aux=False, **kw):
     t = problem_to(pb, DEV)
     aux_stream = torch.cuda.Stream() if aux else None
-    out, lse = hydra.hydragen_attention(t["q"], t["pk"], t["pv"], t["sk"], t["sv"], t["lens"], return_lse=True,
+    out, lse = H.hydragen_attention(t["q"], t["pk"], t["pv"], t["sk"], t["sv"], t["lens"], return_lse=True,
                                         aux_stream=aux_stream, **kw)
     torch.cuda.synchronize()
     return out, lse
@@ -81,7 +82,7 @@ def test_prefix_tc_parity(B, Hq, Hkv, P, dist, impl):
     hydra.set_config("prefix_variant", impl if impl >= 3 else 3)
     pb = synth.make_problem(B, Hq, Hkv, 128, P, 1, dtype="bf16", dist=dist, seed=3)
     t = problem_to(pb, DEV)
-    o, lse = hydra.prefix_attn(t["q"], t["pk"], t["pv"])
+    o, lse = H.prefix_attn(t["q"], t["pk"], t["pv"])
     torch.cuda.synchronize()
     ref, lref = oracle.prefix_only(pb)
     assert_parity(o, ref, lse, lref, what=f"prefix {B},{Hq},{Hkv},{P}")
@@ -93,7 +94,7 @@ def test_prefix_tc_splits(splits):
     hydra.set_config("prefix_splits", splits)
     pb = synth.make_problem(20, 8, 2, 128, 1100, 1, dtype="bf16", dist="mixed", seed=4)
     t = problem_to(pb, DEV)
-    o, lse = hydra.prefix_attn(t["q"], t["pk"], t["pv"])
+    o, lse = H.prefix_attn(t["q"], t["pk"], t["pv"])
     torch.cuda.synchronize()
     ref, lref = oracle.prefix_only(pb)
     assert_parity(o, ref, lse, lref, what=f"prefix splits={splits}")
@@ -111,7 +112,7 @@ def test_prefix_tc2_growing_max(variant, poly):
     pb.pk = synth.gen.f32_to_bf16_bits((pb.f32("pk") * ramp).astype(np.float32))
     t = problem_to(pb, DEV)
     try:
-        o, lse = hydra.prefix_attn(t["q"], t["pk"], t["pv"])
+        o, lse = H.prefix_attn(t["q"], t["pk"], t["pv"])
         torch.cuda.synchronize()
     finally:
         hydra.set_config("prefix_poly", 4)
@@ -127,7 +128,7 @@ def test_prefix_tc2_stream_k_ctas(ctas, variant):
     hydra.set_config("prefix_variant", variant)
     pb = synth.make_problem(300, 8, 2, 128, 1100, 1, dtype="bf16", dist="boundary", seed=4)
     t = problem_to(pb, DEV)
-    o, lse = hydra.prefix_attn(t["q"], t["pk"], t["pv"])
+    o, lse = H.prefix_attn(t["q"], t["pk"], t["pv"])
     torch.cuda.synchronize()
     ref, lref = oracle.prefix_only(pb)
     assert_parity(o, ref, lse, lref, what=f"prefix ctas={ctas}")
@@ -137,7 +138,7 @@ def test_prefix_simt_bf16():
     hydra.set_config("prefix_impl", 1)
     pb = synth.make_problem(9, 8, 2, 128, 333, 1, dtype="bf16", dist="mixed", seed=5)
     t = problem_to(pb, DEV)
-    o, lse = hydra.prefix_attn(t["q"], t["pk"], t["pv"])
+    o, lse = H.prefix_attn(t["q"], t["pk"], t["pv"])
     torch.cuda.synchronize()
     ref, lref = oracle.prefix_only(pb)
     assert_parity(o, ref, lse, lref, what="prefix SIMT")
@@ -156,7 +157,7 @@ def test_suffix_parity(B, Hq, Hkv, d, S, impl):
     lens[0] = S
     pb = synth.make_problem(B, Hq, Hkv, d, 0, S, lens=lens, dtype="bf16", dist="mixed", seed=6)
     t = problem_to(pb, DEV)
-    o, lse = hydra.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
+    o, lse = H.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
     torch.cuda.synchronize()
     ref, lref = oracle.suffix_only(pb)
     assert_parity(o, ref, lse, lref, what="suffix")
@@ -168,7 +169,7 @@ def test_suffix_splits(splits):
     pb = synth.make_problem(6, 8, 2, 128, 0, 200, lens=[200, 3, 0, 150, 64, 1], dtype="bf16", dist="boundary",
                             seed=7)
     t = problem_to(pb, DEV)
-    o, lse = hydra.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
+    o, lse = H.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
     torch.cuda.synchronize()
     ref, lref = oracle.suffix_only(pb)
     assert_parity(o, ref, lse, lref, what=f"suffix splits={splits}")
@@ -233,7 +234,7 @@ def test_suffix_tc_ctas_and_ragged(ctas, cb):
     lens = [0, 1, 127, 128, 129, 255, 256, 300, 17, 0, 384]
     pb = synth.make_problem(len(lens), 8, 1, 128, 0, 384, lens=lens, dtype="bf16", dist="boundary", seed=18)
     t = problem_to(pb, DEV)
-    o, lse = hydra.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
+    o, lse = H.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
     torch.cuda.synchronize()
     ref, lref = oracle.suffix_only(pb)
     assert_parity(o, ref, lse, lref, what=f"suffix tc ctas={ctas} cb={cb}")
@@ -249,7 +250,7 @@ def test_suffix_tc_ragged_repeat():
     t = problem_to(pb, DEV)
     ref, lref = oracle.suffix_only(pb)
     for _ in range(8):
-        o, lse = hydra.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
+        o, lse = H.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
         torch.cuda.synchronize()
         assert_parity(o, ref, lse, lref, what="suffix tc ragged repeat")
 
@@ -282,14 +283,19 @@ def test_determinism_bitwise():
     assert torch.equal(a, b) and torch.equal(la, lb)
 
 
-def test_sabotage_combine_bug_is_caught(monkeypatch):
-    """dropping the rescaling factor of the combine must fail parity."""
-    pb = synth.make_problem(8, 8, 2, 128, 500, 60, dtype="bf16", dist="mixed", seed=12)
-    ref, _ = oracle.flat_attention(pb)
-    monkeypatch.setenv("HYDRA_INJECT_COMBINE_BUG", "1")
-    out, _ = run_flat(pb)
-    mx, mean, _ = errors(out, ref)
-    assert mx > 2e-2 or mean > 2e-3, "sabotaged combine passed the parity gate"
+def test_lens_out_of_range_is_clamped():
+    """lens[b] outside [0, S_cap] violates the documented precondition; the release kernels
+    clamp it (hydra.h): lens > S_cap attends all S_cap rows, lens < 0 none -- never a read
+    past the cache (both suffix kernels)."""
+    pb = synth.make_problem(4, 8, 2, 128, 100, 32, lens=[32, 0, 5, 32], dtype="bf16", dist="mixed", seed=3)
+    ref, lref = oracle.flat_attention(pb)
+    for impl in (1, 2):
+        hydra.set_config("suffix_impl", impl)
+        t = problem_to(pb, DEV)
+        t["lens"].copy_(torch.tensor([40, -3, 5, 1 << 30], dtype=torch.int32))
+        out, lse = H.hydragen_attention(t["q"], t["pk"], t["pv"], t["sk"], t["sv"], t["lens"], return_lse=True)
+        torch.cuda.synchronize()
+        assert_parity(out, ref, lse, lref, what=f"clamped lens impl={impl}")
 
 
 # ---------------------------------------------------------------- tree (§3.3)
@@ -311,7 +317,7 @@ def test_tree_parity(impl, dtype):
     t = tree_to(tp, DEV)
     tree = hydra.Tree(tp.parent, tp.node_off, tp.node_len, tp.leaf_of_seq)
     assert tree.depth() == 3 and tree.group_size(0) == 15 and tree.group_size(4) == 5
-    out, lse = hydra.tree_attention(t["q"], tree, t["node_k"], t["node_v"], t["sk"], t["sv"], t["lens"],
+    out, lse = H.tree_attention(t["q"], tree, t["node_k"], t["node_v"], t["sk"], t["sv"], t["lens"],
                                     return_lse=True)
     torch.cuda.synchronize()
     ref, lref = oracle.tree_attention(tp)
@@ -331,7 +337,7 @@ def test_tree_sm_partitioned(k, per, g):
                                  seed=23, lens=np.arange(2 * per) % 301)
     t = tree_to(tp, DEV)
     tree = hydra.Tree(tp.parent, tp.node_off, tp.node_len, tp.leaf_of_seq)
-    out, lse = hydra.tree_attention(t["q"], tree, t["node_k"], t["node_v"], t["sk"], t["sv"], t["lens"],
+    out, lse = H.tree_attention(t["q"], tree, t["node_k"], t["node_v"], t["sk"], t["sv"], t["lens"],
                                     return_lse=True, aux_stream=torch.cuda.Stream())
     torch.cuda.synchronize()
     assert hydra.get_config("last_overlap_k") == k
@@ -340,12 +346,47 @@ def test_tree_sm_partitioned(k, per, g):
     tree.destroy()
 
 
+def test_tree_first_use_is_captured_in_a_graph():
+    """A prepared tree's attention is a pure launch sequence (hydra.h): its FIRST call can be
+    captured in a CUDA graph (the paper's CUDA-graph requirement), and the replay is
+    exact; an unprepared tree refuses capture with nothing launched."""
+    parent, node_len, leaf = synth.two_level_tree(300, 3, 150, 40)
+    tp = synth.make_tree_problem(parent, node_len, leaf, 8, 2, 128, 64, lens=np.arange(120) % 65, dtype="bf16",
+                                 dist="mixed", seed=33)
+    t = tree_to(tp, DEV)
+    ref, lref = oracle.tree_attention(tp)
+    cold = hydra.Tree(tp.parent, tp.node_off, tp.node_len, tp.leaf_of_seq)
+    out = torch.full((120, 8, 128), float("nan"), dtype=torch.bfloat16, device=DEV)
+    lse = torch.full((120, 8), float("nan"), dtype=torch.float32, device=DEV)
+    ws = H.nan_bytes(hydra.workspace_bytes_tree(t["q"], cold, 2, 64), DEV)
+    g = torch.cuda.CUDAGraph()
+    with pytest.raises(hydra.HydraError, match="prepare"):
+        with torch.cuda.graph(g):
+            hydra.tree_attention(t["q"], cold, t["node_k"], t["node_v"], t["sk"], t["sv"], t["lens"], out=out,
+                                 lse_out=lse, workspace=ws)
+    cold.destroy()
+    torch.cuda.synchronize()
+    for aux in (None, torch.cuda.Stream()):
+        tree = hydra.Tree(tp.parent, tp.node_off, tp.node_len, tp.leaf_of_seq, heads=(8, 2))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):  # the tree's first call
+            hydra.tree_attention(t["q"], tree, t["node_k"], t["node_v"], t["sk"], t["sv"], t["lens"], out=out,
+                                 lse_out=lse, workspace=ws, aux_stream=aux)
+        for _ in range(2):
+            out.fill_(float("nan")); lse.fill_(float("nan")); ws.fill_(0xFF)
+            g.replay()
+            torch.cuda.synchronize()
+            assert_parity(out, ref, lse, lref, what=f"captured tree aux={aux is not None}")
+        del g
+        tree.destroy()
+
+
 def test_one_level_tree_equals_flat():
     pb = synth.make_problem(20, 8, 2, 128, 400, 30, dtype="bf16", dist="mixed", seed=14)
     t = problem_to(pb, DEV)
     tree = hydra.Tree([-1], [0], [pb.P], np.zeros(pb.B, np.int32))
-    a = hydra.tree_attention(t["q"], tree, t["pk"], t["pv"], t["sk"], t["sv"], t["lens"])
-    b = hydra.hydragen_attention(t["q"], t["pk"], t["pv"], t["sk"], t["sv"], t["lens"])
+    a = H.tree_attention(t["q"], tree, t["pk"], t["pv"], t["sk"], t["sv"], t["lens"])
+    b = H.hydragen_attention(t["q"], t["pk"], t["pv"], t["sk"], t["sv"], t["lens"])
     torch.cuda.synchronize()
     ref, _ = oracle.flat_attention(pb)
     assert_parity(a, ref, what="one-level tree")
@@ -364,7 +405,7 @@ def test_combine_f16_parts_and_identity():
         ref_o, ref_l = oracle.combine(ref_o, ref_l, o[i], l[i])
     ot = torch.tensor(o, dtype=torch.float16, device=DEV)
     lt = torch.tensor(l, dtype=torch.float32, device=DEV)
-    out, lse = hydra.combine(ot, lt, out_dtype=torch.float32)
+    out, lse = H.combine(ot, lt, out_dtype=torch.float32)
     torch.cuda.synchronize()
     ref16 = ot.cpu().double().numpy()  # the exact fp16 values the kernel read
     l32 = lt.cpu().double().numpy()
@@ -413,7 +454,7 @@ def test_tree_large_groups(impl, per, g):
     tp = synth.make_tree_problem(parent, node_len, leaf, 4 * g, 4, 128, 24, dtype="bf16", dist="boundary", seed=19)
     t = tree_to(tp, DEV)
     tree = hydra.Tree(tp.parent, tp.node_off, tp.node_len, tp.leaf_of_seq)
-    out, lse = hydra.tree_attention(t["q"], tree, t["node_k"], t["node_v"], t["sk"], t["sv"], t["lens"],
+    out, lse = H.tree_attention(t["q"], tree, t["node_k"], t["node_v"], t["sk"], t["sv"], t["lens"],
                                     return_lse=True)
     torch.cuda.synchronize()
     ref, lref = oracle.tree_attention(tp)
@@ -434,7 +475,7 @@ def test_suffix_tc_split_k(splits, g):
         lens = [700, 0, 1, 128, 256 + 5, 511]
         pb = synth.make_problem(B, Hkv * g, Hkv, 128, 0, S, lens=lens, dtype="bf16", dist="mixed", seed=40 + g)
         t = problem_to(pb, DEV)
-        o, l = hydra.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
+        o, l = H.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
         torch.cuda.synchronize()
         ref, lref = oracle.suffix_only(pb)
         assert_parity(o, ref, l, lref, what=f"suffix_tc split-K s={splits} g={g}")
@@ -451,14 +492,14 @@ def test_suffix_gqa_long_suffix_auto():
     lens = rng.integers(1500, S + 1, B).astype(np.int32)
     pb = synth.make_problem(B, Hq, Hkv, 128, 0, S, lens=lens, dtype="bf16", dist="mixed", seed=77)
     t = problem_to(pb, DEV)
-    o, l = hydra.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
+    o, l = H.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
     torch.cuda.synchronize()
     rows = np.array([(b, h) for b in (0, 1, 63, 127) for h in (0, 7, 8, 31)])
     ref, lref = oracle.suffix_only(pb, rows=rows)
     assert_parity(o[rows[:, 0], rows[:, 1]], ref, l[rows[:, 0], rows[:, 1]], lref, what="auto split long suffix")
     pc = synth.paginate(pb, 64, seed=2)
     kp, vp = (torch.from_numpy(x).view(torch.bfloat16).to(DEV) for x in (pc.k_pool, pc.v_pool))
-    o2, l2 = hydra.suffix_attn_paged(t["q"], kp, vp, torch.from_numpy(pc.block_table).to(DEV), t["lens"], S_cap=S)
+    o2, l2 = H.suffix_attn_paged(t["q"], kp, vp, torch.from_numpy(pc.block_table).to(DEV), t["lens"], S_cap=S)
     torch.cuda.synchronize()
     assert torch.equal(o, o2) and torch.equal(l, l2)
 
@@ -483,7 +524,7 @@ def test_combine_part_counts_and_odd_rows(n, rows):
         ref_o, ref_l = oracle.combine(ref_o, ref_l, o_ref[i], l[i])
     ot = torch.tensor(o, dtype=torch.float32, device=DEV)
     lt = torch.tensor(l, dtype=torch.float32, device=DEV)
-    out, lse = hydra.combine(ot, lt, out_dtype=torch.float32)
+    out, lse = H.combine(ot, lt, out_dtype=torch.float32)
     torch.cuda.synchronize()
     got = out.cpu().numpy()
     assert np.isfinite(got).all()

@@ -10,6 +10,7 @@ import torch
 
 import oracle
 import synth
+from tests import nanfill as H
 from tests.util import assert_parity, problem_to, tree_to
 
 hydra = pytest.importorskip("paper_2402_05099_b200")
@@ -42,7 +43,7 @@ def test_tree_partitioned_repeat(per, g, k):
     ref, lref = oracle.tree_attention(tp)
     aux = torch.cuda.Stream()
     for _ in range(6):
-        out, lse = hydra.tree_attention(t["q"], tree, t["node_k"], t["node_v"], t["sk"], t["sv"], t["lens"],
+        out, lse = H.tree_attention(t["q"], tree, t["node_k"], t["node_v"], t["sk"], t["sv"], t["lens"],
                                         return_lse=True, aux_stream=aux)
         torch.cuda.synchronize()
         assert_parity(out, ref, lse, lref, what=f"tree partitioned k={k} (repeat)")
@@ -59,7 +60,7 @@ def test_flat_partitioned_repeat():
     ref, lref = oracle.flat_attention(pb)
     aux = torch.cuda.Stream()
     for _ in range(6):
-        out, lse = hydra.hydragen_attention(t["q"], t["pk"], t["pv"], t["sk"], t["sv"], t["lens"], return_lse=True,
+        out, lse = H.hydragen_attention(t["q"], t["pk"], t["pv"], t["sk"], t["sv"], t["lens"], return_lse=True,
                                             aux_stream=aux)
         torch.cuda.synchronize()
         assert_parity(out, ref, lse, lref, what="flat partitioned (repeat)")
