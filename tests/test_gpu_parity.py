@@ -23,7 +23,7 @@ pytestmark = pytest.mark.gpu
 
 @pytest.fixture(autouse=True)
 def _reset_config():
-    keys = ("prefix_impl", "prefix_splits", "suffix_splits", "tc_debug_variant", "prefix_ctas", "suffix_impl",
+    keys = ("prefix_impl", "prefix_splits", "suffix_splits", "prefix_ctas", "suffix_impl",
             "suffix_ctas", "overlap_prefix_ctas")
     for k in keys:
         hydra.set_config(k, 0)
