@@ -46,12 +46,18 @@ CONFIGS = {
     # prefix sequence split across ranks + NCCL all-gather of (O fp16, LSE) (dist.seqsplit_attention)
     "c4": dict(B=512, Hq=32, Hkv=8, d=128, P=32768, S=128, kind="seqsplit",
                name="Llama-3-8B GQA attention shape (32 q / 8 kv, d=128), B=512, prefix 32768 split along the "
-                    "sequence across ranks with an NCCL (O, LSE) all-gather, suffix 128"),
+                    "sequence across ranks with one NCCL all-to-all of packed (O fp16, LSE) rows, suffix 128"),
     # the paper's long-document shape (P:198, 19,947-token document,
     # Yi-6B-200k-like heads 32 q / 4 kv); suffix length assumed 128 (the paper gives none)
     "c6_longdoc": dict(B=256, Hq=32, Hkv=4, d=128, P=19947, S=128,
                        name="long-document shape (Yi-6B-like 32 q / 4 kv heads, d=128), B=256, prefix 19947, "
                             "suffix 128 (assumed)"),
+    # SURVEY §8(f) NEXT-2 on N GPUs: the long document's prefix split along the sequence (4 KV
+    # heads cap head sharding at 4 GPUs); B sweep with --batch-sweep 64,256,1024
+    "c6_seqsplit": dict(B=256, Hq=32, Hkv=4, d=128, P=19947, S=128, kind="seqsplit",
+                        name="long-document shape (Yi-6B-like 32 q / 4 kv heads, d=128), B=256, prefix 19947 split "
+                             "along the sequence across ranks with one NCCL all-to-all of packed (O fp16, LSE) rows, "
+                             "suffix 128 (assumed)"),
     # two-level sharing tree (tree_attention)
     "c5": dict(B=1024, Hq=32, Hkv=32, d=128, P=4096, S=512, kind="tree", branches=16, branch_len=1024,
                name="tree sharing: 4096-token root -> 16 branches x 1024 tokens -> 64 sequences each with 512-token "
@@ -82,6 +88,10 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--paged-page-size", type=int, default=16,
                     help="also time the step with the suffix in a paged cache of this page size (0 = skip)")
+    ap.add_argument("--batch-sweep", default="",
+                    help="comma-separated batch sizes: one JSON line per B (seqsplit and flat configs)")
+    ap.add_argument("--exchange", default="alltoall", choices=["alltoall", "allgather"],
+                    help="sequence-split exchange (seqsplit configs)")
     return ap.parse_args()
 
 
@@ -262,7 +272,7 @@ def run_tree(args, cfg):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(torch, dist, dev, world, rank)
     B, Hq, Hkv, d, S = cfg["B"], cfg["Hq"], cfg["Hkv"], cfg["d"], cfg["S"]
     nbr, blen = cfg["branches"], cfg["branch_len"]
     if Hkv % world:
@@ -274,7 +284,7 @@ def run_tree(args, cfg):
     t = lambda a: torch.from_numpy(a).view(torch.bfloat16).to(dev)
     q, nk, nv, sk, sv = t(tp.q), t(tp.node_k), t(tp.node_v), t(tp.sk), t(tp.sv)
     lens = torch.from_numpy(tp.lens.astype(np.int32)).to(dev)
-    tree = hydra.Tree(tp.parent, tp.node_off, tp.node_len, tp.leaf_of_seq)
+    tree = hydra.Tree(tp.parent, tp.node_off, tp.node_len, tp.leaf_of_seq, heads=(Hq_r, Hkv_r))
     capture, time_fn = make_timer(torch, dist, dev, world)
     aux = torch.cuda.Stream(priority=-1)
     # node attention on k SMs || tensor-core suffix on the rest (aux stream), or sequential:
@@ -343,11 +353,26 @@ def run_tree(args, cfg):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
-        dist.destroy_process_group()
+
+
+def init_dist(torch, dist, dev, world, rank):
+    """NCCL process group for N ranks (torchrun env), or a 1-rank group for N = 1."""
+    if dist.is_initialized():
+        return
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        import socket
+
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        dist.init_process_group("nccl", device_id=dev, init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
 
 
 def run_seqsplit(args, cfg):
-    """C4: prefix split along the sequence across ranks, NCCL all-gather of (O fp16, LSE) + combine."""
+    """C4 / C6 on N ranks: prefix split along the sequence, one packed all-to-all + Eq. 5 merge
+    (dist.SeqSplit), suffix of each rank's batch shard on a side stream during the exchange."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -361,64 +386,115 @@ def run_seqsplit(args, cfg):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=dev, init_method=None if world > 1 else "tcp://127.0.0.1:%d"
-                                % (29500 + os.getpid() % 1000), rank=rank, world_size=world)
+    init_dist(torch, dist, dev, world, rank)
     B, Hq, Hkv, d, P, S = cfg["B"], cfg["Hq"], cfg["Hkv"], cfg["d"], cfg["P"], cfg["S"]
     p0, p1 = hdist.shard_range(P, world, rank)
-    b0, b1 = hdist.shard_range(B, world, rank)
+    b0, b1 = hdist.batch_shard(B, world, rank)
     # every rank draws the same q; its own prefix shard and batch-shard suffixes (seeded per rank)
     pq = synth.make_problem(B, Hq, Hkv, d, 0, 0, dtype="bf16", seed=args.seed)
-    pr = synth.make_problem(b1 - b0, Hq, Hkv, d, p1 - p0, S, dtype="bf16", seed=args.seed + 1 + rank)
+    pr = synth.make_problem(max(1, b1 - b0), Hq, Hkv, d, p1 - p0, S, dtype="bf16", seed=args.seed + 1 + rank)
     t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).view(torch.bfloat16).to(dev)
-    q, pk, pv, sk, sv = t(pq.q), t(pr.pk), t(pr.pv), t(pr.sk), t(pr.sv)
-    lens = torch.from_numpy(pr.lens.astype(np.int32)).to(dev)
+    q, pk, pv, sk, sv = t(pq.q), t(pr.pk), t(pr.pv), t(pr.sk)[:b1 - b0], t(pr.sv)[:b1 - b0]
+    lens = torch.from_numpy(pr.lens.astype(np.int32)).to(dev)[:b1 - b0]
     in_bytes = sum(x.numel() * x.element_size() for x in (q, pk, pv, sk, sv))
     flush = l2_flush_buffer(torch, dev, in_bytes)  # a rank's shard fits in L2 at 8 GPUs
     capture, time_fn = make_timer(torch, dist, dev, world, flush=flush)
-    fn = lambda: hdist.seqsplit_attention(q, pk, pv, sk, sv, lens)
+    plan = hdist.SeqSplit(B, Hq, d, device=dev, exchange=args.exchange)
+    fn = lambda: plan(q, pk, pv, sk, sv, lens)
     try:
         g = capture(fn)
-        run = g.replay
-        graphed = True
+        run, graphed = g.replay, True
     except Exception:  # NCCL capture unsupported here: time eagerly
         run, graphed = fn, False
     with ClockSampler(local) as clk:
         ms = time_fn(run, args.steps, args.warmup)
+    # the phases alone (same buffers, CUDA graphs where possible): prefix, suffix, exchange
+    kk = max(5, args.steps // 4)
+    ms_pre = time_fn(capture(lambda: hydra.prefix_attn(q, pk, pv, out=plan.o_p, lse_out=plan.l_p)).replay, kk, 3)
+    ms_suf = (time_fn(capture(lambda: hydra.suffix_attn(q[b0:b1], sk, sv, lens, out=plan.o_s[0].view(b1 - b0, Hq, d),
+                                                         lse_out=plan.l_s[0].view(b1 - b0, Hq))).replay, kk, 3)
+              if b1 > b0 else 0.0)
+    try:
+        ms_ex = time_fn(capture(plan._collective).replay, kk, 3)
+    except Exception:
+        ms_ex = time_fn(plan._collective, kk, 3)
     pk_ = peaks()
     flops = 4.0 * B * Hq * (p1 - p0) * d
-    g_pre = capture(lambda: hydra.prefix_attn(q, pk, pv))
-    ms_pre = time_fn(g_pre.replay, max(5, args.steps // 4), 3)
     tc = float(pk_.get("bf16_tflops", 1590.0))
     line = base_line(args, cfg, world, ms, B)
     line["config"] = {"workload": args.config, "description": cfg["name"], "B": B, "Hq": Hq, "Hkv": Hkv, "d": d,
                       "prefix_len": P, "suffix_len": S, "parallelism": f"prefix sequence split x{world}",
-                      "prefix_tokens_per_rank": p1 - p0,
-                      "exchange": "NCCL all_to_all_single of fp16 O + fp32 LSE by batch shard",
-                      "exchange_bytes_per_rank": B * Hq * (d * 2 + 4), "cuda_graph": graphed,
+                      "prefix_tokens_per_rank": p1 - p0, "batch_shard": [b0, b1],
+                      "exchange": f"one NCCL {args.exchange} of packed rows [O fp16 | LSE f32 | pad] "
+                                  f"({plan.row_bytes} B per row), merged with the suffix part in one combine",
+                      "exchange_bytes_sent_per_rank": plan.exchange_bytes(), "cuda_graph": graphed,
                       "l2": ("no flush: %.2f GB of inputs per rank > 2 x 126 MB L2" % (in_bytes / 1e9)) if flush is None
                       else "L2 flushed (256 MB write) before every timed step: %.3f GB of inputs per rank" % (in_bytes / 1e9)}
-    line["roofline"] = {"bound": "tensor", "kernel": "prefix_tc2_kernel (tcgen05)",
+    line["roofline"] = {"bound": "tensor", "kernel": "prefix_tc2_kernel (tcgen05), this rank's prefix shard",
                         "achieved": round(flops / (ms_pre * 1e-3) / 1e12, 1), "peak": tc, "unit": "TFLOP/s",
                         "frac": round(flops / (ms_pre * 1e-3) / 1e12 / tc, 4), "traffic": None,
                         "algorithmic_flops_per_launch": flops, "launch_ms": round(ms_pre, 5)}
+    line["phases_alone_ms"] = {"prefix": round(ms_pre, 5), "suffix": round(ms_suf, 5), "exchange": round(ms_ex, 5),
+                               "sum": round(ms_pre + ms_suf + ms_ex, 5), "step": round(ms, 5),
+                               "note": "each phase timed alone (max over ranks); the step overlaps the suffix "
+                                       "with the exchange on a side stream"}
     line["clocks"] = clk.summary()
-    line["gpu_launches"] = args.steps * 6
+    line["gpu_launches"] = args.steps * 5  # prefix (+ -inf fill), pack, suffix, merge; + NCCL's own kernel
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.barrier()
-    dist.destroy_process_group()
+    hdist.release_plans()
+    del plan
+
+
+def self_launch(args):
+    """`bench.py --gpus N` without a torchrun environment: start N ranks with torchrun on this node
+    (one per GPU) and pass their output through; fail loudly when fewer GPUs are visible."""
+    import socket
+
+    import torch
+
+    n = torch.cuda.device_count()
+    if n < args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} requested but {n} CUDA device(s) visible"}), flush=True)
+        sys.exit(2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.run(cmd).returncode)
 
 
 def main():
     args = parse()
     if args.impl == "reference":
         return reference_arm(args)
-    kind = CONFIGS[args.config].get("kind")
-    if kind == "tree":
-        return run_tree(args, dict(CONFIGS[args.config]))
-    if kind == "seqsplit":
-        return run_seqsplit(args, dict(CONFIGS[args.config]))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} does not match WORLD_SIZE={world}")
+    cfg = dict(CONFIGS[args.config])
+    batches = [int(x) for x in args.batch_sweep.split(",") if x.strip()] or [cfg["B"]]
+    kind = cfg.get("kind")
+    for B in batches:
+        c = dict(cfg, B=B)
+        if B != cfg["B"]:
+            c["name"] = cfg["name"].replace("B=%d" % cfg["B"], "B=%d" % B)
+        if kind == "tree":
+            run_tree(args, c)
+        elif kind == "seqsplit":
+            run_seqsplit(args, c)
+        else:
+            run_flat(args, c)
+    import torch.distributed as dist
+
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
+def run_flat(args, cfg):
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -429,14 +505,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        args.gpus = world
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        init_dist(torch, dist, dev, world, rank)
 
-    cfg = dict(CONFIGS[args.config])
     B, Hq, Hkv, d, P, S = cfg["B"], cfg["Hq"], cfg["Hkv"], cfg["d"], cfg["P"], cfg["S"]
     if Hkv % world:
         raise SystemExit(f"Hkv={Hkv} is not divisible by {world} GPUs (head sharding)")
@@ -723,7 +796,6 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
-        dist.destroy_process_group()
 
 
 def e2e_leg(args, hydra, torch, dev, world, host_t, dev_t, ws, out, B):

@@ -150,6 +150,43 @@ HYDRA_API hydra_status hydra_combine(int64_t rows, int32_t d, int32_t n_parts,
                            void *out, hydra_dtype out_dtype, float *lse_out, void *stream);
 
 /*
+ * hydra_combine_ex -- the same Eq. 5 combine over two groups of parts with explicit row
+ * strides (elements; 0 = dense rows: d for O, 1 for LSE):
+ *   group A: n_parts parts in o_dtype (F32, or F16 partials received from other GPUs), part p
+ *            row r at o_parts + p*o_part_stride + r*o_row_stride, LSE at
+ *            lse_parts[p*lse_part_stride + r*lse_row_stride];
+ *   group B: n_parts_f32 parts in F32 (may be 0), addressed the same way;
+ *   out row r at out + r*out_row_stride (out_dtype), lse_out[r*lse_out_row_stride] (nullable).
+ * Every row merges all n_parts + n_parts_f32 parts at once.  Row strides let one call read or
+ * write a buffer whose rows interleave O and LSE -- the multi-GPU layer packs a rank's
+ * (O f16 | LSE f32) rows with one call and merges the N received pieces with the local suffix
+ * part with one call (paper_2402_05099_b200/dist.py).  For d = 128 / 256 the O bases and
+ * strides must be 16-byte (F32) or 8-byte (F16) aligned (EINVAL).  Output rows must not
+ * overlap input rows.
+ */
+typedef struct {
+  int64_t rows;
+  int32_t d;
+  int32_t n_parts;
+  const void *o_parts;
+  hydra_dtype o_dtype;
+  int64_t o_part_stride, o_row_stride;
+  const float *lse_parts;
+  int64_t lse_part_stride, lse_row_stride;
+  int32_t n_parts_f32;
+  const float *o_parts_f32;
+  int64_t o_f32_part_stride, o_f32_row_stride;
+  const float *lse_parts_f32;
+  int64_t lse_f32_part_stride, lse_f32_row_stride;
+  void *out;
+  hydra_dtype out_dtype;
+  int64_t out_row_stride;
+  float *lse_out;
+  int64_t lse_out_row_stride;
+} hydra_combine_desc;
+HYDRA_API hydra_status hydra_combine_ex(const hydra_combine_desc *c, void *stream);
+
+/*
  * hydra_attn -- the whole decode-step attention of App. B `hydragen_attention`
  * (P:347-399): prefix (hydra_prefix_attn) || suffix (hydra_suffix_attn) ->
  * combine, writing out[B,Hq,d] (out_dtype) and optionally lse_out[B,Hq].

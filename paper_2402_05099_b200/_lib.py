@@ -26,7 +26,8 @@ EXPORTED = ["hydra_prefix_attn", "hydra_suffix_attn", "hydra_combine", "hydra_at
             "hydra_tree_destroy", "hydra_tree_depth", "hydra_tree_group_size", "hydra_tree_workspace_size",
             "hydra_tree_attn", "hydra_workspace_size", "hydra_set_config", "hydra_get_config",
             "hydra_last_error", "hydra_version", "hydra_append_kv", "hydra_suffix_attn_paged", "hydra_attn_paged",
-            "hydra_append_kv_paged", "hydra_tree_attn_paged", "hydra_tree_prepare", "hydra_debug_lens_violations"]
+            "hydra_append_kv_paged", "hydra_tree_attn_paged", "hydra_tree_prepare", "hydra_debug_lens_violations",
+            "hydra_combine_ex"]
 
 
 class HydraError(RuntimeError):
@@ -44,6 +45,19 @@ class Paging(ctypes.Structure):
     """hydra_paging (include/hydra.h): block table [B, bt_stride] of a paged suffix cache."""
     _fields_ = [("block_table", ctypes.c_void_p), ("bt_stride", ctypes.c_int64), ("page_size", ctypes.c_int32),
                 ("n_pages", ctypes.c_int64)]
+
+
+class CombineDesc(ctypes.Structure):
+    """hydra_combine_desc (include/hydra.h): two part groups with part / row strides."""
+    _fields_ = [("rows", ctypes.c_int64), ("d", ctypes.c_int32), ("n_parts", ctypes.c_int32),
+                ("o_parts", ctypes.c_void_p), ("o_dtype", ctypes.c_int32), ("o_part_stride", ctypes.c_int64),
+                ("o_row_stride", ctypes.c_int64), ("lse_parts", ctypes.c_void_p), ("lse_part_stride", ctypes.c_int64),
+                ("lse_row_stride", ctypes.c_int64), ("n_parts_f32", ctypes.c_int32), ("o_parts_f32", ctypes.c_void_p),
+                ("o_f32_part_stride", ctypes.c_int64), ("o_f32_row_stride", ctypes.c_int64),
+                ("lse_parts_f32", ctypes.c_void_p), ("lse_f32_part_stride", ctypes.c_int64),
+                ("lse_f32_row_stride", ctypes.c_int64), ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32),
+                ("out_row_stride", ctypes.c_int64), ("lse_out", ctypes.c_void_p),
+                ("lse_out_row_stride", ctypes.c_int64)]
 
 
 _lib = None
@@ -67,6 +81,7 @@ def load():
         "hydra_suffix_attn": (st, [_HP, _i64, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp,
                                    _vp, _sz, _vp]),
         "hydra_combine": (st, [_i64, _i32, _i32, _vp, _i32, _i64, _vp, _i64, _vp, _i32, _vp, _vp]),
+        "hydra_combine_ex": (st, [ctypes.POINTER(CombineDesc), _vp]),
         "hydra_attn": (st, [_HP, _i64, _vp, _i64, _i64, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _i64, _i64,
                             _i64, _vp, _vp, _i32, _vp, _vp, _sz, _vp, _vp]),
         "hydra_tree_create": (st, [_vp, _vp, _vp, _i32, _vp, _i64, ctypes.POINTER(_vp)]),

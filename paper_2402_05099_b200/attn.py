@@ -315,40 +315,64 @@ def hydragen_attention_paged(q: torch.Tensor, prefix_k: torch.Tensor, prefix_v: 
 
 
 def combine(o_parts: torch.Tensor, lse_parts: torch.Tensor, out_dtype=torch.bfloat16, return_lse: bool = True,
-            out: Optional[torch.Tensor] = None, lse_out: Optional[torch.Tensor] = None, stream=None):
-    """n-ary LSE combine (Eq. 5 / App. B combine_lse).
+            out: Optional[torch.Tensor] = None, lse_out: Optional[torch.Tensor] = None, stream=None,
+            o_parts_f32: Optional[torch.Tensor] = None, lse_parts_f32: Optional[torch.Tensor] = None):
+    """n-ary LSE combine (Eq. 5 / App. B combine_lse), hydra_combine_ex.
 
-    o_parts: [n, rows, d] (f32 or f16, rows may be any leading shape flattened; parts may
-    sit at any stride, e.g. slices of an all-gathered exchange buffer), lse_parts: [n, rows]
-    f32.  Returns (out [rows, d] in out_dtype, lse [rows] f32).  out_dtype float16 (from f32
+    o_parts: [n, rows, d] (f32 or f16; any part and row strides, head dim contiguous -- e.g.
+    slices of an exchange buffer whose rows interleave O and LSE), lse_parts: [n, rows] f32
+    (any strides).  Optional second group o_parts_f32 [m, rows, d] / lse_parts_f32 [m, rows]
+    in f32, merged in the same pass.  out: [rows, d] with a contiguous head dim (row stride
+    free); lse_out: [rows] (any stride).  Returns (out, lse).  out_dtype float16 (from f32
     parts) packs partials for a cross-GPU exchange.
     """
-    n = o_parts.shape[0]
     d = o_parts.shape[-1]
-    o2 = o_parts.reshape(n, -1, d)
-    l2 = lse_parts.reshape(n, -1)
-    rows = o2.shape[1]
+    o2 = o_parts if o_parts.dim() == 3 else o_parts.reshape(o_parts.shape[0], -1, d)
+    l2 = lse_parts if lse_parts.dim() == 2 else lse_parts.reshape(lse_parts.shape[0], -1)
+    n, rows = o2.shape[0], o2.shape[1]
     if o2.dtype not in (torch.float32, torch.float16):
         raise TypeError("o_parts must be f32 or f16")
-    if l2.shape[1] != rows or l2.dtype != torch.float32:
-        raise ValueError("lse_parts must be f32 with one value per row of each part")
-    if o2.stride(2) != 1 or (rows > 1 and o2.stride(1) != d) or (rows > 1 and l2.stride(1) != 1):
-        raise ValueError("parts must be row-contiguous")
+    if l2.dtype != torch.float32 or tuple(l2.shape) != (n, rows):
+        raise ValueError("lse_parts must be f32 [n, rows] with one value per row of each part")
+    if o2.stride(2) != 1:
+        raise ValueError("the head dim of o_parts must be contiguous")
+    m = 0
+    if o_parts_f32 is not None:
+        if o_parts_f32.dtype != torch.float32 or o_parts_f32.dim() != 3 or o_parts_f32.shape[1:] != (rows, d) \
+                or o_parts_f32.stride(2) != 1:
+            raise ValueError("o_parts_f32 must be f32 [m, rows, d] with a contiguous head dim")
+        m = o_parts_f32.shape[0]
+        if lse_parts_f32 is None or lse_parts_f32.dtype != torch.float32 or tuple(lse_parts_f32.shape) != (m, rows):
+            raise ValueError("lse_parts_f32 must be f32 [m, rows]")
     if out is None:
         out = torch.empty(rows, d, dtype=out_dtype, device=o_parts.device)
     if out.dtype not in (torch.bfloat16, torch.float32, torch.float16):
         raise TypeError("out must be bf16, f32 or (from f32 parts) f16")
-    if out.numel() != rows * d or not out.is_contiguous():
-        raise ValueError("out must be a contiguous [rows, d] tensor")
+    out2 = out.reshape(rows, d) if out.is_contiguous() and out.numel() == rows * d else out
+    if tuple(out2.shape) != (rows, d) or out2.stride(1) != 1:
+        raise ValueError("out must be a [rows, d] tensor with a contiguous head dim")
     lse = lse_out if lse_out is not None else (
         torch.empty(rows, dtype=torch.float32, device=o_parts.device) if return_lse else None)
-    if lse is not None and (lse.dtype != torch.float32 or lse.numel() != rows or not lse.is_contiguous()):
-        raise ValueError("lse_out must be a contiguous f32 tensor of one value per row")
-    _require_cuda(o_parts, lse_parts, out, lse)
+    lse2 = None
+    if lse is not None:
+        lse2 = lse.reshape(rows) if lse.is_contiguous() and lse.numel() == rows else lse
+        if lse2.dtype != torch.float32 or tuple(lse2.shape) != (rows,):
+            raise ValueError("lse_out must be an f32 tensor of one value per row")
+    _require_cuda(o_parts, lse_parts, out, lse, o_parts_f32, lse_parts_f32)
+    c = _lib.CombineDesc()
+    c.rows, c.d, c.n_parts = rows, d, n
+    c.o_parts, c.o_dtype, c.o_part_stride, c.o_row_stride = o2.data_ptr(), _DT[o2.dtype], o2.stride(0), o2.stride(1)
+    c.lse_parts, c.lse_part_stride, c.lse_row_stride = l2.data_ptr(), l2.stride(0), l2.stride(1)
+    if m:
+        c.n_parts_f32, c.o_parts_f32 = m, o_parts_f32.data_ptr()
+        c.o_f32_part_stride, c.o_f32_row_stride = o_parts_f32.stride(0), o_parts_f32.stride(1)
+        c.lse_parts_f32 = lse_parts_f32.data_ptr()
+        c.lse_f32_part_stride, c.lse_f32_row_stride = lse_parts_f32.stride(0), lse_parts_f32.stride(1)
+    c.out, c.out_dtype, c.out_row_stride = out2.data_ptr(), _DT[out2.dtype], out2.stride(0)
+    if lse2 is not None:
+        c.lse_out, c.lse_out_row_stride = lse2.data_ptr(), lse2.stride(0)
     with _on(o_parts.device):
-        check(_lib.load().hydra_combine(rows, d, n, o2.data_ptr(), _DT[o2.dtype], o2.stride(0), l2.data_ptr(),
-                                        l2.stride(0), out.data_ptr(), _DT[out.dtype], _ptr(lse),
-                                        _stream_ptr(stream, o_parts.device)), "hydra_combine")
+        check(_lib.load().hydra_combine_ex(ctypes.byref(c), _stream_ptr(stream, o_parts.device)), "hydra_combine_ex")
     return out, lse
 
 

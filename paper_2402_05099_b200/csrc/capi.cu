@@ -518,13 +518,17 @@ static hydra_status run_combine(int64_t rows, int d, int n, const PartsView &src
   CombineParams c{};
   c.rows = rows;
   c.d = d;
-  c.n_parts = n;
-  c.o_parts = src.o;
-  c.o_part_stride = src.o_stride;
-  c.lse_parts = src.lse;
-  c.lse_part_stride = src.lse_stride;
+  c.n_a = n;
+  c.o_a = src.o;
+  c.o_a_part = src.o_stride;
+  c.o_a_row = d;
+  c.l_a = src.lse;
+  c.l_a_part = src.lse_stride;
+  c.l_a_row = 1;
   c.out = out;
+  c.out_row = d;
   c.lse_out = lse_out;
+  c.lse_out_row = 1;
   c.inject_bug = inject_combine_bug() ? 1 : 0;
   hydra_status st = launch_combine(c, HYDRA_F32, out_dtype, s);
   return st == HYDRA_OK ? st : cuda_fail("combine launch");
@@ -651,33 +655,81 @@ extern "C" hydra_status hydra_suffix_attn_paged(const hydra_heads *h, int64_t B,
                      ws_bytes, stream, S_cap > 0 ? pg : nullptr);
 }
 
+extern "C" hydra_status hydra_combine_ex(const hydra_combine_desc *c, void *stream) {
+  if (!c) return fail(HYDRA_EINVAL, "combine descriptor is NULL");
+  const int64_t d = c->d;
+  if (c->rows < 0 || d <= 0 || c->n_parts < 0 || c->n_parts_f32 < 0 || c->n_parts + c->n_parts_f32 <= 0)
+    return fail(HYDRA_ESHAPE, "rows >= 0, d > 0 and at least one part required");
+  if ((c->n_parts > 0 && (!c->o_parts || !c->lse_parts)) ||
+      (c->n_parts_f32 > 0 && (!c->o_parts_f32 || !c->lse_parts_f32)) || !c->out)
+    return fail(HYDRA_EINVAL, "null pointer argument");
+  if (c->n_parts > 0 && c->o_dtype != HYDRA_F32 && c->o_dtype != HYDRA_F16)
+    return fail(HYDRA_EUNSUPPORTED, "o_dtype must be F32 or F16");
+  const hydra_dtype od = c->n_parts > 0 ? c->o_dtype : HYDRA_F32;
+  if (c->out_dtype != HYDRA_F32 && c->out_dtype != HYDRA_BF16 && !(c->out_dtype == HYDRA_F16 && od == HYDRA_F32))
+    return fail(HYDRA_EUNSUPPORTED, "out_dtype must be F32 or BF16 (F16 only from F32 parts)");
+  const int64_t o_row = c->o_row_stride ? c->o_row_stride : d, of_row = c->o_f32_row_stride ? c->o_f32_row_stride : d;
+  const int64_t l_row = c->lse_row_stride ? c->lse_row_stride : 1;
+  const int64_t lf_row = c->lse_f32_row_stride ? c->lse_f32_row_stride : 1;
+  const int64_t out_row = c->out_row_stride ? c->out_row_stride : d, lo_row = c->lse_out_row_stride ? c->lse_out_row_stride : 1;
+  if (o_row < d || of_row < d || out_row < d || l_row < 1 || lf_row < 1 || lo_row < 1 || c->o_part_stride < 0 ||
+      c->lse_part_stride < 0 || c->o_f32_part_stride < 0 || c->lse_f32_part_stride < 0)
+    return fail(HYDRA_ESHAPE, "row strides must cover a row (O >= d, LSE >= 1) and part strides be >= 0");
+  if (d == 128 || d == 256) {  // vector loads: 16 B of f32 or 8 B of f16 per lane
+    const int64_t a = od == HYDRA_F16 ? 8 : 16, es = od == HYDRA_F16 ? 2 : 4;
+    if (c->n_parts > 0 && (reinterpret_cast<uintptr_t>(c->o_parts) % a || (c->o_part_stride * es) % a ||
+                           (o_row * es) % a))
+      return fail(HYDRA_EINVAL, "o_parts and its strides must be %d-byte aligned", (int)a);
+    if (c->n_parts_f32 > 0 && (reinterpret_cast<uintptr_t>(c->o_parts_f32) % 16 || (c->o_f32_part_stride * 4) % 16 ||
+                               (of_row * 4) % 16))
+      return fail(HYDRA_EINVAL, "o_parts_f32 and its strides must be 16-byte aligned");
+  }
+  CombineParams p{};
+  p.rows = c->rows;
+  p.d = (int32_t)d;
+  p.n_a = c->n_parts;
+  p.o_a = c->o_parts;
+  p.o_a_part = c->o_part_stride;
+  p.o_a_row = o_row;
+  p.l_a = c->lse_parts;
+  p.l_a_part = c->lse_part_stride;
+  p.l_a_row = l_row;
+  p.n_b = c->n_parts_f32;
+  p.o_b = c->o_parts_f32;
+  p.o_b_part = c->o_f32_part_stride;
+  p.o_b_row = of_row;
+  p.l_b = c->lse_parts_f32;
+  p.l_b_part = c->lse_f32_part_stride;
+  p.l_b_row = lf_row;
+  p.out = c->out;
+  p.out_row = out_row;
+  p.lse_out = c->lse_out;
+  p.lse_out_row = lo_row;
+  p.inject_bug = inject_combine_bug() ? 1 : 0;
+  hydra_status st = launch_combine(p, od, c->out_dtype, reinterpret_cast<cudaStream_t>(stream));
+  return st == HYDRA_OK ? st : cuda_fail("combine launch");
+}
+
 extern "C" hydra_status hydra_combine(int64_t rows, int32_t d, int32_t n_parts, const void *o_parts,
                                       hydra_dtype o_dtype, int64_t o_part_stride, const float *lse_parts,
                                       int64_t lse_part_stride, void *out, hydra_dtype out_dtype, float *lse_out,
                                       void *stream) {
   if (rows < 0 || d <= 0 || n_parts <= 0) return fail(HYDRA_ESHAPE, "rows >= 0, d > 0, n_parts > 0 required");
-  if (!o_parts || !lse_parts || !out) return fail(HYDRA_EINVAL, "null pointer argument");
-  if (o_dtype != HYDRA_F32 && o_dtype != HYDRA_F16) return fail(HYDRA_EUNSUPPORTED, "o_dtype must be F32 or F16");
-  if (out_dtype != HYDRA_F32 && out_dtype != HYDRA_BF16 && !(out_dtype == HYDRA_F16 && o_dtype == HYDRA_F32))
-    return fail(HYDRA_EUNSUPPORTED, "out_dtype must be F32 or BF16 (F16 only from F32 parts)");
   if (n_parts > 1 && (o_part_stride < rows * d || lse_part_stride < rows))
     return fail(HYDRA_ESHAPE, "part strides overlap the rows of a part");
-  if ((d == 128 || d == 256) && (reinterpret_cast<uintptr_t>(o_parts) % 16 ||
-                                 (o_part_stride * (int64_t)elem_size(o_dtype == HYDRA_F16 ? HYDRA_BF16 : HYDRA_F32)) % 16))
-    return fail(HYDRA_EINVAL, "o_parts and o_part_stride must be 16-byte aligned");
-  CombineParams c{};
+  hydra_combine_desc c{};
   c.rows = rows;
   c.d = d;
   c.n_parts = n_parts;
   c.o_parts = o_parts;
+  c.o_dtype = o_dtype;
   c.o_part_stride = o_part_stride;
   c.lse_parts = lse_parts;
   c.lse_part_stride = lse_part_stride;
   c.out = out;
+  c.out_dtype = out_dtype;
   c.lse_out = lse_out;
-  c.inject_bug = inject_combine_bug() ? 1 : 0;
-  hydra_status st = launch_combine(c, o_dtype, out_dtype, reinterpret_cast<cudaStream_t>(stream));
-  return st == HYDRA_OK ? st : cuda_fail("combine launch");
+  return hydra_combine_ex(&c, stream);
 }
 
 // ------------------------------------------------------------------ composite

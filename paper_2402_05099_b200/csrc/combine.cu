@@ -1,13 +1,16 @@
 // combine.cu -- n-ary LSE combine (Eq. 5 P:98-105 in App. B's
 // max-stabilised form P:333-344, folded over n parts; associativity S:154).
 //
-// One warp per output row.  For row r:
-//   m   = max_p lse_p[r]                     (parts with lse = -inf are empty: skipped)
+// For row r over the parts p (parts with lse = -inf are empty: skipped, their O never used):
+//   m   = max_p lse_p[r]
 //   w_p = exp(lse_p[r] - m)
-//   O   = sum_p w_p * O_p[r] / sum_p w_p     -> out (bf16 RNE or f32)
+//   O   = sum_p w_p * O_p[r] / sum_p w_p     -> out (bf16 RNE, f32, or f16 for packing)
 //   lse = m + ln(sum_p w_p)                  (the merged LSE a recursive combine needs)
-// Partial outputs are read with 16-byte vector loads (d % 128 == 0 for f32 parts,
-// d % 256 == 0 for f16 parts), otherwise element-wise.  HBM-bound: it reads
+// The parts come in two groups: group A in o_dtype (f32, or f16 partials received from
+// other GPUs) and an optional group B in f32 (e.g. the local suffix partial merged with the
+// received prefix pieces in the same pass).  Every pointer has a part stride and a row
+// stride, so the kernel reads an exchange buffer whose rows interleave O and LSE in place,
+// and writes such a buffer (dist.py's packed (O f16 | LSE f32) rows).  HBM-bound: it reads
 // n*(d*sizeof(O)+4) and writes d*sizeof(out)(+4) bytes per row.
 #include "common.cuh"
 #include "internal.h"
@@ -21,47 +24,65 @@ __device__ __forceinline__ float ld_part<float>(const float *p) { return __ldg(p
 template <>
 __device__ __forceinline__ float ld_part<__half>(const __half *p) { return __half2float(__ldg(p)); }
 
+template <typename OT>
+__device__ __forceinline__ const void *part_o(const CombineParams &p, int q, int64_t row) {
+  if (q < p.n_a) return reinterpret_cast<const OT *>(p.o_a) + q * p.o_a_part + row * p.o_a_row;
+  return p.o_b + (q - p.n_a) * p.o_b_part + row * p.o_b_row;
+}
+__device__ __forceinline__ float part_lse(const CombineParams &p, int q, int64_t row) {
+  return q < p.n_a ? __ldg(p.l_a + q * p.l_a_part + row * p.l_a_row)
+                   : __ldg(p.l_b + (q - p.n_a) * p.l_b_part + row * p.l_b_row);
+}
+// 4 consecutive elements of part q's row (16-B aligned for f32, 8-B for f16)
+template <typename OT>
+__device__ __forceinline__ void ld4(const CombineParams &p, int q, int64_t row, int e, float *f) {
+  if (q < p.n_a && sizeof(OT) == 2) {
+    const __half *src = reinterpret_cast<const __half *>(part_o<OT>(p, q, row)) + e;
+    const uint2 v = __ldg(reinterpret_cast<const uint2 *>(src));
+    const __half2 a = *reinterpret_cast<const __half2 *>(&v.x);
+    const __half2 b = *reinterpret_cast<const __half2 *>(&v.y);
+    f[0] = __low2float(a); f[1] = __high2float(a); f[2] = __low2float(b); f[3] = __high2float(b);
+  } else {
+    const float *src = reinterpret_cast<const float *>(part_o<OT>(p, q, row)) + e;
+    const float4 v = __ldg(reinterpret_cast<const float4 *>(src));
+    f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w;
+  }
+}
+template <typename OT>
+__device__ __forceinline__ float ld1(const CombineParams &p, int q, int64_t row, int e) {
+  if (q < p.n_a) return ld_part<OT>(reinterpret_cast<const OT *>(part_o<OT>(p, q, row)) + e);
+  return __ldg(reinterpret_cast<const float *>(part_o<OT>(p, q, row)) + e);
+}
+
+// General kernel: any number of parts, VEC floats per lane (VEC = 0: element-wise, any d).
 template <typename OT, typename OutT, int VEC>
 __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
   const int64_t row = (int64_t)blockIdx.x * 8 + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   if (row >= p.rows) return;
-  const OT *o_parts = reinterpret_cast<const OT *>(p.o_parts);
-
+  const int n = p.n_a + p.n_b;
   float m = -INFINITY;
-  for (int q = 0; q < p.n_parts; ++q) m = fmaxf(m, __ldg(p.lse_parts + q * p.lse_part_stride + row));
-  OutT *out = reinterpret_cast<OutT *>(p.out) + row * p.d;
+  for (int q = 0; q < n; ++q) m = fmaxf(m, part_lse(p, q, row));
+  OutT *out = reinterpret_cast<OutT *>(p.out) + row * p.out_row;
   if (m == -INFINITY) {  // every part empty: sentinel (0, -inf)
     for (int e = lane; e < p.d; e += 32) out[e] = OutT(0.f);
-    if (p.lse_out && lane == 0) p.lse_out[row] = -INFINITY;
+    if (p.lse_out && lane == 0) p.lse_out[row * p.lse_out_row] = -INFINITY;
     return;
   }
-  float acc[VEC > 0 ? VEC : 1];
-  const int per_lane = VEC > 0 ? VEC : 0;
-  (void)per_lane;
   float den = 0.f;
   if constexpr (VEC > 0) {
+    float acc[VEC];
 #pragma unroll
     for (int i = 0; i < VEC; ++i) acc[i] = 0.f;
-    for (int q = 0; q < p.n_parts; ++q) {
-      const float lq = __ldg(p.lse_parts + q * p.lse_part_stride + row);
+    for (int q = 0; q < n; ++q) {
+      const float lq = part_lse(p, q, row);
       if (lq == -INFINITY) continue;
       const float w = p.inject_bug ? 1.f : expf(lq - m);
       den += w;
-      const OT *src = o_parts + q * p.o_part_stride + row * p.d;
 #pragma unroll
       for (int c = 0; c < VEC / 4; ++c) {
-        const int e = (c * 32 + lane) * 4;
         float f[4];
-        if constexpr (sizeof(OT) == 4) {
-          const float4 v = __ldg(reinterpret_cast<const float4 *>(src + e));
-          f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w;
-        } else {
-          const uint2 v = __ldg(reinterpret_cast<const uint2 *>(src + e));
-          const __half2 a = *reinterpret_cast<const __half2 *>(&v.x);
-          const __half2 b = *reinterpret_cast<const __half2 *>(&v.y);
-          f[0] = __low2float(a); f[1] = __high2float(a); f[2] = __low2float(b); f[3] = __high2float(b);
-        }
+        ld4<OT>(p, q, row, (c * 32 + lane) * 4, f);
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[c * 4 + i] = fmaf(w, f[i], acc[c * 4 + i]);
       }
@@ -74,30 +95,30 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
       for (int i = 0; i < 4; ++i) out[e + i] = OutT(acc[c * 4 + i] * inv);
     }
   } else {
-    for (int q = 0; q < p.n_parts; ++q) {
-      const float lq = __ldg(p.lse_parts + q * p.lse_part_stride + row);
+    for (int q = 0; q < n; ++q) {
+      const float lq = part_lse(p, q, row);
       if (lq != -INFINITY) den += p.inject_bug ? 1.f : expf(lq - m);
     }
     const float inv = 1.f / den;
     for (int e = lane; e < p.d; e += 32) {
       float a = 0.f;
-      for (int q = 0; q < p.n_parts; ++q) {
-        const float lq = __ldg(p.lse_parts + q * p.lse_part_stride + row);
+      for (int q = 0; q < n; ++q) {
+        const float lq = part_lse(p, q, row);
         if (lq == -INFINITY) continue;
         const float w = p.inject_bug ? 1.f : expf(lq - m);
-        a = fmaf(w, ld_part<OT>(o_parts + q * p.o_part_stride + row * p.d + e), a);
+        a = fmaf(w, ld1<OT>(p, q, row, e), a);
       }
       out[e] = OutT(a * inv);
     }
   }
-  if (p.lse_out && lane == 0) p.lse_out[row] = m + logf(den);
+  if (p.lse_out && lane == 0) p.lse_out[row * p.lse_out_row] = m + logf(den);
 }
 
-// d = 128, n_parts <= 8: the same arithmetic with the memory latency paid twice per row
-// instead of twice per part -- all LSEs loaded together, then all non-empty parts' 512-B
-// rows together (16 B per lane), then the weighted sum.  The part loop of combine_kernel
-// serialises a dependent LSE load and O load per part, so with 3-8 parts it ran at 30-50 %
-// of HBM bandwidth (e.g. 22 us instead of ~12 at C3).
+// d = 128, at most 8 parts: the same arithmetic with the memory latency paid twice per row
+// instead of twice per part -- all LSEs loaded together, then all parts' 512-B rows together
+// (16 B per lane), then the weighted sum.  The part loop of combine_kernel serialises a
+// dependent LSE load and O load per part, so with 3-8 parts it ran at 30-50 % of HBM
+// bandwidth (e.g. 22 us instead of ~12 at C3).
 template <typename OT, typename OutT, int NP, int RPW>
 __global__ void __launch_bounds__(256) combine_kernel_p8(const CombineParams p) {
   // NP: parts rounded up (2, 4 or 8); RPW rows per warp.  Every part's LSE and O loads of all
@@ -107,7 +128,7 @@ __global__ void __launch_bounds__(256) combine_kernel_p8(const CombineParams p) 
   const int64_t row0 = ((int64_t)blockIdx.x * 8 + threadIdx.x / 32) * RPW;
   const int lane = threadIdx.x % 32;
   if (row0 >= p.rows) return;
-  const OT *o_parts = reinterpret_cast<const OT *>(p.o_parts);
+  const int n = p.n_a + p.n_b;
   float lq[RPW][NP], f[RPW][NP][4];
 #pragma unroll
   for (int k = 0; k < RPW; ++k) {
@@ -115,19 +136,9 @@ __global__ void __launch_bounds__(256) combine_kernel_p8(const CombineParams p) 
 #pragma unroll
     for (int q = 0; q < NP; ++q) {
       lq[k][q] = -INFINITY;
-      if (q < p.n_parts && row < p.rows) {
-        lq[k][q] = __ldg(p.lse_parts + q * p.lse_part_stride + row);
-        const OT *src = o_parts + q * p.o_part_stride + row * p.d + lane * 4;
-        if constexpr (sizeof(OT) == 4) {
-          const float4 v = __ldg(reinterpret_cast<const float4 *>(src));
-          f[k][q][0] = v.x; f[k][q][1] = v.y; f[k][q][2] = v.z; f[k][q][3] = v.w;
-        } else {
-          const uint2 v = __ldg(reinterpret_cast<const uint2 *>(src));
-          const __half2 a = *reinterpret_cast<const __half2 *>(&v.x);
-          const __half2 b = *reinterpret_cast<const __half2 *>(&v.y);
-          f[k][q][0] = __low2float(a); f[k][q][1] = __high2float(a);
-          f[k][q][2] = __low2float(b); f[k][q][3] = __high2float(b);
-        }
+      if (q < n && row < p.rows) {
+        lq[k][q] = part_lse(p, q, row);
+        ld4<OT>(p, q, row, lane * 4, f[k][q]);
       }
     }
   }
@@ -138,11 +149,11 @@ __global__ void __launch_bounds__(256) combine_kernel_p8(const CombineParams p) 
     float m = -INFINITY;
 #pragma unroll
     for (int q = 0; q < NP; ++q) m = fmaxf(m, lq[k][q]);
-    OutT *out = reinterpret_cast<OutT *>(p.out) + row * p.d;
+    OutT *out = reinterpret_cast<OutT *>(p.out) + row * p.out_row;
     if (m == -INFINITY) {  // every part empty: sentinel (0, -inf)
 #pragma unroll
       for (int i = 0; i < 4; ++i) out[lane * 4 + i] = OutT(0.f);
-      if (p.lse_out && lane == 0) p.lse_out[row] = -INFINITY;
+      if (p.lse_out && lane == 0) p.lse_out[row * p.lse_out_row] = -INFINITY;
       continue;
     }
     float acc[4] = {0.f, 0.f, 0.f, 0.f}, den = 0.f;
@@ -157,7 +168,7 @@ __global__ void __launch_bounds__(256) combine_kernel_p8(const CombineParams p) 
     const float inv = 1.f / den;
 #pragma unroll
     for (int i = 0; i < 4; ++i) out[lane * 4 + i] = OutT(acc[i] * inv);
-    if (p.lse_out && lane == 0) p.lse_out[row] = m + logf(den);
+    if (p.lse_out && lane == 0) p.lse_out[row * p.lse_out_row] = m + logf(den);
   }
 }
 
@@ -165,11 +176,12 @@ template <typename OT, typename OutT>
 static cudaError_t launch_c(const CombineParams &p, cudaStream_t s) {
   const dim3 grid((unsigned)((p.rows + 7) / 8));
   const dim3 grid2((unsigned)((p.rows + 15) / 16));  // two rows per warp
-  if (p.d == 128 && p.n_parts <= 2)
+  const int n = p.n_a + p.n_b;
+  if (p.d == 128 && n <= 2)
     combine_kernel_p8<OT, OutT, 2, 2><<<grid2, 256, 0, s>>>(p);
-  else if (p.d == 128 && p.n_parts <= 4)
+  else if (p.d == 128 && n <= 4)
     combine_kernel_p8<OT, OutT, 4, 2><<<grid2, 256, 0, s>>>(p);
-  else if (p.d == 128 && p.n_parts <= 8)
+  else if (p.d == 128 && n <= 8)
     combine_kernel_p8<OT, OutT, 8, 2><<<grid2, 256, 0, s>>>(p);
   else if (p.d == 128)
     combine_kernel<OT, OutT, 4><<<grid, 256, 0, s>>>(p);

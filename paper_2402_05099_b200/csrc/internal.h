@@ -61,16 +61,25 @@ struct DecodeParams {
 hydra_status launch_decode(const DecodeParams &p, hydra_dtype dt, int d, cudaStream_t s);
 
 // ---------------------------------------------------------------- combine
+// Two part groups: A (o_dtype: f32 or f16) and B (f32, may be empty); strides in elements.
 struct CombineParams {
   int64_t rows;
-  int32_t d, n_parts;
-  const void *o_parts;
-  int64_t o_part_stride;
-  const float *lse_parts;
-  int64_t lse_part_stride;
+  int32_t d;
+  int32_t n_a;
+  const void *o_a;
+  int64_t o_a_part, o_a_row;
+  const float *l_a;
+  int64_t l_a_part, l_a_row;
+  int32_t n_b;
+  const float *o_b;
+  int64_t o_b_part, o_b_row;
+  const float *l_b;
+  int64_t l_b_part, l_b_row;
   void *out;
+  int64_t out_row;
   float *lse_out;
-  int32_t inject_bug;
+  int64_t lse_out_row;
+  int32_t inject_bug;  // testing build only: w_p = 1 (the sabotage of S:522)
 };
 hydra_status launch_combine(const CombineParams &p, hydra_dtype o_dtype, hydra_dtype out_dtype,
                             cudaStream_t s);

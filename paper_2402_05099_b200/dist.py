@@ -5,28 +5,35 @@ Two ways the shared-prefix decode attention shards (SURVEY §8(e)
 * **KV-head sharding** (`head_shard`, `head_sharded_attention`): rank r owns KV heads
   [r*Hkv/N, (r+1)*Hkv/N) and their g*Hkv/N query heads, with their prefix and suffix
   K/V slices.  There is no collective: this is the tensor-parallel layout of the paper's
-  end-to-end runs; the output stays head-sharded for the output projection.
+  end-to-end runs; the output stays head-sharded for the output projection.  The
+  library takes strided tensors, so a rank's head slice of full-width tensors is passed
+  without a copy.
 
-* **Prefix sequence split** (`seqsplit_attention`), for a very long prefix with few KV
-  heads (Yi-6B has 4 KV heads, so head sharding stops at 4 GPUs): rank r owns
-  prefix tokens [r*P/N, (r+1)*P/N) for all heads and the batch shard
-  [r*B/N, (r+1)*B/N) of the suffixes.  Each rank
+* **Prefix sequence split** (`SeqSplit`, `seqsplit_attention`), for a very long prefix with
+  few KV heads (Yi-6B has 4 KV heads, so head sharding stops at 4 GPUs): rank r owns
+  prefix tokens [r*P/N, (r+1)*P/N) for all heads and the batch shard `batch_shard(B, N, r)`
+  of the suffixes.  Per decode step each rank
     1. attends all B*g stacked queries to its prefix shard (tcgen05 prefix kernel),
-    2. packs (O fp16, LSE fp32) of all rows (the combine kernel doing a 1-part combine with
-       an f16 output); the rows of each destination rank's batch shard are contiguous,
-    3. exchanges them all-to-all over NCCL (NVLink / NVSwitch): every rank receives only the
-       N pieces of its own batch shard's rows -- 1/N of what an all-gather moves
-       (`exchange="allgather"` keeps the all-gather of whole blocks for comparison),
-    4. runs suffix attention for its batch shard,
-    5. merges the N prefix pieces of its rows straight out of the received buffer
-       (strided parts), then merges that with its suffix part -- both with the Eq. 5
-       combine kernel, exactly as the single-GPU decomposition.
-  fp16 (not bf16) is used for exchanged O: |O_r| <= max|V|, and fp16's 11-bit mantissa
-  keeps the delivered bf16 output inside the parity gate.
+    2. packs every row's (O, LSE) into one exchange buffer with ONE combine launch: rows of
+       [O (fp16, d) | LSE (f32) | pad] (272 B at d = 128), batch shard c's rows contiguous,
+    3. exchanges it with ONE all-to-all (NCCL over NVLink / NVSwitch): every rank receives
+       only the N pieces of its own batch shard's rows -- B*Hq*272 bytes per rank in total,
+       1/N of what an all-gather moves (`exchange="allgather"` is kept for comparison),
+    4. meanwhile runs suffix attention for its batch shard on a second stream (it needs no
+       prefix data), so the suffix overlaps the exchange,
+    5. merges the N received prefix pieces and its suffix part in ONE Eq. 5 combine launch
+       (hydra_combine_ex: f16 parts read in place from the received rows + one f32 part).
+  fp16 (not bf16) carries the exchanged O: |O_r| <= max|V| for a normalised partial, and
+  fp16's 11-bit mantissa keeps the delivered bf16 output inside the parity gate (SURVEY
+  §8(c)); an |O_r| beyond fp16's range (|V| > 65504) is detected after the pack and raises
+  (`exchange_dtype=torch.float32` moves 528-byte rows instead).
 
-The kernel calls go through an `ops` object (default: the CUDA library) so the
-orchestration -- shard ranges, exchange layout, strides -- is exercised by world-size-2
-gloo tests on CPU with reference ops.
+With a gloo process group and CUDA tensors (the CPU-side tests of the CUDA path: two ranks
+sharing one GPU), the exchange is staged through pinned host memory; with NCCL the whole
+step, exchange included, is CUDA-graph capturable.  All buffers belong to the `SeqSplit`
+plan and are allocated once.  The kernel calls go through an `ops` object (default: the
+CUDA library), so the orchestration is also exercised by world-size-2/3 gloo tests on CPU
+with fp64 oracle ops.
 """
 from __future__ import annotations
 
@@ -37,10 +44,17 @@ import torch.distributed as dist
 
 
 def shard_range(n: int, world: int, rank: int) -> Tuple[int, int]:
-    """Contiguous near-equal split of range(n) across `world` ranks."""
+    """Contiguous near-equal split of range(n) across `world` ranks (prefix tokens, heads)."""
     base, rem = divmod(n, world)
     lo = rank * base + min(rank, rem)
     return lo, lo + base + (1 if rank < rem else 0)
+
+
+def batch_shard(B: int, world: int, rank: int) -> Tuple[int, int]:
+    """Batch shard of the sequence split: ceil(B/N) sequences per rank, so every rank's rows
+    form one contiguous slot of the exchange buffer (the last ranks may hold fewer, or none)."""
+    mb = -(-B // world)
+    return min(B, rank * mb), min(B, (rank + 1) * mb)
 
 
 def head_shard(Hq: int, Hkv: int, world: int, rank: int):
@@ -60,115 +74,192 @@ class KernelOps:
 
         self._a = attn
 
-    def prefix(self, q, k, v, scale=None):
-        return self._a.prefix_attn(q, k, v, scale=scale)
+    def prefix(self, q, k, v, scale=None, out=None, lse_out=None):
+        return self._a.prefix_attn(q, k, v, scale=scale, out=out, lse_out=lse_out)
 
     def suffix(self, q, k, v, lens, scale=None, out=None, lse_out=None):
         return self._a.suffix_attn(q, k, v, lens, scale=scale, out=out, lse_out=lse_out)
 
-    def combine(self, o_parts, lse_parts, out_dtype=torch.bfloat16, out=None, lse_out=None):
-        return self._a.combine(o_parts, lse_parts, out_dtype=out_dtype, out=out, lse_out=lse_out)
+    def combine(self, o_parts, lse_parts, out_dtype=torch.bfloat16, out=None, lse_out=None, o_parts_f32=None,
+                lse_parts_f32=None):
+        return self._a.combine(o_parts, lse_parts, out_dtype=out_dtype, out=out, lse_out=lse_out,
+                               o_parts_f32=o_parts_f32, lse_parts_f32=lse_parts_f32)
 
-    def attention(self, q, pk, pv, sk, sv, lens, scale=None):
-        return self._a.hydragen_attention(q, pk, pv, sk, sv, lens, scale=scale)
+    def attention(self, q, pk, pv, sk, sv, lens, scale=None, out=None):
+        return self._a.hydragen_attention(q, pk, pv, sk, sv, lens, scale=scale, out=out)
 
 
-def head_sharded_attention(q_local, pk_local, pv_local, sk_local, sv_local, lens, scale=None, ops=None):
-    """Attention for this rank's KV-head shard (no communication)."""
+def head_sharded_attention(q, pk, pv, sk, sv, lens, scale=None, ops=None, world: Optional[int] = None,
+                           rank: Optional[int] = None, out=None):
+    """Attention for one rank's KV-head shard (no communication).
+
+    With world/rank None the tensors are this rank's shard already.  Otherwise they hold all
+    heads and the rank's slice (q[:, h0:h1], K/V[..., j0:j1, :]) is passed as strided views --
+    no copy -- and the output [B, (h1-h0), d] is that rank's head slice."""
     ops = ops or KernelOps()
-    return ops.attention(q_local, pk_local, pv_local, sk_local, sv_local, lens, scale=scale)
+    if world is not None:
+        (h0, h1), (j0, j1) = head_shard(q.shape[1], pk.shape[1], world, rank)
+        q, pk, pv, sk, sv = q[:, h0:h1], pk[:, j0:j1], pv[:, j0:j1], sk[:, :, j0:j1], sv[:, :, j0:j1]
+    return ops.attention(q, pk, pv, sk, sv, lens, scale=scale, out=out)
 
 
-def exchange_layout(B: int, Hq: int, d: int, exchange_dtype=torch.float16):
-    """Byte layout of one rank's packed block: [O (B*Hq*d, exchange_dtype) | LSE (B*Hq, f32)]."""
+def exchange_layout(d: int, exchange_dtype=torch.float16):
+    """Bytes of one exchanged row [O (d, exchange_dtype) | LSE (f32) | pad to 16 B] and the LSE's
+    offset in it."""
     esz = torch.empty((), dtype=exchange_dtype).element_size()
-    o_bytes = B * Hq * d * esz
-    o_bytes = (o_bytes + 15) // 16 * 16  # keep the LSE region 16-B aligned
-    return o_bytes, B * Hq * 4
+    return (d * esz + 4 + 15) // 16 * 16, d * esz
+
+
+class SeqSplit:
+    """Plan and buffers of the prefix sequence split for one rank (see the module docstring).
+
+    B, Hq, d: the whole batch's query shape (q is replicated on every rank).  Calling the
+    plan with this rank's prefix shard and batch-shard suffixes returns this rank's output
+    rows [nb, Hq, d] (and LSEs)."""
+
+    def __init__(self, B: int, Hq: int, d: int, group: Optional[dist.ProcessGroup] = None, device=None,
+                 exchange_dtype=torch.float16, out_dtype=torch.bfloat16, exchange: str = "alltoall", ops=None):
+        if exchange not in ("alltoall", "allgather"):
+            raise ValueError("exchange must be 'alltoall' or 'allgather'")
+        self.ops = ops or KernelOps()
+        self.group = group
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        self.B, self.Hq, self.d = B, Hq, d
+        self.dev = torch.device(device) if device is not None else torch.device("cpu")
+        self.edt, self.out_dtype, self.exchange = exchange_dtype, out_dtype, exchange
+        self.b0, self.b1 = batch_shard(B, self.world, self.rank)
+        self.nb = self.b1 - self.b0
+        self.mb = -(-B // self.world)
+        self.row_bytes, lse_off = exchange_layout(d, exchange_dtype)
+        esz = torch.empty((), dtype=exchange_dtype).element_size()
+        slot_rows = self.mb * Hq
+        self.slot_rows = slot_rows
+        W = self.world
+        # exchange buffers: slot c (rows of batch shard c) at rows [c*slot_rows, (c+1)*slot_rows)
+        self.send = torch.zeros(W * slot_rows * self.row_bytes, dtype=torch.uint8, device=self.dev)
+        n_recv = W * slot_rows if exchange == "alltoall" else W * W * slot_rows
+        self.recv = torch.zeros(n_recv * self.row_bytes, dtype=torch.uint8, device=self.dev)
+        re, rf = self.row_bytes // esz, self.row_bytes // 4
+        self.send_o = self.send.view(exchange_dtype).view(W * slot_rows, re)[:B * Hq, :d]
+        self.send_l = self.send.view(torch.float32).view(W * slot_rows, rf)[:B * Hq, lse_off // 4]
+        if exchange == "alltoall":  # piece p = my rows as computed by rank p
+            ro = self.recv.view(exchange_dtype).view(W, slot_rows, re)
+            rl = self.recv.view(torch.float32).view(W, slot_rows, rf)
+            self.recv_o, self.recv_l = ro[:, :self.nb * Hq, :d], rl[:, :self.nb * Hq, lse_off // 4]
+        else:  # rank p's whole send buffer at [p]; my rows start at b0*Hq
+            ro = self.recv.view(exchange_dtype).view(W, W * slot_rows, re)
+            rl = self.recv.view(torch.float32).view(W, W * slot_rows, rf)
+            r0, r1 = self.b0 * Hq, self.b1 * Hq
+            self.recv_o, self.recv_l = ro[:, r0:r1, :d], rl[:, r0:r1, lse_off // 4]
+        self.o_p = torch.empty(B, Hq, d, dtype=torch.float32, device=self.dev)
+        self.l_p = torch.empty(B, Hq, dtype=torch.float32, device=self.dev)
+        self.o_s = torch.empty(1, max(self.nb, 1) * Hq, d, dtype=torch.float32, device=self.dev)
+        self.l_s = torch.empty(1, max(self.nb, 1) * Hq, dtype=torch.float32, device=self.dev)
+        self.out = torch.empty(max(self.nb, 1) * Hq, d, dtype=out_dtype, device=self.dev)
+        self.lse = torch.empty(max(self.nb, 1) * Hq, dtype=torch.float32, device=self.dev)
+        self.cuda = self.dev.type == "cuda"
+        backend = dist.get_backend(group)
+        self.staged = self.cuda and backend != "nccl"  # gloo: no CUDA collectives -> stage on the host
+        if self.staged:
+            self.h_send = torch.empty(self.send.numel(), dtype=torch.uint8).pin_memory()
+            self.h_recv = torch.empty(self.recv.numel(), dtype=torch.uint8).pin_memory()
+        if self.cuda:
+            self.side = torch.cuda.Stream(device=self.dev)
+            self.ev_packed = torch.cuda.Event()
+            self.ev_suffix = torch.cuda.Event()
+        self.overflow = None
+
+    def exchange_bytes(self) -> int:
+        """Bytes this rank sends per step (its slots for the other ranks)."""
+        return (self.world - 1) * self.slot_rows * self.row_bytes if self.exchange == "alltoall" else \
+            (self.world - 1) * self.send.numel()
+
+    def _collective(self):
+        if self.staged:
+            self.h_send.copy_(self.send)
+            hs, hr = self.h_send, self.h_recv
+        else:
+            hs, hr = self.send, self.recv
+        if self.exchange == "alltoall":
+            dist.all_to_all_single(hr, hs, group=self.group)
+        else:
+            dist.all_gather_into_tensor(hr, hs, group=self.group)
+        if self.staged:
+            self.recv.copy_(self.h_recv)
+
+    def __call__(self, q, pk_shard, pv_shard, sk_local, sv_local, lens_local, scale=None, return_lse=False,
+                 check_range: bool = False):
+        B, Hq, d = self.B, self.Hq, self.d
+        if tuple(q.shape) != (B, Hq, d):
+            raise ValueError(f"q must be [{B}, {Hq}, {d}] (the plan's shape)")
+        if sk_local.shape[0] != self.nb:
+            raise ValueError(f"this rank's batch shard holds {self.nb} sequences (batch_shard), got {sk_local.shape[0]}")
+        ops = self.ops
+        # 1. prefix pieces of all B*Hq rows over the local prefix shard
+        ops.prefix(q, pk_shard, pv_shard, scale=scale, out=self.o_p, lse_out=self.l_p)
+        # 2. one pack: (O f16 | LSE f32) rows, batch shard c's rows in slot c
+        ops.combine(self.o_p.view(1, B * Hq, d), self.l_p.view(1, B * Hq), out_dtype=self.edt, out=self.send_o,
+                    lse_out=self.send_l)
+        if check_range and self.edt == torch.float16:
+            self.overflow = (~torch.isfinite(self.send_o)).any()
+        cur = torch.cuda.current_stream(self.dev) if self.cuda else None
+        # 4. suffix of the local batch shard on the side stream, overlapping the exchange
+        if self.nb > 0:
+            if self.cuda:
+                self.ev_packed.record(cur)
+                self.side.wait_event(self.ev_packed)
+                with torch.cuda.stream(self.side):
+                    ops.suffix(q[self.b0:self.b1], sk_local, sv_local, lens_local, scale=scale,
+                               out=self.o_s[0].view(self.nb, Hq, d), lse_out=self.l_s[0].view(self.nb, Hq))
+                self.ev_suffix.record(self.side)
+            else:
+                ops.suffix(q[self.b0:self.b1], sk_local, sv_local, lens_local, scale=scale,
+                           out=self.o_s[0].view(self.nb, Hq, d), lse_out=self.l_s[0].view(self.nb, Hq))
+        # 3. the exchange (one collective)
+        self._collective()
+        if self.nb == 0:
+            out = self.out[:0].view(0, Hq, d)
+            return (out, self.lse[:0].view(0, Hq)) if return_lse else out
+        if self.cuda:
+            cur.wait_event(self.ev_suffix)
+        # 5. one merge: N received prefix pieces (f16, read in place) + the suffix part (f32)
+        rows = self.nb * Hq
+        out, lse = ops.combine(self.recv_o, self.recv_l, out_dtype=self.out_dtype, out=self.out[:rows],
+                               lse_out=self.lse[:rows], o_parts_f32=self.o_s[:, :rows], lse_parts_f32=self.l_s[:, :rows])
+        if check_range and self.overflow is not None and bool(self.overflow):
+            raise OverflowError("a prefix partial O exceeds the fp16 range (|V| > 65504): use exchange_dtype=float32")
+        out = out.view(self.nb, Hq, d)
+        return (out, lse.view(self.nb, Hq)) if return_lse else out
+
+
+_PLANS = {}
 
 
 def seqsplit_attention(q: torch.Tensor, pk_shard: torch.Tensor, pv_shard: torch.Tensor,
                        sk_local: torch.Tensor, sv_local: torch.Tensor, lens_local: torch.Tensor,
                        group: Optional[dist.ProcessGroup] = None, scale: Optional[float] = None,
                        exchange_dtype=torch.float16, out_dtype=None, ops=None, return_lse: bool = False,
-                       exchange: str = "alltoall"):
-    """Prefix sequence split across the ranks of `group` (see module docstring).
+                       exchange: str = "alltoall", check_range: bool = False):
+    """Prefix sequence split across the ranks of `group` (see the module docstring).
 
     q: [B, Hq, d] replicated on every rank; pk/pv_shard: this rank's prefix tokens
     [P_r, Hkv, d]; sk/sv_local, lens_local: the suffixes of this rank's batch shard
-    (`shard_range(B, world, rank)`).  Returns the attention output of this rank's batch
-    shard, [B_r, Hq, d].
+    (`batch_shard(B, world, rank)`).  Returns this rank's output rows [nb, Hq, d].  The plan
+    (buffers) is cached per shape, so repeated calls allocate nothing.
     """
-    ops = ops or KernelOps()
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
     B, Hq, d = q.shape
-    b0, b1 = shard_range(B, world, rank)
-    nb = b1 - b0
-    dev = q.device
     out_dtype = out_dtype or (torch.bfloat16 if q.dtype == torch.bfloat16 else torch.float32)
-
-    # 1-2. prefix pieces of all B*Hq rows over the local prefix shard, packed for the exchange
-    o_p, l_p = ops.prefix(q, pk_shard, pv_shard, scale=scale)
-    if exchange == "alltoall":
-        # One slot of ceil(B/N) rows per destination rank; rank c's batch-shard rows are
-        # packed at the start of slot c (pad rows are sent but never read).  Equal slots:
-        # all_to_all_single without split sizes (the split-size form hangs process-group
-        # teardown after CUDA-graph capture with this NCCL build).
-        mb = -(-B // world)
-        o_send = torch.empty(world * mb * Hq, d, dtype=exchange_dtype, device=dev)
-        l_send = torch.empty(world * mb * Hq, dtype=torch.float32, device=dev)
-        if B % world == 0:  # slots are exactly the shards: one pack for all rows
-            ops.combine(o_p.view(1, B * Hq, d), l_p.view(1, B * Hq), out=o_send, lse_out=l_send)
-        else:
-            for c in range(world):
-                c0, c1 = shard_range(B, world, c)
-                if c1 > c0:
-                    ops.combine(o_p[c0:c1].reshape(1, (c1 - c0) * Hq, d), l_p[c0:c1].reshape(1, (c1 - c0) * Hq),
-                                out=o_send[c * mb * Hq:(c * mb + c1 - c0) * Hq],
-                                lse_out=l_send[c * mb * Hq:(c * mb + c1 - c0) * Hq])
-        o_all = torch.empty(world * mb * Hq, d, dtype=exchange_dtype, device=dev)
-        l_all = torch.empty(world * mb * Hq, dtype=torch.float32, device=dev)
-        dist.all_to_all_single(o_all, o_send, group=group)
-        dist.all_to_all_single(l_all, l_send, group=group)
-        return _finish(q, sk_local, sv_local, lens_local, o_all.view(world, mb * Hq, d)[:, : nb * Hq],
-                       l_all.view(world, mb * Hq)[:, : nb * Hq], b0, b1, scale, out_dtype, ops, return_lse)
-    o_bytes, l_bytes = exchange_layout(B, Hq, d, exchange_dtype)
-    block = o_bytes + l_bytes
-    send = torch.empty(block, dtype=torch.uint8, device=dev)
-    o_send = send[: B * Hq * d * torch.empty((), dtype=exchange_dtype).element_size()].view(exchange_dtype)
-    l_send = send[o_bytes:].view(torch.float32)
-    ops.combine(o_p.view(1, B * Hq, d), l_p.view(1, B * Hq), out=o_send.view(B * Hq, d), lse_out=l_send)
-
-    # 3. all-gather the packed blocks
-    recv = torch.empty(world * block, dtype=torch.uint8, device=dev)
-    dist.all_gather_into_tensor(recv, send, group=group)
-    blocks = recv.view(world, block)
-    esz = torch.empty((), dtype=exchange_dtype).element_size()
-    o_all = blocks[:, : B * Hq * d * esz].view(exchange_dtype).view(world, B, Hq, d)
-    l_all = blocks[:, o_bytes:].view(torch.float32).view(world, B, Hq)
-    return _finish(q, sk_local, sv_local, lens_local, o_all[:, b0:b1].reshape(world, nb * Hq, d),
-                   l_all[:, b0:b1].reshape(world, nb * Hq), b0, b1, scale, out_dtype, ops, return_lse)
+    key = (B, Hq, d, str(q.device), exchange_dtype, out_dtype, exchange, id(group), type(ops).__name__,
+           dist.get_world_size(group), dist.get_rank(group))
+    plan = _PLANS.get(key)
+    if plan is None:
+        plan = _PLANS[key] = SeqSplit(B, Hq, d, group=group, device=q.device, exchange_dtype=exchange_dtype,
+                                      out_dtype=out_dtype, exchange=exchange, ops=ops)
+    plan.ops = ops or plan.ops
+    return plan(q, pk_shard, pv_shard, sk_local, sv_local, lens_local, scale=scale, return_lse=return_lse,
+                check_range=check_range)
 
 
-def _finish(q, sk_local, sv_local, lens_local, o_parts, l_parts, b0, b1, scale, out_dtype, ops, return_lse):
-    """Steps 4-5: suffix of the batch shard, merge of the N exchanged prefix pieces of its
-    rows (o_parts [N, rows, d], l_parts [N, rows], strided parts allowed), final merge."""
-    B, Hq, d = q.shape
-    nb = b1 - b0
-    dev = q.device
-    # 4. suffix of the local batch shard, written straight into part 1
-    parts = torch.empty(2, nb * Hq, d, dtype=torch.float32, device=dev)
-    lparts = torch.empty(2, nb * Hq, dtype=torch.float32, device=dev)
-    if nb > 0:
-        ops.suffix(q[b0:b1], sk_local, sv_local, lens_local, scale=scale, out=parts[1].view(nb, Hq, d),
-                   lse_out=lparts[1].view(nb, Hq))
-        # 5a. merge the world prefix pieces of these rows (strided parts of the exchanged buffer)
-        ops.combine(o_parts, l_parts, out=parts[0], lse_out=lparts[0])
-        # 5b. prefix (+) suffix
-        out, lse = ops.combine(parts, lparts, out_dtype=out_dtype)
-    else:
-        out = torch.empty(0, d, dtype=out_dtype, device=dev)
-        lse = torch.empty(0, dtype=torch.float32, device=dev)
-    out = out.view(nb, Hq, d)
-    return (out, lse.view(nb, Hq)) if return_lse else out
+def release_plans():
+    """Drop the cached sequence-split plans (their buffers)."""
+    _PLANS.clear()

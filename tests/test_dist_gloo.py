@@ -29,10 +29,15 @@ def _np(t: torch.Tensor):
 class OracleOps:
     """fp64 oracle stand-ins for the kernel calls (test infrastructure)."""
 
-    def prefix(self, q, k, v, scale=None):
+    def prefix(self, q, k, v, scale=None, out=None, lse_out=None):
         B = q.shape[0]
         o, l = oracle.attention_segments(_np(q), [[(_np(k), _np(v))]] * B, k.shape[1], scale)
-        return torch.from_numpy(o).float(), torch.from_numpy(l).float()
+        o, l = torch.from_numpy(o).float(), torch.from_numpy(l).float()
+        if out is None:
+            return o, l
+        out.copy_(o)
+        lse_out.copy_(l)
+        return out, lse_out
 
     def suffix(self, q, k, v, lens, scale=None, out=None, lse_out=None):
         kn, vn = _np(k), _np(v)
@@ -42,9 +47,13 @@ class OracleOps:
         lse_out.copy_(torch.from_numpy(l).float())
         return out, lse_out
 
-    def combine(self, o_parts, lse_parts, out_dtype=torch.bfloat16, out=None, lse_out=None):
+    def combine(self, o_parts, lse_parts, out_dtype=torch.bfloat16, out=None, lse_out=None, o_parts_f32=None,
+                lse_parts_f32=None):
         o = o_parts.double().numpy()
         l = lse_parts.double().numpy()
+        if o_parts_f32 is not None:  # the second (f32) part group is merged in the same pass
+            o = np.concatenate([o, o_parts_f32.double().numpy()])
+            l = np.concatenate([l, lse_parts_f32.double().numpy()])
         ro, rl = o[0], l[0]
         for i in range(1, o.shape[0]):
             ro, rl = oracle.combine(ro, rl, o[i], l[i])
@@ -56,7 +65,7 @@ class OracleOps:
         lse_out.copy_(torch.from_numpy(rl).float().view(lse_out.shape))
         return out, lse_out
 
-    def attention(self, q, pk, pv, sk, sv, lens, scale=None):
+    def attention(self, q, pk, pv, sk, sv, lens, scale=None, out=None):
         B = q.shape[0]
         segs = [[(_np(pk), _np(pv)), (_np(sk)[b, :int(lens[b])], _np(sv)[b, :int(lens[b])])] for b in range(B)]
         o, _ = oracle.attention_segments(_np(q), segs, pk.shape[1], scale)
@@ -77,7 +86,8 @@ def _worker(rank, world, port, mode, exchange, outdir):
 
     try:
         lens_all = [12, 0, 5, 12, 1, 7, 3]
-        B = 6 if world == 2 else 7  # world 3: unequal batch shards (3, 2, 2 rows) for the all-to-all splits
+        # world 3: unequal batch shards (3, 3, 1 rows); world 4: B = 5 leaves rank 3 without sequences
+        B = {2: 6, 3: 7, 4: 5}[world]
         Hq, Hkv, d, P, S = 8, 2, 32, 90, 12
         pb = synth.make_problem(B, Hq, Hkv, d, P, S, lens=lens_all[:B], dtype="bf16", dist="mixed", seed=21)
         tt = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).view(torch.bfloat16)
@@ -87,22 +97,19 @@ def _worker(rank, world, port, mode, exchange, outdir):
         ops = OracleOps()
         if mode.startswith("seqsplit"):
             p0, p1 = hdist.shard_range(P, world, rank)
-            b0, b1 = hdist.shard_range(B, world, rank)
+            b0, b1 = hdist.batch_shard(B, world, rank)
             out, lse = hdist.seqsplit_attention(q, pk[p0:p1], pv[p0:p1], sk[b0:b1], sv[b0:b1], lens[b0:b1],
                                                 exchange_dtype=exchange, out_dtype=torch.float32, ops=ops,
                                                 return_lse=True,
                                                 exchange="allgather" if mode.endswith("ag") else "alltoall")
-            err = float(np.abs(out.double().numpy() - ref[b0:b1]).max())
-            lerr = float(np.abs(lse.double().numpy() - lref[b0:b1]).max())
+            err = float(np.abs(out.double().numpy() - ref[b0:b1]).max()) if b1 > b0 else 0.0
+            lerr = float(np.abs(lse.double().numpy() - lref[b0:b1]).max()) if b1 > b0 else 0.0
             tol = 1e-6 if exchange == torch.float32 else 4e-3
             assert out.shape == (b1 - b0, Hq, d)
             assert err <= tol, f"rank {rank}: seq-split max err {err}"
             assert lerr <= 1e-6, f"rank {rank}: lse err {lerr}"
         else:
-            (h0, h1), (j0, j1) = hdist.head_shard(Hq, Hkv, world, rank)
-            out = hdist.head_sharded_attention(q[:, h0:h1].contiguous(), pk[:, j0:j1].contiguous(),
-                                               pv[:, j0:j1].contiguous(), sk[:, :, j0:j1].contiguous(),
-                                               sv[:, :, j0:j1].contiguous(), lens, ops=ops)
+            out = hdist.head_sharded_attention(q, pk, pv, sk, sv, lens, ops=ops, world=world, rank=rank)
             # gather the head shards and compare the full output
             full = [torch.empty_like(out) for _ in range(world)]
             dist.all_gather(full, out)
@@ -116,6 +123,7 @@ def _worker(rank, world, port, mode, exchange, outdir):
 
 @pytest.mark.parametrize("mode,exchange,world", [("seqsplit-a2a", torch.float32, 2), ("seqsplit-a2a", torch.float16, 2),
                                                  ("seqsplit-a2a", torch.float16, 3), ("seqsplit-ag", torch.float16, 2),
+                                                 ("seqsplit-a2a", torch.float16, 4), ("seqsplit-ag", torch.float16, 3),
                                                  ("heads", torch.float16, 2)])
 def test_world_gloo(mode, exchange, world):
     with tempfile.TemporaryDirectory() as td:
@@ -137,5 +145,7 @@ def test_shard_ranges_partition():
     assert hdist.head_shard(32, 8, 4, 1) == ((8, 16), (2, 4))
     with pytest.raises(ValueError):
         hdist.head_shard(40, 40, 3, 0)
-    o, l = hdist.exchange_layout(512, 32, 128, torch.float16)
-    assert o == 512 * 32 * 128 * 2 and l == 512 * 32 * 4  # C4: 4.26 MB per rank
+    assert hdist.exchange_layout(128, torch.float16) == (272, 256)  # O f16 | LSE f32 | pad: 16-B rows
+    assert hdist.exchange_layout(128, torch.float32) == (528, 512)
+    assert [hdist.batch_shard(7, 3, r) for r in range(3)] == [(0, 3), (3, 6), (6, 7)]
+    assert [hdist.batch_shard(5, 4, r) for r in range(4)] == [(0, 2), (2, 4), (4, 5), (5, 5)]
