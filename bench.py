@@ -58,6 +58,12 @@ CONFIGS = {
                         name="long-document shape (Yi-6B-like 32 q / 4 kv heads, d=128), B=256, prefix 19947 split "
                              "along the sequence across ranks with one NCCL all-to-all of packed (O fp16, LSE) rows, "
                              "suffix 128 (assumed)"),
+    # the paper's attention microbenchmark grid (§4.2, App. D.2
+    # P:547): 8 q / 1 kv heads, d=128; Hydragen vs per-sequence attention over each sequence's
+    # own copy of prefix || suffix (paper_2402_05099_b200.baseline); one JSON line per point
+    "grid": dict(B=1024, Hq=8, Hkv=1, d=128, P=16384, S=256, kind="grid",
+                 batches=(32, 128, 512, 1024), prefixes=(1024, 4096, 16384), suffixes=(64, 256),
+                 name="attention microbenchmark grid (paper §4.2): 8 q / 1 kv heads, d=128"),
     # two-level sharing tree (tree_attention)
     "c5": dict(B=1024, Hq=32, Hkv=32, d=128, P=4096, S=512, kind="tree", branches=16, branch_len=1024,
                name="tree sharing: 4096-token root -> 16 branches x 1024 tokens -> 64 sequences each with 512-token "
@@ -447,6 +453,94 @@ def run_seqsplit(args, cfg):
     del plan
 
 
+def run_grid(args, cfg):
+    """NEXT-1: speedup of Hydragen attention over per-sequence attention on the paper's
+    microbenchmark shape, App. D.2 protocol: CUDA graph per call, the L2 flushed (a 2 x L2
+    write) before every timed replay, mean and median over the timed replays."""
+    import numpy as np
+    import torch
+
+    import synth
+    import paper_2402_05099_b200 as hydra
+    from paper_2402_05099_b200 import baseline
+
+    if int(os.environ.get("RANK", "0")) != 0:
+        return  # one GPU's microbenchmark: other ranks idle
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
+    torch.cuda.set_device(dev)
+    Hq, Hkv, d = cfg["Hq"], cfg["Hkv"], cfg["d"]
+    flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
+    iters, warm = max(5, args.steps), max(3, args.warmup)
+
+    def graph_times(fn):
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):
+            fn()
+        torch.cuda.current_stream(dev).wait_stream(s)
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            fn()
+        for _ in range(warm):
+            g.replay()
+        evs = []
+        for _ in range(iters):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            g.replay()
+            b.record()
+            evs.append((a, b))
+        torch.cuda.synchronize(dev)
+        t = [a.elapsed_time(b) for a, b in evs]
+        return statistics.mean(t), statistics.median(t)
+
+    best = None
+    for P in cfg["prefixes"]:
+        for S in cfg["suffixes"]:
+            for B in cfg["batches"]:
+                pb = synth.make_problem(B, Hq, Hkv, d, P, S, dtype="bf16", dist="mixed", seed=args.seed)
+                t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).view(torch.bfloat16).to(dev)
+                q, pk, pv, sk, sv = t(pb.q), t(pb.pk), t(pb.pv), t(pb.sk), t(pb.sv)
+                lens = torch.from_numpy(pb.lens.astype(np.int32)).to(dev)
+                ws = torch.empty(hydra.attn_workspace_bytes(q, P, S, Hkv), dtype=torch.uint8, device=dev)
+                out = torch.empty(B, Hq, d, dtype=torch.bfloat16, device=dev)
+                h_mean, h_med = graph_times(lambda: hydra.hydragen_attention(q, pk, pv, sk, sv, lens, out=out,
+                                                                             workspace=ws))
+                fk, fv, flens = baseline.per_sequence_cache(pk, pv, sk, sv, lens)
+                o_b = torch.empty(B, Hq, d, dtype=torch.float32, device=dev)
+                l_b = torch.empty(B, Hq, dtype=torch.float32, device=dev)
+                h = hydra._lib.Heads(Hq, Hkv, d, 0.0, hydra._lib.HYDRA_BF16)
+                import ctypes
+
+                wsb = torch.empty(max(1, hydra.load().hydra_workspace_size(hydra._lib.HYDRA_OP_SUFFIX, ctypes.byref(h), B,
+                                                                           0, P + S, 0)), dtype=torch.uint8, device=dev)
+                b_mean, b_med = graph_times(lambda: baseline.per_sequence_attention(q, fk, fv, flens, workspace=wsb,
+                                                                                    out=o_b, lse_out=l_b))
+                line = {"metric": "Hydragen attention speedup over per-sequence attention (paper §4.2 microbenchmark)",
+                        "value": round(b_mean / h_mean, 3), "unit": "x", "higher_is_better": True, "n_gpus": 1,
+                        "steps": iters, "warmup": warm, "dtype": "bf16",
+                        "data": "synthetic (seeded PCG64 N(0,1) K/V rounded to bf16, 'mixed' needle queries)",
+                        "config": {"workload": "grid", "B": B, "Hq": Hq, "Hkv": Hkv, "d": d, "prefix_len": P,
+                                   "suffix_len": S, "l2": "flushed (2 x 126 MB write) before every timed replay"},
+                        "hydragen_ms": {"mean": round(h_mean, 5), "median": round(h_med, 5)},
+                        "per_sequence_ms": {"mean": round(b_mean, 5), "median": round(b_med, 5)},
+                        "speedup_median": round(b_med / h_med, 3),
+                        "baseline": "each sequence attends over its own copy of prefix || suffix with this library's "
+                                    "per-sequence kernels (paper_2402_05099_b200.baseline; P:160)",
+                        "timing": "App. D.2 (P:547): CUDA graph per call, L2 flushed before every replay, "
+                                  f"{warm} warm-up and {iters} timed replays, mean and median"}
+                print(json.dumps(line), flush=True)
+                if best is None or line["value"] > best["value"]:
+                    best = line
+                del fk, fv, q, pk, pv, sk, sv, ws, wsb, o_b, l_b, out
+                torch.cuda.empty_cache()
+    print(json.dumps({"metric": "max Hydragen attention speedup over per-sequence attention (paper §4.2; paper: "
+                                ">16x on A100, P:27)", "value": best["value"], "unit": "x",
+                      "at": best["config"]}), flush=True)
+
+
 def self_launch(args):
     """`bench.py --gpus N` without a torchrun environment: start N ranks with torchrun on this node
     (one per GPU) and pass their output through; fail loudly when fewer GPUs are visible."""
@@ -482,6 +576,9 @@ def main():
         c = dict(cfg, B=B)
         if B != cfg["B"]:
             c["name"] = cfg["name"].replace("B=%d" % cfg["B"], "B=%d" % B)
+        if kind == "grid":
+            run_grid(args, c)
+            break
         if kind == "tree":
             run_tree(args, c)
         elif kind == "seqsplit":

@@ -46,6 +46,7 @@ struct Config {
   int64_t prefix_impl = 0, prefix_splits = 0, prefix_ctas = 0, prefix_stages = 3, prefix_poly = 4, prefix_variant = 6;
   int64_t suffix_impl = 0, suffix_splits = 0, suffix_ctas = 0, suffix_unroll = 4, suffix_cb = 2;
   int64_t overlap_prefix_ctas = 0;
+  int64_t fuse_combine = 1;  // 1: Eq. 5 merged in the kernel epilogues (fused.cuh); 0: separate combine launch
   // Measurement: cudaEvent_t handles hydra_attn / hydra_attn_paged record around the prefix (on
   // its stream) and the suffix launches, so a benchmark can time each kernel within the step
   // (also inside a captured graph); 0 = off.  [0] prefix begin, [1] prefix end, [2] suffix
@@ -86,6 +87,7 @@ const Key kKeys[] = {
     {"suffix_impl", &Config::suffix_impl, false},         {"suffix_splits", &Config::suffix_splits, false},
     {"suffix_ctas", &Config::suffix_ctas, false},         {"suffix_unroll", &Config::suffix_unroll, false},
     {"suffix_cb", &Config::suffix_cb, false},             {"overlap_prefix_ctas", &Config::overlap_prefix_ctas, false},
+    {"fuse_combine", &Config::fuse_combine, false},
     {"tc_debug_variant", &Config::tc_debug, true},        {"prefix_trace", &Config::prefix_trace, true},
     {"suffix_trace", &Config::suffix_trace, true},        {"inject_combine_bug", &Config::inject_combine_bug, true},
     {"mutate", &Config::mutate, true},
@@ -346,6 +348,9 @@ static int overlap_prefix_ctas(const hydra_heads *h, int64_t B, int64_t P, int64
   return best_k;
 }
 
+// fused Eq. 5 arrival counters (int32 per row), after the partial slots in the workspace
+static size_t counter_bytes(int64_t rows) { return ((size_t)rows * sizeof(int32_t) + 255) / 256 * 256; }
+
 static size_t part_bytes(const hydra_heads *h, int64_t B) {
   return (size_t)B * h->num_q_heads * ((size_t)h->head_dim + 1) * sizeof(float);
 }
@@ -368,7 +373,8 @@ static PartsView parts_in_ws(void *ws, const hydra_heads *h, int64_t B, int n) {
 
 static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, int64_t q_sb, int64_t q_sh,
                                int64_t P, const void *k, const void *v, int64_t kv_st, int64_t kv_sh, int splits,
-                               const PartsView &dst, cudaStream_t s, int tc2_ctas = 0) {
+                               const PartsView &dst, cudaStream_t s, int tc2_ctas = 0,
+                               const FusedCombine *fc = nullptr) {
   const int g = h->num_q_heads / h->num_kv_heads;
   const float sl2 = scale_of(h) * 1.4426950408889634f;
   const PrefixKind kind = prefix_kind(h, B * g, P, tc2_ctas);
@@ -399,10 +405,12 @@ static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, i
     a.poly_every = (int32_t)g_cfg.prefix_poly;
     a.variant = (int32_t)g_cfg.prefix_variant;
     a.mutate = (int32_t)g_cfg.mutate;
+    if (fc) a.fc = *fc;
     hydra_status st;
     if (kind == PK_TC2) {
-      // stream-K pieces leave some slots of a row unwritten: mark every slot empty first
-      if (splits > 1 && launch_fill_neg_inf(dst.lse, dst.lse_stride * splits, s) != HYDRA_OK)
+      // stream-K pieces leave some slots of a row unwritten: mark every slot empty first (the
+      // fused merge knows which slots hold a row's pieces and needs no fill)
+      if (!fc && splits > 1 && launch_fill_neg_inf(dst.lse, dst.lse_stride * splits, s) != HYDRA_OK)
         return cuda_fail("fill");
       st = launch_prefix_tc2(a, tc2_ctas > 0 ? tc2_ctas : prefix_ctas(), s);
     } else {
@@ -440,7 +448,8 @@ static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, i
 static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, int64_t q_sb, int64_t q_sh,
                                const void *k, const void *v, int64_t s_sb, int64_t s_st, int64_t s_sh,
                                int64_t S_cap, const int32_t *lens, int splits, const PartsView &dst,
-                               cudaStream_t s, int tc_ctas = 0, const hydra_paging *pg = nullptr) {
+                               cudaStream_t s, int tc_ctas = 0, const hydra_paging *pg = nullptr,
+                               const FusedCombine *fc = nullptr) {
   const int g = h->num_q_heads / h->num_kv_heads;
   if (kTesting && launch_lens_check(lens, B, S_cap, s) != HYDRA_OK) return cuda_fail("lens check");
   if (use_suffix_tc(h, B, S_cap, tc_ctas > 0)) {
@@ -465,6 +474,7 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
     a.trace = reinterpret_cast<void *>((intptr_t)g_cfg.suffix_trace);
     a.debug = (int32_t)g_cfg.tc_debug;
     a.mutate = (int32_t)g_cfg.mutate;
+    if (fc) a.fc = *fc;
     a.n_split = splits;
     a.split_len = (int32_t)(((S_cap + splits - 1) / splits + 127) / 128 * 128);
     a.o_split_stride = dst.o_stride;
@@ -504,6 +514,7 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
   p.lse = dst.lse;
   p.o_split_stride = dst.o_stride;
   p.lse_split_stride = dst.lse_stride;
+  if (fc) p.fc = *fc;
   if (pg) {
     p.block_table = pg->block_table;
     p.bt_stride = pg->bt_stride;
@@ -550,10 +561,11 @@ extern "C" size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, 
       const int s = suffix_splits(h, B, S_cap);
       return s > 1 ? pb * s : 0;
     }
-    case HYDRA_OP_ATTN: {  // enough for both the sequential and the SM-partitioned schedule
+    case HYDRA_OP_ATTN: {  // enough for both the sequential and the SM-partitioned schedule (+ fused counters)
       const int k = overlap_prefix_ctas(h, B, P, S_cap);
       const int np = std::max(prefix_splits(h, B, P), k > 0 ? prefix_splits(h, B, P, k) : 1);
-      return pb * (size_t)(np + std::max(suffix_splits(h, B, S_cap), suffix_splits(h, B, S_cap, k > 0)));
+      return pb * (size_t)(np + std::max(suffix_splits(h, B, S_cap), suffix_splits(h, B, S_cap, k > 0))) +
+             counter_bytes(B * h->num_q_heads);
     }
   }
   return 0;
@@ -733,6 +745,16 @@ extern "C" hydra_status hydra_combine(int64_t rows, int32_t d, int32_t n_parts, 
 }
 
 // ------------------------------------------------------------------ composite
+// The fused Eq. 5 path (fused.cuh) of hydra_attn: bf16, d = 128, both parts present, a prefix
+// kernel with a device-known piece layout (the persistent kernel's stream-K plan, variants
+// 3 / 5 / 6, or the one-tile kernel's fixed splits), and either suffix kernel.
+static bool attn_fused(const hydra_heads *h, int64_t B, int64_t P, int64_t S_cap, int k_over) {
+  if (!g_cfg.fuse_combine || h->dtype != HYDRA_BF16 || h->head_dim != 128 || P <= 0 || S_cap <= 0) return false;
+  const PrefixKind k = prefix_kind(h, B * (h->num_q_heads / h->num_kv_heads), P, k_over);
+  return (k == PK_TC2 && g_cfg.prefix_variant != 4) || k == PK_TC1;
+}
+
+// ------------------------------------------------------------------ composite
 namespace {
 struct StreamEvents {
   cudaEvent_t fork = nullptr, join = nullptr;
@@ -774,14 +796,43 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
   if (k_over == 0) sa = s;
   g_cfg.last_overlap_k = k_over;
   const int sms = device_sm_count();
+  const int g = h->num_q_heads / h->num_kv_heads;
   const int np = prefix_splits(h, B, P, k_over), ns = suffix_splits(h, B, S_cap, k_over > 0);
-  const size_t need = part_bytes(h, B) * (np + ns);
+  const bool fused = attn_fused(h, B, P, S_cap, k_over);
+  const int64_t rows = B * h->num_q_heads;
+  const size_t need = part_bytes(h, B) * (np + ns) + (fused ? counter_bytes(rows) : 0);
   if (!ws || ws_bytes < need) return fail(HYDRA_ENOMEM, "workspace too small: need %zu bytes", need);
   PartsView all = parts_in_ws(ws, h, B, np + ns);
   PartsView pre = all, suf = all;
   suf.o = all.o + all.o_stride * np;
   suf.lse = all.lse + all.lse_stride * np;
-  const int64_t rows = B * h->num_q_heads;
+
+  // Fused Eq. 5 (fused.cuh): the prefix and suffix epilogues count every row's parts and the
+  // writer of its last part merges it into `out`; the counters (after the partial slots in the
+  // workspace) are zeroed here, before the fork -- no slot fill, no combine launch.
+  FusedCombine fc{};
+  if (fused) {
+    fc.cnt = reinterpret_cast<int32_t *>(reinterpret_cast<char *>(ws) + part_bytes(h, B) * (np + ns));
+    fc.o_pre = pre.o;
+    fc.lse_pre = pre.lse;
+    fc.o_suf = suf.o;
+    fc.lse_suf = suf.lse;
+    fc.o_slot = all.o_stride;
+    fc.lse_slot = all.lse_stride;
+    fc.n_suf = ns;
+    fc.g = g;
+    fc.Hq = h->num_q_heads;
+    fc.Hkv = h->num_kv_heads;
+    fc.out = out;
+    fc.out_f32 = out_dtype == HYDRA_F32;
+    fc.lse_out = lse_out;
+    fc.inject_bug = inject_combine_bug() ? 1 : 0;
+    if (prefix_kind(h, B * g, P, k_over) == PK_TC2)
+      prefix_tc2_plan_into(fc, B, g, h->num_kv_heads, P, k_over > 0 ? k_over : prefix_ctas(), prefix_bn());
+    else
+      fc.n_pre_splits = np;
+    if (cudaMemsetAsync(fc.cnt, 0, sizeof(int32_t) * rows, s) != cudaSuccess) return cuda_fail("counter reset");
+  }
 
   if (sa != s) {
     if (cudaEventRecord(events().fork, s) != cudaSuccess || cudaStreamWaitEvent(sa, events().fork, 0) != cudaSuccess)
@@ -789,7 +840,7 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
   }
   if (P > 0) {
     record_step_ev(0, sa);
-    st = run_prefix(h, B, q, q_sb, q_sh, P, pk, pv, kv_st, kv_sh, np, pre, sa, k_over);
+    st = run_prefix(h, B, q, q_sb, q_sh, P, pk, pv, kv_st, kv_sh, np, pre, sa, k_over, fused ? &fc : nullptr);
     record_step_ev(1, sa);
   } else {
     st = launch_fill_neg_inf(pre.lse, rows, sa);
@@ -803,7 +854,7 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
                                  : 0;
     record_step_ev(2, s);
     st = run_suffix(h, B, q, q_sb, q_sh, sk, sv, s_sb, s_st, s_sh, S_cap, lens, ns, suf, s,
-                    k_over > 0 ? std::max(1, sms - k_eff) : 0, pg);
+                    k_over > 0 ? std::max(1, sms - k_eff) : 0, pg, fused ? &fc : nullptr);
     record_step_ev(3, s);
   } else {
     st = launch_fill_neg_inf(suf.lse, rows, s);
@@ -814,6 +865,7 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
     if (cudaEventRecord(events().join, sa) != cudaSuccess || cudaStreamWaitEvent(s, events().join, 0) != cudaSuccess)
       return cuda_fail("join");
   }
+  if (fused) return HYDRA_OK;  // merged in the epilogues
   return run_combine(rows, h->head_dim, np + ns, all, out, out_dtype, lse_out, s);
 }
 

@@ -17,6 +17,7 @@
 // loaded (poisoned padding cannot leak in).
 #include "common.cuh"
 #include "internal.h"
+#include "fused.cuh"
 
 namespace hydra {
 
@@ -168,6 +169,28 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeParams p) 
     if (e == 0)
       p.lse[(int64_t)split * p.lse_split_stride + (int64_t)b * p.Hq + h] = (M + log2f(L)) * HYDRA_LN2;
   }
+  if constexpr (D == 128) {
+    // Fused Eq. 5 (fused.cuh): this split's part of the CTA's GQ rows is stored; count the
+    // arrivals and merge the rows it completed (thread = dim).
+    if (p.fc.cnt) {
+      __shared__ uint32_t fc_mask;
+      __threadfence();
+      __syncthreads();
+      if (tid < 32) {
+        const bool last = tid < GQ && fc_arrive(p.fc, (int64_t)b * p.Hq + h0 + tid, fc_expected(p.fc, b, h0 + tid));
+        const uint32_t m2 = __ballot_sync(0xffffffffu, last);
+        if (tid == 0) fc_mask = m2;
+      }
+      __syncthreads();
+      uint32_t m2 = fc_mask;
+      if (m2) __threadfence();
+      while (m2) {
+        const int i = __ffs(m2) - 1;
+        m2 &= m2 - 1;
+        fc_merge_row_dim(p.fc, (int64_t)b * p.Hq + h0 + i, fc_prefix_pieces(p.fc, b, h0 + i), tid);
+      }
+    }
+  }
 }
 
 template <typename T, int D, int GQ, int U>
@@ -204,6 +227,7 @@ static cudaError_t launch_d(const DecodeParams &p, cudaStream_t s) {
 
 hydra_status launch_decode(const DecodeParams &p, hydra_dtype dt, int d, cudaStream_t s) {
   if (p.n_seq <= 0 || p.n_splits <= 0) return HYDRA_OK;
+  if (p.fc.cnt && (d != 128 || p.fc.n_suf != p.n_splits)) return HYDRA_EINVAL;
   cudaError_t e = cudaErrorInvalidValue;
   if (dt == HYDRA_BF16) {
     switch (d) {

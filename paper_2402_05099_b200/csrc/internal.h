@@ -28,6 +28,25 @@ int device_sm_count();
 hydra_status launch_lens_check(const int32_t *lens, int64_t B, int64_t S_cap, cudaStream_t s);
 int64_t read_lens_violations(bool reset);
 
+// ---------------------------------------------------------------- fused Eq. 5 combine (fused.cuh)
+// Per-row arrival counting: the epilogue that writes a row's last partial merges the row.
+struct FusedCombine {
+  int32_t *cnt;                 // [B*Hq] arrival counters (zero before the launches); null = not fused
+  const float *o_pre, *lse_pre;  // prefix piece k of row r: o_pre + k*o_slot + r*128, lse_pre[k*lse_slot + r]
+  const float *o_suf, *lse_suf;  // suffix part s of row r:  o_suf + s*o_slot + r*128, lse_suf[s*lse_slot + r]
+  int64_t o_slot, lse_slot;
+  int32_t n_suf;                // suffix parts per row (1, or the split count)
+  // Prefix pieces covering a row's 256-row pair (persistent kernel, grouped stream-K plan) or
+  // the fixed split count (one-tile kernel, sk_total == 0).
+  int64_t sk_total;
+  int32_t sk_G, sk_group, sk_nb, sk_npairs, n_pre_splits;
+  int32_t g, Hq, Hkv;
+  void *out;                    // [B*Hq, 128] bf16 (out_f32 = 0) or f32
+  int32_t out_f32;
+  float *lse_out;               // [B*Hq] merged LSE (nullable)
+  int32_t inject_bug;           // testing build only: w_p = 1
+};
+
 // ---------------------------------------------------------------- SIMT decode kernel
 // One CTA = one (sequence-slot b, KV head j, head chunk, KV split).  Used for the
 // suffix (§3.2), the fp32 reference-mode prefix / tree nodes, and odd shapes.
@@ -56,6 +75,7 @@ struct DecodeParams {
   const int32_t *block_table;
   int64_t bt_stride;
   int32_t page_shift;
+  FusedCombine fc;  // fc.cnt != null: merge each completed row in the epilogue (d = 128, bf16 suffix only)
 };
 
 hydra_status launch_decode(const DecodeParams &p, hydra_dtype dt, int d, cudaStream_t s);
@@ -119,6 +139,7 @@ struct PrefixTcArgs {
   int32_t debug_variant;
   void *trace = nullptr;  // diagnostics only (config key prefix_trace): device buffer for CTA-0 timestamps
   int32_t mutate = 0;     // testing build only: parity-suite mutation (prefix_tc2 epilogue store skip)
+  FusedCombine fc{};      // fc.cnt != null: fused Eq. 5 merge in the epilogue (flat mode)
   int32_t poly_every = 0;  // v3: every k-th exp2 column pair on the FMA pipe (0 = all MUFU)
   int32_t variant = 3;     // persistent kernel: 3 (128-token blocks) or 4 (64-token, double-buffered S)
   int32_t stages;  // K/V pipeline stages: 2 (160 KB smem, leaves room for co-resident suffix CTAs) or 3
@@ -130,6 +151,9 @@ hydra_status launch_prefix_tc(const PrefixTcArgs &a, cudaStream_t s);
 hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s);
 int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn);
 int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn);
+// The flat-mode stream-K plan of launch_prefix_tc2 over n_ctas CTAs, as the fused combine
+// needs it (which partial slots hold a row's pieces): fills fc.sk_*.
+void prefix_tc2_plan_into(FusedCombine &fc, int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn);
 // Persistent tensor-core suffix kernel (bf16, d = 128, g <= 16), TMA-fed.
 struct SuffixTcArgs {
   const void *q;
@@ -154,6 +178,7 @@ struct SuffixTcArgs {
   // (O, LSE) partial at o + sp * o_split_stride, lse + sp * lse_split_stride
   int32_t n_split, split_len;
   int64_t o_split_stride, lse_split_stride;
+  FusedCombine fc;  // fc.cnt != null: fused Eq. 5 merge in the epilogue
 };
 bool suffix_tc_supported(const hydra_heads *h);
 hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s);

@@ -30,6 +30,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "ptx.cuh"
+#include "fused.cuh"
 
 namespace hydra {
 
@@ -70,7 +71,29 @@ struct __align__(64) PrefixTcKernelParams {
   float *o, *lse;
   int64_t o_slot_stride, lse_slot_stride;
   int32_t debug_variant;  // bring-up switch: bit0 swaps the V descriptor LBO/SBO
+  FusedCombine fc;        // fc.cnt != null: the Eq. 5 merge of every completed row in this epilogue
 };
+
+// Fused Eq. 5 (fused.cuh): count this warp's rows; merge the rows this split completed.
+__device__ __forceinline__ void tc1_fused_arrive(const FusedCombine &F, bool live, int64_t seq, int h, int Hq,
+                                                 int lane) {
+  __threadfence();
+  __syncwarp();
+  const int64_t row = seq * Hq + h;
+  int n_pre = 0;
+  bool last = false;
+  if (live) {
+    n_pre = fc_prefix_pieces(F, seq, h);
+    last = fc_arrive(F, row, n_pre + F.n_suf);
+  }
+  unsigned mask = __ballot_sync(0xffffffffu, last);
+  if (mask) __threadfence();
+  while (mask) {
+    const int src = __ffs(mask) - 1;
+    mask &= mask - 1;
+    fc_merge_row_warp(F, __shfl_sync(0xffffffffu, row, src), __shfl_sync(0xffffffffu, n_pre, src), lane);
+  }
+}
 
 template <int NS>
 __global__ void __launch_bounds__(tc::kThreads, 1) prefix_tc_kernel(const __grid_constant__ PrefixTcKernelParams P) {
@@ -111,13 +134,17 @@ __global__ void __launch_bounds__(tc::kThreads, 1) prefix_tc_kernel(const __grid
   if (nblk == 0) {  // empty KV range for this split: the (0, -inf) sentinel
     if (warp >= 2) {
       const int64_t rr = row0 + 32 * (warp % 4) + lane;
-      if (rr < n_rows) {
-        const int64_t seq = P.seq_list ? P.seq_list[task.seq_off + rr / P.g] : rr / P.g;
-        const int h = j * P.g + (int)(rr % P.g);
+      const bool live = rr < n_rows;
+      int64_t seq = 0;
+      int h = 0;
+      if (live) {
+        seq = P.seq_list ? P.seq_list[task.seq_off + rr / P.g] : rr / P.g;
+        h = j * P.g + (int)(rr % P.g);
         P.lse[out_slot * P.lse_slot_stride + seq * P.Hq + h] = -INFINITY;
         float4 *o = reinterpret_cast<float4 *>(P.o + out_slot * P.o_slot_stride + (seq * P.Hq + h) * HD);
         for (int c = 0; c < HD / 4; ++c) o[c] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
+      if (P.fc.cnt) tc1_fused_arrive(P.fc, live, seq, h, P.Hq, lane);
     }
     return;
   }
@@ -356,6 +383,7 @@ __global__ void __launch_bounds__(tc::kThreads, 1) prefix_tc_kernel(const __grid
       }
     }
     if (live) P.lse[out_slot * P.lse_slot_stride + seq * P.Hq + h] = (m2 + log2f(l)) * HYDRA_LN2;
+    if (P.fc.cnt) tc1_fused_arrive(P.fc, live, seq, h, P.Hq, lane);
   }
 
   ptx::tc_fence_before();
@@ -410,6 +438,8 @@ hydra_status launch_prefix_tc(const PrefixTcArgs &a, cudaStream_t s) {
   P.o_slot_stride = a.o_slot_stride;
   P.lse_slot_stride = a.lse_slot_stride;
   P.debug_variant = a.debug_variant;
+  P.fc = a.fc;
+  if (P.fc.cnt && (a.tasks || P.fc.n_pre_splits != a.n_splits || P.fc.sk_total != 0)) return HYDRA_EINVAL;
   const int n_x = a.tasks ? a.n_tasks : (int)(((int64_t)a.B * a.g + tc::BM - 1) / tc::BM);
   if (n_x == 0) return HYDRA_OK;
   const dim3 grid(n_x, a.Hkv, a.n_splits);

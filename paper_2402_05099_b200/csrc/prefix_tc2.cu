@@ -35,6 +35,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "ptx.cuh"
+#include "fused.cuh"
 
 namespace hydra {
 
@@ -86,6 +87,7 @@ struct __align__(64) PrefixTc2Params {
   int32_t debug;         // timing experiments only (invalid results): bit 1 no softmax math, bit 2 no K/V TMA
   long long *trace;      // diagnostics: CTA 0 event timestamps (clock64), see tools/prefix_trace.py; null = off
   int32_t mutate;        // testing build only: 1 = CTA 0 skips one 4-row store group of its epilogues
+  FusedCombine fc;       // fc.cnt != null: the Eq. 5 merge of every completed row in this epilogue (fused.cuh)
   float *o, *lse;
   int64_t o_slot_stride, lse_slot_stride;
 };
@@ -173,6 +175,27 @@ __device__ __forceinline__ bool seg_next(const PrefixTc2Params &P, SegIter &s, I
   it.nblk = len;
   s.x += len;
   return true;
+}
+
+// Fused Eq. 5 (fused.cuh): after this warp's rows of a piece are stored, count each live row's
+// arrival; the warp merges the rows this piece completed, one row at a time.
+__device__ __forceinline__ void tc2_fused_arrive(const PrefixTc2Params &P, bool live, int64_t seq, int h, int lane) {
+  __threadfence();
+  __syncwarp();
+  const int64_t row = seq * P.Hq + h;
+  int n_pre = 0;
+  bool last = false;
+  if (live) {
+    n_pre = fc_prefix_pieces(P.fc, seq, h);
+    last = fc_arrive(P.fc, row, n_pre + P.fc.n_suf);
+  }
+  unsigned mask = __ballot_sync(0xffffffffu, last);
+  if (mask) __threadfence();
+  while (mask) {
+    const int src = __ffs(mask) - 1;
+    mask &= mask - 1;
+    fc_merge_row_warp(P.fc, __shfl_sync(0xffffffffu, row, src), __shfl_sync(0xffffffffu, n_pre, src), lane);
+  }
 }
 
 // kPolyEvery -- 0: all exp2 on MUFU; k: every k-th column pair on the FMA pipe.
@@ -374,6 +397,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
           P.lse[it.slot * P.lse_slot_stride + seq * P.Hq + h] = -INFINITY;
           for (int c = 0; c < HD / 4; ++c) reinterpret_cast<float4 *>(orow)[c] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
+        if (P.fc.cnt) tc2_fused_arrive(P, live, seq, h, lane);
         continue;
       }
       // ---- Q row -> sQ (canonical K-major SWIZZLE_128B: 16-B chunk c of row r at c ^ (r % 8))
@@ -606,6 +630,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
       ptx::tc_fence_before();
       ptx::warp_arrive(&o_free[t]);
       if (live) P.lse[it.slot * P.lse_slot_stride + seq * P.Hq + h] = (m2 + log2f(l)) * HYDRA_LN2;
+      if (P.fc.cnt) tc2_fused_arrive(P, live, seq, h, lane);
       // the staging writes to sQ were generic-proxy; order them before the next item's Q writes+TMA reads
       ptx::fence_proxy_async_smem();
     }
@@ -1014,6 +1039,16 @@ int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn) {
   return tc2_plan(B, g, Hkv, P, n_ctas, bn).ctas;
 }
 
+void prefix_tc2_plan_into(FusedCombine &fc, int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn) {
+  const Tc2Plan pl = tc2_plan(B, g, Hkv, P, n_ctas, bn);
+  fc.sk_total = pl.total;
+  fc.sk_group = pl.group;
+  fc.sk_G = pl.ctas / pl.group;
+  fc.sk_nb = (int32_t)((P + bn - 1) / bn);
+  fc.sk_npairs = (int32_t)((B * g + 255) / 256);
+  fc.n_pre_splits = 0;
+}
+
 template <int kPoly, bool kPP, bool kSplit = false>
 static cudaError_t tc2_launch(const PrefixTc2Params &P, int grid, cudaStream_t s) {
   const cudaError_t attr = ensure_smem_attr(reinterpret_cast<const void *>(prefix_tc2_kernel<kPoly, kPP, kSplit>),
@@ -1069,6 +1104,11 @@ hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s
   P.lse = a.lse;
   P.o_slot_stride = a.o_slot_stride;
   P.lse_slot_stride = a.lse_slot_stride;
+  P.fc = a.fc;
+  if (P.fc.cnt) {  // fused Eq. 5: flat mode, variants 3 / 5 / 6; the plan must be this launch's
+    if (a.tasks || v4 || P.fc.sk_total != pl.total || P.fc.sk_G != pl.ctas / pl.group || P.fc.sk_group != pl.group)
+      return HYDRA_EINVAL;
+  }
   const int64_t work = a.tasks ? P.n_items : P.total_blocks;
   if (work == 0) return HYDRA_OK;
   const int grid = a.tasks ? (int)(n_ctas > 0 && n_ctas < work ? n_ctas : work) : pl.ctas;

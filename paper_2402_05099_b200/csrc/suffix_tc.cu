@@ -40,6 +40,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "ptx.cuh"
+#include "fused.cuh"
 
 namespace hydra {
 
@@ -105,6 +106,7 @@ struct __align__(64) SuffixTcParams {
   // [sp * split_len, (sp + 1) * split_len) of sequence b; its (O, LSE) go to slot sp
   int32_t n_split, split_len;
   int64_t o_split_stride, lse_split_stride;
+  FusedCombine fc;  // fc.cnt != null: the epilogue warps count each row's part and merge completed rows
 };
 namespace stc {
 constexpr int kTraceN = 1024;
@@ -495,7 +497,8 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
       len_next = item_len_raw<SPLIT>(P, item + gridDim.x);
       const int nblk = (len + BT - 1) / BT;
       const int64_t row0 = (int64_t)ir.b * P.Hq + (int64_t)ir.j * g;
-      if (nblk == 0) {  // empty suffix (or split): (0, -inf) sentinel
+      if (nblk == 0) {  // empty suffix (or split): (0, -inf) sentinel (fused: written by the epilogue warps)
+        if (P.fc.cnt) continue;
         for (int h = 0; h < g; ++h) {
           P.o[ir.o_off + (row0 + h) * HD + r] = 0.f;
           if (r == 0) P.lse[ir.lse_off + row0 + h] = -INFINITY;
@@ -626,11 +629,43 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
     const int r = quarter * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     uint32_t item_no = 0;
+    __shared__ uint32_t fc_mask;  // fused Eq. 5: rows of the current item completed by this part
+    // Fused Eq. 5 (fused.cuh): the 4 epilogue warps' stores of an item's part precede the
+    // arrivals (one per row, warp 8); every completed row is merged by all 128 threads.
+    auto fused_arrive = [&](const ItemRef &ir, int64_t row0) {
+      __threadfence();
+      named_bar_sync(2, 128);
+      if (warp == 8) {
+        const bool last = lane < G && fc_arrive(P.fc, row0 + lane, fc_expected(P.fc, ir.b, ir.j * G + lane));
+        const uint32_t m = __ballot_sync(0xffffffffu, last);
+        if (lane == 0) fc_mask = m;
+      }
+      named_bar_sync(2, 128);
+      uint32_t m = fc_mask;
+      if (m) __threadfence();
+      while (m) {
+        const int h = __ffs(m) - 1;
+        m &= m - 1;
+        fc_merge_row_dim(P.fc, row0 + h, fc_prefix_pieces(P.fc, ir.b, ir.j * G + h), r);
+      }
+    };
     int len_next = item_len_raw<SPLIT>(P, blockIdx.x);
     for (int item = blockIdx.x; item < P.n_items; item += gridDim.x) {
       const int len = item_len_of<SPLIT>(P, item, len_next);
       len_next = item_len_raw<SPLIT>(P, item + gridDim.x);
-      if (len <= 0) continue;
+      if (len <= 0) {
+        if (P.fc.cnt) {  // fused: the empty part (0, -inf) is written and counted here
+          const ItemRef ir = item_ref<SPLIT>(P, item);
+          const int64_t row0 = (int64_t)ir.b * P.Hq + (int64_t)ir.j * g;
+#pragma unroll
+          for (int h = 0; h < G; ++h) {
+            P.o[ir.o_off + (row0 + h) * HD + r] = 0.f;
+            if (r == h) P.lse[ir.lse_off + row0 + h] = -INFINITY;
+          }
+          fused_arrive(ir, row0);
+        }
+        continue;
+      }
       const ItemRef ir = item_ref<SPLIT>(P, item);
       const int64_t row0 = (int64_t)ir.b * P.Hq + (int64_t)ir.j * g;
       const uint32_t ob = item_no & 1, ph = (item_no >> 1) & 1;
@@ -656,6 +691,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
         if (!(skip0 && h == 0)) P.o[ir.o_off + (row0 + h) * HD + r] = __uint_as_float(ov[h]) / L[h];
         if (r == h) P.lse[ir.lse_off + row0 + h] = (M[h] + log2f(L[h])) * HYDRA_LN2;
       }
+      if (P.fc.cnt) fused_arrive(ir, row0);
       ++item_no;
     }
   }
@@ -738,6 +774,8 @@ hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s)
   P.debug = kTesting ? a.debug : 0;
   P.mutate = kTesting ? a.mutate : 0;
   P.S_cap = (int32_t)std::min<int64_t>(a.S_cap, INT32_MAX);
+  P.fc = a.fc;
+  if (P.fc.cnt && P.fc.n_suf != P.n_split) return HYDRA_EINVAL;
   P.block_table = a.block_table;
   P.bt_stride = a.bt_stride;
   if (paged) {

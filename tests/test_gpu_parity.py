@@ -27,7 +27,7 @@ def _reset_config():
             "suffix_ctas", "overlap_prefix_ctas")
     for k in keys:
         hydra.set_config(k, 0)
-    defaults = {"prefix_variant": 6, "suffix_cb": 2, "prefix_poly": 4}  # the library defaults
+    defaults = {"prefix_variant": 6, "suffix_cb": 2, "prefix_poly": 4, "fuse_combine": 1}  # the library defaults
     for k, v in defaults.items():
         hydra.set_config(k, v)
     yield
@@ -197,6 +197,33 @@ def test_composite_parity(B, Hq, Hkv, d, P, S, dist, aux):
     assert_parity(out, ref, lse, lref, what="composite")
 
 
+@pytest.mark.parametrize("B,Hq,Hkv,P,S,impls", [
+    (40, 8, 8, 1000, 200, (3, 2)), (24, 32, 8, 513, 33, (3, 2)), (300, 8, 2, 2100, 300, (3, 1)),
+    (33, 4, 1, 700, 129, (2, 2)), (64, 40, 40, 300, 0, (0, 0)), (5, 8, 2, 129, 140, (2, 1))])
+@pytest.mark.parametrize("aux", [False, True])
+def test_fused_combine_matches_separate_combine(B, Hq, Hkv, P, S, impls, aux):
+    """The Eq. 5 merge fused into the kernel epilogues (fused.cuh: the writer of a row's last
+    part merges it) against the separate combine launch (fuse_combine = 0): the same parts
+    merged in the same order, so the outputs are bitwise equal -- for the persistent and the
+    one-tile prefix kernels, both suffix kernels, both schedules, ragged and empty suffixes."""
+    pi, si = impls
+    hydra.set_config("prefix_impl", pi)
+    hydra.set_config("suffix_impl", si)
+    lens = np.random.default_rng(B + P).integers(0, S + 1, B)
+    if S:
+        lens[0] = 0
+    pb = synth.make_problem(B, Hq, Hkv, 128, P, max(S, 1), lens=lens, dtype="bf16", dist="mixed", seed=61)
+    res = []
+    for fuse in (1, 0):
+        hydra.set_config("fuse_combine", fuse)
+        res.append(run_flat(pb, aux=aux))
+    hydra.set_config("fuse_combine", 1)
+    (a, la), (b, lb) = res
+    ref, lref = oracle.flat_attention(pb)
+    assert_parity(a, ref, la, lref, what="fused")
+    assert torch.equal(a, b) and torch.equal(la, lb), (a.float() - b.float()).abs().max()
+
+
 @pytest.mark.parametrize("k", [1, 50, 100, 147])
 @pytest.mark.parametrize("B,Hq,Hkv,P,S", [(40, 8, 8, 1000, 200), (24, 32, 8, 513, 33)])
 def test_composite_sm_partitioned(k, B, Hq, Hkv, P, S):
@@ -296,6 +323,25 @@ def test_lens_out_of_range_is_clamped():
         out, lse = H.hydragen_attention(t["q"], t["pk"], t["pv"], t["sk"], t["sv"], t["lens"], return_lse=True)
         torch.cuda.synchronize()
         assert_parity(out, ref, lse, lref, what=f"clamped lens impl={impl}")
+
+
+@pytest.mark.parametrize("impl", [1, 2])
+@pytest.mark.parametrize("B,P,S", [(32, 1024, 64), (7, 300, 129)])
+def test_per_sequence_baseline_parity(impl, B, P, S):
+    """The microbenchmark's comparison path (bench.py --config grid; P:160 / P:177-192): each
+    sequence attends over its own copy of prefix || suffix with the per-sequence kernels --
+    the same attention, so it must match the oracle like the Hydragen path does."""
+    from paper_2402_05099_b200 import baseline
+
+    hydra.set_config("suffix_impl", impl)
+    lens = np.random.default_rng(B).integers(0, S + 1, B)
+    pb = synth.make_problem(B, 8, 1, 128, P, S, lens=lens, dtype="bf16", dist="mixed", seed=50)
+    t = problem_to(pb, DEV)
+    fk, fv, flens = baseline.per_sequence_cache(t["pk"], t["pv"], t["sk"], t["sv"], t["lens"])
+    o, l = H.suffix_attn(t["q"], fk, fv, flens)
+    torch.cuda.synchronize()
+    ref, lref = oracle.flat_attention(pb)
+    assert_parity(o, ref, l, lref, what=f"per-sequence baseline impl={impl}")
 
 
 # ---------------------------------------------------------------- tree (§3.3)
