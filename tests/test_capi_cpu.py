@@ -89,7 +89,7 @@ def test_validation_errors(lib):
     need = lib.hydra_workspace_size(_lib.HYDRA_OP_ATTN, ctypes.byref(h), 1024, 16384, 256, 0)
     assert need >= 2 * 1024 * 40 * 129 * 4
     st = lib.hydra_attn(ctypes.byref(h), 1024, FAKE, 40 * 128, 128, 16384, FAKE, FAKE, 40 * 128, 128, FAKE, FAKE,
-                        256 * 40 * 128, 40 * 128, 128, 256, FAKE, FAKE, 0, None, FAKE, need - 1, None, None)
+                        256 * 40 * 128, 40 * 128, 128, 256, FAKE, FAKE, 0, None, FAKE, need // 2, None, None)
     assert st == _lib.HYDRA_ENOMEM
 
 
