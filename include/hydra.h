@@ -350,6 +350,11 @@ HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, i
  *   "suffix_unroll"       tokens in flight per row group of the SIMT suffix kernel (4 or 8)
  *   "overlap_prefix_ctas" SM split of hydra_attn with an aux stream (prefix CTAs)
  *   "prefix_stages"       K/V pipeline stages of the one-tile kernel (2 or 3)
+ *   "fuse_combine"        hydra_attn's Eq. 5 merge: 0 (default) a separate combine launch; 1 in
+ *                         the suffix kernel's epilogue in the sequential schedule; 2 also in the
+ *                         SM-partitioned schedule (per-row arrival counters, the writer of a
+ *                         row's last part merges it).  Same bits in every mode; 1 and 2 were
+ *                         measured slower (profiles/r2_fuse_ab.jsonl)
  *   "ev_prefix_begin" / "ev_prefix_end" / "ev_suffix_begin" / "ev_suffix_end"
  *                         measurement: a cudaEvent_t (as an integer) that hydra_attn records
  *                         right before / after its prefix (on the prefix's stream) or suffix

@@ -46,7 +46,13 @@ struct Config {
   int64_t prefix_impl = 0, prefix_splits = 0, prefix_ctas = 0, prefix_stages = 3, prefix_poly = 4, prefix_variant = 6;
   int64_t suffix_impl = 0, suffix_splits = 0, suffix_ctas = 0, suffix_unroll = 4, suffix_cb = 2;
   int64_t overlap_prefix_ctas = 0;
-  int64_t fuse_combine = 1;  // 1: Eq. 5 merged in the kernel epilogues (fused.cuh); 0: separate combine launch
+  // Eq. 5 merged in the kernel epilogues (fused.cuh): 1 in the sequential schedule only (the
+  // suffix merges each row after the prefix kernel), 2 also in the SM-partitioned schedule
+  // (arrival counters), 0 never: a separate combine launch (default).  Measured
+  // (tools/fuse_ab.py, profiles/r2_fuse_ab.jsonl): the epilogue merges serialise a memory
+  // round trip per row behind each item -- C3@16K 0.93 (1) / 3.93 (2) vs 0.96 ms overlapped,
+  // 1.12 vs 1.06 sequential; C4 0.82 vs 0.30 ms; C6 0.28 vs 0.12 ms.
+  int64_t fuse_combine = 0;
   // Measurement: cudaEvent_t handles hydra_attn / hydra_attn_paged record around the prefix (on
   // its stream) and the suffix launches, so a benchmark can time each kernel within the step
   // (also inside a captured graph); 0 = off.  [0] prefix begin, [1] prefix end, [2] suffix
@@ -749,7 +755,7 @@ extern "C" hydra_status hydra_combine(int64_t rows, int32_t d, int32_t n_parts, 
 // kernel with a device-known piece layout (the persistent kernel's stream-K plan, variants
 // 3 / 5 / 6, or the one-tile kernel's fixed splits), and either suffix kernel.
 static bool attn_fused(const hydra_heads *h, int64_t B, int64_t P, int64_t S_cap, int k_over) {
-  if (!g_cfg.fuse_combine || h->dtype != HYDRA_BF16 || h->head_dim != 128 || P <= 0 || S_cap <= 0) return false;
+  if (!g_cfg.fuse_combine || (k_over > 0 && g_cfg.fuse_combine < 2) || h->dtype != HYDRA_BF16 || h->head_dim != 128 || P <= 0 || S_cap <= 0) return false;
   const PrefixKind k = prefix_kind(h, B * (h->num_q_heads / h->num_kv_heads), P, k_over);
   return (k == PK_TC2 && g_cfg.prefix_variant != 4) || k == PK_TC1;
 }
@@ -827,11 +833,13 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
     fc.out_f32 = out_dtype == HYDRA_F32;
     fc.lse_out = lse_out;
     fc.inject_bug = inject_combine_bug() ? 1 : 0;
+    fc.pre_done = sa == s ? 1 : 0;  // one stream: the suffix launch follows the prefix kernel
     if (prefix_kind(h, B * g, P, k_over) == PK_TC2)
       prefix_tc2_plan_into(fc, B, g, h->num_kv_heads, P, k_over > 0 ? k_over : prefix_ctas(), prefix_bn());
     else
       fc.n_pre_splits = np;
-    if (cudaMemsetAsync(fc.cnt, 0, sizeof(int32_t) * rows, s) != cudaSuccess) return cuda_fail("counter reset");
+    if (!(fc.pre_done && ns == 1) && cudaMemsetAsync(fc.cnt, 0, sizeof(int32_t) * rows, s) != cudaSuccess)
+      return cuda_fail("counter reset");
   }
 
   if (sa != s) {

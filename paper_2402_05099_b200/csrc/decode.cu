@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeParams p) 
     // arrivals and merge the rows it completed (thread = dim).
     if (p.fc.cnt) {
       __shared__ uint32_t fc_mask;
-      __threadfence();
+      if (fc_counting(p.fc)) __threadfence();
       __syncthreads();
       if (tid < 32) {
         const bool last = tid < GQ && fc_arrive(p.fc, (int64_t)b * p.Hq + h0 + tid, fc_expected(p.fc, b, h0 + tid));

@@ -8,8 +8,10 @@
 //   * the writer whose increment completes the count (prefix pieces + suffix parts, known
 //     on the device from the launch plan) merges all parts of the row and writes the final
 //     bf16 / f32 output and the merged LSE, then resets the counter.
-// The prefix and suffix kernels may run in either order or concurrently (the SM-partitioned
-// schedule), so there is no waiting anywhere: the merge happens exactly once per row, as
+// With pre_done (the sequential schedule: the suffix launch follows the prefix on one stream)
+// only the suffix parts are counted, and a single suffix part merges without any atomic.
+// Otherwise the prefix and suffix kernels may run in either order or concurrently (the
+// SM-partitioned schedule), so there is no waiting anywhere: the merge happens exactly once per row, as
 // soon as its last part exists.  The caller zeroes the counters before the launches (one
 // memset node) -- this replaces the -inf slot fill and the combine launch of the unfused
 // path.  Partials of other writers are read with ld.global.cg (L2, never a stale L1 line).
@@ -38,12 +40,16 @@ __device__ __forceinline__ int fc_prefix_pieces(const FusedCombine &F, int64_t b
 }
 
 __device__ __forceinline__ int fc_expected(const FusedCombine &F, int64_t b, int h) {
-  return fc_prefix_pieces(F, b, h) + F.n_suf;
+  return F.pre_done ? F.n_suf : fc_prefix_pieces(F, b, h) + F.n_suf;
 }
+
+// The counters are in use unless the prefix is known complete and the suffix has one part.
+__device__ __forceinline__ bool fc_counting(const FusedCombine &F) { return !(F.pre_done && F.n_suf == 1); }
 
 // Called by the writer of a part after its stores (and a __threadfence): counts the arrival,
 // true when this arrival completes the row.
 __device__ __forceinline__ bool fc_arrive(const FusedCombine &F, int64_t row, int expected) {
+  if (expected == 1) return true;  // the only writer of the row's parts (pre_done, one suffix part)
   int old;
   asm volatile("atom.add.acq_rel.gpu.s32 %0, [%1], 1;" : "=r"(old) : "l"(F.cnt + row) : "memory");
   return old + 1 == expected;
@@ -89,7 +95,7 @@ __device__ __forceinline__ void fc_merge_row_warp(const FusedCombine &F, int64_t
   }
   if (lane == 0) {
     if (F.lse_out) F.lse_out[row] = m == -INFINITY ? -INFINITY : m + logf(den);
-    F.cnt[row] = 0;  // ready for the next call (stream-ordered after this kernel)
+    if (fc_counting(F)) F.cnt[row] = 0;  // ready for the next call (stream-ordered after this kernel)
   }
 }
 
@@ -115,7 +121,7 @@ __device__ __forceinline__ void fc_merge_row_dim(const FusedCombine &F, int64_t 
     reinterpret_cast<__nv_bfloat16 *>(F.out)[row * 128 + e] = __float2bfloat16_rn(acc);
   if (e == 0) {
     if (F.lse_out) F.lse_out[row] = m == -INFINITY ? -INFINITY : m + logf(den);
-    F.cnt[row] = 0;
+    if (fc_counting(F)) F.cnt[row] = 0;
   }
 }
 

@@ -45,6 +45,10 @@ struct FusedCombine {
   int32_t out_f32;
   float *lse_out;               // [B*Hq] merged LSE (nullable)
   int32_t inject_bug;           // testing build only: w_p = 1
+  // 1: the prefix kernel completed before the suffix launch (same stream, sequential schedule):
+  // the prefix neither counts nor merges, the suffix parts alone are counted (expected = n_suf),
+  // and with one suffix part its writer merges at once -- no atomics, no counter reset
+  int32_t pre_done;
 };
 
 // ---------------------------------------------------------------- SIMT decode kernel

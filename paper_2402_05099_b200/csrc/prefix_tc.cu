@@ -77,6 +77,7 @@ struct __align__(64) PrefixTcKernelParams {
 // Fused Eq. 5 (fused.cuh): count this warp's rows; merge the rows this split completed.
 __device__ __forceinline__ void tc1_fused_arrive(const FusedCombine &F, bool live, int64_t seq, int h, int Hq,
                                                  int lane) {
+  if (F.pre_done) return;  // sequential schedule: the suffix kernel counts and merges
   __threadfence();
   __syncwarp();
   const int64_t row = seq * Hq + h;

@@ -180,6 +180,7 @@ __device__ __forceinline__ bool seg_next(const PrefixTc2Params &P, SegIter &s, I
 // Fused Eq. 5 (fused.cuh): after this warp's rows of a piece are stored, count each live row's
 // arrival; the warp merges the rows this piece completed, one row at a time.
 __device__ __forceinline__ void tc2_fused_arrive(const PrefixTc2Params &P, bool live, int64_t seq, int h, int lane) {
+  if (P.fc.pre_done) return;  // sequential schedule: the suffix kernel counts and merges
   __threadfence();
   __syncwarp();
   const int64_t row = seq * P.Hq + h;

@@ -633,7 +633,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
     // Fused Eq. 5 (fused.cuh): the 4 epilogue warps' stores of an item's part precede the
     // arrivals (one per row, warp 8); every completed row is merged by all 128 threads.
     auto fused_arrive = [&](const ItemRef &ir, int64_t row0) {
-      __threadfence();
+      if (fc_counting(P.fc)) __threadfence();
       named_bar_sync(2, 128);
       if (warp == 8) {
         const bool last = lane < G && fc_arrive(P.fc, row0 + lane, fc_expected(P.fc, ir.b, ir.j * G + lane));

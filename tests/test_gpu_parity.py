@@ -27,7 +27,7 @@ def _reset_config():
             "suffix_ctas", "overlap_prefix_ctas")
     for k in keys:
         hydra.set_config(k, 0)
-    defaults = {"prefix_variant": 6, "suffix_cb": 2, "prefix_poly": 4, "fuse_combine": 1}  # the library defaults
+    defaults = {"prefix_variant": 6, "suffix_cb": 2, "prefix_poly": 4, "fuse_combine": 0}  # the library defaults
     for k, v in defaults.items():
         hydra.set_config(k, v)
     yield
@@ -205,7 +205,8 @@ def test_fused_combine_matches_separate_combine(B, Hq, Hkv, P, S, impls, aux):
     """The Eq. 5 merge fused into the kernel epilogues (fused.cuh: the writer of a row's last
     part merges it) against the separate combine launch (fuse_combine = 0): the same parts
     merged in the same order, so the outputs are bitwise equal -- for the persistent and the
-    one-tile prefix kernels, both suffix kernels, both schedules, ragged and empty suffixes."""
+    one-tile prefix kernels, both suffix kernels, both schedules, ragged and empty suffixes.
+    fuse_combine = 2 forces the arrival-counter protocol in the SM-partitioned schedule too."""
     pi, si = impls
     hydra.set_config("prefix_impl", pi)
     hydra.set_config("suffix_impl", si)
@@ -214,14 +215,16 @@ def test_fused_combine_matches_separate_combine(B, Hq, Hkv, P, S, impls, aux):
         lens[0] = 0
     pb = synth.make_problem(B, Hq, Hkv, 128, P, max(S, 1), lens=lens, dtype="bf16", dist="mixed", seed=61)
     res = []
-    for fuse in (1, 0):
+    for fuse in (1, 2, 0):  # sequential only, counters in both schedules, never (default)
         hydra.set_config("fuse_combine", fuse)
         res.append(run_flat(pb, aux=aux))
-    hydra.set_config("fuse_combine", 1)
-    (a, la), (b, lb) = res
+    hydra.set_config("fuse_combine", 0)
+    (a, la), (c, lc), (b, lb) = res
     ref, lref = oracle.flat_attention(pb)
     assert_parity(a, ref, la, lref, what="fused")
+    assert_parity(c, ref, lc, lref, what="fused, counters")
     assert torch.equal(a, b) and torch.equal(la, lb), (a.float() - b.float()).abs().max()
+    assert torch.equal(c, b) and torch.equal(lc, lb), (c.float() - b.float()).abs().max()
 
 
 @pytest.mark.parametrize("k", [1, 50, 100, 147])
