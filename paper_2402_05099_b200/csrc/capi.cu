@@ -113,7 +113,7 @@ extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
       return fail(HYDRA_EINVAL, "config key '%s' exists only in the testing build (libhydra_test.so)", key);
     int64_t v = value;
     if (!strcmp(key, "prefix_poly")) v = (v == 0 || v == 3 || v == 4 || v == 8 || (kTesting && v == -1)) ? v : 4;
-    if (!strcmp(key, "prefix_variant")) v = (v == 3 || v == 4 || v == 5) ? v : 6;
+    if (!strcmp(key, "prefix_variant")) v = (v == 3 || v == 4 || v == 5 || v == 9) ? v : 6;
     if (!strcmp(key, "prefix_stages")) v = (v == 2 ? 2 : 3);
     if (!strcmp(key, "suffix_cb")) v = (v == 1 ? 1 : 2);
     if (!strcmp(key, "suffix_unroll")) v = (v >= 8 ? 8 : v >= 4 ? 4 : 2);
@@ -127,6 +127,7 @@ extern "C" int64_t hydra_get_config(const char *key) {
   if (!key) return -1;
   if (!strcmp(key, "last_overlap_k")) return g_cfg.last_overlap_k;
   if (!strcmp(key, "testing_build")) return kTesting ? 1 : 0;
+  if (!strcmp(key, "pair_max_ctas")) return prefix_pair_plan(1 << 20, 1, 1, 1 << 20, 1 << 20).ctas;  // resident CTA pairs x 2
   for (int i = 0; i < 4; ++i)
     if (!strcmp(key, kStepEvKeys[i])) return g_cfg.step_ev[i];
   for (const Key &k : kKeys)
@@ -246,6 +247,8 @@ static int suffix_splits(const hydra_heads *h, int64_t B, int64_t S_cap, bool ov
 enum PrefixKind { PK_SIMT = 1, PK_TC1 = 2, PK_TC2 = 3 };
 static int prefix_ctas() { return g_cfg.prefix_ctas > 0 ? (int)g_cfg.prefix_ctas : device_sm_count(); }
 static int prefix_bn() { return g_cfg.prefix_variant == 4 ? 64 : 128; }  // KV tokens per persistent-kernel block
+// flat mode of the persistent prefix kernel on CTA pairs (variant 9, prefix_pair.cu)
+static bool pair_mode(int g) { return g_cfg.prefix_variant == 9 && prefix_pair_supported(g); }
 // B/P-dependent choice (rows = stacked query rows per KV head, P = KV tokens per row):
 // the persistent kernel amortises its per-segment Q load / epilogue only when every CTA
 // owns enough 128-token blocks; small problems run the one-tile kernel (more parallelism).
@@ -302,7 +305,8 @@ static int prefix_splits(const hydra_heads *h, int64_t B, int64_t P, int tc2_cta
   const int g = h->num_q_heads / h->num_kv_heads;
   switch (prefix_kind(h, B * g, P, tc2_ctas)) {
     case PK_TC2:
-      return prefix_tc2_slots(B, g, h->num_kv_heads, P, tc2_ctas > 0 ? tc2_ctas : prefix_ctas(), prefix_bn());
+      return prefix_tc2_slots(B, g, h->num_kv_heads, P, tc2_ctas > 0 ? tc2_ctas : prefix_ctas(), prefix_bn(),
+                              pair_mode(g));
     case PK_TC1:
       return prefix_splits_tc(((B * g + 127) / 128) * h->num_kv_heads, P);
     default:
@@ -336,7 +340,7 @@ static int overlap_prefix_ctas(const hydra_heads *h, int64_t B, int64_t P, int64
   double best = 1e300;
   for (int k = 8; k <= sms - 8; ++k) {
     if (prefix_kind(h, B * g, P, k) != PK_TC2) break;  // too few blocks per CTA beyond this k
-    if (prefix_tc2_ctas(B, g, h->num_kv_heads, P, k, prefix_bn()) != k) continue;  // plan would idle SMs
+    if (prefix_tc2_ctas(B, g, h->num_kv_heads, P, k, prefix_bn(), pair_mode(g)) != k) continue;  // plan would idle SMs
     const double t = std::max(pair_blocks / (k * R_P), suffix_tc_us(h, B, S_cap, sms - k, R_S, BW));
     if (t < best) {
       best = t;
@@ -757,7 +761,7 @@ extern "C" hydra_status hydra_combine(int64_t rows, int32_t d, int32_t n_parts, 
 static bool attn_fused(const hydra_heads *h, int64_t B, int64_t P, int64_t S_cap, int k_over) {
   if (!g_cfg.fuse_combine || (k_over > 0 && g_cfg.fuse_combine < 2) || h->dtype != HYDRA_BF16 || h->head_dim != 128 || P <= 0 || S_cap <= 0) return false;
   const PrefixKind k = prefix_kind(h, B * (h->num_q_heads / h->num_kv_heads), P, k_over);
-  return (k == PK_TC2 && g_cfg.prefix_variant != 4) || k == PK_TC1;
+  return (k == PK_TC2 && g_cfg.prefix_variant != 4 && !pair_mode(h->num_q_heads / h->num_kv_heads)) || k == PK_TC1;
 }
 
 // ------------------------------------------------------------------ composite
@@ -857,8 +861,7 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
   if (st) return st;
   if (S_cap > 0) {
     // the suffix takes every SM the prefix plan leaves free (the plan may round k down)
-    const int k_eff = k_over > 0 ? prefix_tc2_ctas(B, h->num_q_heads / h->num_kv_heads, h->num_kv_heads, P, k_over,
-                                                   prefix_bn())
+    const int k_eff = k_over > 0 ? prefix_tc2_ctas(B, g, h->num_kv_heads, P, k_over, prefix_bn(), pair_mode(g))
                                  : 0;
     record_step_ev(2, s);
     st = run_suffix(h, B, q, q_sb, q_sh, sk, sv, s_sb, s_st, s_sh, S_cap, lens, ns, suf, s,

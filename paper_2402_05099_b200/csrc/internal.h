@@ -153,11 +153,21 @@ hydra_status launch_prefix_tc(const PrefixTcArgs &a, cudaStream_t s);
 // v3: persistent, two 128-row query tiles per CTA; flat mode is stream-K over n_ctas CTAs
 // (partial slots per row = prefix_tc2_slots), task mode deals (task, head, split) items.
 hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s);
-int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn);
-int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn);
+int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn, bool pair = false);
+int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn, bool pair = false);
 // The flat-mode stream-K plan of launch_prefix_tc2 over n_ctas CTAs, as the fused combine
 // needs it (which partial slots hold a row's pieces): fills fc.sk_*.
 void prefix_tc2_plan_into(FusedCombine &fc, int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn);
+// CTA-pair (cta_group::2) persistent prefix kernel, flat mode, 128 % g == 0 (prefix_pair.cu):
+// same grouped stream-K plan as launch_prefix_tc2 with a CTA pair as the worker.
+struct PairPlan {
+  int group, workers, ctas;
+  int64_t total;
+};
+bool prefix_pair_supported(int g);
+PairPlan prefix_pair_plan(int64_t B, int g, int Hkv, int64_t P, int n_ctas);
+int prefix_pair_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas);
+hydra_status launch_prefix_pair(const PrefixTcArgs &a, int n_ctas, cudaStream_t s);
 // Persistent tensor-core suffix kernel (bf16, d = 128, g <= 16), TMA-fed.
 struct SuffixTcArgs {
   const void *q;

@@ -1028,7 +1028,8 @@ static Tc2Plan tc2_plan(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn
 }
 
 // Flat mode: number of partial slots per row the schedule over n_ctas CTAs produces.
-int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn) {
+int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn, bool pair) {
+  if (pair) return prefix_pair_slots(B, g, Hkv, P, n_ctas);
   const Tc2Plan pl = tc2_plan(B, g, Hkv, P, n_ctas, bn);
   if (pl.total <= 0) return 1;
   const int64_t nb = (P + bn - 1) / bn;
@@ -1036,7 +1037,8 @@ int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn) {
   return (int)((nb + range - 1) / range + 1);
 }
 
-int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn) {
+int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn, bool pair) {
+  if (pair) return prefix_pair_plan(B, g, Hkv, P, n_ctas).ctas;
   return tc2_plan(B, g, Hkv, P, n_ctas, bn).ctas;
 }
 
@@ -1064,6 +1066,7 @@ static cudaError_t tc4_attr() {
 }
 
 hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s) {
+  if (a.variant == 9 && !a.tasks && prefix_pair_supported(a.g)) return launch_prefix_pair(a, n_ctas, s);
   const int poly = a.poly_every;
   const bool v4 = a.variant == 4;
   const int bn = v4 ? tc4::BN : tc2::BN;
@@ -1119,7 +1122,7 @@ hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s
   }
   const bool spec = a.variant == 5;
   cudaError_t e;
-  if (a.variant == 6) {  // split P publication
+  if (a.variant == 6 || a.variant == 9) {  // split P publication (9: task mode / other g of the pair kernel)
     e = poly == 4 ? tc2_launch<4, false, true>(P, grid, s) : tc2_launch<0, false, true>(P, grid, s);
     return e == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
   }

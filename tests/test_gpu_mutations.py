@@ -8,6 +8,7 @@ tests/nanfill.py exactly as the parity tests do, and reports whether the parity 
 caught the mutation:
   combine_bug        Eq. 5 combine without its rescaling (w_p = 1)
   skip_prefix_store  persistent tcgen05 prefix kernel: CTA 0 skips one 4-row store group
+  skip_pair_store    CTA-pair prefix kernel: worker 0 skips the stores of 4 rows
   skip_suffix_store  tensor-core suffix kernel: CTA 0 skips head 0's row of its first item
   clean              no mutation: the same calls must pass (control)
 Also: the testing build's device check of the lens precondition counts lens[b] > S_cap and
@@ -37,6 +38,7 @@ res = {}
 def run(case):
     for k in ("prefix_impl", "suffix_impl", "inject_combine_bug", "mutate"):
         hydra.set_config(k, 0)
+    hydra.set_config("prefix_variant", 6)
     if case in ("combine_bug", "clean_composite"):
         if case == "combine_bug":
             hydra.set_config("inject_combine_bug", 1)
@@ -44,10 +46,13 @@ def run(case):
         t = problem_to(pb, DEV)
         out, lse = H.hydragen_attention(t["q"], t["pk"], t["pv"], t["sk"], t["sv"], t["lens"], return_lse=True)
         ref, lref = oracle.flat_attention(pb)
-    elif case in ("skip_prefix_store", "clean_prefix"):
+    elif case in ("skip_prefix_store", "clean_prefix", "skip_pair_store", "clean_pair"):
         hydra.set_config("prefix_impl", 3)
+        hydra.set_config("prefix_variant", 9 if "pair" in case else 6)
         if case == "skip_prefix_store":
             hydra.set_config("mutate", 1)
+        if case == "skip_pair_store":
+            hydra.set_config("mutate", 3)
         pb = synth.make_problem(300, 8, 2, 128, 1100, 1, dtype="bf16", dist="mixed", seed=4)
         t = problem_to(pb, DEV)
         out, lse = H.prefix_attn(t["q"], t["pk"], t["pv"])
@@ -67,8 +72,8 @@ def run(case):
     except AssertionError as e:
         return "caught: " + str(e)[:80]
 
-for case in ("clean_composite", "combine_bug", "clean_prefix", "skip_prefix_store", "clean_suffix",
-             "skip_suffix_store"):
+for case in ("clean_composite", "combine_bug", "clean_prefix", "skip_prefix_store", "clean_pair", "skip_pair_store",
+             "clean_suffix", "skip_suffix_store"):
     res[case] = run(case)
 
 # lens precondition: device check in the testing build
@@ -94,12 +99,12 @@ def results():
     return json.loads(line[0][7:])
 
 
-@pytest.mark.parametrize("case", ["clean_composite", "clean_prefix", "clean_suffix"])
+@pytest.mark.parametrize("case", ["clean_composite", "clean_prefix", "clean_pair", "clean_suffix"])
 def test_unmutated_testing_build_passes(results, case):
     assert results[case] == "pass", results[case]
 
 
-@pytest.mark.parametrize("case", ["combine_bug", "skip_prefix_store", "skip_suffix_store"])
+@pytest.mark.parametrize("case", ["combine_bug", "skip_prefix_store", "skip_pair_store", "skip_suffix_store"])
 def test_mutation_is_caught(results, case):
     assert results[case].startswith("caught"), f"{case} passed the parity gate"
 

@@ -73,11 +73,12 @@ PREFIX_SHAPES = [
 
 @pytest.mark.parametrize("B,Hq,Hkv,P", PREFIX_SHAPES)
 @pytest.mark.parametrize("dist", ["mixed", "boundary"])
-@pytest.mark.parametrize("impl", [2, 3, 4, 5, 6])
+@pytest.mark.parametrize("impl", [2, 3, 4, 5, 6, 9])
 def test_prefix_tc_parity(B, Hq, Hkv, P, dist, impl):
     # 2: one-tile tcgen05 kernel, 3: persistent two-tile (128-token blocks), 4: same with 64-token
     # blocks and double-buffered scores, 5: 3 with the speculative (running-max) softmax,
-    # 6: 3 with P published in two halves (default)
+    # 6: 3 with P published in two halves (default), 9: CTA-pair kernel (cta_group::2, M = 256,
+    # double-buffered scores, token-split softmax; prefix_pair.cu)
     hydra.set_config("prefix_impl", min(impl, 3))
     hydra.set_config("prefix_variant", impl if impl >= 3 else 3)
     pb = synth.make_problem(B, Hq, Hkv, 128, P, 1, dtype="bf16", dist=dist, seed=3)
@@ -100,7 +101,7 @@ def test_prefix_tc_splits(splits):
     assert_parity(o, ref, lse, lref, what=f"prefix splits={splits}")
 
 
-@pytest.mark.parametrize("variant,poly", [(3, 0), (5, 0), (5, 4), (5, 8), (3, 4), (6, 0), (6, 4)])
+@pytest.mark.parametrize("variant,poly", [(3, 0), (5, 0), (5, 4), (5, 8), (3, 4), (6, 0), (6, 4), (9, 0), (9, 4)])
 def test_prefix_tc2_growing_max(variant, poly):
     """Scores that grow along the prefix: the running max is raised block after block, which
     exercises the O/l correction and, for the speculative softmax, the redo path."""
@@ -121,7 +122,7 @@ def test_prefix_tc2_growing_max(variant, poly):
 
 
 @pytest.mark.parametrize("ctas", [1, 3, 7, 64, 148, 100000])
-@pytest.mark.parametrize("variant", [3, 4, 5, 6])
+@pytest.mark.parametrize("variant", [3, 4, 5, 6, 9])
 def test_prefix_tc2_stream_k_ctas(ctas, variant):
     """Stream-K piece boundaries fall inside items for most CTA counts; every piece is merged."""
     hydra.set_config("prefix_ctas", ctas)
@@ -132,6 +133,37 @@ def test_prefix_tc2_stream_k_ctas(ctas, variant):
     torch.cuda.synchronize()
     ref, lref = oracle.prefix_only(pb)
     assert_parity(o, ref, lse, lref, what=f"prefix ctas={ctas}")
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,P", [(1024, 40, 40, 700), (512, 32, 8, 1500), (256, 32, 4, 999), (77, 16, 1, 300),
+                                        (5, 12, 4, 2000), (64, 64, 2, 129)])
+@pytest.mark.parametrize("ctas", [0, 6, 60])
+def test_prefix_pair_shapes(B, Hq, Hkv, P, ctas):
+    """CTA-pair kernel: MHA and GQA g = 4 / 8 / 16 / 32 (Q tiles by a 4-D TMA box of 128/g
+    sequences), g = 3 (unsupported: the two-tile kernel runs instead), partial pairs (B*g not a
+    multiple of 256), prefix tails inside the second token half of a block, grouped and
+    ungrouped stream-K plans."""
+    hydra.set_config("prefix_impl", 3)
+    hydra.set_config("prefix_variant", 9)
+    hydra.set_config("prefix_ctas", ctas)
+    pb = synth.make_problem(B, Hq, Hkv, 128, P, 1, dtype="bf16", dist="boundary", seed=B + P)
+    t = problem_to(pb, DEV)
+    o, lse = H.prefix_attn(t["q"], t["pk"], t["pv"])
+    torch.cuda.synchronize()
+    ref, lref = oracle.prefix_only(pb)
+    assert_parity(o, ref, lse, lref, what=f"pair prefix {B},{Hq},{Hkv},{P} ctas={ctas}")
+
+
+@pytest.mark.parametrize("aux", [False, True])
+@pytest.mark.parametrize("B,Hq,Hkv,P,S", [(40, 8, 8, 1000, 200), (24, 32, 8, 513, 33), (300, 8, 2, 2100, 300)])
+def test_composite_pair_prefix(B, Hq, Hkv, P, S, aux):
+    """hydra_attn with the CTA-pair prefix kernel in the sequential and the SM-partitioned schedule."""
+    hydra.set_config("prefix_variant", 9)
+    lens = np.random.default_rng(B + S).integers(0, S + 1, B)
+    pb = synth.make_problem(B, Hq, Hkv, 128, P, S, lens=lens, dtype="bf16", dist="mixed", seed=71)
+    out, lse = run_flat(pb, aux=aux)
+    ref, lref = oracle.flat_attention(pb)
+    assert_parity(out, ref, lse, lref, what="composite, pair prefix")
 
 
 def test_prefix_simt_bf16():
