@@ -336,10 +336,14 @@ HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, i
 /*
  * Tuning switches, per calling thread (thread-local; 0 = automatic unless stated):
  *   "prefix_impl"         1 SIMT, 2 one-tile tcgen05 kernel, 3 persistent two-tile tcgen05 kernel
- *   "prefix_variant"      persistent kernel: 6 (default: 128-token blocks, P published in two
- *                         64-token halves), 3 (128-token blocks), 4 (64-token blocks,
- *                         double-buffered scores), 5 (3 + speculative running-max softmax)
+ *   "prefix_variant"      persistent kernel: 9 (default: CTA-pair kernel, cta_group::2 M = 256
+ *                         MMAs, three score buffers, blocks alternating between two softmax
+ *                         warpgroups; flat mode with 128 % g == 0, else 6 runs), 6 (one CTA, two
+ *                         128-row tiles, P published in two 64-token halves), 3 (6 without the
+ *                         split), 4 (64-token blocks, double-buffered scores), 5 (3 + speculative
+ *                         running-max softmax)
  *   "prefix_poly"         4 (default): every 4th exp2 pair on the FMA pipe; 0 all exp2 on MUFU; 3 / 8
+ *                         (variants 3-6), 2 / 3 (variant 9)
  *   "prefix_splits"       KV splits of the one-tile / SIMT prefix kernels
  *   "prefix_ctas"         CTAs of the persistent prefix kernel
  *   "suffix_impl"         1 SIMT split-K GEMV, 2 persistent TMA-fed tensor-core kernel

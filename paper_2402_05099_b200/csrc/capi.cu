@@ -43,7 +43,7 @@ static hydra_status cuda_fail(const char *what) {
 // different threads never see each other's switches or measurement events (hydra.h:
 // "reentrant"); a thread that never calls hydra_set_config runs the automatic choices.
 struct Config {
-  int64_t prefix_impl = 0, prefix_splits = 0, prefix_ctas = 0, prefix_stages = 3, prefix_poly = 4, prefix_variant = 6;
+  int64_t prefix_impl = 0, prefix_splits = 0, prefix_ctas = 0, prefix_stages = 3, prefix_poly = 4, prefix_variant = 9;
   int64_t suffix_impl = 0, suffix_splits = 0, suffix_ctas = 0, suffix_unroll = 4, suffix_cb = 2;
   int64_t overlap_prefix_ctas = 0;
   // Eq. 5 merged in the kernel epilogues (fused.cuh): 1 in the sequential schedule only (the
@@ -112,8 +112,8 @@ extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
     if (k.testing_only && !kTesting)
       return fail(HYDRA_EINVAL, "config key '%s' exists only in the testing build (libhydra_test.so)", key);
     int64_t v = value;
-    if (!strcmp(key, "prefix_poly")) v = (v == 0 || v == 3 || v == 4 || v == 8 || (kTesting && v == -1)) ? v : 4;
-    if (!strcmp(key, "prefix_variant")) v = (v == 3 || v == 4 || v == 5 || v == 9) ? v : 6;
+    if (!strcmp(key, "prefix_poly")) v = (v == 0 || v == 2 || v == 3 || v == 4 || v == 8 || (kTesting && v == -1)) ? v : 4;
+    if (!strcmp(key, "prefix_variant")) v = (v == 3 || v == 4 || v == 5 || v == 6) ? v : 9;
     if (!strcmp(key, "prefix_stages")) v = (v == 2 ? 2 : 3);
     if (!strcmp(key, "suffix_cb")) v = (v == 1 ? 1 : 2);
     if (!strcmp(key, "suffix_unroll")) v = (v >= 8 ? 8 : v >= 4 ? 4 : 2);

@@ -25,11 +25,13 @@
 // WG) over 64 columns each instead of one warp over 128: half the serial chain per block.
 //
 // Roles per CTA (384 threads):
-//   warp 0      TMA producer (both CTAs): this CTA's Q tile (2 buffers), K tokens
-//               [64*rank, +64) of each block (4-stage ring), V dims [64*rank, +64) of each
-//               block (4-stage ring); completions counted on the LEADER's barriers
+//   warp 0      TMA producer (both CTAs): this CTA's Q tile (2 buffers) and K tokens
+//               [64*rank, +64) of each block (4-stage ring); completions counted on the
+//               LEADER's barriers
+//   warp 2      TMA producer (both CTAs): V dims [64*rank, +64) of each block (4-stage ring)
 //   warp 1      TMEM allocation (both CTAs, cta_group::2) and, in the leader only, the single
-//               MMA-issuing thread:  S(0) S(1) | PV_a(n) PV_b(n) S(n+2) | ...
+//               MMA-issuing thread:  S(0) S(1) | PV_a(n) PV_b(n) S(n+2) | ...  (polls its
+//               barriers: try_wait's suspension cost ~500 cycles of reaction per block)
 //   warps 4-7   softmax WG a (thread = query row = TMEM lane), warps 8-11 WG b
 // Schedule: grouped stream-K over (head, 128-token block) as prefix_tc2.cu, with the CTA pair
 // as the worker: pair p of a group takes query rows [256p, 256p+256) of every head.
@@ -61,14 +63,32 @@ constexpr int VHALF = BN * 128;       // 16 KB: 128 tokens x this CTA's 64 dims
 constexpr int OFF_Q = 0;
 constexpr int OFF_K = OFF_Q + NQ * QTILE;
 constexpr int OFF_V = OFF_K + NSK * KHALF;
-constexpr int OFF_X = OFF_V + NSV * VHALF;  // (m, l) exchange [item parity][WG][128 rows][2]
-constexpr int OFF_BAR = OFF_X + 2 * 2 * BM * 2 * 4;
-// kf, ke [NSK]; vf, ve [NSV]; qf, qe [NQ]; sf [2]; pfa [2]; pfb [2]; pvd [2]; ordy; ofree
-constexpr int N_BARS = 2 * NSK + 2 * NSV + 2 * NQ + 2 + 2 + 2 + 2 + 2;
+constexpr int NSB = 3;                      // score buffers in TMEM
+#ifndef HYDRA_PAIR_POLL_NS
+#define HYDRA_PAIR_POLL_NS 64
+#endif
+constexpr int kPollSleepNs = HYDRA_PAIR_POLL_NS;
+#ifndef HYDRA_PAIR_MMA_WARP
+#define HYDRA_PAIR_MMA_WARP 1
+#endif
+constexpr int kMmaWarp = HYDRA_PAIR_MMA_WARP;  // 1 or 3 (warp 1 allocates TMEM either way)  // MMA thread's back-off between barrier probe rounds
+constexpr int O_COL = NSB * BN;             // O accumulator: TMEM columns [384, 512)
+constexpr int OFF_X = OFF_V + NSV * VHALF;  // row max / sum exchange [parity][WG][128 rows]
+constexpr int OFF_BAR = OFF_X + 6 * BM * 4;  // m exchange [WG][128] + epilogue (m, l) [WG][128][2]
+// kf, ke [NSK]; vf, ve [NSV]; qf, qe [NQ]; sf [NSB]; pf [NSB]; ordy; ofree
+constexpr int N_BARS = 2 * NSK + 2 * NSV + 2 * NQ + 2 * NSB + 2;
 constexpr int BYTES = OFF_BAR + N_BARS * 8 + 16;
 constexpr int ALLOC = BYTES + 1024;
 static_assert(ALLOC <= 232448, "prefix_pair smem over the 227 KB opt-in limit");
 constexpr uint32_t TMEM_COLS = 512;
+// diagnostics (testing build): per block, clock64 of cluster 0's events.  Rows 0-5 WG a warp 4
+// lane 0 of the leader (S wait begin, S ready, S in registers, max done, exps done, P arrived),
+// 6-11 the same for WG b, 12 / 13 MMA thread saw P_a / P_b, 14 S(n+2) issued, 16-21 WG a of the
+// peer CTA.
+constexpr int kTraceN = 1024;
+__device__ __forceinline__ void trace(long long *tr, int row, uint32_t i) {
+  if (kTesting && tr && i < (uint32_t)kTraceN) tr[row * kTraceN + i] = clock64();
+}
 }  // namespace pr
 
 struct __align__(64) PrefixPairParams {
@@ -86,6 +106,9 @@ struct __align__(64) PrefixPairParams {
   float *o, *lse;
   int64_t o_slot_stride, lse_slot_stride;
   int32_t mutate;  // testing build only: 3 = worker 0 skips one 4-row group of its stores
+  long long *trace;  // testing build only: cluster-0 event timestamps [kTraceRows][kTraceN] (tools/pair_trace.py)
+  int32_t debug;     // testing build only, timing experiments (invalid results): 4 = no K/V TMA after the ring
+                     // fill, 2 = no softmax (P published as soon as S lands)
 };
 
 namespace pr {
@@ -168,7 +191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
   uint64_t *kf = bars, *ke = kf + NSK, *vf = ke + NSK, *ve = vf + NSV, *qf = ve + NSV, *qe = qf + NQ;
-  uint64_t *sf = qe + NQ, *pfa = sf + 2, *pfb = pfa + 2, *pvd = pfb + 2, *ordy = pvd + 2, *ofree = ordy + 1;
+  uint64_t *sf = qe + NQ, *pf = sf + NSB, *ordy = pf + NSB, *ofree = ordy + 1;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + N_BARS);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = ptx::cluster_ctarank();
@@ -189,14 +212,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
       ptx::mbar_init(&qf[i], 1);
       ptx::mbar_init(&qe[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NSB; ++i) {
       ptx::mbar_init(&sf[i], 1);
-      ptx::mbar_init(&pfa[i], 8);  // 4 warps x 2 CTAs (leader's copy)
-      ptx::mbar_init(&pfb[i], 8);
-      ptx::mbar_init(&pvd[i], 1);
+      ptx::mbar_init(&pf[i], 8);  // the 4 warps of the block's WG x 2 CTAs (leader's copy)
     }
     ptx::mbar_init(ordy, 1);
-    ptx::mbar_init(ofree, 16);  // 8 softmax warps x 2 CTAs (leader's copy)
+    ptx::mbar_init(ofree, 16);
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc_pair<TMEM_COLS>(tmem_slot);
@@ -205,17 +226,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    // ================= TMA producer (both CTAs) =================
+  if (warp == 0 || warp == 2) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
+    // ================= TMA producers (both CTAs): warp 0 Q + K, warp 2 V =================
+    // (separate threads, so a K tile is issued as soon as its slot frees, independently of V)
     if (ptx::elect_one()) {
+      const bool kq_role = warp == 0;
       const uint32_t kf0 = ptx::mapa(ptx::smem_u32(kf), 0), vf0 = ptx::mapa(ptx::smem_u32(vf), 0),
                      qf0 = ptx::mapa(ptx::smem_u32(qf), 0);
       uint32_t kq = 0, vq = 0, qi = 0;
+      long long *tr = (kTesting && P.trace && blockIdx.x == 0 && kq_role) ? P.trace : nullptr;
       Iter si;
       it_begin(P, si);
       Item it;
       while (it_next(P, si, it)) {
-        {
+        if (kq_role) {
           const int qb = qi % NQ;
           ptx::mbar_wait(&qe[qb], ((qi / NQ) & 1) ^ 1);
           if (rank == 0) ptx::mbar_arrive_expect_tx(&qf[qb], 2 * QTILE);
@@ -227,39 +252,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
         }
         for (int n = 0; n < it.nblk; ++n) {
           const int t0 = (it.blk_begin + n) * BN;
-          const int ks = kq % NSK;
-          ptx::mbar_wait(&ke[ks], ((kq / NSK) & 1) ^ 1);
-          if (rank == 0) ptx::mbar_arrive_expect_tx(&kf[ks], 2 * KHALF);
-          uint8_t *sK = smem + OFF_K + ks * KHALF;
-          ptx::tma_load_3d_pair(sK, &P.tmK, kf0 + ks * 8, 0, it.j, t0 + 64 * (int)rank);
-          ptx::tma_load_3d_pair(sK + KPANEL, &P.tmK, kf0 + ks * 8, 64, it.j, t0 + 64 * (int)rank);
-          ++kq;
-          const int vs = vq % NSV;
-          ptx::mbar_wait(&ve[vs], ((vq / NSV) & 1) ^ 1);
-          if (rank == 0) ptx::mbar_arrive_expect_tx(&vf[vs], 2 * VHALF);
-          ptx::tma_load_3d_pair(smem + OFF_V + vs * VHALF, &P.tmV, vf0 + vs * 8, 64 * (int)rank, it.j, t0);
-          ++vq;
+          if (kTesting && (P.debug & 4) && (kq_role ? kq : vq) >= (uint32_t)NSK) {  // timing experiment only
+            uint64_t *e = kq_role ? &ke[kq % NSK] : &ve[vq % NSV];
+            ptx::mbar_wait(e, (((kq_role ? kq : vq) / NSK) & 1) ^ 1);
+            if (rank == 0) ptx::mbar_arrive(kq_role ? &kf[kq % NSK] : &vf[vq % NSV]);
+            if (kq_role)
+              ++kq;
+            else
+              ++vq;
+            continue;
+          }
+          if (kq_role) {
+            const int ks = kq % NSK;
+            ptx::mbar_wait(&ke[ks], ((kq / NSK) & 1) ^ 1);
+            trace(tr, 20, kq);
+            if (rank == 0) ptx::mbar_arrive_expect_tx(&kf[ks], 2 * KHALF);
+            uint8_t *sK = smem + OFF_K + ks * KHALF;
+            ptx::tma_load_3d_pair(sK, &P.tmK, kf0 + ks * 8, 0, it.j, t0 + 64 * (int)rank);
+            ptx::tma_load_3d_pair(sK + KPANEL, &P.tmK, kf0 + ks * 8, 64, it.j, t0 + 64 * (int)rank);
+            ++kq;
+          } else {
+            const int vs = vq % NSV;
+            ptx::mbar_wait(&ve[vs], ((vq / NSV) & 1) ^ 1);
+            if (rank == 0) ptx::mbar_arrive_expect_tx(&vf[vs], 2 * VHALF);
+            ptx::tma_load_3d_pair(smem + OFF_V + vs * VHALF, &P.tmV, vf0 + vs * 8, 64 * (int)rank, it.j, t0);
+            ++vq;
+          }
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == kMmaWarp) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
     // ================= MMA issuer (leader CTA, one thread) =================
     if (rank == 0 && ptx::elect_one()) {
       constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(2 * BM, BN, false);  // S = Q K^T, M = 256
       constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(2 * BM, HD, true);  // O += P V, V MN-major
+      long long *tr = (kTesting && P.trace && blockIdx.x == 0) ? P.trace : nullptr;
       Cursor cs, cp;
       cs.init(P);
       cp.init(P);
       uint32_t gs = 0, gp = 0, oi = 0;
-      auto issue_s = [&]() {
+      // S(gs) = Q K(gs)^T into score buffer gs % NSB; `ready` = its Q (first block of an item) and
+      // K tile were already seen landed
+      auto issue_s = [&](bool ready) {
         if (!cs.valid) return;
         const int qb = cs.qi % NQ;
-        if (cs.n == 0) {
-          ptx::mbar_wait(&qf[qb], (cs.qi / NQ) & 1);
-          ptx::tc_fence_after();
+        const int ks = gs % NSK, sb = gs % NSB;
+        if (!ready) {
+          if (cs.n == 0) ptx::mbar_poll(&qf[qb], (cs.qi / NQ) & 1);
+          ptx::mbar_poll(&kf[ks], (gs / NSK) & 1);
         }
-        const int ks = gs % NSK, sb = gs % 2;
-        ptx::mbar_wait(&kf[ks], (gs / NSK) & 1);
+        trace(tr, 21, gs);
         ptx::tc_fence_after();
         const uint32_t qa = ptx::smem_u32(smem + OFF_Q + qb * QTILE), ka = ptx::smem_u32(smem + OFF_K + ks * KHALF);
 #pragma unroll
@@ -269,51 +312,78 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
         ptx::mma2_commit(&sf[sb]);
         ptx::mma2_commit(&ke[ks]);
         if (cs.n == cs.it.nblk - 1) ptx::mma2_commit(&qe[qb]);
+        trace(tr, 14, gs);
         ++gs;
         cs.advance(P);
       };
-      issue_s();
-      issue_s();
+      for (int i = 0; i < NSB; ++i) issue_s(false);
+      // Per block: PV(gp) (both token halves into the one O), then S(gp + NSB) into the score
+      // buffer PV(gp) just read.  A barrier probe costs ~150 cycles of latency
+      // (tools/pair_trace.py), so every barrier this block still needs is probed together each
+      // round (independent SYNCS.PHASECHK in flight at once) instead of one after another.
       while (cp.valid) {
-        const int sb = gp % 2, vs = gp % NSV;
+        const int sb = gp % NSB, vs = gp % NSV;
         const uint32_t acc0 = cp.n > 0 ? 1u : 0u;
-        if (cp.n == 0) {  // O_a / O_b drained by the previous item's epilogue (both CTAs)
-          ptx::mbar_wait_cluster(ofree, (oi & 1) ^ 1);
-          ++oi;
-        }
-        ptx::mbar_wait(&vf[vs], (gp / NSV) & 1);
+        const bool s_next = cs.valid;
+        const int qb = cs.qi % NQ, ks = gs % NSK;
+        const uint32_t qpar = (cs.qi / NQ) & 1, kpar = (gs / NSK) & 1, ppar = (gp / NSB) & 1;
+        bool of = cp.n != 0, v = false, a = false, k = !s_next, q = !(s_next && cs.n == 0);
+        do {
+          if (!of) of = ptx::mbar_test_wait(ofree, (oi & 1) ^ 1);  // previous item's epilogue done with O
+          if (!v) v = ptx::mbar_test_wait(&vf[vs], (gp / NSV) & 1);
+          if (!a) a = ptx::mbar_test_wait(&pf[sb], ppar);
+          if (!k) k = ptx::mbar_test_wait(&kf[ks], kpar);
+          if (!q) q = ptx::mbar_test_wait(&qf[qb], qpar);
+          if (!(of && v && a)) __nanosleep(kPollSleepNs);  // yield issue slots to the softmax warps of this SMSP
+        } while (!(of && v && a));
+        if (cp.n == 0) ++oi;
+        trace(tr, 12, gp);
+        ptx::tc_fence_after();
         const uint32_t va = ptx::smem_u32(smem + OFF_V + vs * VHALF);
-        ptx::mbar_wait_cluster(&pfa[sb], (gp / 2) & 1);
-        ptx::tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          ptx::mma2_ts(tmem + 256, tmem + sb * BN + kk * 8, ptx::smem_desc_sw128(va + kk * 2048, 16, 1024), idesc_pv,
-                       acc0 | (kk > 0));
-        ptx::mbar_wait_cluster(&pfb[sb], (gp / 2) & 1);
-        ptx::tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          ptx::mma2_ts(tmem + 384, tmem + sb * BN + 64 + kk * 8, ptx::smem_desc_sw128(va + (4 + kk) * 2048, 16, 1024),
-                       idesc_pv, acc0 | (kk > 0));
-        ptx::mma2_commit(&ve[vs]);
-        ptx::mma2_commit(&pvd[sb]);
-        if (cp.n == cp.it.nblk - 1) ptx::mma2_commit(ordy);
+        for (int kk = 0; kk < 8; ++kk)  // P(gp): bf16 pairs in the first 64 columns of its score buffer
+          ptx::mma2_ts(tmem + O_COL, tmem + sb * BN + kk * 8,
+                       ptx::smem_desc_sw128(va + kk * 2048, 16, 1024), idesc_pv, acc0 | (kk > 0));
+        trace(tr, 19, gp);
+        if (cp.n == cp.it.nblk - 1) ptx::mma2_commit(ordy);  // the item's last PV: epilogue may read O
         ++gp;
         cp.advance(P);
-        issue_s();  // S(gp + 1): overwrites the score buffer whose P the PV above consumed
+        while (!(k && q)) {
+          if (!k) k = ptx::mbar_test_wait(&kf[ks], kpar);
+          if (!q) q = ptx::mbar_test_wait(&qf[qb], qpar);
+          if (!(k && q)) __nanosleep(kPollSleepNs);
+        }
+        trace(tr, 22, gs);
+        // S(gp - 1 + NSB) right behind the PV (it overwrites the score buffer whose P the PV read),
+        // then the V slot release: one commit covering both, off the path to the next score MMA
+        issue_s(true);
+        ptx::mma2_commit(&ve[vs]);
       }
     }
   } else if (warp >= 4) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 208;" ::: "memory");
     // ================= softmax / epilogue (both CTAs) =================
-    const int x = (warp - 4) / 4;  // 0: tokens 0-63 of each block (O_a), 1: tokens 64-127 (O_b)
+    // Block n of an item goes to WG (n & 1) (warps 4-7 even, 8-11 odd).  The running max is one
+    // chain through the blocks: the WG of block n receives m(n-1) from the other WG (shared
+    // memory + named barrier of the two warps holding the same rows), decides m(n) and passes
+    // it on right after its row max, then spends the rest of the block on exp2 / P while the
+    // other WG already works on block n+1.  P(n) is scaled by m(n); O is one accumulator,
+    // rescaled (rarely: the max is raised only by > 8, log2 units) by the WG whose block
+    // raised m, after PV(n-1) landed.  Each WG keeps its own l relative to the last m it used.
+    const int x = (warp - 4) / 4;
     const int quarter = warp % 4;
     const int r = quarter * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const uint32_t pf0 = ptx::mapa(ptx::smem_u32(x == 0 ? pfa : pfb), 0), of0 = ptx::mapa(ptx::smem_u32(ofree), 0);
-    float *xch = reinterpret_cast<float *>(smem + OFF_X);
+    const uint32_t pf0 = ptx::mapa(ptx::smem_u32(pf), 0), of0 = ptx::mapa(ptx::smem_u32(ofree), 0);
+    float *xch = reinterpret_cast<float *>(smem + OFF_X);  // [2 slots][128 rows]
+    const int bar_out = 1 + quarter + 4 * x, bar_in = 1 + quarter + 4 * (1 - x), bar_epi = 9 + quarter;
+    long long *tr = (kTesting && P.trace && blockIdx.x < 2 && quarter == 0 && lane == 0 && (rank == 0 || x == 0))
+                        ? P.trace : nullptr;
+    const int tb = rank == 0 ? 6 * x : 16 - 1;  // trace row base (peer: rows 16 / 17 via +1 / +2 below)
     const float c2 = P.scale_log2;
     const uint64_t cc = ptx::pack2(c2, c2);
-    uint32_t gs = 0, oi = 0;
+    const uint32_t o_col = tmem + lane_base + O_COL;
+    uint32_t gs0 = 0, oi = 0;  // global index of the item's first block; items done
     Iter si;
     it_begin(P, si);
     Item it;
@@ -322,57 +392,74 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
       const bool live = rr < (int64_t)P.B * P.g;
       const int64_t seq = live ? rr / P.g : 0;
       const int h = it.j * P.g + (int)(rr % P.g);
-      float m2 = -INFINITY, l = 0.f;
-      for (int n = 0; n < it.nblk; ++n, ++gs) {
-        const int sb = gs % 2;
-        ptx::mbar_wait(&sf[sb], (gs / 2) & 1);
+      float m_own = -INFINITY, l = 0.f;
+      for (int n = x; n < it.nblk; n += 2) {
+        const uint32_t gs = gs0 + n;
+        const int sb = gs % NSB;
+        if (rank == 0) trace(tr, tb + 0, gs);
+        ptx::mbar_wait(&sf[sb], (gs / NSB) & 1);
+        trace(tr, tb + 1, gs);
         ptx::tc_fence_after();
-        const uint32_t s_col = tmem + lane_base + sb * BN + 64 * x;
-        const int64_t rem = P.P - (int64_t)(it.blk_begin + n) * BN - 64 * x;  // valid tokens of this half
-        uint32_t sr[2][32];
-        ptx::tmem_ld32(s_col, sr[0]);
-        ptx::tmem_ld32(s_col + 32, sr[1]);
-        ptx::tmem_ld_wait();
-        ptx::reg_fence32(sr[0]);
-        ptx::reg_fence32(sr[1]);
-        if (rem < 64) {
+        if (kTesting && (P.debug & 2)) {  // timing experiment only: the MMA pipeline without the softmax
+          if (n > 0) ptx::named_bar_sync(bar_in, 64);
+          if (n + 1 < it.nblk) ptx::named_bar_arrive(bar_out, 64);
+          ptx::tc_fence_before();
+          ptx::warp_arrive_cluster(pf0 + sb * 8);
+          if (rank == 0) trace(tr, tb + 5, gs);
+          continue;
+        }
+        const uint32_t s_col = tmem + lane_base + sb * BN;
+        const int64_t rem = P.P - (int64_t)(it.blk_begin + n) * BN;  // valid tokens of this block
+        uint32_t sr[4][32];
 #pragma unroll
-          for (int c = 0; c < 2; ++c)
+        for (int c = 0; c < 4; ++c) ptx::tmem_ld32(s_col + 32 * c, sr[c]);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) ptx::reg_fence32(sr[c]);
+        if (rank == 0) trace(tr, tb + 2, gs);
+        if (rem < BN) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
 #pragma unroll
             for (int i = 0; i < 32; ++i)
               if (c * 32 + i >= rem) sr[c][i] = 0xff800000u;
         }
+        // row max of the 128 scores: 8 independent FMNMX3 chains over column pairs
+        auto sv = [&](int j) { return __uint_as_float(sr[j >> 5][j & 31]); };
         float acc[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          acc[k] = ptx::fmax3(__uint_as_float(sr[0][4 * k]), __uint_as_float(sr[0][4 * k + 1]),
-                              __uint_as_float(sr[0][4 * k + 2]));
+        for (int k = 0; k < 8; ++k) acc[k] = sv(k);
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          acc[k] = ptx::fmax3(acc[k], __uint_as_float(sr[0][4 * k + 3]), __uint_as_float(sr[1][4 * k]));
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          acc[k] = ptx::fmax3(acc[k], __uint_as_float(sr[1][4 * k + 1]), __uint_as_float(sr[1][4 * k + 2]));
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] = fmaxf(acc[k], __uint_as_float(sr[1][4 * k + 3]));
-        const float mx = fmaxf(ptx::fmax3(acc[0], acc[1], acc[2]),
-                               fmaxf(ptx::fmax3(acc[3], acc[4], acc[5]), fmaxf(acc[6], acc[7])));
-        const float mnew = mx * c2;
-        // the running max is raised only when a row's max grows by > 8 (log2 units): P <= 256,
-        // and the O correction below is rare; exact because the epilogue divides by l
-        const bool any = __any_sync(0xffffffffu, mnew > m2 + 8.0f);
-        float alpha = 1.f;
-        if (any) {
-          const float mt = fmaxf(m2, mnew);
-          alpha = fast_exp2(m2 - mt);  // 0 while m2 is -inf
-          m2 = mt;
+        for (int j = 8; j < BN; j += 2) acc[(j / 2) % 8] = ptx::fmax3(acc[(j / 2) % 8], sv(j), sv(j + 1));
+        const float mnew = fmaxf(ptx::fmax3(acc[0], acc[1], acc[2]),
+                                 fmaxf(ptx::fmax3(acc[3], acc[4], acc[5]), fmaxf(acc[6], acc[7]))) * c2;
+        // m(n-1) from the other WG (the item's first block starts the chain at -inf)
+        float m_in = -INFINITY;
+        if (n > 0) {
+          ptx::named_bar_sync(bar_in, 64);
+          m_in = xch[(1 - x) * BM + r];
         }
-        // a half whose tokens are all masked so far keeps m2 = -inf: its p = 2^-inf = 0
-        const float mu = m2 == -INFINITY ? 0.f : m2;
+        // raised only when a row's max grows by > 8 (log2 units): P <= 256, rare O correction;
+        // exact because the epilogue divides by l.  Both CTAs' warps of these rows agree.
+        const bool any = __any_sync(0xffffffffu, mnew > m_in + 8.0f);
+        const float m_n = any ? fmaxf(m_in, mnew) : m_in;
+        if (n + 1 < it.nblk) {  // pass m(n) on
+          xch[x * BM + r] = m_n;
+          ptx::named_bar_arrive(bar_out, 64);
+        }
+        // this WG's l follows the last m it used
+        l *= (m_own == m_n) ? 1.f : fast_exp2(m_own - m_n);
+        m_own = m_n;
+        // a row whose tokens are all masked so far keeps m = -inf: its p = 2^-inf = 0
+        const float mu = m_n == -INFINITY ? 0.f : m_n;
         const uint64_t nm = ptx::pack2(-mu, -mu);
+        if (rank == 0 && tr) {
+          asm volatile("" ::"l"(nm));
+          trace(tr, tb + 3, gs);
+        }
         uint64_t sacc[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
+        for (int c = 0; c < 4; ++c) {
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -389,16 +476,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
             sacc[i % 4] = ptx::add2(sacc[i % 4], ptx::pack2(p0, p1));
             pk[i] = ptx::cvt_bf16x2(p0, p1);
           }
-          ptx::tmem_st16(s_col + c * 16, pk);  // P(n) of this half -> its first 32 score columns
+          ptx::tmem_st16(s_col + c * 16, pk);  // P(n) -> the first 64 columns of its score buffer
         }
         float s0, s1, s2, s3;
         ptx::unpack2(ptx::add2(sacc[0], sacc[1]), s0, s1);
         ptx::unpack2(ptx::add2(sacc[2], sacc[3]), s2, s3);
-        l = l * alpha + ((s0 + s1) + (s2 + s3));
-        if (any && n >= 1) {  // rare: rescale O_x once PV(n-1) has landed in it
-          ptx::mbar_wait(&pvd[(gs - 1) % 2], ((gs - 1) / 2) & 1);
+        l += (s0 + s1) + (s2 + s3);
+        if (rank == 0 && tr) {
+          asm volatile("" ::"f"(l));
+          trace(tr, tb + 4, gs);
+        }
+        if (any && n >= 1 && m_in != -INFINITY) {  // rare: O *= 2^(m(n-1) - m(n)) once PV(n-1) landed
+          const float alpha = fast_exp2(m_in - m_n);
+          ptx::mbar_wait(&ve[(gs - 1) % NSV], ((gs - 1) / NSV) & 1);  // PV(n-1) done (its V slot freed)
           ptx::tc_fence_after();
-          const uint32_t o_col = tmem + lane_base + 256 + 128 * x;
 #pragma unroll 1
           for (int c = 0; c < 4; ++c) {
             uint32_t ov[32];
@@ -412,45 +503,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::warp_arrive_cluster(pf0 + sb * 8);
+        trace(tr, tb + (rank == 0 ? 5 : 2), gs);
+        if (kTesting && P.trace && blockIdx.x < 2 && lane == 0)  // every warp's arrival: rows 23-26 / 27-30 (peer)
+          trace(P.trace, 23 + 4 * (int)rank + quarter, gs);
       }
-      // ---- epilogue: merge the two halves' states (Eq. 5 with two parts), O / L, LSE
+      // ---- epilogue: (m, l) of both WGs -> L relative to the final m; O / L (this WG's 64 columns)
       ptx::mbar_wait(ordy, oi & 1);
       ptx::tc_fence_after();
-      float *xb = xch + (oi & 1) * (2 * BM * 2);
-      xb[(x * BM + r) * 2] = m2;
-      xb[(x * BM + r) * 2 + 1] = l;
-      ptx::named_bar_sync(1, 256);
-      const float mo = xb[((1 - x) * BM + r) * 2], lo = xb[((1 - x) * BM + r) * 2 + 1];
-      const float M = fmaxf(m2, mo);
-      const float ws = m2 == -INFINITY ? 0.f : fast_exp2(m2 - M), wo = mo == -INFINITY ? 0.f : fast_exp2(mo - M);
-      const float L = l * ws + lo * wo;
+      float *xe = xch + 2 * BM;  // [WG][128 rows][2]
+      xe[(x * BM + r) * 2] = m_own;
+      xe[(x * BM + r) * 2 + 1] = l;
+      ptx::named_bar_sync(bar_epi, 64);
+      const float mo = xe[((1 - x) * BM + r) * 2], lo = xe[((1 - x) * BM + r) * 2 + 1];
+      const float M = fmaxf(m_own, mo);
+      const float L = (m_own == -INFINITY ? 0.f : l * fast_exp2(m_own - M)) + (mo == -INFINITY ? 0.f : lo * fast_exp2(mo - M));
       const float inv = 1.f / L;
-      const float wa = (x == 0 ? ws : wo) * inv, wb = (x == 0 ? wo : ws) * inv;
       float *orow = P.o + it.slot * P.o_slot_stride + (seq * P.Hq + h) * HD + 64 * x;
       const bool skip = kTesting && P.mutate == 3 && blockIdx.x == 0 && quarter == 0 && lane < 4;
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {
-        uint32_t va[32], vb[32];
-        ptx::tmem_ld32(tmem + lane_base + 256 + 64 * x + 32 * c, va);
-        ptx::tmem_ld32(tmem + lane_base + 384 + 64 * x + 32 * c, vb);
+        uint32_t ov[32];
+        ptx::tmem_ld32(o_col + 64 * x + 32 * c, ov);
         ptx::tmem_ld_wait();
         if (live && !skip) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            float4 v;
-            v.x = __uint_as_float(va[4 * i]) * wa + __uint_as_float(vb[4 * i]) * wb;
-            v.y = __uint_as_float(va[4 * i + 1]) * wa + __uint_as_float(vb[4 * i + 1]) * wb;
-            v.z = __uint_as_float(va[4 * i + 2]) * wa + __uint_as_float(vb[4 * i + 2]) * wb;
-            v.w = __uint_as_float(va[4 * i + 3]) * wa + __uint_as_float(vb[4 * i + 3]) * wb;
-            reinterpret_cast<float4 *>(orow)[c * 8 + i] = v;
-          }
+          for (int i = 0; i < 8; ++i)
+            reinterpret_cast<float4 *>(orow)[c * 8 + i] =
+                make_float4(__uint_as_float(ov[4 * i]) * inv, __uint_as_float(ov[4 * i + 1]) * inv,
+                            __uint_as_float(ov[4 * i + 2]) * inv, __uint_as_float(ov[4 * i + 3]) * inv);
         }
       }
       ptx::tc_fence_before();
       ptx::warp_arrive_cluster(of0);
       if (x == 0 && live) P.lse[it.slot * P.lse_slot_stride + seq * P.Hq + h] = (M + log2f(L)) * HYDRA_LN2;
+      // the exchange slots are reused by the next item's first blocks: both WGs past the reads
+      ptx::named_bar_sync(bar_epi, 64);
+      gs0 += it.nblk;
       ++oi;
     }
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
   }
 
   ptx::tc_fence_before();
@@ -517,9 +609,12 @@ int prefix_pair_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas) {
 }
 
 hydra_status launch_prefix_pair(const PrefixTcArgs &a, int n_ctas, cudaStream_t s) {
-  if (a.tasks || !prefix_pair_supported(a.g) || (a.poly_every != 0 && a.poly_every != 4)) return HYDRA_EINVAL;
-  const void *fn = a.poly_every == 4 ? reinterpret_cast<const void *>(prefix_pair_kernel<4>)
-                                     : reinterpret_cast<const void *>(prefix_pair_kernel<0>);
+  const int poly = a.poly_every;
+  if (a.tasks || !prefix_pair_supported(a.g) || !(poly == 0 || poly == 2 || poly == 3 || poly == 4)) return HYDRA_EINVAL;
+  const void *fn = poly == 4   ? reinterpret_cast<const void *>(prefix_pair_kernel<4>)
+                   : poly == 3 ? reinterpret_cast<const void *>(prefix_pair_kernel<3>)
+                   : poly == 2 ? reinterpret_cast<const void *>(prefix_pair_kernel<2>)
+                               : reinterpret_cast<const void *>(prefix_pair_kernel<0>);
   if (ensure_smem_attr(fn, pr::ALLOC) != cudaSuccess) return HYDRA_ECUDA;
   PrefixPairParams P;
   memset(&P, 0, sizeof(P));
@@ -553,11 +648,15 @@ hydra_status launch_prefix_pair(const PrefixTcArgs &a, int n_ctas, cudaStream_t 
   P.o_slot_stride = a.o_slot_stride;
   P.lse_slot_stride = a.lse_slot_stride;
   P.mutate = kTesting ? a.mutate : 0;
+  P.trace = kTesting ? reinterpret_cast<long long *>(a.trace) : nullptr;
+  P.debug = kTesting ? a.debug_variant : 0;
   if (pl.total <= 0) return HYDRA_OK;
-  if (a.poly_every == 4)
-    prefix_pair_kernel<4><<<pl.ctas, pr::kThreads, pr::ALLOC, s>>>(P);
-  else
-    prefix_pair_kernel<0><<<pl.ctas, pr::kThreads, pr::ALLOC, s>>>(P);
+  switch (poly) {
+    case 4: prefix_pair_kernel<4><<<pl.ctas, pr::kThreads, pr::ALLOC, s>>>(P); break;
+    case 3: prefix_pair_kernel<3><<<pl.ctas, pr::kThreads, pr::ALLOC, s>>>(P); break;
+    case 2: prefix_pair_kernel<2><<<pl.ctas, pr::kThreads, pr::ALLOC, s>>>(P); break;
+    default: prefix_pair_kernel<0><<<pl.ctas, pr::kThreads, pr::ALLOC, s>>>(P); break;
+  }
   return cudaGetLastError() == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
 }
 

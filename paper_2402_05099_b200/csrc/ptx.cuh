@@ -76,6 +76,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   }
 }
 
+// Spin on the non-suspending probe: for a thread whose reaction time is on the critical path
+// (the MMA issuer), where try_wait's suspension measured ~500 cycles between the barrier's
+// completion and the waiter's wake-up (tools/pair_trace.py).
+__device__ __forceinline__ void mbar_poll(uint64_t *bar, uint32_t parity) {
+  while (!mbar_test_wait(bar, parity)) {
+  }
+}
+
 // Named barriers (ids 1..15; 0 is __syncthreads).  `n` counts threads, a multiple of 32.
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -111,6 +119,12 @@ __device__ __forceinline__ void tma_load_4d(void *smem_dst, const void *tmap, ui
       " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(smem_dst)),
       "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
+}
+// Warm L2 with a tile (no smem destination, no completion).
+__device__ __forceinline__ void tma_prefetch_3d(const void *tmap, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(tmap), "r"(c0), "r"(c1),
+               "r"(c2)
+               : "memory");
 }
 // Same with an L2 cache-policy hint (createpolicy value).
 __device__ __forceinline__ void tma_load_3d_hint(void *smem_dst, const void *tmap, uint64_t *bar, int c0, int c1,

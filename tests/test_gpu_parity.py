@@ -27,7 +27,7 @@ def _reset_config():
             "suffix_ctas", "overlap_prefix_ctas")
     for k in keys:
         hydra.set_config(k, 0)
-    defaults = {"prefix_variant": 6, "suffix_cb": 2, "prefix_poly": 4, "fuse_combine": 0}  # the library defaults
+    defaults = {"prefix_variant": 9, "suffix_cb": 2, "prefix_poly": 4, "fuse_combine": 0}  # the library defaults
     for k, v in defaults.items():
         hydra.set_config(k, v)
     yield
@@ -240,6 +240,7 @@ def test_fused_combine_matches_separate_combine(B, Hq, Hkv, P, S, impls, aux):
     one-tile prefix kernels, both suffix kernels, both schedules, ragged and empty suffixes.
     fuse_combine = 2 forces the arrival-counter protocol in the SM-partitioned schedule too."""
     pi, si = impls
+    hydra.set_config("prefix_variant", 6)  # the fused protocol's stream-K piece plan (not the CTA-pair kernel)
     hydra.set_config("prefix_impl", pi)
     hydra.set_config("suffix_impl", si)
     lens = np.random.default_rng(B + P).integers(0, S + 1, B)

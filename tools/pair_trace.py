@@ -1,0 +1,61 @@
+"""Cluster-0 event timeline of the CTA-pair prefix kernel (testing build; diagnostics).
+    HYDRA_TESTING=1 python tools/pair_trace.py [poly] [B Hq Hkv P]
+Per block (median over the steady state): S ready -> registers -> max -> exps -> P arrived for
+both token halves of the leader, the MMA thread's view, and the block period."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2402_05099_b200 as hydra
+
+assert hydra.get_config("testing_build") == 1, "run with HYDRA_TESTING=1"
+dev = torch.device("cuda:0")
+poly = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+B, H, Hkv, P = (int(x) for x in sys.argv[2:6]) if len(sys.argv) > 5 else (1024, 40, 40, 16384)
+N, R = 1024, 32
+tr = torch.zeros(R * N, dtype=torch.int64, device=dev)
+hydra.set_config("prefix_impl", 3)
+hydra.set_config("prefix_poly", poly)
+hydra.set_config("prefix_variant", 9)
+hydra.set_config("tc_debug_variant", int(os.environ.get("TC_DEBUG", 0)))
+g = torch.Generator(device=dev)
+g.manual_seed(0)
+q = torch.randn(B, H, 128, device=dev, generator=g).bfloat16()
+pk = torch.randn(P, Hkv, 128, device=dev, generator=g).bfloat16()
+pv = torch.randn(P, Hkv, 128, device=dev, generator=g).bfloat16()
+ws = torch.empty(hydra.attn_workspace_bytes(q, P, 1, Hkv) * 2, dtype=torch.uint8, device=dev)
+for _ in range(3):
+    hydra.prefix_attn(q, pk, pv, workspace=ws)
+torch.cuda.synchronize()
+hydra.set_config("prefix_trace", tr.data_ptr())
+hydra.prefix_attn(q, pk, pv, workspace=ws)
+torch.cuda.synchronize()
+hydra.set_config("prefix_trace", 0)
+hydra.set_config("tc_debug_variant", 0)
+T = tr.view(R, N).cpu().numpy().astype(np.int64)
+t0 = T[T > 0].min()
+T = np.where(T > 0, T - t0, 0)
+med = lambda a: float(np.median(a)) if len(a) else float("nan")
+# WG a (rows 0-5) takes the even blocks of an item, WG b (rows 6-11) the odd ones
+for x, base in (("a", 0), ("b", 6)):
+    idx = np.nonzero(T[base + 5] > 0)[0]
+    idx = idx[len(idx) // 4: 3 * len(idx) // 4]
+    r = lambda k: T[base + k, idx]
+    print(f"WG {x} ({len(idx)} blocks): waitS {med(r(1) - r(0)):.0f}  ld {med(r(2) - r(1)):.0f}  max+m(n-1) {med(r(3) - r(2)):.0f}  "
+          f"exps {med(r(4) - r(3)):.0f}  st+arrive {med(r(5) - r(4)):.0f}  S->P {med(r(5) - r(1)):.0f}  "
+          f"own-block period {med(np.diff(r(1))):.0f}")
+# per block (any WG): P arrival time = max over the two WGs' rows 5 (one of them is 0)
+Parr = np.maximum(T[5], T[11])
+idx = np.nonzero((Parr > 0) & (T[12] > 0))[0]
+idx = idx[len(idx) // 4: 3 * len(idx) // 4]
+print(f"block period (S ready n -> n+1): {med(np.diff(np.maximum(T[1], T[7])[idx])):.0f}")
+print(f"MMA per block n, relative to P(n) arrival: saw P(+V) {med(T[12, idx] - Parr[idx]):.0f}  PV issued {med(T[19, idx] - Parr[idx]):.0f}"
+      f"  K(n+3) seen {med(T[22, idx + 3] - Parr[idx]):.0f}  S(n+3) issued {med(T[14, idx + 3] - Parr[idx]):.0f}"
+      f"  S(n+3) ready {med(np.maximum(T[1], T[7])[idx + 3] - Parr[idx]):.0f}")
+W = T[23:31, idx]
+print("per-warp P arrival relative to the earliest of the 8 (leader q0-3, peer q0-3):",
+      " ".join(f"{med(W[i] - W.min(axis=0)):.0f}" for i in range(8)), "  MMA saw P - last arrival",
+      f"{med(T[12, idx] - W.max(axis=0)):.0f}")

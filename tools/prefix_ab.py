@@ -10,7 +10,7 @@ import torch
 
 import paper_2402_05099_b200 as hydra
 
-variants = [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "6,9").split(",")]
+variants = (sys.argv[1] if len(sys.argv) > 1 else "6,9").split(",")  # prefix_variant values, or t1 (one-tile kernel)
 SH = {"c3": (1024, 40, 40, 16384), "c4": (512, 32, 8, 32768), "c6": (256, 32, 4, 19947), "c2": (256, 32, 32, 2048)}
 shapes = (sys.argv[2] if len(sys.argv) > 2 else "c3,c4,c6,c2").split(",")
 ctas = int(os.environ.get("CTAS", 0))
@@ -26,8 +26,8 @@ for name in shapes:
     flops = 4.0 * B * Hq * P * 128
     ref = None
     for v in variants:
-        hydra.set_config("prefix_impl", 3)
-        hydra.set_config("prefix_variant", v)
+        hydra.set_config("prefix_impl", 2 if v == "t1" else 3)
+        hydra.set_config("prefix_variant", 9 if v == "t1" else int(v))
         hydra.set_config("prefix_ctas", ctas)
         fn = lambda: hydra.prefix_attn(q, pk, pv, workspace=ws)
         o, lse = fn()
