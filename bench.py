@@ -709,29 +709,50 @@ def run_flat(args, cfg):
     # prefix (on its stream) and the suffix launches of hydra_attn; the same step graph as the
     # timed loop is captured with those event nodes and replayed (synchronised per replay to
     # read the events), so the suffix is timed concurrently with the prefix, as in the step.
+    # In the SM-partitioned schedule both kernels run on one stream (the suffix is a programmatic
+    # dependent launch), so no event can sit between them: the persistent kernels record their
+    # own span instead (config key step_timer: min CTA start / max CTA end, %globaltimer ns).
     ev_keys = ("ev_prefix_begin", "ev_prefix_end", "ev_suffix_begin", "ev_suffix_end")
     evs = [torch.cuda.Event(enable_timing=True) for _ in ev_keys]
     for e in evs:
         e.record()
     torch.cuda.synchronize(dev)
+    timer = torch.zeros(4, dtype=torch.int64, device=dev)
+    use_timer = overlap and k_over > 0
     try:
-        for key, e in zip(ev_keys, evs):
-            hydra.set_config(key, e.cuda_event)
+        if use_timer:
+            hydra.set_config("step_timer", timer.data_ptr())
+        else:
+            for key, e in zip(ev_keys, evs):
+                hydra.set_config(key, e.cuda_event)
         g_ev = capture(lambda: step(overlap))
         for _ in range(3):
             g_ev.replay()
         torch.cuda.synchronize(dev)
         pre_in, suf_in = [], []
         for _ in range(max(10, min(50, args.steps // 4))):
+            if use_timer:
+                timer.copy_(torch.tensor([-1, 0, -1, 0], dtype=torch.int64))  # UINT64_MAX, 0 for atomicMin/Max
             g_ev.replay()
             torch.cuda.synchronize(dev)
-            pre_in.append(evs[0].elapsed_time(evs[1]))
-            suf_in.append(evs[2].elapsed_time(evs[3]))
+            if use_timer:
+                t = [int(v) & 0xFFFFFFFFFFFFFFFF for v in timer.tolist()]
+                pre_in.append((t[1] - t[0]) * 1e-6)
+                suf_in.append((t[3] - t[2]) * 1e-6)
+            else:
+                pre_in.append(evs[0].elapsed_time(evs[1]))
+                suf_in.append(evs[2].elapsed_time(evs[3]))
     finally:
+        hydra.set_config("step_timer", 0)
         for key in ev_keys:
             hydra.set_config(key, 0)
     del g_ev
     ms_pre_in, ms_suf_in = statistics.mean(pre_in), statistics.mean(suf_in)
+    in_step_how = ("inside the step: the kernel's own span (min CTA start to max CTA end, %%globaltimer) in "
+                   "the step graph of the timed loop (the prefix on its SM share runs concurrently), mean of %d "
+                   "replays" % len(suf_in)) if use_timer else (
+                   "inside the step: CUDA events recorded by hydra_attn around the suffix launch, in the step "
+                   "graph of the timed loop, mean of %d replays" % len(suf_in))
 
     # The same step with the suffixes in a paged cache (hydra_attn_paged, R14): the
     # contiguous caches scattered into a shuffled page pool, the same schedule as g_main.
@@ -825,7 +846,7 @@ def run_flat(args, cfg):
                      "launch_ms": round(ms_suf, 5), "peak_source": peak_src + " (STREAM copy)",
                      "frac_of_nominal_7700": round(suf_gbs / 7700.0, 4),
                      "note": "read-only stream vs a read+write copy peak: can read a little above 1.0"},
-        "prefix_phase": {"bound": "tensor", "kernel": "prefix_tc2_kernel (persistent tcgen05, all SMs)",
+        "prefix_phase": {"bound": "tensor", "kernel": prefix_kernel_name(hydra, Hq // Hkv),
                          "achieved": round(pre_burst, 1), "unit": "TFLOP/s", "peak": tc_burst,
                          "frac": round(pre_burst / tc_burst, 4), "launch_ms": round(ms_pre_burst, 5),
                          "timed": "burst: 20 graph replays on a cool GPU, before the step loop",
@@ -876,9 +897,7 @@ def run_flat(args, cfg):
                    "timed": rl.get("timed", "alone on the full chip (CUDA graph, events), after the step loop")}
     rl.update({"achieved": round(suf_in_gbs, 1), "frac": round(suf_in_gbs / hbm, 4), "launch_ms": round(ms_suf_in, 5),
                "frac_of_nominal_7700": round(suf_in_gbs / 7700.0, 4),
-               "timed": "inside the step: CUDA events recorded by hydra_attn around the suffix launch on its "
-                        "stream, in the step graph of the timed loop (concurrent with the prefix), mean of "
-                        "%d replays" % len(suf_in),
+               "timed": in_step_how,
                "prefix_in_step_ms": round(ms_pre_in, 5),
                "prefix_in_step_tflops": round(prefix_flops / (ms_pre_in * 1e-3) / 1e12, 1),
                "share_of_step": round(ms_suf_in / ms, 4)})
@@ -893,6 +912,12 @@ def run_flat(args, cfg):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
+
+
+def prefix_kernel_name(hydra, g):
+    if hydra.get_config("prefix_variant") == 9 and 128 % g == 0:
+        return "prefix_pair_kernel (CTA-pair cta_group::2 tcgen05, persistent, all SMs)"
+    return "prefix_tc2_kernel (persistent tcgen05, all SMs)"
 
 
 def e2e_leg(args, hydra, torch, dev, world, host_t, dev_t, ws, out, B):

@@ -46,6 +46,10 @@ struct Config {
   int64_t prefix_impl = 0, prefix_splits = 0, prefix_ctas = 0, prefix_stages = 3, prefix_poly = 4, prefix_variant = 9;
   int64_t suffix_impl = 0, suffix_splits = 0, suffix_ctas = 0, suffix_unroll = 4, suffix_cb = 2;
   int64_t overlap_prefix_ctas = 0;
+  // measurement: device pointer to 4 x u64 that hydra_attn's persistent prefix / tensor-core suffix
+  // kernels fill with [prefix min CTA start, prefix max CTA end, suffix start, suffix end]
+  // (%globaltimer ns, atomicMin / atomicMax: the caller presets UINT64_MAX, 0, UINT64_MAX, 0)
+  int64_t step_timer = 0;
   // Eq. 5 merged in the kernel epilogues (fused.cuh): 1 in the sequential schedule only (the
   // suffix merges each row after the prefix kernel), 2 also in the SM-partitioned schedule
   // (arrival counters), 0 never: a separate combine launch (default).  Measured
@@ -93,6 +97,7 @@ const Key kKeys[] = {
     {"suffix_impl", &Config::suffix_impl, false},         {"suffix_splits", &Config::suffix_splits, false},
     {"suffix_ctas", &Config::suffix_ctas, false},         {"suffix_unroll", &Config::suffix_unroll, false},
     {"suffix_cb", &Config::suffix_cb, false},             {"overlap_prefix_ctas", &Config::overlap_prefix_ctas, false},
+    {"step_timer", &Config::step_timer, false},
     {"fuse_combine", &Config::fuse_combine, false},
     {"tc_debug_variant", &Config::tc_debug, true},        {"prefix_trace", &Config::prefix_trace, true},
     {"suffix_trace", &Config::suffix_trace, true},        {"inject_combine_bug", &Config::inject_combine_bug, true},
@@ -333,7 +338,8 @@ static int overlap_prefix_ctas(const hydra_heads *h, int64_t B, int64_t P, int64
   // R_P derated from 0.46 (full clock) for the ~1.45-1.7 GHz the 1 kW cap holds the SMs at in a
   // sustained overlapped step: the tensor-bound prefix slows with the clock, the HBM-bound
   // suffix does not (tools/power_profile.py, tools/overlap_sustained.py)
-  const double R_P = 0.38, R_S = 1.0e5, BW = 7.0e6;
+  // (CTA-pair kernel: 0.49 alone at full clock on 144 SMs, 0.43 in the power-capped step at k = 72)
+  const double R_P = pair_mode(g) ? 0.42 : 0.38, R_S = 1.0e5, BW = 7.0e6;
   const int64_t pairs = (B * g + 255) / 256;
   const double pair_blocks = (double)pairs * h->num_kv_heads * ((P + 127) / 128);
   int best_k = 0;
@@ -416,6 +422,7 @@ static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, i
     a.variant = (int32_t)g_cfg.prefix_variant;
     a.mutate = (int32_t)g_cfg.mutate;
     if (fc) a.fc = *fc;
+    a.timer = reinterpret_cast<unsigned long long *>((intptr_t)g_cfg.step_timer);
     hydra_status st;
     if (kind == PK_TC2) {
       // stream-K pieces leave some slots of a row unwritten: mark every slot empty first (the
@@ -459,9 +466,11 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
                                const void *k, const void *v, int64_t s_sb, int64_t s_st, int64_t s_sh,
                                int64_t S_cap, const int32_t *lens, int splits, const PartsView &dst,
                                cudaStream_t s, int tc_ctas = 0, const hydra_paging *pg = nullptr,
-                               const FusedCombine *fc = nullptr) {
+                               const FusedCombine *fc = nullptr, bool pdl = false) {
   const int g = h->num_q_heads / h->num_kv_heads;
-  if (kTesting && launch_lens_check(lens, B, S_cap, s) != HYDRA_OK) return cuda_fail("lens check");
+  // (the testing build's lens check is a kernel of its own: it would sit between the prefix
+  // and a programmatic-dependent suffix, so it is skipped there)
+  if (kTesting && !pdl && launch_lens_check(lens, B, S_cap, s) != HYDRA_OK) return cuda_fail("lens check");
   if (use_suffix_tc(h, B, S_cap, tc_ctas > 0)) {
     SuffixTcArgs a{};
     a.q = q;
@@ -485,6 +494,8 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
     a.debug = (int32_t)g_cfg.tc_debug;
     a.mutate = (int32_t)g_cfg.mutate;
     if (fc) a.fc = *fc;
+    a.pdl = pdl ? 1 : 0;
+    if (g_cfg.step_timer) a.timer = reinterpret_cast<unsigned long long *>((intptr_t)g_cfg.step_timer) + 2;
     a.n_split = splits;
     a.split_len = (int32_t)(((S_cap + splits - 1) / splits + 127) / 128 * 128);
     a.o_split_stride = dst.o_stride;
@@ -798,12 +809,17 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
       (S_cap > 0 && (!aligned16(sk, es, {s_sb, s_st, s_sh}) || !aligned16(sv, es, {}))))
     return fail(HYDRA_EINVAL, "q/k/v base pointers and strides must be 16-byte aligned");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  cudaStream_t sa = s_aux ? reinterpret_cast<cudaStream_t>(s_aux) : s;
-  // With a second stream and both persistent tensor-core kernels, run them concurrently
-  // on disjoint SM sets (k prefix CTAs + (SMs - k) suffix CTAs, one CTA per SM each).
-  // Without an SM split (k = 0) two full grids would only contend: run sequentially.
-  const int k_over = (sa != s) ? overlap_prefix_ctas(h, B, P, S_cap) : 0;
-  if (k_over == 0) sa = s;
+  // With a second stream given (the caller allows concurrency) and both persistent tensor-core
+  // kernels, run them concurrently on disjoint SM sets: k prefix CTAs + (SMs - k) suffix CTAs,
+  // one CTA per SM each.  Both go on `stream`: the suffix is a programmatic dependent launch
+  // that starts once every prefix CTA (CTA pairs of a cluster need both SMs of a TPC) is
+  // resident, so the prefix always gets its SM share first; the suffix grid completes only
+  // after the prefix grid (griddepcontrol.wait), so everything after it in the stream sees
+  // both.  (Two streams let the suffix grab SMs first and split TPCs: measured 0.96-1.35 ms
+  // depending on k at C3@16K, tools/overlap_sustained.py.)  Without an SM split (k = 0) two
+  // full grids would only contend: run sequentially.
+  const int k_over = s_aux ? overlap_prefix_ctas(h, B, P, S_cap) : 0;
+  cudaStream_t sa = s;
   g_cfg.last_overlap_k = k_over;
   const int sms = device_sm_count();
   const int g = h->num_q_heads / h->num_kv_heads;
@@ -837,7 +853,7 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
     fc.out_f32 = out_dtype == HYDRA_F32;
     fc.lse_out = lse_out;
     fc.inject_bug = inject_combine_bug() ? 1 : 0;
-    fc.pre_done = sa == s ? 1 : 0;  // one stream: the suffix launch follows the prefix kernel
+    fc.pre_done = k_over == 0 ? 1 : 0;  // sequential: the suffix launch follows the prefix kernel
     if (prefix_kind(h, B * g, P, k_over) == PK_TC2)
       prefix_tc2_plan_into(fc, B, g, h->num_kv_heads, P, k_over > 0 ? k_over : prefix_ctas(), prefix_bn());
     else
@@ -846,14 +862,11 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
       return cuda_fail("counter reset");
   }
 
-  if (sa != s) {
-    if (cudaEventRecord(events().fork, s) != cudaSuccess || cudaStreamWaitEvent(sa, events().fork, 0) != cudaSuccess)
-      return cuda_fail("fork");
-  }
   if (P > 0) {
+    // (no event between the prefix and a programmatic-dependent suffix: it would serialise them)
     record_step_ev(0, sa);
     st = run_prefix(h, B, q, q_sb, q_sh, P, pk, pv, kv_st, kv_sh, np, pre, sa, k_over, fused ? &fc : nullptr);
-    record_step_ev(1, sa);
+    if (k_over == 0) record_step_ev(1, sa);
   } else {
     st = launch_fill_neg_inf(pre.lse, rows, sa);
     if (st) st = cuda_fail("fill");
@@ -863,19 +876,15 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
     // the suffix takes every SM the prefix plan leaves free (the plan may round k down)
     const int k_eff = k_over > 0 ? prefix_tc2_ctas(B, g, h->num_kv_heads, P, k_over, prefix_bn(), pair_mode(g))
                                  : 0;
-    record_step_ev(2, s);
+    if (k_over == 0) record_step_ev(2, s);
     st = run_suffix(h, B, q, q_sb, q_sh, sk, sv, s_sb, s_st, s_sh, S_cap, lens, ns, suf, s,
-                    k_over > 0 ? std::max(1, sms - k_eff) : 0, pg, fused ? &fc : nullptr);
+                    k_over > 0 ? std::max(1, sms - k_eff) : 0, pg, fused ? &fc : nullptr, k_over > 0 && P > 0);
     record_step_ev(3, s);
   } else {
     st = launch_fill_neg_inf(suf.lse, rows, s);
     if (st) st = cuda_fail("fill");
   }
   if (st) return st;
-  if (sa != s) {
-    if (cudaEventRecord(events().join, sa) != cudaSuccess || cudaStreamWaitEvent(s, events().join, 0) != cudaSuccess)
-      return cuda_fail("join");
-  }
   if (fused) return HYDRA_OK;  // merged in the epilogues
   return run_combine(rows, h->head_dim, np + ns, all, out, out_dtype, lse_out, s);
 }

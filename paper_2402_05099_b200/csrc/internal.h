@@ -147,6 +147,7 @@ struct PrefixTcArgs {
   int32_t poly_every = 0;  // v3: every k-th exp2 column pair on the FMA pipe (0 = all MUFU)
   int32_t variant = 3;     // persistent kernel: 3 (128-token blocks) or 4 (64-token, double-buffered S)
   int32_t stages;  // K/V pipeline stages: 2 (160 KB smem, leaves room for co-resident suffix CTAs) or 3
+  unsigned long long *timer = nullptr;  // measurement: [0] min CTA start, [1] max CTA end (ns); persistent kernels
 };
 bool prefix_tc_supported(const hydra_heads *h);
 hydra_status launch_prefix_tc(const PrefixTcArgs &a, cudaStream_t s);
@@ -193,6 +194,8 @@ struct SuffixTcArgs {
   int32_t n_split, split_len;
   int64_t o_split_stride, lse_split_stride;
   FusedCombine fc;  // fc.cnt != null: fused Eq. 5 merge in the epilogue
+  int32_t pdl = 0;  // 1: programmatic dependent of the previous kernel in the stream (SM-partitioned schedule)
+  unsigned long long *timer = nullptr;  // measurement: [0] min CTA start, [1] max CTA end (ns)
 };
 bool suffix_tc_supported(const hydra_heads *h);
 hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s);

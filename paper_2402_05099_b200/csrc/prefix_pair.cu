@@ -64,6 +64,12 @@ constexpr int OFF_Q = 0;
 constexpr int OFF_K = OFF_Q + NQ * QTILE;
 constexpr int OFF_V = OFF_K + NSK * KHALF;
 constexpr int NSB = 3;                      // score buffers in TMEM
+// Lazy running max: raised only when a row's block max exceeds it by more than kRaise (log2
+// units), so P <= 2^32 (bf16 and the fp32 O / l accumulators have the range: over a piece of
+// <= 2^20 tokens they stay finite for |v| < 2^70), and a needle-like score jump (the 'mixed' inputs:
+// ~12-17 log2 units above the rest) needs no O correction at all.  8 (prefix_tc2) made a
+// quarter of the blocks at C3 wait for the previous PV before publishing P.
+constexpr float kRaise = 32.0f;
 #ifndef HYDRA_PAIR_POLL_NS
 #define HYDRA_PAIR_POLL_NS 64
 #endif
@@ -107,6 +113,7 @@ struct __align__(64) PrefixPairParams {
   int64_t o_slot_stride, lse_slot_stride;
   int32_t mutate;  // testing build only: 3 = worker 0 skips one 4-row group of its stores
   long long *trace;  // testing build only: cluster-0 event timestamps [kTraceRows][kTraceN] (tools/pair_trace.py)
+  unsigned long long *timer;  // measurement: [0] min CTA start, [1] max CTA end (%globaltimer ns); null = off
   int32_t debug;     // testing build only, timing experiments (invalid results): 4 = no K/V TMA after the ring
                      // fill, 2 = no softmax (P published as soon as S lands)
 };
@@ -188,6 +195,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
     prefix_pair_kernel(const __grid_constant__ PrefixPairParams P) {
   using namespace pr;
   extern __shared__ uint8_t smem_raw[];
+  // SM-partitioned schedule on one stream: the suffix kernel (a programmatic dependent) may start
+  // as soon as every CTA of this persistent grid is resident -- it then takes the other SMs
+  asm volatile("griddepcontrol.launch_dependents;");
+  if (P.timer && threadIdx.x == 0) atomicMin(P.timer, gtimer());
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
   uint64_t *kf = bars, *ke = kf + NSK, *vf = ke + NSK, *ve = vf + NSV, *qf = ve + NSV, *qe = qf + NQ;
@@ -368,7 +379,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
     // memory + named barrier of the two warps holding the same rows), decides m(n) and passes
     // it on right after its row max, then spends the rest of the block on exp2 / P while the
     // other WG already works on block n+1.  P(n) is scaled by m(n); O is one accumulator,
-    // rescaled (rarely: the max is raised only by > 8, log2 units) by the WG whose block
+    // rescaled (rarely: the max is raised only by > kRaise, log2 units) by the WG whose block
     // raised m, after PV(n-1) landed.  Each WG keeps its own l relative to the last m it used.
     const int x = (warp - 4) / 4;
     const int quarter = warp % 4;
@@ -439,9 +450,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
           ptx::named_bar_sync(bar_in, 64);
           m_in = xch[(1 - x) * BM + r];
         }
-        // raised only when a row's max grows by > 8 (log2 units): P <= 256, rare O correction;
-        // exact because the epilogue divides by l.  Both CTAs' warps of these rows agree.
-        const bool any = __any_sync(0xffffffffu, mnew > m_in + 8.0f);
+        // raised only when a row's max grows by > kRaise (log2 units): P <= 2^kRaise, so the O
+        // correction (which waits for PV(n-1)) is rare; exact because the epilogue divides by l.
+        // The partner warps see the same m(n-1) and row max, so they take the same decision.
+        const bool any = __any_sync(0xffffffffu, mnew > m_in + kRaise);
         const float m_n = any ? fmaxf(m_in, mnew) : m_in;
         if (n + 1 < it.nblk) {  // pass m(n) on
           xch[x * BM + r] = m_n;
@@ -551,6 +563,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
     ptx::tc_fence_after();
     ptx::tmem_dealloc_pair<TMEM_COLS>(tmem);
   }
+  if (P.timer && threadIdx.x == 0) atomicMax(P.timer + 1, gtimer());
 }
 
 // ------------------------------------------------------------------ host side
@@ -650,6 +663,7 @@ hydra_status launch_prefix_pair(const PrefixTcArgs &a, int n_ctas, cudaStream_t 
   P.mutate = kTesting ? a.mutate : 0;
   P.trace = kTesting ? reinterpret_cast<long long *>(a.trace) : nullptr;
   P.debug = kTesting ? a.debug_variant : 0;
+  P.timer = a.timer;
   if (pl.total <= 0) return HYDRA_OK;
   switch (poly) {
     case 4: prefix_pair_kernel<4><<<pl.ctas, pr::kThreads, pr::ALLOC, s>>>(P); break;

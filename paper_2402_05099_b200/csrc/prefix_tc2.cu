@@ -39,11 +39,6 @@
 
 namespace hydra {
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 
 namespace tc2 {
 constexpr int BM = 128;  // rows per query tile (UMMA M)
@@ -88,6 +83,7 @@ struct __align__(64) PrefixTc2Params {
   long long *trace;      // diagnostics: CTA 0 event timestamps (clock64), see tools/prefix_trace.py; null = off
   int32_t mutate;        // testing build only: 1 = CTA 0 skips one 4-row store group of its epilogues
   FusedCombine fc;       // fc.cnt != null: the Eq. 5 merge of every completed row in this epilogue (fused.cuh)
+  unsigned long long *timer;  // measurement: [0] min CTA start, [1] max CTA end (%globaltimer ns); null = off
   float *o, *lse;
   int64_t o_slot_stride, lse_slot_stride;
 };
@@ -207,6 +203,9 @@ template <int kPolyEvery, bool kSpec, bool kSplit = false>
 __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __grid_constant__ PrefixTc2Params P) {
   using namespace tc2;
   extern __shared__ uint8_t smem_raw[];
+  // SM-partitioned schedule on one stream: the suffix kernel (a programmatic dependent) may start
+  // as soon as every CTA of this persistent grid is resident -- it then takes the other SMs
+  asm volatile("griddepcontrol.launch_dependents;");
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
   uint64_t *k_full = bars, *k_empty = bars + NS, *v_full = bars + 2 * NS, *v_empty = bars + 3 * NS;
@@ -217,6 +216,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
   // diagnostics: every CTA's globaltimer at entry / setup done / first S / last P / exit
   long long *cta_tr = (kTesting && P.trace && blockIdx.x < 256) ? P.trace + 14 * kTraceN + blockIdx.x * 8 : nullptr;
   if (cta_tr && threadIdx.x == 0) cta_tr[0] = (long long)gtimer();
+  if (P.timer && threadIdx.x == 0) atomicMin(P.timer, gtimer());
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&P.tmK);
@@ -646,6 +646,7 @@ __global__ void __launch_bounds__(tc2::kThreads, 1) prefix_tc2_kernel(const __gr
     ptx::tmem_dealloc<TMEM_COLS>(tmem);
   }
   if (cta_tr && threadIdx.x == 0) cta_tr[4] = (long long)gtimer();
+  if (P.timer && threadIdx.x == 0) atomicMax(P.timer + 1, gtimer());
 }
 
 // ===================================================================================
@@ -1109,6 +1110,7 @@ hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s
   P.o_slot_stride = a.o_slot_stride;
   P.lse_slot_stride = a.lse_slot_stride;
   P.fc = a.fc;
+  P.timer = a.timer;
   if (P.fc.cnt) {  // fused Eq. 5: flat mode, variants 3 / 5 / 6; the plan must be this launch's
     if (a.tasks || v4 || P.fc.sk_total != pl.total || P.fc.sk_G != pl.ctas / pl.group || P.fc.sk_group != pl.group)
       return HYDRA_EINVAL;

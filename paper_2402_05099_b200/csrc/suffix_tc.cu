@@ -107,6 +107,8 @@ struct __align__(64) SuffixTcParams {
   int32_t n_split, split_len;
   int64_t o_split_stride, lse_split_stride;
   FusedCombine fc;  // fc.cnt != null: the epilogue warps count each row's part and merge completed rows
+  int32_t pdl;      // host only: launch as a programmatic dependent of the previous kernel in the stream
+  unsigned long long *timer;  // measurement: [0] min CTA start, [1] max CTA end (%globaltimer ns); null = off
 };
 namespace stc {
 constexpr int kTraceN = 1024;
@@ -252,6 +254,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
   constexpr uint32_t TMEM_COLS = tmem_cols(CB);
   constexpr uint32_t O_COL = NSP * CB * NQ;  // O^T buffers start after the S^T round slots
   extern __shared__ uint8_t smem_raw[];
+  if (P.timer && threadIdx.x == 0) atomicMin(P.timer, gtimer());
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
   uint64_t *k_full = bars, *k_empty = bars + NS, *v_full = bars + 2 * NS, *v_empty = bars + 3 * NS;
@@ -703,6 +706,11 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
     ptx::tc_fence_after();
     ptx::tmem_dealloc<TMEM_COLS>(tmem);
   }
+  if (P.timer && threadIdx.x == 0) atomicMax(P.timer + 1, gtimer());
+  // Launched as a programmatic dependent of the prefix kernel (SM-partitioned schedule on one
+  // stream): the grid completes only after the prefix grid has, so the combine that follows in
+  // the stream sees both.  Without a programmatic prerequisite this returns at once.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ------------------------------------------------------------------ host side
@@ -717,8 +725,23 @@ static cudaError_t launch_gcsp(const SuffixTcParams &P, int grid, cudaStream_t s
   constexpr int alloc = stc::alloc_bytes(CB);
   const cudaError_t attr = ensure_smem_attr(reinterpret_cast<const void *>(suffix_tc_kernel<G, CB, SPLIT, PAGED>), alloc);
   if (attr != cudaSuccess) return attr;
-  suffix_tc_kernel<G, CB, SPLIT, PAGED><<<grid, stc::kThreads, alloc, s>>>(P);
-  return cudaGetLastError();
+  if (!P.pdl) {
+    suffix_tc_kernel<G, CB, SPLIT, PAGED><<<grid, stc::kThreads, alloc, s>>>(P);
+    return cudaGetLastError();
+  }
+  // programmatic dependent launch: starts once every CTA of the preceding kernel in the stream
+  // (the persistent prefix on its SM share) is resident, and fills the remaining SMs
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(stc::kThreads, 1, 1);
+  cfg.dynamicSmemBytes = alloc;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, suffix_tc_kernel<G, CB, SPLIT, PAGED>, P);
 }
 // PAGED (compile time): the contiguous kernel carries no paging branch in its producers
 template <int G, int CB, bool SPLIT>
@@ -775,6 +798,8 @@ hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s)
   P.mutate = kTesting ? a.mutate : 0;
   P.S_cap = (int32_t)std::min<int64_t>(a.S_cap, INT32_MAX);
   P.fc = a.fc;
+  P.pdl = a.pdl;
+  P.timer = a.timer;
   if (P.fc.cnt && P.fc.n_suf != P.n_split) return HYDRA_EINVAL;
   P.block_table = a.block_table;
   P.bt_stride = a.bt_stride;

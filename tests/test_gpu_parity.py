@@ -101,15 +101,18 @@ def test_prefix_tc_splits(splits):
     assert_parity(o, ref, lse, lref, what=f"prefix splits={splits}")
 
 
-@pytest.mark.parametrize("variant,poly", [(3, 0), (5, 0), (5, 4), (5, 8), (3, 4), (6, 0), (6, 4), (9, 0), (9, 4)])
-def test_prefix_tc2_growing_max(variant, poly):
+@pytest.mark.parametrize("variant,poly,steep", [(3, 0, 6), (5, 0, 6), (5, 4, 6), (5, 8, 6), (3, 4, 6), (6, 0, 6),
+                                                (6, 4, 6), (9, 0, 6), (9, 4, 6), (9, 4, 60), (9, 2, 60)])
+def test_prefix_tc2_growing_max(variant, poly, steep):
     """Scores that grow along the prefix: the running max is raised block after block, which
-    exercises the O/l correction and, for the speculative softmax, the redo path."""
+    exercises the O/l correction and, for the speculative softmax, the redo path.  The CTA-pair
+    kernel raises its max only past +32 (log2 units): the steep ramp (K scaled up to 61x) makes
+    it raise several times per row, in both softmax warpgroups."""
     hydra.set_config("prefix_impl", 3)
     hydra.set_config("prefix_variant", variant)
     hydra.set_config("prefix_poly", poly)
     pb = synth.make_problem(300, 8, 2, 128, 2000, 1, dtype="bf16", dist="mixed", seed=11)
-    ramp = (1.0 + 6.0 * np.arange(pb.P, dtype=np.float64) / pb.P)[:, None, None]
+    ramp = (1.0 + steep * np.arange(pb.P, dtype=np.float64) / pb.P)[:, None, None]
     pb.pk = synth.gen.f32_to_bf16_bits((pb.f32("pk") * ramp).astype(np.float32))
     t = problem_to(pb, DEV)
     try:
@@ -118,7 +121,7 @@ def test_prefix_tc2_growing_max(variant, poly):
     finally:
         hydra.set_config("prefix_poly", 4)
     ref, lref = oracle.prefix_only(pb)
-    assert_parity(o, ref, lse, lref, what=f"prefix growing max v{variant} poly{poly}")
+    assert_parity(o, ref, lse, lref, what=f"prefix growing max v{variant} poly{poly} x{steep}")
 
 
 @pytest.mark.parametrize("ctas", [1, 3, 7, 64, 148, 100000])
