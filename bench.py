@@ -77,6 +77,8 @@ NCU_TRAFFIC = {
     ("c3_16k", "decode_attn_kernel"): 5379746000 + 6668800,    # profiles/r1o_suffix_decode_raw.csv
     ("c3_16k", "suffix_tc_kernel"): 5379274000 + 25441024,     # profiles/r1o_suffix_tc_76_raw.csv (76 CTAs, k = 72)
     ("c3_16k", "prefix_tc2_kernel"): 355092736 + 21645312,     # profiles/r1o_prefix_tc2_raw.csv (variant 6, poly 4)
+    ("c3_16k", "prefix_pair_kernel"): 350497280 + 21158144,    # profiles/r2_pair_c3_raw.csv (variant 9, poly 4)
+    ("c3_16k", "suffix_tc_kernel@84"): 5379332000 + 26637568,  # profiles/r2_suffix_tc_84_raw.csv (84 CTAs, k = 64)
 }
 
 
@@ -856,7 +858,7 @@ def run_flat(args, cfg):
                                        "timed": "back-to-back replays for ~1 s vs the sustained cuBLAS loop"},
                          "after_step_loop": {"achieved": round(pre_tflops, 1), "launch_ms": round(ms_pre, 5)},
                          "frac_of_spec_2250": round(pre_burst / 2250.0, 4), "flops_per_launch": prefix_flops,
-                         "traffic": NCU_TRAFFIC.get((args.config, "prefix_tc2_kernel")),
+                         "traffic": NCU_TRAFFIC.get((args.config, prefix_kernel_name(hydra, Hq // Hkv).split()[0])),
                          "algorithmic_bytes_per_launch": prefix_bytes},
         "step_roofline": {"t_roof_ms": round(t_roof * 1e3, 5), "frac": round(t_roof * 1e3 / ms, 4),
                           "ms_sequential": round(ms_seq, 5), "ms_overlap": round(ms_over, 5)},
@@ -883,7 +885,9 @@ def run_flat(args, cfg):
             "bound": "hbm", "kernel": "suffix_tc_kernel on %d SMs (prefix on %d SMs), the overlapped step's dominant kernel"
             % (sms - k_over, k_over),
             "achieved": round(b_k, 1), "peak": hbm, "unit": "GB/s", "frac": round(b_k / hbm, 4),
-            "traffic": NCU_TRAFFIC.get((args.config, "suffix_tc_kernel")), "algorithmic_bytes_per_launch": suffix_bytes,
+            "traffic": NCU_TRAFFIC.get((args.config, "suffix_tc_kernel@%d" % (sms - k_over)),
+                                       NCU_TRAFFIC.get((args.config, "suffix_tc_kernel"))),
+            "algorithmic_bytes_per_launch": suffix_bytes,
             "launch_ms": in_step["ms_suffix"], "peak_source": peak_src + " (STREAM copy)",
             "frac_of_nominal_7700": round(b_k / 7700.0, 4),
             "timed": "alone on its SM share (CUDA graph, events), after the step loop",

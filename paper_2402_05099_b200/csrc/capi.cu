@@ -266,8 +266,13 @@ static PrefixKind prefix_kind(const hydra_heads *h, int64_t rows = -1, int64_t P
   // pipeline fill: 24 on an SM share (the overlap split needs the persistent kernel), 40 on
   // the full chip (tools/prefix_shapes.py: C6 at 34 blocks per CTA, one-tile kernel 104 us vs
   // 108 us; C4 at 110 blocks, persistent 266 vs 312 us).
+  // The CTA-pair kernel (one worker = 2 CTAs) keeps its pipeline full at fewer blocks: from 16
+  // per worker (tools/prefix_ab.py: C6, 67 per worker, 0.084 ms vs 0.097 one-tile; C2, 7 per
+  // worker, 0.031 vs 0.024 one-tile).
   const int64_t blocks = ((rows + 255) / 256) * h->num_kv_heads * ((P + 127) / 128);
-  return blocks >= (ctas > 0 ? 24 : 40) * (int64_t)(ctas > 0 ? ctas : prefix_ctas()) ? PK_TC2 : PK_TC1;
+  const int64_t n = ctas > 0 ? ctas : prefix_ctas();
+  if (pair_mode((int)(h->num_q_heads / h->num_kv_heads))) return blocks >= 8 * n ? PK_TC2 : PK_TC1;
+  return blocks >= (ctas > 0 ? 24 : 40) * n ? PK_TC2 : PK_TC1;
 }
 static bool use_tc(const hydra_heads *h) { return prefix_kind(h) != PK_SIMT; }
 
