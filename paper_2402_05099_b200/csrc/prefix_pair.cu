@@ -77,7 +77,8 @@ constexpr int kPollSleepNs = HYDRA_PAIR_POLL_NS;
 #ifndef HYDRA_PAIR_MMA_WARP
 #define HYDRA_PAIR_MMA_WARP 1
 #endif
-constexpr int kMmaWarp = HYDRA_PAIR_MMA_WARP;  // 1 or 3 (warp 1 allocates TMEM either way)  // MMA thread's back-off between barrier probe rounds
+constexpr int kMmaWarp = HYDRA_PAIR_MMA_WARP;  // 1 or 3 (warp 1 allocates TMEM either way)
+  // MMA thread's back-off between barrier probe rounds
 constexpr int O_COL = NSB * BN;             // O accumulator: TMEM columns [384, 512)
 constexpr int OFF_X = OFF_V + NSV * VHALF;  // row max / sum exchange [parity][WG][128 rows]
 constexpr int OFF_BAR = OFF_X + 6 * BM * 4;  // m exchange [WG][128] + epilogue (m, l) [WG][128][2]
@@ -470,6 +471,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
           trace(tr, tb + 3, gs);
         }
         uint64_t sacc[4] = {0, 0, 0, 0};
+        // exp2(s*c2 - m) -> bf16 P in the first 64 columns of the score buffer, row sums
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t pk[16];
@@ -488,7 +490,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
             sacc[i % 4] = ptx::add2(sacc[i % 4], ptx::pack2(p0, p1));
             pk[i] = ptx::cvt_bf16x2(p0, p1);
           }
-          ptx::tmem_st16(s_col + c * 16, pk);  // P(n) -> the first 64 columns of its score buffer
+          ptx::tmem_st16(s_col + c * 16, pk);
         }
         float s0, s1, s2, s3;
         ptx::unpack2(ptx::add2(sacc[0], sacc[1]), s0, s1);
