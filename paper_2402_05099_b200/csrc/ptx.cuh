@@ -126,6 +126,11 @@ __device__ __forceinline__ void tma_prefetch_3d(const void *tmap, int c0, int c1
                "r"(c2)
                : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_4d(const void *tmap, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(tmap), "r"(c0),
+               "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
 // Same with an L2 cache-policy hint (createpolicy value).
 __device__ __forceinline__ void tma_load_3d_hint(void *smem_dst, const void *tmap, uint64_t *bar, int c0, int c1,
                                                  int c2, uint64_t policy) {

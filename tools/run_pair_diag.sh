@@ -1,2 +1,1 @@
-for v in l0 l1; do echo "== $v" >> gpurun_out/pair_trace.log; HYDRA_LIB_PATH=paper_2402_05099_b200/libhydra_var_$v.so timeout 120 python tools/pair_trace.py 4 >> gpurun_out/pair_trace.log 2>&1; HYDRA_LIB_PATH=paper_2402_05099_b200/libhydra_var_$v.so timeout 100 python tools/prefix_ab.py 9 >> gpurun_out/pair_trace.log 2>&1; done
-timeout 100 python tools/prefix_ab.py 9 >> gpurun_out/pair_trace.log 2>&1
+for v in p0 p2 p4; do echo "== $v" >> gpurun_out/suf_ab.log; HYDRA_LIB_PATH=paper_2402_05099_b200/libhydra_var_$v.so timeout 100 python tools/suffix_shapes_ab.py >> gpurun_out/suf_ab.log 2>&1; done
