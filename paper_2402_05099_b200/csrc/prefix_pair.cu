@@ -200,6 +200,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
   // as soon as every CTA of this persistent grid is resident -- it then takes the other SMs
   asm volatile("griddepcontrol.launch_dependents;");
   if (P.timer && threadIdx.x == 0) atomicMin(P.timer, gtimer());
+  // diagnostics (testing build): every CTA's %globaltimer at entry / setup done / exit, rows 32..
+  long long *cta_tr = (kTesting && P.trace && blockIdx.x < 1024) ? P.trace + 32 * kTraceN + blockIdx.x * 4 : nullptr;
+  if (cta_tr && threadIdx.x == 0) cta_tr[0] = (long long)gtimer();
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
   uint64_t *kf = bars, *ke = kf + NSK, *vf = ke + NSK, *ve = vf + NSV, *qf = ve + NSV, *qe = qf + NQ;
@@ -237,6 +240,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
   ptx::cluster_sync();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (cta_tr && threadIdx.x == 0) cta_tr[1] = (long long)gtimer();
 
   if (warp == 0 || warp == 2) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
@@ -555,6 +559,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
       gs0 += it.nblk;
       ++oi;
     }
+    if (cta_tr && warp == 4 && lane == 0) cta_tr[2] = (long long)gtimer();  // this CTA's softmax / epilogues done
   } else {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
   }
@@ -566,6 +571,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
     ptx::tmem_dealloc_pair<TMEM_COLS>(tmem);
   }
   if (P.timer && threadIdx.x == 0) atomicMax(P.timer + 1, gtimer());
+  if (cta_tr && threadIdx.x == 0) cta_tr[3] = (long long)gtimer();
 }
 
 // ------------------------------------------------------------------ host side

@@ -7,16 +7,17 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2402_05099_b200 as hydra
 ks = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "56,60,64,68,72,76,80").split(",")]
-B, H, P, S = 1024, 40, int(os.environ.get("P", 16384)), 256
+B, H, P, S = int(os.environ.get("B", 1024)), int(os.environ.get("H", 40)), int(os.environ.get("P", 16384)), int(os.environ.get("S", 256))
+HKV = int(os.environ.get("HKV", H))
 dev = torch.device("cuda:0")
 g = torch.Generator(device=dev); g.manual_seed(0)
 q = torch.randn(B, H, 128, device=dev, generator=g).bfloat16()
-pk = torch.randn(P, H, 128, device=dev, generator=g).bfloat16()
-pv = torch.randn(P, H, 128, device=dev, generator=g).bfloat16()
-sk = torch.randn(B, S, H, 128, device=dev, generator=g).bfloat16()
-sv = torch.randn(B, S, H, 128, device=dev, generator=g).bfloat16()
+pk = torch.randn(P, HKV, 128, device=dev, generator=g).bfloat16()
+pv = torch.randn(P, HKV, 128, device=dev, generator=g).bfloat16()
+sk = torch.randn(B, S, HKV, 128, device=dev, generator=g).bfloat16()
+sv = torch.randn(B, S, HKV, 128, device=dev, generator=g).bfloat16()
 lens = torch.full((B,), S, dtype=torch.int32, device=dev)
-ws = torch.empty(hydra.attn_workspace_bytes(q, P, S, H) * 2, dtype=torch.uint8, device=dev)
+ws = torch.empty(hydra.attn_workspace_bytes(q, P, S, HKV) * 4, dtype=torch.uint8, device=dev)
 out = torch.empty(B, H, 128, dtype=torch.bfloat16, device=dev)
 aux = torch.cuda.Stream(priority=-1)
 def graph(fn):

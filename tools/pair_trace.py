@@ -15,7 +15,7 @@ assert hydra.get_config("testing_build") == 1, "run with HYDRA_TESTING=1"
 dev = torch.device("cuda:0")
 poly = int(sys.argv[1]) if len(sys.argv) > 1 else 4
 B, H, Hkv, P = (int(x) for x in sys.argv[2:6]) if len(sys.argv) > 5 else (1024, 40, 40, 16384)
-N, R = 1024, 32
+N, R = 1024, 36
 tr = torch.zeros(R * N, dtype=torch.int64, device=dev)
 hydra.set_config("prefix_impl", 3)
 hydra.set_config("prefix_poly", poly)
@@ -59,3 +59,11 @@ W = T[23:31, idx]
 print("per-warp P arrival relative to the earliest of the 8 (leader q0-3, peer q0-3):",
       " ".join(f"{med(W[i] - W.min(axis=0)):.0f}" for i in range(8)), "  MMA saw P - last arrival",
       f"{med(T[12, idx] - W.max(axis=0)):.0f}")
+C = tr.view(-1)[32 * N: 36 * N].view(1024, 4).cpu().numpy().astype(np.int64)
+n_cta = int((C[:, 0] > 0).sum())
+C = C[:n_cta]
+t0 = C[:, 0].min()
+us = lambda x: (x - t0) / 1000.0
+print(f"CTAs: {n_cta}; entry spread {us(C[:,0]).max():.2f} us, setup done median {np.median(us(C[:,1])):.2f} us, "
+      f"softmax done min/median/max {us(C[:,2]).min():.2f}/{np.median(us(C[:,2])):.2f}/{us(C[:,2]).max():.2f} us, "
+      f"exit max {us(C[:,3]).max():.2f} us")

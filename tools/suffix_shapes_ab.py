@@ -9,6 +9,8 @@ import torch
 import paper_2402_05099_b200 as hydra
 
 SH = {"c3": (1024, 40, 40, 256), "c4": (512, 32, 8, 128), "c6": (256, 32, 4, 128), "c2": (256, 32, 32, 128)}
+if os.environ.get("SHAPES"):  # name:B,H,HKV,S;...
+    SH = {k: tuple(int(x) for x in v.split(",")) for k, v in (e.split(":") for e in os.environ["SHAPES"].split(";"))}
 dev = torch.device("cuda:0")
 ctas = int(os.environ.get("CTAS", 0))
 for name, (B, H, HKV, S) in SH.items():
