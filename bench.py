@@ -196,18 +196,26 @@ def l2_flush_buffer(torch, dev, input_bytes):
     return torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
 
 
+# per-step statistics of the last timed_steps call (the median next to the mean it returns)
+LAST_TIMING = {}
+
+
 def timed_steps(torch, run, k, flush):
-    """Device time of k steps (ms per step).  Without `flush`: one event pair around k
-    back-to-back steps.  With `flush`: the buffer is overwritten before every step and only
-    the steps themselves are timed (one event pair per step, summed)."""
+    """Device time of k steps (ms per step, the mean).  Without `flush`: k back-to-back steps
+    between the first and the last of k+1 events (an event before every step also gives each
+    step's own time: median / min / max in LAST_TIMING).  With `flush`: the buffer is
+    overwritten before every step and only the steps themselves are timed (one event pair
+    per step, summed)."""
     if flush is None:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(k):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(k + 1)]
+        evs[0].record()
+        for i in range(k):
             run()
-        e1.record()
+            evs[i + 1].record()
         torch.cuda.synchronize()
-        return e0.elapsed_time(e1) / k
+        per = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(k))
+        LAST_TIMING.update(median_ms=per[k // 2], min_ms=per[0], max_ms=per[-1], n=k, flushed=False)
+        return evs[0].elapsed_time(evs[-1]) / k
     evs = []
     for _ in range(k):
         flush.zero_()
@@ -217,7 +225,9 @@ def timed_steps(torch, run, k, flush):
         c.record()
         evs.append((a, c))
     torch.cuda.synchronize()
-    return sum(a.elapsed_time(c) for a, c in evs) / k
+    per = sorted(a.elapsed_time(c) for a, c in evs)
+    LAST_TIMING.update(median_ms=per[k // 2], min_ms=per[0], max_ms=per[-1], n=k, flushed=True)
+    return sum(per) / k
 
 
 def make_timer(torch, dist, dev, world, flush=None):
@@ -687,6 +697,12 @@ def run_flat(args, cfg):
     with ClockSampler(local) as clk:
         ms = time_graph(g_main, args.steps, args.warmup)
     clocks = clk.summary()
+    step_stats = {k: (round(v, 5) if isinstance(v, float) else v) for k, v in LAST_TIMING.items()}
+    # the same step with L2 flushed (256 MB written) before every timed step: the inputs
+    # already exceed L2, so this should match the back-to-back figure
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ms_flushed = timed_steps(torch, g_main.replay, max(10, min(50, args.steps // 4)), flush_buf)
+    del flush_buf
 
     # Flatness (north_star: total time at B=1024 should drop < 15% when the prefix grows
     # from 1K to 16K): the same suffixes with the prefix cut to its first 1024 tokens,
@@ -719,28 +735,35 @@ def run_flat(args, cfg):
     for e in evs:
         e.record()
     torch.cuda.synchronize(dev)
-    timer = torch.zeros(4, dtype=torch.int64, device=dev)
+    M = 8  # steps per timer graph: each step records into its own slots, the M run back to back
+    timer = torch.zeros(M, 4, dtype=torch.int64, device=dev)
+    timer_init = torch.tensor([-1, 0, -1, 0], dtype=torch.int64, device=dev).repeat(M, 1)  # UINT64_MAX, 0
     use_timer = overlap and k_over > 0
     try:
         if use_timer:
-            hydra.set_config("step_timer", timer.data_ptr())
+            def steps_timed():
+                for i in range(M):
+                    hydra.set_config("step_timer", timer[i].data_ptr())
+                    step(overlap)
+            g_ev = capture(steps_timed)
         else:
             for key, e in zip(ev_keys, evs):
                 hydra.set_config(key, e.cuda_event)
-        g_ev = capture(lambda: step(overlap))
+            g_ev = capture(lambda: step(overlap))
         for _ in range(3):
             g_ev.replay()
         torch.cuda.synchronize(dev)
         pre_in, suf_in = [], []
-        for _ in range(max(10, min(50, args.steps // 4))):
+        for _ in range(max(10, min(50, args.steps // 4)) // (M if use_timer else 1) + 1):
             if use_timer:
-                timer.copy_(torch.tensor([-1, 0, -1, 0], dtype=torch.int64))  # UINT64_MAX, 0 for atomicMin/Max
+                timer.copy_(timer_init)  # stream-ordered before the replay: no host sync
             g_ev.replay()
             torch.cuda.synchronize(dev)
             if use_timer:
-                t = [int(v) & 0xFFFFFFFFFFFFFFFF for v in timer.tolist()]
-                pre_in.append((t[1] - t[0]) * 1e-6)
-                suf_in.append((t[3] - t[2]) * 1e-6)
+                for row in timer.tolist():
+                    t = [int(v) & 0xFFFFFFFFFFFFFFFF for v in row]
+                    pre_in.append((t[1] - t[0]) * 1e-6)
+                    suf_in.append((t[3] - t[2]) * 1e-6)
             else:
                 pre_in.append(evs[0].elapsed_time(evs[1]))
                 suf_in.append(evs[2].elapsed_time(evs[3]))
@@ -750,9 +773,9 @@ def run_flat(args, cfg):
             hydra.set_config(key, 0)
     del g_ev
     ms_pre_in, ms_suf_in = statistics.mean(pre_in), statistics.mean(suf_in)
-    in_step_how = ("inside the step: the kernel's own span (min CTA start to max CTA end, %%globaltimer) in "
-                   "the step graph of the timed loop (the prefix on its SM share runs concurrently), mean of %d "
-                   "replays" % len(suf_in)) if use_timer else (
+    in_step_how = ("inside the step: the kernel's own span (min CTA start to max CTA end, %%globaltimer), the "
+                   "prefix on its SM share concurrently, in graphs of %d back-to-back steps, mean of %d steps"
+                   % (M, len(suf_in))) if use_timer else (
                    "inside the step: CUDA events recorded by hydra_attn around the suffix launch, in the step "
                    "graph of the timed loop, mean of %d replays" % len(suf_in))
 
@@ -862,6 +885,9 @@ def run_flat(args, cfg):
                          "algorithmic_bytes_per_launch": prefix_bytes},
         "step_roofline": {"t_roof_ms": round(t_roof * 1e3, 5), "frac": round(t_roof * 1e3 / ms, 4),
                           "ms_sequential": round(ms_seq, 5), "ms_overlap": round(ms_over, 5)},
+        "step_time": dict(step_stats, mean_ms=round(ms, 5), ms_l2_flushed=round(ms_flushed, 5),
+                          note="per-step events inside the back-to-back timed loop; ms_l2_flushed: 256 MB "
+                               "written before each of its steps, only the steps timed"),
         "clocks": clocks,
         "gpu_launches": args.steps * 4,  # fill (-inf partial slots), prefix, suffix, combine
     }
