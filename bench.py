@@ -98,6 +98,8 @@ def parse():
                     help="also time the step with the suffix in a paged cache of this page size (0 = skip)")
     ap.add_argument("--batch-sweep", default="",
                     help="comma-separated batch sizes: one JSON line per B (seqsplit and flat configs)")
+    ap.add_argument("--overlap-k", type=int, default=0,
+                    help="force the SM split of the overlapped step (prefix CTAs; 0 = the library's planner)")
     ap.add_argument("--exchange", default="alltoall", choices=["alltoall", "allgather"],
                     help="sequence-split exchange (seqsplit configs)")
     return ap.parse_args()
@@ -684,7 +686,9 @@ def run_flat(args, cfg):
         ms_pre_sus = time_graph(g_pre, n_sus, 0)
     clocks_pre = clk_pre.summary()
 
-    # pick the step variant (prefix || suffix on two streams, or sequential) on a short probe
+    # pick the step variant (prefix || suffix on disjoint SMs, or sequential) on a short probe
+    if args.overlap_k > 0:
+        hydra.set_config("overlap_prefix_ctas", args.overlap_k)
     g_over = capture(lambda: step(True))
     k_over = int(hydra.get_config("last_overlap_k"))  # SM split chosen for the overlapped step
     g_seq = capture(lambda: step(False))

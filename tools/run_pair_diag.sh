@@ -1,2 +1,1 @@
-HYDRA_TESTING=1 timeout 120 python tools/pair_trace.py 4 256 32 4 19947 > gpurun_out/pair_trace.log 2>&1
-HYDRA_TESTING=1 timeout 120 python tools/pair_trace.py 4 >> gpurun_out/pair_trace.log 2>&1
+for k in 56 60 64 68; do timeout 300 python bench.py --no-cpu-baseline --no-e2e --paged-page-size 0 --overlap-k $k > gpurun_out/bench_k$k.log 2>&1; done
