@@ -100,7 +100,7 @@ def parse():
                     help="comma-separated batch sizes: one JSON line per B (seqsplit and flat configs)")
     ap.add_argument("--overlap-k", type=int, default=0,
                     help="force the SM split of the overlapped step (prefix CTAs; 0 = the library's planner)")
-    ap.add_argument("--exchange", default="alltoall", choices=["alltoall", "allgather"],
+    ap.add_argument("--exchange", default="alltoall", choices=["alltoall", "allgather", "p2p"],
                     help="sequence-split exchange (seqsplit configs)")
     return ap.parse_args()
 

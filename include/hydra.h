@@ -183,6 +183,16 @@ typedef struct {
   int64_t out_row_stride;
   float *lse_out;
   int64_t lse_out_row_stride;
+  /* Scattered output (table_rows > 0; then out / lse_out are ignored): output row r goes to
+   * out_table[r / table_rows] + (r % table_rows) * out_row_stride, its LSE to
+   * lse_out_table[r / table_rows][(r % table_rows) * lse_out_row_stride] (lse_out_table
+   * nullable).  Device arrays of ceil(rows / table_rows) device pointers, which may point into
+   * other GPUs' memory (peer-mapped / symmetric buffers): the multi-GPU layer's pack writes each
+   * batch shard's rows straight into the owning GPU's receive buffer over NVLink.  The caller
+   * orders those stores before the owner reads them (a cross-GPU barrier after this call). */
+  void *const *out_table;
+  float *const *lse_out_table;
+  int64_t table_rows;
 } hydra_combine_desc;
 HYDRA_API hydra_status hydra_combine_ex(const hydra_combine_desc *c, void *stream);
 

@@ -11,6 +11,7 @@ from .attn import (  # noqa: F401
     append_kv_paged,
     attn_workspace_bytes,
     combine,
+    combine_scatter,
     hydragen_attention,
     hydragen_attention_paged,
     prefix_attn,

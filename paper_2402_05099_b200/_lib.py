@@ -57,7 +57,8 @@ class CombineDesc(ctypes.Structure):
                 ("lse_parts_f32", ctypes.c_void_p), ("lse_f32_part_stride", ctypes.c_int64),
                 ("lse_f32_row_stride", ctypes.c_int64), ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32),
                 ("out_row_stride", ctypes.c_int64), ("lse_out", ctypes.c_void_p),
-                ("lse_out_row_stride", ctypes.c_int64)]
+                ("lse_out_row_stride", ctypes.c_int64), ("out_table", ctypes.c_void_p),
+                ("lse_out_table", ctypes.c_void_p), ("table_rows", ctypes.c_int64)]
 
 
 _lib = None

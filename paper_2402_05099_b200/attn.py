@@ -376,6 +376,44 @@ def combine(o_parts: torch.Tensor, lse_parts: torch.Tensor, out_dtype=torch.bflo
     return out, lse
 
 
+def combine_scatter(o_parts: torch.Tensor, lse_parts: torch.Tensor, out_table: torch.Tensor, table_rows: int,
+                    out_row_stride: int, out_dtype=torch.float16, lse_table: Optional[torch.Tensor] = None,
+                    lse_row_stride: int = 1, stream=None):
+    """The combine of `combine` with a scattered output (hydra_combine_ex, table_rows > 0): row r
+    goes to out_table[r // table_rows] + (r % table_rows) * out_row_stride (elements of out_dtype)
+    and its LSE to lse_table[r // table_rows] + (r % table_rows) * lse_row_stride (f32 elements).
+    out_table / lse_table: int64 device tensors of device addresses -- e.g. other GPUs' receive
+    buffers mapped through symmetric memory, so the pack of the sequence split stores each batch
+    shard's rows straight into the owning GPU (paper_2402_05099_b200.dist, exchange="p2p").
+    o_parts [n, rows, d] f32, lse_parts [n, rows] f32 as in `combine`."""
+    d = o_parts.shape[-1]
+    if o_parts.dim() != 3 or o_parts.dtype != torch.float32 or o_parts.stride(2) != 1:
+        raise ValueError("o_parts must be f32 [n, rows, d] with a contiguous head dim")
+    n, rows = o_parts.shape[0], o_parts.shape[1]
+    if lse_parts.dtype != torch.float32 or tuple(lse_parts.shape) != (n, rows):
+        raise ValueError("lse_parts must be f32 [n, rows]")
+    if table_rows <= 0 or out_row_stride < d:
+        raise ValueError("table_rows must be > 0 and out_row_stride >= d")
+    n_tab = -(-rows // table_rows)
+    for t, name in ((out_table, "out_table"), (lse_table, "lse_table")):
+        if t is not None and (t.dtype != torch.int64 or t.dim() != 1 or t.numel() < n_tab or not t.is_contiguous()):
+            raise ValueError(f"{name} must be a contiguous int64 tensor of >= {n_tab} device addresses")
+    if out_dtype not in (torch.float16, torch.float32, torch.bfloat16):
+        raise TypeError("out_dtype must be f16, f32 or bf16")
+    _require_cuda(o_parts, lse_parts, out_table, lse_table)
+    c = _lib.CombineDesc()
+    c.rows, c.d, c.n_parts = rows, d, n
+    c.o_parts, c.o_dtype, c.o_part_stride, c.o_row_stride = (o_parts.data_ptr(), _DT[o_parts.dtype],
+                                                             o_parts.stride(0), o_parts.stride(1))
+    c.lse_parts, c.lse_part_stride, c.lse_row_stride = lse_parts.data_ptr(), lse_parts.stride(0), lse_parts.stride(1)
+    c.out_dtype, c.out_row_stride, c.lse_out_row_stride = _DT[out_dtype], out_row_stride, lse_row_stride
+    c.out_table, c.table_rows = out_table.data_ptr(), table_rows
+    if lse_table is not None:
+        c.lse_out_table = lse_table.data_ptr()
+    with _on(o_parts.device):
+        check(_lib.load().hydra_combine_ex(ctypes.byref(c), _stream_ptr(stream, o_parts.device)), "hydra_combine_ex")
+
+
 # ------------------------------------------------------------------ whole decode-step attention
 def attn_workspace_bytes(q, prefix_len: int, suffix_cap: int, Hkv: int, scale=None) -> int:
     q = _squeeze_q(q)

@@ -698,9 +698,11 @@ extern "C" hydra_status hydra_combine_ex(const hydra_combine_desc *c, void *stre
   const int64_t d = c->d;
   if (c->rows < 0 || d <= 0 || c->n_parts < 0 || c->n_parts_f32 < 0 || c->n_parts + c->n_parts_f32 <= 0)
     return fail(HYDRA_ESHAPE, "rows >= 0, d > 0 and at least one part required");
+  const bool scatter = c->table_rows > 0;
   if ((c->n_parts > 0 && (!c->o_parts || !c->lse_parts)) ||
-      (c->n_parts_f32 > 0 && (!c->o_parts_f32 || !c->lse_parts_f32)) || !c->out)
+      (c->n_parts_f32 > 0 && (!c->o_parts_f32 || !c->lse_parts_f32)) || (scatter ? !c->out_table : !c->out))
     return fail(HYDRA_EINVAL, "null pointer argument");
+  if (c->table_rows < 0) return fail(HYDRA_ESHAPE, "table_rows must be >= 0");
   if (c->n_parts > 0 && c->o_dtype != HYDRA_F32 && c->o_dtype != HYDRA_F16)
     return fail(HYDRA_EUNSUPPORTED, "o_dtype must be F32 or F16");
   const hydra_dtype od = c->n_parts > 0 ? c->o_dtype : HYDRA_F32;
@@ -743,6 +745,11 @@ extern "C" hydra_status hydra_combine_ex(const hydra_combine_desc *c, void *stre
   p.out_row = out_row;
   p.lse_out = c->lse_out;
   p.lse_out_row = lo_row;
+  if (scatter) {
+    p.out_table = c->out_table;
+    p.lse_out_table = c->lse_out_table;
+    p.table_rows = c->table_rows;
+  }
   p.inject_bug = inject_combine_bug() ? 1 : 0;
   hydra_status st = launch_combine(p, od, c->out_dtype, reinterpret_cast<cudaStream_t>(stream));
   return st == HYDRA_OK ? st : cuda_fail("combine launch");

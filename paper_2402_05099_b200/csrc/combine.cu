@@ -54,6 +54,24 @@ __device__ __forceinline__ float ld1(const CombineParams &p, int q, int64_t row,
   return __ldg(reinterpret_cast<const float *>(part_o<OT>(p, q, row)) + e);
 }
 
+// Output row r: dense (out + r * out_row) or scattered through the table (table_rows > 0).
+template <typename OutT>
+__device__ __forceinline__ OutT *out_ptr(const CombineParams &p, int64_t row) {
+  if (p.table_rows > 0) {
+    const int64_t t = row / p.table_rows;
+    return reinterpret_cast<OutT *>(p.out_table[t]) + (row - t * p.table_rows) * p.out_row;
+  }
+  return reinterpret_cast<OutT *>(p.out) + row * p.out_row;
+}
+__device__ __forceinline__ float *lse_ptr(const CombineParams &p, int64_t row) {
+  if (p.table_rows > 0) {
+    if (!p.lse_out_table) return nullptr;
+    const int64_t t = row / p.table_rows;
+    return p.lse_out_table[t] + (row - t * p.table_rows) * p.lse_out_row;
+  }
+  return p.lse_out ? p.lse_out + row * p.lse_out_row : nullptr;
+}
+
 // General kernel: any number of parts, VEC floats per lane (VEC = 0: element-wise, any d).
 template <typename OT, typename OutT, int VEC>
 __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
@@ -63,10 +81,11 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
   const int n = p.n_a + p.n_b;
   float m = -INFINITY;
   for (int q = 0; q < n; ++q) m = fmaxf(m, part_lse(p, q, row));
-  OutT *out = reinterpret_cast<OutT *>(p.out) + row * p.out_row;
+  OutT *out = out_ptr<OutT>(p, row);
+  float *lse_o = lse_ptr(p, row);
   if (m == -INFINITY) {  // every part empty: sentinel (0, -inf)
     for (int e = lane; e < p.d; e += 32) out[e] = OutT(0.f);
-    if (p.lse_out && lane == 0) p.lse_out[row * p.lse_out_row] = -INFINITY;
+    if (lse_o && lane == 0) *lse_o = -INFINITY;
     return;
   }
   float den = 0.f;
@@ -111,7 +130,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
       out[e] = OutT(a * inv);
     }
   }
-  if (p.lse_out && lane == 0) p.lse_out[row * p.lse_out_row] = m + logf(den);
+  if (lse_o && lane == 0) *lse_o = m + logf(den);
 }
 
 // d = 128, at most 8 parts: the same arithmetic with the memory latency paid twice per row
@@ -149,11 +168,12 @@ __global__ void __launch_bounds__(256) combine_kernel_p8(const CombineParams p) 
     float m = -INFINITY;
 #pragma unroll
     for (int q = 0; q < NP; ++q) m = fmaxf(m, lq[k][q]);
-    OutT *out = reinterpret_cast<OutT *>(p.out) + row * p.out_row;
+    OutT *out = out_ptr<OutT>(p, row);
+    float *lse_o = lse_ptr(p, row);
     if (m == -INFINITY) {  // every part empty: sentinel (0, -inf)
 #pragma unroll
       for (int i = 0; i < 4; ++i) out[lane * 4 + i] = OutT(0.f);
-      if (p.lse_out && lane == 0) p.lse_out[row * p.lse_out_row] = -INFINITY;
+      if (lse_o && lane == 0) *lse_o = -INFINITY;
       continue;
     }
     float acc[4] = {0.f, 0.f, 0.f, 0.f}, den = 0.f;
@@ -168,7 +188,7 @@ __global__ void __launch_bounds__(256) combine_kernel_p8(const CombineParams p) 
     const float inv = 1.f / den;
 #pragma unroll
     for (int i = 0; i < 4; ++i) out[lane * 4 + i] = OutT(acc[i] * inv);
-    if (p.lse_out && lane == 0) p.lse_out[row * p.lse_out_row] = m + logf(den);
+    if (lse_o && lane == 0) *lse_o = m + logf(den);
   }
 }
 

@@ -103,6 +103,11 @@ struct CombineParams {
   int64_t out_row;
   float *lse_out;
   int64_t lse_out_row;
+  // scattered output (table_rows > 0): row r goes to table [r / table_rows], row r % table_rows
+  // (out_row / lse_out_row strides) -- e.g. straight into other GPUs' receive buffers
+  void *const *out_table;
+  float *const *lse_out_table;
+  int64_t table_rows;
   int32_t inject_bug;  // testing build only: w_p = 1 (the sabotage of S:522)
 };
 hydra_status launch_combine(const CombineParams &p, hydra_dtype o_dtype, hydra_dtype out_dtype,

@@ -18,7 +18,12 @@ Two ways the shared-prefix decode attention shards (SURVEY §8(e)
        [O (fp16, d) | LSE (f32) | pad] (272 B at d = 128), batch shard c's rows contiguous,
     3. exchanges it with ONE all-to-all (NCCL over NVLink / NVSwitch): every rank receives
        only the N pieces of its own batch shard's rows -- B*Hq*272 bytes per rank in total,
-       1/N of what an all-gather moves (`exchange="allgather"` is kept for comparison),
+       1/N of what an all-gather moves (`exchange="allgather"` is kept for comparison).
+       With `exchange="p2p"` there is no collective: the receive buffers live in symmetric
+       memory (torch.distributed._symmetric_memory), the pack of step 2 stores batch shard c's
+       rows straight into rank c's buffer over NVLink (hydra_combine_ex with an output
+       table of peer addresses: the computation and the transfer are one kernel), and a
+       device-side barrier orders those stores before the merge,
     4. meanwhile runs suffix attention for its batch shard on a second stream (it needs no
        prefix data), so the suffix overlaps the exchange,
     5. merges the N received prefix pieces and its suffix part in ONE Eq. 5 combine launch
@@ -85,6 +90,11 @@ class KernelOps:
         return self._a.combine(o_parts, lse_parts, out_dtype=out_dtype, out=out, lse_out=lse_out,
                                o_parts_f32=o_parts_f32, lse_parts_f32=lse_parts_f32)
 
+    def combine_scatter(self, o_parts, lse_parts, out_table, table_rows, out_row_stride, out_dtype, lse_table,
+                        lse_row_stride):
+        return self._a.combine_scatter(o_parts, lse_parts, out_table, table_rows, out_row_stride,
+                                       out_dtype=out_dtype, lse_table=lse_table, lse_row_stride=lse_row_stride)
+
     def attention(self, q, pk, pv, sk, sv, lens, scale=None, out=None):
         return self._a.hydragen_attention(q, pk, pv, sk, sv, lens, scale=scale, out=out)
 
@@ -119,8 +129,8 @@ class SeqSplit:
 
     def __init__(self, B: int, Hq: int, d: int, group: Optional[dist.ProcessGroup] = None, device=None,
                  exchange_dtype=torch.float16, out_dtype=torch.bfloat16, exchange: str = "alltoall", ops=None):
-        if exchange not in ("alltoall", "allgather"):
-            raise ValueError("exchange must be 'alltoall' or 'allgather'")
+        if exchange not in ("alltoall", "allgather", "p2p"):
+            raise ValueError("exchange must be 'alltoall', 'allgather' or 'p2p'")
         self.ops = ops or KernelOps()
         self.group = group
         self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
@@ -137,12 +147,35 @@ class SeqSplit:
         W = self.world
         # exchange buffers: slot c (rows of batch shard c) at rows [c*slot_rows, (c+1)*slot_rows)
         self.send = torch.zeros(W * slot_rows * self.row_bytes, dtype=torch.uint8, device=self.dev)
-        n_recv = W * slot_rows if exchange == "alltoall" else W * W * slot_rows
-        self.recv = torch.zeros(n_recv * self.row_bytes, dtype=torch.uint8, device=self.dev)
+        n_recv = W * W * slot_rows if exchange == "allgather" else W * slot_rows
+        self.symm = None
+        if exchange == "p2p":
+            # receive buffer in symmetric memory: every rank maps every peer's over NVLink, and the
+            # pack kernel stores each batch shard's rows straight into the owner's buffer at
+            # piece [my rank] -- the exchange is the pack's own stores, ordered by a barrier
+            try:
+                import torch.distributed._symmetric_memory as symm_mem
+            except ImportError as e:  # pragma: no cover - depends on the torch build
+                raise RuntimeError("exchange='p2p' needs torch.distributed._symmetric_memory") from e
+            if self.dev.type != "cuda":
+                raise ValueError("exchange='p2p' needs CUDA tensors")
+            self.recv = symm_mem.empty(n_recv * self.row_bytes, dtype=torch.uint8, device=self.dev)
+            self.recv.zero_()
+            self.symm = symm_mem.rendezvous(self.recv, group if group is not None else dist.group.WORLD)
+            peer_base = [self.symm.get_buffer(p, (n_recv * self.row_bytes,), torch.uint8).data_ptr()
+                         for p in range(W)]
+            delta = self.recv.data_ptr() - peer_base[self.rank]  # the tensor's offset in its allocation
+            peer_base = [b + delta for b in peer_base]
+            mine = self.rank * slot_rows * self.row_bytes  # my piece in every peer's buffer
+            self.out_table = torch.tensor([b + mine for b in peer_base], dtype=torch.int64, device=self.dev)
+            self.lse_table = torch.tensor([b + mine + lse_off for b in peer_base], dtype=torch.int64,
+                                          device=self.dev)
+        else:
+            self.recv = torch.zeros(n_recv * self.row_bytes, dtype=torch.uint8, device=self.dev)
         re, rf = self.row_bytes // esz, self.row_bytes // 4
         self.send_o = self.send.view(exchange_dtype).view(W * slot_rows, re)[:B * Hq, :d]
         self.send_l = self.send.view(torch.float32).view(W * slot_rows, rf)[:B * Hq, lse_off // 4]
-        if exchange == "alltoall":  # piece p = my rows as computed by rank p
+        if exchange != "allgather":  # piece p = my rows as computed by rank p
             ro = self.recv.view(exchange_dtype).view(W, slot_rows, re)
             rl = self.recv.view(torch.float32).view(W, slot_rows, rf)
             self.recv_o, self.recv_l = ro[:, :self.nb * Hq, :d], rl[:, :self.nb * Hq, lse_off // 4]
@@ -159,7 +192,7 @@ class SeqSplit:
         self.lse = torch.empty(max(self.nb, 1) * Hq, dtype=torch.float32, device=self.dev)
         self.cuda = self.dev.type == "cuda"
         backend = dist.get_backend(group)
-        self.staged = self.cuda and backend != "nccl"  # gloo: no CUDA collectives -> stage on the host
+        self.staged = self.cuda and backend != "nccl" and exchange != "p2p"  # gloo: stage on the host
         if self.staged:
             self.h_send = torch.empty(self.send.numel(), dtype=torch.uint8).pin_memory()
             self.h_recv = torch.empty(self.recv.numel(), dtype=torch.uint8).pin_memory()
@@ -171,10 +204,14 @@ class SeqSplit:
 
     def exchange_bytes(self) -> int:
         """Bytes this rank sends per step (its slots for the other ranks)."""
-        return (self.world - 1) * self.slot_rows * self.row_bytes if self.exchange == "alltoall" else \
+        return (self.world - 1) * self.slot_rows * self.row_bytes if self.exchange != "allgather" else \
             (self.world - 1) * self.send.numel()
 
     def _collective(self):
+        if self.exchange == "p2p":
+            # every rank's stores into my buffer (and mine into theirs) are complete and visible
+            self.symm.barrier(channel=0)
+            return
         if self.staged:
             self.h_send.copy_(self.send)
             hs, hr = self.h_send, self.h_recv
@@ -197,11 +234,17 @@ class SeqSplit:
         ops = self.ops
         # 1. prefix pieces of all B*Hq rows over the local prefix shard
         ops.prefix(q, pk_shard, pv_shard, scale=scale, out=self.o_p, lse_out=self.l_p)
-        # 2. one pack: (O f16 | LSE f32) rows, batch shard c's rows in slot c
-        ops.combine(self.o_p.view(1, B * Hq, d), self.l_p.view(1, B * Hq), out_dtype=self.edt, out=self.send_o,
-                    lse_out=self.send_l)
+        # 2. one pack: (O f16 | LSE f32) rows, batch shard c's rows in slot c -- with p2p the pack
+        #    stores batch shard c's rows straight into rank c's receive buffer (piece [my rank])
+        if self.exchange == "p2p":
+            esz = torch.empty((), dtype=self.edt).element_size()
+            ops.combine_scatter(self.o_p.view(1, B * Hq, d), self.l_p.view(1, B * Hq), self.out_table,
+                                self.slot_rows, self.row_bytes // esz, self.edt, self.lse_table, self.row_bytes // 4)
+        else:
+            ops.combine(self.o_p.view(1, B * Hq, d), self.l_p.view(1, B * Hq), out_dtype=self.edt, out=self.send_o,
+                        lse_out=self.send_l)
         if check_range and self.edt == torch.float16:
-            self.overflow = (~torch.isfinite(self.send_o)).any()
+            self.overflow = (~torch.isfinite(self.recv_o if self.exchange == "p2p" else self.send_o)).any()
         cur = torch.cuda.current_stream(self.dev) if self.cuda else None
         # 4. suffix of the local batch shard on the side stream, overlapping the exchange
         if self.nb > 0:

@@ -528,6 +528,70 @@ def test_seqsplit_single_rank_nccl():
         tdist.destroy_process_group()
 
 
+def test_seqsplit_single_rank_p2p():
+    """exchange="p2p" on a 1-rank NCCL group: the pack stores into the (symmetric-memory) receive
+    buffer through the output table, then the device barrier and the merge -- the multi-rank
+    data path with the one GPU this environment has (skipped if symmetric memory is missing)."""
+    import socket
+
+    import torch.distributed as tdist
+    from paper_2402_05099_b200 import dist as hdist
+
+    if not tdist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        tdist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                 device_id=torch.device(DEV))
+    try:
+        pb = synth.make_problem(24, 32, 8, 128, 700, 40, dtype="bf16", dist="mixed", seed=33)
+        t = problem_to(pb, DEV)
+        try:
+            out, lse = hdist.seqsplit_attention(t["q"], t["pk"], t["pv"], t["sk"], t["sv"], t["lens"],
+                                                exchange="p2p", return_lse=True)
+        except (RuntimeError, NotImplementedError) as e:
+            pytest.skip(f"symmetric memory unavailable: {e}")
+        torch.cuda.synchronize()
+        ref, lref = oracle.flat_attention(pb)
+        assert_parity(out, ref, lse, lref, what="seqsplit p2p")
+        a2a = hdist.seqsplit_attention(t["q"], t["pk"], t["pv"], t["sk"], t["sv"], t["lens"], exchange="alltoall")
+        assert torch.equal(out, a2a)
+    finally:
+        hdist.release_plans()
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("rows,table_rows,edt", [(1000, 256, torch.float16), (777, 100, torch.float32),
+                                                  (64, 64, torch.bfloat16)])
+def test_combine_scatter_matches_combine(rows, table_rows, edt):
+    """hydra_combine_ex with an output table (the p2p pack): rows scattered over several buffers
+    with interleaved (O | LSE) rows equal the dense combine bit for bit, and nothing outside the
+    addressed rows is written."""
+    g = torch.Generator(device=DEV)
+    g.manual_seed(rows)
+    d = 128
+    o = torch.randn(3, rows, d, device=DEV, generator=g)
+    lse = torch.randn(3, rows, device=DEV, generator=g)
+    lse[1, ::7] = -float("inf")
+    ref, lref = hydra.combine(o, lse, out_dtype=edt)
+    n_tab = -(-rows // table_rows)
+    esz = torch.empty((), dtype=edt).element_size()
+    row_bytes = (d * esz + 4 + 15) // 16 * 16
+    bufs = [torch.full((table_rows * row_bytes + 64,), 0x7F, dtype=torch.uint8, device=DEV) for _ in range(n_tab)]
+    otab = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device=DEV)
+    ltab = torch.tensor([b.data_ptr() + d * esz for b in bufs], dtype=torch.int64, device=DEV)
+    hydra.combine_scatter(o, lse, otab, table_rows, row_bytes // esz, out_dtype=edt, lse_table=ltab,
+                          lse_row_stride=row_bytes // 4)
+    torch.cuda.synchronize()
+    for t, b in enumerate(bufs):
+        r0, r1 = t * table_rows, min(rows, (t + 1) * table_rows)
+        n = r1 - r0
+        got_o = b[:n * row_bytes].view(n, row_bytes)[:, :d * esz].contiguous().view(edt).view(n, d)
+        got_l = b[:n * row_bytes].view(n, row_bytes)[:, d * esz:d * esz + 4].contiguous().view(torch.float32).view(n)
+        assert torch.equal(got_o, ref[r0:r1]) and torch.equal(got_l, lref[r0:r1])
+        assert bool((b[n * row_bytes:] == 0x7F).all()), "stores past the table's rows"
+
+
 @pytest.mark.parametrize("impl", [0, 2, 3, 4, 5, 6])
 @pytest.mark.parametrize("per,g", [(300, 1), (100, 4)])
 def test_tree_large_groups(impl, per, g):

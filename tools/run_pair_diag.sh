@@ -1,1 +1,1 @@
-for k in 56 60 64 68; do timeout 300 python bench.py --no-cpu-baseline --no-e2e --paged-page-size 0 --overlap-k $k > gpurun_out/bench_k$k.log 2>&1; done
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "scatter or p2p or seqsplit or combine" > gpurun_out/pytest_p2p.log 2>&1; tail -15 gpurun_out/pytest_p2p.log
