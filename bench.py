@@ -893,7 +893,9 @@ def run_flat(args, cfg):
                           note="per-step events inside the back-to-back timed loop; ms_l2_flushed: 256 MB "
                                "written before each of its steps, only the steps timed"),
         "clocks": clocks,
-        "gpu_launches": args.steps * 4,  # fill (-inf partial slots), prefix, suffix, combine
+        # prefix, suffix, combine (+ the -inf fill of the partial slots, which the CTA-pair prefix
+        # kernel does itself)
+        "gpu_launches": args.steps * (3 if prefix_kernel_name(hydra, Hq // Hkv).startswith("prefix_pair") else 4),
     }
     if flat:
         line["flatness"] = flat

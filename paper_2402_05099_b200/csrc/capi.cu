@@ -432,7 +432,9 @@ static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, i
     if (kind == PK_TC2) {
       // stream-K pieces leave some slots of a row unwritten: mark every slot empty first (the
       // fused merge knows which slots hold a row's pieces and needs no fill)
-      if (!fc && splits > 1 && launch_fill_neg_inf(dst.lse, dst.lse_stride * splits, s) != HYDRA_OK)
+      // (the CTA-pair kernel marks them itself: the piece that ends a unit fills the later slots)
+      if (!fc && splits > 1 && !(pair_mode(g) && !a.tasks) &&
+          launch_fill_neg_inf(dst.lse, dst.lse_stride * splits, s) != HYDRA_OK)
         return cuda_fail("fill");
       st = launch_prefix_tc2(a, tc2_ctas > 0 ? tc2_ctas : prefix_ctas(), s);
     } else {

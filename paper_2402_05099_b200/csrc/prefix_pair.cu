@@ -112,6 +112,8 @@ struct __align__(64) PrefixPairParams {
   int32_t group;         // pairs (workers) per group: n_pairs when grouped, else 1
   float *o, *lse;
   int64_t o_slot_stride, lse_slot_stride;
+  int32_t n_slots;  // partial slots per row the caller reserved: the piece ending a (pair, head) unit
+                    // marks the slots after its own empty (LSE -inf), so no separate fill runs
   int32_t mutate;  // testing build only: 3 = worker 0 skips one 4-row group of its stores
   long long *trace;  // testing build only: cluster-0 event timestamps [kTraceRows][kTraceN] (tools/pair_trace.py)
   unsigned long long *timer;  // measurement: [0] min CTA start, [1] max CTA end (%globaltimer ns); null = off
@@ -553,7 +555,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
       }
       ptx::tc_fence_before();
       ptx::warp_arrive_cluster(of0);
-      if (x == 0 && live) P.lse[it.slot * P.lse_slot_stride + seq * P.Hq + h] = (M + log2f(L)) * HYDRA_LN2;
+      if (x == 0 && live) {
+        float *lrow = P.lse + seq * P.Hq + h;
+        lrow[it.slot * P.lse_slot_stride] = (M + log2f(L)) * HYDRA_LN2;
+        if (it.blk_begin + it.nblk == P.nb)  // the unit's last piece: later slots hold no piece of it
+          for (int sl = it.slot + 1; sl < P.n_slots; ++sl) lrow[sl * P.lse_slot_stride] = -INFINITY;
+      }
       // the exchange slots are reused by the next item's first blocks: both WGs past the reads
       ptx::named_bar_sync(bar_epi, 64);
       gs0 += it.nblk;
@@ -668,6 +675,7 @@ hydra_status launch_prefix_pair(const PrefixTcArgs &a, int n_ctas, cudaStream_t 
   P.lse = a.lse;
   P.o_slot_stride = a.o_slot_stride;
   P.lse_slot_stride = a.lse_slot_stride;
+  P.n_slots = a.n_splits;
   P.mutate = kTesting ? a.mutate : 0;
   P.trace = kTesting ? reinterpret_cast<long long *>(a.trace) : nullptr;
   P.debug = kTesting ? a.debug_variant : 0;
