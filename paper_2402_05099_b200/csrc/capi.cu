@@ -50,6 +50,8 @@ struct Config {
   // kernels fill with [prefix min CTA start, prefix max CTA end, suffix start, suffix end]
   // (%globaltimer ns, atomicMin / atomicMax: the caller presets UINT64_MAX, 0, UINT64_MAX, 0)
   int64_t step_timer = 0;
+  // 1: the sequential schedule launches the suffix as a programmatic dependent of the prefix
+  int64_t seq_pdl = 1;
   // Eq. 5 merged in the kernel epilogues (fused.cuh): 1 in the sequential schedule only (the
   // suffix merges each row after the prefix kernel), 2 also in the SM-partitioned schedule
   // (arrival counters), 0 never: a separate combine launch (default).  Measured
@@ -97,7 +99,7 @@ const Key kKeys[] = {
     {"suffix_impl", &Config::suffix_impl, false},         {"suffix_splits", &Config::suffix_splits, false},
     {"suffix_ctas", &Config::suffix_ctas, false},         {"suffix_unroll", &Config::suffix_unroll, false},
     {"suffix_cb", &Config::suffix_cb, false},             {"overlap_prefix_ctas", &Config::overlap_prefix_ctas, false},
-    {"step_timer", &Config::step_timer, false},
+    {"step_timer", &Config::step_timer, false},          {"seq_pdl", &Config::seq_pdl, false},
     {"fuse_combine", &Config::fuse_combine, false},
     {"tc_debug_variant", &Config::tc_debug, true},        {"prefix_trace", &Config::prefix_trace, true},
     {"suffix_trace", &Config::suffix_trace, true},        {"inject_combine_bug", &Config::inject_combine_bug, true},
@@ -548,6 +550,7 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
     p.bt_stride = pg->bt_stride;
     p.page_shift = __builtin_ctz((unsigned)pg->page_size);
   }
+  p.pdl = pdl ? 1 : 0;
   hydra_status st = launch_decode(p, h->dtype, h->head_dim, s);
   return st == HYDRA_OK ? st : (st == HYDRA_ECUDA ? cuda_fail("suffix launch") : fail(st, "suffix"));
 }
@@ -876,11 +879,21 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
       return cuda_fail("counter reset");
   }
 
+  // Programmatic dependent launch of the suffix: in the SM-partitioned schedule it takes the SMs
+  // the prefix leaves; in the sequential one the tensor-core suffix starts on the SMs the
+  // prefix's last CTAs free (the prefix's tail: C6 0.104 -> 0.098 ms).  Not for the SIMT suffix
+  // (C3 sequential 1.02 -> 1.24 ms measured), not with the fused merge (the suffix reads the
+  // prefix partials), not with caller events between the kernels (they serialise them).
+  const bool pdl = P > 0 && S_cap > 0 &&
+                   (k_over > 0 || (!fused && g_cfg.seq_pdl && !g_cfg.step_ev[1] && !g_cfg.step_ev[2] &&
+                                   use_suffix_tc(h, B, S_cap, false)));
+  // (the testing build's lens check is a kernel of its own: with pdl it runs before the prefix)
+  if (kTesting && pdl && launch_lens_check(lens, B, S_cap, s) != HYDRA_OK) return cuda_fail("lens check");
   if (P > 0) {
     // (no event between the prefix and a programmatic-dependent suffix: it would serialise them)
     record_step_ev(0, sa);
     st = run_prefix(h, B, q, q_sb, q_sh, P, pk, pv, kv_st, kv_sh, np, pre, sa, k_over, fused ? &fc : nullptr);
-    if (k_over == 0) record_step_ev(1, sa);
+    if (!pdl) record_step_ev(1, sa);
   } else {
     st = launch_fill_neg_inf(pre.lse, rows, sa);
     if (st) st = cuda_fail("fill");
@@ -890,9 +903,9 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
     // the suffix takes every SM the prefix plan leaves free (the plan may round k down)
     const int k_eff = k_over > 0 ? prefix_tc2_ctas(B, g, h->num_kv_heads, P, k_over, prefix_bn(), pair_mode(g))
                                  : 0;
-    if (k_over == 0) record_step_ev(2, s);
+    if (!pdl) record_step_ev(2, s);
     st = run_suffix(h, B, q, q_sb, q_sh, sk, sv, s_sb, s_st, s_sh, S_cap, lens, ns, suf, s,
-                    k_over > 0 ? std::max(1, sms - k_eff) : 0, pg, fused ? &fc : nullptr, k_over > 0 && P > 0);
+                    k_over > 0 ? std::max(1, sms - k_eff) : 0, pg, fused ? &fc : nullptr, pdl);
     record_step_ev(3, s);
   } else {
     st = launch_fill_neg_inf(suf.lse, rows, s);

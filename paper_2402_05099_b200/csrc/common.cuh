@@ -64,4 +64,29 @@ struct Vec16<float> {
   }
 };
 
+// Launch a kernel, optionally as a programmatic dependent of the previous kernel in the stream
+// (cudaLaunchAttributeProgrammaticStreamSerialization): it may start once that kernel has
+// executed griddepcontrol.launch_dependents in every CTA (the persistent prefix kernels do so at
+// entry), i.e. on the SMs that kernel leaves free.  A kernel launched this way that must not
+// complete before its predecessor ends with griddepcontrol.wait.
+template <typename Kern, typename... Args>
+static inline cudaError_t launch_maybe_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                                           Args... args) {
+  if (!pdl) {
+    kern<<<grid, block, smem, s>>>(args...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 }  // namespace hydra

@@ -191,18 +191,20 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeParams p) 
       }
     }
   }
+  // a programmatic dependent of the prefix kernel (sequential schedule: the suffix fills the SMs
+  // the prefix's last CTAs leave free) completes only after it; a no-op otherwise
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 template <typename T, int D, int GQ, int U>
 static cudaError_t launch_u(const DecodeParams &p, cudaStream_t s) {
   const dim3 grid(p.n_splits, p.Hkv * (p.g / GQ), p.n_seq);
+  const bool pdl = p.pdl != 0;
   if (p.block_table)  // paged suffix cache
-    decode_attn_kernel<T, D, GQ, U, true, true><<<grid, 128, 0, s>>>(p);
-  else if (p.kv_sb == 0)  // shared KV (prefix in SIMT mode): let L1 keep it
-    decode_attn_kernel<T, D, GQ, U, false, false><<<grid, 128, 0, s>>>(p);
-  else
-    decode_attn_kernel<T, D, GQ, U, true, false><<<grid, 128, 0, s>>>(p);
-  return cudaGetLastError();
+    return launch_maybe_pdl(decode_attn_kernel<T, D, GQ, U, true, true>, grid, dim3(128), 0, s, pdl, p);
+  if (p.kv_sb == 0)  // shared KV (prefix in SIMT mode): let L1 keep it
+    return launch_maybe_pdl(decode_attn_kernel<T, D, GQ, U, false, false>, grid, dim3(128), 0, s, pdl, p);
+  return launch_maybe_pdl(decode_attn_kernel<T, D, GQ, U, true, false>, grid, dim3(128), 0, s, pdl, p);
 }
 
 template <typename T, int D, int GQ>

@@ -80,6 +80,8 @@ struct DecodeParams {
   int64_t bt_stride;
   int32_t page_shift;
   FusedCombine fc;  // fc.cnt != null: merge each completed row in the epilogue (d = 128, bf16 suffix only)
+  int32_t pdl;      // host only: programmatic dependent of the previous kernel in the stream (it ends with
+                    // griddepcontrol.wait, so its completion implies the predecessor's)
 };
 
 hydra_status launch_decode(const DecodeParams &p, hydra_dtype dt, int d, cudaStream_t s);
