@@ -453,6 +453,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
                                  fmaxf(ptx::fmax3(acc[3], acc[4], acc[5]), fmaxf(acc[6], acc[7]))) * c2;
         // m(n-1) from the other WG (the item's first block starts the chain at -inf)
         float m_in = -INFINITY;
+        if (rank == 0 && tr) {
+          asm volatile("" ::"f"(mnew));
+          trace(tr, 15 + 3 * x, gs);  // row max done (rows 15 / 18, tools/pair_trace.py)
+        }
         if (n > 0) {
           ptx::named_bar_sync(bar_in, 64);
           m_in = xch[(1 - x) * BM + r];

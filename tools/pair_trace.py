@@ -44,6 +44,8 @@ for x, base in (("a", 0), ("b", 6)):
     idx = np.nonzero(T[base + 5] > 0)[0]
     idx = idx[len(idx) // 4: 3 * len(idx) // 4]
     r = lambda k: T[base + k, idx]
+    mrow = T[15 + (3 if x == "b" else 0), idx]
+    print(f"WG {x}: row max {med(mrow - r(2)):.0f}  wait for m(n-1) + decide {med(r(3) - mrow):.0f}")
     print(f"WG {x} ({len(idx)} blocks): waitS {med(r(1) - r(0)):.0f}  ld {med(r(2) - r(1)):.0f}  max+m(n-1) {med(r(3) - r(2)):.0f}  "
           f"exps {med(r(4) - r(3)):.0f}  st+arrive {med(r(5) - r(4)):.0f}  S->P {med(r(5) - r(1)):.0f}  "
           f"own-block period {med(np.diff(r(1))):.0f}")
