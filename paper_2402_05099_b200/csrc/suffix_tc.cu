@@ -47,7 +47,14 @@ namespace hydra {
 namespace stc {
 constexpr int BT = 128;   // tokens per block (UMMA M of S^T, K of PV)
 constexpr int HD = 128;   // head dim (UMMA K of S^T, M of PV)
-constexpr int NQ = 16;    // padded query heads per KV group (UMMA N)
+constexpr int NQ = 16;    // padded query heads per KV group (smem / TMEM layout)
+// UMMA N actually issued: the g heads padded to 8 when g <= 8 -- the rows past g are zero, and
+// an MHA GEMV at N = 16 spent 16x the useful tensor work (energy under the 1 kW cap)
+#ifndef HYDRA_SUFFIX_MMA_N8
+#define HYDRA_SUFFIX_MMA_N8 1
+#endif
+template <int G>
+constexpr int kMmaN = (HYDRA_SUFFIX_MMA_N8 && G <= 8) ? 8 : 16;
 constexpr int NS = 3;     // K stages and V stages (separate rings: K frees after S, V after PV)
 constexpr int kThreads = 448;  // warp 0 K producer, 1 score MMA, 2-5 softmax, 6 V producer, 7 Q producer,
                                // 8-11 epilogue, 12 PV MMA, 13 paged-cache block-table loader
@@ -403,7 +410,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
       // S(n) needs K(n) landed and S^T slot n % NSP consumed by the softmax (p_full of round
       // n - NSP).  Two issuing threads, each blocking on one barrier at a time: a score MMA
       // never waits behind a V tile and a PV MMA never waits behind a K tile.
-      constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BT, NQ, false);  // A=K, B=Q^T (K-major)
+      constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(BT, kMmaN<G>, false);  // A=K, B=Q^T (K-major)
       long long *tr = blockIdx.x == 0 ? P.trace : nullptr;
       RoundCursor<CB, SPLIT> sc;
       sc.init(P);
@@ -440,7 +447,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
     // could not tell the tile's phase from the one two loads earlier.
     if (!(kTesting && (P.debug & 256))) {
       const bool leader = ptx::elect_one();
-      constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(HD, NQ, false) | (1u << 15);  // A=V^T (MN-major), B=P^T
+      constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(HD, kMmaN<G>, false) | (1u << 15);  // A=V^T (MN-major), B=P^T
       long long *tr = (blockIdx.x == 0 && leader) ? P.trace : nullptr;
       RoundCursor<CB, SPLIT> pc;
       pc.init(P);
