@@ -353,7 +353,15 @@ HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, i
  *                         split), 4 (64-token blocks, double-buffered scores), 5 (3 + speculative
  *                         running-max softmax)
  *   "prefix_poly"         4 (default): every 4th exp2 pair on the FMA pipe; 0 all exp2 on MUFU; 3 / 8
- *                         (variants 3-6), 2 / 3 (variant 9)
+ *                         (variants 3-6); variant 9: 0 or 4
+ *   "pair_cluster"        CTA-pair kernel: CTA pairs per cluster that share every K/V tile by TMA
+ *                         multicast (1, 2 or 4; 0 = automatic: the most that divides the stream-K
+ *                         group without idling SMs)
+ *   "seq_pdl"             1 (default): in the sequential schedule the tensor-core suffix is a
+ *                         programmatic dependent launch of the prefix (starts in its tail); 0 off
+ *   "step_timer"          measurement: device address of 4 x u64 the persistent prefix / suffix
+ *                         kernels fill with their spans (%globaltimer ns: prefix start, end,
+ *                         suffix start, end; preset UINT64_MAX, 0, UINT64_MAX, 0)
  *   "prefix_splits"       KV splits of the one-tile / SIMT prefix kernels
  *   "prefix_ctas"         CTAs of the persistent prefix kernel
  *   "suffix_impl"         1 SIMT split-K GEMV, 2 persistent TMA-fed tensor-core kernel

@@ -52,6 +52,8 @@ struct Config {
   int64_t step_timer = 0;
   // 1: the sequential schedule launches the suffix as a programmatic dependent of the prefix
   int64_t seq_pdl = 1;
+  // CTA-pair prefix kernel: pairs per cluster sharing K/V tiles by multicast (0 auto, 1, 2, 4)
+  int64_t pair_cluster = 0;
   // Eq. 5 merged in the kernel epilogues (fused.cuh): 1 in the sequential schedule only (the
   // suffix merges each row after the prefix kernel), 2 also in the SM-partitioned schedule
   // (arrival counters), 0 never: a separate combine launch (default).  Measured
@@ -100,6 +102,7 @@ const Key kKeys[] = {
     {"suffix_ctas", &Config::suffix_ctas, false},         {"suffix_unroll", &Config::suffix_unroll, false},
     {"suffix_cb", &Config::suffix_cb, false},             {"overlap_prefix_ctas", &Config::overlap_prefix_ctas, false},
     {"step_timer", &Config::step_timer, false},          {"seq_pdl", &Config::seq_pdl, false},
+    {"pair_cluster", &Config::pair_cluster, false},
     {"fuse_combine", &Config::fuse_combine, false},
     {"tc_debug_variant", &Config::tc_debug, true},        {"prefix_trace", &Config::prefix_trace, true},
     {"suffix_trace", &Config::suffix_trace, true},        {"inject_combine_bug", &Config::inject_combine_bug, true},
@@ -119,7 +122,8 @@ extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
     if (k.testing_only && !kTesting)
       return fail(HYDRA_EINVAL, "config key '%s' exists only in the testing build (libhydra_test.so)", key);
     int64_t v = value;
-    if (!strcmp(key, "prefix_poly")) v = (v == 0 || v == 2 || v == 3 || v == 4 || v == 8 || (kTesting && v == -1)) ? v : 4;
+    if (!strcmp(key, "prefix_poly")) v = (v == 0 || v == 3 || v == 4 || v == 8 || (kTesting && v == -1)) ? v : 4;
+    if (!strcmp(key, "pair_cluster")) v = (v == 1 || v == 2 || v == 4) ? v : 0;
     if (!strcmp(key, "prefix_variant")) v = (v == 3 || v == 4 || v == 5 || v == 6) ? v : 9;
     if (!strcmp(key, "prefix_stages")) v = (v == 2 ? 2 : 3);
     if (!strcmp(key, "suffix_cb")) v = (v == 1 ? 1 : 2);
@@ -134,7 +138,10 @@ extern "C" int64_t hydra_get_config(const char *key) {
   if (!key) return -1;
   if (!strcmp(key, "last_overlap_k")) return g_cfg.last_overlap_k;
   if (!strcmp(key, "testing_build")) return kTesting ? 1 : 0;
-  if (!strcmp(key, "pair_max_ctas")) return prefix_pair_plan(1 << 20, 1, 1, 1 << 20, 1 << 20).ctas;  // resident CTA pairs x 2
+  // resident CTAs of the CTA-pair kernel in clusters of 1 / 2 / 4 pairs (2 x pairs, 1024 x 4 groups)
+  if (!strcmp(key, "pair_max_ctas")) return prefix_pair_plan(1024, 1, 1, 1 << 20, 1 << 20, 1).ctas;
+  if (!strcmp(key, "pair_max_ctas_c2")) return prefix_pair_plan(1024, 1, 1, 1 << 20, 1 << 20, 2).ctas;
+  if (!strcmp(key, "pair_max_ctas_c4")) return prefix_pair_plan(1024, 1, 1, 1 << 20, 1 << 20, 4).ctas;
   for (int i = 0; i < 4; ++i)
     if (!strcmp(key, kStepEvKeys[i])) return g_cfg.step_ev[i];
   for (const Key &k : kKeys)
@@ -318,7 +325,7 @@ static int prefix_splits(const hydra_heads *h, int64_t B, int64_t P, int tc2_cta
   switch (prefix_kind(h, B * g, P, tc2_ctas)) {
     case PK_TC2:
       return prefix_tc2_slots(B, g, h->num_kv_heads, P, tc2_ctas > 0 ? tc2_ctas : prefix_ctas(), prefix_bn(),
-                              pair_mode(g));
+                              pair_mode(g), (int)g_cfg.pair_cluster);
     case PK_TC1:
       return prefix_splits_tc(((B * g + 127) / 128) * h->num_kv_heads, P);
     default:
@@ -353,7 +360,8 @@ static int overlap_prefix_ctas(const hydra_heads *h, int64_t B, int64_t P, int64
   double best = 1e300;
   for (int k = 8; k <= sms - 8; ++k) {
     if (prefix_kind(h, B * g, P, k) != PK_TC2) break;  // too few blocks per CTA beyond this k
-    if (prefix_tc2_ctas(B, g, h->num_kv_heads, P, k, prefix_bn(), pair_mode(g)) != k) continue;  // plan would idle SMs
+    if (prefix_tc2_ctas(B, g, h->num_kv_heads, P, k, prefix_bn(), pair_mode(g), (int)g_cfg.pair_cluster) != k)
+      continue;  // plan would idle SMs
     const double t = std::max(pair_blocks / (k * R_P), suffix_tc_us(h, B, S_cap, sms - k, R_S, BW));
     if (t < best) {
       best = t;
@@ -430,6 +438,7 @@ static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, i
     a.mutate = (int32_t)g_cfg.mutate;
     if (fc) a.fc = *fc;
     a.timer = reinterpret_cast<unsigned long long *>((intptr_t)g_cfg.step_timer);
+    a.pair_cluster = (int32_t)g_cfg.pair_cluster;
     hydra_status st;
     if (kind == PK_TC2) {
       // stream-K pieces leave some slots of a row unwritten: mark every slot empty first (the
@@ -901,7 +910,8 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
   if (st) return st;
   if (S_cap > 0) {
     // the suffix takes every SM the prefix plan leaves free (the plan may round k down)
-    const int k_eff = k_over > 0 ? prefix_tc2_ctas(B, g, h->num_kv_heads, P, k_over, prefix_bn(), pair_mode(g))
+    const int k_eff = k_over > 0 ? prefix_tc2_ctas(B, g, h->num_kv_heads, P, k_over, prefix_bn(), pair_mode(g),
+                                                   (int)g_cfg.pair_cluster)
                                  : 0;
     if (!pdl) record_step_ev(2, s);
     st = run_suffix(h, B, q, q_sb, q_sh, sk, sv, s_sb, s_st, s_sh, S_cap, lens, ns, suf, s,

@@ -155,14 +155,15 @@ struct PrefixTcArgs {
   int32_t variant = 3;     // persistent kernel: 3 (128-token blocks) or 4 (64-token, double-buffered S)
   int32_t stages;  // K/V pipeline stages: 2 (160 KB smem, leaves room for co-resident suffix CTAs) or 3
   unsigned long long *timer = nullptr;  // measurement: [0] min CTA start, [1] max CTA end (ns); persistent kernels
+  int32_t pair_cluster = 0;  // CTA-pair kernel: pairs per cluster (0 = automatic)
 };
 bool prefix_tc_supported(const hydra_heads *h);
 hydra_status launch_prefix_tc(const PrefixTcArgs &a, cudaStream_t s);
 // v3: persistent, two 128-row query tiles per CTA; flat mode is stream-K over n_ctas CTAs
 // (partial slots per row = prefix_tc2_slots), task mode deals (task, head, split) items.
 hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s);
-int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn, bool pair = false);
-int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn, bool pair = false);
+int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn, bool pair = false, int pair_cluster = 0);
+int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn, bool pair = false, int pair_cluster = 0);
 // The flat-mode stream-K plan of launch_prefix_tc2 over n_ctas CTAs, as the fused combine
 // needs it (which partial slots hold a row's pieces): fills fc.sk_*.
 void prefix_tc2_plan_into(FusedCombine &fc, int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn);
@@ -170,11 +171,13 @@ void prefix_tc2_plan_into(FusedCombine &fc, int64_t B, int g, int Hkv, int64_t P
 // same grouped stream-K plan as launch_prefix_tc2 with a CTA pair as the worker.
 struct PairPlan {
   int group, workers, ctas;
+  int cluster;  // CTA pairs per cluster (1, 2, 4): they share every K/V tile by TMA multicast
   int64_t total;
 };
 bool prefix_pair_supported(int g);
-PairPlan prefix_pair_plan(int64_t B, int g, int Hkv, int64_t P, int n_ctas);
-int prefix_pair_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas);
+// forced_cluster: 0 = automatic, 1 / 2 / 4 = pairs per cluster (config key pair_cluster)
+PairPlan prefix_pair_plan(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int forced_cluster = 0);
+int prefix_pair_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int forced_cluster = 0);
 hydra_status launch_prefix_pair(const PrefixTcArgs &a, int n_ctas, cudaStream_t s);
 // Persistent tensor-core suffix kernel (bf16, d = 128, g <= 16), TMA-fed.
 struct SuffixTcArgs {

@@ -193,9 +193,13 @@ struct Cursor {
 };
 }  // namespace pr
 
-template <int kPolyEvery>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
-    prefix_pair_kernel(const __grid_constant__ PrefixPairParams P) {
+// kC: CTA pairs per cluster (1, 2 or 4).  The kC pairs of a cluster are members of one
+// stream-K group (same heads and blocks, different query rows), so every K / V tile they need is
+// the same: each CTA loads a 1/kC piece of its half tile and multicasts it to the CTAs with the
+// same rank in their pair -- L2 -> SM traffic / kC.  (Measured with the K/V loads switched off:
+// the prefix alone at the power cap ran 13 % faster at 12 % higher SM clock -- tools/pair_power.py.)
+template <int kPolyEvery, int kC>
+__global__ void __launch_bounds__(pr::kThreads, 1) prefix_pair_kernel(const __grid_constant__ PrefixPairParams P) {
   using namespace pr;
   extern __shared__ uint8_t smem_raw[];
   // SM-partitioned schedule on one stream: the suffix kernel (a programmatic dependent) may start
@@ -211,7 +215,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
   uint64_t *sf = qe + NQ, *pf = sf + NSB, *ordy = pf + NSB, *ofree = ordy + 1;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + N_BARS);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const uint32_t rank = ptx::cluster_ctarank();
+  const uint32_t crank = ptx::cluster_ctarank();
+  const uint32_t rank = crank & 1;       // rank within the CTA pair (0: the pair's MMA leader)
+  const uint32_t pip = crank >> 1;       // pair within the cluster
+  const uint32_t lead = crank & ~1u;     // cluster rank of this pair's leader
+  constexpr uint16_t kAll = (uint16_t)((1u << (2 * kC)) - 1);
+  const uint16_t pair_mask = (uint16_t)(3u << (2 * pip));
+  const uint16_t half_mask = (uint16_t)((kC == 1 ? 1u : kC == 2 ? 0x5u : 0x55u) << rank);  // same rank-in-pair
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&P.tmQ);
@@ -219,11 +229,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
     ptx::prefetch_tmap(&P.tmV);
     for (int i = 0; i < NSK; ++i) {
       ptx::mbar_init(&kf[i], 1);
-      ptx::mbar_init(&ke[i], 1);
+      ptx::mbar_init(&ke[i], kC);  // one release per pair of the cluster
     }
     for (int i = 0; i < NSV; ++i) {
       ptx::mbar_init(&vf[i], 1);
-      ptx::mbar_init(&ve[i], 1);
+      ptx::mbar_init(&ve[i], kC);
     }
     for (int i = 0; i < NQ; ++i) {
       ptx::mbar_init(&qf[i], 1);
@@ -250,8 +260,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
     // (separate threads, so a K tile is issued as soon as its slot frees, independently of V)
     if (ptx::elect_one()) {
       const bool kq_role = warp == 0;
-      const uint32_t kf0 = ptx::mapa(ptx::smem_u32(kf), 0), vf0 = ptx::mapa(ptx::smem_u32(vf), 0),
-                     qf0 = ptx::mapa(ptx::smem_u32(qf), 0);
+      const uint32_t kf0 = ptx::mapa(ptx::smem_u32(kf), lead), vf0 = ptx::mapa(ptx::smem_u32(vf), lead),
+                     qf0 = ptx::mapa(ptx::smem_u32(qf), lead);
       uint32_t kq = 0, vq = 0, qi = 0;
       long long *tr = (kTesting && P.trace && blockIdx.x == 0 && kq_role) ? P.trace : nullptr;
       Iter si;
@@ -286,14 +296,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
             trace(tr, 20, kq);
             if (rank == 0) ptx::mbar_arrive_expect_tx(&kf[ks], 2 * KHALF);
             uint8_t *sK = smem + OFF_K + ks * KHALF;
-            ptx::tma_load_3d_pair(sK, &P.tmK, kf0 + ks * 8, 0, it.j, t0 + 64 * (int)rank);
-            ptx::tma_load_3d_pair(sK + KPANEL, &P.tmK, kf0 + ks * 8, 64, it.j, t0 + 64 * (int)rank);
+            if constexpr (kC == 1) {
+              ptx::tma_load_3d_pair(sK, &P.tmK, kf0 + ks * 8, 0, it.j, t0 + 64 * (int)rank);
+              ptx::tma_load_3d_pair(sK + KPANEL, &P.tmK, kf0 + ks * 8, 64, it.j, t0 + 64 * (int)rank);
+            } else {  // this CTA's piece of the half tile: panel pip % 2, token rows (pip / 2) * 32 (kC = 4)
+              const int panel = kC == 2 ? (int)pip : (int)(pip & 1), trow = kC == 2 ? 0 : (int)(pip >> 1) * 32;
+              ptx::tma_load_3d_pair_mc(sK + panel * KPANEL + trow * 128, &P.tmK, kf0 + ks * 8, 64 * panel, it.j,
+                                       t0 + 64 * (int)rank + trow, half_mask);
+            }
             ++kq;
           } else {
             const int vs = vq % NSV;
             ptx::mbar_wait(&ve[vs], ((vq / NSV) & 1) ^ 1);
             if (rank == 0) ptx::mbar_arrive_expect_tx(&vf[vs], 2 * VHALF);
-            ptx::tma_load_3d_pair(smem + OFF_V + vs * VHALF, &P.tmV, vf0 + vs * 8, 64 * (int)rank, it.j, t0);
+            if constexpr (kC == 1) {
+              ptx::tma_load_3d_pair(smem + OFF_V + vs * VHALF, &P.tmV, vf0 + vs * 8, 64 * (int)rank, it.j, t0);
+            } else {  // token rows [pip * 128 / kC, +128 / kC) of this half's 64 dims
+              const int trow = (int)pip * (BN / kC);
+              ptx::tma_load_3d_pair_mc(smem + OFF_V + vs * VHALF + trow * 128, &P.tmV, vf0 + vs * 8, 64 * (int)rank,
+                                       it.j, t0 + trow, half_mask);
+            }
             ++vq;
           }
         }
@@ -302,7 +324,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
   } else if (warp == kMmaWarp) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
     // ================= MMA issuer (leader CTA, one thread) =================
-    if (rank == 0 && ptx::elect_one()) {
+    if (rank == 0 && ptx::elect_one()) {  // the pair's leader
       constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(2 * BM, BN, false);  // S = Q K^T, M = 256
       constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(2 * BM, HD, true);  // O += P V, V MN-major
       long long *tr = (kTesting && P.trace && blockIdx.x == 0) ? P.trace : nullptr;
@@ -327,9 +349,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
         for (int kk = 0; kk < HD / 16; ++kk)
           ptx::mma2_ss(tmem + sb * BN, ptx::smem_desc_sw128(qa + (kk / 4) * QPANEL + (kk % 4) * 32, 16, 1024),
                        ptx::smem_desc_sw128(ka + (kk / 4) * KPANEL + (kk % 4) * 32, 16, 1024), idesc_s, kk > 0);
-        ptx::mma2_commit(&sf[sb]);
-        ptx::mma2_commit(&ke[ks]);
-        if (cs.n == cs.it.nblk - 1) ptx::mma2_commit(&qe[qb]);
+        ptx::mma2_commit(&sf[sb], pair_mask);
+        ptx::mma2_commit(&ke[ks], kAll);  // every CTA of the cluster: its K piece went to all pairs
+        if (cs.n == cs.it.nblk - 1) ptx::mma2_commit(&qe[qb], pair_mask);
         trace(tr, 14, gs);
         ++gs;
         cs.advance(P);
@@ -363,7 +385,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
           ptx::mma2_ts(tmem + O_COL, tmem + sb * BN + kk * 8,
                        ptx::smem_desc_sw128(va + kk * 2048, 16, 1024), idesc_pv, acc0 | (kk > 0));
         trace(tr, 19, gp);
-        if (cp.n == cp.it.nblk - 1) ptx::mma2_commit(ordy);  // the item's last PV: epilogue may read O
+        if (cp.n == cp.it.nblk - 1) ptx::mma2_commit(ordy, pair_mask);  // the item's last PV: epilogue may read O
         ++gp;
         cp.advance(P);
         while (!(k && q)) {
@@ -375,7 +397,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
         // S(gp - 1 + NSB) right behind the PV (it overwrites the score buffer whose P the PV read),
         // then the V slot release: one commit covering both, off the path to the next score MMA
         issue_s(true);
-        ptx::mma2_commit(&ve[vs]);
+        ptx::mma2_commit(&ve[vs], kAll);
       }
     }
   } else if (warp >= 4) {
@@ -392,7 +414,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
     const int quarter = warp % 4;
     const int r = quarter * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const uint32_t pf0 = ptx::mapa(ptx::smem_u32(pf), 0), of0 = ptx::mapa(ptx::smem_u32(ofree), 0);
+    const uint32_t pf0 = ptx::mapa(ptx::smem_u32(pf), lead), of0 = ptx::mapa(ptx::smem_u32(ofree), lead);
     float *xch = reinterpret_cast<float *>(smem + OFF_X);  // [2 slots][128 rows]
     const int bar_out = 1 + quarter + 4 * x, bar_in = 1 + quarter + 4 * (1 - x), bar_epi = 9 + quarter;
     long long *tr = (kTesting && P.trace && blockIdx.x < 2 && quarter == 0 && lane == 0 && (rank == 0 || x == 0))
@@ -588,43 +610,70 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pr::kThreads, 1)
 // ------------------------------------------------------------------ host side
 bool prefix_pair_supported(int g) { return g >= 1 && g <= 128 && 128 % g == 0; }
 
-// Clusters of two that can be resident at once on this device (cached per device).
-static int max_pair_workers() {
-  static int cached[64] = {0};
+template <int kPoly, int kC>
+static const void *pair_fn() {
+  return reinterpret_cast<const void *>(prefix_pair_kernel<kPoly, kC>);
+}
+static const void *pair_kernel(int poly, int kC) {
+  if (poly == 4) return kC == 4 ? pair_fn<4, 4>() : kC == 2 ? pair_fn<4, 2>() : pair_fn<4, 1>();
+  return kC == 4 ? pair_fn<0, 4>() : kC == 2 ? pair_fn<0, 2>() : pair_fn<0, 1>();
+}
+
+// CTA pairs that can be resident at once in clusters of kC pairs (cached per device and kC).
+static int max_pair_workers(int kC) {
+  static int cached[64][3] = {};
+  const int ci = kC == 4 ? 2 : kC == 2 ? 1 : 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) return 74;
-  if (cached[dev] > 0) return cached[dev];
-  if (ensure_smem_attr(reinterpret_cast<const void *>(prefix_pair_kernel<4>), pr::ALLOC) != cudaSuccess) {
-    cudaGetLastError();
-    return device_sm_count() / 2;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(2 * 148, 1, 1);
-  cfg.blockDim = dim3(pr::kThreads, 1, 1);
-  cfg.dynamicSmemBytes = pr::ALLOC;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
+  if (cached[dev][ci] > 0) return cached[dev][ci];
+  const void *fn = pair_kernel(4, kC);
   int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, (void *)prefix_pair_kernel<4>, &cfg) != cudaSuccess || n <= 0) {
-    cudaGetLastError();
-    n = device_sm_count() / 2;
+  if (ensure_smem_attr(fn, pr::ALLOC) == cudaSuccess) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * 148, 1, 1);
+    cfg.blockDim = dim3(pr::kThreads, 1, 1);
+    cfg.dynamicSmemBytes = pr::ALLOC;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2 * kC;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) n = 0;
   }
-  cached[dev] = n;
-  return n;
+  cudaGetLastError();
+  if (n <= 0) n = device_sm_count() / (2 * kC);
+  cached[dev][ci] = n * kC;
+  return n * kC;
 }
 
-PairPlan prefix_pair_plan(int64_t B, int g, int Hkv, int64_t P, int n_ctas) {
-  const int workers = std::max(1, std::min(n_ctas / 2, max_pair_workers()));
+// Pairs per cluster: the largest kC in {4, 2} that divides the group (n_pairs; the grouped
+// plan) without leaving fewer workers than kC = 1 would use; config key pair_cluster forces it.
+static int choose_cluster(int64_t n_pairs, int n_workers_req, int forced) {
+  if (forced == 1 || n_pairs < 2) return 1;
+  auto workers = [&](int kC) {
+    const int w = std::min(n_workers_req, max_pair_workers(kC));
+    return 2 * n_pairs <= w ? (int)(w / n_pairs * n_pairs) : 0;  // grouped plan only
+  };
+  const int w1 = std::max(workers(1), 1);
+  for (int kC : {4, 2}) {
+    if (forced > 1 && kC != forced) continue;
+    if (n_pairs % kC == 0 && workers(kC) >= (forced > 1 ? 1 : w1)) return kC;
+  }
+  return 1;
+}
+
+PairPlan prefix_pair_plan(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int forced_cluster) {
   const int64_t nb = (P + pr::BN - 1) / pr::BN;
   const int64_t n_pairs = (B * g + 255) / 256;
+  const int kC = choose_cluster(n_pairs, std::max(1, n_ctas / 2), forced_cluster);
+  const int workers = std::max(1, std::min(n_ctas / 2, max_pair_workers(kC)));
   PairPlan pl;
+  pl.cluster = kC;
   pl.group = (n_pairs > 1 && 2 * n_pairs <= workers) ? (int)n_pairs : 1;
+  if (pl.group == 1) pl.cluster = 1;
   pl.total = pl.group > 1 ? (int64_t)Hkv * nb : n_pairs * Hkv * nb;
   const int64_t G = std::min<int64_t>(workers / pl.group, pl.total);
   pl.workers = (int)(std::max<int64_t>(G, 1) * pl.group);
@@ -632,8 +681,8 @@ PairPlan prefix_pair_plan(int64_t B, int g, int Hkv, int64_t P, int n_ctas) {
   return pl;
 }
 
-int prefix_pair_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas) {
-  const PairPlan pl = prefix_pair_plan(B, g, Hkv, P, n_ctas);
+int prefix_pair_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int forced_cluster) {
+  const PairPlan pl = prefix_pair_plan(B, g, Hkv, P, n_ctas, forced_cluster);
   if (pl.total <= 0) return 1;
   const int64_t nb = (P + pr::BN - 1) / pr::BN;
   const int64_t range = pl.total / (pl.workers / pl.group);  // >= 1
@@ -642,11 +691,9 @@ int prefix_pair_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas) {
 
 hydra_status launch_prefix_pair(const PrefixTcArgs &a, int n_ctas, cudaStream_t s) {
   const int poly = a.poly_every;
-  if (a.tasks || !prefix_pair_supported(a.g) || !(poly == 0 || poly == 2 || poly == 3 || poly == 4)) return HYDRA_EINVAL;
-  const void *fn = poly == 4   ? reinterpret_cast<const void *>(prefix_pair_kernel<4>)
-                   : poly == 3 ? reinterpret_cast<const void *>(prefix_pair_kernel<3>)
-                   : poly == 2 ? reinterpret_cast<const void *>(prefix_pair_kernel<2>)
-                               : reinterpret_cast<const void *>(prefix_pair_kernel<0>);
+  if (a.tasks || !prefix_pair_supported(a.g) || !(poly == 0 || poly == 4)) return HYDRA_EINVAL;
+  const PairPlan pl = prefix_pair_plan(a.B, a.g, a.Hkv, a.P, n_ctas, a.pair_cluster);
+  const void *fn = pair_kernel(poly, pl.cluster);
   if (ensure_smem_attr(fn, pr::ALLOC) != cudaSuccess) return HYDRA_ECUDA;
   PrefixPairParams P;
   memset(&P, 0, sizeof(P));
@@ -660,7 +707,9 @@ hydra_status launch_prefix_pair(const PrefixTcArgs &a, int n_ctas, cudaStream_t 
   {
     const uint64_t dims[3] = {(uint64_t)pr::HD, (uint64_t)a.Hkv, (uint64_t)a.kv_total};
     const uint64_t strides[2] = {(uint64_t)a.kv_sh * 2, (uint64_t)a.kv_st * 2};
-    const uint32_t boxk[3] = {64, 1, 64}, boxv[3] = {64, 1, (uint32_t)pr::BN};
+    // multicast pieces (pl.cluster pairs share every tile): K panels of 64 tokens (32 at 4 pairs),
+    // V rows of 128 / pairs tokens
+    const uint32_t boxk[3] = {64, 1, pl.cluster == 4 ? 32u : 64u}, boxv[3] = {64, 1, (uint32_t)(pr::BN / pl.cluster)};
     if (!encode_bf16_map(&P.tmK, 3, a.k, dims, strides, boxk)) return HYDRA_ECUDA;
     if (!encode_bf16_map(&P.tmV, 3, a.v, dims, strides, boxv)) return HYDRA_ECUDA;
   }
@@ -672,7 +721,6 @@ hydra_status launch_prefix_pair(const PrefixTcArgs &a, int n_ctas, cudaStream_t 
   P.B = a.B;
   P.n_pairs = (int32_t)(((int64_t)a.B * a.g + 255) / 256);
   P.nb = (int32_t)((a.P + pr::BN - 1) / pr::BN);
-  const PairPlan pl = prefix_pair_plan(a.B, a.g, a.Hkv, a.P, n_ctas);
   P.total_blocks = pl.total;
   P.group = pl.group;
   P.o = a.o;
@@ -685,13 +733,28 @@ hydra_status launch_prefix_pair(const PrefixTcArgs &a, int n_ctas, cudaStream_t 
   P.debug = kTesting ? a.debug_variant : 0;
   P.timer = a.timer;
   if (pl.total <= 0) return HYDRA_OK;
-  switch (poly) {
-    case 4: prefix_pair_kernel<4><<<pl.ctas, pr::kThreads, pr::ALLOC, s>>>(P); break;
-    case 3: prefix_pair_kernel<3><<<pl.ctas, pr::kThreads, pr::ALLOC, s>>>(P); break;
-    case 2: prefix_pair_kernel<2><<<pl.ctas, pr::kThreads, pr::ALLOC, s>>>(P); break;
-    default: prefix_pair_kernel<0><<<pl.ctas, pr::kThreads, pr::ALLOC, s>>>(P); break;
-  }
-  return cudaGetLastError() == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(pl.ctas, 1, 1);
+  cfg.blockDim = dim3(pr::kThreads, 1, 1);
+  cfg.dynamicSmemBytes = pr::ALLOC;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2 * pl.cluster;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  if (poly == 4)
+    e = pl.cluster == 4   ? cudaLaunchKernelEx(&cfg, prefix_pair_kernel<4, 4>, P)
+        : pl.cluster == 2 ? cudaLaunchKernelEx(&cfg, prefix_pair_kernel<4, 2>, P)
+                          : cudaLaunchKernelEx(&cfg, prefix_pair_kernel<4, 1>, P);
+  else
+    e = pl.cluster == 4   ? cudaLaunchKernelEx(&cfg, prefix_pair_kernel<0, 4>, P)
+        : pl.cluster == 2 ? cudaLaunchKernelEx(&cfg, prefix_pair_kernel<0, 2>, P)
+                          : cudaLaunchKernelEx(&cfg, prefix_pair_kernel<0, 1>, P);
+  return e == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
 }
 
 }  // namespace hydra

@@ -1029,8 +1029,8 @@ static Tc2Plan tc2_plan(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn
 }
 
 // Flat mode: number of partial slots per row the schedule over n_ctas CTAs produces.
-int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn, bool pair) {
-  if (pair) return prefix_pair_slots(B, g, Hkv, P, n_ctas);
+int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn, bool pair, int pair_cluster) {
+  if (pair) return prefix_pair_slots(B, g, Hkv, P, n_ctas, pair_cluster);
   const Tc2Plan pl = tc2_plan(B, g, Hkv, P, n_ctas, bn);
   if (pl.total <= 0) return 1;
   const int64_t nb = (P + bn - 1) / bn;
@@ -1038,8 +1038,8 @@ int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn, b
   return (int)((nb + range - 1) / range + 1);
 }
 
-int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn, bool pair) {
-  if (pair) return prefix_pair_plan(B, g, Hkv, P, n_ctas).ctas;
+int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn, bool pair, int pair_cluster) {
+  if (pair) return prefix_pair_plan(B, g, Hkv, P, n_ctas, pair_cluster).ctas;
   return tc2_plan(B, g, Hkv, P, n_ctas, bn).ctas;
 }
 

@@ -242,6 +242,16 @@ __device__ __forceinline__ void tma_load_3d_pair(void *smem_dst, const void *tma
       "l"(tmap), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// The same into this smem offset of every CTA in `mask` (cluster ranks), each destination's
+// completion counted on its pair leader's barrier at `bar_cluster`'s offset.
+__device__ __forceinline__ void tma_load_3d_pair_mc(void *smem_dst, const void *tmap, uint32_t bar_cluster, int c0,
+                                                    int c1, int c2, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(smem_dst)),
+      "l"(tmap), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_4d_pair(void *smem_dst, const void *tmap, uint32_t bar_cluster, int c0,
                                                  int c1, int c2, int c3) {
   asm volatile(

@@ -24,7 +24,7 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(autouse=True)
 def _reset_config():
     keys = ("prefix_impl", "prefix_splits", "suffix_splits", "prefix_ctas", "suffix_impl",
-            "suffix_ctas", "overlap_prefix_ctas")
+            "suffix_ctas", "overlap_prefix_ctas", "pair_cluster")
     for k in keys:
         hydra.set_config(k, 0)
     defaults = {"prefix_variant": 9, "suffix_cb": 2, "prefix_poly": 4, "fuse_combine": 0}  # the library defaults
@@ -102,7 +102,7 @@ def test_prefix_tc_splits(splits):
 
 
 @pytest.mark.parametrize("variant,poly,steep", [(3, 0, 6), (5, 0, 6), (5, 4, 6), (5, 8, 6), (3, 4, 6), (6, 0, 6),
-                                                (6, 4, 6), (9, 0, 6), (9, 4, 6), (9, 4, 60), (9, 2, 60)])
+                                                (6, 4, 6), (9, 0, 6), (9, 4, 6), (9, 4, 60), (9, 0, 60)])
 def test_prefix_tc2_growing_max(variant, poly, steep):
     """Scores that grow along the prefix: the running max is raised block after block, which
     exercises the O/l correction and, for the speculative softmax, the redo path.  The CTA-pair
@@ -140,8 +140,8 @@ def test_prefix_tc2_stream_k_ctas(ctas, variant):
 
 @pytest.mark.parametrize("B,Hq,Hkv,P", [(1024, 40, 40, 700), (512, 32, 8, 1500), (256, 32, 4, 999), (77, 16, 1, 300),
                                         (5, 12, 4, 2000), (64, 64, 2, 129)])
-@pytest.mark.parametrize("ctas", [0, 6, 60])
-def test_prefix_pair_shapes(B, Hq, Hkv, P, ctas):
+@pytest.mark.parametrize("ctas,cluster", [(0, 0), (6, 0), (60, 0), (0, 1), (0, 2), (0, 4), (64, 4), (32, 2)])
+def test_prefix_pair_shapes(B, Hq, Hkv, P, ctas, cluster):
     """CTA-pair kernel: MHA and GQA g = 4 / 8 / 16 / 32 (Q tiles by a 4-D TMA box of 128/g
     sequences), g = 3 (unsupported: the two-tile kernel runs instead), partial pairs (B*g not a
     multiple of 256), prefix tails inside the second token half of a block, grouped and
@@ -149,12 +149,16 @@ def test_prefix_pair_shapes(B, Hq, Hkv, P, ctas):
     hydra.set_config("prefix_impl", 3)
     hydra.set_config("prefix_variant", 9)
     hydra.set_config("prefix_ctas", ctas)
+    hydra.set_config("pair_cluster", cluster)  # pairs per cluster sharing K/V by multicast (0 = auto)
     pb = synth.make_problem(B, Hq, Hkv, 128, P, 1, dtype="bf16", dist="boundary", seed=B + P)
     t = problem_to(pb, DEV)
-    o, lse = H.prefix_attn(t["q"], t["pk"], t["pv"])
-    torch.cuda.synchronize()
+    try:
+        o, lse = H.prefix_attn(t["q"], t["pk"], t["pv"])
+        torch.cuda.synchronize()
+    finally:
+        hydra.set_config("pair_cluster", 0)
     ref, lref = oracle.prefix_only(pb)
-    assert_parity(o, ref, lse, lref, what=f"pair prefix {B},{Hq},{Hkv},{P} ctas={ctas}")
+    assert_parity(o, ref, lse, lref, what=f"pair prefix {B},{Hq},{Hkv},{P} ctas={ctas} cluster={cluster}")
 
 
 @pytest.mark.parametrize("aux", [False, True])

@@ -28,6 +28,7 @@ def graph(fn):
     with torch.cuda.graph(gr): fn()
     return gr
 graphs = {}
+hydra.set_config("pair_cluster", int(os.environ.get("CLUSTER", 0)))
 if os.environ.get("POLY") is not None:
     hydra.set_config("prefix_poly", int(os.environ["POLY"]))
 for k in ks:

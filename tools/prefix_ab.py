@@ -29,6 +29,7 @@ for name in shapes:
         hydra.set_config("prefix_impl", 2 if v == "t1" else 3)
         hydra.set_config("prefix_variant", 9 if v == "t1" else int(v))
         hydra.set_config("prefix_ctas", ctas)
+        hydra.set_config("pair_cluster", int(os.environ.get("CLUSTER", 0)))
         fn = lambda: hydra.prefix_attn(q, pk, pv, workspace=ws)
         o, lse = fn()
         torch.cuda.synchronize()
