@@ -681,12 +681,23 @@ PairPlan prefix_pair_plan(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int 
   return pl;
 }
 
+// Partial slots per row = the most stream-K pieces any (pair, head) unit is cut into: the groups
+// owning its first and last block, exactly (an extra, always-empty slot would cost the combine a
+// full read of its O rows).
 int prefix_pair_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int forced_cluster) {
   const PairPlan pl = prefix_pair_plan(B, g, Hkv, P, n_ctas, forced_cluster);
   if (pl.total <= 0) return 1;
   const int64_t nb = (P + pr::BN - 1) / pr::BN;
-  const int64_t range = pl.total / (pl.workers / pl.group);  // >= 1
-  return (int)((nb + range - 1) / range + 1);
+  const int64_t G = pl.workers / pl.group;
+  auto group_of = [&](int64_t x) {  // largest c with floor(c * total / G) <= x
+    int64_t c = x * G / pl.total;
+    while (c + 1 < G && (c + 1) * pl.total / G <= x) ++c;
+    while (c > 0 && c * pl.total / G > x) --c;
+    return c;
+  };
+  int64_t most = 1;
+  for (int64_t u = 0; u < pl.total / nb; ++u) most = std::max(most, group_of(u * nb + nb - 1) - group_of(u * nb) + 1);
+  return (int)most;
 }
 
 hydra_status launch_prefix_pair(const PrefixTcArgs &a, int n_ctas, cudaStream_t s) {
