@@ -25,10 +25,11 @@
 // WG) over 64 columns each instead of one warp over 128: half the serial chain per block.
 //
 // Roles per CTA (384 threads):
-//   warp 0      TMA producer (both CTAs): this CTA's Q tile (2 buffers) and K tokens
-//               [64*rank, +64) of each block (4-stage ring); completions counted on the
-//               LEADER's barriers
+//   warp 0      TMA producer (both CTAs): K tokens [64*rank, +64) of each block (4-stage
+//               ring); completions counted on the pair LEADER's barriers
 //   warp 2      TMA producer (both CTAs): V dims [64*rank, +64) of each block (4-stage ring)
+//   warp 3      TMA producer (both CTAs): the Q tile of each item (2 buffers), as early as a
+//               buffer frees
 //   warp 1      TMEM allocation (both CTAs, cta_group::2) and, in the leader only, the single
 //               MMA-issuing thread:  S(0) S(1) | PV_a(n) PV_b(n) S(n+2) | ...  (polls its
 //               barriers: try_wait's suspension cost ~500 cycles of reaction per block)
@@ -78,12 +79,13 @@ constexpr int kPollSleepNs = HYDRA_PAIR_POLL_NS;
 #define HYDRA_PAIR_MMA_WARP 1
 #endif
 constexpr int kMmaWarp = HYDRA_PAIR_MMA_WARP;  // 1 or 3 (warp 1 allocates TMEM either way)
+
   // MMA thread's back-off between barrier probe rounds
 constexpr int O_COL = NSB * BN;             // O accumulator: TMEM columns [384, 512)
 constexpr int OFF_X = OFF_V + NSV * VHALF;  // row max / sum exchange [parity][WG][128 rows]
 constexpr int OFF_BAR = OFF_X + 6 * BM * 4;  // m exchange [WG][128] + epilogue (m, l) [WG][128][2]
-// kf, ke [NSK]; vf, ve [NSV]; qf, qe [NQ]; sf [NSB]; pf [NSB]; ordy; ofree
-constexpr int N_BARS = 2 * NSK + 2 * NSV + 2 * NQ + 2 * NSB + 2;
+// kf, ke [NSK]; vf, ve [NSV]; qf, qe [NQ]; sf [NSB]; pf [NSB]; ordy; ofree; xfree [NQ]
+constexpr int N_BARS = 2 * NSK + 2 * NSV + 3 * NQ + 2 * NSB + 2;
 constexpr int BYTES = OFF_BAR + N_BARS * 8 + 16;
 constexpr int ALLOC = BYTES + 1024;
 static_assert(ALLOC <= 232448, "prefix_pair smem over the 227 KB opt-in limit");
@@ -118,7 +120,7 @@ struct __align__(64) PrefixPairParams {
   long long *trace;  // testing build only: cluster-0 event timestamps [kTraceRows][kTraceN] (tools/pair_trace.py)
   unsigned long long *timer;  // measurement: [0] min CTA start, [1] max CTA end (%globaltimer ns); null = off
   int32_t debug;     // testing build only, timing experiments (invalid results): 4 = no K/V TMA after the ring
-                     // fill, 2 = no softmax (P published as soon as S lands)
+                     // fill, 2 = no softmax (P published as soon as S lands), 8 = no epilogue O stores
 };
 
 namespace pr {
@@ -206,13 +208,13 @@ __global__ void __launch_bounds__(pr::kThreads, 1) prefix_pair_kernel(const __gr
   // as soon as every CTA of this persistent grid is resident -- it then takes the other SMs
   asm volatile("griddepcontrol.launch_dependents;");
   if (P.timer && threadIdx.x == 0) atomicMin(P.timer, gtimer());
-  // diagnostics (testing build): every CTA's %globaltimer at entry / setup done / exit, rows 32..
-  long long *cta_tr = (kTesting && P.trace && blockIdx.x < 1024) ? P.trace + 32 * kTraceN + blockIdx.x * 4 : nullptr;
+  // diagnostics (testing build): every CTA's %globaltimer at entry / setup done / exit, rows 40..
+  long long *cta_tr = (kTesting && P.trace && blockIdx.x < 1024) ? P.trace + 40 * kTraceN + blockIdx.x * 4 : nullptr;
   if (cta_tr && threadIdx.x == 0) cta_tr[0] = (long long)gtimer();
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
   uint64_t *kf = bars, *ke = kf + NSK, *vf = ke + NSK, *ve = vf + NSV, *qf = ve + NSV, *qe = qf + NQ;
-  uint64_t *sf = qe + NQ, *pf = sf + NSB, *ordy = pf + NSB, *ofree = ordy + 1;
+  uint64_t *sf = qe + NQ, *pf = sf + NSB, *ordy = pf + NSB, *ofree = ordy + 1, *xfree = ofree + 1;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + N_BARS);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t crank = ptx::cluster_ctarank();
@@ -238,6 +240,7 @@ __global__ void __launch_bounds__(pr::kThreads, 1) prefix_pair_kernel(const __gr
     for (int i = 0; i < NQ; ++i) {
       ptx::mbar_init(&qf[i], 1);
       ptx::mbar_init(&qe[i], 1);
+      ptx::mbar_init(&xfree[i], 8);  // this CTA's 8 softmax warps: done staging the epilogue in Q buffer i
     }
     for (int i = 0; i < NSB; ++i) {
       ptx::mbar_init(&sf[i], 1);
@@ -254,30 +257,44 @@ __global__ void __launch_bounds__(pr::kThreads, 1) prefix_pair_kernel(const __gr
   const uint32_t tmem = *tmem_slot;
   if (cta_tr && threadIdx.x == 0) cta_tr[1] = (long long)gtimer();
 
-  if (warp == 0 || warp == 2) {
+  if (warp == 3) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
-    // ================= TMA producers (both CTAs): warp 0 Q + K, warp 2 V =================
+    // ================= Q producer (both CTAs): this CTA's 128 stacked query rows per item =================
+    // Its own thread, so the next item's Q is loaded as soon as its buffer is free (the item two
+    // back has finished its score MMAs and its epilogue staging), not behind the current item's
+    // K loads: issued there, it landed ~3 K cycles after the current item's epilogue.
+    if (ptx::elect_one()) {
+      const uint32_t qf0 = ptx::mapa(ptx::smem_u32(qf), lead);
+      uint32_t qi = 0;
+      Iter si;
+      it_begin(P, si);
+      Item it;
+      while (it_next(P, si, it)) {
+        const int qb = qi % NQ;
+        ptx::mbar_wait(&qe[qb], ((qi / NQ) & 1) ^ 1);
+        ptx::mbar_wait(&xfree[qb], ((qi / NQ) & 1) ^ 1);  // and the epilogue staged there is done
+        if (rank == 0) ptx::mbar_arrive_expect_tx(&qf[qb], 2 * QTILE);
+        const int b0 = (int)((it.row0 + BM * rank) / P.g);
+        uint8_t *sQ = smem + OFF_Q + qb * QTILE;
+        ptx::tma_load_4d_pair(sQ, &P.tmQ, qf0 + qb * 8, 0, 0, it.j, b0);
+        ptx::tma_load_4d_pair(sQ + QPANEL, &P.tmQ, qf0 + qb * 8, 64, 0, it.j, b0);
+        if (kTesting && P.trace && blockIdx.x == 0) trace(P.trace, 36, qi);  // Q(qi) issued
+        ++qi;
+      }
+    }
+  } else if (warp == 0 || warp == 2) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
+    // ================= TMA producers (both CTAs): warp 0 K, warp 2 V =================
     // (separate threads, so a K tile is issued as soon as its slot frees, independently of V)
     if (ptx::elect_one()) {
       const bool kq_role = warp == 0;
-      const uint32_t kf0 = ptx::mapa(ptx::smem_u32(kf), lead), vf0 = ptx::mapa(ptx::smem_u32(vf), lead),
-                     qf0 = ptx::mapa(ptx::smem_u32(qf), lead);
-      uint32_t kq = 0, vq = 0, qi = 0;
+      const uint32_t kf0 = ptx::mapa(ptx::smem_u32(kf), lead), vf0 = ptx::mapa(ptx::smem_u32(vf), lead);
+      uint32_t kq = 0, vq = 0;
       long long *tr = (kTesting && P.trace && blockIdx.x == 0 && kq_role) ? P.trace : nullptr;
       Iter si;
       it_begin(P, si);
       Item it;
       while (it_next(P, si, it)) {
-        if (kq_role) {
-          const int qb = qi % NQ;
-          ptx::mbar_wait(&qe[qb], ((qi / NQ) & 1) ^ 1);
-          if (rank == 0) ptx::mbar_arrive_expect_tx(&qf[qb], 2 * QTILE);
-          const int b0 = (int)((it.row0 + BM * rank) / P.g);
-          uint8_t *sQ = smem + OFF_Q + qb * QTILE;
-          ptx::tma_load_4d_pair(sQ, &P.tmQ, qf0 + qb * 8, 0, 0, it.j, b0);
-          ptx::tma_load_4d_pair(sQ + QPANEL, &P.tmQ, qf0 + qb * 8, 64, 0, it.j, b0);
-          ++qi;
-        }
         for (int n = 0; n < it.nblk; ++n) {
           const int t0 = (it.blk_begin + n) * BN;
           if (kTesting && (P.debug & 4) && (kq_role ? kq : vq) >= (uint32_t)NSK) {  // timing experiment only
@@ -554,31 +571,59 @@ __global__ void __launch_bounds__(pr::kThreads, 1) prefix_pair_kernel(const __gr
           trace(P.trace, 23 + 4 * (int)rank + quarter, gs);
       }
       // ---- epilogue: (m, l) of both WGs -> L relative to the final m; O / L (this WG's 64 columns)
+      if (rank == 0 && tr && x == 0) trace(tr, 32, oi);  // rows 32-35: item oi's epilogue (WG a, leader)
       ptx::mbar_wait(ordy, oi & 1);
+      if (rank == 0 && tr && x == 0) trace(tr, 33, oi);
       ptx::tc_fence_after();
       float *xe = xch + 2 * BM;  // [WG][128 rows][2]
       xe[(x * BM + r) * 2] = m_own;
       xe[(x * BM + r) * 2 + 1] = l;
       ptx::named_bar_sync(bar_epi, 64);
+      if (rank == 0 && tr && x == 0) trace(tr, 35, oi);  // (m, l) exchanged
       const float mo = xe[((1 - x) * BM + r) * 2], lo = xe[((1 - x) * BM + r) * 2 + 1];
       const float M = fmaxf(m_own, mo);
       const float L = (m_own == -INFINITY ? 0.f : l * fast_exp2(m_own - M)) + (mo == -INFINITY ? 0.f : lo * fast_exp2(mo - M));
       const float inv = 1.f / L;
-      float *orow = P.o + it.slot * P.o_slot_stride + (seq * P.Hq + h) * HD + 64 * x;
-      const bool skip = kTesting && P.mutate == 3 && blockIdx.x == 0 && quarter == 0 && lane < 4;
+      // O / L through shared memory into coalesced stores: this warp's 32 rows x 32 columns at a
+      // time (XOR-swizzled, 4 KB of the item's Q buffer, free once the item's last PV landed),
+      // then 4 rows x 128 B per store instruction.  Storing straight from the TMEM layout (each
+      // lane 16 B of a different row, rows Hq*512 B apart) made the epilogue ~8 K cycles.
+      const uint64_t my_row =
+          live ? reinterpret_cast<uint64_t>(P.o + it.slot * P.o_slot_stride + (seq * P.Hq + h) * HD + 64 * x) : 0ull;
+      uint32_t *stage = reinterpret_cast<uint32_t *>(smem + OFF_Q + (oi % NQ) * QTILE + (warp - 4) * 4096);
+      const int cg = lane % 8;
 #pragma unroll 1
       for (int c = 0; c < 2; ++c) {
         uint32_t ov[32];
         ptx::tmem_ld32(o_col + 64 * x + 32 * c, ov);
         ptx::tmem_ld_wait();
-        if (live && !skip) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            reinterpret_cast<float4 *>(orow)[c * 8 + i] =
-                make_float4(__uint_as_float(ov[4 * i]) * inv, __uint_as_float(ov[4 * i + 1]) * inv,
-                            __uint_as_float(ov[4 * i + 2]) * inv, __uint_as_float(ov[4 * i + 3]) * inv);
+        if (rank == 0 && tr && x == 0 && c == 0) {
+          asm volatile("" ::"r"(ov[0]), "r"(ov[31]));
+          trace(tr, 31, oi);  // chunk 0 in registers
         }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) stage[lane * 32 + (i ^ lane)] = __float_as_uint(__uint_as_float(ov[i]) * inv);
+        __syncwarp();
+#pragma unroll
+        for (int rw4 = 0; rw4 < 8; ++rw4) {
+          const int rw = rw4 * 4 + lane / 8;
+          const uint64_t base = __shfl_sync(0xffffffffu, my_row, rw);
+          float4 v;
+          v.x = __uint_as_float(stage[rw * 32 + ((cg * 4 + 0) ^ rw)]);
+          v.y = __uint_as_float(stage[rw * 32 + ((cg * 4 + 1) ^ rw)]);
+          v.z = __uint_as_float(stage[rw * 32 + ((cg * 4 + 2) ^ rw)]);
+          v.w = __uint_as_float(stage[rw * 32 + ((cg * 4 + 3) ^ rw)]);
+          // testing build: the parity suite's "unwritten rows" mutation (must fail parity)
+          const bool skip = kTesting && P.mutate == 3 && blockIdx.x == 0 && quarter == 0 && rw4 == 0;
+          if (base && !skip && !(kTesting && (P.debug & 8))) reinterpret_cast<float4 *>(base)[c * 8 + cg] = v;
+        }
+        __syncwarp();
+        if (rank == 0 && tr && x == 0) trace(tr, 38 + c, oi);  // chunk c stored
       }
+      // the staging writes were generic-proxy: order them before the next Q load (TMA) there
+      ptx::fence_proxy_async_smem();
+      ptx::warp_arrive(&xfree[oi % NQ]);
+      if (rank == 0 && tr && x == 0) trace(tr, 34, oi);
       ptx::tc_fence_before();
       ptx::warp_arrive_cluster(of0);
       if (x == 0 && live) {
