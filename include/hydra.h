@@ -353,7 +353,9 @@ HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, i
  *                         split), 4 (64-token blocks, double-buffered scores), 5 (3 + speculative
  *                         running-max softmax)
  *   "prefix_poly"         4 (default): every 4th exp2 pair on the FMA pipe; 0 all exp2 on MUFU; 3 / 8
- *                         (variants 3-6); variant 9: 0 or 4
+ *                         (variants 3-6; variant 9 reads "pair_poly")
+ *   "pair_poly"           CTA-pair kernel: 0 (default) all exp2 on MUFU; 4 every 4th pair on the FMA
+ *                         pipe
  *   "pair_cluster"        CTA-pair kernel: CTA pairs per cluster that share every K/V tile by TMA
  *                         multicast (1, 2 or 4; 0 = automatic: the most that divides the stream-K
  *                         group without idling SMs)

@@ -54,6 +54,7 @@ struct Config {
   int64_t seq_pdl = 1;
   // CTA-pair prefix kernel: pairs per cluster sharing K/V tiles by multicast (0 auto, 1, 2, 4)
   int64_t pair_cluster = 0;
+  int64_t pair_poly = 0;  // all exponentials on the MUFU: measured faster than 4 on the pair kernel (issue/latency-bound)
   // Eq. 5 merged in the kernel epilogues (fused.cuh): 1 in the sequential schedule only (the
   // suffix merges each row after the prefix kernel), 2 also in the SM-partitioned schedule
   // (arrival counters), 0 never: a separate combine launch (default).  Measured
@@ -103,6 +104,7 @@ const Key kKeys[] = {
     {"suffix_cb", &Config::suffix_cb, false},             {"overlap_prefix_ctas", &Config::overlap_prefix_ctas, false},
     {"step_timer", &Config::step_timer, false},          {"seq_pdl", &Config::seq_pdl, false},
     {"pair_cluster", &Config::pair_cluster, false},
+    {"pair_poly", &Config::pair_poly, false},
     {"fuse_combine", &Config::fuse_combine, false},
     {"tc_debug_variant", &Config::tc_debug, true},        {"prefix_trace", &Config::prefix_trace, true},
     {"suffix_trace", &Config::suffix_trace, true},        {"inject_combine_bug", &Config::inject_combine_bug, true},
@@ -122,8 +124,9 @@ extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
     if (k.testing_only && !kTesting)
       return fail(HYDRA_EINVAL, "config key '%s' exists only in the testing build (libhydra_test.so)", key);
     int64_t v = value;
-    if (!strcmp(key, "prefix_poly")) v = (v == 0 || v == 3 || v == 4 || v == 8 || (kTesting && v == -1)) ? v : 4;
+    if (!strcmp(key, "prefix_poly")) v = (v == 0 || v == 3 || v == 4 || v == 8 || (kTesting && (v == -1 || v == 2))) ? v : 4;
     if (!strcmp(key, "pair_cluster")) v = (v == 1 || v == 2 || v == 4) ? v : 0;
+    if (!strcmp(key, "pair_poly")) v = (v == 4 || (kTesting && (v == 2 || v == 3))) ? v : 0;
     if (!strcmp(key, "prefix_variant")) v = (v == 3 || v == 4 || v == 5 || v == 6) ? v : 9;
     if (!strcmp(key, "prefix_stages")) v = (v == 2 ? 2 : 3);
     if (!strcmp(key, "suffix_cb")) v = (v == 1 ? 1 : 2);
@@ -439,6 +442,7 @@ static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, i
     if (fc) a.fc = *fc;
     a.timer = reinterpret_cast<unsigned long long *>((intptr_t)g_cfg.step_timer);
     a.pair_cluster = (int32_t)g_cfg.pair_cluster;
+    a.pair_poly = (int32_t)g_cfg.pair_poly;
     hydra_status st;
     if (kind == PK_TC2) {
       // stream-K pieces leave some slots of a row unwritten: mark every slot empty first (the

@@ -156,6 +156,7 @@ struct PrefixTcArgs {
   int32_t stages;  // K/V pipeline stages: 2 (160 KB smem, leaves room for co-resident suffix CTAs) or 3
   unsigned long long *timer = nullptr;  // measurement: [0] min CTA start, [1] max CTA end (ns); persistent kernels
   int32_t pair_cluster = 0;  // CTA-pair kernel: pairs per cluster (0 = automatic)
+  int32_t pair_poly = 0;     // CTA-pair kernel: every k-th exp2 pair on the FMA pipe (0 = all MUFU)
 };
 bool prefix_tc_supported(const hydra_heads *h);
 hydra_status launch_prefix_tc(const PrefixTcArgs &a, cudaStream_t s);

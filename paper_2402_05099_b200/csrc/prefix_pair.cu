@@ -362,6 +362,11 @@ __global__ void __launch_bounds__(pr::kThreads, 1) prefix_pair_kernel(const __gr
         trace(tr, 21, gs);
         ptx::tc_fence_after();
         const uint32_t qa = ptx::smem_u32(smem + OFF_Q + qb * QTILE), ka = ptx::smem_u32(smem + OFF_K + ks * KHALF);
+#ifndef HYDRA_PAIR_DUP_S
+#define HYDRA_PAIR_DUP_S 1
+#endif
+#pragma unroll
+        for (int rep = 0; rep < HYDRA_PAIR_DUP_S; ++rep)  // diagnostics: > 1 re-issues identical score MMAs
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk)
           ptx::mma2_ss(tmem + sb * BN, ptx::smem_desc_sw128(qa + (kk / 4) * QPANEL + (kk % 4) * 32, 16, 1024),
@@ -659,9 +664,21 @@ template <int kPoly, int kC>
 static const void *pair_fn() {
   return reinterpret_cast<const void *>(prefix_pair_kernel<kPoly, kC>);
 }
+template <int kPoly>
+static const void *pair_fn_c(int kC) {
+  return kC == 4 ? pair_fn<kPoly, 4>() : kC == 2 ? pair_fn<kPoly, 2>() : pair_fn<kPoly, 1>();
+}
+// poly (config key pair_poly): every poly-th exponential pair on the FMA pipe (0 = all on the
+// MUFU).  The release build carries 0 (default) and 4; the testing build also 2 and 3.  Measured
+// (profiles/r2f_poly_ab.jsonl): 0 beats 4 by 1-2.5 % on every shape, 3 and 2 are slower still --
+// this kernel's softmax is bound by its latency chain and issue, not by MUFU throughput.
+static bool pair_poly_ok(int poly) { return poly == 0 || poly == 4 || (kTesting && (poly == 2 || poly == 3)); }
 static const void *pair_kernel(int poly, int kC) {
-  if (poly == 4) return kC == 4 ? pair_fn<4, 4>() : kC == 2 ? pair_fn<4, 2>() : pair_fn<4, 1>();
-  return kC == 4 ? pair_fn<0, 4>() : kC == 2 ? pair_fn<0, 2>() : pair_fn<0, 1>();
+#ifdef HYDRA_TESTING
+  if (poly == 2) return pair_fn_c<2>(kC);
+  if (poly == 3) return pair_fn_c<3>(kC);
+#endif
+  return poly == 4 ? pair_fn_c<4>(kC) : pair_fn_c<0>(kC);
 }
 
 // CTA pairs that can be resident at once in clusters of kC pairs (cached per device and kC).
@@ -746,8 +763,8 @@ int prefix_pair_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int forc
 }
 
 hydra_status launch_prefix_pair(const PrefixTcArgs &a, int n_ctas, cudaStream_t s) {
-  const int poly = a.poly_every;
-  if (a.tasks || !prefix_pair_supported(a.g) || !(poly == 0 || poly == 4)) return HYDRA_EINVAL;
+  const int poly = a.pair_poly;
+  if (a.tasks || !prefix_pair_supported(a.g) || !pair_poly_ok(poly)) return HYDRA_EINVAL;
   const PairPlan pl = prefix_pair_plan(a.B, a.g, a.Hkv, a.P, n_ctas, a.pair_cluster);
   const void *fn = pair_kernel(poly, pl.cluster);
   if (ensure_smem_attr(fn, pr::ALLOC) != cudaSuccess) return HYDRA_ECUDA;
@@ -801,15 +818,7 @@ hydra_status launch_prefix_pair(const PrefixTcArgs &a, int n_ctas, cudaStream_t 
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e;
-  if (poly == 4)
-    e = pl.cluster == 4   ? cudaLaunchKernelEx(&cfg, prefix_pair_kernel<4, 4>, P)
-        : pl.cluster == 2 ? cudaLaunchKernelEx(&cfg, prefix_pair_kernel<4, 2>, P)
-                          : cudaLaunchKernelEx(&cfg, prefix_pair_kernel<4, 1>, P);
-  else
-    e = pl.cluster == 4   ? cudaLaunchKernelEx(&cfg, prefix_pair_kernel<0, 4>, P)
-        : pl.cluster == 2 ? cudaLaunchKernelEx(&cfg, prefix_pair_kernel<0, 2>, P)
-                          : cudaLaunchKernelEx(&cfg, prefix_pair_kernel<0, 1>, P);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, reinterpret_cast<void (*)(PrefixPairParams)>(const_cast<void *>(fn)), P);
   return e == cudaSuccess ? HYDRA_OK : HYDRA_ECUDA;
 }
 

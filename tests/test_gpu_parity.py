@@ -27,7 +27,7 @@ def _reset_config():
             "suffix_ctas", "overlap_prefix_ctas", "pair_cluster")
     for k in keys:
         hydra.set_config(k, 0)
-    defaults = {"prefix_variant": 9, "suffix_cb": 2, "prefix_poly": 4, "fuse_combine": 0}  # the library defaults
+    defaults = {"prefix_variant": 9, "suffix_cb": 2, "prefix_poly": 4, "pair_poly": 0, "fuse_combine": 0}  # the library defaults
     for k, v in defaults.items():
         hydra.set_config(k, v)
     yield
@@ -111,6 +111,7 @@ def test_prefix_tc2_growing_max(variant, poly, steep):
     hydra.set_config("prefix_impl", 3)
     hydra.set_config("prefix_variant", variant)
     hydra.set_config("prefix_poly", poly)
+    hydra.set_config("pair_poly", poly)
     pb = synth.make_problem(300, 8, 2, 128, 2000, 1, dtype="bf16", dist="mixed", seed=11)
     ramp = (1.0 + steep * np.arange(pb.P, dtype=np.float64) / pb.P)[:, None, None]
     pb.pk = synth.gen.f32_to_bf16_bits((pb.f32("pk") * ramp).astype(np.float32))
@@ -120,6 +121,7 @@ def test_prefix_tc2_growing_max(variant, poly, steep):
         torch.cuda.synchronize()
     finally:
         hydra.set_config("prefix_poly", 4)
+        hydra.set_config("pair_poly", 0)
     ref, lref = oracle.prefix_only(pb)
     assert_parity(o, ref, lse, lref, what=f"prefix growing max v{variant} poly{poly} x{steep}")
 

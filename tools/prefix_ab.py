@@ -1,6 +1,6 @@
 """Prefix kernel alone: time per launch and TFLOP/s for prefix_variant values on the C3 / C4 / C6
 prefix shapes (diagnostics).   python tools/prefix_ab.py [variants] [shapes]
-    variants: comma list (default 6,9); shapes: c3,c4,c6,c2 (default all)"""
+    variants: comma list (default 6,9); "9p2" = variant 9 with pair_poly 2 (testing build for 2 / 3); shapes: c3,c4,c6,c2 (default all)"""
 import json
 import os
 import sys
@@ -26,8 +26,11 @@ for name in shapes:
     flops = 4.0 * B * Hq * P * 128
     ref = None
     for v in variants:
+        vv, _, poly = v.partition("p")
         hydra.set_config("prefix_impl", 2 if v == "t1" else 3)
-        hydra.set_config("prefix_variant", 9 if v == "t1" else int(v))
+        hydra.set_config("prefix_variant", 9 if v == "t1" else int(vv))
+        hydra.set_config("prefix_poly", int(poly) if poly else 4)
+        hydra.set_config("pair_poly", int(poly) if poly else 0)
         hydra.set_config("prefix_ctas", ctas)
         hydra.set_config("pair_cluster", int(os.environ.get("CLUSTER", 0)))
         fn = lambda: hydra.prefix_attn(q, pk, pv, workspace=ws)
