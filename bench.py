@@ -221,12 +221,31 @@ def mark_shared(line):
     return line
 
 
+class L2Flush:
+    """Evicts the step's inputs from L2 between timed steps: writes a 2 x L2 buffer, then reads
+    another 2 x L2 buffer.  The read matters: after a write-only flush L2 holds ~126 MB of DIRTY
+    lines, and the timed step that follows pays their write-back to HBM (measured: a fixed
+    ~15-19 us on every short step, e.g. the C6 suffix, tools/suffix_shapes_ab.py); after the
+    read L2 holds clean, unrelated lines only."""
+
+    DESC = "L2 flushed before every timed step (2 x 126 MB written, then another 2 x 126 MB read: no dirty line left)"
+
+    def __init__(self, torch, dev, nbytes=None):
+        n = nbytes or 2 * L2_BYTES
+        self.w = torch.empty(n, dtype=torch.uint8, device=dev)
+        self.r = torch.zeros(n, dtype=torch.uint8, device=dev)
+
+    def __call__(self):
+        self.w.zero_()
+        self.r.sum()
+
+
 def l2_flush_buffer(torch, dev, input_bytes):
-    """A buffer of 2x the L2 to overwrite between timed steps when the step's inputs would
-    otherwise stay L2-resident (e.g. a rank's shard at 8 GPUs); None when inputs > 2x L2."""
+    """An L2Flush to run between timed steps when the step's inputs would otherwise stay
+    L2-resident (e.g. a rank's shard at 8 GPUs); None when inputs > 2x L2."""
     if input_bytes >= 2 * L2_BYTES:
         return None
-    return torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
+    return L2Flush(torch, dev)
 
 
 # per-step statistics of the last timed_steps call (the median next to the mean it returns)
@@ -236,8 +255,8 @@ LAST_TIMING = {}
 def timed_steps(torch, run, k, flush):
     """Device time of k steps (ms per step, the mean).  Without `flush`: k back-to-back steps
     between the first and the last of k+1 events (an event before every step also gives each
-    step's own time: median / min / max in LAST_TIMING).  With `flush`: the buffer is
-    overwritten before every step and only the steps themselves are timed (one event pair
+    step's own time: median / min / max in LAST_TIMING).  With `flush` (an L2Flush): L2 is
+    flushed before every step and only the steps themselves are timed (one event pair
     per step, summed)."""
     if flush is None:
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(k + 1)]
@@ -251,7 +270,7 @@ def timed_steps(torch, run, k, flush):
         return evs[0].elapsed_time(evs[-1]) / k
     evs = []
     for _ in range(k):
-        flush.zero_()
+        flush()
         a, c = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         run()
@@ -477,7 +496,7 @@ def run_seqsplit(args, cfg):
                                   f"({plan.row_bytes} B per row), merged with the suffix part in one combine",
                       "exchange_bytes_sent_per_rank": plan.exchange_bytes(), "cuda_graph": graphed,
                       "l2": ("no flush: %.2f GB of inputs per rank > 2 x 126 MB L2" % (in_bytes / 1e9)) if flush is None
-                      else "L2 flushed (256 MB write) before every timed step: %.3f GB of inputs per rank" % (in_bytes / 1e9)}
+                      else L2Flush.DESC + ": %.3f GB of inputs per rank" % (in_bytes / 1e9)}
     line["roofline"] = {"bound": "tensor", "kernel": prefix_kernel_name(hydra, Hq // Hkv) + ", this rank's prefix shard",
                         "achieved": round(flops / (ms_pre * 1e-3) / 1e12, 1), "peak": tc, "unit": "TFLOP/s",
                         "frac": round(flops / (ms_pre * 1e-3) / 1e12 / tc, 4), "traffic": None,
@@ -497,8 +516,8 @@ def run_seqsplit(args, cfg):
 
 def run_grid(args, cfg):
     """NEXT-1: speedup of Hydragen attention over per-sequence attention on the paper's
-    microbenchmark shape, App. D.2 protocol: CUDA graph per call, the L2 flushed (a 2 x L2
-    write) before every timed replay, mean and median over the timed replays."""
+    microbenchmark shape, App. D.2 protocol: CUDA graph per call, the L2 flushed (L2Flush: a
+    2 x L2 write, then a 2 x L2 read) before every timed replay, mean and median over the timed replays."""
     import numpy as np
     import torch
 
@@ -511,7 +530,7 @@ def run_grid(args, cfg):
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
     torch.cuda.set_device(dev)
     Hq, Hkv, d = cfg["Hq"], cfg["Hkv"], cfg["d"]
-    flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
+    flush = L2Flush(torch, dev)
     iters, warm = max(5, args.steps), max(3, args.warmup)
 
     def graph_times(fn):
@@ -528,7 +547,7 @@ def run_grid(args, cfg):
             g.replay()
         evs = []
         for _ in range(iters):
-            flush.zero_()
+            flush()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             g.replay()
@@ -565,7 +584,7 @@ def run_grid(args, cfg):
                         "steps": iters, "warmup": warm, "dtype": "bf16",
                         "data": "synthetic (seeded PCG64 N(0,1) K/V rounded to bf16, 'mixed' needle queries)",
                         "config": {"workload": "grid", "B": B, "Hq": Hq, "Hkv": Hkv, "d": d, "prefix_len": P,
-                                   "suffix_len": S, "l2": "flushed (2 x 126 MB write) before every timed replay"},
+                                   "suffix_len": S, "l2": L2Flush.DESC},
                         "hydragen_ms": {"mean": round(h_mean, 5), "median": round(h_med, 5)},
                         "per_sequence_ms": {"mean": round(b_mean, 5), "median": round(b_med, 5)},
                         "speedup_median": round(b_med / h_med, 3),
@@ -729,7 +748,7 @@ def run_flat(args, cfg):
     step_stats = {k: (round(v, 5) if isinstance(v, float) else v) for k, v in LAST_TIMING.items()}
     # the same step with L2 flushed (256 MB written) before every timed step: the inputs
     # already exceed L2, so this should match the back-to-back figure
-    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_buf = L2Flush(torch, dev)
     ms_flushed = timed_steps(torch, g_main.replay, max(10, min(50, args.steps // 4)), flush_buf)
     del flush_buf
 
@@ -889,7 +908,7 @@ def run_flat(args, cfg):
                    "prefix_len": P, "suffix_len": S, "parallelism": f"kv-head shard x{world}" if world > 1 else "1 GPU",
                    "heads_per_gpu": Hq_r, "overlap_prefix_suffix": overlap,
                    "l2": (f"no flush: {in_bytes / 1e9:.2f} GB of inputs per step > 2 x 126 MB L2" if flush is None else
-                          f"L2 flushed (256 MB write) before every timed step: {in_bytes / 1e9:.3f} GB of inputs per rank"),
+                          L2Flush.DESC + f": {in_bytes / 1e9:.3f} GB of inputs per rank"),
                    "timing": "CUDA graph of one step, CUDA events over K replays, max over ranks"},
         "roofline": {"bound": "hbm", "kernel": ("suffix_tc_kernel (tensor-core GEMV, all SMs; GQA g = %d; the sequential schedule's suffix)" % (Hq // Hkv)
                                                 if Hq // Hkv >= 2 else
@@ -915,8 +934,8 @@ def run_flat(args, cfg):
         "step_roofline": {"t_roof_ms": round(t_roof * 1e3, 5), "frac": round(t_roof * 1e3 / ms, 4),
                           "ms_sequential": round(ms_seq, 5), "ms_overlap": round(ms_over, 5)},
         "step_time": dict(step_stats, mean_ms=round(ms, 5), ms_l2_flushed=round(ms_flushed, 5),
-                          note="per-step events inside the back-to-back timed loop; ms_l2_flushed: 256 MB "
-                               "written before each of its steps, only the steps timed"),
+                          note="per-step events inside the back-to-back timed loop; ms_l2_flushed: L2Flush "
+                               "before each of its steps, only the steps timed"),
         "clocks": clocks,
         # prefix, suffix, combine (+ the -inf fill of the partial slots, which the CTA-pair prefix
         # kernel does itself)

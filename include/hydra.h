@@ -366,7 +366,8 @@ HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, i
  *                         suffix start, end; preset UINT64_MAX, 0, UINT64_MAX, 0)
  *   "prefix_splits"       KV splits of the one-tile / SIMT prefix kernels
  *   "prefix_ctas"         CTAs of the persistent prefix kernel
- *   "suffix_impl"         1 SIMT split-K GEMV, 2 persistent TMA-fed tensor-core kernel
+ *   "suffix_impl"         1 SIMT split-K GEMV, 2 persistent TMA-fed tensor-core kernel, 3 the short-suffix
+ *                         tensor-core kernel (g >= 2, S_cap <= 256; 3 CTAs per SM; automatic there)
  *   "suffix_splits"       KV splits of the suffix kernels (tensor-core kernel: split-K over
  *                         tokens, only when set; SIMT kernel: automatic when 0)
  *   "suffix_ctas"         CTAs of the persistent suffix kernel

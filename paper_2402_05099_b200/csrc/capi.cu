@@ -207,7 +207,7 @@ static int heads_per_cta(int g) {
 // B = 512: 67 vs 96 us; g = 16: 108 vs 357-410 us; MHA (g = 1): 0.83 vs 0.79 ms at C3.
 static bool use_suffix_tc(const hydra_heads *h, int64_t B, int64_t S_cap, bool overlap = false) {
   if (g_cfg.suffix_impl == 1 || S_cap <= 0 || !suffix_tc_supported(h)) return false;
-  if (g_cfg.suffix_impl == 2) return true;
+  if (g_cfg.suffix_impl == 2 || g_cfg.suffix_impl == 3) return true;
   const int64_t items = B * h->num_kv_heads, sms = device_sm_count();
   if (overlap) return items >= 2 * sms;
   // (also with fewer items than SMs: 64-128 items of 1-8K-token suffixes, 62-64 us against
@@ -527,6 +527,14 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
       a.bt_stride = pg->bt_stride;
       a.n_pages = pg->n_pages;
       a.page_size = pg->page_size;
+    }
+    // Short grouped-query suffixes (<= 2 blocks): the three-CTAs-per-SM kernel, on the full chip
+    // (auto) or on request (suffix_impl 3).  Measured (tools/suffix_shapes_ab.py): C6's g = 8
+    // 128-token suffixes 26.8 -> see DESIGN.md §7; C4's g = 4.
+    const bool short_ok = tc_ctas == 0 && !pg && !fc && splits <= 1 && suffix_short_supported(g, S_cap);
+    if (short_ok && (g_cfg.suffix_impl == 3 || (g_cfg.suffix_impl == 0 && g_cfg.suffix_ctas == 0))) {
+      hydra_status st = launch_suffix_short(a, (int)g_cfg.suffix_ctas, s);
+      return st == HYDRA_OK ? st : cuda_fail("suffix (short) tcgen05 launch");
     }
     const int ctas = tc_ctas > 0 ? tc_ctas : (g_cfg.suffix_ctas > 0 ? (int)g_cfg.suffix_ctas : device_sm_count());
     hydra_status st = launch_suffix_tc(a, ctas, s);

@@ -210,6 +210,10 @@ struct SuffixTcArgs {
 };
 bool suffix_tc_supported(const hydra_heads *h);
 hydra_status launch_suffix_tc(const SuffixTcArgs &a, int n_ctas, cudaStream_t s);
+// short grouped-query suffixes (S_cap <= 256, g in {2, 4, 8, 16}, contiguous, unsplit, unfused):
+// three small CTAs per SM (suffix_short.cu); n_ctas 0 = 3 x SMs
+bool suffix_short_supported(int g, int64_t S_cap);
+hydra_status launch_suffix_short(const SuffixTcArgs &a, int n_ctas, cudaStream_t s);
 hydra_status launch_append_kv(const void *k_new, const void *v_new, int64_t nb, int64_t nh, void *sk, void *sv,
                               int64_t s_sb, int64_t s_st, int64_t s_sh, int64_t S_cap, int32_t Hkv, int32_t d,
                               size_t es, int64_t B, int32_t *lens, cudaStream_t s,

@@ -262,6 +262,9 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
   constexpr uint32_t O_COL = NSP * CB * NQ;  // O^T buffers start after the S^T round slots
   extern __shared__ uint8_t smem_raw[];
   if (P.timer && threadIdx.x == 0) atomicMin(P.timer, gtimer());
+  // diagnostics (testing build): every CTA's %globaltimer at entry / setup done / exit, rows 13-15
+  long long *cta_tr = (kTesting && P.trace && blockIdx.x < kTraceN) ? P.trace + 13 * kTraceN + blockIdx.x : nullptr;
+  if (cta_tr && threadIdx.x == 0) cta_tr[0] = (long long)gtimer();
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
   uint64_t *k_full = bars, *k_empty = bars + NS, *v_full = bars + 2 * NS, *v_empty = bars + 3 * NS;
@@ -314,6 +317,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (cta_tr && threadIdx.x == 0) cta_tr[kTraceN] = (long long)gtimer();
 
   if (warp == 13) {
     // ================= paged cache: block-table entries into the page-id ring =================
@@ -714,6 +718,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
     ptx::tmem_dealloc<TMEM_COLS>(tmem);
   }
   if (P.timer && threadIdx.x == 0) atomicMax(P.timer + 1, gtimer());
+  if (cta_tr && threadIdx.x == 0) cta_tr[2 * kTraceN] = (long long)gtimer();
   // Launched as a programmatic dependent of the prefix kernel (SM-partitioned schedule on one
   // stream): the grid completes only after the prefix grid has, so the combine that follows in
   // the stream sees both.  Without a programmatic prerequisite this returns at once.

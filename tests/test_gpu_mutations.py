@@ -10,6 +10,7 @@ caught the mutation:
   skip_prefix_store  persistent tcgen05 prefix kernel: CTA 0 skips one 4-row store group
   skip_pair_store    CTA-pair prefix kernel: worker 0 skips the stores of 4 rows
   skip_suffix_store  tensor-core suffix kernel: CTA 0 skips head 0's row of its first item
+  skip_short_store   short-suffix kernel (suffix_short.cu): the same skipped row
   clean              no mutation: the same calls must pass (control)
 Also: the testing build's device check of the lens precondition counts lens[b] > S_cap and
 lens[b] < 0 (hydra_debug_lens_violations)."""
@@ -57,6 +58,14 @@ def run(case):
         t = problem_to(pb, DEV)
         out, lse = H.prefix_attn(t["q"], t["pk"], t["pv"])
         ref, lref = oracle.prefix_only(pb)
+    elif case in ("clean_short", "skip_short_store"):
+        hydra.set_config("suffix_impl", 3)
+        if case == "skip_short_store":
+            hydra.set_config("mutate", 2)
+        pb = synth.make_problem(40, 8, 2, 128, 0, 200, dtype="bf16", dist="mixed", seed=7)
+        t = problem_to(pb, DEV)
+        out, lse = H.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
+        ref, lref = oracle.suffix_only(pb)
     else:
         hydra.set_config("suffix_impl", 2)
         if case == "skip_suffix_store":
@@ -73,7 +82,7 @@ def run(case):
         return "caught: " + str(e)[:80]
 
 for case in ("clean_composite", "combine_bug", "clean_prefix", "skip_prefix_store", "clean_pair", "skip_pair_store",
-             "clean_suffix", "skip_suffix_store"):
+             "clean_suffix", "skip_suffix_store", "clean_short", "skip_short_store"):
     res[case] = run(case)
 
 # lens precondition: device check in the testing build
@@ -99,12 +108,13 @@ def results():
     return json.loads(line[0][7:])
 
 
-@pytest.mark.parametrize("case", ["clean_composite", "clean_prefix", "clean_pair", "clean_suffix"])
+@pytest.mark.parametrize("case", ["clean_composite", "clean_prefix", "clean_pair", "clean_suffix", "clean_short"])
 def test_unmutated_testing_build_passes(results, case):
     assert results[case] == "pass", results[case]
 
 
-@pytest.mark.parametrize("case", ["combine_bug", "skip_prefix_store", "skip_pair_store", "skip_suffix_store"])
+@pytest.mark.parametrize("case", ["combine_bug", "skip_prefix_store", "skip_pair_store", "skip_suffix_store",
+                                  "skip_short_store"])
 def test_mutation_is_caught(results, case):
     assert results[case].startswith("caught"), f"{case} passed the parity gate"
 

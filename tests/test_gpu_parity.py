@@ -327,6 +327,61 @@ def test_suffix_tc_ragged_repeat():
         assert_parity(o, ref, lse, lref, what="suffix tc ragged repeat")
 
 
+@pytest.mark.parametrize("g", [2, 4, 8])
+@pytest.mark.parametrize("ctas", [0, 1, 7])
+def test_suffix_short_ragged(g, ctas):
+    """Short-suffix kernel (suffix_short.cu, S_cap <= 256): ragged lens incl. 0, 1, 127, 128,
+    129 and 256 with NaN-poisoned padding (V rows past lens[b] must be zeroed), every GQA width
+    it takes, a grid of all resident CTAs (0), one CTA walking every item, and 7 (items dealt
+    unevenly).  Same arithmetic as the persistent tensor-core kernel with 2-block rounds: the
+    two agree bit for bit."""
+    hydra.set_config("suffix_impl", 3)
+    hydra.set_config("suffix_ctas", ctas)
+    lens = [0, 1, 127, 128, 129, 255, 256, 200, 17, 0, 64, 128, 1]
+    Hkv = 2
+    pb = synth.make_problem(len(lens), g * Hkv, Hkv, 128, 0, 256, lens=lens, dtype="bf16", dist="boundary", seed=40 + g)
+    t = problem_to(pb, DEV)
+    o, lse = H.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
+    torch.cuda.synchronize()
+    ref, lref = oracle.suffix_only(pb)
+    assert_parity(o, ref, lse, lref, what=f"suffix short g={g} ctas={ctas}")
+    hydra.set_config("suffix_impl", 2)
+    hydra.set_config("suffix_ctas", 0)
+    o2, lse2 = H.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
+    torch.cuda.synchronize()
+    assert torch.equal(o, o2) and torch.equal(lse, lse2), (o - o2).abs().max()
+
+
+def test_suffix_short_two_block_jump_and_repeat():
+    """Scores that jump between the two blocks of an item (the round max must cover both),
+    many items (3 CTAs per SM, several items per CTA), repeated 6x on NaN-filled outputs."""
+    hydra.set_config("suffix_impl", 3)
+    rng = np.random.default_rng(5)
+    lens = rng.integers(0, 257, 700)
+    pb = synth.make_problem(700, 32, 4, 128, 0, 256, lens=lens, dtype="bf16", dist="mixed", seed=44)
+    ramp = np.ones((pb.S_cap, 1, 1))
+    ramp[128:] = 9.0  # block 2 of every item scores ~9x higher
+    pb.sk = synth.gen.f32_to_bf16_bits((pb.f32("sk") * ramp[None]).astype(np.float32))
+    t = problem_to(pb, DEV)
+    ref, lref = oracle.suffix_only(pb)
+    for _ in range(6):
+        o, lse = H.suffix_attn(t["q"], t["sk"], t["sv"], t["lens"])
+        torch.cuda.synchronize()
+        assert_parity(o, ref, lse, lref, what="suffix short two-block jump")
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,P,S", [(256, 32, 4, 1500, 128), (96, 32, 8, 700, 200), (50, 16, 8, 300, 40)])
+def test_composite_short_suffix_auto(B, Hq, Hkv, P, S):
+    """The automatic choice (suffix_impl 0) routes short GQA suffixes to the short kernel, in
+    the sequential schedule as a programmatic dependent of the prefix: whole step vs oracle."""
+    rng = np.random.default_rng(B)
+    lens = rng.integers(0, S + 1, B)
+    pb = synth.make_problem(B, Hq, Hkv, 128, P, S, lens=lens, dtype="bf16", dist="mixed", seed=45)
+    out, lse = run_flat(pb)
+    ref, lref = oracle.flat_attention(pb)
+    assert_parity(out, ref, lse, lref, what=f"short-suffix composite B={B} g={Hq // Hkv}")
+
+
 def test_composite_f32_output_is_tighter():
     pb = synth.make_problem(16, 8, 2, 128, 600, 50, dtype="bf16", dist="mixed", seed=9)
     out, lse = run_flat(pb, out_dtype=torch.float32)

@@ -24,12 +24,30 @@ if PAGED:
 else:
     call = lambda: hydra.suffix_attn(q, sk, sv, lens)
 N = 1024
-tr = torch.zeros(13, N, dtype=torch.int64, device=dev)
+tr = torch.zeros(16, N, dtype=torch.int64, device=dev)
 hydra.set_config("suffix_impl", 2); hydra.set_config("suffix_ctas", ctas); hydra.set_config("suffix_cb", cb)
 hydra.set_config("tc_debug_variant", int(os.environ.get("DEBUG", 0)))
 for _ in range(2):
     call()
 torch.cuda.synchronize()
+gr = torch.cuda.CUDAGraph()
+st = torch.cuda.Stream(); st.wait_stream(torch.cuda.current_stream())
+with torch.cuda.stream(st):
+    call()
+torch.cuda.current_stream().wait_stream(st)
+with torch.cuda.graph(gr):
+    call()
+for _ in range(3):
+    gr.replay()
+ga, gb_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+ga.record()
+for _ in range(20):
+    gr.replay()
+gb_.record()
+torch.cuda.synchronize()
+gms = ga.elapsed_time(gb_) / 20
+print(f"graph-replayed (no trace): {gms * 1e3:.1f} us = {2 * B * S * HKV * 256 / gms / 1e9:.0f} GB/s")
+del gr
 hydra.set_config("suffix_trace", tr.data_ptr())
 e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
 e0.record(); call(); e1.record()
@@ -38,6 +56,12 @@ hydra.set_config("suffix_trace", 0); hydra.set_config("tc_debug_variant", 0); hy
 ms = e0.elapsed_time(e1)
 print(f"cb={cb} ctas={ctas} ms={ms:.3f} GB/s/SM={2*B*S*HKV*256/ms/1e6/ctas:.1f}")
 t = tr.cpu().numpy().astype(np.float64)
+nc = min(ctas, N)
+ct = t[13:16, :nc]
+t0 = ct[0].min()
+print("CTA spans (us from the first CTA entry): entry max %.2f, setup done median %.2f max %.2f, exit min %.2f median %.2f max %.2f"
+      % ((ct[0].max() - t0) / 1e3, np.median(ct[1] - t0) / 1e3, (ct[1].max() - t0) / 1e3, (ct[2].min() - t0) / 1e3,
+         np.median(ct[2] - t0) / 1e3, (ct[2].max() - t0) / 1e3))
 names = ["sm_wait0", "s_full", "ld", "max", "p_arrive", "epi0", "epi1", "mma_S", "mma_PV", "tma_K", "tma_V"]
 lo, hi = 50, 400  # steady-state window (rounds / blocks)
 def med(x): return float(np.median(x)) if len(x) else float("nan")
