@@ -735,6 +735,7 @@ def run_flat(args, cfg):
         hydra.set_config("overlap_prefix_ctas", args.overlap_k)
     g_over = capture(lambda: step(True))
     k_over = int(hydra.get_config("last_overlap_k"))  # SM split chosen for the overlapped step
+    ov_simt = bool(hydra.get_config("last_overlap_simt"))  # ... with the SIMT suffix as the prefix's dependent
     g_seq = capture(lambda: step(False))
     probe = max(3, min(20, args.steps // 5))
     ms_over = time_graph(g_over, probe, 2)
@@ -857,7 +858,17 @@ def run_flat(args, cfg):
     ms_suf = time_graph(g_suf, kk, 3)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     in_step = None
-    if overlap and k_over > 0:
+    if overlap and k_over > 0 and ov_simt:
+        # prefix on k persistent CTAs, the SIMT suffix (full grid) its programmatic dependent: the
+        # dominant kernel stays the SIMT suffix (timed inside the step by its span below)
+        try:
+            hydra.set_config("prefix_ctas", k_over)
+            ms_pre_k = time_graph(capture(lambda: hydra.prefix_attn(q, pk, pv, workspace=ws)), kk, 3)
+        finally:
+            hydra.set_config("prefix_ctas", 0)
+        in_step = {"prefix_ctas": k_over, "suffix": "SIMT kernel, full grid, programmatic dependent of the prefix",
+                   "ms_prefix": round(ms_pre_k, 5), "ms_suffix": round(ms_suf, 5)}
+    elif overlap and k_over > 0:
         # the kernels as the overlapped step runs them: prefix on k SMs || tensor-core suffix on
         # the other SMs (timed one at a time, so without the other's HBM/L2/power interference)
         try:
@@ -907,6 +918,9 @@ def run_flat(args, cfg):
         "config": {"workload": args.config, "description": cfg["name"], "B": B, "Hq": Hq, "Hkv": Hkv, "d": d,
                    "prefix_len": P, "suffix_len": S, "parallelism": f"kv-head shard x{world}" if world > 1 else "1 GPU",
                    "heads_per_gpu": Hq_r, "overlap_prefix_suffix": overlap,
+                   "schedule": ("sequential" if not (overlap and k_over > 0) else
+                                "prefix on %d CTAs, SIMT suffix its programmatic dependent (full grid)" % k_over if ov_simt else
+                                "prefix on %d CTAs || tensor-core suffix on the other SMs" % k_over),
                    "l2": (f"no flush: {in_bytes / 1e9:.2f} GB of inputs per step > 2 x 126 MB L2" if flush is None else
                           L2Flush.DESC + f": {in_bytes / 1e9:.3f} GB of inputs per rank"),
                    "timing": "CUDA graph of one step, CUDA events over K replays, max over ranks"},
@@ -950,7 +964,7 @@ def run_flat(args, cfg):
         j = clocks["power_w"] * ms * 1e-3
         line["energy"] = {"board_power_w": clocks["power_w"], "joules_per_step": round(j, 5),
                           "queries_per_joule": round(B / j, 1), "samples": clocks["samples"]}
-    if in_step:
+    if in_step and not ov_simt:
         # the overlapped step's dominant kernel: the tensor-core suffix on (SMs - k) SMs
         b_k = suffix_bytes / (in_step["ms_suffix"] * 1e-3) / 1e9
         f_k = prefix_flops / (in_step["ms_prefix"] * 1e-3) / 1e12
@@ -969,6 +983,8 @@ def run_flat(args, cfg):
             "timed": "alone on its SM share (CUDA graph, events), after the step loop",
             "prefix_tflops_on_k_sms": round(f_k, 1), "prefix_launch_ms_on_k_sms": in_step["ms_prefix"]}
 
+    if in_step and ov_simt:
+        line["overlap_parts_alone"] = in_step
     # the dominant kernel's figure as it runs inside the step (events on its own stream);
     # the kernel timed alone stays as `alone`
     suf_in_gbs = suffix_bytes / (ms_suf_in * 1e-3) / 1e9

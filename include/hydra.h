@@ -359,6 +359,9 @@ HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, i
  *   "pair_cluster"        CTA-pair kernel: CTA pairs per cluster that share every K/V tile by TMA
  *                         multicast (1, 2 or 4; 0 = automatic: the most that divides the stream-K
  *                         group without idling SMs)
+ *   "overlap_simt"        0 (default) automatic, 1 force, 2 never: hydra_attn's SM-partitioned schedule with
+ *                         the SIMT suffix (MHA) as the prefix's programmatic dependent over its full grid,
+ *                         the prefix on >= 32 persistent CTAs (taken when the prefix is light)
  *   "seq_pdl"             1 (default): in the sequential schedule the tensor-core suffix is a
  *                         programmatic dependent launch of the prefix (starts in its tail); 0 off
  *   "step_timer"          measurement: device address of 4 x u64 the persistent prefix / suffix
@@ -391,7 +394,8 @@ HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, i
  *   "mutate"              1: the persistent prefix kernel's CTA 0 skips one 4-row store group of
  *                         its epilogues; 2: the tensor-core suffix's CTA 0 skips head 0's output
  *                         row of its first item (unwritten rows the parity suite must catch)
- * hydra_get_config also answers "last_overlap_k" (prefix CTAs of this thread's last hydra_attn /
+ * hydra_get_config also answers "last_overlap_simt" (1 when that split ran the SIMT suffix as the
+ * prefix's programmatic dependent over its full grid) and "last_overlap_k" (prefix CTAs of this thread's last hydra_attn /
  * hydra_tree_attn overlap split, 0 = sequential) and "testing_build" (1 in libhydra_test.so).
  * Returns HYDRA_EINVAL for an unknown key.
  */

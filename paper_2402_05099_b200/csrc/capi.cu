@@ -52,6 +52,7 @@ struct Config {
   int64_t step_timer = 0;
   // 1: the sequential schedule launches the suffix as a programmatic dependent of the prefix
   int64_t seq_pdl = 1;
+  int64_t overlap_simt = 0;  // 0 auto, 1 force, 2 never: the SIMT-dependent overlap schedule (overlap_prefix_ctas)
   // CTA-pair prefix kernel: pairs per cluster sharing K/V tiles by multicast (0 auto, 1, 2, 4)
   int64_t pair_cluster = 0;
   int64_t pair_poly = 0;  // all exponentials on the MUFU: measured faster than 4 on the pair kernel (issue/latency-bound)
@@ -70,6 +71,7 @@ struct Config {
   // testing build only (libhydra_test.so): timing experiments, diagnostics, sabotage
   int64_t tc_debug = 0, prefix_trace = 0, suffix_trace = 0, inject_combine_bug = 0, mutate = 0;
   int64_t last_overlap_k = 0;  // read-only: prefix CTAs of this thread's last overlap split (0 = sequential)
+  int64_t last_overlap_simt = 0;  // read-only: 1 when that split ran the SIMT suffix as the prefix's dependent
 };
 static thread_local Config g_cfg;
 static const char *kStepEvKeys[4] = {"ev_prefix_begin", "ev_prefix_end", "ev_suffix_begin", "ev_suffix_end"};
@@ -103,6 +105,7 @@ const Key kKeys[] = {
     {"suffix_ctas", &Config::suffix_ctas, false},         {"suffix_unroll", &Config::suffix_unroll, false},
     {"suffix_cb", &Config::suffix_cb, false},             {"overlap_prefix_ctas", &Config::overlap_prefix_ctas, false},
     {"step_timer", &Config::step_timer, false},          {"seq_pdl", &Config::seq_pdl, false},
+    {"overlap_simt", &Config::overlap_simt, false},
     {"pair_cluster", &Config::pair_cluster, false},
     {"pair_poly", &Config::pair_poly, false},
     {"fuse_combine", &Config::fuse_combine, false},
@@ -140,6 +143,7 @@ extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
 extern "C" int64_t hydra_get_config(const char *key) {
   if (!key) return -1;
   if (!strcmp(key, "last_overlap_k")) return g_cfg.last_overlap_k;
+  if (!strcmp(key, "last_overlap_simt")) return g_cfg.last_overlap_simt;
   if (!strcmp(key, "testing_build")) return kTesting ? 1 : 0;
   // resident CTAs of the CTA-pair kernel in clusters of 1 / 2 / 4 pairs (2 x pairs, 1024 x 4 groups)
   if (!strcmp(key, "pair_max_ctas")) return prefix_pair_plan(1024, 1, 1, 1 << 20, 1 << 20, 1).ctas;
@@ -346,9 +350,37 @@ static int prefix_splits(const hydra_heads *h, int64_t B, int64_t P, int tc2_cta
 // Candidates are multiples of the prefix plan's group size so no SM is left idle; on ties
 // (suffix-bound) the smallest k wins.  Measured at C3@16K: k = 56-60 best (0.86 ms).
 // 0 = no overlap.
-static int overlap_prefix_ctas(const hydra_heads *h, int64_t B, int64_t P, int64_t S_cap) {
-  if (P <= 0 || S_cap <= 0 || !use_suffix_tc(h, B, S_cap, true)) return 0;
+static int overlap_prefix_ctas(const hydra_heads *h, int64_t B, int64_t P, int64_t S_cap, bool *simt = nullptr) {
+  if (simt) *simt = false;
+  if (P <= 0 || S_cap <= 0) return 0;
   const int g = h->num_q_heads / h->num_kv_heads;
+  // SIMT-dependent overlap: where the sequential schedule's suffix is the SIMT kernel (MHA) and
+  // the prefix is light, the prefix runs on a few persistent CTAs (>= 32, the plan's nearest
+  // valid count) and the SIMT suffix is its programmatic dependent with its full grid: its CTAs
+  // stream on every other SM from the start and spread to all SMs as the prefix ends (only its
+  // last CTA waits for the prefix grid, decode.cu).  Taken when the prefix on those CTAs
+  // (model rate R_P below) needs at most 0.6x the suffix's full-chip streaming time.  Measured
+  // (tools/config_ab.py, profiles/r2s_simt.jsonl): C2 0.104 -> 0.092 ms, C3@1K 0.804 -> 0.788;
+  // C3@16K keeps the tensor-core split (prefix too heavy: 0.96 ms this way vs 0.91-0.95).
+  if (g_cfg.overlap_simt != 2 && simt && !use_suffix_tc(h, B, S_cap, false) && prefix_kind(h, B * g, P, 8) == PK_TC2) {
+    const int sms = device_sm_count();
+    int k = 0;
+    const int k0 = g_cfg.overlap_prefix_ctas > 0 ? (int)g_cfg.overlap_prefix_ctas : 32;
+    for (int c = k0; c <= sms / 2 && !k; ++c)
+      if (prefix_kind(h, B * g, P, c) == PK_TC2 &&
+          prefix_tc2_ctas(B, g, h->num_kv_heads, P, c, prefix_bn(), pair_mode(g), (int)g_cfg.pair_cluster) == c)
+        k = c;
+    if (k > 0) {
+      const double R_P = pair_mode(g) ? 0.42 : 0.38, BW = 7.0e6;
+      const double pair_blocks = (double)((B * g + 255) / 256) * h->num_kv_heads * ((P + 127) / 128);
+      const double bytes = (double)B * h->num_kv_heads * S_cap * h->head_dim * 4.0;
+      if (g_cfg.overlap_simt == 1 || pair_blocks / (k * R_P) <= 0.6 * bytes / BW) {
+        *simt = true;
+        return k;
+      }
+    }
+  }
+  if (!use_suffix_tc(h, B, S_cap, true)) return 0;
   if (prefix_kind(h, B * g, P, 8) != PK_TC2) return 0;  // not even 8 persistent CTAs' worth of blocks
   const int sms = device_sm_count();
   if (g_cfg.overlap_prefix_ctas > 0) return (int)std::min<int64_t>(g_cfg.overlap_prefix_ctas, sms - 1);
@@ -572,6 +604,7 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
     p.page_shift = __builtin_ctz((unsigned)pg->page_size);
   }
   p.pdl = pdl ? 1 : 0;
+  if (g_cfg.step_timer) p.timer = reinterpret_cast<unsigned long long *>((intptr_t)g_cfg.step_timer) + 2;
   hydra_status st = launch_decode(p, h->dtype, h->head_dim, s);
   return st == HYDRA_OK ? st : (st == HYDRA_ECUDA ? cuda_fail("suffix launch") : fail(st, "suffix"));
 }
@@ -613,9 +646,11 @@ extern "C" size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, 
       const int s = suffix_splits(h, B, S_cap);
       return s > 1 ? pb * s : 0;
     }
-    case HYDRA_OP_ATTN: {  // enough for both the sequential and the SM-partitioned schedule (+ fused counters)
-      const int k = overlap_prefix_ctas(h, B, P, S_cap);
-      const int np = std::max(prefix_splits(h, B, P), k > 0 ? prefix_splits(h, B, P, k) : 1);
+    case HYDRA_OP_ATTN: {  // enough for both the sequential and the SM-partitioned schedules (+ fused counters)
+      bool simt = false;
+      const int k = overlap_prefix_ctas(h, B, P, S_cap), k2 = overlap_prefix_ctas(h, B, P, S_cap, &simt);
+      const int np = std::max({prefix_splits(h, B, P), k > 0 ? prefix_splits(h, B, P, k) : 1,
+                               k2 > 0 ? prefix_splits(h, B, P, k2) : 1});
       return pb * (size_t)(np + std::max(suffix_splits(h, B, S_cap), suffix_splits(h, B, S_cap, k > 0))) +
              counter_bytes(B * h->num_q_heads);
     }
@@ -856,13 +891,15 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
   // both.  (Two streams let the suffix grab SMs first and split TPCs: measured 0.96-1.35 ms
   // depending on k at C3@16K, tools/overlap_sustained.py.)  Without an SM split (k = 0) two
   // full grids would only contend: run sequentially.
-  const int k_over = s_aux ? overlap_prefix_ctas(h, B, P, S_cap) : 0;
+  bool ov_simt = false;  // SM-partitioned with the SIMT suffix as the prefix's dependent (full grid)
+  const int k_over = s_aux ? overlap_prefix_ctas(h, B, P, S_cap, &ov_simt) : 0;
   cudaStream_t sa = s;
   g_cfg.last_overlap_k = k_over;
+  g_cfg.last_overlap_simt = ov_simt ? 1 : 0;
   const int sms = device_sm_count();
   const int g = h->num_q_heads / h->num_kv_heads;
-  const int np = prefix_splits(h, B, P, k_over), ns = suffix_splits(h, B, S_cap, k_over > 0);
-  const bool fused = attn_fused(h, B, P, S_cap, k_over);
+  const int np = prefix_splits(h, B, P, k_over), ns = suffix_splits(h, B, S_cap, k_over > 0 && !ov_simt);
+  const bool fused = !ov_simt && attn_fused(h, B, P, S_cap, k_over);  // (the SIMT dependent never fuses)
   const int64_t rows = B * h->num_q_heads;
   const size_t need = part_bytes(h, B) * (np + ns) + (fused ? counter_bytes(rows) : 0);
   if (!ws || ws_bytes < need) return fail(HYDRA_ENOMEM, "workspace too small: need %zu bytes", need);
@@ -927,7 +964,7 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
                                  : 0;
     if (!pdl) record_step_ev(2, s);
     st = run_suffix(h, B, q, q_sb, q_sh, sk, sv, s_sb, s_st, s_sh, S_cap, lens, ns, suf, s,
-                    k_over > 0 ? std::max(1, sms - k_eff) : 0, pg, fused ? &fc : nullptr, pdl);
+                    k_over > 0 && !ov_simt ? std::max(1, sms - k_eff) : 0, pg, fused ? &fc : nullptr, pdl);
     record_step_ev(3, s);
   } else {
     st = launch_fill_neg_inf(suf.lse, rows, s);

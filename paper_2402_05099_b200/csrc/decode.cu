@@ -33,6 +33,9 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeParams p) 
   __shared__ float sm_acc[NG][GQ][D];
 
   const int tid = threadIdx.x;
+  const int64_t cta_lin = ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  const int64_t n_cta = (int64_t)gridDim.x * gridDim.y * gridDim.z;
+  if (p.timer && tid == 0 && cta_lin == 0) atomicMin(p.timer, gtimer());
   const int lane = tid % TPR;
   const int grp = tid / TPR;
   const int split = blockIdx.x;
@@ -191,9 +194,13 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeParams p) 
       }
     }
   }
-  // a programmatic dependent of the prefix kernel (sequential schedule: the suffix fills the SMs
-  // the prefix's last CTAs leave free) completes only after it; a no-op otherwise
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // A programmatic dependent of the prefix kernel (the suffix fills the SMs the prefix leaves free)
+  // must complete only after it: the LAST CTA in launch order waits for the prefix grid, so this
+  // grid cannot complete earlier, while every other CTA exits at once and frees its slot for
+  // the next CTA (waiting in every CTA parked the CTAs started beside the prefix until it ended:
+  // that was why this kernel measured slower as a dependent).  A no-op otherwise.
+  if (p.timer && tid == 0 && cta_lin >= n_cta - 1024) atomicMax(p.timer + 1, gtimer());
+  if (cta_lin == n_cta - 1) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 template <typename T, int D, int GQ, int U>

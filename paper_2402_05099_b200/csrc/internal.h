@@ -80,8 +80,10 @@ struct DecodeParams {
   int64_t bt_stride;
   int32_t page_shift;
   FusedCombine fc;  // fc.cnt != null: merge each completed row in the epilogue (d = 128, bf16 suffix only)
-  int32_t pdl;      // host only: programmatic dependent of the previous kernel in the stream (it ends with
-                    // griddepcontrol.wait, so its completion implies the predecessor's)
+  int32_t pdl;      // host only: programmatic dependent of the previous kernel in the stream (its last CTA
+                    // ends with griddepcontrol.wait, so its completion implies the predecessor's)
+  unsigned long long *timer = nullptr;  // measurement: [0] first CTA's start, [1] max end over the last
+                                        // 1024 CTAs in launch order (%globaltimer ns); null = off
 };
 
 hydra_status launch_decode(const DecodeParams &p, hydra_dtype dt, int d, cudaStream_t s);

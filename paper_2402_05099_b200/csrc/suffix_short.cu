@@ -329,8 +329,10 @@ __global__ void __launch_bounds__(ssh::kThreads, ssh::kCtasPerSm)
     ptx::tmem_dealloc<TMEM_COLS>(tmem);
   }
   if (P.timer && threadIdx.x == 0) atomicMax(P.timer + 1, gtimer());
-  // as a programmatic dependent of the prefix kernel: complete only after it (see suffix_tc.cu)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  // As a programmatic dependent of the prefix kernel: complete only after it.  Only the last CTA
+  // in launch order waits (decode.cu): the others exit and free their slot for later CTAs, so
+  // the SMs the prefix leaves idle keep working through the grid while the prefix runs.
+  if (blockIdx.x == gridDim.x - 1) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ------------------------------------------------------------------ host side
@@ -375,8 +377,7 @@ hydra_status launch_suffix_short(const SuffixTcArgs &a, int n_ctas, cudaStream_t
   P.mutate = kTesting ? a.mutate : 0;
   P.timer = a.timer;
   if (P.n_items == 0) return HYDRA_OK;
-  const int cap = ssh::kCtasPerSm * device_sm_count();
-  const int grid = std::min(P.n_items, n_ctas > 0 ? std::min(n_ctas, cap) : cap);
+  const int grid = std::min(P.n_items, n_ctas > 0 ? n_ctas : ssh::kCtasPerSm * device_sm_count());
   const bool pdl = a.pdl != 0;
   cudaError_t e = cudaErrorInvalidValue;
   switch (g) {

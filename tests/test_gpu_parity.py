@@ -24,7 +24,7 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(autouse=True)
 def _reset_config():
     keys = ("prefix_impl", "prefix_splits", "suffix_splits", "prefix_ctas", "suffix_impl",
-            "suffix_ctas", "overlap_prefix_ctas", "pair_cluster")
+            "suffix_ctas", "overlap_prefix_ctas", "pair_cluster", "overlap_simt")
     for k in keys:
         hydra.set_config(k, 0)
     defaults = {"prefix_variant": 9, "suffix_cb": 2, "prefix_poly": 4, "pair_poly": 0, "fuse_combine": 0}  # the library defaults
@@ -282,6 +282,26 @@ def test_composite_sm_partitioned(k, B, Hq, Hkv, P, S):
     out, lse = run_flat(pb, aux=True)
     ref, lref = oracle.flat_attention(pb)
     assert_parity(out, ref, lse, lref, what=f"partitioned k={k}")
+
+
+@pytest.mark.parametrize("B,Hq,Hkv,P,S", [(64, 8, 8, 4096, 300), (40, 16, 16, 2100, 129), (300, 4, 4, 4200, 64)])
+def test_composite_simt_dependent(B, Hq, Hkv, P, S):
+    """SM-partitioned schedule with the SIMT suffix (MHA) as the programmatic dependent of a
+    prefix on a few persistent CTAs (overlap_simt forced; shapes with >= 8 blocks per prefix CTA at
+    32 CTAs, the persistent kernel's minimum): the suffix grid's CTAs run beside the
+    prefix and only its last CTA waits for the prefix grid -- the combine after it must still
+    see every prefix part (ragged lens, NaN-poisoned padding, NaN-filled outputs)."""
+    hydra.set_config("overlap_simt", 1)
+    try:
+        rng = np.random.default_rng(B)
+        lens = rng.integers(0, S + 1, B)
+        pb = synth.make_problem(B, Hq, Hkv, 128, P, S, lens=lens, dtype="bf16", dist="boundary", seed=46)
+        out, lse = run_flat(pb, aux=True)
+        assert hydra.get_config("last_overlap_simt") == 1 and hydra.get_config("last_overlap_k") >= 32
+    finally:
+        hydra.set_config("overlap_simt", 0)
+    ref, lref = oracle.flat_attention(pb)
+    assert_parity(out, ref, lse, lref, what=f"SIMT-dependent overlap B={B} H={Hq}")
 
 
 def test_composite_auto_overlap_small_shard():

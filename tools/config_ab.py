@@ -1,5 +1,5 @@
 """Step time of hydragen_attention (sequential and SM-partitioned) for values of one config key
-on several shapes (diagnostics).   KEY=seq_pdl VALUES=0,1 python tools/config_ab.py [shape,...]"""
+on several shapes (diagnostics).   KEY=seq_pdl VALUES=0,1 [EXTRA=k=v,..] [FLUSH=1] python tools/config_ab.py [shape,...]"""
 import json
 import os
 import sys
@@ -31,10 +31,31 @@ def graph(fn):
     return gr
 
 
+FLUSH = os.environ.get("FLUSH") == "1"  # L2 flushed (write + read) before every timed replay
+if FLUSH:
+    fw = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    fr = torch.zeros(512 << 20, dtype=torch.uint8, device=dev)
+for kv in filter(None, os.environ.get("EXTRA", "").split(",")):  # other keys held fixed: k=v,...
+    k_, v_ = kv.split("=")
+    hydra.set_config(k_, int(v_))
+
+
 def t(gr, iters=50):
     for _ in range(5):
         gr.replay()
     torch.cuda.synchronize()
+    if FLUSH:
+        ts = []
+        for _ in range(iters):
+            fw.zero_()
+            fr.sum()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            gr.replay()
+            e1.record()
+            ts.append((e0, e1))
+        torch.cuda.synchronize()
+        return round(sorted(a.elapsed_time(b) for a, b in ts)[iters // 2], 4)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(iters):

@@ -13,12 +13,13 @@ import paper_2402_05099_b200 as hydra
 
 assert hydra.get_config("testing_build") == 1, "run with HYDRA_TESTING=1"
 dev = torch.device("cuda:0")
-poly = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+poly = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 B, H, Hkv, P = (int(x) for x in sys.argv[2:6]) if len(sys.argv) > 5 else (1024, 40, 40, 16384)
 N, R = 1024, 44
 tr = torch.zeros(R * N, dtype=torch.int64, device=dev)
 hydra.set_config("prefix_impl", 3)
 hydra.set_config("prefix_poly", poly)
+hydra.set_config("pair_poly", poly)
 hydra.set_config("prefix_variant", 9)
 hydra.set_config("tc_debug_variant", int(os.environ.get("TC_DEBUG", 0)))
 g = torch.Generator(device=dev)
