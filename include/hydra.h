@@ -356,6 +356,9 @@ HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, i
  *                         (variants 3-6; variant 9 reads "pair_poly")
  *   "pair_poly"           CTA-pair kernel: 0 (default) all exp2 on MUFU; 4 every 4th pair on the FMA
  *                         pipe
+ *   "pair_item_cost"      CTA-pair kernel: stream-K group boundaries balance blocks + this many
+ *                         block-equivalents per item a group touches (default 0 = uniform split;
+ *                         5 measured no faster: C6 0.098 -> 0.102 ms, C3@16K 0.840 -> 0.835)
  *   "pair_cluster"        CTA-pair kernel: CTA pairs per cluster that share every K/V tile by TMA
  *                         multicast (1, 2 or 4; 0 = automatic: the most that divides the stream-K
  *                         group without idling SMs)

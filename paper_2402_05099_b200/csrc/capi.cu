@@ -56,6 +56,7 @@ struct Config {
   // CTA-pair prefix kernel: pairs per cluster sharing K/V tiles by multicast (0 auto, 1, 2, 4)
   int64_t pair_cluster = 0;
   int64_t pair_poly = 0;  // all exponentials on the MUFU: measured faster than 4 on the pair kernel (issue/latency-bound)
+  int64_t pair_item_cost = 0;  // stream-K group boundaries balance blocks + this x items (0 = uniform; measured no gain)
   // Eq. 5 merged in the kernel epilogues (fused.cuh): 1 in the sequential schedule only (the
   // suffix merges each row after the prefix kernel), 2 also in the SM-partitioned schedule
   // (arrival counters), 0 never: a separate combine launch (default).  Measured
@@ -108,6 +109,7 @@ const Key kKeys[] = {
     {"overlap_simt", &Config::overlap_simt, false},
     {"pair_cluster", &Config::pair_cluster, false},
     {"pair_poly", &Config::pair_poly, false},
+    {"pair_item_cost", &Config::pair_item_cost, false},
     {"fuse_combine", &Config::fuse_combine, false},
     {"tc_debug_variant", &Config::tc_debug, true},        {"prefix_trace", &Config::prefix_trace, true},
     {"suffix_trace", &Config::suffix_trace, true},        {"inject_combine_bug", &Config::inject_combine_bug, true},
@@ -130,6 +132,7 @@ extern "C" hydra_status hydra_set_config(const char *key, int64_t value) {
     if (!strcmp(key, "prefix_poly")) v = (v == 0 || v == 3 || v == 4 || v == 8 || (kTesting && (v == -1 || v == 2))) ? v : 4;
     if (!strcmp(key, "pair_cluster")) v = (v == 1 || v == 2 || v == 4) ? v : 0;
     if (!strcmp(key, "pair_poly")) v = (v == 4 || (kTesting && (v == 2 || v == 3))) ? v : 0;
+    if (!strcmp(key, "pair_item_cost")) v = std::max<int64_t>(0, std::min<int64_t>(v, 64));
     if (!strcmp(key, "prefix_variant")) v = (v == 3 || v == 4 || v == 5 || v == 6) ? v : 9;
     if (!strcmp(key, "prefix_stages")) v = (v == 2 ? 2 : 3);
     if (!strcmp(key, "suffix_cb")) v = (v == 1 ? 1 : 2);
@@ -332,7 +335,7 @@ static int prefix_splits(const hydra_heads *h, int64_t B, int64_t P, int tc2_cta
   switch (prefix_kind(h, B * g, P, tc2_ctas)) {
     case PK_TC2:
       return prefix_tc2_slots(B, g, h->num_kv_heads, P, tc2_ctas > 0 ? tc2_ctas : prefix_ctas(), prefix_bn(),
-                              pair_mode(g), (int)g_cfg.pair_cluster);
+                              pair_mode(g), (int)g_cfg.pair_cluster, (int)g_cfg.pair_item_cost);
     case PK_TC1:
       return prefix_splits_tc(((B * g + 127) / 128) * h->num_kv_heads, P);
     default:
@@ -475,6 +478,7 @@ static hydra_status run_prefix(const hydra_heads *h, int64_t B, const void *q, i
     a.timer = reinterpret_cast<unsigned long long *>((intptr_t)g_cfg.step_timer);
     a.pair_cluster = (int32_t)g_cfg.pair_cluster;
     a.pair_poly = (int32_t)g_cfg.pair_poly;
+    a.pair_item_cost = (int32_t)g_cfg.pair_item_cost;
     hydra_status st;
     if (kind == PK_TC2) {
       // stream-K pieces leave some slots of a row unwritten: mark every slot empty first (the

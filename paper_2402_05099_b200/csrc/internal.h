@@ -159,13 +159,15 @@ struct PrefixTcArgs {
   unsigned long long *timer = nullptr;  // measurement: [0] min CTA start, [1] max CTA end (ns); persistent kernels
   int32_t pair_cluster = 0;  // CTA-pair kernel: pairs per cluster (0 = automatic)
   int32_t pair_poly = 0;     // CTA-pair kernel: every k-th exp2 pair on the FMA pipe (0 = all MUFU)
+  int32_t pair_item_cost = 0;  // CTA-pair kernel: stream-K boundaries balance blocks + this x items (0 = uniform)
 };
 bool prefix_tc_supported(const hydra_heads *h);
 hydra_status launch_prefix_tc(const PrefixTcArgs &a, cudaStream_t s);
 // v3: persistent, two 128-row query tiles per CTA; flat mode is stream-K over n_ctas CTAs
 // (partial slots per row = prefix_tc2_slots), task mode deals (task, head, split) items.
 hydra_status launch_prefix_tc2(const PrefixTcArgs &a, int n_ctas, cudaStream_t s);
-int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn, bool pair = false, int pair_cluster = 0);
+int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn, bool pair = false, int pair_cluster = 0,
+                     int pair_item_cost = 0);
 int prefix_tc2_ctas(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn, bool pair = false, int pair_cluster = 0);
 // The flat-mode stream-K plan of launch_prefix_tc2 over n_ctas CTAs, as the fused combine
 // needs it (which partial slots hold a row's pieces): fills fc.sk_*.
@@ -180,7 +182,7 @@ struct PairPlan {
 bool prefix_pair_supported(int g);
 // forced_cluster: 0 = automatic, 1 / 2 / 4 = pairs per cluster (config key pair_cluster)
 PairPlan prefix_pair_plan(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int forced_cluster = 0);
-int prefix_pair_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int forced_cluster = 0);
+int prefix_pair_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int forced_cluster = 0, int item_cost = 0);
 hydra_status launch_prefix_pair(const PrefixTcArgs &a, int n_ctas, cudaStream_t s);
 // Persistent tensor-core suffix kernel (bf16, d = 128, g <= 16), TMA-fed.
 struct SuffixTcArgs {

@@ -98,6 +98,7 @@ constexpr int kTraceN = 1024;
 __device__ __forceinline__ void trace(long long *tr, int row, uint32_t i) {
   if (kTesting && tr && i < (uint32_t)kTraceN) tr[row * kTraceN + i] = clock64();
 }
+constexpr int kMaxGroups = 80;  // stream-K groups per launch (<= 74 CTA pairs on 148 SMs)
 }  // namespace pr
 
 struct __align__(64) PrefixPairParams {
@@ -121,6 +122,7 @@ struct __align__(64) PrefixPairParams {
   unsigned long long *timer;  // measurement: [0] min CTA start, [1] max CTA end (%globaltimer ns); null = off
   int32_t debug;     // testing build only, timing experiments (invalid results): 4 = no K/V TMA after the ring
                      // fill, 2 = no softmax (P published as soon as S lands), 8 = no epilogue O stores
+  int64_t bound[pr::kMaxGroups + 1];  // stream-K group c walks blocks [bound[c], bound[c+1]) (pair_bounds)
 };
 
 namespace pr {
@@ -139,9 +141,7 @@ struct Iter {
 __device__ __forceinline__ int n_workers() { return gridDim.x / 2; }
 __device__ __forceinline__ int worker() { return blockIdx.x / 2; }
 __device__ __forceinline__ int n_groups(const PrefixPairParams &P) { return n_workers() / P.group; }
-__device__ __forceinline__ int64_t sk_start(const PrefixPairParams &P, int64_t c) {
-  return c * P.total_blocks / n_groups(P);
-}
+__device__ __forceinline__ int64_t sk_start(const PrefixPairParams &P, int64_t c) { return P.bound[c]; }
 __device__ __forceinline__ void it_begin(const PrefixPairParams &P, Iter &s) {
   const int grp = worker() / P.group;
   if (grp >= n_groups(P)) {
@@ -743,23 +743,81 @@ PairPlan prefix_pair_plan(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int 
   return pl;
 }
 
-// Partial slots per row = the most stream-K pieces any (pair, head) unit is cut into: the groups
-// owning its first and last block, exactly (an extra, always-empty slot would cost the combine a
-// full read of its O rows).
-int prefix_pair_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int forced_cluster) {
+// Stream-K group boundaries over the flattened (unit, 128-token block) space.  Uniform: group c
+// takes blocks [c * total / G, (c + 1) * total / G).  Balanced (item_cost > 0): a group also pays
+// item_cost blocks for every item (piece of a unit) it touches -- the Q load, the pipeline restart
+// and the epilogue of an item cost ~5 us, about 5 block periods (tools/pair_trace.py PER_CTA at C6:
+// the 3 of 9 groups whose range crossed a head boundary finished 5.5 us after the others) -- and
+// the boundaries equalise blocks + item_cost x items: the smallest per-group budget T for which a
+// greedy walk covers every block with G groups (binary search).  Measured (profiles/r2x_balance.jsonl):
+// no faster -- C6 0.098 -> 0.102 ms with cost 5 (the slow groups of the trace were not slow for
+// their extra item), C3@16K overlapped 0.840 -> 0.835 -- so the default is uniform (config 0).
+static void pair_bounds(const PairPlan &pl, int64_t nb, int item_cost, int64_t *bound) {
+  const int64_t G = pl.workers / pl.group, total = pl.total;
+  for (int64_t c = 0; c <= G; ++c) bound[c] = c * total / G;
+  if (item_cost <= 0 || total < 4 * G || nb <= 0) return;
+  const double t = item_cost;
+  auto end_of = [&](int64_t a, double T) -> int64_t {  // furthest end of a group starting at block a
+    const int64_t u = a / nb, o = a % nb;
+    double R = T - t;  // the first item
+    const int64_t rest = nb - o;
+    if (R < (double)rest) return std::min(total, a + std::max<int64_t>(1, (int64_t)R));
+    R -= (double)rest;
+    int64_t e = (u + 1) * nb;
+    const int64_t k = (int64_t)(R / (t + (double)nb));
+    e += k * nb;
+    R -= (double)k * (t + (double)nb);
+    if (R > t) e += (int64_t)(R - t);
+    return std::min(total, e);
+  };
+  auto fits = [&](double T) {
+    int64_t a = 0;
+    for (int64_t c = 0; c < G && a < total; ++c) a = end_of(a, T);
+    return a >= total;
+  };
+  double lo = (double)total / G, hi = (double)total / G + t * ((double)total / nb + 2.0) + (double)nb;
+  if (!fits(hi)) return;
+  for (int it = 0; it < 48; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (fits(mid)) hi = mid; else lo = mid;
+  }
+  int64_t a = 0;
+  for (int64_t c = 0; c < G; ++c) {
+    bound[c] = a;
+    a = c + 1 == G ? total : end_of(a, hi);
+  }
+  bound[G] = total;
+}
+
+// The most pieces any unit is cut into under these boundaries (units in order, two pointers).
+static int pair_max_pieces(const int64_t *bound, int64_t G, int64_t total, int64_t nb) {
+  int64_t most = 1, c = 0;
+  for (int64_t u = 0; u < total / nb; ++u) {
+    while (c + 1 < G && bound[c + 1] <= u * nb) ++c;  // group of the unit's first block
+    int64_t d = c;
+    while (d + 1 < G && bound[d + 1] <= u * nb + nb - 1) ++d;  // ... and of its last block
+    most = std::max(most, d - c + 1);
+  }
+  return (int)most;
+}
+
+// Partial slots per row = the most stream-K pieces any (pair, head) unit is cut into, under the
+// uniform boundaries (the fused Eq. 5 plan counts pieces with them) or the balanced ones,
+// whichever is more (an extra, always-empty slot would cost the combine a full read of its O rows).
+int prefix_pair_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int forced_cluster, int item_cost) {
   const PairPlan pl = prefix_pair_plan(B, g, Hkv, P, n_ctas, forced_cluster);
   if (pl.total <= 0) return 1;
   const int64_t nb = (P + pr::BN - 1) / pr::BN;
   const int64_t G = pl.workers / pl.group;
-  auto group_of = [&](int64_t x) {  // largest c with floor(c * total / G) <= x
-    int64_t c = x * G / pl.total;
-    while (c + 1 < G && (c + 1) * pl.total / G <= x) ++c;
-    while (c > 0 && c * pl.total / G > x) --c;
-    return c;
-  };
-  int64_t most = 1;
-  for (int64_t u = 0; u < pl.total / nb; ++u) most = std::max(most, group_of(u * nb + nb - 1) - group_of(u * nb) + 1);
-  return (int)most;
+  if (G > pr::kMaxGroups) return 1;
+  int64_t bound[pr::kMaxGroups + 1];
+  pair_bounds(pl, nb, 0, bound);
+  int most = pair_max_pieces(bound, G, pl.total, nb);
+  if (item_cost > 0) {
+    pair_bounds(pl, nb, item_cost, bound);
+    most = std::max(most, pair_max_pieces(bound, G, pl.total, nb));
+  }
+  return most;
 }
 
 hydra_status launch_prefix_pair(const PrefixTcArgs &a, int n_ctas, cudaStream_t s) {
@@ -806,6 +864,9 @@ hydra_status launch_prefix_pair(const PrefixTcArgs &a, int n_ctas, cudaStream_t 
   P.debug = kTesting ? a.debug_variant : 0;
   P.timer = a.timer;
   if (pl.total <= 0) return HYDRA_OK;
+  if (pl.workers / pl.group > pr::kMaxGroups) return HYDRA_EINVAL;
+  // the fused Eq. 5 plan (fused.cuh) counts pieces with the uniform boundaries
+  pair_bounds(pl, P.nb, a.fc.cnt ? 0 : a.pair_item_cost, P.bound);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.ctas, 1, 1);
   cfg.blockDim = dim3(pr::kThreads, 1, 1);

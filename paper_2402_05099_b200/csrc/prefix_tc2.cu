@@ -1029,8 +1029,9 @@ static Tc2Plan tc2_plan(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn
 }
 
 // Flat mode: number of partial slots per row the schedule over n_ctas CTAs produces.
-int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn, bool pair, int pair_cluster) {
-  if (pair) return prefix_pair_slots(B, g, Hkv, P, n_ctas, pair_cluster);
+int prefix_tc2_slots(int64_t B, int g, int Hkv, int64_t P, int n_ctas, int bn, bool pair, int pair_cluster,
+                     int pair_item_cost) {
+  if (pair) return prefix_pair_slots(B, g, Hkv, P, n_ctas, pair_cluster, pair_item_cost);
   const Tc2Plan pl = tc2_plan(B, g, Hkv, P, n_ctas, bn);
   if (pl.total <= 0) return 1;
   const int64_t nb = (P + bn - 1) / bn;
