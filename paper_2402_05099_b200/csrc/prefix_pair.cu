@@ -55,7 +55,20 @@ constexpr int HD = 128;     // head dim
 constexpr int NQ = 2;       // Q buffers
 constexpr int NSK = 4;      // K stages
 constexpr int NSV = 4;      // V stages
+// HYDRA_PAIR_SPLIT_ISSUE: the score MMAs are issued from warp 3's thread (SM sub-partition 3, next
+// to the Q loads: one polling loop runs both) and the PV MMAs stay on warp 1, so the cost an
+// MMA-issuing warp puts on the softmax warps of its sub-partition (~600 cycles per block,
+// tools/pair_trace.py) is split between two of them.  S(n+3) then waits for PV(n) to COMPLETE
+// (barrier sfree) instead of queueing behind it in one thread.  Measured SLOWER (profiles/
+// r2z_pair_split_issue_ab.log: C3 1164 -> 1082, C4 1236 -> 1134, C6 1013 -> 919 TFLOP/s; parity
+// green): the wait for PV(n)'s completion costs more than the shared issue slots did.  Kept as a
+// compile-time option, off.
+#ifndef HYDRA_PAIR_SPLIT_ISSUE
+#define HYDRA_PAIR_SPLIT_ISSUE 0
+#endif
+constexpr bool kSplitIssue = HYDRA_PAIR_SPLIT_ISSUE != 0;
 constexpr int kThreads = 384;
+constexpr int kLowRegs = 88;  // producer / MMA warps (softmax warps: 208; 16 K registers per sub-partition)
 constexpr int QPANEL = BM * 128;      // 128 rows x 128 B
 constexpr int QTILE = 2 * QPANEL;     // 32 KB
 constexpr int KPANEL = 64 * 128;      // 64 tokens x 128 B
@@ -84,8 +97,8 @@ constexpr int kMmaWarp = HYDRA_PAIR_MMA_WARP;  // 1 or 3 (warp 1 allocates TMEM 
 constexpr int O_COL = NSB * BN;             // O accumulator: TMEM columns [384, 512)
 constexpr int OFF_X = OFF_V + NSV * VHALF;  // row max / sum exchange [parity][WG][128 rows]
 constexpr int OFF_BAR = OFF_X + 6 * BM * 4;  // m exchange [WG][128] + epilogue (m, l) [WG][128][2]
-// kf, ke [NSK]; vf, ve [NSV]; qf, qe [NQ]; sf [NSB]; pf [NSB]; ordy; ofree; xfree [NQ]
-constexpr int N_BARS = 2 * NSK + 2 * NSV + 3 * NQ + 2 * NSB + 2;
+// kf, ke [NSK]; vf, ve [NSV]; qf, qe [NQ]; sf [NSB]; pf [NSB]; ordy; ofree; xfree [NQ]; sfree [NSB]
+constexpr int N_BARS = 2 * NSK + 2 * NSV + 3 * NQ + 3 * NSB + 2;
 constexpr int BYTES = OFF_BAR + N_BARS * 8 + 16;
 constexpr int ALLOC = BYTES + 1024;
 static_assert(ALLOC <= 232448, "prefix_pair smem over the 227 KB opt-in limit");
@@ -215,6 +228,7 @@ __global__ void __launch_bounds__(pr::kThreads, 1) prefix_pair_kernel(const __gr
   uint64_t *bars = reinterpret_cast<uint64_t *>(smem + OFF_BAR);
   uint64_t *kf = bars, *ke = kf + NSK, *vf = ke + NSK, *ve = vf + NSV, *qf = ve + NSV, *qe = qf + NQ;
   uint64_t *sf = qe + NQ, *pf = sf + NSB, *ordy = pf + NSB, *ofree = ordy + 1, *xfree = ofree + 1;
+  uint64_t *sfree = xfree + NQ;  // split issue: PV(n) done, score buffer n % NSB may be overwritten
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + N_BARS);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t crank = ptx::cluster_ctarank();
@@ -245,6 +259,7 @@ __global__ void __launch_bounds__(pr::kThreads, 1) prefix_pair_kernel(const __gr
     for (int i = 0; i < NSB; ++i) {
       ptx::mbar_init(&sf[i], 1);
       ptx::mbar_init(&pf[i], 8);  // the 4 warps of the block's WG x 2 CTAs (leader's copy)
+      ptx::mbar_init(&sfree[i], 1);
     }
     ptx::mbar_init(ordy, 1);
     ptx::mbar_init(ofree, 16);
@@ -258,12 +273,64 @@ __global__ void __launch_bounds__(pr::kThreads, 1) prefix_pair_kernel(const __gr
   if (cta_tr && threadIdx.x == 0) cta_tr[1] = (long long)gtimer();
 
   if (warp == 3) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kLowRegs) : "memory");
     // ================= Q producer (both CTAs): this CTA's 128 stacked query rows per item =================
     // Its own thread, so the next item's Q is loaded as soon as its buffer is free (the item two
     // back has finished its score MMAs and its epilogue staging), not behind the current item's
     // K loads: issued there, it landed ~3 K cycles after the current item's epilogue.
-    if (ptx::elect_one()) {
+    const bool elected = ptx::elect_one();  // once, converged (elect.sync takes the full warp)
+    if (kSplitIssue && rank == 0 && elected) {
+      // Q producer and score-MMA issuer in one polling loop (split issue, the pair's leader)
+      const uint32_t qf0 = ptx::mapa(ptx::smem_u32(qf), lead);
+      constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(2 * BM, BN, false);
+      long long *tr = (kTesting && P.trace && blockIdx.x == 0) ? P.trace : nullptr;
+      uint32_t qi = 0, gs = 0;
+      Iter si;
+      it_begin(P, si);
+      Item it;
+      bool q_more = it_next(P, si, it);
+      Cursor cs;
+      cs.init(P);
+      while (q_more || cs.valid) {
+        bool progress = false;
+        if (q_more) {  // the next item's Q once its buffer is free (score MMAs and epilogue staging done)
+          const int qb = qi % NQ;
+          const uint32_t par = ((qi / NQ) & 1) ^ 1;
+          if (ptx::mbar_test_wait(&qe[qb], par) && ptx::mbar_test_wait(&xfree[qb], par)) {
+            ptx::mbar_arrive_expect_tx(&qf[qb], 2 * QTILE);
+            const int b0 = (int)(it.row0 / P.g);
+            uint8_t *sQ = smem + OFF_Q + qb * QTILE;
+            ptx::tma_load_4d_pair(sQ, &P.tmQ, qf0 + qb * 8, 0, 0, it.j, b0);
+            ptx::tma_load_4d_pair(sQ + QPANEL, &P.tmQ, qf0 + qb * 8, 64, 0, it.j, b0);
+            ++qi;
+            q_more = it_next(P, si, it);
+            progress = true;
+          }
+        }
+        if (cs.valid) {  // S(gs): its buffer's PV(gs - NSB) done, its Q (first block) and K landed
+          const int qb = cs.qi % NQ, ks = gs % NSK, sb = gs % NSB;
+          if ((gs < (uint32_t)NSB || ptx::mbar_test_wait(&sfree[sb], ((gs / NSB) - 1) & 1)) &&
+              (cs.n != 0 || ptx::mbar_test_wait(&qf[qb], (cs.qi / NQ) & 1)) &&
+              ptx::mbar_test_wait(&kf[ks], (gs / NSK) & 1)) {
+            trace(tr, 22, gs);
+            ptx::tc_fence_after();
+            const uint32_t qa = ptx::smem_u32(smem + OFF_Q + qb * QTILE), ka = ptx::smem_u32(smem + OFF_K + ks * KHALF);
+#pragma unroll
+            for (int kk = 0; kk < HD / 16; ++kk)
+              ptx::mma2_ss(tmem + sb * BN, ptx::smem_desc_sw128(qa + (kk / 4) * QPANEL + (kk % 4) * 32, 16, 1024),
+                           ptx::smem_desc_sw128(ka + (kk / 4) * KPANEL + (kk % 4) * 32, 16, 1024), idesc_s, kk > 0);
+            ptx::mma2_commit(&sf[sb], pair_mask);
+            ptx::mma2_commit(&ke[ks], kAll);
+            if (cs.n == cs.it.nblk - 1) ptx::mma2_commit(&qe[qb], pair_mask);
+            trace(tr, 14, gs);
+            ++gs;
+            cs.advance(P);
+            progress = true;
+          }
+        }
+        if (!progress) __nanosleep(kPollSleepNs);
+      }
+    } else if (elected) {
       const uint32_t qf0 = ptx::mapa(ptx::smem_u32(qf), lead);
       uint32_t qi = 0;
       Iter si;
@@ -283,7 +350,7 @@ __global__ void __launch_bounds__(pr::kThreads, 1) prefix_pair_kernel(const __gr
       }
     }
   } else if (warp == 0 || warp == 2) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kLowRegs) : "memory");
     // ================= TMA producers (both CTAs): warp 0 K, warp 2 V =================
     // (separate threads, so a K tile is issued as soon as its slot frees, independently of V)
     if (ptx::elect_one()) {
@@ -339,7 +406,7 @@ __global__ void __launch_bounds__(pr::kThreads, 1) prefix_pair_kernel(const __gr
       }
     }
   } else if (warp == kMmaWarp) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kLowRegs) : "memory");
     // ================= MMA issuer (leader CTA, one thread) =================
     if (rank == 0 && ptx::elect_one()) {  // the pair's leader
       constexpr uint32_t idesc_s = ptx::idesc_bf16_f32(2 * BM, BN, false);  // S = Q K^T, M = 256
@@ -378,7 +445,8 @@ __global__ void __launch_bounds__(pr::kThreads, 1) prefix_pair_kernel(const __gr
         ++gs;
         cs.advance(P);
       };
-      for (int i = 0; i < NSB; ++i) issue_s(false);
+      if constexpr (!kSplitIssue)
+        for (int i = 0; i < NSB; ++i) issue_s(false);
       // Per block: PV(gp) (both token halves into the one O), then S(gp + NSB) into the score
       // buffer PV(gp) just read.  A barrier probe costs ~150 cycles of latency
       // (tools/pair_trace.py), so every barrier this block still needs is probed together each
@@ -386,7 +454,7 @@ __global__ void __launch_bounds__(pr::kThreads, 1) prefix_pair_kernel(const __gr
       while (cp.valid) {
         const int sb = gp % NSB, vs = gp % NSV;
         const uint32_t acc0 = cp.n > 0 ? 1u : 0u;
-        const bool s_next = cs.valid;
+        const bool s_next = !kSplitIssue && cs.valid;
         const int qb = cs.qi % NQ, ks = gs % NSK;
         const uint32_t qpar = (cs.qi / NQ) & 1, kpar = (gs / NSK) & 1, ppar = (gp / NSB) & 1;
         bool of = cp.n != 0, v = false, a = false, k = !s_next, q = !(s_next && cs.n == 0);
@@ -408,6 +476,13 @@ __global__ void __launch_bounds__(pr::kThreads, 1) prefix_pair_kernel(const __gr
                        ptx::smem_desc_sw128(va + kk * 2048, 16, 1024), idesc_pv, acc0 | (kk > 0));
         trace(tr, 19, gp);
         if (cp.n == cp.it.nblk - 1) ptx::mma2_commit(ordy, pair_mask);  // the item's last PV: epilogue may read O
+        if constexpr (kSplitIssue) {  // the score thread may overwrite buffer sb; the V slot is free
+          ptx::mma2_commit(&sfree[sb], (uint16_t)(1u << lead));
+          ptx::mma2_commit(&ve[vs], kAll);
+          ++gp;
+          cp.advance(P);
+          continue;
+        }
         ++gp;
         cp.advance(P);
         while (!(k && q)) {
@@ -644,7 +719,7 @@ __global__ void __launch_bounds__(pr::kThreads, 1) prefix_pair_kernel(const __gr
     }
     if (cta_tr && warp == 4 && lane == 0) cta_tr[2] = (long long)gtimer();  // this CTA's softmax / epilogues done
   } else {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kLowRegs) : "memory");
   }
 
   ptx::tc_fence_before();
