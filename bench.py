@@ -77,7 +77,11 @@ NCU_TRAFFIC = {
     ("c3_16k", "decode_attn_kernel"): 5379746000 + 6668800,    # profiles/r1o_suffix_decode_raw.csv
     ("c3_16k", "suffix_tc_kernel"): 5379274000 + 25441024,     # profiles/r1o_suffix_tc_76_raw.csv (76 CTAs, k = 72)
     ("c3_16k", "prefix_tc2_kernel"): 355092736 + 21645312,     # profiles/r1o_prefix_tc2_raw.csv (variant 6, poly 4)
-    ("c3_16k", "prefix_pair_kernel"): 350497280 + 21158144,    # profiles/r2_pair_c3_raw.csv (variant 9, poly 4)
+    ("c3_16k", "prefix_pair_kernel"): 349904640 + 21081600,    # profiles/r2u_pair_c3_raw.csv (variant 9, pair_poly 0)
+    ("c6_longdoc", "suffix_short_kernel"): 69250560 + 1515264,  # profiles/r2u_suffix_short_c6_raw.csv
+    ("c4_1gpu", "suffix_short_kernel"): 272669952 + 13087232,   # profiles/r2u_suffix_short_c4_raw.csv
+    ("c4_1gpu", "prefix_pair_kernel"): 138497792 + 8392704,     # profiles/r3_pair_c4_raw.csv
+    ("c6_longdoc", "prefix_pair_kernel"): 43016448 + 1049600,   # profiles/r3_pair_c6_raw.csv
     ("c3_16k", "suffix_tc_kernel@84"): 5379332000 + 26637568,  # profiles/r2_suffix_tc_84_raw.csv (84 CTAs, k = 64)
 }
 
@@ -725,6 +729,25 @@ def run_flat(args, cfg):
     # under the 1 kW power cap).
     g_pre = capture(lambda: hydra.prefix_attn(q, pk, pv, workspace=ws))
     ms_pre_burst = time_graph(g_pre, 20, 3)
+    # the prefix KERNEL alone (prefix_attn also merges the kernel's stream-K pieces with a combine
+    # launch): the persistent kernel's own span (config key step_timer), 20 graph replays
+    pre_span = []
+    tmr = torch.zeros(4, dtype=torch.int64, device=dev)
+    tmr_init = torch.tensor([-1, 0, -1, 0], dtype=torch.int64, device=dev)
+    try:
+        hydra.set_config("step_timer", tmr.data_ptr())
+        g_span = capture(lambda: hydra.prefix_attn(q, pk, pv, workspace=ws))
+    finally:
+        hydra.set_config("step_timer", 0)
+    for _ in range(20):
+        tmr.copy_(tmr_init)
+        g_span.replay()
+        torch.cuda.synchronize(dev)
+        t4 = [int(v) & 0xFFFFFFFFFFFFFFFF for v in tmr.tolist()]
+        if t4[1] > 0 and t4[0] != 0xFFFFFFFFFFFFFFFF:
+            pre_span.append((t4[1] - t4[0]) * 1e-6)
+    del g_span
+    ms_pre_span = statistics.median(pre_span) if pre_span else None
     n_sus = max(20, int(1000.0 / max(ms_pre_burst, 1e-3)))
     with ClockSampler(local) as clk_pre:
         ms_pre_sus = time_graph(g_pre, n_sus, 0)
@@ -924,11 +947,14 @@ def run_flat(args, cfg):
                    "l2": (f"no flush: {in_bytes / 1e9:.2f} GB of inputs per step > 2 x 126 MB L2" if flush is None else
                           L2Flush.DESC + f": {in_bytes / 1e9:.3f} GB of inputs per rank"),
                    "timing": "CUDA graph of one step, CUDA events over K replays, max over ranks"},
-        "roofline": {"bound": "hbm", "kernel": ("suffix_tc_kernel (tensor-core GEMV, all SMs; GQA g = %d; the sequential schedule's suffix)" % (Hq // Hkv)
+        "roofline": {"bound": "hbm", "kernel": (("suffix_short_kernel (tensor-core GEMV, 3 CTAs per SM; GQA g = %d; the sequential schedule's suffix)"
+                                                 if Hq // Hkv in (2, 4, 8) and S <= 256 else
+                                                 "suffix_tc_kernel (tensor-core GEMV, all SMs; GQA g = %d; the sequential schedule's suffix)") % (Hq // Hkv)
                                                 if Hq // Hkv >= 2 else
                                                 "suffix split-K GEMV (decode_attn_kernel, all SMs; the sequential schedule's dominant kernel)"),
                      "achieved": round(suf_gbs, 1), "peak": hbm, "unit": "GB/s", "frac": round(suf_gbs / hbm, 4),
-                     "traffic": NCU_TRAFFIC.get((args.config, "suffix_tc_kernel" if Hq // Hkv >= 2 else "decode_attn_kernel")),
+                     "traffic": NCU_TRAFFIC.get((args.config, ("suffix_short_kernel" if Hq // Hkv in (2, 4, 8) and S <= 256 else
+                                                               "suffix_tc_kernel") if Hq // Hkv >= 2 else "decode_attn_kernel")),
                      "algorithmic_bytes_per_launch": suffix_bytes,
                      "launch_ms": round(ms_suf, 5), "peak_source": peak_src + " (STREAM copy)",
                      "frac_of_nominal_7700": round(suf_gbs / 7700.0, 4),
@@ -943,6 +969,12 @@ def run_flat(args, cfg):
                                        "timed": "back-to-back replays for ~1 s vs the sustained cuBLAS loop"},
                          "after_step_loop": {"achieved": round(pre_tflops, 1), "launch_ms": round(ms_pre, 5)},
                          "frac_of_spec_2250": round(pre_burst / 2250.0, 4), "flops_per_launch": prefix_flops,
+                         "kernel_span": ({"launch_ms": round(ms_pre_span, 5),
+                                          "achieved": round(prefix_flops / (ms_pre_span * 1e-3) / 1e12, 1),
+                                          "frac": round(prefix_flops / (ms_pre_span * 1e-3) / 1e12 / tc_burst, 4),
+                                          "timed": "the kernel's own span (first CTA start to last CTA end), median of 20 "
+                                                   "graph replays; launch_ms above also holds the combine of its pieces"}
+                                         if ms_pre_span else None),
                          "traffic": NCU_TRAFFIC.get((args.config, prefix_kernel_name(hydra, Hq // Hkv).split()[0])),
                          "algorithmic_bytes_per_launch": prefix_bytes},
         "step_roofline": {"t_roof_ms": round(t_roof * 1e3, 5), "frac": round(t_roof * 1e3 / ms, 4),
@@ -997,6 +1029,23 @@ def run_flat(args, cfg):
                "prefix_in_step_ms": round(ms_pre_in, 5),
                "prefix_in_step_tflops": round(prefix_flops / (ms_pre_in * 1e-3) / 1e12, 1),
                "share_of_step": round(ms_suf_in / ms, 4)})
+    if ms_pre_in > ms_suf_in:
+        # the prefix is the step's dominant kernel (C4, C6): it becomes `roofline` (tensor-bound, timed
+        # inside the step, against the sustained bf16 figure); the suffix figure stays as roofline_suffix
+        line["roofline_suffix"] = line["roofline"]
+        pre_in_tf = prefix_flops / (ms_pre_in * 1e-3) / 1e12
+        pname = prefix_kernel_name(hydra, Hq // Hkv)
+        line["roofline"] = {
+            "bound": "tensor", "kernel": pname + ", the step's dominant kernel",
+            "achieved": round(pre_in_tf, 1), "peak": tc_sust, "unit": "TFLOP/s", "frac": round(pre_in_tf / tc_sust, 4),
+            "traffic": NCU_TRAFFIC.get((args.config, pname.split()[0])),
+            "algorithmic_flops_per_launch": prefix_flops, "algorithmic_bytes_per_launch": prefix_bytes,
+            "launch_ms": round(ms_pre_in, 5), "peak_source": peak_src + " (sustained cuBLAS bf16 loop)",
+            "timed": in_step_how.replace("around the suffix launch", "around the prefix launch"),
+            "share_of_step": round(ms_pre_in / ms, 4), "frac_of_spec_2250": round(pre_in_tf / 2250.0, 4),
+            "frac_of_burst_peak": round(pre_in_tf / tc_burst, 4),
+            "alone": {"achieved": round(pre_burst, 1), "peak": tc_burst, "frac": round(pre_burst / tc_burst, 4),
+                      "launch_ms": round(ms_pre_burst, 5), "timed": "burst: 20 graph replays on a cool GPU"}}
 
     if not args.no_e2e:
         line["e2e"] = e2e_leg(args, hydra, torch, dev, world, (hq, hpk, hpv, hsk, hsv, hlens),

@@ -52,6 +52,7 @@ struct Config {
   int64_t step_timer = 0;
   // 1: the sequential schedule launches the suffix as a programmatic dependent of the prefix
   int64_t seq_pdl = 1;
+  int64_t combine_pdl = 0;  // hydra_attn's combine as a programmatic dependent of the suffix kernel
   int64_t overlap_simt = 0;  // 0 auto, 1 force, 2 never: the SIMT-dependent overlap schedule (overlap_prefix_ctas)
   // CTA-pair prefix kernel: pairs per cluster sharing K/V tiles by multicast (0 auto, 1, 2, 4)
   int64_t pair_cluster = 0;
@@ -107,6 +108,7 @@ const Key kKeys[] = {
     {"suffix_cb", &Config::suffix_cb, false},             {"overlap_prefix_ctas", &Config::overlap_prefix_ctas, false},
     {"step_timer", &Config::step_timer, false},          {"seq_pdl", &Config::seq_pdl, false},
     {"overlap_simt", &Config::overlap_simt, false},
+    {"combine_pdl", &Config::combine_pdl, false},
     {"pair_cluster", &Config::pair_cluster, false},
     {"pair_poly", &Config::pair_poly, false},
     {"pair_item_cost", &Config::pair_item_cost, false},
@@ -614,7 +616,7 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
 }
 
 static hydra_status run_combine(int64_t rows, int d, int n, const PartsView &src, void *out, hydra_dtype out_dtype,
-                                float *lse_out, cudaStream_t s) {
+                                float *lse_out, cudaStream_t s, bool pdl = false) {
   CombineParams c{};
   c.rows = rows;
   c.d = d;
@@ -630,6 +632,7 @@ static hydra_status run_combine(int64_t rows, int d, int n, const PartsView &src
   c.lse_out = lse_out;
   c.lse_out_row = 1;
   c.inject_bug = inject_combine_bug() ? 1 : 0;
+  c.pdl = pdl ? 1 : 0;
   hydra_status st = launch_combine(c, HYDRA_F32, out_dtype, s);
   return st == HYDRA_OK ? st : cuda_fail("combine launch");
 }
@@ -976,7 +979,9 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
   }
   if (st) return st;
   if (fused) return HYDRA_OK;  // merged in the epilogues
-  return run_combine(rows, h->head_dim, np + ns, all, out, out_dtype, lse_out, s);
+  // (not behind a caller event: an event node between the kernels would serialise them anyway)
+  return run_combine(rows, h->head_dim, np + ns, all, out, out_dtype, lse_out, s,
+                     g_cfg.combine_pdl && !g_cfg.step_ev[3]);
 }
 
 extern "C" hydra_status hydra_attn(const hydra_heads *h, int64_t B, const void *q, int64_t q_sb, int64_t q_sh,

@@ -75,6 +75,9 @@ __device__ __forceinline__ float *lse_ptr(const CombineParams &p, int64_t row) {
 // General kernel: any number of parts, VEC floats per lane (VEC = 0: element-wise, any d).
 template <typename OT, typename OutT, int VEC>
 __global__ void __launch_bounds__(256) combine_kernel(const CombineParams p) {
+  // as a programmatic dependent (the step's suffix kernel precedes): wait for that grid's
+  // completion and memory before reading any part; a no-op for a normal launch
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t row = (int64_t)blockIdx.x * 8 + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   if (row >= p.rows) return;
@@ -144,6 +147,7 @@ __global__ void __launch_bounds__(256) combine_kernel_p8(const CombineParams p) 
   // RPW rows are issued together, before any decision on their values (one memory round trip
   // per RPW rows).  An empty part's O slot may be unwritten workspace: it is loaded but never
   // used (skipped below, not multiplied by 0, so garbage or NaN cannot leak in).
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // programmatic dependent: see combine_kernel
   const int64_t row0 = ((int64_t)blockIdx.x * 8 + threadIdx.x / 32) * RPW;
   const int lane = threadIdx.x % 32;
   if (row0 >= p.rows) return;
@@ -197,19 +201,14 @@ static cudaError_t launch_c(const CombineParams &p, cudaStream_t s) {
   const dim3 grid((unsigned)((p.rows + 7) / 8));
   const dim3 grid2((unsigned)((p.rows + 15) / 16));  // two rows per warp
   const int n = p.n_a + p.n_b;
-  if (p.d == 128 && n <= 2)
-    combine_kernel_p8<OT, OutT, 2, 2><<<grid2, 256, 0, s>>>(p);
-  else if (p.d == 128 && n <= 4)
-    combine_kernel_p8<OT, OutT, 4, 2><<<grid2, 256, 0, s>>>(p);
-  else if (p.d == 128 && n <= 8)
-    combine_kernel_p8<OT, OutT, 8, 2><<<grid2, 256, 0, s>>>(p);
-  else if (p.d == 128)
-    combine_kernel<OT, OutT, 4><<<grid, 256, 0, s>>>(p);
-  else if (p.d == 256)
-    combine_kernel<OT, OutT, 8><<<grid, 256, 0, s>>>(p);
-  else
-    combine_kernel<OT, OutT, 0><<<grid, 256, 0, s>>>(p);
-  return cudaGetLastError();
+  const bool pdl = p.pdl != 0;
+  const dim3 blk(256);
+  if (p.d == 128 && n <= 2) return launch_maybe_pdl(combine_kernel_p8<OT, OutT, 2, 2>, grid2, blk, 0, s, pdl, p);
+  if (p.d == 128 && n <= 4) return launch_maybe_pdl(combine_kernel_p8<OT, OutT, 4, 2>, grid2, blk, 0, s, pdl, p);
+  if (p.d == 128 && n <= 8) return launch_maybe_pdl(combine_kernel_p8<OT, OutT, 8, 2>, grid2, blk, 0, s, pdl, p);
+  if (p.d == 128) return launch_maybe_pdl(combine_kernel<OT, OutT, 4>, grid, blk, 0, s, pdl, p);
+  if (p.d == 256) return launch_maybe_pdl(combine_kernel<OT, OutT, 8>, grid, blk, 0, s, pdl, p);
+  return launch_maybe_pdl(combine_kernel<OT, OutT, 0>, grid, blk, 0, s, pdl, p);
 }
 
 hydra_status launch_combine(const CombineParams &p, hydra_dtype o_dtype, hydra_dtype out_dtype,

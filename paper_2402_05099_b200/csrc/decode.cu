@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(const DecodeParams p) 
   // the next CTA (waiting in every CTA parked the CTAs started beside the prefix until it ended:
   // that was why this kernel measured slower as a dependent).  A no-op otherwise.
   if (p.timer && tid == 0 && cta_lin >= n_cta - 1024) atomicMax(p.timer + 1, gtimer());
+  asm volatile("griddepcontrol.launch_dependents;");  // the combine may launch as the last CTAs drain
   if (cta_lin == n_cta - 1) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 

@@ -113,6 +113,7 @@ struct CombineParams {
   float *const *lse_out_table;
   int64_t table_rows;
   int32_t inject_bug;  // testing build only: w_p = 1 (the sabotage of S:522)
+  int32_t pdl;         // host only: programmatic dependent of the previous kernel (it waits for that grid at entry)
 };
 hydra_status launch_combine(const CombineParams &p, hydra_dtype o_dtype, hydra_dtype out_dtype,
                             cudaStream_t s);

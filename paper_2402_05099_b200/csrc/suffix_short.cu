@@ -332,6 +332,7 @@ __global__ void __launch_bounds__(ssh::kThreads, ssh::kCtasPerSm)
   // As a programmatic dependent of the prefix kernel: complete only after it.  Only the last CTA
   // in launch order waits (decode.cu): the others exit and free their slot for later CTAs, so
   // the SMs the prefix leaves idle keep working through the grid while the prefix runs.
+  asm volatile("griddepcontrol.launch_dependents;");  // the combine may launch as the last CTAs drain
   if (blockIdx.x == gridDim.x - 1) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 

@@ -722,6 +722,7 @@ __global__ void __launch_bounds__(stc::kThreads, 1) suffix_tc_kernel(const __gri
   // Launched as a programmatic dependent of the prefix kernel (SM-partitioned schedule on one
   // stream): the grid completes only after the prefix grid has, so the combine that follows in
   // the stream sees both.  Without a programmatic prerequisite this returns at once.
+  asm volatile("griddepcontrol.launch_dependents;");  // the combine may launch as the CTAs drain
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
