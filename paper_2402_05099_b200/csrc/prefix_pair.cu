@@ -40,6 +40,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstring>
 
 #include "common.cuh"
@@ -67,6 +68,15 @@ constexpr int NSV = 4;      // V stages
 #define HYDRA_PAIR_SPLIT_ISSUE 0
 #endif
 constexpr bool kSplitIssue = HYDRA_PAIR_SPLIT_ISSUE != 0;
+// HYDRA_PAIR_SPEC: speculative softmax -- a warpgroup computes P(n) with its own previous running max
+// right after loading S(n) and checks m(n) afterwards (recomputing P only when the max moved).
+// Bit-identical results; measured ~1 % SLOWER (profiles/r3e_pair_spec_softmax_ab.log: C3 1164 -> 1153,
+// C4 1235 -> 1220 TFLOP/s), so the row max and the m hand-off are not what bounds the block period.
+// Kept as a compile-time option, off.
+#ifndef HYDRA_PAIR_SPEC
+#define HYDRA_PAIR_SPEC 0
+#endif
+constexpr bool kSpec = HYDRA_PAIR_SPEC != 0;
 constexpr int kThreads = 384;
 constexpr int kLowRegs = 88;  // producer / MMA warps (softmax warps: 208; 16 K registers per sub-partition)
 constexpr int QPANEL = BM * 128;      // 128 rows x 128 B
@@ -561,13 +571,59 @@ __global__ void __launch_bounds__(pr::kThreads, 1) prefix_pair_kernel(const __gr
             for (int i = 0; i < 32; ++i)
               if (c * 32 + i >= rem) sr[c][i] = 0xff800000u;
         }
-        // row max of the 128 scores: 8 independent FMNMX3 chains over column pairs
-        auto sv = [&](int j) { return __uint_as_float(sr[j >> 5][j & 31]); };
+        // exp2(s*c2 - mu) -> bf16 P in the first 64 columns of the score buffer; returns the row sum.
+        // With kMax it also folds the 128 scores into 8 FMNMX3 chains (acc), interleaved with the
+        // exponentials so the ALU work fills the MUFU's issue gaps.
         float acc[8];
+        auto exps = [&](float mu, auto kmax) -> float {
+          constexpr bool kMax = decltype(kmax)::value;
+          const uint64_t nm = ptx::pack2(-mu, -mu);
+          uint64_t sacc[4] = {0, 0, 0, 0};
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] = sv(k);
+          for (int c = 0; c < 4; ++c) {
+            uint32_t pk[16];
 #pragma unroll
-        for (int j = 8; j < BN; j += 2) acc[(j / 2) % 8] = ptx::fmax3(acc[(j / 2) % 8], sv(j), sv(j + 1));
+            for (int i = 0; i < 16; ++i) {
+              const float a0 = __uint_as_float(sr[c][2 * i]), a1 = __uint_as_float(sr[c][2 * i + 1]);
+              if constexpr (kMax) {
+                const int k = (c * 16 + i) % 8;
+                acc[k] = (c == 0 && i < 8) ? fmaxf(a0, a1) : ptx::fmax3(acc[k], a0, a1);
+              }
+              float x0, x1;
+              ptx::unpack2(ptx::fma2(ptx::pack2(a0, a1), cc, nm), x0, x1);
+              float p0, p1;
+              if (kPolyEvery > 0 && (i % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1) {
+                ptx::exp2_poly2(x0, x1, p0, p1);
+              } else {
+                p0 = fast_exp2(x0);
+                p1 = fast_exp2(x1);
+              }
+              sacc[i % 4] = ptx::add2(sacc[i % 4], ptx::pack2(p0, p1));
+              pk[i] = ptx::cvt_bf16x2(p0, p1);
+            }
+            ptx::tmem_st16(s_col + c * 16, pk);
+          }
+          float s0, s1, s2, s3;
+          ptx::unpack2(ptx::add2(sacc[0], sacc[1]), s0, s1);
+          ptx::unpack2(ptx::add2(sacc[2], sacc[3]), s2, s3);
+          return (s0 + s1) + (s2 + s3);
+        };
+        // Speculative (kSpec, this WG's own previous m known): P(n) with that stale max at once,
+        // the row max folded in; m(n-1) / m(n) are checked afterwards and P recomputed only if m(n)
+        // differs (the max was raised in block n-1 or n: rare, kRaise) -- so the exponentials no
+        // longer wait for the row max and the m hand-off between the warpgroups.
+        const bool spec = kSpec && m_own != -INFINITY;
+        float rs = 0.f;
+        if (spec) {
+          rs = exps(m_own, std::true_type{});
+        } else {
+          // row max of the 128 scores: 8 independent FMNMX3 chains over column pairs
+          auto sv = [&](int j) { return __uint_as_float(sr[j >> 5][j & 31]); };
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[k] = sv(k);
+#pragma unroll
+          for (int j = 8; j < BN; j += 2) acc[(j / 2) % 8] = ptx::fmax3(acc[(j / 2) % 8], sv(j), sv(j + 1));
+        }
         const float mnew = fmaxf(ptx::fmax3(acc[0], acc[1], acc[2]),
                                  fmaxf(ptx::fmax3(acc[3], acc[4], acc[5]), fmaxf(acc[6], acc[7]))) * c2;
         // m(n-1) from the other WG (the item's first block starts the chain at -inf)
@@ -589,42 +645,14 @@ __global__ void __launch_bounds__(pr::kThreads, 1) prefix_pair_kernel(const __gr
           xch[x * BM + r] = m_n;
           ptx::named_bar_arrive(bar_out, 64);
         }
+        const bool redo = !spec || __any_sync(0xffffffffu, m_n != m_own);
         // this WG's l follows the last m it used
         l *= (m_own == m_n) ? 1.f : fast_exp2(m_own - m_n);
         m_own = m_n;
+        if (rank == 0 && tr) trace(tr, tb + 3, gs);
         // a row whose tokens are all masked so far keeps m = -inf: its p = 2^-inf = 0
-        const float mu = m_n == -INFINITY ? 0.f : m_n;
-        const uint64_t nm = ptx::pack2(-mu, -mu);
-        if (rank == 0 && tr) {
-          asm volatile("" ::"l"(nm));
-          trace(tr, tb + 3, gs);
-        }
-        uint64_t sacc[4] = {0, 0, 0, 0};
-        // exp2(s*c2 - m) -> bf16 P in the first 64 columns of the score buffer, row sums
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            float x0, x1;
-            ptx::unpack2(ptx::fma2(ptx::pack2(__uint_as_float(sr[c][2 * i]), __uint_as_float(sr[c][2 * i + 1])), cc, nm),
-                         x0, x1);
-            float p0, p1;
-            if (kPolyEvery > 0 && (i % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1) {
-              ptx::exp2_poly2(x0, x1, p0, p1);
-            } else {
-              p0 = fast_exp2(x0);
-              p1 = fast_exp2(x1);
-            }
-            sacc[i % 4] = ptx::add2(sacc[i % 4], ptx::pack2(p0, p1));
-            pk[i] = ptx::cvt_bf16x2(p0, p1);
-          }
-          ptx::tmem_st16(s_col + c * 16, pk);
-        }
-        float s0, s1, s2, s3;
-        ptx::unpack2(ptx::add2(sacc[0], sacc[1]), s0, s1);
-        ptx::unpack2(ptx::add2(sacc[2], sacc[3]), s2, s3);
-        l += (s0 + s1) + (s2 + s3);
+        if (redo) rs = exps(m_n == -INFINITY ? 0.f : m_n, std::false_type{});
+        l += rs;
         if (rank == 0 && tr) {
           asm volatile("" ::"f"(l));
           trace(tr, tb + 4, gs);
