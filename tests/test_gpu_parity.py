@@ -24,7 +24,7 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(autouse=True)
 def _reset_config():
     keys = ("prefix_impl", "prefix_splits", "suffix_splits", "prefix_ctas", "suffix_impl",
-            "suffix_ctas", "overlap_prefix_ctas", "pair_cluster", "overlap_simt")
+            "suffix_ctas", "overlap_prefix_ctas", "pair_cluster", "overlap_simt", "pair_item_cost", "combine_pdl")
     for k in keys:
         hydra.set_config(k, 0)
     defaults = {"prefix_variant": 9, "suffix_cb": 2, "prefix_poly": 4, "pair_poly": 0, "fuse_combine": 0}  # the library defaults
@@ -302,6 +302,26 @@ def test_composite_simt_dependent(B, Hq, Hkv, P, S):
         hydra.set_config("overlap_simt", 0)
     ref, lref = oracle.flat_attention(pb)
     assert_parity(out, ref, lse, lref, what=f"SIMT-dependent overlap B={B} H={Hq}")
+
+
+@pytest.mark.parametrize("key,val", [("pair_item_cost", 5), ("pair_item_cost", 40), ("combine_pdl", 1)])
+@pytest.mark.parametrize("B,Hq,Hkv,P,S", [(256, 32, 4, 5000, 100), (96, 16, 16, 3000, 200)])
+def test_composite_optional_schedules(key, val, B, Hq, Hkv, P, S):
+    """Schedule options that are off by default stay correct: cost-balanced stream-K group
+    boundaries of the CTA-pair prefix (its pieces cut units unevenly; the slot count must cover
+    them) and the combine as a programmatic dependent of the suffix kernel."""
+    hydra.set_config(key, val)
+    try:
+        rng = np.random.default_rng(B + val)
+        lens = rng.integers(0, S + 1, B)
+        pb = synth.make_problem(B, Hq, Hkv, 128, P, S, lens=lens, dtype="bf16", dist="mixed", seed=47)
+        out, lse = run_flat(pb)
+        out2, lse2 = run_flat(pb, aux=True)
+    finally:
+        hydra.set_config(key, 0)
+    ref, lref = oracle.flat_attention(pb)
+    assert_parity(out, ref, lse, lref, what=f"{key}={val} sequential")
+    assert_parity(out2, ref, lse2, lref, what=f"{key}={val} overlapped")
 
 
 def test_composite_auto_overlap_small_shard():
