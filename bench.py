@@ -881,7 +881,10 @@ def run_flat(args, cfg):
     ms_suf = time_graph(g_suf, kk, 3)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     in_step = None
-    if overlap and k_over > 0 and ov_simt:
+    short_share = Hq // Hkv in (2, 4, 8) and S <= 256  # the short-suffix kernel on the suffix's share
+    if overlap and k_over > 0 and short_share:
+        pass  # its share cannot be isolated for an "alone" timing: the in-step spans below stand
+    elif overlap and k_over > 0 and ov_simt:
         # prefix on k persistent CTAs, the SIMT suffix (full grid) its programmatic dependent: the
         # dominant kernel stays the SIMT suffix (timed inside the step by its span below)
         try:
@@ -943,6 +946,8 @@ def run_flat(args, cfg):
                    "heads_per_gpu": Hq_r, "overlap_prefix_suffix": overlap,
                    "schedule": ("sequential" if not (overlap and k_over > 0) else
                                 "prefix on %d CTAs, SIMT suffix its programmatic dependent (full grid)" % k_over if ov_simt else
+                                "prefix on %d CTAs || short-suffix kernel (3 CTAs per SM) on the other SMs" % k_over
+                                if Hq // Hkv in (2, 4, 8) and S <= 256 else
                                 "prefix on %d CTAs || tensor-core suffix on the other SMs" % k_over),
                    "l2": (f"no flush: {in_bytes / 1e9:.2f} GB of inputs per step > 2 x 126 MB L2" if flush is None else
                           L2Flush.DESC + f": {in_bytes / 1e9:.3f} GB of inputs per rank"),

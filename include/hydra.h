@@ -362,6 +362,9 @@ HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, i
  *   "pair_cluster"        CTA-pair kernel: CTA pairs per cluster that share every K/V tile by TMA
  *                         multicast (1, 2 or 4; 0 = automatic: the most that divides the stream-K
  *                         group without idling SMs)
+ *   "overlap_short"       1 (default): hydra_attn's SM-partitioned schedule runs short GQA suffixes (g = 2/4/8,
+ *                         S_cap <= 256, contiguous) on the short-suffix kernel, 3 CTAs per SM of the
+ *                         suffix's share, and plans the split for it; 0: the persistent kernel
  *   "overlap_simt"        0 (default) automatic, 1 force, 2 never: hydra_attn's SM-partitioned schedule with
  *                         the SIMT suffix (MHA) as the prefix's programmatic dependent over its full grid,
  *                         the prefix on >= 32 persistent CTAs (taken when the prefix is light)

@@ -52,7 +52,8 @@ struct Config {
   int64_t step_timer = 0;
   // 1: the sequential schedule launches the suffix as a programmatic dependent of the prefix
   int64_t seq_pdl = 1;
-  int64_t combine_pdl = 0;  // hydra_attn's combine as a programmatic dependent of the suffix kernel
+  int64_t combine_pdl = 0;
+  int64_t overlap_short = 1;  // SM-partitioned schedule: the short-suffix kernel on the suffix's SM share  // hydra_attn's combine as a programmatic dependent of the suffix kernel
   int64_t overlap_simt = 0;  // 0 auto, 1 force, 2 never: the SIMT-dependent overlap schedule (overlap_prefix_ctas)
   // CTA-pair prefix kernel: pairs per cluster sharing K/V tiles by multicast (0 auto, 1, 2, 4)
   int64_t pair_cluster = 0;
@@ -109,6 +110,7 @@ const Key kKeys[] = {
     {"step_timer", &Config::step_timer, false},          {"seq_pdl", &Config::seq_pdl, false},
     {"overlap_simt", &Config::overlap_simt, false},
     {"combine_pdl", &Config::combine_pdl, false},
+    {"overlap_short", &Config::overlap_short, false},
     {"pair_cluster", &Config::pair_cluster, false},
     {"pair_poly", &Config::pair_poly, false},
     {"pair_item_cost", &Config::pair_item_cost, false},
@@ -355,7 +357,8 @@ static int prefix_splits(const hydra_heads *h, int64_t B, int64_t P, int tc2_cta
 // Candidates are multiples of the prefix plan's group size so no SM is left idle; on ties
 // (suffix-bound) the smallest k wins.  Measured at C3@16K: k = 56-60 best (0.86 ms).
 // 0 = no overlap.
-static int overlap_prefix_ctas(const hydra_heads *h, int64_t B, int64_t P, int64_t S_cap, bool *simt = nullptr) {
+static int overlap_prefix_ctas(const hydra_heads *h, int64_t B, int64_t P, int64_t S_cap, bool *simt = nullptr,
+                               bool paged = false) {
   if (simt) *simt = false;
   if (P <= 0 || S_cap <= 0) return 0;
   const int g = h->num_q_heads / h->num_kv_heads;
@@ -407,6 +410,31 @@ static int overlap_prefix_ctas(const hydra_heads *h, int64_t B, int64_t P, int64
       best = t;
       best_k = k;
     }
+  }
+  // Short GQA suffixes (suffix_short_kernel, three CTAs per SM) on the suffix's SM share
+  // (overlap_short, default on): the tensor-bound prefix keeps all but one stream-K group's worth of
+  // SMs and the short kernel streams the suffix beside it at ~50 GB/s per SM.  Model: t(k) =
+  // max(prefix on k, suffix on SMs - k), against the sequential prefix + suffix (+ ~8 us of tail).
+  // Measured (tools/config_ab.py, profiles/r3j_ovshort.jsonl): C6 0.098 -> 0.090 ms, C4 0.259 ->
+  // 0.243 ms at k = 128 (8 of 9 groups).
+  if (g_cfg.overlap_short && !paged && g_cfg.suffix_impl == 0 && g_cfg.overlap_prefix_ctas == 0 &&
+      suffix_short_supported(g, S_cap)) {
+    const double R_P = pair_mode(g) ? 0.42 : 0.38, R_SH = 5.0e4, BW = 7.0e6;
+    const double bytes = (double)B * h->num_kv_heads * S_cap * h->head_dim * 4.0;
+    int bk = 0;
+    double bt = 1e300;
+    for (int k = 8; k <= sms - 8; ++k) {
+      if (prefix_kind(h, B * g, P, k) != PK_TC2) break;
+      if (prefix_tc2_ctas(B, g, h->num_kv_heads, P, k, prefix_bn(), pair_mode(g), (int)g_cfg.pair_cluster) != k) continue;
+      const double t = std::max(pair_blocks / (k * R_P), bytes / std::min((sms - k) * R_SH, BW));
+      if (t < bt) {
+        bt = t;
+        bk = k;
+      }
+    }
+    const int kf = prefix_tc2_ctas(B, g, h->num_kv_heads, P, sms, prefix_bn(), pair_mode(g), (int)g_cfg.pair_cluster);
+    const double t_seq = pair_blocks / (kf * R_P) + bytes / BW + 8.0;
+    return bk > 0 && bt < t_seq ? bk : 0;
   }
   // GQA: the sequential schedule runs the tensor-core suffix on every SM, which the split
   // starves of SMs when the suffix is short (C6: 146 us on 12 SMs against 29 us on 148).
@@ -569,9 +597,15 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
     // Short grouped-query suffixes (<= 2 blocks): the three-CTAs-per-SM kernel, on the full chip
     // (auto) or on request (suffix_impl 3).  Measured (tools/suffix_shapes_ab.py): C6's g = 8
     // 128-token suffixes 26.8 -> see DESIGN.md §7; C4's g = 4.
-    const bool short_ok = tc_ctas == 0 && !pg && !fc && splits <= 1 && suffix_short_supported(g, S_cap);
-    if (short_ok && (g_cfg.suffix_impl == 3 || (g_cfg.suffix_impl == 0 && g_cfg.suffix_ctas == 0))) {
+    const bool short_ok = !pg && !fc && splits <= 1 && suffix_short_supported(g, S_cap);
+    if (short_ok && tc_ctas == 0 && (g_cfg.suffix_impl == 3 || (g_cfg.suffix_impl == 0 && g_cfg.suffix_ctas == 0))) {
       hydra_status st = launch_suffix_short(a, (int)g_cfg.suffix_ctas, s);
+      return st == HYDRA_OK ? st : cuda_fail("suffix (short) tcgen05 launch");
+    }
+    // SM-partitioned schedule with short GQA suffixes (overlap_short): three short-kernel CTAs per
+    // SM of the suffix's share, a programmatic dependent of the prefix
+    if (short_ok && tc_ctas > 0 && g_cfg.overlap_short && g_cfg.suffix_impl == 0) {
+      hydra_status st = launch_suffix_short(a, 3 * tc_ctas, s);
       return st == HYDRA_OK ? st : cuda_fail("suffix (short) tcgen05 launch");
     }
     const int ctas = tc_ctas > 0 ? tc_ctas : (g_cfg.suffix_ctas > 0 ? (int)g_cfg.suffix_ctas : device_sm_count());
@@ -899,7 +933,7 @@ static hydra_status attn_impl(const hydra_heads *h, int64_t B, const void *q, in
   // depending on k at C3@16K, tools/overlap_sustained.py.)  Without an SM split (k = 0) two
   // full grids would only contend: run sequentially.
   bool ov_simt = false;  // SM-partitioned with the SIMT suffix as the prefix's dependent (full grid)
-  const int k_over = s_aux ? overlap_prefix_ctas(h, B, P, S_cap, &ov_simt) : 0;
+  const int k_over = s_aux ? overlap_prefix_ctas(h, B, P, S_cap, &ov_simt, pg != nullptr) : 0;
   cudaStream_t sa = s;
   g_cfg.last_overlap_k = k_over;
   g_cfg.last_overlap_simt = ov_simt ? 1 : 0;

@@ -324,6 +324,22 @@ def test_composite_optional_schedules(key, val, B, Hq, Hkv, P, S):
     assert_parity(out2, ref, lse2, lref, what=f"{key}={val} overlapped")
 
 
+@pytest.mark.parametrize("k", [16, 64, 128])
+@pytest.mark.parametrize("B,Hq,Hkv,P,S", [(256, 32, 4, 6000, 128), (120, 16, 4, 3000, 200), (64, 16, 8, 2500, 40)])
+def test_composite_short_suffix_on_share(k, B, Hq, Hkv, P, S):
+    """SM-partitioned schedule with the short-suffix kernel on the suffix's SM share (overlap_short,
+    the default for short GQA suffixes): 3 x (SMs - k) short CTAs as the prefix's programmatic
+    dependent, ragged lens with NaN-poisoned padding, NaN-filled outputs."""
+    hydra.set_config("overlap_prefix_ctas", k)
+    rng = np.random.default_rng(k + B)
+    lens = rng.integers(0, S + 1, B)
+    pb = synth.make_problem(B, Hq, Hkv, 128, P, S, lens=lens, dtype="bf16", dist="boundary", seed=48)
+    out, lse = run_flat(pb, aux=True)
+    assert hydra.get_config("last_overlap_k") > 0
+    ref, lref = oracle.flat_attention(pb)
+    assert_parity(out, ref, lse, lref, what=f"short suffix on the share k={k} g={Hq // Hkv}")
+
+
 def test_composite_auto_overlap_small_shard():
     """A 5-KV-head shard (C3 on 8 GPUs, scaled down): too few prefix blocks for 148 persistent
     CTAs but enough for the automatic SM split, which must pick the persistent kernel for its
