@@ -368,6 +368,8 @@ HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, i
  *   "overlap_simt"        0 (default) automatic, 1 force, 2 never: hydra_attn's SM-partitioned schedule with
  *                         the SIMT suffix (MHA) as the prefix's programmatic dependent over its full grid,
  *                         the prefix on >= 32 persistent CTAs (taken when the prefix is light)
+ *   "combine_pdl"         1: hydra_attn's combine is a programmatic dependent of the suffix kernel
+ *                         (waits for it at entry); 0 (default; measured within noise)
  *   "seq_pdl"             1 (default): in the sequential schedule the tensor-core suffix is a
  *                         programmatic dependent launch of the prefix (starts in its tail); 0 off
  *   "step_timer"          measurement: device address of 4 x u64 the persistent prefix / suffix
@@ -398,8 +400,9 @@ HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, i
  *   "prefix_trace" / "suffix_trace"  device buffer for CTA-0 timestamps (tools/)
  *   "inject_combine_bug"  1: the combine drops its rescaling (w_p = 1) -- the sabotage of S:522
  *   "mutate"              1: the persistent prefix kernel's CTA 0 skips one 4-row store group of
- *                         its epilogues; 2: the tensor-core suffix's CTA 0 skips head 0's output
- *                         row of its first item (unwritten rows the parity suite must catch)
+ *                         its epilogues; 2: the tensor-core suffix's (persistent or short) CTA 0
+ *                         skips head 0's output row of its first item; 3: the CTA-pair prefix's
+ *                         worker 0 skips 4 rows (unwritten rows the parity suite must catch)
  * hydra_get_config also answers "last_overlap_simt" (1 when that split ran the SIMT suffix as the
  * prefix's programmatic dependent over its full grid) and "last_overlap_k" (prefix CTAs of this thread's last hydra_attn /
  * hydra_tree_attn overlap split, 0 = sequential) and "testing_build" (1 in libhydra_test.so).

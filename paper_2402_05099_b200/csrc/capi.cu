@@ -595,8 +595,8 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
       a.page_size = pg->page_size;
     }
     // Short grouped-query suffixes (<= 2 blocks): the three-CTAs-per-SM kernel, on the full chip
-    // (auto) or on request (suffix_impl 3).  Measured (tools/suffix_shapes_ab.py): C6's g = 8
-    // 128-token suffixes 26.8 -> see DESIGN.md §7; C4's g = 4.
+    // (auto) or on request (suffix_impl 3).  Measured alone (tools/suffix_span.py, kernel span):
+    // C6's g = 8 128-token suffixes 18.4 -> 13.3 us, C4's g = 4 46.5 -> 42.2 us.
     const bool short_ok = !pg && !fc && splits <= 1 && suffix_short_supported(g, S_cap);
     if (short_ok && tc_ctas == 0 && (g_cfg.suffix_impl == 3 || (g_cfg.suffix_impl == 0 && g_cfg.suffix_ctas == 0))) {
       hydra_status st = launch_suffix_short(a, (int)g_cfg.suffix_ctas, s);
