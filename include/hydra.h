@@ -368,8 +368,8 @@ HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, i
  *   "overlap_simt"        0 (default) automatic, 1 force, 2 never: hydra_attn's SM-partitioned schedule with
  *                         the SIMT suffix (MHA) as the prefix's programmatic dependent over its full grid,
  *                         the prefix on >= 32 persistent CTAs (taken when the prefix is light)
- *   "combine_pdl"         1: hydra_attn's combine is a programmatic dependent of the suffix kernel
- *                         (waits for it at entry); 0 (default; measured within noise)
+ *   "combine_pdl"         1 (default): hydra_attn's combine is a programmatic dependent of the suffix
+ *                         kernel (waits for it at entry; -0.5 to -1 us per step); 0 a normal launch
  *   "seq_pdl"             1 (default): in the sequential schedule the tensor-core suffix is a
  *                         programmatic dependent launch of the prefix (starts in its tail); 0 off
  *   "step_timer"          measurement: device address of 4 x u64 the persistent prefix / suffix

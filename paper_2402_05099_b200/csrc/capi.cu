@@ -52,7 +52,7 @@ struct Config {
   int64_t step_timer = 0;
   // 1: the sequential schedule launches the suffix as a programmatic dependent of the prefix
   int64_t seq_pdl = 1;
-  int64_t combine_pdl = 0;
+  int64_t combine_pdl = 1;  // -0.5 to -1 us per step (C6 / C4 / C2, profiles/r3p_combine_pdl_ab.jsonl)
   int64_t overlap_short = 1;  // SM-partitioned schedule: the short-suffix kernel on the suffix's SM share  // hydra_attn's combine as a programmatic dependent of the suffix kernel
   int64_t overlap_simt = 0;  // 0 auto, 1 force, 2 never: the SIMT-dependent overlap schedule (overlap_prefix_ctas)
   // CTA-pair prefix kernel: pairs per cluster sharing K/V tiles by multicast (0 auto, 1, 2, 4)

@@ -24,10 +24,11 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(autouse=True)
 def _reset_config():
     keys = ("prefix_impl", "prefix_splits", "suffix_splits", "prefix_ctas", "suffix_impl",
-            "suffix_ctas", "overlap_prefix_ctas", "pair_cluster", "overlap_simt", "pair_item_cost", "combine_pdl")
+            "suffix_ctas", "overlap_prefix_ctas", "pair_cluster", "overlap_simt", "pair_item_cost")
     for k in keys:
         hydra.set_config(k, 0)
-    defaults = {"prefix_variant": 9, "suffix_cb": 2, "prefix_poly": 4, "pair_poly": 0, "fuse_combine": 0}  # the library defaults
+    defaults = {"prefix_variant": 9, "suffix_cb": 2, "prefix_poly": 4, "pair_poly": 0, "fuse_combine": 0,
+                "combine_pdl": 1, "overlap_short": 1}  # the library defaults
     for k, v in defaults.items():
         hydra.set_config(k, v)
     yield
@@ -304,7 +305,7 @@ def test_composite_simt_dependent(B, Hq, Hkv, P, S):
     assert_parity(out, ref, lse, lref, what=f"SIMT-dependent overlap B={B} H={Hq}")
 
 
-@pytest.mark.parametrize("key,val", [("pair_item_cost", 5), ("pair_item_cost", 40), ("combine_pdl", 1)])
+@pytest.mark.parametrize("key,val", [("pair_item_cost", 5), ("pair_item_cost", 40), ("combine_pdl", 0)])
 @pytest.mark.parametrize("B,Hq,Hkv,P,S", [(256, 32, 4, 5000, 100), (96, 16, 16, 3000, 200)])
 def test_composite_optional_schedules(key, val, B, Hq, Hkv, P, S):
     """Schedule options that are off by default stay correct: cost-balanced stream-K group
@@ -318,7 +319,7 @@ def test_composite_optional_schedules(key, val, B, Hq, Hkv, P, S):
         out, lse = run_flat(pb)
         out2, lse2 = run_flat(pb, aux=True)
     finally:
-        hydra.set_config(key, 0)
+        hydra.set_config(key, {"combine_pdl": 1}.get(key, 0))  # back to the library default
     ref, lref = oracle.flat_attention(pb)
     assert_parity(out, ref, lse, lref, what=f"{key}={val} sequential")
     assert_parity(out2, ref, lse2, lref, what=f"{key}={val} overlapped")
