@@ -827,6 +827,16 @@ static int choose_cluster(int64_t n_pairs, int n_workers_req, int forced) {
     if (forced > 1 && kC != forced) continue;
     if (n_pairs % kC == 0 && workers(kC) >= (forced > 1 ? 1 : w1)) return kC;
   }
+  // Groups of >= 8 pairs (C4, C6: 2048 stacked rows per KV head): 2 pairs per cluster even at the
+  // cost of one stream-K group -- inside a sustained step the multicast's saved L2 -> SM traffic is
+  // worth more (C4 sequential 0.253-0.263 -> 0.236 ms, C6 0.088-0.090 -> 0.084-0.085 ms,
+  // profiles/r3s_pair_cluster_step_ab.jsonl; same-box A/B of this rule, profiles/
+  // r3v_pair_cluster_rule_ab.log: sequential C6 0.102-0.104 -> 0.098 ms, C4 0.257 -> 0.243 ms, the
+  // short-suffix overlap unchanged), although alone, unthrottled, 144 CTAs without multicast are
+  // ~1 % faster.
+#ifndef HYDRA_PAIR_CLUSTER_LEGACY
+  if (forced == 0 && n_pairs >= 8 && n_pairs % 2 == 0 && workers(2) > 0 && workers(2) >= w1 - n_pairs) return 2;
+#endif
   return 1;
 }
 
