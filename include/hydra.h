@@ -200,8 +200,17 @@ HYDRA_API hydra_status hydra_combine_ex(const hydra_combine_desc *c, void *strea
  * hydra_attn -- the whole decode-step attention of App. B `hydragen_attention`
  * (P:347-399): prefix (hydra_prefix_attn) || suffix (hydra_suffix_attn) ->
  * combine, writing out[B,Hq,d] (out_dtype) and optionally lse_out[B,Hq].
- * If s_aux is non-NULL the prefix runs on s_aux concurrently with the suffix on
- * stream and is joined back into stream with an event before the combine.
+ * Everything is launched on `stream`.  s_aux non-NULL means the caller allows the prefix and
+ * the suffix to run concurrently: the suffix then becomes a programmatic dependent launch of
+ * the prefix on disjoint SMs -- the persistent tensor-core suffix on the SMs the prefix leaves
+ * (heavy prefix), the short-suffix kernel on all but one stream-K group's SMs (short GQA
+ * suffixes), or the SIMT suffix over its full grid beside a prefix on >= 32 CTAs (light MHA
+ * prefix) -- whichever the planner finds faster than prefix-then-suffix (config keys
+ * overlap_prefix_ctas, overlap_short, overlap_simt; hydra_get_config("last_overlap_k") /
+ * "last_overlap_simt" report the choice).  Without s_aux the two run one after the other (GQA
+ * tensor-core suffixes still start in the prefix's tail as its programmatic dependents).  s_aux
+ * itself receives no work.  The combine follows on `stream` (a programmatic dependent of the
+ * suffix, waiting for it at entry).
  * Requires ws_bytes >= hydra_workspace_size(HYDRA_OP_ATTN, h, B, P, S_cap, 0).
  */
 HYDRA_API hydra_status hydra_attn(const hydra_heads *h, int64_t B,
