@@ -372,7 +372,7 @@ HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, i
  *                         multicast (1, 2 or 4; 0 = automatic: the most that divides the stream-K
  *                         group without idling SMs)
  *   "overlap_short"       1 (default): hydra_attn's SM-partitioned schedule runs short GQA suffixes (g = 2/4/8,
- *                         S_cap <= 256, contiguous) on the short-suffix kernel, 3 CTAs per SM of the
+ *                         S_cap <= 128, contiguous) on the short-suffix kernel, 3 CTAs per SM of the
  *                         suffix's share, and plans the split for it; 0: the persistent kernel
  *   "overlap_simt"        0 (default) automatic, 1 force, 2 never: hydra_attn's SM-partitioned schedule with
  *                         the SIMT suffix (MHA) as the prefix's programmatic dependent over its full grid,
@@ -387,7 +387,8 @@ HYDRA_API size_t hydra_workspace_size(int op, const hydra_heads *h, int64_t B, i
  *   "prefix_splits"       KV splits of the one-tile / SIMT prefix kernels
  *   "prefix_ctas"         CTAs of the persistent prefix kernel
  *   "suffix_impl"         1 SIMT split-K GEMV, 2 persistent TMA-fed tensor-core kernel, 3 the short-suffix
- *                         tensor-core kernel (g >= 2, S_cap <= 256; 3 CTAs per SM; automatic there)
+ *                         tensor-core kernel (g = 2/4/8, S_cap <= 256; 3 CTAs per SM; automatic for
+ *                         S_cap <= 128)
  *   "suffix_splits"       KV splits of the suffix kernels (tensor-core kernel: split-K over
  *                         tokens, only when set; SIMT kernel: automatic when 0)
  *   "suffix_ctas"         CTAs of the persistent suffix kernel

@@ -216,6 +216,13 @@ static int heads_per_cta(int g) {
 // query heads and accumulators in registers (2 CTAs/SM at g = 8).  Measured on B200
 // (tools/suffix_shapes.py, L2 flushed): g = 8, B = 256, S = 128: 28 vs 66-117 us; g = 4,
 // B = 512: 67 vs 96 us; g = 16: 108 vs 357-410 us; MHA (g = 1): 0.83 vs 0.79 ms at C3.
+// The short-suffix kernel where it is chosen automatically: one-block items (S_cap <= 128).  With
+// two-block items the persistent kernel's 2-block rounds measured faster on some shapes (tools/
+// suffix_span.py, profiles/r4a_suffix_short_vs_tc.jsonl: 64 x 8 kv heads x 256 tokens 13.1 vs
+// 16.5 us, 128 x 8 x 256 21.7 vs 24.6 us) while one-block items favour the short kernel (1024 x 8 x
+// 64: 64.6 vs 89.0 us; 2048 x 4 x 128: 88.7 vs 102.5 us).  suffix_impl 3 forces it up to 256.
+static bool short_auto(int g, int64_t S_cap) { return suffix_short_supported(g, S_cap) && S_cap <= 128; }
+
 static bool use_suffix_tc(const hydra_heads *h, int64_t B, int64_t S_cap, bool overlap = false) {
   if (g_cfg.suffix_impl == 1 || S_cap <= 0 || !suffix_tc_supported(h)) return false;
   if (g_cfg.suffix_impl == 2 || g_cfg.suffix_impl == 3) return true;
@@ -418,7 +425,7 @@ static int overlap_prefix_ctas(const hydra_heads *h, int64_t B, int64_t P, int64
   // Measured (tools/config_ab.py, profiles/r3j_ovshort.jsonl): C6 0.098 -> 0.090 ms, C4 0.259 ->
   // 0.243 ms at k = 128 (8 of 9 groups).
   if (g_cfg.overlap_short && !paged && g_cfg.suffix_impl == 0 && g_cfg.overlap_prefix_ctas == 0 &&
-      suffix_short_supported(g, S_cap)) {
+      short_auto(g, S_cap)) {
     const double R_P = pair_mode(g) ? 0.42 : 0.38, R_SH = 5.0e4, BW = 7.0e6;
     const double bytes = (double)B * h->num_kv_heads * S_cap * h->head_dim * 4.0;
     int bk = 0;
@@ -598,13 +605,14 @@ static hydra_status run_suffix(const hydra_heads *h, int64_t B, const void *q, i
     // (auto) or on request (suffix_impl 3).  Measured alone (tools/suffix_span.py, kernel span):
     // C6's g = 8 128-token suffixes 18.4 -> 13.3 us, C4's g = 4 46.5 -> 42.2 us.
     const bool short_ok = !pg && !fc && splits <= 1 && suffix_short_supported(g, S_cap);
-    if (short_ok && tc_ctas == 0 && (g_cfg.suffix_impl == 3 || (g_cfg.suffix_impl == 0 && g_cfg.suffix_ctas == 0))) {
+    if (short_ok && tc_ctas == 0 &&
+        (g_cfg.suffix_impl == 3 || (g_cfg.suffix_impl == 0 && g_cfg.suffix_ctas == 0 && short_auto(g, S_cap)))) {
       hydra_status st = launch_suffix_short(a, (int)g_cfg.suffix_ctas, s);
       return st == HYDRA_OK ? st : cuda_fail("suffix (short) tcgen05 launch");
     }
     // SM-partitioned schedule with short GQA suffixes (overlap_short): three short-kernel CTAs per
     // SM of the suffix's share, a programmatic dependent of the prefix
-    if (short_ok && tc_ctas > 0 && g_cfg.overlap_short && g_cfg.suffix_impl == 0) {
+    if (short_ok && tc_ctas > 0 && g_cfg.overlap_short && g_cfg.suffix_impl == 0 && short_auto(g, S_cap)) {
       hydra_status st = launch_suffix_short(a, 3 * tc_ctas, s);
       return st == HYDRA_OK ? st : cuda_fail("suffix (short) tcgen05 launch");
     }

@@ -326,7 +326,8 @@ def test_composite_optional_schedules(key, val, B, Hq, Hkv, P, S):
 
 
 @pytest.mark.parametrize("k", [16, 64, 128])
-@pytest.mark.parametrize("B,Hq,Hkv,P,S", [(256, 32, 4, 6000, 128), (120, 16, 4, 3000, 200), (64, 16, 8, 2500, 40)])
+@pytest.mark.parametrize("B,Hq,Hkv,P,S", [(256, 32, 4, 6000, 128), (120, 16, 4, 3000, 96), (64, 16, 8, 2500, 40),
+                                         (120, 16, 4, 3000, 200)])
 def test_composite_short_suffix_on_share(k, B, Hq, Hkv, P, S):
     """SM-partitioned schedule with the short-suffix kernel on the suffix's SM share (overlap_short,
     the default for short GQA suffixes): 3 x (SMs - k) short CTAs as the prefix's programmatic
@@ -427,7 +428,8 @@ def test_suffix_short_two_block_jump_and_repeat():
         assert_parity(o, ref, lse, lref, what="suffix short two-block jump")
 
 
-@pytest.mark.parametrize("B,Hq,Hkv,P,S", [(256, 32, 4, 1500, 128), (96, 32, 8, 700, 200), (50, 16, 8, 300, 40)])
+@pytest.mark.parametrize("B,Hq,Hkv,P,S", [(256, 32, 4, 1500, 128), (96, 32, 8, 700, 100), (50, 16, 8, 300, 40),
+                                         (96, 32, 8, 700, 200)])
 def test_composite_short_suffix_auto(B, Hq, Hkv, P, S):
     """The automatic choice (suffix_impl 0) routes short GQA suffixes to the short kernel, in
     the sequential schedule as a programmatic dependent of the prefix: whole step vs oracle."""
